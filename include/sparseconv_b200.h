@@ -1,0 +1,209 @@
+/*
+ * sparseconv_b200.h — C ABI of the B200-native sparse-convolution engine.
+ *
+ * The reference (arxiv 2204.10319 CPU package `sparseconv`, read-only at
+ * /root/reference/pkg/src/sparseconv) is pure Python: its operator API is a
+ * set of numpy functions, so the "FFI" a maintainer would bind is exactly the
+ * list below, one entry point per reference function on the hot path
+ * (SURVEY.md §8(a)/(b)).  Each declaration cites the reference symbol it
+ * replaces as file:line relative to pkg/src/sparseconv/.
+ *
+ * Conventions
+ *  - All data pointers are DEVICE pointers owned and allocated by the caller
+ *    (torch tensors passed as raw addresses in the Python binding).  Nothing
+ *    is allocated or freed across the ABI; scratch space is a caller-provided
+ *    workspace whose size is queried first (…_workspace()).
+ *  - Work is enqueued on the caller's stream (`scb_stream_t` = cudaStream_t)
+ *    and is asynchronous unless stated otherwise.
+ *  - Coordinates are int32 rows (batch, x1..xD), D = 1..4 (core.py:90,106-107).
+ *  - Every function returns SCB_OK (0) or an error code; scb_last_error()
+ *    returns a thread-local message (the Python layer re-raises it as the
+ *    matching ValueError / KeyError of the reference).
+ *  - Numerics: kernel maps, output coordinates, plans and gathers are
+ *    bit-exact w.r.t. the reference; GEMM/scatter are f32-accumulated.
+ */
+#ifndef SPARSECONV_B200_H
+#define SPARSECONV_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef void* scb_stream_t; /* cudaStream_t */
+
+enum scb_status { SCB_OK = 0, SCB_EINVAL = 1, SCB_ECUDA = 2, SCB_EUNSUPPORTED = 3 };
+enum scb_dtype { SCB_F32 = 0, SCB_F16 = 1 };
+enum scb_index_kind { SCB_INDEX_HASH = 0, SCB_INDEX_GRID = 1 };
+
+/* Geometry of one coordinate set: spatial rank, batch count and boundary.
+ * Mirrors SparseTensor.{boundary,batch_size} (core.py:90-94). */
+typedef struct {
+  int32_t dim;        /* spatial rank D, 1..4 */
+  int32_t _pad;
+  int64_t batch_size; /* batch column is in [0, batch_size) */
+  int64_t extent[4];  /* boundary per spatial dim */
+} scb_grid_t;
+
+/* One GEMM problem of the grouped contraction: `rows` buffer rows starting at
+ * `a_row` (of the gather buffer when a_src == 0, of the feature matrix when
+ * a_src == 1 — the centre offset) times weight slice `b_index`, written to
+ * partial rows starting at `c_row`. */
+typedef struct {
+  int64_t a_row;
+  int64_t c_row;
+  int32_t rows;
+  int32_t b_index;
+  int32_t a_src;
+  int32_t _pad;
+} scb_segment_t;
+
+#define SCB_MAX_SEGMENTS 128
+#define SCB_TILE_ROWS 128 /* buffer slabs are padded to this many rows */
+
+const char* scb_last_error(void);
+int32_t scb_abi_version(void);
+/* Number of SMs of the current device (for grid sizing in the host layer). */
+int32_t scb_device_sm_count(void);
+
+/* ---------------------------------------------------------------- index
+ * Replaces HashIndex (mapping.py:122-189), GridIndex (mapping.py:82-119) and
+ * build_index (mapping.py:195-208).  Hash: open addressing, linear probing,
+ * table = next pow2 >= 2N slots (load <= 0.5) of 64-bit keys + int32 rows.
+ * Grid: dense int32 table over batch x boundary.
+ * `status` (device, 2 x int32, zeroed by this call) receives the number of
+ * duplicate keys and out-of-bounds rows found while building — the
+ * SparseTensor validation of core.py:112-120. */
+int64_t scb_hash_slots(int64_t n);
+int32_t scb_index_build(int32_t kind, const int32_t* coords, int64_t n, const scb_grid_t* grid,
+                        int64_t* table_keys, int32_t* table_rows, int64_t slots,
+                        int32_t* status, scb_stream_t stream);
+/* HashIndex.query / GridIndex.query: row per probe, -1 (MISS) when absent or
+ * out of bounds (mapping.py:106-119, 166-189). */
+int32_t scb_index_query(int32_t kind, const int32_t* probes, int64_t n, const scb_grid_t* grid,
+                        const int64_t* table_keys, const int32_t* table_rows, int64_t slots,
+                        int32_t* rows_out, scb_stream_t stream);
+
+/* ---------------------------------------------------------------- output coordinates
+ * Replaces compute_output_coords (mapping.py:216-248) for stride > 1: fused
+ * candidate generation (offset subtraction, modular and boundary checks, key
+ * flattening) then radix sort + unique on 64-bit keys, so the result is in
+ * ascending flat-key order.  `offset_base` is the lowest per-dimension offset
+ * of the window (-(K-1)/2 for odd K, 0 for even K: mapping.py:63-79 and its
+ * EVEN_KERNEL_OFFSET_BASE hook, mapping.py:26).  `out_keys` needs room for
+ * scb_output_coords_capacity() keys; `n_out` (device int64) receives the
+ * count.  scb_unflatten turns keys back into coordinate rows. */
+int64_t scb_output_coords_capacity(int64_t n_in, int32_t dim, int32_t kernel_size, int32_t stride);
+int64_t scb_output_coords_workspace(int64_t n_in, int32_t dim, int32_t kernel_size, int32_t stride);
+int32_t scb_output_coords(const int32_t* in_coords, int64_t n_in, const scb_grid_t* out_grid,
+                          int32_t kernel_size, int32_t offset_base, int32_t stride,
+                          void* workspace, int64_t ws_bytes, int64_t* out_keys, int64_t* n_out,
+                          scb_stream_t stream);
+int32_t scb_unflatten(const int64_t* keys, int64_t n, const scb_grid_t* grid, int32_t* coords,
+                      scb_stream_t stream);
+
+/* ---------------------------------------------------------------- kernel map
+ * Replaces map_search (mapping.py:289-319) and derive_symmetric_maps
+ * (mapping.py:322-339).  One pass over outputs x searched offsets writes the
+ * hit matrix hits[V][n_out] (input row or -1).  With `symmetric` (stride 1,
+ * odd K) only offsets 0..centre are probed and the mirror entry
+ * hits[V-1-n][j] = k is filled directly, which is exactly the order the
+ * reference's stable re-sort produces. */
+int32_t scb_map_search(int32_t kind, const int32_t* out_coords, int64_t n_out,
+                       const scb_grid_t* in_grid, int32_t kernel_size, int32_t offset_base,
+                       int32_t stride, int32_t symmetric, const int64_t* table_keys, const int32_t* table_rows,
+                       int64_t slots, int32_t* hits, scb_stream_t stream);
+/* Per-offset compaction of a hit matrix into the canonical CSR map
+ * (offset_ptr[V+1] int64, in_idx/out_idx int32, entries of each offset sorted
+ * by output row).  Two phases so the caller can size in_idx/out_idx:
+ * scb_map_count fills offset_ptr (device) — read offset_ptr[V] after a sync —
+ * then scb_map_compact writes the entries. */
+int64_t scb_map_workspace(int32_t volume, int64_t n_out);
+int32_t scb_map_count(const int32_t* hits, int32_t volume, int64_t n_out, void* workspace,
+                      int64_t* offset_ptr, scb_stream_t stream);
+int32_t scb_map_compact(const int32_t* hits, int32_t volume, int64_t n_out, const void* workspace,
+                        const int64_t* offset_ptr, int32_t* in_idx, int32_t* out_idx,
+                        scb_stream_t stream);
+/* KernelMap.swap_roles (mapping.py:277-286): scatter a CSR map into the hit
+ * matrix of the transposed map, hits_t[V][n_in]; compact it with the two
+ * calls above. */
+int32_t scb_map_transpose(const int64_t* offset_ptr, const int32_t* in_idx, const int32_t* out_idx,
+                          int32_t volume, int64_t total, int64_t n_in, int32_t* hits_t,
+                          scb_stream_t stream);
+
+/* ---------------------------------------------------------------- plan
+ * Replaces build_gather_scatter_plan (mapping.py:377-418).  The B200 buffer
+ * keeps the reference's offset-major order but starts every offset's slice
+ * on a SCB_TILE_ROWS boundary so GEMM tiles never straddle offsets:
+ * slab_ptr[n] = sum_{m<n, m != skip} roundup(|M_m|, tile).  Outputs:
+ * buf_in[rows_pad] (input row per buffer row, -1 on padding rows) and
+ * pos[n_out][V] (buffer row per (output, offset), -1 when absent) — the
+ * output-stationary CSR of the reference in fixed-width form.  `skip_offset`
+ * is the centre offset on stride-1 odd-K layers, else -1.  When `status`
+ * (device int32, nullable) is given, entries that repeat an (output, offset)
+ * pair — impossible for a searched map, possible for a hand-built one — are
+ * counted there instead of silently overwriting. */
+int32_t scb_plan_build(const int64_t* offset_ptr, const int32_t* in_idx, const int32_t* out_idx,
+                       int32_t volume, int64_t total, int64_t n_out, int32_t skip_offset,
+                       int32_t tile_rows, int32_t* buf_in, int64_t rows_pad, int32_t* pos,
+                       int32_t* status, scb_stream_t stream);
+
+/* ---------------------------------------------------------------- movement
+ * gather (execution.py:159-180, kernels.py:28-35): buffer[r] =
+ * features[buf_in[r]] (zero row when buf_in[r] < 0), 128-bit vector copies,
+ * bit-exact.  `ld_*` are row strides in elements. */
+int32_t scb_gather(int32_t dtype, const void* features, int64_t n_in, int32_t channels,
+                   int64_t ld_feat, const int32_t* buf_in, int64_t rows, void* buffer,
+                   int64_t ld_buf, scb_stream_t stream);
+/* scatter_accumulate, output-stationary (execution.py:183-218,
+ * kernels.py:38-50) fused with the centre-offset add (execution.py:423-428)
+ * and an optional pointwise epilogue (execution.py:554-576):
+ *   acc = sum_{n ascending} partial[pos[k][n]]   (f32, one write per row)
+ *   acc += partial[center_row + k]               (if center_row >= 0)
+ *   acc = acc * scale + shift (if scale), + bias (if bias), max(0,.) if relu
+ *   out[k] = (out_dtype) acc */
+int32_t scb_scatter(const float* partial, int64_t ldp, const int32_t* pos, int32_t volume,
+                    int64_t n_out, int32_t c_out, int64_t center_row, int32_t out_dtype, void* out,
+                    int64_t ld_out, const float* scale, const float* shift, const float* bias,
+                    int32_t relu, scb_stream_t stream);
+/* pointwise_apply (execution.py:554-576) on a feature matrix in place:
+ * op 0 = relu, 1 = bias_add, 2 = bn_fold (scale, shift).  f32 compute, cast
+ * back to the storage dtype. */
+int32_t scb_pointwise(int32_t dtype, void* features, int64_t n, int32_t channels, int32_t op,
+                      const float* a, const float* b, scb_stream_t stream);
+/* Residual glue for the MinkUNet workload (not a reference layer kind):
+ * out = relu?(x + y), same shape/dtype. */
+int32_t scb_add(int32_t dtype, const void* x, const void* y, void* out, int64_t count, int32_t relu,
+                scb_stream_t stream);
+/* quantize_features FP16 path (core.py:219-238): f32 -> f16 RNE with
+ * saturation to +-65504; `n_saturated` (device int64) counts clamps. */
+int32_t scb_quantize_f16(const float* in, void* out, int64_t count, int64_t* n_saturated,
+                         scb_stream_t stream);
+
+/* ---------------------------------------------------------------- grouped GEMM
+ * execute_groups (execution.py:331-368) + the centre matmul
+ * (execution.py:423-424) as ONE persistent launch over a tile table built
+ * from `segments` (one per scheduled offset / group member).
+ *  - F16 (FP16-storage path): tcgen05.mma kind::f16, A/B staged by TMA,
+ *    f32 accumulators in TMEM, TMA-stored f32 partials.  Weights must be
+ *    packed by scb_pack_weights_f16 into [V][n_pad][k_pad] (K-major, zero
+ *    padded; n_pad = roundup(c_out,16), k_pad = roundup(c_in,16)).
+ *  - F32 (FP32 path): exact-f32 SIMT FMA (TF32 would miss the 1e-4 target,
+ *    SURVEY.md §7.3 item 5); weights are the reference's [V][c_in][c_out] f32.
+ * `a_buffer` has `a_rows` rows of stride `lda`; `a_features` (centre) has
+ * `f_rows` rows of stride `ldf`.  Partials: `c_rows` rows of stride `ldc`
+ * (ldc = n_pad for F16, c_out for F32). */
+int32_t scb_pack_weights_f16(const float* w, int32_t volume, int32_t c_in, int32_t c_out,
+                             void* packed, int32_t k_pad, int32_t n_pad, scb_stream_t stream);
+int32_t scb_grouped_gemm(int32_t dtype, const void* a_buffer, int64_t a_rows, int64_t lda,
+                         const void* a_features, int64_t f_rows, int64_t ldf, int32_t c_in,
+                         const void* weights, int32_t volume, int32_t c_out, float* partial,
+                         int64_t c_rows, int64_t ldc, const scb_segment_t* segments,
+                         int32_t n_segments, scb_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SPARSECONV_B200_H */

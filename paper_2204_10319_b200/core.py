@@ -1,0 +1,270 @@
+"""Device-resident core types: the drop-in twins of the reference's
+``SparseTensor``, ``WeightTensor`` and ``PrecisionMode`` (reference
+``core.py:25-171``) plus ``quantize_features`` (``core.py:219-238``).
+
+A ``SparseTensor`` here keeps its coordinates as an int32 ``(N, 1+D)`` CUDA
+tensor (batch column first) and its features as an ``(N, C)`` float16/float32
+CUDA tensor.  It accepts the reference's numpy inputs unchanged.  Tensors
+that share a coordinate set (every stride-1 layer output) share one
+``CoordinateSet``, which owns the device index and the kernel maps built
+over it, so maps are built once per level — results
+are identical to rebuilding them, as the reference does.
+"""
+
+from __future__ import annotations
+
+import warnings
+from enum import Enum
+
+import numpy as np
+import torch
+
+from . import _native as nat
+
+FP16_MAX = float(np.finfo(np.float16).max)
+
+
+class PrecisionMode(Enum):
+    """Feature storage precision (reference core.py:25-43).  Reductions always
+    run in at least 32-bit."""
+
+    FP32 = "fp32"
+    FP16_STORAGE = "fp16"
+
+    @property
+    def storage_dtype(self) -> np.dtype:
+        return np.dtype(np.float16) if self is PrecisionMode.FP16_STORAGE else np.dtype(np.float32)
+
+    @property
+    def torch_dtype(self) -> torch.dtype:
+        return torch.float16 if self is PrecisionMode.FP16_STORAGE else torch.float32
+
+    @property
+    def element_bytes(self) -> int:
+        return self.storage_dtype.itemsize
+
+
+def flatten_coords(coords, boundary, batch_size: int = 1):
+    """Batch-major flat key (reference core.py:46-66), numpy or torch."""
+    total = int(batch_size)
+    for b in boundary:
+        if int(b) <= 0:
+            raise ValueError("boundary extents must be positive")
+        total *= int(b)
+    if total >= 1 << 62:
+        raise ValueError("coordinate space too large to key into int64")
+    if isinstance(coords, torch.Tensor):
+        c = coords.to(torch.int64)
+        key = c[:, 0].clone()
+    else:
+        c = np.asarray(coords, dtype=np.int64)
+        key = c[:, 0].copy()
+    for d, b in enumerate(boundary):
+        key = key * int(b) + c[:, d + 1]
+    return key
+
+
+def unflatten_coords(keys, boundary, batch_size: int = 1):
+    """Inverse of :func:`flatten_coords` (reference core.py:69-79)."""
+    is_t = isinstance(keys, torch.Tensor)
+    rem = keys.to(torch.int64).clone() if is_t else np.asarray(keys, dtype=np.int64).copy()
+    cols = [None] * (len(boundary) + 1)
+    for d in range(len(boundary) - 1, -1, -1):
+        cols[d + 1] = rem % int(boundary[d])
+        rem = rem // int(boundary[d])
+    cols[0] = rem
+    return torch.stack(cols, 1) if is_t else np.stack(cols, 1)
+
+
+def _device() -> torch.device:
+    nat.require_cuda()
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def as_device_coords(coords) -> torch.Tensor:
+    dev = _device()
+    if isinstance(coords, torch.Tensor):
+        return coords.to(device=dev, dtype=torch.int32).contiguous()
+    arr = np.asarray(coords)
+    if arr.size and (arr.max() > np.iinfo(np.int32).max or arr.min() < np.iinfo(np.int32).min):
+        raise ValueError("coordinates exceed the int32 range of the device layout")
+    return torch.from_numpy(np.ascontiguousarray(arr, dtype=np.int32)).to(dev)
+
+
+def as_device_features(features) -> torch.Tensor:
+    dev = _device()
+    if isinstance(features, torch.Tensor):
+        f = features.to(dev)
+    else:
+        f = torch.from_numpy(np.ascontiguousarray(features)).to(dev)
+    if f.dtype not in (torch.float16, torch.float32):
+        f = f.to(torch.float32)
+    return f.contiguous()
+
+
+class CoordinateSet:
+    """One coordinate set on the device plus everything derived from it:
+    indexes by kind and kernel maps by (kernel_size, stride) — the
+    level-keyed map cache."""
+
+    __slots__ = ("coords", "boundary", "batch_size", "indexes", "maps", "__weakref__")
+
+    def __init__(self, coords: torch.Tensor, boundary, batch_size: int):
+        self.coords = coords
+        self.boundary = tuple(int(b) for b in boundary)
+        self.batch_size = int(batch_size)
+        self.indexes = {}
+        self.maps = {}
+
+    @property
+    def num_points(self) -> int:
+        return int(self.coords.shape[0])
+
+
+class SparseTensor:
+    """Unique integer coordinates paired with a feature row each
+    (reference core.py:82-143), resident in HBM."""
+
+    __slots__ = ("coords", "features", "stride", "boundary", "batch_size", "_cset")
+
+    def __init__(self, coords, features, stride: int = 1, boundary=(), batch_size: int = 1,
+                 *, validate: bool = True, coordset: CoordinateSet | None = None):
+        boundary = tuple(int(b) for b in boundary)
+        if coordset is not None:
+            c = coordset.coords
+        else:
+            c = as_device_coords(coords)
+        f = as_device_features(features)
+        if c.ndim != 2 or c.shape[1] != 1 + len(boundary):
+            raise ValueError(
+                f"coords shape {tuple(c.shape)} does not match boundary of rank {len(boundary)}")
+        if not 1 <= len(boundary) <= 4:
+            raise ValueError("spatial rank must be between 1 and 4")
+        if f.ndim != 2 or f.shape[0] != c.shape[0]:
+            raise ValueError("feature rows must match coordinate rows")
+        if int(stride) < 1:
+            raise ValueError("stride must be a positive integer")
+        if coordset is None:
+            coordset = CoordinateSet(c, boundary, batch_size)
+            if validate and c.shape[0]:
+                _validate(coordset)
+        self.coords = c
+        self.features = f
+        self.stride = int(stride)
+        self.boundary = boundary
+        self.batch_size = int(batch_size)
+        self._cset = coordset
+
+    # -- reference API --------------------------------------------------
+    @property
+    def num_points(self) -> int:
+        return int(self.coords.shape[0])
+
+    @property
+    def num_channels(self) -> int:
+        return int(self.features.shape[1])
+
+    @property
+    def spatial_dims(self) -> int:
+        return len(self.boundary)
+
+    def replace_features(self, features) -> "SparseTensor":
+        """Same coordinates (and coordinate set), new feature matrix."""
+        return SparseTensor(None, features, self.stride, self.boundary, self.batch_size,
+                            coordset=self._cset)
+
+    # -- host views (tests, I/O) ------------------------------------------
+    def coords_numpy(self) -> np.ndarray:
+        return self.coords.cpu().numpy().astype(np.int64)
+
+    def features_numpy(self) -> np.ndarray:
+        return self.features.cpu().numpy()
+
+    @property
+    def coordset(self) -> CoordinateSet:
+        return self._cset
+
+
+def _validate(cset: CoordinateSet) -> None:
+    """Range and uniqueness checks of reference core.py:112-120, on device."""
+    c = cset.coords
+    b = c[:, 0]
+    if int(b.min()) < 0 or int(b.max()) >= cset.batch_size:
+        raise ValueError("batch index out of range")
+    bound = torch.tensor(cset.boundary, device=c.device, dtype=torch.int32)
+    sp = c[:, 1:]
+    if bool((sp < 0).any()) or bool((sp >= bound).any()):
+        raise ValueError("coordinate outside boundary")
+    from .mapping import build_index  # local import: mapping depends on core
+    idx = build_index(cset, "hash")
+    if idx.duplicates:
+        raise ValueError("coordinate rows must be unique")
+
+
+class WeightTensor:
+    """Convolution weights, one C_in x C_out matrix per kernel offset
+    (reference core.py:146-171).  Keeps the reference's f32 host array and
+    lazily materialises the device copies the kernels need: f32
+    ``(V, C_in, C_out)`` for the FP32 path and the K-major padded fp16 pack of
+    the tcgen05 path."""
+
+    __slots__ = ("weights", "kernel_size", "dim", "_dev32", "_packed")
+
+    def __init__(self, weights, kernel_size: int, dim: int):
+        if isinstance(weights, torch.Tensor):
+            weights = weights.detach().cpu().numpy()
+        w = np.ascontiguousarray(weights, dtype=np.float32)
+        if w.ndim != 3:
+            raise ValueError("weights must be a (K**D, C_in, C_out) stack")
+        if w.shape[0] != kernel_size ** dim:
+            raise ValueError(f"expected {kernel_size ** dim} weight slices, got {w.shape[0]}")
+        w.setflags(write=False)
+        self.weights = w
+        self.kernel_size = int(kernel_size)
+        self.dim = int(dim)
+        self._dev32 = None
+        self._packed = None
+
+    @property
+    def c_in(self) -> int:
+        return self.weights.shape[1]
+
+    @property
+    def c_out(self) -> int:
+        return self.weights.shape[2]
+
+    def device_f32(self) -> torch.Tensor:
+        if self._dev32 is None:
+            self._dev32 = torch.from_numpy(np.array(self.weights)).to(_device())
+        return self._dev32
+
+    def packed_f16(self) -> tuple[torch.Tensor, int, int]:
+        """[V][n_pad][k_pad] fp16 (transposed, zero padded) + (k_pad, n_pad)."""
+        if self._packed is None:
+            v, ci, co = self.weights.shape
+            k_pad, n_pad = (ci + 15) // 16 * 16, (co + 15) // 16 * 16
+            out = torch.empty((v, n_pad, k_pad), dtype=torch.float16, device=_device())
+            nat.call("scb_pack_weights_f16", nat.ptr(self.device_f32()), v, ci, co, nat.ptr(out),
+                     k_pad, n_pad, nat.stream_handle())
+            self._packed = (out, k_pad, n_pad)
+        return self._packed
+
+
+def quantize_features(t: SparseTensor, mode: PrecisionMode) -> SparseTensor:
+    """Convert feature storage precision (reference core.py:219-238): FP16
+    rounds to nearest and saturates to +-65504 with a warning."""
+    if mode is PrecisionMode.FP32:
+        if t.features.dtype == torch.float32:
+            return t
+        return t.replace_features(t.features.to(torch.float32))
+    if t.features.dtype == torch.float16:
+        return t
+    src = t.features.contiguous()
+    out = torch.empty(src.shape, dtype=torch.float16, device=src.device)
+    sat = torch.zeros(1, dtype=torch.int64, device=src.device)
+    nat.call("scb_quantize_f16", nat.ptr(src), nat.ptr(out), src.numel(), nat.ptr(sat),
+             nat.stream_handle())
+    n_sat = int(sat.item())
+    if n_sat:
+        warnings.warn(f"{n_sat} feature element(s) saturated to the fp16 range")
+    return t.replace_features(out)

@@ -1,0 +1,18 @@
+// Error state and device queries of the C ABI (include/sparseconv_b200.h).
+#include "common.cuh"
+
+namespace scb {
+static thread_local std::string g_last_error;
+void set_error(const std::string& msg) { g_last_error = msg; }
+}  // namespace scb
+
+extern "C" const char* scb_last_error(void) { return scb::g_last_error.c_str(); }
+
+extern "C" int32_t scb_abi_version(void) { return 1; }
+
+extern "C" int32_t scb_device_sm_count(void) {
+  int dev = 0, v = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+  if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return -1;
+  return v;
+}

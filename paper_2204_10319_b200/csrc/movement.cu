@@ -1,0 +1,299 @@
+// Data movement on sm_100a: gather into the offset-major buffer, the
+// output-stationary scatter (+ centre add + pointwise epilogue), pointwise
+// ops, residual add, fp16 quantisation and fp16 weight packing.  All are
+// HBM-bound streaming kernels: 128-bit vector accesses, grids
+// sized in multiples of the SM count, no atomics.
+#include "common.cuh"
+
+namespace scb {
+
+static int sm_count() {
+  static int n = [] {
+    int dev = 0, v = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
+  return n;
+}
+
+static int blocks_for(long long work, int threads, int per_sm = 8) {
+  long long b = (work + threads - 1) / threads;
+  long long cap = (long long)sm_count() * per_sm;
+  if (b < 1) b = 1;
+  return (int)(b < cap ? b : cap);
+}
+
+// ------------------------------------------------------------------ gather
+// buffer[r, :] = features[buf_in[r], :], vector type VT (16/8/4/2 bytes).
+// One thread moves one vector; rows are walked in buffer order so stores are
+// fully coalesced and the (L2-resident) feature rows are read with 128-bit
+// loads.  Padding rows (buf_in < 0) are zero-filled so the GEMM never sees
+// non-finite garbage.
+template <typename VT>
+__global__ void __launch_bounds__(256) gather_kernel(const VT* __restrict__ feat, long long ldf_v,
+                                                     const int* __restrict__ buf_in,
+                                                     long long rows, int vecs_per_row,
+                                                     VT* __restrict__ buf, long long ldb_v) {
+  const long long total = rows * vecs_per_row;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long r = t / vecs_per_row;
+    const int v = (int)(t - r * vecs_per_row);
+    const int src = __ldg(buf_in + r);
+    VT val;
+    if (src >= 0) {
+      val = __ldg(feat + src * ldf_v + v);
+    } else {
+      memset(&val, 0, sizeof(VT));
+    }
+    buf[r * ldb_v + v] = val;
+  }
+}
+
+template <typename VT>
+static void launch_gather(const void* f, long long ldf_b, const int* buf_in, long long rows,
+                          long long row_b, void* buf, long long ldb_b, cudaStream_t s) {
+  const int vpr = (int)(row_b / sizeof(VT));
+  gather_kernel<VT><<<blocks_for(rows * vpr, 256), 256, 0, s>>>(
+      (const VT*)f, ldf_b / (long long)sizeof(VT), buf_in, rows, vpr, (VT*)buf,
+      ldb_b / (long long)sizeof(VT));
+}
+
+// ------------------------------------------------------------------ scatter
+template <typename T> __device__ __forceinline__ void store_out(T* p, float v);
+template <> __device__ __forceinline__ void store_out<float>(float* p, float v) { *p = v; }
+template <> __device__ __forceinline__ void store_out<__half>(__half* p, float v) {
+  *p = __float2half_rn(v);
+}
+
+struct Epi {
+  const float* scale;
+  const float* shift;
+  const float* bias;
+  int relu;
+};
+
+__device__ __forceinline__ float epilogue(float a, int c, const Epi& e) {
+  if (e.scale) a = a * __ldg(e.scale + c) + __ldg(e.shift + c);
+  if (e.bias) a = a + __ldg(e.bias + c);
+  if (e.relu) a = fmaxf(a, 0.f);
+  return a;
+}
+
+// Output-stationary fold (kernels.py:38-50): one thread group owns output row
+// k, walks its V buffer positions in ascending offset order (== ascending
+// buffer row, the reference's fold order), accumulates in f32 registers and
+// writes the row exactly once.  Each thread owns 4 consecutive channels
+// (float4 loads of the partial rows).
+template <typename OutT, int VEC>
+__global__ void __launch_bounds__(256) scatter_kernel(const float* __restrict__ partial,
+                                                      long long ldp,
+                                                      const int* __restrict__ pos, int V,
+                                                      long long n_out, int c_out, int groups,
+                                                      long long center_row,
+                                                      OutT* __restrict__ out, long long ldo,
+                                                      Epi e) {
+  const long long total = n_out * groups;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long k = t / groups;
+    const int c0 = (int)(t - k * groups) * VEC;
+    float acc[VEC];
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) acc[i] = 0.f;
+    const int* pk = pos + k * V;
+    for (int n = 0; n < V; ++n) {
+      const int r = __ldg(pk + n);
+      if (r < 0) continue;
+      const float* src = partial + (long long)r * ldp + c0;
+      if constexpr (VEC == 4) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(src));
+        acc[0] += v.x; acc[1] += v.y; acc[2] += v.z; acc[3] += v.w;
+      } else {
+#pragma unroll
+        for (int i = 0; i < VEC; ++i)
+          if (c0 + i < c_out) acc[i] += __ldg(src + i);
+      }
+    }
+    if (center_row >= 0) {
+      const float* src = partial + (center_row + k) * ldp + c0;
+#pragma unroll
+      for (int i = 0; i < VEC; ++i)
+        if (c0 + i < c_out) acc[i] += __ldg(src + i);
+    }
+#pragma unroll
+    for (int i = 0; i < VEC; ++i)
+      if (c0 + i < c_out) store_out<OutT>(out + k * ldo + c0 + i, epilogue(acc[i], c0 + i, e));
+  }
+}
+
+// ------------------------------------------------------------------ pointwise
+template <typename T> __device__ __forceinline__ float ld_f(const T* p);
+template <> __device__ __forceinline__ float ld_f<float>(const float* p) { return *p; }
+template <> __device__ __forceinline__ float ld_f<__half>(const __half* p) { return __half2float(*p); }
+
+template <typename T>
+__global__ void pointwise_kernel(T* __restrict__ x, long long n, int c, int op,
+                                 const float* __restrict__ a, const float* __restrict__ b) {
+  const long long total = n * c;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int ch = (int)(i % c);
+    float v = ld_f<T>(x + i);
+    if (op == 0) v = fmaxf(v, 0.f);
+    else if (op == 1) v = v + __ldg(a + ch);
+    else v = v * __ldg(a + ch) + __ldg(b + ch);
+    store_out<T>(x + i, v);
+  }
+}
+
+template <typename T>
+__global__ void add_kernel(const T* __restrict__ x, const T* __restrict__ y, T* __restrict__ o,
+                           long long n, int relu) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    float v = ld_f<T>(x + i) + ld_f<T>(y + i);
+    if (relu) v = fmaxf(v, 0.f);
+    store_out<T>(o + i, v);
+  }
+}
+
+__global__ void quantize_kernel(const float* __restrict__ in, __half* __restrict__ out,
+                                long long n, unsigned long long* sat) {
+  unsigned int local = 0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const float v = in[i];
+    __half h = __float2half_rn(v);
+    if (__hisinf(h) && isfinite(v)) {
+      h = __float2half_rn(v > 0 ? 65504.f : -65504.f);
+      ++local;
+    }
+    out[i] = h;
+  }
+  if (local) atomicAdd(sat, (unsigned long long)local);
+}
+
+// w[V][c_in][c_out] f32 -> packed[V][n_pad][k_pad] f16 (K-major B operand of
+// the tcgen05 GEMM), zero padded.
+__global__ void pack_weights_kernel(const float* __restrict__ w, int V, int c_in, int c_out,
+                                    __half* __restrict__ packed, int k_pad, int n_pad) {
+  const long long total = (long long)V * n_pad * k_pad;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int kk = (int)(i % k_pad);
+    const int nn = (int)((i / k_pad) % n_pad);
+    const int v = (int)(i / ((long long)k_pad * n_pad));
+    float val = 0.f;
+    if (kk < c_in && nn < c_out) val = w[((long long)v * c_in + kk) * c_out + nn];
+    packed[i] = __float2half_rn(val);
+  }
+}
+
+}  // namespace scb
+
+using namespace scb;
+
+extern "C" int32_t scb_gather(int32_t dtype, const void* features, int64_t n_in, int32_t channels,
+                              int64_t ld_feat, const int32_t* buf_in, int64_t rows, void* buffer,
+                              int64_t ld_buf, scb_stream_t stream) {
+  (void)n_in;
+  SCB_CHECK_ARG(dtype == SCB_F32 || dtype == SCB_F16, "dtype must be f32 or f16");
+  SCB_CHECK_ARG(channels >= 1 && ld_feat >= channels && ld_buf >= channels, "bad strides");
+  if (rows == 0) return SCB_OK;
+  const int es = dtype == SCB_F32 ? 4 : 2;
+  const long long row_b = (long long)channels * es, ldf_b = ld_feat * es, ldb_b = ld_buf * es;
+  const uintptr_t align = (uintptr_t)features | (uintptr_t)buffer;
+  auto fits = [&](long long w) {
+    return row_b % w == 0 && ldf_b % w == 0 && ldb_b % w == 0 && align % w == 0;
+  };
+  cudaStream_t s = as_stream(stream);
+  if (fits(16)) launch_gather<int4>(features, ldf_b, buf_in, rows, row_b, buffer, ldb_b, s);
+  else if (fits(8)) launch_gather<int2>(features, ldf_b, buf_in, rows, row_b, buffer, ldb_b, s);
+  else if (fits(4)) launch_gather<int>(features, ldf_b, buf_in, rows, row_b, buffer, ldb_b, s);
+  else launch_gather<short>(features, ldf_b, buf_in, rows, row_b, buffer, ldb_b, s);
+  SCB_LAUNCHED();
+  return SCB_OK;
+}
+
+extern "C" int32_t scb_scatter(const float* partial, int64_t ldp, const int32_t* pos,
+                               int32_t volume, int64_t n_out, int32_t c_out, int64_t center_row,
+                               int32_t out_dtype, void* out, int64_t ld_out, const float* scale,
+                               const float* shift, const float* bias, int32_t relu,
+                               scb_stream_t stream) {
+  SCB_CHECK_ARG(out_dtype == SCB_F32 || out_dtype == SCB_F16, "dtype must be f32 or f16");
+  SCB_CHECK_ARG((scale == nullptr) == (shift == nullptr), "scale and shift go together");
+  if (n_out == 0) return SCB_OK;
+  Epi e{scale, shift, bias, relu};
+  cudaStream_t s = as_stream(stream);
+  const bool vec4 = (c_out % 4 == 0) && (ldp % 4 == 0) && ((uintptr_t)partial % 16 == 0);
+  const int groups = vec4 ? c_out / 4 : c_out;
+  const long long work = n_out * groups;
+  const int nb = blocks_for(work, 256, 16);
+  if (out_dtype == SCB_F32) {
+    if (vec4)
+      scatter_kernel<float, 4><<<nb, 256, 0, s>>>(partial, ldp, pos, volume, n_out, c_out, groups,
+                                                  center_row, (float*)out, ld_out, e);
+    else
+      scatter_kernel<float, 1><<<nb, 256, 0, s>>>(partial, ldp, pos, volume, n_out, c_out, groups,
+                                                  center_row, (float*)out, ld_out, e);
+  } else {
+    if (vec4)
+      scatter_kernel<__half, 4><<<nb, 256, 0, s>>>(partial, ldp, pos, volume, n_out, c_out, groups,
+                                                   center_row, (__half*)out, ld_out, e);
+    else
+      scatter_kernel<__half, 1><<<nb, 256, 0, s>>>(partial, ldp, pos, volume, n_out, c_out, groups,
+                                                   center_row, (__half*)out, ld_out, e);
+  }
+  SCB_LAUNCHED();
+  return SCB_OK;
+}
+
+extern "C" int32_t scb_pointwise(int32_t dtype, void* features, int64_t n, int32_t channels,
+                                 int32_t op, const float* a, const float* b,
+                                 scb_stream_t stream) {
+  SCB_CHECK_ARG(op >= 0 && op <= 2, "unknown pointwise op");
+  SCB_CHECK_ARG(op == 0 || a, "missing parameter vector");
+  SCB_CHECK_ARG(op != 2 || b, "missing shift vector");
+  if (n * channels == 0) return SCB_OK;
+  cudaStream_t s = as_stream(stream);
+  const int nb = blocks_for(n * channels, 256);
+  if (dtype == SCB_F32) pointwise_kernel<float><<<nb, 256, 0, s>>>((float*)features, n, channels, op, a, b);
+  else pointwise_kernel<__half><<<nb, 256, 0, s>>>((__half*)features, n, channels, op, a, b);
+  SCB_LAUNCHED();
+  return SCB_OK;
+}
+
+extern "C" int32_t scb_add(int32_t dtype, const void* x, const void* y, void* out, int64_t count,
+                           int32_t relu, scb_stream_t stream) {
+  if (count == 0) return SCB_OK;
+  cudaStream_t s = as_stream(stream);
+  const int nb = blocks_for(count, 256);
+  if (dtype == SCB_F32) add_kernel<float><<<nb, 256, 0, s>>>((const float*)x, (const float*)y, (float*)out, count, relu);
+  else add_kernel<__half><<<nb, 256, 0, s>>>((const __half*)x, (const __half*)y, (__half*)out, count, relu);
+  SCB_LAUNCHED();
+  return SCB_OK;
+}
+
+extern "C" int32_t scb_quantize_f16(const float* in, void* out, int64_t count, int64_t* n_saturated,
+                                    scb_stream_t stream) {
+  cudaStream_t s = as_stream(stream);
+  SCB_CUDA(cudaMemsetAsync(n_saturated, 0, sizeof(int64_t), s));
+  if (count == 0) return SCB_OK;
+  quantize_kernel<<<blocks_for(count, 256), 256, 0, s>>>(in, (__half*)out, count,
+                                                         (unsigned long long*)n_saturated);
+  SCB_LAUNCHED();
+  return SCB_OK;
+}
+
+extern "C" int32_t scb_pack_weights_f16(const float* w, int32_t volume, int32_t c_in,
+                                        int32_t c_out, void* packed, int32_t k_pad, int32_t n_pad,
+                                        scb_stream_t stream) {
+  SCB_CHECK_ARG(k_pad >= c_in && n_pad >= c_out, "padding smaller than the weight shape");
+  const long long total = (long long)volume * k_pad * n_pad;
+  if (total == 0) return SCB_OK;
+  pack_weights_kernel<<<blocks_for(total, 256), 256, 0, as_stream(stream)>>>(
+      w, volume, c_in, c_out, (__half*)packed, k_pad, n_pad);
+  SCB_LAUNCHED();
+  return SCB_OK;
+}

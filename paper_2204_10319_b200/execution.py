@@ -1,0 +1,637 @@
+"""Gather -> grouped GEMM -> scatter on the B200, behind the reference's
+execution API (reference ``execution.py``).
+
+Layer data flow (device side):
+
+    mapping   index + map search (+ output coords when strided), cached per
+              coordinate set and (K, stride)            [mapping.py kernels]
+    gather    buffer[slab rows] = features[buf_in]       [scb_gather]
+    matmul    one persistent tcgen05 launch over every scheduled offset
+              (+ the centre offset read straight from the features)
+                                                          [scb_grouped_gemm]
+    scatter   output-stationary f32 fold + centre add + optional epilogue,
+              one write per output row                     [scb_scatter]
+
+Numerics: FP16 storage rounds weights to fp16 for
+the tensor cores and accumulates in f32 (tolerance 1e-2 relative L2); FP32
+storage runs an exact-f32 FMA GEMM (tolerance 1e-4).  The grouping strategy
+(eps, S) changes the tile order of the persistent launch, never the result.
+"""
+
+from __future__ import annotations
+
+import warnings
+from contextlib import contextmanager, nullcontext
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as nat
+from .core import CoordinateSet, PrecisionMode, SparseTensor, WeightTensor
+from .mapping import (DEFAULT_GRID_CELL_CAP, GatherScatterPlan, GridCapacityError, KernelMap,
+                      KernelOffsets, build_gather_scatter_plan, build_index,
+                      compute_output_coords, downsample_boundary, enumerate_offsets, map_search,
+                      _cells)
+
+GATHER_ORDERS = ("weight_stationary", "input_stationary")
+SCATTER_ORDERS = ("weight_stationary", "output_stationary")
+
+
+class StageTimer:
+    """Per-(layer, stage) device time over a forward pass, measured with CUDA
+    events on the compute stream (reference StageTimer, execution.py:39-58)."""
+
+    STAGES = ("mapping", "gather", "matmul", "scatter", "other")
+
+    def __init__(self):
+        self._events: list[tuple[str, str, torch.cuda.Event, torch.cuda.Event]] = []
+        self._samples: dict[tuple[str, str], float] = {}
+
+    @contextmanager
+    def section(self, layer: str, stage: str):
+        start = torch.cuda.Event(enable_timing=True)
+        end = torch.cuda.Event(enable_timing=True)
+        start.record()
+        try:
+            yield
+        finally:
+            end.record()
+            self._events.append((layer, stage, start, end))
+
+    @property
+    def samples(self) -> dict[tuple[str, str], float]:
+        if self._events:
+            torch.cuda.synchronize()
+            for layer, stage, s, e in self._events:
+                key = (layer, stage)
+                self._samples[key] = self._samples.get(key, 0.0) + s.elapsed_time(e) / 1e3
+            self._events.clear()
+        return dict(self._samples)
+
+
+def _timed(timer, layer, stage):
+    return timer.section(layer, stage) if timer is not None else nullcontext()
+
+
+@dataclass(frozen=True)
+class LayerStrategy:
+    """Tuned grouping parameters (execution.py:61-93)."""
+
+    eps: float = 0.0
+    threshold: float = 0.0
+    index_kind: str | None = None
+
+    def __post_init__(self):
+        if not 0.0 <= self.eps <= 1.0:
+            raise ValueError("eps must lie in [0, 1]")
+        if self.threshold < 0:
+            raise ValueError("threshold must be non-negative")
+
+    @staticmethod
+    def separate() -> "LayerStrategy":
+        return LayerStrategy(0.0, 0.0)
+
+    @staticmethod
+    def symmetric_pairs() -> "LayerStrategy":
+        return LayerStrategy(0.0, float("inf"))
+
+    @staticmethod
+    def dense_group() -> "LayerStrategy":
+        return LayerStrategy(1.0, float("inf"))
+
+
+@dataclass(frozen=True)
+class LayerSpec:
+    """Static description of a convolution layer (execution.py:96-113)."""
+
+    kernel_size: int
+    stride: int
+    c_in: int
+    c_out: int
+    transposed: bool = False
+    reuse_key: str | None = None
+    index_kind: str | None = None
+    strategy: LayerStrategy | None = None
+
+    def __post_init__(self):
+        if self.stride not in (1, 2):
+            raise ValueError(f"unsupported stride {self.stride}")
+        if self.transposed and not self.reuse_key:
+            raise ValueError("transposed layers need the reuse key of a strided layer")
+
+
+def resolve_strategy(spec: LayerSpec, strategy: LayerStrategy | None) -> LayerStrategy:
+    """Explicit argument, then the LayerSpec override, then separate
+    (execution.py:116-123)."""
+    if strategy is not None:
+        return strategy
+    if spec.strategy is not None:
+        return spec.strategy
+    return LayerStrategy.separate()
+
+
+@dataclass(eq=False)
+class CachedMap:
+    """A strided layer's map plus its input-side geometry (execution.py:126-134)."""
+
+    kmap: KernelMap
+    in_coords: torch.Tensor
+    in_boundary: tuple
+    in_stride: int
+    in_coordset: CoordinateSet | None = None
+
+
+@dataclass
+class ExecOptions:
+    """Per-call knobs; numerics are invariant under all of them
+    (execution.py:137-156).  ``map_reuse`` keeps maps built over a
+    coordinate set for later layers at the same level (result-identical)."""
+
+    order: str = "locality"
+    fused: bool = True
+    index_kind: str | None = None
+    grid_cell_cap: int = DEFAULT_GRID_CELL_CAP
+    layer_label: str = "layer"
+    timer: StageTimer | None = None
+    traffic_log: list | None = None
+    workload_log: list | None = None
+    plan_log: list | None = None
+    map_reuse: bool = True
+
+    def __post_init__(self):
+        if self.order not in ("locality", "weight"):
+            raise ValueError(f"unknown order {self.order!r}")
+        if not self.fused and self.order == "locality":
+            warnings.warn("locality order requires fused movement; using weight order")
+            self.order = "weight"
+
+
+# ====================================================================== movement API
+
+def _features_of(x) -> torch.Tensor:
+    if isinstance(x, SparseTensor):
+        return x.features
+    if isinstance(x, torch.Tensor):
+        return x.contiguous()
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+def _buffer_ld(dtype, c: int) -> int:
+    return (c + 7) // 8 * 8 if dtype == torch.float16 else c
+
+
+def _gather_padded(features: torch.Tensor, plan: GatherScatterPlan, c: int) -> torch.Tensor:
+    ld = _buffer_ld(features.dtype, c)
+    buf = torch.empty((max(plan.rows_pad, 1), ld), dtype=features.dtype, device=features.device)
+    nat.call("scb_gather", nat.dtype_code(features.dtype), nat.ptr(features), features.shape[0], c,
+             features.stride(0), nat.ptr(plan.buf_in), plan.rows_pad, nat.ptr(buf), ld,
+             nat.stream_handle())
+    return buf
+
+
+def gather(features, plan: GatherScatterPlan, order: str = "weight_stationary") -> torch.Tensor:
+    """Offset-partitioned buffer in the reference layout (execution.py:159-180);
+    both orders are the same bit-exact device copy."""
+    if order not in GATHER_ORDERS:
+        raise ValueError(f"unknown gather order {order!r}")
+    f = _features_of(features)
+    if f.shape[0] != plan.n_in:
+        raise ValueError("plan does not match the feature row count")
+    buf = _gather_padded(f, plan, f.shape[1])
+    return buf[plan.padded_rows(buf), : f.shape[1]].contiguous()
+
+
+def scatter_accumulate(buffer, plan: GatherScatterPlan, n_out: int,
+                       order: str = "weight_stationary", out_dtype=np.float32) -> torch.Tensor:
+    """Fold buffer rows into output rows in ascending buffer-row order
+    (execution.py:183-218): one f32 output-stationary pass on the device."""
+    if order not in SCATTER_ORDERS:
+        raise ValueError(f"unknown scatter order {order!r}")
+    b = _features_of(buffer).to(torch.float32)
+    if b.shape[0] != plan.total:
+        raise ValueError("buffer rows do not match the plan")
+    c = b.shape[1]
+    padded = torch.zeros((max(plan.rows_pad, 1), c), dtype=torch.float32, device=b.device)
+    if plan.total:
+        padded[plan.padded_rows(b)] = b
+    odt = torch.float16 if np.dtype(out_dtype) == np.float16 else torch.float32
+    out = torch.empty((n_out, c), dtype=odt, device=b.device)
+    nat.call("scb_scatter", nat.ptr(padded), c, nat.ptr(plan.pos), plan.pos.shape[1], n_out, c, -1,
+             nat.dtype_code(odt), nat.ptr(out), c, None, None, None, 0, nat.stream_handle())
+    return out
+
+
+# ====================================================================== grouping (host, O(V))
+
+def partition_groups(map_sizes, eps: float, schedule) -> list[tuple[int, int]]:
+    """Alg. 3 greedy grouping of scheduled offsets (execution.py:221-247)."""
+    if not 0.0 <= eps <= 1.0:
+        raise ValueError("eps must lie in [0, 1]")
+    sizes = np.asarray(map_sizes, dtype=np.int64)
+    schedule = list(schedule)
+    ranges, i = [], 0
+    while i < len(schedule):
+        lo = hi = int(sizes[schedule[i]])
+        start = i
+        i += 1
+        while i < len(schedule):
+            n = int(sizes[schedule[i]])
+            nlo, nhi = min(lo, n), max(hi, n)
+            if (0.0 if nhi == 0 else 1.0 - nlo / nhi) > eps:
+                break
+            lo, hi = nlo, nhi
+            i += 1
+        ranges.append((start, i))
+    return ranges
+
+
+@dataclass(frozen=True)
+class MatmulGroup:
+    start: int
+    end: int
+    mode: str
+    padded_rows: int = 0
+
+
+@dataclass(frozen=True)
+class GroupingStrategy:
+    """Partition of the scheduled offsets into matmul groups
+    (execution.py:258-293)."""
+
+    eps: float
+    threshold: float
+    schedule: tuple
+    groups: tuple
+    symmetric: bool
+    volume: int
+
+    def members(self, group: MatmulGroup) -> list[int]:
+        sched = list(self.schedule[group.start:group.end])
+        if self.symmetric:
+            sched += [self.volume - 1 - n for n in sched]
+        return sched
+
+    def validate(self, map_sizes) -> None:
+        sizes = np.asarray(map_sizes, dtype=np.int64)
+        if sizes.shape[0] != self.volume:
+            raise ValueError("map sizes do not match the strategy volume")
+        covered = []
+        for g in self.groups:
+            covered.extend(range(g.start, g.end))
+            mem = self.members(g)
+            hi = max((int(sizes[m]) for m in mem), default=0)
+            lo = min((int(sizes[m]) for m in mem), default=0)
+            if (g.mode == "batched") != (hi < self.threshold):
+                raise ValueError("group mode disagrees with the threshold")
+            if g.mode == "batched" and hi > 0 and 1.0 - lo / hi > self.eps + 1e-12:
+                raise ValueError("batched group exceeds the padding tolerance")
+        if covered != list(range(len(self.schedule))):
+            raise ValueError("groups do not partition the schedule")
+
+
+def schedule_for(offsets: KernelOffsets, stride: int) -> tuple[list[int], bool]:
+    """First half without centre + mirrors on stride-1 odd K, else all
+    offsets (execution.py:296-306)."""
+    c = offsets.center
+    if stride == 1 and c is not None and offsets.volume > 1:
+        return list(range(c)), True
+    return list(range(offsets.volume)), False
+
+
+def build_grouping(map_sizes, eps: float, threshold: float, schedule=None,
+                   symmetric: bool = False) -> GroupingStrategy:
+    """Concrete GroupingStrategy for a workload (execution.py:309-328)."""
+    sizes = np.asarray(map_sizes, dtype=np.int64)
+    schedule = list(range(sizes.shape[0])) if schedule is None else list(schedule)
+    groups = []
+    for start, end in partition_groups(sizes, eps, schedule):
+        mem = list(schedule[start:end])
+        if symmetric:
+            mem += [sizes.shape[0] - 1 - n for n in mem]
+        hi = max((int(sizes[m]) for m in mem), default=0)
+        if hi < threshold:
+            groups.append(MatmulGroup(start, end, "batched", sum(hi - int(sizes[m]) for m in mem)))
+        else:
+            groups.append(MatmulGroup(start, end, "sequential", 0))
+    return GroupingStrategy(eps, threshold, tuple(schedule), tuple(groups), symmetric,
+                            sizes.shape[0])
+
+
+# ====================================================================== GEMM
+
+def _segments(grouping: GroupingStrategy, slab_ptr: np.ndarray, sizes: np.ndarray,
+              extra=()) -> "ctypes.Array":
+    segs = []
+    seen = set()
+    for g in grouping.groups:
+        for m in grouping.members(g):
+            if m in seen or sizes[m] == 0:
+                continue
+            seen.add(m)
+            segs.append((int(slab_ptr[m]), int(slab_ptr[m]), int(sizes[m]), int(m), 0))
+    segs.extend(extra)
+    if len(segs) > nat.MAX_SEGMENTS:
+        raise ValueError("too many GEMM segments for one launch")
+    arr = (nat.SegmentT * max(len(segs), 1))()
+    for i, (a, c, r, b, src) in enumerate(segs):
+        arr[i].a_row, arr[i].c_row, arr[i].rows, arr[i].b_index, arr[i].a_src = a, c, r, b, src
+    return arr, len(segs)
+
+
+def _weights_for(w: WeightTensor, dtype):
+    if dtype == torch.float16:
+        packed, _, n_pad = w.packed_f16()
+        return packed, n_pad
+    return w.device_f32(), w.c_out
+
+
+def _grouped_gemm(dtype, buffer, rows_pad, features, w: WeightTensor, segs, nseg, c_rows):
+    wt, ldc = _weights_for(w, dtype)
+    partial = torch.empty((max(c_rows, 1), ldc), dtype=torch.float32, device=wt.device)
+    nat.call("scb_grouped_gemm", nat.dtype_code(dtype), nat.ptr(buffer), max(rows_pad, 1),
+             buffer.stride(0), nat.ptr(features), 0 if features is None else features.shape[0],
+             0 if features is None else features.stride(0), w.c_in, nat.ptr(wt), w.weights.shape[0],
+             w.c_out, nat.ptr(partial), max(c_rows, 1), ldc, segs, nseg, nat.stream_handle())
+    return partial, ldc
+
+
+def execute_groups(buffer, weights, strategy: GroupingStrategy, map_sizes) -> torch.Tensor:
+    """Grouped multiplies over an offset-partitioned buffer in the reference
+    layout (execution.py:331-368); returns the f32 partial buffer."""
+    sizes = np.asarray(map_sizes, dtype=np.int64)
+    if isinstance(weights, WeightTensor):
+        w = weights
+    else:
+        wa = np.asarray(weights.cpu() if isinstance(weights, torch.Tensor) else weights,
+                        dtype=np.float32)
+        w = WeightTensor(wa, wa.shape[0], 1)  # a plain (V, C_in, C_out) stack
+    if sizes.shape[0] != w.weights.shape[0]:
+        raise ValueError("map sizes do not match the weight slices")
+    strategy.validate(sizes)
+    b = _features_of(buffer)
+    starts = np.zeros(sizes.shape[0] + 1, dtype=np.int64)
+    np.cumsum(sizes, out=starts[1:])
+    if b.shape[0] != starts[-1]:
+        raise ValueError("buffer rows do not match the map sizes")
+    tile = nat.TILE_ROWS
+    slab = np.zeros_like(starts)
+    np.cumsum((sizes + tile - 1) // tile * tile, out=slab[1:])
+    rows_pad = int(slab[-1])
+    ld = _buffer_ld(b.dtype, b.shape[1])
+    padded = torch.zeros((max(rows_pad, 1), ld), dtype=b.dtype, device=b.device)
+    idx = [torch.arange(int(slab[n]), int(slab[n] + sizes[n])) for n in range(sizes.shape[0])
+           if sizes[n]]
+    prow = torch.cat(idx).to(b.device) if idx else torch.empty(0, dtype=torch.int64, device=b.device)
+    if prow.numel():
+        padded[prow, : b.shape[1]] = b
+    segs, nseg = _segments(strategy, slab, sizes)
+    partial, _ = _grouped_gemm(b.dtype, padded, rows_pad, None, w, segs, nseg, rows_pad)
+    return partial[prow, : w.c_out].contiguous()
+
+
+# ====================================================================== layers
+
+def _direct_center(dtype, c_in: int) -> bool:
+    """The centre offset reads the feature matrix in place when the TMA row
+    stride allows it (16-byte multiple); otherwise it is gathered too."""
+    return dtype == torch.float32 or c_in % 8 == 0
+
+
+def _run_dataflow(features: torch.Tensor, kmap: KernelMap, w: WeightTensor,
+                  grouping: GroupingStrategy, opts: ExecOptions, center: int | None,
+                  epilogue: dict | None = None) -> torch.Tensor:
+    """Gather -> grouped GEMM (+ centre) -> scatter; returns storage-dtype rows."""
+    label, timer = opts.layer_label, opts.timer
+    dt = features.dtype
+    c_in, c_out = w.c_in, w.c_out
+    direct = center is not None and _direct_center(dt, c_in)
+    plan = build_gather_scatter_plan(kmap, skip_center=direct)
+    if opts.plan_log is not None:
+        opts.plan_log.append((label, plan))
+    sizes = plan.sizes
+    with _timed(timer, label, "gather"):
+        buf = _gather_padded(features, plan, c_in)
+    extra = []
+    center_row = -1
+    c_rows = plan.rows_pad
+    if direct:
+        center_row = plan.rows_pad
+        extra.append((0, center_row, features.shape[0], center, 1))
+        c_rows += (features.shape[0] + nat.TILE_ROWS - 1) // nat.TILE_ROWS * nat.TILE_ROWS
+    elif center is not None and sizes[center]:
+        # centre gathered like any other offset (C_in not 16-byte aligned)
+        extra.append((int(plan.slab_ptr[center]), int(plan.slab_ptr[center]),
+                      int(sizes[center]), center, 0))
+    segs, nseg = _segments(grouping, plan.slab_ptr, sizes, extra)
+    with _timed(timer, label, "matmul"):
+        partial, ldc = _grouped_gemm(dt, buf, plan.rows_pad, features if direct else None, w,
+                                     segs, nseg, c_rows)
+    out = torch.empty((kmap.n_out, c_out), dtype=dt, device=features.device)
+    ep = epilogue or {}
+    with _timed(timer, label, "scatter"):
+        nat.call("scb_scatter", nat.ptr(partial), ldc, nat.ptr(plan.pos), plan.pos.shape[1],
+                 kmap.n_out, c_out, center_row, nat.dtype_code(dt), nat.ptr(out), c_out,
+                 nat.ptr(ep.get("scale")), nat.ptr(ep.get("shift")), nat.ptr(ep.get("bias")),
+                 int(bool(ep.get("relu", False))), nat.stream_handle())
+    return out
+
+
+def _pointwise_matmul(t: SparseTensor, w: WeightTensor, opts: ExecOptions, epilogue=None):
+    """K=1, s=1 fast path (execution.py:472-477): out = features @ W[0]."""
+    f = t.features
+    dt = f.dtype
+    n = f.shape[0]
+    n_rows = (n + nat.TILE_ROWS - 1) // nat.TILE_ROWS * nat.TILE_ROWS
+    if _direct_center(dt, w.c_in):
+        segs, nseg = _segments(GroupingStrategy(0, 0, (), (), False, 1), np.zeros(2, np.int64),
+                               np.zeros(1, np.int64), [(0, 0, n, 0, 1)])
+        partial, ldc = _grouped_gemm(dt, f, n, f, w, segs, nseg, n_rows)
+    else:
+        ld = _buffer_ld(dt, w.c_in)
+        buf = torch.zeros((max(n_rows, 1), ld), dtype=dt, device=f.device)
+        buf[:n, : w.c_in] = f
+        segs, nseg = _segments(GroupingStrategy(0, 0, (), (), False, 1), np.zeros(2, np.int64),
+                               np.zeros(1, np.int64), [(0, 0, n, 0, 0)])
+        partial, ldc = _grouped_gemm(dt, buf, n_rows, None, w, segs, nseg, n_rows)
+    out = torch.empty((n, w.c_out), dtype=dt, device=f.device)
+    ident = _identity_pos(n, f.device)
+    ep = epilogue or {}
+    nat.call("scb_scatter", nat.ptr(partial), ldc, nat.ptr(ident), 1, n, w.c_out, -1,
+             nat.dtype_code(dt), nat.ptr(out), w.c_out, nat.ptr(ep.get("scale")),
+             nat.ptr(ep.get("shift")), nat.ptr(ep.get("bias")), int(bool(ep.get("relu", False))),
+             nat.stream_handle())
+    return out
+
+
+_IDENT = {}
+
+
+def _identity_pos(n: int, device) -> torch.Tensor:
+    t = _IDENT.get(device)
+    if t is None or t.shape[0] < n:
+        t = torch.arange(max(n, 1024) * 2, dtype=torch.int32, device=device).view(-1, 1)
+        _IDENT[device] = t
+    return t[:max(n, 1)]
+
+
+def _record_workload(opts, spec, sizes, symmetric, schedule, in_coords, out_coords, boundary,
+                     batch_size):
+    if opts.workload_log is None:
+        return
+    opts.workload_log.append({
+        "layer": opts.layer_label, "map_sizes": np.asarray(sizes, dtype=np.int64),
+        "schedule": list(schedule), "symmetric": symmetric, "c_in": spec.c_in,
+        "c_out": spec.c_out, "kernel_size": spec.kernel_size, "stride": spec.stride,
+        "in_coords": in_coords, "out_coords": out_coords, "boundary": tuple(boundary),
+        "batch_size": batch_size})
+
+
+def _record_traffic(opts, plan, c_in, c_out, dtype, n_in, n_out):
+    """Algorithmic bytes of the staged path (SURVEY.md §8(d) formulas)."""
+    if opts.traffic_log is None:
+        return
+    e = 2 if dtype == torch.float16 else 4
+    m = plan.total
+    opts.traffic_log.append((opts.layer_label, {
+        "gather_bytes": e * n_in * c_in + e * m * c_in + 4 * m,
+        "scatter_bytes": 4 * m * c_out + e * n_out * c_out + 4 * m,
+        "gemm_flops": 2 * (plan.kmap.total) * c_in * c_out}))
+
+
+def _check_channels(t, w, spec, msg=None):
+    if t.num_channels != spec.c_in or w.c_in != spec.c_in or w.c_out != spec.c_out:
+        raise ValueError(msg or (
+            f"channel mismatch: tensor {t.num_channels}, spec {spec.c_in}->{spec.c_out}, "
+            f"weights {w.c_in}->{w.c_out}"))
+
+
+def sparse_conv_forward(t: SparseTensor, w: WeightTensor, spec: LayerSpec,
+                        strategy: LayerStrategy | None = None, map_cache: dict | None = None,
+                        options: ExecOptions | None = None, *,
+                        epilogue: dict | None = None) -> SparseTensor:
+    """One sparse convolution layer on the B200 (execution.py:450-509).
+
+    ``epilogue`` (B200 extension) fuses
+    ``{"scale", "shift", "bias", "relu"}`` into the scatter's single write."""
+    opts = options or ExecOptions()
+    _check_channels(t, w, spec)
+    label, timer = opts.layer_label, opts.timer
+    strat = resolve_strategy(spec, strategy)
+    if spec.kernel_size == 1 and spec.stride == 1:
+        with _timed(timer, label, "matmul"):
+            out = _pointwise_matmul(t, w, opts, epilogue)
+        _record_workload(opts, spec, np.array([t.num_points]), False, [0], t.coords, t.coords,
+                         t.boundary, t.batch_size)
+        return t.replace_features(out)
+
+    offsets = enumerate_offsets(t.spatial_dims, spec.kernel_size)
+    cset = t.coordset
+    with _timed(timer, label, "mapping"):
+        kind = opts.index_kind or strat.index_kind or spec.index_kind or "auto"
+        if kind == "grid" and _cells(t.boundary, t.batch_size) > opts.grid_cell_cap:
+            raise GridCapacityError(
+                f"grid index needs {_cells(t.boundary, t.batch_size)} cells "
+                f"(cap {opts.grid_cell_cap}); use the hash index")
+        key = (spec.kernel_size, spec.stride, offsets.base)
+        hit = cset.maps.get(key) if opts.map_reuse else None
+        if hit is None:
+            if spec.stride == 1:
+                out_boundary = t.boundary
+                out_cset = cset
+            else:
+                out_boundary = downsample_boundary(t.boundary, spec.stride)
+                oc = compute_output_coords(t, offsets, spec.stride, out_boundary, t.batch_size)
+                out_cset = CoordinateSet(oc, out_boundary, t.batch_size)
+            index = build_index(cset, kind, cell_cap=opts.grid_cell_cap)
+            kmap = map_search(index, out_cset.coords, offsets, spec.stride)
+            hit = (out_cset, kmap)
+            if opts.map_reuse:
+                cset.maps[key] = hit
+        out_cset, kmap = hit
+        if map_cache is not None and spec.reuse_key:
+            map_cache[spec.reuse_key] = CachedMap(kmap, t.coords, t.boundary, t.stride, cset)
+    schedule, symmetric = schedule_for(offsets, spec.stride)
+    sizes = kmap.sizes
+    center = offsets.center if (spec.stride == 1 and offsets.center is not None) else None
+    if center is not None:
+        sizes[center] = 0
+    _record_workload(opts, spec, sizes, symmetric, schedule, t.coords, out_cset.coords,
+                     t.boundary, t.batch_size)
+    grouping = build_grouping(sizes, strat.eps, strat.threshold, schedule, symmetric)
+    out = _run_dataflow(t.features, kmap, w, grouping, opts, center, epilogue)
+    with _timed(timer, label, "other"):
+        result = SparseTensor(None, out, stride=t.stride * spec.stride,
+                              boundary=out_cset.boundary, batch_size=t.batch_size,
+                              coordset=out_cset)
+        if opts.traffic_log is not None:
+            _record_traffic(opts, build_gather_scatter_plan(kmap, center is not None), spec.c_in,
+                            spec.c_out, t.features.dtype, t.num_points, kmap.n_out)
+    return result
+
+
+def inverse_conv_forward(t: SparseTensor, w: WeightTensor, spec: LayerSpec, map_cache: dict,
+                         strategy: LayerStrategy | None = None,
+                         options: ExecOptions | None = None, *,
+                         epilogue: dict | None = None) -> SparseTensor:
+    """Transposed layer replaying a cached strided map with roles swapped
+    (execution.py:512-551)."""
+    opts = options or ExecOptions()
+    _check_channels(t, w, spec, "channel mismatch on inverse layer")
+    if spec.reuse_key not in map_cache:
+        raise KeyError(f"no cached map under reuse key {spec.reuse_key!r}")
+    entry: CachedMap = map_cache[spec.reuse_key]
+    if entry.kmap.n_out != t.num_points:
+        raise ValueError("tensor does not match the cached map's output side")
+    if entry.kmap.offsets.kernel_size != spec.kernel_size:
+        raise ValueError("kernel size differs from the cached map")
+    label, timer = opts.layer_label, opts.timer
+    strat = resolve_strategy(spec, strategy)
+    with _timed(timer, label, "mapping"):
+        swapped = entry.kmap.swap_roles()
+    schedule = list(range(swapped.offsets.volume))
+    sizes = swapped.sizes
+    _record_workload(opts, spec, sizes, False, schedule, t.coords, entry.in_coords,
+                     entry.in_boundary, t.batch_size)
+    grouping = build_grouping(sizes, strat.eps, strat.threshold, schedule, False)
+    out = _run_dataflow(t.features, swapped, w, grouping, opts, None, epilogue)
+    with _timed(timer, label, "other"):
+        cset = entry.in_coordset or CoordinateSet(entry.in_coords, entry.in_boundary, t.batch_size)
+        result = SparseTensor(None, out, stride=entry.in_stride, boundary=entry.in_boundary,
+                              batch_size=t.batch_size, coordset=cset)
+    return result
+
+
+_POINTWISE = {"relu": 0, "bias_add": 1, "bn_fold": 2}
+
+
+def _param(x, c, name):
+    if x is None:
+        raise ValueError(f"{name} is required")
+    a = np.asarray(x.cpu() if isinstance(x, torch.Tensor) else x, dtype=np.float32)
+    if a.shape != (c,):
+        raise ValueError(f"{name} length must match the channel count")
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def pointwise_apply(t: SparseTensor, op: str, *, bias=None, scale=None,
+                    shift=None) -> SparseTensor:
+    """relu / bias_add / bn_fold on the device (execution.py:554-576)."""
+    if op not in _POINTWISE:
+        raise ValueError(f"unknown pointwise op {op!r}")
+    c = t.num_channels
+    a = b = None
+    if op == "bias_add":
+        try:
+            a = _param(bias, c, "bias")
+        except ValueError:
+            raise ValueError("bias length must match the channel count")
+    elif op == "bn_fold":
+        try:
+            a, b = _param(scale, c, "scale"), _param(shift, c, "shift")
+        except ValueError:
+            raise ValueError("scale/shift length must match the channel count")
+    out = t.features.clone()
+    nat.call("scb_pointwise", nat.dtype_code(out.dtype), nat.ptr(out), out.shape[0], c,
+             _POINTWISE[op], nat.ptr(a), nat.ptr(b), nat.stream_handle())
+    return t.replace_features(out)

@@ -1,0 +1,412 @@
+"""Kernel-map construction on the device: the drop-in twin of the reference's
+``mapping.py`` (offsets, indexes, output coordinates, map search, symmetric
+maps, gather/scatter plans).  Every function here enqueues sm_100a kernels
+from ``libsparseconv_b200.so``; the host only handles shapes and the one
+data-dependent size per map.
+
+Map entries follow the reference convention: entry ``(j, k)`` of offset ``n``
+means input coordinate ``p_j == stride * q_k + delta_n``; within an offset
+entries are sorted by output row ``k`` (mapping.py:289-319).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from itertools import product
+
+import numpy as np
+import torch
+
+from . import _native as nat
+from .core import CoordinateSet, as_device_coords
+
+MISS = -1
+
+# The reference's grid-index cell cap (mapping.py:21).  On the device "auto"
+# additionally refuses grids above DEVICE_GRID_CAP cells (an int32 table of
+# 512 MiB) and uses the hash index instead: maps are identical either way.
+DEFAULT_GRID_CELL_CAP = 1 << 31
+DEVICE_GRID_CAP = 1 << 27
+
+# Base of the per-dimension offset window for even K (mapping.py:23-26); the
+# reference's tests monkeypatch it to -1 as a negative control and so can ours.
+EVEN_KERNEL_OFFSET_BASE = 0
+
+
+class GridCapacityError(ValueError):
+    """Grid index would exceed its cell cap; build a hash index instead."""
+
+
+@dataclass(frozen=True, eq=False)
+class KernelOffsets:
+    """Ordered kernel offsets delta in Z^D, lexicographic (mapping.py:33-60)."""
+
+    offsets: np.ndarray
+    kernel_size: int
+    dim: int
+
+    def __post_init__(self):
+        off = np.ascontiguousarray(self.offsets, dtype=np.int64)
+        off.setflags(write=False)
+        object.__setattr__(self, "offsets", off)
+
+    @property
+    def volume(self) -> int:
+        return self.offsets.shape[0]
+
+    @property
+    def center(self) -> int | None:
+        return (self.volume - 1) // 2 if self.kernel_size % 2 == 1 else None
+
+    @property
+    def base(self) -> int:
+        """Lowest offset per dimension (what the kernels enumerate from)."""
+        return int(self.offsets[0, 0]) if self.volume else 0
+
+
+def enumerate_offsets(dim: int, kernel_size: int) -> KernelOffsets:
+    """All K**D offsets in lexicographic order (mapping.py:63-79)."""
+    if not 1 <= dim <= 4:
+        raise ValueError("dim must be between 1 and 4")
+    if kernel_size < 1:
+        raise ValueError("kernel_size must be >= 1")
+    lo = -((kernel_size - 1) // 2) if kernel_size % 2 == 1 else EVEN_KERNEL_OFFSET_BASE
+    axis = range(lo, lo + kernel_size)
+    return KernelOffsets(np.array(list(product(axis, repeat=dim)), dtype=np.int64).reshape(-1, dim),
+                         kernel_size, dim)
+
+
+def _cells(boundary, batch_size) -> int:
+    c = int(batch_size)
+    for b in boundary:
+        c *= int(b)
+    return c
+
+
+def _as_cset(coords, boundary, batch_size) -> CoordinateSet:
+    if isinstance(coords, CoordinateSet):
+        return coords
+    if hasattr(coords, "coordset"):  # a SparseTensor
+        return coords.coordset
+    return CoordinateSet(as_device_coords(coords), tuple(boundary), batch_size)
+
+
+class CoordinateIndex:
+    """Device coordinate index: open-addressing hash (HashIndex,
+    mapping.py:122-189) or dense grid (GridIndex, mapping.py:82-119)."""
+
+    def __init__(self, cset: CoordinateSet, kind: str):
+        self.kind = kind
+        self.boundary = cset.boundary
+        self.batch_size = cset.batch_size
+        self.size = cset.num_points
+        self._grid = nat.make_grid(self.boundary, self.batch_size)
+        dev = cset.coords.device
+        status = torch.zeros(2, dtype=torch.int32, device=dev)
+        if kind == "hash":
+            self.slots = int(nat.load().scb_hash_slots(self.size))
+            self.keys = torch.empty(self.slots, dtype=torch.int64, device=dev)
+            self.rows = torch.empty(self.slots, dtype=torch.int32, device=dev)
+            code = nat.SCB_INDEX_HASH
+        else:
+            self.slots = _cells(self.boundary, self.batch_size)
+            self.keys = None
+            self.rows = torch.empty(self.slots, dtype=torch.int32, device=dev)
+            code = nat.SCB_INDEX_GRID
+        self.code = code
+        nat.call("scb_index_build", code, nat.ptr(cset.coords), self.size, self._grid,
+                 nat.ptr(self.keys), nat.ptr(self.rows), self.slots, nat.ptr(status),
+                 nat.stream_handle())
+        self._status = status
+
+    @property
+    def duplicates(self) -> int:
+        return int(self._status[0].item())
+
+    def query(self, coords) -> torch.Tensor:
+        """Row per query coordinate; MISS (-1) where absent or out of bounds."""
+        q = as_device_coords(coords)
+        out = torch.empty(q.shape[0], dtype=torch.int32, device=q.device)
+        nat.call("scb_index_query", self.code, nat.ptr(q), q.shape[0], self._grid,
+                 nat.ptr(self.keys), nat.ptr(self.rows), self.slots, nat.ptr(out),
+                 nat.stream_handle())
+        return out
+
+
+def build_index(coords, kind: str = "auto", boundary=None, batch_size: int = 1,
+                cell_cap: int = DEFAULT_GRID_CELL_CAP) -> CoordinateIndex:
+    """Build (or reuse) a device coordinate index (mapping.py:195-208).
+    ``coords`` may be a SparseTensor, a CoordinateSet or raw coordinates with
+    ``boundary``/``batch_size``."""
+    cset = _as_cset(coords, boundary, batch_size)
+    cells = _cells(cset.boundary, cset.batch_size)
+    if kind == "grid":
+        if cells > cell_cap:
+            raise GridCapacityError(
+                f"grid index needs {cells} cells (cap {cell_cap}); use the hash index")
+    elif kind == "auto":
+        kind = "grid" if cells <= min(cell_cap, DEVICE_GRID_CAP) else "hash"
+    elif kind != "hash":
+        raise ValueError(f"unknown index kind {kind!r}")
+    idx = cset.indexes.get(kind)
+    if idx is None:
+        idx = CoordinateIndex(cset, kind)
+        cset.indexes[kind] = idx
+    return idx
+
+
+def downsample_boundary(boundary, stride: int) -> tuple[int, ...]:
+    """ceil(b / stride) per dimension (mapping.py:211-213)."""
+    return tuple(-(-int(b) // stride) for b in boundary)
+
+
+def compute_output_coords(in_coords, offsets: KernelOffsets, stride: int, out_boundary,
+                          batch_size: int = 1) -> torch.Tensor:
+    """Active output coordinates (mapping.py:216-248).  Stride 1 returns the
+    input coordinates; stride > 1 runs the fused candidate kernel and a 64-bit
+    radix sort + unique, so rows come out in ascending flat-key order.
+    Returns an int32 device tensor."""
+    if stride < 1:
+        raise ValueError("stride must be >= 1")
+    c = in_coords.coords if hasattr(in_coords, "coords") else as_device_coords(in_coords)
+    if stride == 1:
+        return c
+    dim = c.shape[1] - 1
+    lib = nat.load()
+    n_in = c.shape[0]
+    grid = nat.make_grid(out_boundary, batch_size)
+    cap = int(lib.scb_output_coords_capacity(n_in, dim, offsets.kernel_size, stride))
+    ws_bytes = int(lib.scb_output_coords_workspace(n_in, dim, offsets.kernel_size, stride))
+    ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=c.device)
+    keys = torch.empty(max(cap, 1), dtype=torch.int64, device=c.device)
+    n_out = torch.zeros(1, dtype=torch.int64, device=c.device)
+    nat.call("scb_output_coords", nat.ptr(c), n_in, grid, offsets.kernel_size, offsets.base,
+             stride, nat.ptr(ws), ws_bytes, nat.ptr(keys), nat.ptr(n_out), nat.stream_handle())
+    n = int(n_out.item())
+    out = torch.empty((n, dim + 1), dtype=torch.int32, device=c.device)
+    nat.call("scb_unflatten", nat.ptr(keys), n, grid, nat.ptr(out), nat.stream_handle())
+    return out
+
+
+def _compact(hits: torch.Tensor, volume: int, n_out: int):
+    """Hit matrix [V][n_out] -> CSR map (offset_ptr device, sizes host,
+    in_idx, out_idx).  One D2H of V+1 int64 (the map sizes)."""
+    lib = nat.load()
+    dev = hits.device
+    ws = torch.empty(max(int(lib.scb_map_workspace(volume, n_out)), 8), dtype=torch.uint8,
+                     device=dev)
+    ptr = torch.empty(volume + 1, dtype=torch.int64, device=dev)
+    s = nat.stream_handle()
+    nat.call("scb_map_count", nat.ptr(hits), volume, n_out, nat.ptr(ws), nat.ptr(ptr), s)
+    host_ptr = ptr.cpu().numpy()
+    total = int(host_ptr[-1])
+    in_idx = torch.empty(max(total, 1), dtype=torch.int32, device=dev)
+    out_idx = torch.empty(max(total, 1), dtype=torch.int32, device=dev)
+    nat.call("scb_map_compact", nat.ptr(hits), volume, n_out, nat.ptr(ws), nat.ptr(ptr),
+             nat.ptr(in_idx), nat.ptr(out_idx), s)
+    return ptr, np.diff(host_ptr).astype(np.int64), in_idx[:total], out_idx[:total]
+
+
+class KernelMap:
+    """Per-offset (input row, output row) pairs in device CSR form
+    (mapping.py:251-286)."""
+
+    def __init__(self, offset_ptr, sizes, in_idx, out_idx, offsets: KernelOffsets, stride: int,
+                 n_in: int, n_out: int, symmetric: bool = False, trusted: bool = False):
+        self.trusted = bool(trusted)          # produced by map_search: one entry per (k, n)
+        self.offset_ptr = offset_ptr        # device int64 [V+1]
+        self._sizes = np.asarray(sizes, dtype=np.int64)
+        self.in_idx = in_idx                # device int32 [|M|]
+        self.out_idx = out_idx              # device int32 [|M|]
+        self.offsets = offsets
+        self.stride = int(stride)
+        self.n_in = int(n_in)
+        self.n_out = int(n_out)
+        self.symmetric = bool(symmetric)
+        self._pairs = None
+        self._plans = {}
+        self._swapped = None
+
+    @property
+    def sizes(self) -> np.ndarray:
+        return self._sizes.copy()
+
+    @property
+    def buffer_offsets(self) -> np.ndarray:
+        out = np.zeros(self._sizes.shape[0] + 1, dtype=np.int64)
+        np.cumsum(self._sizes, out=out[1:])
+        return out
+
+    @property
+    def total(self) -> int:
+        return int(self._sizes.sum())
+
+    @property
+    def pairs(self) -> list[np.ndarray]:
+        """Host copy in the reference layout: one (m_n, 2) int64 array per offset."""
+        if self._pairs is None:
+            j = self.in_idx.cpu().numpy().astype(np.int64)
+            k = self.out_idx.cpu().numpy().astype(np.int64)
+            st = self.buffer_offsets
+            self._pairs = [np.stack([j[st[n]:st[n + 1]], k[st[n]:st[n + 1]]], axis=1)
+                           for n in range(self._sizes.shape[0])]
+        return self._pairs
+
+    def swap_roles(self) -> "KernelMap":
+        """Input/output roles exchanged, entries re-sorted by the new output
+        row (mapping.py:277-286): a transposed hit matrix plus compaction."""
+        if self._swapped is None:
+            V = self._sizes.shape[0]
+            hits = torch.empty((V, max(self.n_in, 1)), dtype=torch.int32,
+                               device=self.in_idx.device)
+            nat.call("scb_map_transpose", nat.ptr(self.offset_ptr), nat.ptr(self.in_idx),
+                     nat.ptr(self.out_idx), V, self.total, self.n_in, nat.ptr(hits),
+                     nat.stream_handle())
+            ptr, sizes, ii, oi = _compact(hits, V, self.n_in)
+            self._swapped = KernelMap(ptr, sizes, ii, oi, self.offsets, self.stride,
+                                      self.n_out, self.n_in, trusted=self.trusted)
+        return self._swapped
+
+
+def map_search(in_index: CoordinateIndex, out_coords, offsets: KernelOffsets, stride: int,
+               use_symmetry: bool | None = None) -> KernelMap:
+    """Kernel map: entry (j, k) whenever stride*q_k + delta_n is input j
+    (mapping.py:289-319).  Stride-1 odd-K maps probe only offsets up to the
+    centre and fill the mirrored half in the same pass (mapping.py:322-339)."""
+    oc = out_coords.coords if hasattr(out_coords, "coords") else as_device_coords(out_coords)
+    volume, center = offsets.volume, offsets.center
+    if use_symmetry is None:
+        use_symmetry = stride == 1 and center is not None and volume > 1
+    if use_symmetry and (stride != 1 or center is None):
+        raise ValueError("symmetric search requires stride 1 and odd kernel size")
+    n_out = oc.shape[0]
+    if use_symmetry and n_out != in_index.size:
+        raise ValueError("symmetric search needs the output set to equal the input set")
+    hits = torch.empty((volume, max(n_out, 1)), dtype=torch.int32, device=oc.device)
+    grid = nat.make_grid(in_index.boundary, in_index.batch_size)
+    nat.call("scb_map_search", in_index.code, nat.ptr(oc), n_out, grid, offsets.kernel_size,
+             offsets.base, stride, int(bool(use_symmetry)), nat.ptr(in_index.keys),
+             nat.ptr(in_index.rows), in_index.slots, nat.ptr(hits), nat.stream_handle())
+    ptr, sizes, ii, oi = _compact(hits, volume, n_out)
+    return KernelMap(ptr, sizes, ii, oi, offsets, stride, in_index.size, n_out,
+                     symmetric=bool(use_symmetry), trusted=True)
+
+
+def derive_symmetric_maps(half_map: KernelMap) -> KernelMap:
+    """Complete a stride-1 odd-K map from its lower half (mapping.py:322-339):
+    M[V-1-n] = reversed M[n], sorted by the new output row."""
+    if half_map.stride != 1:
+        raise ValueError("symmetric maps exist only for stride-1 layers")
+    center = half_map.offsets.center
+    if center is None:
+        raise ValueError("symmetric maps exist only for odd kernel sizes")
+    V, n = half_map.offsets.volume, half_map.n_out
+    dev = half_map.in_idx.device
+    s = nat.stream_handle()
+    # direct rows: hits[m][k] = j  (the transpose kernel with roles exchanged)
+    direct = torch.empty((V, max(n, 1)), dtype=torch.int32, device=dev)
+    nat.call("scb_map_transpose", nat.ptr(half_map.offset_ptr), nat.ptr(half_map.out_idx),
+             nat.ptr(half_map.in_idx), V, half_map.total, n, nat.ptr(direct), s)
+    mirror = torch.empty_like(direct)
+    nat.call("scb_map_transpose", nat.ptr(half_map.offset_ptr), nat.ptr(half_map.in_idx),
+             nat.ptr(half_map.out_idx), V, half_map.total, n, nat.ptr(mirror), s)
+    hits = direct.clone()
+    lower = torch.arange(center, device=dev)
+    hits[V - 1 - lower] = mirror[lower]
+    ptr, sizes, ii, oi = _compact(hits, V, n)
+    return KernelMap(ptr, sizes, ii, oi, half_map.offsets, 1, half_map.n_in, n, symmetric=True,
+                     trusted=True)
+
+
+class GatherScatterPlan:
+    """Device plan over a kernel map (mapping.py:342-418).
+
+    B200 layout: offset n's buffer slice starts at ``slab_ptr[n]``, a multiple
+    of the GEMM tile height, so no tile straddles two offsets.  ``buf_in``
+    (input row per buffer row, -1 on padding) drives the gather and ``pos``
+    ([n_out][V], buffer row per output and offset) drives the
+    output-stationary scatter.  The reference's compact CSR views
+    (``row_input``, ``in_indptr``, ...) are available as host arrays."""
+
+    def __init__(self, kmap: KernelMap, skip_center: bool = False, tile_rows: int = nat.TILE_ROWS):
+        skipped = None
+        if skip_center:
+            skipped = kmap.offsets.center
+            if skipped is None or kmap.stride != 1:
+                raise ValueError("skip_center requires a stride-1 odd-K map")
+        self.kmap = kmap
+        self.n_in, self.n_out = kmap.n_in, kmap.n_out
+        self.skipped_offset = skipped
+        self.tile_rows = int(tile_rows)
+        sizes = kmap.sizes
+        if skipped is not None:
+            sizes[skipped] = 0
+        self._sizes = sizes
+        self.buffer_offsets = np.zeros(sizes.shape[0] + 1, dtype=np.int64)
+        np.cumsum(sizes, out=self.buffer_offsets[1:])
+        self.total = int(self.buffer_offsets[-1])
+        padded = (sizes + tile_rows - 1) // tile_rows * tile_rows
+        self.slab_ptr = np.zeros(sizes.shape[0] + 1, dtype=np.int64)
+        np.cumsum(padded, out=self.slab_ptr[1:])
+        self.rows_pad = int(self.slab_ptr[-1])
+        V = sizes.shape[0]
+        dev = kmap.in_idx.device
+        self.buf_in = torch.empty(max(self.rows_pad, 1), dtype=torch.int32, device=dev)
+        self.pos = torch.empty((max(self.n_out, 1), V), dtype=torch.int32, device=dev)
+        status = None if kmap.trusted else torch.zeros(1, dtype=torch.int32, device=dev)
+        nat.call("scb_plan_build", nat.ptr(kmap.offset_ptr), nat.ptr(kmap.in_idx),
+                 nat.ptr(kmap.out_idx), V, kmap.total, self.n_out,
+                 -1 if skipped is None else skipped, self.tile_rows, nat.ptr(self.buf_in),
+                 self.rows_pad, nat.ptr(self.pos), nat.ptr(status), nat.stream_handle())
+        if status is not None and int(status.item()):
+            raise ValueError("kernel map has more than one entry for an (output, offset) pair")
+        self._csr = None
+
+    @property
+    def sizes(self) -> np.ndarray:
+        return self._sizes.copy()
+
+    # ---- reference CSR views (host numpy, computed on demand) -------------
+    def _views(self):
+        if self._csr is None:
+            pairs = self.kmap.pairs
+            kept = [p for n, p in enumerate(pairs) if n != self.skipped_offset and p.shape[0]]
+            st = np.concatenate(kept, 0) if kept else np.empty((0, 2), np.int64)
+            ri, ro = np.ascontiguousarray(st[:, 0]), np.ascontiguousarray(st[:, 1])
+            ip = np.zeros(self.n_in + 1, np.int64)
+            np.cumsum(np.bincount(ri, minlength=self.n_in), out=ip[1:])
+            op = np.zeros(self.n_out + 1, np.int64)
+            np.cumsum(np.bincount(ro, minlength=self.n_out), out=op[1:])
+            self._csr = dict(row_input=ri, row_output=ro, in_indptr=ip,
+                             in_rows=np.argsort(ri, kind="stable").astype(np.int64),
+                             out_indptr=op, out_rows=np.argsort(ro, kind="stable").astype(np.int64))
+        return self._csr
+
+    row_input = property(lambda self: self._views()["row_input"])
+    row_output = property(lambda self: self._views()["row_output"])
+    in_indptr = property(lambda self: self._views()["in_indptr"])
+    in_rows = property(lambda self: self._views()["in_rows"])
+    out_indptr = property(lambda self: self._views()["out_indptr"])
+    out_rows = property(lambda self: self._views()["out_rows"])
+    in_counts = property(lambda self: np.diff(self.in_indptr))
+    out_counts = property(lambda self: np.diff(self.out_indptr))
+
+    def padded_rows(self, compact: torch.Tensor) -> torch.Tensor:
+        """Index of each compact (reference-layout) buffer row in the padded
+        device layout."""
+        idx = [torch.arange(self.slab_ptr[n], self.slab_ptr[n] + self._sizes[n])
+               for n in range(self._sizes.shape[0]) if self._sizes[n]]
+        if not idx:
+            return torch.empty(0, dtype=torch.int64, device=compact.device)
+        return torch.cat(idx).to(compact.device)
+
+
+def build_gather_scatter_plan(kmap: KernelMap, skip_center: bool = False) -> GatherScatterPlan:
+    """Lay out the buffer and build both stationary indexes (mapping.py:377-418);
+    cached on the map."""
+    key = bool(skip_center)
+    plan = kmap._plans.get(key)
+    if plan is None:
+        plan = GatherScatterPlan(kmap, skip_center)
+        kmap._plans[key] = plan
+    return plan
