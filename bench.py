@@ -1,0 +1,408 @@
+"""Benchmark: MinkUNet scans/sec on SemanticKITTI-shaped synthetic scans
+(BASELINE.json metric).
+
+    python bench.py [--gpus N --steps K --warmup W --impl {engine,reference}]
+
+One process per GPU (torchrun for N > 1).  Scans are independent, so every
+rank runs its own batch of scans (seeds rank*B .. rank*B+B-1, packed into one
+batched SparseTensor with a shared boundary) with no data-path collective:
+weak scaling.  Default workload = config 5's per-GPU shard: MinkUNet 1.0x,
+FP16 feature storage, B = 8 scans per GPU per step (64 scans at N = 8).
+
+`value`   whole-job scans/s with inputs resident in HBM (device-timed with
+          CUDA events, max over ranks), L2 flushed between timed steps.
+`e2e`     the same through the public API with host buffers: pinned H2D of
+          coords + features, SparseTensor construction (validated),
+          Network forward, D2H of the logits, every step.
+`roofline` the dominant stage kernel (algorithmic bytes / its event time).
+`cpu_baseline` the CPU oracle port of the same graph on this host (rank 0,
+          N = 1), on a bounded sample (azimuth sectors of a scan).
+`--impl reference` times that CPU path alone (the reference arm).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "MinkUNet scans/sec (SemanticKITTI shape)"
+UNIT = "scans/s"
+SECTORS = 8
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("engine", "reference"), default="engine")
+    ap.add_argument("--width", type=float, default=1.0)
+    ap.add_argument("--scans-per-gpu", type=int, default=8)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ data
+
+def load_scans(seeds):
+    from paper_2204_10319_b200 import workloads
+    cache = Path(os.environ.get("SCB_SCAN_CACHE", "/tmp/scb_scans"))
+    out = []
+    for s in seeds:
+        f = cache / f"scan{s}.npz"
+        if f.exists():
+            d = np.load(f)
+            out.append((d["c"], d["f"], tuple(int(x) for x in d["b"])))
+            continue
+        c, fe, b = workloads.semantickitti_scan(s)
+        try:
+            cache.mkdir(parents=True, exist_ok=True)
+            np.savez(f, c=c, f=fe, b=np.array(b))
+        except OSError:
+            pass
+        out.append((c, fe, b))
+    return out
+
+
+def pack(scans):
+    """B scans -> one batched tensor with a shared boundary (SURVEY §8(e):
+    bit-identical to separate runs)."""
+    boundary = tuple(int(max(s[2][d] for s in scans)) for d in range(3))
+    coords = np.concatenate([np.concatenate([np.full((s[0].shape[0], 1), i, np.int64),
+                                             s[0][:, 1:]], 1) for i, s in enumerate(scans)])
+    feats = np.concatenate([s[1] for s in scans]).astype(np.float32)
+    return coords, feats, boundary
+
+
+def sectors(scan, n=SECTORS):
+    """Azimuth sectors of one scan (features hold absolute x, y)."""
+    c, f, b = scan
+    ang = np.mod(np.arctan2(f[:, 1], f[:, 0]), 2 * np.pi)
+    sid = np.minimum((ang / (2 * np.pi / n)).astype(int), n - 1)
+    return [(c[sid == k], f[sid == k], b) for k in range(n)]
+
+
+# ------------------------------------------------------------------ CPU path (oracle port)
+
+_W = {}
+
+
+def _cpu_worker_init(width):
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    from paper_2204_10319_b200.minkunet import build_params
+    _W["width"] = width
+    _W["params"] = build_params(width, 4, 0)
+
+
+def _cpu_worker_run(item):
+    from oracle import sparseconv_oracle as O
+    from paper_2204_10319_b200.minkunet import forward_oracle
+    c, f, b = item
+    t0 = time.perf_counter()
+    forward_oracle(_W["params"], _W["width"], c, O.quantize(f, "fp16"), b)
+    return time.perf_counter() - t0
+
+
+class CpuPath:
+    """The reference's CPU path (oracle port) over P worker processes, each
+    running the full MinkUNet graph on one azimuth sector (1/8 scan) per step."""
+
+    def __init__(self, width, scans, procs):
+        import multiprocessing as mp
+        os.environ["OPENBLAS_NUM_THREADS"] = "1"
+        os.environ["OMP_NUM_THREADS"] = "1"
+        os.environ["MKL_NUM_THREADS"] = "1"
+        self.items = [sec for s in scans for sec in sectors(s)]
+        self.procs = max(1, min(procs, len(self.items)))
+        self.pool = mp.get_context("spawn").Pool(self.procs, _cpu_worker_init, (width,))
+        self.cursor = 0
+
+    def step(self):
+        batch = [self.items[(self.cursor + i) % len(self.items)] for i in range(self.procs)]
+        self.cursor += self.procs
+        t0 = time.perf_counter()
+        self.pool.map(_cpu_worker_run, batch, chunksize=1)
+        return time.perf_counter() - t0, self.procs / SECTORS  # seconds, scans processed
+
+    def close(self):
+        self.pool.close()
+        self.pool.join()
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def run_reference(args):
+    """--impl reference: rank 0 alone times the CPU path; others exit."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    n_scans = 2
+    scans = load_scans(range(n_scans))
+    procs = min(os.cpu_count() or 1, 64)
+    cpu = CpuPath(args.width, scans, procs)
+    for _ in range(args.warmup):
+        cpu.step()
+    secs, done = 0.0, 0.0
+    for _ in range(args.steps):
+        s, d = cpu.step()
+        secs += s
+        done += d
+    cpu.close()
+    value = done / secs
+    sample = (f"{cpu.procs} worker processes x 1 azimuth sector (1/{SECTORS} scan) of MinkUNet "
+              f"{args.width}x per step, FP16 storage, oracle port (numpy/OpenBLAS 1 thread each)")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f16-storage/f32-accumulate", "data": "synthetic",
+        "config": workload_config(args, 1),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cpu.procs, "kind": "port",
+                         "sample": sample, "cpu": cpu_model()},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(args, world):
+    return {"workload": f"MinkUNet {args.width}x, {args.scans_per_gpu} SemanticKITTI-shaped "
+                        f"raycast scans per GPU per step (~120k voxels each, 0.05 m), FP16 storage",
+            "model": f"MinkUNet-{args.width}x", "global_batch": args.scans_per_gpu * world,
+            "scans_per_gpu": args.scans_per_gpu, "parallelism": f"scan-sharded x{world}",
+            "l2": "flushed (256 MiB write) before every timed step; per-step buffers >> L2"}
+
+
+# ------------------------------------------------------------------ clocks
+
+class Clocks:
+    def __init__(self, path):
+        self.path = path
+        self.proc = None
+
+    def start(self):
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "--query-gpu=index,clocks.sm,clocks.max.sm,power.draw,"
+                 "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=self.fh, stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def stop(self, gpu_index):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait()
+        self.fh.close()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            p = [x.strip() for x in line.split(",")]
+            if len(p) < 9 or p[0] != str(gpu_index):
+                continue
+            try:
+                sm.append(float(p[1]))
+                mx = float(p[2])
+            except ValueError:
+                continue
+            for name, v in zip(names, p[5:9]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ engine
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+
+    import paper_2204_10319_b200 as sc
+    from paper_2204_10319_b200 import _native as nat
+    from paper_2204_10319_b200.minkunet import EngineMinkUNet
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    B = args.scans_per_gpu
+
+    scans = load_scans(range(rank * B, rank * B + B))
+    coords, feats, boundary = pack(scans)
+    model = EngineMinkUNet(args.width, 4, 0)
+    coords_d = torch.from_numpy(coords.astype(np.int32)).to(dev)
+    feats_d = torch.from_numpy(feats).to(dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def step(timer=None, traffic=None):
+        t = sc.SparseTensor(coords_d, feats_d, 1, boundary, B, validate=False)
+        t = sc.quantize_features(t, sc.PrecisionMode.FP16_STORAGE)
+        return model.forward(t, sc.ExecOptions(timer=timer, traffic_log=traffic,
+                                               index_kind="hash"))
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # ---------------- device-resident timed region
+    timer, traffic = sc.StageTimer(), []
+    clocks = Clocks(str(ROOT / f"gpurun_out/clocks_rank{rank}.csv")
+                    if (ROOT / "gpurun_out").exists() else f"/tmp/clocks_rank{rank}.csv")
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    clocks.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = nat.load().scb_launch_count()
+    for i in range(args.steps):
+        flush.fill_(i & 0xFF)  # L2 flush, outside the step's events
+        evs[i][0].record()
+        out = step(timer, traffic)
+        evs[i][1].record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = nat.load().scb_launch_count() - launches0
+    clk = clocks.stop(local)
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    total_s = torch.tensor(sum(step_ms) / 1e3, device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(total_s, op=dist.ReduceOp.MAX)
+    total_s = float(total_s)
+    value = B * world * args.steps / total_s
+
+    # ---------------- roofline of the dominant stage kernel
+    stages = {}
+    for (layer, stage), s in timer.samples.items():
+        stages[stage] = stages.get(stage, 0.0) + s
+    bytes_by = {"gather": 0, "matmul": 0, "scatter": 0}
+    flops = 0
+    for _, rec in traffic:
+        bytes_by["gather"] += rec["gather_bytes"]
+        bytes_by["matmul"] += rec["gemm_bytes"]
+        bytes_by["scatter"] += rec["scatter_bytes"]
+        flops += rec["gemm_flops"]
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) \
+        if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    tc_peak = peaks.get("bf16_tflops", 1590.0)
+    dom = max(("gather", "matmul", "scatter"), key=lambda k: stages.get(k, 0.0))
+    kernel_name = {"gather": "scb gather_kernel", "matmul": "scb grouped_gemm_f16_kernel (tcgen05)",
+                   "scatter": "scb scatter_kernel"}[dom]
+    ach = bytes_by[dom] / stages[dom] / 1e9
+    roof = {"bound": "hbm", "kernel": kernel_name, "achieved": ach, "peak": hbm_peak,
+            "unit": "GB/s", "frac": ach / hbm_peak, "traffic": None,
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6.65 TB/s",
+            "per_stage": {k: {"ms_per_step": 1e3 * stages.get(k, 0.0) / args.steps,
+                              "GBps": (bytes_by[k] / stages[k] / 1e9) if stages.get(k) else None}
+                          for k in ("gather", "matmul", "scatter")},
+            "gemm_tflops": flops / stages["matmul"] / 1e12 if stages.get("matmul") else None,
+            "gemm_tensor_frac": (flops / stages["matmul"] / 1e12) / tc_peak
+            if stages.get("matmul") else None,
+            "mapping_ms_per_step": 1e3 * stages.get("mapping", 0.0) / args.steps,
+            "other_ms_per_step": 1e3 * stages.get("other", 0.0) / args.steps}
+
+    # ---------------- end to end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        h_coords = torch.from_numpy(coords.astype(np.int32)).pin_memory()
+        h_feats = torch.from_numpy(feats).pin_memory()
+        h_out = torch.empty((coords.shape[0], 19), dtype=torch.float16).pin_memory()
+
+        def e2e_step():
+            c = h_coords.to(dev, non_blocking=True)
+            f = h_feats.to(dev, non_blocking=True)
+            t = sc.SparseTensor(c, f, 1, boundary, B)  # validated, as a user would
+            t = sc.quantize_features(t, sc.PrecisionMode.FP16_STORAGE)
+            o = model.forward(t, sc.ExecOptions(index_kind="hash"))
+            h_out.copy_(o.features, non_blocking=True)
+            return o
+
+        for _ in range(args.warmup):
+            e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            e2e_step()
+        e1.record()
+        torch.cuda.synchronize()
+        es = torch.tensor(e0.elapsed_time(e1) / 1e3, device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(es, op=dist.ReduceOp.MAX)
+        e2e = {"value": B * world * args.steps / float(es), "unit": UNIT,
+               "h2d_bytes_per_step": int(h_coords.numel() * 4 + h_feats.numel() * 4),
+               "d2h_bytes_per_step": int(h_out.numel() * 2),
+               "path": "pinned H2D -> SparseTensor(validate) -> quantize -> MinkUNet -> D2H logits"}
+
+    # ---------------- CPU baseline (rank 0, N = 1)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        procs = min(os.cpu_count() or 1, 64)
+        path = CpuPath(args.width, scans[:2], procs)
+        path.step()  # warm (spawn + imports)
+        secs, done = 0.0, 0.0
+        while secs < args.cpu_seconds:
+            s, d = path.step()
+            secs += s
+            done += d
+        path.close()
+        cpu = {"value": done / secs, "unit": UNIT, "cores": path.procs, "kind": "port",
+               "sample": f"{path.procs} processes x 1 azimuth sector (1/{SECTORS} scan) per round,"
+                         f" {done:.2f} scans in {secs:.1f} s; oracle port of the same MinkUNet "
+                         "graph (numpy, 1 BLAS thread per process)", "cpu": cpu_model()}
+
+    if world > 1:
+        dist.barrier()
+    if rank == 0:
+        n_vox = int(coords.shape[0])
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * total_s / args.steps,
+            "ms_per_scan": 1e3 * total_s / (args.steps * B), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f16-storage/f32-accumulate",
+            "data": "synthetic (raycast LiDAR scans, random-init weights)",
+            "config": dict(workload_config(args, world), voxels_per_gpu=n_vox),
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+            "clocks": clk, "step_ms": step_ms,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -66,6 +66,9 @@ const char* scb_last_error(void);
 int32_t scb_abi_version(void);
 /* Number of SMs of the current device (for grid sizing in the host layer). */
 int32_t scb_device_sm_count(void);
+/* Kernels this library has launched in this process (CUB sort passes inside
+ * scb_output_coords excluded). */
+int64_t scb_launch_count(void);
 
 /* ---------------------------------------------------------------- index
  * Replaces HashIndex (mapping.py:122-189), GridIndex (mapping.py:82-119) and

@@ -46,6 +46,7 @@ _SIGS = {
     "scb_last_error": (ctypes.c_char_p, []),
     "scb_abi_version": (_I32, []),
     "scb_device_sm_count": (_I32, []),
+    "scb_launch_count": (_I64, []),
     "scb_hash_slots": (_I64, [_I64]),
     "scb_index_build": (_I32, [_I32, _P, _I64, _GP, _P, _P, _I64, _P, _P]),
     "scb_index_query": (_I32, [_I32, _P, _I64, _GP, _P, _P, _I64, _P, _P]),

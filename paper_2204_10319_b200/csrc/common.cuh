@@ -30,7 +30,15 @@ void set_error(const std::string& msg);
     }                                                                               \
   } while (0)
 
-#define SCB_LAUNCHED() SCB_CUDA(cudaGetLastError())
+// Every kernel launch site of the library is followed by SCB_LAUNCHED(), which
+// checks the launch and bumps the process-wide launch counter
+// (scb_launch_count, used by bench.py's gpu_launches).
+void count_launch();
+#define SCB_LAUNCHED()          \
+  do {                          \
+    ::scb::count_launch();      \
+    SCB_CUDA(cudaGetLastError()); \
+  } while (0)
 
 inline cudaStream_t as_stream(scb_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
 

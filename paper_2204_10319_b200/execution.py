@@ -181,11 +181,18 @@ def _buffer_ld(dtype, c: int) -> int:
     return (c + 7) // 8 * 8 if dtype == torch.float16 else c
 
 
+def _ld(t: torch.Tensor | None) -> int:
+    """Row stride in elements (torch reports odd strides for 0-row tensors)."""
+    if t is None:
+        return 0
+    return t.stride(0) if t.shape[0] > 1 else t.shape[1]
+
+
 def _gather_padded(features: torch.Tensor, plan: GatherScatterPlan, c: int) -> torch.Tensor:
     ld = _buffer_ld(features.dtype, c)
     buf = torch.empty((max(plan.rows_pad, 1), ld), dtype=features.dtype, device=features.device)
     nat.call("scb_gather", nat.dtype_code(features.dtype), nat.ptr(features), features.shape[0], c,
-             features.stride(0), nat.ptr(plan.buf_in), plan.rows_pad, nat.ptr(buf), ld,
+             _ld(features), nat.ptr(plan.buf_in), plan.rows_pad, nat.ptr(buf), ld,
              nat.stream_handle())
     return buf
 
@@ -350,8 +357,8 @@ def _grouped_gemm(dtype, buffer, rows_pad, features, w: WeightTensor, segs, nseg
     wt, ldc = _weights_for(w, dtype)
     partial = torch.empty((max(c_rows, 1), ldc), dtype=torch.float32, device=wt.device)
     nat.call("scb_grouped_gemm", nat.dtype_code(dtype), nat.ptr(buffer), max(rows_pad, 1),
-             buffer.stride(0), nat.ptr(features), 0 if features is None else features.shape[0],
-             0 if features is None else features.stride(0), w.c_in, nat.ptr(wt), w.weights.shape[0],
+             _ld(buffer), nat.ptr(features), 0 if features is None else features.shape[0],
+             0 if features is None else _ld(features), w.c_in, nat.ptr(wt), w.weights.shape[0],
              w.c_out, nat.ptr(partial), max(c_rows, 1), ldc, segs, nseg, nat.stream_handle())
     return partial, ldc
 
@@ -434,6 +441,9 @@ def _run_dataflow(features: torch.Tensor, kmap: KernelMap, w: WeightTensor,
                  kmap.n_out, c_out, center_row, nat.dtype_code(dt), nat.ptr(out), c_out,
                  nat.ptr(ep.get("scale")), nat.ptr(ep.get("shift")), nat.ptr(ep.get("bias")),
                  int(bool(ep.get("relu", False))), nat.stream_handle())
+    if opts.traffic_log is not None:
+        _record_traffic(opts, plan, c_in, c_out, dt, features.shape[0], kmap.n_out,
+                        features.shape[0] if direct else 0, kmap.total)
     return out
 
 
@@ -487,16 +497,20 @@ def _record_workload(opts, spec, sizes, symmetric, schedule, in_coords, out_coor
         "batch_size": batch_size})
 
 
-def _record_traffic(opts, plan, c_in, c_out, dtype, n_in, n_out):
-    """Algorithmic bytes of the staged path (SURVEY.md §8(d) formulas)."""
-    if opts.traffic_log is None:
-        return
+def _record_traffic(opts, plan, c_in, c_out, dtype, n_in, n_out, n_center, m_total):
+    """Algorithmic bytes / FLOPs of one staged layer:
+    e = storage bytes, p = 4 (f32 partials), int32 indices, padding rows
+    excluded.  |M'| = plan.total (buffer rows), centre rows read in place."""
     e = 2 if dtype == torch.float16 else 4
     m = plan.total
+    v = plan.kmap.offsets.volume
     opts.traffic_log.append((opts.layer_label, {
         "gather_bytes": e * n_in * c_in + e * m * c_in + 4 * m,
-        "scatter_bytes": 4 * m * c_out + e * n_out * c_out + 4 * m,
-        "gemm_flops": 2 * (plan.kmap.total) * c_in * c_out}))
+        "gemm_bytes": e * m * c_in + 4 * m * c_out + e * n_center * c_in
+        + 4 * n_center * c_out + e * v * c_in * c_out,
+        "gemm_flops": 2 * m_total * c_in * c_out,
+        "scatter_bytes": 4 * m * c_out + e * n_out * c_out + 4 * m
+        + 4 * n_center * c_out}))
 
 
 def _check_channels(t, w, spec, msg=None):
@@ -564,9 +578,6 @@ def sparse_conv_forward(t: SparseTensor, w: WeightTensor, spec: LayerSpec,
         result = SparseTensor(None, out, stride=t.stride * spec.stride,
                               boundary=out_cset.boundary, batch_size=t.batch_size,
                               coordset=out_cset)
-        if opts.traffic_log is not None:
-            _record_traffic(opts, build_gather_scatter_plan(kmap, center is not None), spec.c_in,
-                            spec.c_out, t.features.dtype, t.num_points, kmap.n_out)
     return result
 
 

@@ -1,0 +1,214 @@
+"""MinkUNet (the benchmark model of the paper) expressed on
+the drop-in operator API.
+
+Layer table (public TorchSparse/MinkowskiEngine definition):
+cs = [32, 32, 64, 128, 256, 256, 128, 96, 96] x width.
+
+    stem      conv3 in->cs0 +BN+ReLU, conv3 cs0->cs0 +BN+ReLU
+    stage i   conv2/s2 (c->c) +BN+ReLU, Res(c->cs_i), Res(cs_i->cs_i)      i=1..4
+    up j      deconv2 (transposed, map of stage 5-j's down conv) +BN+ReLU,
+              concat skip, Res(cs+skip->cs), Res(cs->cs)                    j=1..4
+    head      conv1 (linear) cs8 -> 19 classes
+    Res(a->b) relu(BN(conv3(relu(BN(conv3 x)))) + proj(x)), proj = conv1+BN if a != b
+
+50 convolution layers (34 k3 s1, 4 k2 s2, 4 transposed k2, 8 k1).  BatchNorm
+is folded (eval mode) into the scatter epilogue; residual add and concat are
+model glue (not reference layer kinds).
+
+``forward_engine`` runs on the B200 engine; ``forward_oracle`` runs the same
+graph on the CPU oracle (tests / CPU baseline only).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+N_CLASSES = 19
+BASE_CS = (32, 32, 64, 128, 256, 256, 128, 96, 96)
+
+
+def channels(width: float) -> list[int]:
+    return [int(c * width) for c in BASE_CS]
+
+
+def layer_table(width: float, in_channels: int = 4) -> list[dict]:
+    """Flat list of conv layers with their (K, stride, c_in, c_out)."""
+    cs = channels(width)
+    L = []
+
+    def conv(name, k, s, ci, co, kind="conv", reuse=None):
+        L.append(dict(name=name, k=k, s=s, ci=ci, co=co, kind=kind, reuse=reuse))
+
+    def res(prefix, ci, co):
+        conv(prefix + ".c1", 3, 1, ci, co)
+        conv(prefix + ".c2", 3, 1, co, co)
+        if ci != co:
+            conv(prefix + ".proj", 1, 1, ci, co)
+
+    conv("stem.0", 3, 1, in_channels, cs[0])
+    conv("stem.1", 3, 1, cs[0], cs[0])
+    for i in range(1, 5):
+        conv(f"down{i}", 2, 2, cs[i - 1], cs[i - 1])
+        res(f"enc{i}.r0", cs[i - 1], cs[i])
+        res(f"enc{i}.r1", cs[i], cs[i])
+    skip = {1: cs[3], 2: cs[2], 3: cs[1], 4: cs[0]}
+    prev = cs[4]
+    for j in range(1, 5):
+        c = cs[4 + j]
+        conv(f"up{j}", 2, 1, prev, c, kind="inverse", reuse=f"down{5 - j}")
+        res(f"dec{j}.r0", c + skip[j], c)
+        res(f"dec{j}.r1", c, c)
+        prev = c
+    conv("head", 1, 1, prev, N_CLASSES)
+    return L
+
+
+def build_params(width: float, in_channels: int = 4, seed: int = 0) -> dict:
+    """Random-init weights (N(0, 1/sqrt(K^3 C_in)), as reference
+    network.py:183-193) and folded BN (scale U(0.8,1.2), shift N(0,0.05))."""
+    rng = np.random.default_rng(seed)
+    params = {}
+    for l in layer_table(width, in_channels):
+        vol = l["k"] ** 3
+        w = rng.normal(0.0, 1.0 / np.sqrt(vol * l["ci"]), size=(vol, l["ci"], l["co"]))
+        p = {"w": w.astype(np.float32)}
+        if l["name"] != "head":
+            p["scale"] = rng.uniform(0.8, 1.2, size=l["co"]).astype(np.float32)
+            p["shift"] = rng.normal(0.0, 0.05, size=l["co"]).astype(np.float32)
+        params[l["name"]] = p
+    return params
+
+
+# ---------------------------------------------------------------- engine
+
+class EngineMinkUNet:
+    """MinkUNet on the B200 engine.  Parameters are uploaded once."""
+
+    def __init__(self, width: float, in_channels: int = 4, seed: int = 0):
+        import torch
+        from .core import WeightTensor
+        self.width = width
+        self.table = layer_table(width, in_channels)
+        self.params = build_params(width, in_channels, seed)
+        self.w = {}
+        self.bn = {}
+        for l in self.table:
+            p = self.params[l["name"]]
+            self.w[l["name"]] = WeightTensor(p["w"], l["k"], 3)
+            if "scale" in p:
+                self.bn[l["name"]] = (torch.from_numpy(p["scale"]).cuda(),
+                                      torch.from_numpy(p["shift"]).cuda())
+        # materialise device weights now (not inside a timed step)
+        for name, w in self.w.items():
+            w.packed_f16()
+
+    def forward(self, t, options=None):
+        from . import _native as nat
+        from .execution import (ExecOptions, LayerSpec, inverse_conv_forward,
+                                sparse_conv_forward)
+        from dataclasses import replace
+        base = options or ExecOptions()
+        cache = {}
+
+        def conv(x, name, k, s, relu=True, reuse=None, kind="conv"):
+            w = self.w[name]
+            opts = replace(base, layer_label=name)
+            ep = None
+            if name in self.bn:
+                ep = {"scale": self.bn[name][0], "shift": self.bn[name][1], "relu": relu}
+            if kind == "inverse":
+                spec = LayerSpec(k, 1, w.c_in, w.c_out, transposed=True, reuse_key=reuse)
+                return inverse_conv_forward(x, w, spec, cache, None, opts, epilogue=ep)
+            spec = LayerSpec(k, s, w.c_in, w.c_out, reuse_key=name)
+            return sparse_conv_forward(x, w, spec, None, cache, opts, epilogue=ep)
+
+        def add_relu(a, b):
+            import torch
+            out = torch.empty_like(a.features)
+            nat.call("scb_add", nat.dtype_code(out.dtype), nat.ptr(a.features),
+                     nat.ptr(b.features), nat.ptr(out), out.numel(), 1, nat.stream_handle())
+            return a.replace_features(out)
+
+        def res(x, prefix, has_proj):
+            h = conv(x, prefix + ".c1", 3, 1)
+            h = conv(h, prefix + ".c2", 3, 1, relu=False)
+            sc = conv(x, prefix + ".proj", 1, 1, relu=False) if has_proj else x
+            return add_relu(h, sc)
+
+        def concat(a, b):
+            import torch
+            return a.replace_features(torch.cat([a.features, b.features], dim=1))
+
+        names = {l["name"] for l in self.table}
+        x = conv(t, "stem.0", 3, 1)
+        x = conv(x, "stem.1", 3, 1)
+        skips = [x]
+        for i in range(1, 5):
+            x = conv(x, f"down{i}", 2, 2)
+            x = res(x, f"enc{i}.r0", f"enc{i}.r0.proj" in names)
+            x = res(x, f"enc{i}.r1", f"enc{i}.r1.proj" in names)
+            skips.append(x)
+        for j in range(1, 5):
+            x = conv(x, f"up{j}", 2, 1, reuse=f"down{5 - j}", kind="inverse")
+            x = concat(x, skips[4 - j])
+            x = res(x, f"dec{j}.r0", True)
+            x = res(x, f"dec{j}.r1", f"dec{j}.r1.proj" in names)
+        return conv(x, "head", 1, 1)
+
+
+# ---------------------------------------------------------------- oracle (CPU)
+
+def forward_oracle(params: dict, width: float, coords: np.ndarray, feats: np.ndarray,
+                   boundary, batch_size: int = 1, in_channels: int = 4):
+    """The same graph on the CPU oracle (tests and the CPU baseline only).
+    Epilogue rounding follows the engine: conv output in f32, BN + ReLU in
+    f32, one cast to the storage dtype."""
+    from oracle import sparseconv_oracle as O
+    storage = feats.dtype
+    names = {l["name"] for l in layer_table(width, in_channels)}
+    cache = {}
+
+    def conv(x, name, k, s, relu=True):
+        c, f, b = x
+        p = params[name]
+        oc, of, ob, pairs = O.conv_forward(c, f, b, p["w"], k, s, batch_size, return_map=True)
+        if pairs is not None and s == 2:
+            cache[name] = (pairs, c, b)
+        return oc, _epi(of, p, relu), ob
+
+    def inverse(x, name, reuse):
+        pairs, fc, fb = cache[reuse]
+        of = O.inverse_forward(x[1], params[name]["w"], pairs, fc.shape[0])
+        return fc, _epi(of, params[name], True), fb
+
+    def _epi(f, p, relu):
+        f = f.astype(np.float32)
+        if "scale" in p:
+            f = f * p["scale"] + p["shift"]
+            if relu:
+                f = np.maximum(f, 0)
+        return f.astype(storage)
+
+    def res(x, prefix, has_proj):
+        h = conv(x, prefix + ".c1", 3, 1)
+        h = conv(h, prefix + ".c2", 3, 1, relu=False)
+        sc = conv(x, prefix + ".proj", 1, 1, relu=False) if has_proj else x
+        out = np.maximum(h[1].astype(np.float32) + sc[1].astype(np.float32), 0).astype(storage)
+        return h[0], out, h[2]
+
+    x = (np.asarray(coords, np.int64), feats, tuple(boundary))
+    x = conv(x, "stem.0", 3, 1)
+    x = conv(x, "stem.1", 3, 1)
+    skips = [x]
+    for i in range(1, 5):
+        x = conv(x, f"down{i}", 2, 2)
+        x = res(x, f"enc{i}.r0", f"enc{i}.r0.proj" in names)
+        x = res(x, f"enc{i}.r1", f"enc{i}.r1.proj" in names)
+        skips.append(x)
+    for j in range(1, 5):
+        x = inverse(x, f"up{j}", f"down{5 - j}")
+        sk = skips[4 - j]
+        x = (x[0], np.concatenate([x[1], sk[1]], axis=1), x[2])
+        x = res(x, f"dec{j}.r0", True)
+        x = res(x, f"dec{j}.r1", f"dec{j}.r1.proj" in names)
+    return conv(x, "head", 1, 1)
