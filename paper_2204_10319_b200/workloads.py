@@ -72,8 +72,10 @@ def raycast_points(seed: int, beams: int = 64, elev=(-24.9, 2.0), azimuths: int 
     """
     rng = np.random.default_rng(seed)
     centers = rng.uniform(-50, 50, size=(n_boxes * 3, 2))
-    centers = centers[np.linalg.norm(centers, axis=1) > 4.0][:n_boxes]
     half = rng.uniform(0.3, 6.0, size=(centers.shape[0], 2))
+    # no box within 4 m of the sensor (its footprint must not contain it)
+    clear = ((np.abs(centers) - half) > 4.0).any(axis=1)
+    centers, half = centers[clear][:n_boxes], half[clear][:n_boxes]
     height = rng.uniform(0.5, 6.0, size=centers.shape[0])
     box_lo = np.concatenate([centers - half, np.zeros((centers.shape[0], 1))], axis=1)
     box_hi = np.concatenate([centers + half, height[:, None]], axis=1)
