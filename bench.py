@@ -257,7 +257,8 @@ def main():
     dev = torch.device("cuda", local)
     B = args.scans_per_gpu
 
-    scans = load_scans(range(rank * B, rank * B + B))
+    from paper_2204_10319_b200.sharding import shard_seeds
+    scans = load_scans(shard_seeds(rank, world, B))
     coords, feats, boundary = pack(scans)
     model = EngineMinkUNet(args.width, 4, 0)
     coords_d = torch.from_numpy(coords.astype(np.int32)).to(dev)

@@ -1,0 +1,62 @@
+"""Whole-network parity: the MinkUNet bench graph on the B200 engine vs the
+same graph on the CPU oracle, on a cropped raycast scan (FP16 storage), and
+batch packing is equivalent to separate scans."""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _crop(scan, frac):
+    c, f, b = scan
+    keep = f[:, 0] ** 2 + f[:, 1] ** 2 < (frac * 80.0) ** 2  # disc around the sensor
+    return c[keep], f[keep], b
+
+
+@pytest.fixture(scope="module")
+def scan():
+    from paper_2204_10319_b200 import workloads
+    return _crop(workloads.semantickitti_scan(0), 0.25)
+
+
+@pytest.mark.parametrize("width", [0.5, 1.0])
+def test_minkunet_matches_oracle(scan, width):
+    import paper_2204_10319_b200 as sc
+    from oracle import sparseconv_oracle as O
+    from paper_2204_10319_b200.minkunet import EngineMinkUNet, forward_oracle
+    coords, feats, boundary = scan
+    assert coords.shape[0] > 5000
+    model = EngineMinkUNet(width, 4, 0)
+    t = sc.quantize_features(sc.SparseTensor(coords, feats, 1, boundary, 1),
+                             sc.PrecisionMode.FP16_STORAGE)
+    out = model.forward(t)
+    oc, of, ob = forward_oracle(model.params, width, coords, O.quantize(feats, "fp16"), boundary)
+    np.testing.assert_array_equal(out.coords_numpy(), oc)
+    got = out.features_numpy().astype(np.float64)
+    rel = np.linalg.norm(got - of) / np.linalg.norm(of.astype(np.float64))
+    assert rel <= 1e-2, rel
+
+
+def test_packed_batch_equals_separate(scan):
+    """Packing scans along the batch column with a shared boundary is
+    bit-identical to running them one by one."""
+    import paper_2204_10319_b200 as sc
+    from paper_2204_10319_b200.minkunet import EngineMinkUNet
+    c0, f0, b0 = scan
+    c1, f1 = c0[::2].copy(), f0[::2].copy()
+    bnd = b0
+    model = EngineMinkUNet(0.5, 4, 1)
+    outs = []
+    for c, f in ((c0, f0), (c1, f1)):
+        t = sc.quantize_features(sc.SparseTensor(c, f, 1, bnd, 1), sc.PrecisionMode.FP16_STORAGE)
+        outs.append(model.forward(t).features_numpy())
+    pc = np.concatenate([c0, np.concatenate([np.ones((c1.shape[0], 1), np.int64), c1[:, 1:]], 1)])
+    pf = np.concatenate([f0, f1])
+    t = sc.quantize_features(sc.SparseTensor(pc, pf, 1, bnd, 2), sc.PrecisionMode.FP16_STORAGE)
+    packed = model.forward(t)
+    pcn = packed.coords_numpy()
+    pfn = packed.features_numpy()
+    np.testing.assert_array_equal(pfn[pcn[:, 0] == 0], outs[0])
+    np.testing.assert_array_equal(pfn[pcn[:, 0] == 1], outs[1])
