@@ -2,14 +2,15 @@
 NVCC ?= nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
 CSRC := paper_2204_10319_b200/csrc
-SRCS := $(CSRC)/capi.cu $(CSRC)/mapping.cu $(CSRC)/movement.cu $(CSRC)/gemm_sm100.cu
+SRCS := $(CSRC)/capi.cu $(CSRC)/mapping.cu $(CSRC)/movement.cu $(CSRC)/gemm_sm100.cu \
+        $(CSRC)/implicit_sm100.cu
 OBJS := $(patsubst $(CSRC)/%.cu,build/%.o,$(SRCS))
 LIB  := paper_2204_10319_b200/libsparseconv_b200.so
 FLAGS := -O3 -std=c++17 -lineinfo $(ARCH) -Xcompiler -fPIC -Iinclude -Xptxas -v
 
 all: $(LIB)
 
-build/%.o: $(CSRC)/%.cu $(CSRC)/common.cuh include/sparseconv_b200.h
+build/%.o: $(CSRC)/%.cu $(CSRC)/common.cuh $(CSRC)/sm100_ptx.cuh include/sparseconv_b200.h
 	@mkdir -p build
 	$(NVCC) $(FLAGS) -c $< -o $@ 2> build/$*.ptxas.log || (cat build/$*.ptxas.log; false)
 

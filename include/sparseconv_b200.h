@@ -134,6 +134,10 @@ int32_t scb_map_compact(const int32_t* hits, int32_t volume, int64_t n_out, cons
 int32_t scb_map_transpose(const int64_t* offset_ptr, const int32_t* in_idx, const int32_t* out_idx,
                           int32_t volume, int64_t total, int64_t n_in, int32_t* hits_t,
                           scb_stream_t stream);
+/* Same transposition straight from a hit matrix: hits_t[n][hits[n][k]] = k
+ * (no compaction, no host sync; used by the fused dataflow). */
+int32_t scb_hits_transpose(const int32_t* hits, int32_t volume, int64_t n_out, int64_t n_in,
+                           int32_t* hits_t, scb_stream_t stream);
 
 /* ---------------------------------------------------------------- plan
  * Replaces build_gather_scatter_plan (mapping.py:377-418).  The B200 buffer
@@ -164,12 +168,14 @@ int32_t scb_gather(int32_t dtype, const void* features, int64_t n_in, int32_t ch
  * and an optional pointwise epilogue (execution.py:554-576):
  *   acc = sum_{n ascending} partial[pos[k][n]]   (f32, one write per row)
  *   acc += partial[center_row + k]               (if center_row >= 0)
- *   acc = acc * scale + shift (if scale), + bias (if bias), max(0,.) if relu
+ *   acc = acc * scale + shift (if scale), + bias (if bias),
+ *         + residual[k] (if residual: out_dtype, same shape/stride as out),
+ *         max(0,.) if relu
  *   out[k] = (out_dtype) acc */
 int32_t scb_scatter(const float* partial, int64_t ldp, const int32_t* pos, int32_t volume,
                     int64_t n_out, int32_t c_out, int64_t center_row, int32_t out_dtype, void* out,
                     int64_t ld_out, const float* scale, const float* shift, const float* bias,
-                    int32_t relu, scb_stream_t stream);
+                    const void* residual, int32_t relu, scb_stream_t stream);
 /* pointwise_apply (execution.py:554-576) on a feature matrix in place:
  * op 0 = relu, 1 = bias_add, 2 = bn_fold (scale, shift).  f32 compute, cast
  * back to the storage dtype. */
@@ -204,6 +210,23 @@ int32_t scb_grouped_gemm(int32_t dtype, const void* a_buffer, int64_t a_rows, in
                          const void* weights, int32_t volume, int32_t c_out, float* partial,
                          int64_t c_rows, int64_t ldc, const scb_segment_t* segments,
                          int32_t n_segments, scb_stream_t stream);
+
+/* ---------------------------------------------------------------- fused dataflow
+ * gather -> GEMM -> scatter of one layer (the whole of _run_dataflow,
+ * execution.py:409-429, plus the pointwise epilogue) as ONE output-stationary
+ * tcgen05 kernel ("implicit GEMM"):
+ *   out[k] = epi( sum_n features[hits[n][k]] . W[n] ),  absent neighbours = 0,
+ * with epi = *scale + shift, + bias, + residual[k], ReLU (each optional).
+ * `hits` is the [V][n_out] hit matrix of scb_map_search / scb_map_transpose,
+ * so no compaction, plan, gather buffer or partials are needed.  FP16 storage
+ * only; V in {8, 27}; c_in, c_out multiples of 8; weights packed by
+ * scb_pack_weights_f16.  Per-output accumulation runs over the offsets in
+ * ascending order inside the tensor core (f32). */
+int32_t scb_conv_implicit(const void* features, int64_t n_in, int32_t c_in, int64_t ldf,
+                          const int32_t* hits, int32_t volume, int64_t n_out,
+                          const void* weights_packed, int32_t c_out, void* out,
+                          const float* scale, const float* shift, const float* bias,
+                          const void* residual, int32_t relu, scb_stream_t stream);
 
 #ifdef __cplusplus
 }

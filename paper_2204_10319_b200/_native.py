@@ -59,16 +59,19 @@ _SIGS = {
     "scb_map_count": (_I32, [_P, _I32, _I64, _P, _P, _P]),
     "scb_map_compact": (_I32, [_P, _I32, _I64, _P, _P, _P, _P, _P]),
     "scb_map_transpose": (_I32, [_P, _P, _P, _I32, _I64, _I64, _P, _P]),
+    "scb_hits_transpose": (_I32, [_P, _I32, _I64, _I64, _P, _P]),
     "scb_plan_build": (_I32, [_P, _P, _P, _I32, _I64, _I64, _I32, _I32, _P, _I64, _P, _P, _P]),
     "scb_gather": (_I32, [_I32, _P, _I64, _I32, _I64, _P, _I64, _P, _I64, _P]),
     "scb_scatter": (_I32, [_P, _I64, _P, _I32, _I64, _I32, _I64, _I32, _P, _I64, _P, _P, _P,
-                           _I32, _P]),
+                           _P, _I32, _P]),
     "scb_pointwise": (_I32, [_I32, _P, _I64, _I32, _I32, _P, _P, _P]),
     "scb_add": (_I32, [_I32, _P, _P, _P, _I64, _I32, _P]),
     "scb_quantize_f16": (_I32, [_P, _P, _I64, _P, _P]),
     "scb_pack_weights_f16": (_I32, [_P, _I32, _I32, _I32, _P, _I32, _I32, _P]),
     "scb_grouped_gemm": (_I32, [_I32, _P, _I64, _I64, _P, _I64, _I64, _I32, _P, _I32, _I32, _P,
                                 _I64, _I64, ctypes.POINTER(SegmentT), _I32, _P]),
+    "scb_conv_implicit": (_I32, [_P, _I64, _I32, _I64, _P, _I32, _I64, _P, _I32, _P, _P, _P, _P,
+                                 _P, _I32, _P]),
 }
 
 _lib = None

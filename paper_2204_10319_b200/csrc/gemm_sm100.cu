@@ -17,6 +17,7 @@
 #include <cuda.h>
 
 #include "common.cuh"
+#include "sm100_ptx.cuh"
 
 namespace scb {
 namespace tc {
@@ -40,91 +41,8 @@ struct Params {
   Seg seg[MAX_SEG];
 };
 
-// ------------------------------------------------------------------ PTX wrappers
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred P1;\n"
-      "LAB_WAIT:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      "@P1 bra DONE;\n"
-      "bra LAB_WAIT;\n"
-      "DONE:\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int x,
-                                            int y) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
-      "l"(map), "r"(smem_u32(bar)), "r"(x), "r"(y)
-      : "memory");
-}
-__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int x, int y) {
-  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
-                   map),
-               "r"(smem_u32(src)), "r"(x), "r"(y)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_read1() {
-  asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-}
-__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
-__device__ __forceinline__ void fence_async_smem() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-__device__ __forceinline__ void tc_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+using namespace ::scb::ptx;
 
-__device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr, uint32_t sbo, uint32_t layout) {
-  uint64_t d = 0;
-  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
-  d |= (uint64_t)1u << 16;                        // LBO (unused for swizzled K-major)
-  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;    // stride between 8-row groups
-  d |= (uint64_t)1u << 46;                        // descriptor version (sm_100)
-  d |= (uint64_t)layout << 61;                    // swizzle mode
-  return d;
-}
-
-__device__ __forceinline__ void mma_f16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
-                                        uint32_t accumulate) {
-  asm volatile(
-      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
-      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
-}
-__device__ __forceinline__ void mma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                   smem_u32(bar))
-               : "memory");
-}
-
-#define TMEM_LD_X16(taddr, r)                                                                 \
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11," \
-               "%12,%13,%14,%15}, [%16];"                                                     \
-               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),      \
-                 "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]),    \
-                 "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])                           \
-               : "r"(taddr))
-
-__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 __device__ __forceinline__ int find_seg(const Params& p, int t) {
   int lo = 0, hi = p.n_segs;  // largest s with tile_start[s] <= t
@@ -400,7 +318,7 @@ static CUtensorMapSwizzle swizzle_of(int bytes) {
                       : (bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
 }
 
-static bool make_map_2d(CUtensorMap* m, CUtensorMapDataType dt, int esize, const void* base,
+bool encode_map_2d(CUtensorMap* m, CUtensorMapDataType dt, int esize, const void* base,
                         long long inner, long long rows, long long ld, int box_inner, int box_rows,
                         int swz_bytes, std::string& err) {
   EncodeTiledFn fn = encode_fn();
@@ -422,7 +340,7 @@ static bool make_map_2d(CUtensorMap* m, CUtensorMapDataType dt, int esize, const
   return true;
 }
 
-static int device_sms() {
+int device_sms() {
   static int n = [] {
     int dev = 0, v = 148;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
@@ -494,13 +412,13 @@ static int gemm_f16(const void* a_buffer, long long a_rows, long long lda, const
   std::string err;
   const void* a1 = a_features ? a_features : a_buffer;
   const long long a1_rows = a_features ? f_rows : a_rows, a1_ld = a_features ? ldf : lda;
-  bool ok = make_map_2d(&mA0, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, a_buffer, c_in, a_rows, lda, p.kc,
+  bool ok = encode_map_2d(&mA0, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, a_buffer, c_in, a_rows, lda, p.kc,
                         BM, p.swz, err) &&
-            make_map_2d(&mA1, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, a1, c_in, a1_rows, a1_ld, p.kc, BM,
+            encode_map_2d(&mA1, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, a1, c_in, a1_rows, a1_ld, p.kc, BM,
                         p.swz, err) &&
-            make_map_2d(&mB, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, w_packed, k_pad,
+            encode_map_2d(&mB, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, w_packed, k_pad,
                         (long long)volume * n_pad, k_pad, p.kc, n_pad, p.swz, err) &&
-            make_map_2d(&mC, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, partial, n_pad, c_rows, ldc,
+            encode_map_2d(&mC, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, partial, n_pad, c_rows, ldc,
                         p.epi_cols, 32, p.epi_cols * 4, err);
   if (!ok) {
     set_error(std::string("scb_grouped_gemm: ") + err);

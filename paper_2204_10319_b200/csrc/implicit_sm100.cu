@@ -1,0 +1,398 @@
+// Fused gather -> tcgen05 GEMM -> epilogue convolution (the "implicit GEMM"
+// dataflow): one persistent kernel per layer computes
+//
+//   out[k] = epilogue( sum_n  features[hits[n][k]] . W[n] )      (absent -> 0)
+//
+// for 128-row output tiles, accumulating all V offsets in TMEM.  The gather is
+// fused into the MMA operand load (cp.async 16-B row chunks straight into the
+// swizzled UMMA layout, zero-filled for absent neighbours), so neither the
+// gather buffer nor the f32 partials ever reach HBM; each output row is
+// written once (fp16) with BN / bias / residual / ReLU applied in registers.
+// Offsets with no neighbour anywhere in a tile skip their MMAs.
+//
+// Warp roles (320 threads, 1 CTA / SM):
+//   warp 0     TMA producer of the weight chunks (B, K-major fp16)
+//   warp 1     TMEM allocator + single-thread tcgen05.mma issuer
+//   warps 2-5  A producers: one output row each, cp.async gather
+//   warps 6-9  epilogue: tcgen05.ld -> epilogue -> swizzled smem -> TMA store
+#include <cuda.h>
+
+#include "common.cuh"
+#include "sm100_ptx.cuh"
+
+namespace scb {
+namespace ic {
+
+using namespace ::scb::ptx;
+
+constexpr int BM = 128;
+constexpr int THREADS = 320;
+constexpr int LAG = 2;                  // cp.async groups in flight per producer thread
+constexpr int EPI_BUF = 32 * 64;        // 32 rows x 64 B (32 fp16 columns)
+constexpr int EPI_BYTES = 4 * 2 * EPI_BUF;
+
+struct Params {
+  long long n_out, ldf;
+  int c_in, c_out, n_pad, kc, n_kchunks, stages, swz, epi_cols, total_tiles, relu;
+  uint32_t idesc, tmem_cols, a_stage_bytes, stage_bytes, b_tx_bytes;
+  const int* hits;          // [V][n_out] input row or -1
+  const __half* feat;       // [n_in][ldf]
+  const float* scale;       // nullable (with shift)
+  const float* shift;
+  const float* bias;        // nullable
+  const __half* residual;   // nullable, [n_out][c_out]
+};
+
+__device__ __forceinline__ uint32_t swz_off(int row, int chunk, int swz) {
+  if (swz == 128) return row * 128 + ((chunk ^ (row & 7)) << 4);
+  if (swz == 64) return row * 64 + ((chunk ^ ((row >> 1) & 3)) << 4);
+  return row * 32 + ((chunk ^ ((row >> 2) & 1)) << 4);
+}
+
+__device__ __forceinline__ uint32_t pack_half2(float a, float b) {
+  __half2 h = __floats2half2_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+template <int V>
+__global__ void __launch_bounds__(THREADS, 1)
+    implicit_conv_f16_kernel(const __grid_constant__ CUtensorMap tmB,
+                             const __grid_constant__ CUtensorMap tmOut,
+                             const __grid_constant__ Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* epi_base = smem + (size_t)p.stages * p.stage_bytes;
+  uint32_t* flags = (uint32_t*)(epi_base + EPI_BYTES);  // one word per stage, byte per warp
+  uint64_t* full = (uint64_t*)(flags + ((p.stages + 1) & ~1));
+  uint64_t* empty = full + p.stages;
+  uint64_t* tfull = empty + p.stages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t_begin = (int)((long long)p.total_tiles * blockIdx.x / gridDim.x);
+  const int t_end = (int)((long long)p.total_tiles * (blockIdx.x + 1) / gridDim.x);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < p.stages; ++s) {
+      mbar_init(full + s, 4 * 32 + 1);  // 128 gather threads + the B expect_tx arrive
+      mbar_init(empty + s, 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull + a, 1);
+      mbar_init(tempty + a, 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmOut) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(p.tmem_cols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_before();
+  __syncthreads();
+  tc_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ============ B producer: weight chunk (n, kk) per stage via TMA
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = t_begin; t < t_end; ++t)
+        for (int n = 0; n < V; ++n)
+          for (int kk = 0; kk < p.n_kchunks; ++kk) {
+            mbar_wait(empty + stage, phase ^ 1);
+            mbar_expect_tx(full + stage, p.b_tx_bytes);
+            tma_load_2d(smem + (size_t)stage * p.stage_bytes + p.a_stage_bytes, &tmB, full + stage,
+                        kk * p.kc, n * p.n_pad);
+            if (++stage == p.stages) { stage = 0; phase ^= 1; }
+          }
+    }
+  } else if (warp == 1) {
+    // ============ MMA issuer
+    if (lane == 0) {
+      const uint32_t layout = p.swz == 128 ? 2u : (p.swz == 64 ? 4u : 6u);
+      const uint32_t sbo = 8u * (uint32_t)p.swz;
+      int stage = 0, acc = 0;
+      uint32_t phase = 0, acc_phase = 0;
+      for (int t = t_begin; t < t_end; ++t) {
+        mbar_wait(tempty + acc, acc_phase ^ 1);
+        tc_after();
+        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * p.n_pad);
+        uint32_t issued = 0;
+        for (int n = 0; n < V; ++n) {
+          for (int kk = 0; kk < p.n_kchunks; ++kk) {
+            mbar_wait(full + stage, phase);
+            tc_after();
+            const bool valid = flags[stage] != 0u;
+            if (valid || (!issued && n == V - 1)) {
+              const uint32_t sa = smem_u32(smem + (size_t)stage * p.stage_bytes);
+              const uint32_t sb = sa + p.a_stage_bytes;
+              for (int k = 0; k < p.kc / 16; ++k) {
+                mma_f16(d_tmem, make_sdesc(sa + k * 32, sbo, layout),
+                        make_sdesc(sb + k * 32, sbo, layout), p.idesc, issued);
+                issued = 1;
+              }
+            }
+            mma_commit(empty + stage);
+            if (++stage == p.stages) { stage = 0; phase ^= 1; }
+          }
+        }
+        mma_commit(tfull + acc);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else if (warp < 6) {
+    // ============ A producers: row `row` of the tile, all offsets
+    const int row = threadIdx.x - 64;
+    const int wbyte = warp - 2;
+    const int chunks = p.kc / 8;  // 16-B chunks per row per K chunk
+    int cur[V], nxt[V];
+    {
+      const long long k = (long long)t_begin * BM + row;
+#pragma unroll
+      for (int n = 0; n < V; ++n)
+        nxt[n] = (t_begin < t_end && k < p.n_out) ? __ldg(p.hits + (long long)n * p.n_out + k) : -1;
+    }
+    int stage = 0, sig = 0, pending = 0;
+    uint32_t phase = 0;
+    for (int t = t_begin; t < t_end; ++t) {
+#pragma unroll
+      for (int n = 0; n < V; ++n) cur[n] = nxt[n];
+      {  // prefetch the next tile's neighbour rows into registers
+        const long long k = (long long)(t + 1) * BM + row;
+        const bool ok = (t + 1 < t_end) && k < p.n_out;
+#pragma unroll
+        for (int n = 0; n < V; ++n) nxt[n] = ok ? __ldg(p.hits + (long long)n * p.n_out + k) : -1;
+      }
+#pragma unroll
+      for (int n = 0; n < V; ++n) {
+        const int j = cur[n];
+        const bool any = __any_sync(0xffffffffu, j >= 0);
+        const __half* src_row = p.feat + (j >= 0 ? (long long)j * p.ldf : 0);
+        for (int kk = 0; kk < p.n_kchunks; ++kk) {
+          mbar_wait(empty + stage, phase ^ 1);
+          if (lane == 0) reinterpret_cast<uint8_t*>(flags + stage)[wbyte] = any ? 1 : 0;
+          const uint32_t dst = smem_u32(smem + (size_t)stage * p.stage_bytes);
+          for (int c = 0; c < chunks; ++c) {
+            const int col = kk * p.kc + c * 8;
+            const bool ok = j >= 0 && col < p.c_in;
+            cp_async16(dst + swz_off(row, c, p.swz), ok ? (const void*)(src_row + col)
+                                                          : (const void*)p.feat, ok ? 16u : 0u);
+          }
+          cp_async_commit();
+          if (++pending > LAG) {
+            cp_async_wait<LAG>();
+            fence_async_smem();  // generic-proxy smem writes -> visible to tcgen05 (async proxy)
+            mbar_arrive(full + sig);
+            if (++sig == p.stages) sig = 0;
+            --pending;
+          }
+          if (++stage == p.stages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+    cp_async_wait<0>();
+    fence_async_smem();
+    while (pending > 0) {
+      mbar_arrive(full + sig);
+      if (++sig == p.stages) sig = 0;
+      --pending;
+    }
+  } else {
+    // ============ epilogue
+    const int q = warp & 3;
+    uint8_t* bufs = epi_base + (warp - 6) * 2 * EPI_BUF;
+    int acc = 0, nbuf = 0;
+    uint32_t acc_phase = 0;
+    const int chunks = p.n_pad / p.epi_cols;
+    for (int t = t_begin; t < t_end; ++t) {
+      const int row0 = t * BM + 32 * q;
+      const long long k = (long long)row0 + lane;
+      const bool row_ok = k < p.n_out;
+      mbar_wait(tfull + acc, acc_phase);
+      tc_after();
+      for (int j = 0; j < chunks; ++j) {
+        const int c0 = j * p.epi_cols;
+        const uint32_t taddr =
+            tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * p.n_pad + c0);
+        uint32_t r[32];
+        TMEM_LD_X16(taddr, r);
+        if (p.epi_cols == 32) TMEM_LD_X16(taddr + 16, (r + 16));
+        tmem_wait_ld();
+        float v[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+        const int ncol = p.epi_cols;
+        if (p.scale) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (i < ncol && c0 + i < p.c_out)
+              v[i] = v[i] * __ldg(p.scale + c0 + i) + __ldg(p.shift + c0 + i);
+        }
+        if (p.bias) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (i < ncol && c0 + i < p.c_out) v[i] += __ldg(p.bias + c0 + i);
+        }
+        if (p.residual && row_ok) {
+          const uint4* rp = reinterpret_cast<const uint4*>(p.residual + k * p.c_out + c0);
+#pragma unroll
+          for (int g = 0; g < 4; ++g) {
+            if (g * 8 < ncol && c0 + g * 8 < p.c_out) {
+              const uint4 w = __ldg(rp + g);
+              const __half2* h = reinterpret_cast<const __half2*>(&w);
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float2 f = __half22float2(h[e]);
+                v[g * 8 + 2 * e] += f.x;
+                v[g * 8 + 2 * e + 1] += f.y;
+              }
+            }
+          }
+        }
+        if (p.relu) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
+        }
+        uint8_t* buf = bufs + nbuf * EPI_BUF;
+        if (lane == 0) bulk_wait_read1();
+        __syncwarp();
+        if (ncol == 32) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            uint4 w = make_uint4(pack_half2(v[8 * c], v[8 * c + 1]), pack_half2(v[8 * c + 2], v[8 * c + 3]),
+                                 pack_half2(v[8 * c + 4], v[8 * c + 5]), pack_half2(v[8 * c + 6], v[8 * c + 7]));
+            *reinterpret_cast<uint4*>(buf + swz_off(lane, c, 64)) = w;
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            uint4 w = make_uint4(pack_half2(v[8 * c], v[8 * c + 1]), pack_half2(v[8 * c + 2], v[8 * c + 3]),
+                                 pack_half2(v[8 * c + 4], v[8 * c + 5]), pack_half2(v[8 * c + 6], v[8 * c + 7]));
+            *reinterpret_cast<uint4*>(buf + swz_off(lane, c, 32)) = w;
+          }
+        }
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(&tmOut, buf, c0, row0);
+          bulk_commit();
+        }
+        nbuf ^= 1;
+      }
+      tc_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty + acc);
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+    if (lane == 0) bulk_wait_all();
+  }
+
+  tc_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(p.tmem_cols));
+  }
+}
+
+}  // namespace ic
+
+// ------------------------------------------------------------------ host
+bool encode_map_2d(CUtensorMap* m, CUtensorMapDataType dt, int esize, const void* base,
+                   long long inner, long long rows, long long ld, int box_inner, int box_rows,
+                   int swz_bytes, std::string& err);
+int device_sms();
+
+}  // namespace scb
+
+using namespace scb;
+
+extern "C" int32_t scb_conv_implicit(const void* features, int64_t n_in, int32_t c_in,
+                                     int64_t ldf, const int32_t* hits, int32_t volume,
+                                     int64_t n_out, const void* weights_packed, int32_t c_out,
+                                     void* out, const float* scale, const float* shift,
+                                     const float* bias, const void* residual, int32_t relu,
+                                     scb_stream_t stream) {
+  using namespace ic;
+  SCB_CHECK_ARG(volume == 8 || volume == 27, "implicit conv supports K^3 = 8 or 27 offsets");
+  SCB_CHECK_ARG(c_in % 8 == 0 && ldf % 8 == 0, "C_in and its row stride must be multiples of 8");
+  SCB_CHECK_ARG(c_out % 8 == 0, "C_out must be a multiple of 8");
+  SCB_CHECK_ARG((scale == nullptr) == (shift == nullptr), "scale and shift go together");
+  const int n_pad = (c_out + 15) / 16 * 16;
+  const int k_pad = (c_in + 15) / 16 * 16;
+  SCB_CHECK_ARG(n_pad <= 256, "C_out > 256 not supported by the implicit conv");
+  (void)n_in;
+  if (n_out == 0) return SCB_OK;
+  Params p;
+  memset(&p, 0, sizeof(p));
+  p.n_out = n_out;
+  p.ldf = ldf;
+  p.c_in = c_in;
+  p.c_out = c_out;
+  p.n_pad = n_pad;
+  p.kc = (k_pad % 64 == 0) ? 64 : ((k_pad % 32 == 0) ? 32 : 16);
+  p.swz = p.kc * 2;
+  p.n_kchunks = k_pad / p.kc;
+  p.epi_cols = (n_pad % 32 == 0) ? 32 : 16;
+  p.total_tiles = (int)((n_out + BM - 1) / BM);
+  p.relu = relu;
+  p.idesc = (1u << 4) | ((uint32_t)(n_pad >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+  uint32_t cols = 32;
+  while (cols < (uint32_t)(2 * n_pad)) cols *= 2;
+  p.tmem_cols = cols;
+  auto r1024 = [](uint32_t x) { return (x + 1023u) / 1024u * 1024u; };
+  p.a_stage_bytes = r1024((uint32_t)(BM * p.kc * 2));
+  p.stage_bytes = p.a_stage_bytes + r1024((uint32_t)(n_pad * p.kc * 2));
+  p.b_tx_bytes = (uint32_t)(n_pad * p.kc * 2);
+  p.hits = hits;
+  p.feat = (const __half*)features;
+  p.scale = scale;
+  p.shift = shift;
+  p.bias = bias;
+  p.residual = (const __half*)residual;
+  const int smem_cap = 227 * 1024;
+  const int fixed = 1024 + EPI_BYTES + 64 * 4 + 64 * 8 + 64;
+  int stages = (smem_cap - fixed) / (int)p.stage_bytes;
+  if (stages > 16) stages = 16;
+  SCB_CHECK_ARG(stages > LAG, "stage does not fit in shared memory");
+  p.stages = stages;
+  const int smem = fixed + stages * (int)p.stage_bytes;
+
+  CUtensorMap mB, mO;
+  std::string err;
+  if (!encode_map_2d(&mB, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, weights_packed, k_pad,
+                     (long long)volume * n_pad, k_pad, p.kc, n_pad, p.swz, err) ||
+      !encode_map_2d(&mO, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, out, c_out, n_out, c_out,
+                     p.epi_cols, 32, p.epi_cols * 2, err)) {
+    set_error(std::string("scb_conv_implicit: ") + err);
+    return SCB_ECUDA;
+  }
+  cudaStream_t s = as_stream(stream);
+  const int grid = p.total_tiles < device_sms() ? p.total_tiles : device_sms();
+  if (volume == 27) {
+    static bool cfg = false;
+    if (!cfg) {
+      SCB_CUDA(cudaFuncSetAttribute(implicit_conv_f16_kernel<27>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem_cap));
+      cfg = true;
+    }
+    implicit_conv_f16_kernel<27><<<grid, THREADS, smem, s>>>(mB, mO, p);
+  } else {
+    static bool cfg = false;
+    if (!cfg) {
+      SCB_CUDA(cudaFuncSetAttribute(implicit_conv_f16_kernel<8>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem_cap));
+      cfg = true;
+    }
+    implicit_conv_f16_kernel<8><<<grid, THREADS, smem, s>>>(mB, mO, p);
+  }
+  SCB_LAUNCHED();
+  return SCB_OK;
+}

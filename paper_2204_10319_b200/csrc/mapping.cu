@@ -406,6 +406,20 @@ __global__ void map_transpose_kernel(const long long* __restrict__ offset_ptr,
   }
 }
 
+// hits_t[n][hits[n][k]] = k: the transposed map's hit matrix straight from the
+// forward hit matrix (no compaction needed).
+__global__ void hits_transpose_kernel(const int* __restrict__ hits, long long total,
+                                      long long n_out, long long n_in, int* __restrict__ hits_t) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int j = hits[i];
+    if (j >= 0) {
+      const long long n = i / n_out;
+      hits_t[n * n_in + j] = (int)(i - n * n_out);
+    }
+  }
+}
+
 __global__ void plan_build_kernel(const long long* __restrict__ offset_ptr,
                                   const int* __restrict__ in_idx, const int* __restrict__ out_idx,
                                   int V, long long total, int skip, int tile,
@@ -523,6 +537,17 @@ extern "C" int32_t scb_map_transpose(const int64_t* offset_ptr, const int32_t* i
   if (total == 0) return SCB_OK;
   map_transpose_kernel<<<grid_blocks(total, 256), 256, (volume + 1) * sizeof(long long), s>>>(
       (const long long*)offset_ptr, in_idx, out_idx, volume, total, n_in, hits_t);
+  SCB_LAUNCHED();
+  return SCB_OK;
+}
+
+extern "C" int32_t scb_hits_transpose(const int32_t* hits, int32_t volume, int64_t n_out,
+                                      int64_t n_in, int32_t* hits_t, scb_stream_t stream) {
+  cudaStream_t s = as_stream(stream);
+  if (n_in) SCB_CUDA(cudaMemsetAsync(hits_t, 0xFF, (size_t)volume * n_in * sizeof(int32_t), s));
+  const long long total = (long long)volume * n_out;
+  if (total == 0) return SCB_OK;
+  hits_transpose_kernel<<<grid_blocks(total, 256), 256, 0, s>>>(hits, total, n_out, n_in, hits_t);
   SCB_LAUNCHED();
   return SCB_OK;
 }

@@ -29,24 +29,35 @@ static int blocks_for(long long work, int threads, int per_sm = 8) {
 // fully coalesced and the (L2-resident) feature rows are read with 128-bit
 // loads.  Padding rows (buf_in < 0) are zero-filled so the GEMM never sees
 // non-finite garbage.
-template <typename VT>
+template <typename VT, int UNROLL = 4>
 __global__ void __launch_bounds__(256) gather_kernel(const VT* __restrict__ feat, long long ldf_v,
                                                      const int* __restrict__ buf_in,
                                                      long long rows, int vecs_per_row,
                                                      VT* __restrict__ buf, long long ldb_v) {
   const long long total = rows * vecs_per_row;
-  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
-       t += (long long)gridDim.x * blockDim.x) {
-    const long long r = t / vecs_per_row;
-    const int v = (int)(t - r * vecs_per_row);
-    const int src = __ldg(buf_in + r);
-    VT val;
-    if (src >= 0) {
-      val = __ldg(feat + src * ldf_v + v);
-    } else {
-      memset(&val, 0, sizeof(VT));
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  // UNROLL independent (index load -> row load -> store) chains per thread so
+  // each warp keeps several L2 requests in flight.
+  for (long long base = blockIdx.x * (long long)blockDim.x + threadIdx.x; base < total;
+       base += UNROLL * stride) {
+    long long r[UNROLL];
+    int v[UNROLL], src[UNROLL];
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) {
+      const long long t = base + u * stride;
+      r[u] = t / vecs_per_row;
+      v[u] = (int)(t - r[u] * vecs_per_row);
+      src[u] = t < total ? __ldg(buf_in + r[u]) : -1;
     }
-    buf[r * ldb_v + v] = val;
+    VT val[UNROLL];
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) {
+      if (src[u] >= 0) val[u] = __ldg(feat + src[u] * ldf_v + v[u]);
+      else memset(&val[u], 0, sizeof(VT));
+    }
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u)
+      if (base + u * stride < total) buf[r[u] * ldb_v + v[u]] = val[u];
   }
 }
 
@@ -66,16 +77,24 @@ template <> __device__ __forceinline__ void store_out<__half>(__half* p, float v
   *p = __float2half_rn(v);
 }
 
+template <typename T> __device__ __forceinline__ float ld_f(const T* p);
+template <> __device__ __forceinline__ float ld_f<float>(const float* p) { return *p; }
+template <> __device__ __forceinline__ float ld_f<__half>(const __half* p) { return __half2float(*p); }
+
 struct Epi {
   const float* scale;
   const float* shift;
   const float* bias;
+  const void* residual;  // same dtype/shape as the output, nullable
   int relu;
 };
 
-__device__ __forceinline__ float epilogue(float a, int c, const Epi& e) {
+template <typename T>
+__device__ __forceinline__ float epilogue(float a, long long k, int c, long long ldo,
+                                          const Epi& e) {
   if (e.scale) a = a * __ldg(e.scale + c) + __ldg(e.shift + c);
   if (e.bias) a = a + __ldg(e.bias + c);
+  if (e.residual) a = a + ld_f<T>(reinterpret_cast<const T*>(e.residual) + k * ldo + c);
   if (e.relu) a = fmaxf(a, 0.f);
   return a;
 }
@@ -102,17 +121,33 @@ __global__ void __launch_bounds__(256) scatter_kernel(const float* __restrict__ 
 #pragma unroll
     for (int i = 0; i < VEC; ++i) acc[i] = 0.f;
     const int* pk = pos + k * V;
-    for (int n = 0; n < V; ++n) {
-      const int r = __ldg(pk + n);
-      if (r < 0) continue;
-      const float* src = partial + (long long)r * ldp + c0;
-      if constexpr (VEC == 4) {
-        const float4 v = __ldg(reinterpret_cast<const float4*>(src));
-        acc[0] += v.x; acc[1] += v.y; acc[2] += v.z; acc[3] += v.w;
-      } else {
+    // Positions are read CH at a time and all their partial rows are loaded
+    // before any is added, so up to CH row loads are in flight per thread;
+    // the adds still run in ascending offset order (the reference's fold).
+    constexpr int CH = 9;
+    for (int n0 = 0; n0 < V; n0 += CH) {
+      int r[CH];
 #pragma unroll
-        for (int i = 0; i < VEC; ++i)
-          if (c0 + i < c_out) acc[i] += __ldg(src + i);
+      for (int u = 0; u < CH; ++u) r[u] = (n0 + u < V) ? __ldg(pk + n0 + u) : -1;
+      if constexpr (VEC == 4) {
+        float4 v[CH];
+#pragma unroll
+        for (int u = 0; u < CH; ++u)
+          v[u] = r[u] >= 0 ? __ldg(reinterpret_cast<const float4*>(partial + (long long)r[u] * ldp + c0))
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int u = 0; u < CH; ++u) {
+          if (r[u] < 0) continue;
+          acc[0] += v[u].x; acc[1] += v[u].y; acc[2] += v[u].z; acc[3] += v[u].w;
+        }
+      } else {
+        for (int u = 0; u < CH; ++u) {
+          if (r[u] < 0) continue;
+          const float* src = partial + (long long)r[u] * ldp + c0;
+#pragma unroll
+          for (int i = 0; i < VEC; ++i)
+            if (c0 + i < c_out) acc[i] += __ldg(src + i);
+        }
       }
     }
     if (center_row >= 0) {
@@ -123,15 +158,12 @@ __global__ void __launch_bounds__(256) scatter_kernel(const float* __restrict__ 
     }
 #pragma unroll
     for (int i = 0; i < VEC; ++i)
-      if (c0 + i < c_out) store_out<OutT>(out + k * ldo + c0 + i, epilogue(acc[i], c0 + i, e));
+      if (c0 + i < c_out)
+        store_out<OutT>(out + k * ldo + c0 + i, epilogue<OutT>(acc[i], k, c0 + i, ldo, e));
   }
 }
 
 // ------------------------------------------------------------------ pointwise
-template <typename T> __device__ __forceinline__ float ld_f(const T* p);
-template <> __device__ __forceinline__ float ld_f<float>(const float* p) { return *p; }
-template <> __device__ __forceinline__ float ld_f<__half>(const __half* p) { return __half2float(*p); }
-
 template <typename T>
 __global__ void pointwise_kernel(T* __restrict__ x, long long n, int c, int op,
                                  const float* __restrict__ a, const float* __restrict__ b) {
@@ -219,12 +251,13 @@ extern "C" int32_t scb_gather(int32_t dtype, const void* features, int64_t n_in,
 extern "C" int32_t scb_scatter(const float* partial, int64_t ldp, const int32_t* pos,
                                int32_t volume, int64_t n_out, int32_t c_out, int64_t center_row,
                                int32_t out_dtype, void* out, int64_t ld_out, const float* scale,
-                               const float* shift, const float* bias, int32_t relu,
+                               const float* shift, const float* bias, const void* residual,
+                               int32_t relu,
                                scb_stream_t stream) {
   SCB_CHECK_ARG(out_dtype == SCB_F32 || out_dtype == SCB_F16, "dtype must be f32 or f16");
   SCB_CHECK_ARG((scale == nullptr) == (shift == nullptr), "scale and shift go together");
   if (n_out == 0) return SCB_OK;
-  Epi e{scale, shift, bias, relu};
+  Epi e{scale, shift, bias, residual, relu};
   cudaStream_t s = as_stream(stream);
   const bool vec4 = (c_out % 4 == 0) && (ldp % 4 == 0) && ((uintptr_t)partial % 16 == 0);
   const int groups = vec4 ? c_out / 4 : c_out;

@@ -42,7 +42,7 @@ class StageTimer:
     """Per-(layer, stage) device time over a forward pass, measured with CUDA
     events on the compute stream (reference StageTimer, execution.py:39-58)."""
 
-    STAGES = ("mapping", "gather", "matmul", "scatter", "other")
+    STAGES = ("mapping", "gather", "matmul", "scatter", "fused", "other")
 
     def __init__(self):
         self._events: list[tuple[str, str, torch.cuda.Event, torch.cuda.Event]] = []
@@ -146,7 +146,10 @@ class CachedMap:
 class ExecOptions:
     """Per-call knobs; numerics are invariant under all of them
     (execution.py:137-156).  ``map_reuse`` keeps maps built over a
-    coordinate set for later layers at the same level (result-identical)."""
+    coordinate set for later layers at the same level (result-identical).
+    ``dataflow`` selects the staged gather/GEMM/scatter pipeline (default,
+    the reference's structure), the fused implicit-GEMM kernel, or ``auto``
+    (per-layer roofline choice)."""
 
     order: str = "locality"
     fused: bool = True
@@ -158,10 +161,14 @@ class ExecOptions:
     workload_log: list | None = None
     plan_log: list | None = None
     map_reuse: bool = True
+    dataflow: str = "staged"
+
 
     def __post_init__(self):
         if self.order not in ("locality", "weight"):
             raise ValueError(f"unknown order {self.order!r}")
+        if self.dataflow not in ("staged", "fused", "auto"):
+            raise ValueError(f"unknown dataflow {self.dataflow!r}")
         if not self.fused and self.order == "locality":
             warnings.warn("locality order requires fused movement; using weight order")
             self.order = "weight"
@@ -225,7 +232,7 @@ def scatter_accumulate(buffer, plan: GatherScatterPlan, n_out: int,
     odt = torch.float16 if np.dtype(out_dtype) == np.float16 else torch.float32
     out = torch.empty((n_out, c), dtype=odt, device=b.device)
     nat.call("scb_scatter", nat.ptr(padded), c, nat.ptr(plan.pos), plan.pos.shape[1], n_out, c, -1,
-             nat.dtype_code(odt), nat.ptr(out), c, None, None, None, 0, nat.stream_handle())
+             nat.dtype_code(odt), nat.ptr(out), c, None, None, None, None, 0, nat.stream_handle())
     return out
 
 
@@ -405,10 +412,75 @@ def _direct_center(dtype, c_in: int) -> bool:
     return dtype == torch.float32 or c_in % 8 == 0
 
 
+def _epi_args(ep: dict | None):
+    ep = ep or {}
+    res = ep.get("residual")
+    if isinstance(res, SparseTensor):
+        res = res.features
+    return (nat.ptr(ep.get("scale")), nat.ptr(ep.get("shift")), nat.ptr(ep.get("bias")),
+            nat.ptr(res), int(bool(ep.get("relu", False))))
+
+
+def _fused_eligible(dtype, kmap: KernelMap, w: WeightTensor) -> bool:
+    return (dtype == torch.float16 and kmap.offsets.volume in (8, 27) and w.c_in % 8 == 0
+            and w.c_out % 8 == 0 and w.c_out <= 256)
+
+
+def choose_dataflow(opts: ExecOptions, dtype, kmap: KernelMap, w: WeightTensor) -> str:
+    """"staged" (gather -> grouped GEMM -> scatter, the reference's structure)
+    or "fused" (one implicit-GEMM kernel).  ``auto`` compares the two
+    roofline estimates: staged moves the buffer and the f32 partials through
+    HBM; fused multiplies every offset densely (absent rows are zero) but
+    keeps all intermediates on chip."""
+    if opts.dataflow == "staged" or not _fused_eligible(dtype, kmap, w):
+        return "staged"
+    if opts.dataflow == "fused":
+        return "fused"
+    n, v = kmap.n_out, kmap.offsets.volume
+    ci, co = w.c_in, w.c_out
+    m_est = n * (v if v == 8 else 7.5)  # |M|/N of LiDAR maps (SURVEY.md §8(d)); 8 -> upper bound
+    t_staged = (m_est * (4 * ci + 8 * co + 8) + 2 * n * (ci + co)) / 4.5e12 + 25e-6
+    t_fused = max(v * n * ci * co * 2 / 1.1e15, m_est * ci * 2 / 9e12,
+                  2 * n * (ci + co) / 5e12) + 8e-6
+    return "fused" if t_fused <= t_staged else "staged"
+
+
+def _run_fused(features: torch.Tensor, kmap: KernelMap, w: WeightTensor, opts: ExecOptions,
+               epilogue: dict | None) -> torch.Tensor:
+    label, timer = opts.layer_label, opts.timer
+    packed, _, _ = w.packed_f16()
+    f = features.contiguous()
+    out = torch.empty((kmap.n_out, w.c_out), dtype=f.dtype, device=f.device)
+    scale, shift, bias, res, relu = _epi_args(epilogue)
+    with _timed(timer, label, "fused"):
+        nat.call("scb_conv_implicit", nat.ptr(f), f.shape[0], w.c_in, w.c_in, nat.ptr(kmap.hits),
+                 kmap.offsets.volume, kmap.n_out, nat.ptr(packed), w.c_out, nat.ptr(out), scale,
+                 shift, bias, res, relu, nat.stream_handle())
+    if opts.traffic_log is not None:
+        v = kmap.offsets.volume
+        e = 2
+        opts.traffic_log.append((label, {
+            "fused_bytes": e * f.shape[0] * w.c_in + e * kmap.n_out * w.c_out
+            + 4 * v * kmap.n_out + e * v * w.c_in * w.c_out
+            + (e * kmap.n_out * w.c_out if res else 0),
+            "fused_flops_executed": 2 * v * kmap.n_out * w.c_in * w.c_out}))
+    return out
+
+
 def _run_dataflow(features: torch.Tensor, kmap: KernelMap, w: WeightTensor,
-                  grouping: GroupingStrategy, opts: ExecOptions, center: int | None,
-                  epilogue: dict | None = None) -> torch.Tensor:
-    """Gather -> grouped GEMM (+ centre) -> scatter; returns storage-dtype rows."""
+                  strat: LayerStrategy, schedule, symmetric: bool, opts: ExecOptions,
+                  center: int | None, epilogue: dict | None = None, record=None) -> torch.Tensor:
+    """One layer's gather -> GEMM -> scatter; returns storage-dtype rows."""
+    if choose_dataflow(opts, features.dtype, kmap, w) == "fused":
+        if record is not None and opts.workload_log is not None:
+            record(kmap.sizes)
+        return _run_fused(features, kmap, w, opts, epilogue)
+    sizes = kmap.sizes
+    if center is not None:
+        sizes[center] = 0
+    if record is not None:
+        record(sizes)
+    grouping = build_grouping(sizes, strat.eps, strat.threshold, schedule, symmetric)
     label, timer = opts.layer_label, opts.timer
     dt = features.dtype
     c_in, c_out = w.c_in, w.c_out
@@ -435,12 +507,10 @@ def _run_dataflow(features: torch.Tensor, kmap: KernelMap, w: WeightTensor,
         partial, ldc = _grouped_gemm(dt, buf, plan.rows_pad, features if direct else None, w,
                                      segs, nseg, c_rows)
     out = torch.empty((kmap.n_out, c_out), dtype=dt, device=features.device)
-    ep = epilogue or {}
     with _timed(timer, label, "scatter"):
         nat.call("scb_scatter", nat.ptr(partial), ldc, nat.ptr(plan.pos), plan.pos.shape[1],
                  kmap.n_out, c_out, center_row, nat.dtype_code(dt), nat.ptr(out), c_out,
-                 nat.ptr(ep.get("scale")), nat.ptr(ep.get("shift")), nat.ptr(ep.get("bias")),
-                 int(bool(ep.get("relu", False))), nat.stream_handle())
+                 *_epi_args(epilogue), nat.stream_handle())
     if opts.traffic_log is not None:
         _record_traffic(opts, plan, c_in, c_out, dt, features.shape[0], kmap.n_out,
                         features.shape[0] if direct else 0, kmap.total)
@@ -466,10 +536,8 @@ def _pointwise_matmul(t: SparseTensor, w: WeightTensor, opts: ExecOptions, epilo
         partial, ldc = _grouped_gemm(dt, buf, n_rows, None, w, segs, nseg, n_rows)
     out = torch.empty((n, w.c_out), dtype=dt, device=f.device)
     ident = _identity_pos(n, f.device)
-    ep = epilogue or {}
     nat.call("scb_scatter", nat.ptr(partial), ldc, nat.ptr(ident), 1, n, w.c_out, -1,
-             nat.dtype_code(dt), nat.ptr(out), w.c_out, nat.ptr(ep.get("scale")),
-             nat.ptr(ep.get("shift")), nat.ptr(ep.get("bias")), int(bool(ep.get("relu", False))),
+             nat.dtype_code(dt), nat.ptr(out), w.c_out, *_epi_args(epilogue),
              nat.stream_handle())
     return out
 
@@ -566,14 +634,11 @@ def sparse_conv_forward(t: SparseTensor, w: WeightTensor, spec: LayerSpec,
         if map_cache is not None and spec.reuse_key:
             map_cache[spec.reuse_key] = CachedMap(kmap, t.coords, t.boundary, t.stride, cset)
     schedule, symmetric = schedule_for(offsets, spec.stride)
-    sizes = kmap.sizes
     center = offsets.center if (spec.stride == 1 and offsets.center is not None) else None
-    if center is not None:
-        sizes[center] = 0
-    _record_workload(opts, spec, sizes, symmetric, schedule, t.coords, out_cset.coords,
-                     t.boundary, t.batch_size)
-    grouping = build_grouping(sizes, strat.eps, strat.threshold, schedule, symmetric)
-    out = _run_dataflow(t.features, kmap, w, grouping, opts, center, epilogue)
+    record = lambda sizes: _record_workload(opts, spec, sizes, symmetric, schedule, t.coords,
+                                            out_cset.coords, t.boundary, t.batch_size)
+    out = _run_dataflow(t.features, kmap, w, strat, schedule, symmetric, opts, center, epilogue,
+                        record)
     with _timed(timer, label, "other"):
         result = SparseTensor(None, out, stride=t.stride * spec.stride,
                               boundary=out_cset.boundary, batch_size=t.batch_size,
@@ -601,11 +666,10 @@ def inverse_conv_forward(t: SparseTensor, w: WeightTensor, spec: LayerSpec, map_
     with _timed(timer, label, "mapping"):
         swapped = entry.kmap.swap_roles()
     schedule = list(range(swapped.offsets.volume))
-    sizes = swapped.sizes
-    _record_workload(opts, spec, sizes, False, schedule, t.coords, entry.in_coords,
-                     entry.in_boundary, t.batch_size)
-    grouping = build_grouping(sizes, strat.eps, strat.threshold, schedule, False)
-    out = _run_dataflow(t.features, swapped, w, grouping, opts, None, epilogue)
+    record = lambda sizes: _record_workload(opts, spec, sizes, False, schedule, t.coords,
+                                            entry.in_coords, entry.in_boundary, t.batch_size)
+    out = _run_dataflow(t.features, swapped, w, strat, schedule, False, opts, None, epilogue,
+                        record)
     with _timed(timer, label, "other"):
         cset = entry.in_coordset or CoordinateSet(entry.in_coords, entry.in_boundary, t.batch_size)
         result = SparseTensor(None, out, stride=entry.in_stride, boundary=entry.in_boundary,

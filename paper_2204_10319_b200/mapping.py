@@ -208,38 +208,78 @@ def _compact(hits: torch.Tensor, volume: int, n_out: int):
 
 
 class KernelMap:
-    """Per-offset (input row, output row) pairs in device CSR form
-    (mapping.py:251-286)."""
+    """Per-offset (input row, output row) pairs (mapping.py:251-286).
+
+    Two device representations, each built on demand from the other:
+    the hit matrix ``hits[V][n_out]`` (input row or -1; what map search
+    produces and what the fused dataflow consumes, no host sync) and the
+    canonical CSR (``offset_ptr``, ``in_idx``, ``out_idx`` + host ``sizes``;
+    what the staged dataflow and the reference API use, one D2H of V+1 sizes
+    to build)."""
 
     def __init__(self, offset_ptr, sizes, in_idx, out_idx, offsets: KernelOffsets, stride: int,
-                 n_in: int, n_out: int, symmetric: bool = False, trusted: bool = False):
-        self.trusted = bool(trusted)          # produced by map_search: one entry per (k, n)
-        self.offset_ptr = offset_ptr        # device int64 [V+1]
-        self._sizes = np.asarray(sizes, dtype=np.int64)
-        self.in_idx = in_idx                # device int32 [|M|]
-        self.out_idx = out_idx              # device int32 [|M|]
+                 n_in: int, n_out: int, symmetric: bool = False, trusted: bool = False,
+                 hits: torch.Tensor | None = None):
         self.offsets = offsets
         self.stride = int(stride)
         self.n_in = int(n_in)
         self.n_out = int(n_out)
         self.symmetric = bool(symmetric)
+        self.trusted = bool(trusted)  # produced by map search: one entry per (k, n)
+        self._hits = hits
+        self._csr = None
+        if offset_ptr is not None:
+            self._csr = (offset_ptr, np.asarray(sizes, dtype=np.int64), in_idx, out_idx)
         self._pairs = None
         self._plans = {}
         self._swapped = None
 
+    @classmethod
+    def from_hits(cls, hits, offsets, stride, n_in, n_out, symmetric=False) -> "KernelMap":
+        return cls(None, None, None, None, offsets, stride, n_in, n_out, symmetric,
+                   trusted=True, hits=hits)
+
+    # ---- representations ------------------------------------------------
+    def _ensure_csr(self):
+        if self._csr is None:
+            self._csr = _compact(self._hits, self.offsets.volume, self.n_out)
+        return self._csr
+
+    @property
+    def hits(self) -> torch.Tensor:
+        """[V][max(n_out,1)] int32 hit matrix on the device."""
+        if self._hits is None:
+            ptr, _, ii, oi = self._ensure_csr()
+            V = self.offsets.volume
+            h = torch.empty((V, max(self.n_out, 1)), dtype=torch.int32, device=ii.device)
+            # hits[n][out_idx[e]] = in_idx[e]: the transpose kernel with roles exchanged
+            nat.call("scb_map_transpose", nat.ptr(ptr), nat.ptr(oi), nat.ptr(ii), V,
+                     self.total, self.n_out, nat.ptr(h), nat.stream_handle())
+            self._hits = h
+        return self._hits
+
+    offset_ptr = property(lambda self: self._ensure_csr()[0])
+    in_idx = property(lambda self: self._ensure_csr()[2])
+    out_idx = property(lambda self: self._ensure_csr()[3])
+
     @property
     def sizes(self) -> np.ndarray:
-        return self._sizes.copy()
+        return self._ensure_csr()[1].copy()
 
     @property
     def buffer_offsets(self) -> np.ndarray:
-        out = np.zeros(self._sizes.shape[0] + 1, dtype=np.int64)
-        np.cumsum(self._sizes, out=out[1:])
+        sz = self._ensure_csr()[1]
+        out = np.zeros(sz.shape[0] + 1, dtype=np.int64)
+        np.cumsum(sz, out=out[1:])
         return out
 
     @property
     def total(self) -> int:
-        return int(self._sizes.sum())
+        return int(self._ensure_csr()[1].sum())
+
+    @property
+    def device(self):
+        return (self._hits if self._hits is not None else self._csr[2]).device
 
     @property
     def pairs(self) -> list[np.ndarray]:
@@ -249,22 +289,25 @@ class KernelMap:
             k = self.out_idx.cpu().numpy().astype(np.int64)
             st = self.buffer_offsets
             self._pairs = [np.stack([j[st[n]:st[n + 1]], k[st[n]:st[n + 1]]], axis=1)
-                           for n in range(self._sizes.shape[0])]
+                           for n in range(self.offsets.volume)]
         return self._pairs
 
     def swap_roles(self) -> "KernelMap":
         """Input/output roles exchanged, entries re-sorted by the new output
-        row (mapping.py:277-286): a transposed hit matrix plus compaction."""
+        row (mapping.py:277-286).  Transposing the hit matrix produces the
+        re-sorted order directly: the new hit matrix is indexed by new output row."""
         if self._swapped is None:
-            V = self._sizes.shape[0]
-            hits = torch.empty((V, max(self.n_in, 1)), dtype=torch.int32,
-                               device=self.in_idx.device)
-            nat.call("scb_map_transpose", nat.ptr(self.offset_ptr), nat.ptr(self.in_idx),
-                     nat.ptr(self.out_idx), V, self.total, self.n_in, nat.ptr(hits),
-                     nat.stream_handle())
-            ptr, sizes, ii, oi = _compact(hits, V, self.n_in)
-            self._swapped = KernelMap(ptr, sizes, ii, oi, self.offsets, self.stride,
-                                      self.n_out, self.n_in, trusted=self.trusted)
+            V = self.offsets.volume
+            ht = torch.empty((V, max(self.n_in, 1)), dtype=torch.int32, device=self.device)
+            if self._hits is not None:
+                nat.call("scb_hits_transpose", nat.ptr(self._hits), V, self.n_out, self.n_in,
+                         nat.ptr(ht), nat.stream_handle())
+            else:
+                nat.call("scb_map_transpose", nat.ptr(self.offset_ptr), nat.ptr(self.in_idx),
+                         nat.ptr(self.out_idx), V, self.total, self.n_in, nat.ptr(ht),
+                         nat.stream_handle())
+            self._swapped = KernelMap(None, None, None, None, self.offsets, self.stride,
+                                      self.n_out, self.n_in, trusted=self.trusted, hits=ht)
         return self._swapped
 
 
@@ -272,7 +315,9 @@ def map_search(in_index: CoordinateIndex, out_coords, offsets: KernelOffsets, st
                use_symmetry: bool | None = None) -> KernelMap:
     """Kernel map: entry (j, k) whenever stride*q_k + delta_n is input j
     (mapping.py:289-319).  Stride-1 odd-K maps probe only offsets up to the
-    centre and fill the mirrored half in the same pass (mapping.py:322-339)."""
+    centre and fill the mirrored half in the same pass (mapping.py:322-339).
+    Returns a map holding the hit matrix; the CSR form is compacted on first
+    use."""
     oc = out_coords.coords if hasattr(out_coords, "coords") else as_device_coords(out_coords)
     volume, center = offsets.volume, offsets.center
     if use_symmetry is None:
@@ -287,9 +332,8 @@ def map_search(in_index: CoordinateIndex, out_coords, offsets: KernelOffsets, st
     nat.call("scb_map_search", in_index.code, nat.ptr(oc), n_out, grid, offsets.kernel_size,
              offsets.base, stride, int(bool(use_symmetry)), nat.ptr(in_index.keys),
              nat.ptr(in_index.rows), in_index.slots, nat.ptr(hits), nat.stream_handle())
-    ptr, sizes, ii, oi = _compact(hits, volume, n_out)
-    return KernelMap(ptr, sizes, ii, oi, offsets, stride, in_index.size, n_out,
-                     symmetric=bool(use_symmetry), trusted=True)
+    return KernelMap.from_hits(hits, offsets, stride, in_index.size, n_out,
+                               symmetric=bool(use_symmetry))
 
 
 def derive_symmetric_maps(half_map: KernelMap) -> KernelMap:
@@ -301,21 +345,13 @@ def derive_symmetric_maps(half_map: KernelMap) -> KernelMap:
     if center is None:
         raise ValueError("symmetric maps exist only for odd kernel sizes")
     V, n = half_map.offsets.volume, half_map.n_out
-    dev = half_map.in_idx.device
-    s = nat.stream_handle()
-    # direct rows: hits[m][k] = j  (the transpose kernel with roles exchanged)
-    direct = torch.empty((V, max(n, 1)), dtype=torch.int32, device=dev)
-    nat.call("scb_map_transpose", nat.ptr(half_map.offset_ptr), nat.ptr(half_map.out_idx),
-             nat.ptr(half_map.in_idx), V, half_map.total, n, nat.ptr(direct), s)
+    direct = half_map.hits
     mirror = torch.empty_like(direct)
-    nat.call("scb_map_transpose", nat.ptr(half_map.offset_ptr), nat.ptr(half_map.in_idx),
-             nat.ptr(half_map.out_idx), V, half_map.total, n, nat.ptr(mirror), s)
+    nat.call("scb_hits_transpose", nat.ptr(direct), V, n, n, nat.ptr(mirror), nat.stream_handle())
     hits = direct.clone()
-    lower = torch.arange(center, device=dev)
+    lower = torch.arange(center, device=direct.device)
     hits[V - 1 - lower] = mirror[lower]
-    ptr, sizes, ii, oi = _compact(hits, V, n)
-    return KernelMap(ptr, sizes, ii, oi, half_map.offsets, 1, half_map.n_in, n, symmetric=True,
-                     trusted=True)
+    return KernelMap.from_hits(hits, half_map.offsets, 1, half_map.n_in, n, symmetric=True)
 
 
 class GatherScatterPlan:
@@ -350,7 +386,7 @@ class GatherScatterPlan:
         np.cumsum(padded, out=self.slab_ptr[1:])
         self.rows_pad = int(self.slab_ptr[-1])
         V = sizes.shape[0]
-        dev = kmap.in_idx.device
+        dev = kmap.device
         self.buf_in = torch.empty(max(self.rows_pad, 1), dtype=torch.int32, device=dev)
         self.pos = torch.empty((max(self.n_out, 1), V), dtype=torch.int32, device=dev)
         status = None if kmap.trusted else torch.zeros(1, dtype=torch.int32, device=dev)

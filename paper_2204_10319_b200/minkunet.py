@@ -103,37 +103,30 @@ class EngineMinkUNet:
             w.packed_f16()
 
     def forward(self, t, options=None):
-        from . import _native as nat
         from .execution import (ExecOptions, LayerSpec, inverse_conv_forward,
                                 sparse_conv_forward)
         from dataclasses import replace
         base = options or ExecOptions()
         cache = {}
 
-        def conv(x, name, k, s, relu=True, reuse=None, kind="conv"):
+        def conv(x, name, k, s, relu=True, reuse=None, kind="conv", residual=None):
             w = self.w[name]
             opts = replace(base, layer_label=name)
-            ep = None
+            ep = {"relu": relu, "residual": residual}
             if name in self.bn:
-                ep = {"scale": self.bn[name][0], "shift": self.bn[name][1], "relu": relu}
+                ep.update(scale=self.bn[name][0], shift=self.bn[name][1])
             if kind == "inverse":
                 spec = LayerSpec(k, 1, w.c_in, w.c_out, transposed=True, reuse_key=reuse)
                 return inverse_conv_forward(x, w, spec, cache, None, opts, epilogue=ep)
             spec = LayerSpec(k, s, w.c_in, w.c_out, reuse_key=name)
             return sparse_conv_forward(x, w, spec, None, cache, opts, epilogue=ep)
 
-        def add_relu(a, b):
-            import torch
-            out = torch.empty_like(a.features)
-            nat.call("scb_add", nat.dtype_code(out.dtype), nat.ptr(a.features),
-                     nat.ptr(b.features), nat.ptr(out), out.numel(), 1, nat.stream_handle())
-            return a.replace_features(out)
-
         def res(x, prefix, has_proj):
+            # relu(BN(conv2(h)) + shortcut): the residual add and ReLU run in
+            # conv2's epilogue (one write of the block output)
             h = conv(x, prefix + ".c1", 3, 1)
-            h = conv(h, prefix + ".c2", 3, 1, relu=False)
             sc = conv(x, prefix + ".proj", 1, 1, relu=False) if has_proj else x
-            return add_relu(h, sc)
+            return conv(h, prefix + ".c2", 3, 1, relu=True, residual=sc)
 
         def concat(a, b):
             import torch
@@ -181,20 +174,23 @@ def forward_oracle(params: dict, width: float, coords: np.ndarray, feats: np.nda
         of = O.inverse_forward(x[1], params[name]["w"], pairs, fc.shape[0])
         return fc, _epi(of, params[name], True), fb
 
-    def _epi(f, p, relu):
+    def _epi(f, p, relu, residual=None):
         f = f.astype(np.float32)
         if "scale" in p:
             f = f * p["scale"] + p["shift"]
-            if relu:
-                f = np.maximum(f, 0)
+        if residual is not None:
+            f = f + residual.astype(np.float32)
+        if relu:
+            f = np.maximum(f, 0)
         return f.astype(storage)
 
     def res(x, prefix, has_proj):
         h = conv(x, prefix + ".c1", 3, 1)
-        h = conv(h, prefix + ".c2", 3, 1, relu=False)
         sc = conv(x, prefix + ".proj", 1, 1, relu=False) if has_proj else x
-        out = np.maximum(h[1].astype(np.float32) + sc[1].astype(np.float32), 0).astype(storage)
-        return h[0], out, h[2]
+        c, f, b = h
+        p = params[prefix + ".c2"]
+        oc, of, ob = O.conv_forward(c, f, b, p["w"], 3, 1, batch_size)
+        return oc, _epi(of, p, True, sc[1]), ob
 
     x = (np.asarray(coords, np.int64), feats, tuple(boundary))
     x = conv(x, "stem.0", 3, 1)

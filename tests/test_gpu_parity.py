@@ -392,3 +392,67 @@ def test_4d_and_2d_layers_vs_oracle(sc):
                                          sc.LayerSpec(k, s, 8, 8))
             np.testing.assert_array_equal(out.coords_numpy(), oc)
             assert rel_l2(out.features_numpy(), of) <= 1e-4
+
+
+@pytest.mark.parametrize("c_in,c_out", [(64, 64), (32, 48), (16, 16), (96, 128), (256, 256)])
+def test_fused_dataflow_vs_oracle(sc, c_in, c_out):
+    """The implicit-GEMM kernel (gather fused into the tcgen05 operand load)
+    against the oracle: k3 s1, k2 s2 and the transposed k2 layer."""
+    from paper_2204_10319_b200 import workloads
+    coords, _, boundary = workloads.config1_cloud()
+    rng = np.random.default_rng(c_in + 3 * c_out)
+    feats = O.quantize(rng.standard_normal((coords.shape[0], c_in)).astype(np.float32), "fp16")
+    w = rng.normal(0, 1 / np.sqrt(27 * c_in), (27, c_in, c_out)).astype(np.float32)
+    oc, of, _ = O.conv_forward(coords, feats, boundary, w, 3, 1)
+    opts = sc.ExecOptions(dataflow="fused")
+    t = sc.SparseTensor(coords, feats, 1, boundary, 1)
+    out = sc.sparse_conv_forward(t, sc.WeightTensor(w, 3, 3), sc.LayerSpec(3, 1, c_in, c_out),
+                                 None, None, opts)
+    assert rel_l2(out.features_numpy(), of) <= 1e-2
+    w1 = rng.normal(0, 0.1, (8, c_in, c_out)).astype(np.float32)
+    w2 = rng.normal(0, 0.1, (8, c_out, c_in)).astype(np.float32)
+    doc, dof, _, pairs = O.conv_forward(coords, feats, boundary, w1, 2, 2, return_map=True)
+    cache = {}
+    d = sc.sparse_conv_forward(t, sc.WeightTensor(w1, 2, 3),
+                               sc.LayerSpec(2, 2, c_in, c_out, reuse_key="d"), None, cache, opts)
+    np.testing.assert_array_equal(d.coords_numpy(), doc)
+    assert rel_l2(d.features_numpy(), dof) <= 1e-2
+    u = sc.inverse_conv_forward(d, sc.WeightTensor(w2, 2, 3),
+                                sc.LayerSpec(2, 1, c_out, c_in, transposed=True, reuse_key="d"),
+                                cache, None, opts)
+    uf = O.inverse_forward(dof, w2, pairs, coords.shape[0])
+    assert rel_l2(u.features_numpy(), uf) <= 1e-2
+
+
+@pytest.mark.parametrize("dataflow", ["staged", "fused"])
+def test_epilogue_bn_residual_relu(sc, rng, dataflow):
+    coords = random_coords(rng, (20, 20, 20), 0.1)
+    n = coords.shape[0]
+    f = O.quantize(rng.standard_normal((n, 32)).astype(np.float32), "fp16")
+    r = O.quantize(rng.standard_normal((n, 48)).astype(np.float32), "fp16")
+    w = rng.normal(0, 0.05, (27, 32, 48)).astype(np.float32)
+    s = rng.uniform(0.8, 1.2, 48).astype(np.float32)
+    h = rng.normal(0, 0.05, 48).astype(np.float32)
+    _, base, _ = O.conv_forward(coords, f, (20, 20, 20), w, 3, 1)
+    want = np.maximum(base.astype(np.float32) * s + h + r.astype(np.float32), 0)
+    t = sc.SparseTensor(coords, f, 1, (20, 20, 20))
+    res = sc.SparseTensor(coords, r, 1, (20, 20, 20))
+    ep = {"scale": torch.from_numpy(s).cuda(), "shift": torch.from_numpy(h).cuda(),
+          "residual": res, "relu": True}
+    out = sc.sparse_conv_forward(t, sc.WeightTensor(w, 3, 3), sc.LayerSpec(3, 1, 32, 48), None,
+                                 None, sc.ExecOptions(dataflow=dataflow), epilogue=ep)
+    got = out.features_numpy().astype(np.float32)
+    assert rel_l2(got, want) <= 1e-2
+    assert (got >= 0).all()
+
+
+def test_lazy_map_needs_no_compaction_for_fused(sc, rng):
+    coords = random_coords(rng, (16, 16, 16), 0.1)
+    t = sc.SparseTensor(coords, rng.standard_normal((coords.shape[0], 16)).astype(np.float16),
+                        1, (16, 16, 16))
+    w = sc.WeightTensor(rng.normal(0, 0.1, (27, 16, 16)).astype(np.float32), 3, 3)
+    sc.sparse_conv_forward(t, w, sc.LayerSpec(3, 1, 16, 16), None, None,
+                           sc.ExecOptions(dataflow="fused"))
+    (_, kmap), = t.coordset.maps.values()
+    assert kmap._csr is None  # the fused path consumed the hit matrix only
+    assert kmap.total > 0 and kmap._csr is not None  # CSR on demand
