@@ -51,6 +51,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--dataflow", choices=("staged", "fused", "auto"), default="auto")
     return ap.parse_args()
 
 
@@ -269,7 +270,7 @@ def main():
         t = sc.SparseTensor(coords_d, feats_d, 1, boundary, B, validate=False)
         t = sc.quantize_features(t, sc.PrecisionMode.FP16_STORAGE)
         return model.forward(t, sc.ExecOptions(timer=timer, traffic_log=traffic,
-                                               index_kind="hash"))
+                                               index_kind="hash", dataflow=args.dataflow))
 
     for _ in range(args.warmup):
         step()
@@ -307,30 +308,44 @@ def main():
     stages = {}
     for (layer, stage), s in timer.samples.items():
         stages[stage] = stages.get(stage, 0.0) + s
-    bytes_by = {"gather": 0, "matmul": 0, "scatter": 0}
-    flops = 0
+    bytes_by = {"gather": 0, "matmul": 0, "scatter": 0, "fused": 0}
+    flops = fused_flops = 0
     for _, rec in traffic:
-        bytes_by["gather"] += rec["gather_bytes"]
-        bytes_by["matmul"] += rec["gemm_bytes"]
-        bytes_by["scatter"] += rec["scatter_bytes"]
-        flops += rec["gemm_flops"]
+        bytes_by["gather"] += rec.get("gather_bytes", 0)
+        bytes_by["matmul"] += rec.get("gemm_bytes", 0)
+        bytes_by["scatter"] += rec.get("scatter_bytes", 0)
+        bytes_by["fused"] += rec.get("fused_bytes", 0)
+        flops += rec.get("gemm_flops", 0)
+        fused_flops += rec.get("fused_flops_executed", 0)
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) \
         if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
     tc_peak = peaks.get("bf16_tflops", 1590.0)
-    dom = max(("gather", "matmul", "scatter"), key=lambda k: stages.get(k, 0.0))
+    dom = max(("gather", "matmul", "scatter", "fused"), key=lambda k: stages.get(k, 0.0))
     kernel_name = {"gather": "scb gather_kernel", "matmul": "scb grouped_gemm_f16_kernel (tcgen05)",
-                   "scatter": "scb scatter_kernel"}[dom]
+                   "scatter": "scb scatter_kernel",
+                   "fused": "scb implicit_conv_f16_kernel (tcgen05, fused gather/GEMM/scatter)"}[dom]
     ach = bytes_by[dom] / stages[dom] / 1e9
+    traffic_file = ROOT / "profiles" / "latest_traffic.json"
+    measured = json.loads(traffic_file.read_text()) if traffic_file.exists() else {}
     roof = {"bound": "hbm", "kernel": kernel_name, "achieved": ach, "peak": hbm_peak,
-            "unit": "GB/s", "frac": ach / hbm_peak, "traffic": None,
+            "unit": "GB/s", "frac": ach / hbm_peak,
+            "traffic": measured.get(dom, {}).get("dram_bytes_per_launch"),
+            "traffic_source": measured.get("source"),
+            "algorithmic_bytes_per_launch": bytes_by[dom] / max(1, sum(
+                1 for _, r in traffic if (("fused_bytes" in r) if dom == "fused"
+                                          else ("gemm_bytes" in r)))),
             "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6.65 TB/s",
             "per_stage": {k: {"ms_per_step": 1e3 * stages.get(k, 0.0) / args.steps,
                               "GBps": (bytes_by[k] / stages[k] / 1e9) if stages.get(k) else None}
-                          for k in ("gather", "matmul", "scatter")},
+                          for k in ("gather", "matmul", "scatter", "fused")},
             "gemm_tflops": flops / stages["matmul"] / 1e12 if stages.get("matmul") else None,
             "gemm_tensor_frac": (flops / stages["matmul"] / 1e12) / tc_peak
             if stages.get("matmul") else None,
+            "fused_tflops_executed": fused_flops / stages["fused"] / 1e12
+            if stages.get("fused") else None,
+            "fused_tensor_frac": (fused_flops / stages["fused"] / 1e12) / tc_peak
+            if stages.get("fused") else None,
             "mapping_ms_per_step": 1e3 * stages.get("mapping", 0.0) / args.steps,
             "other_ms_per_step": 1e3 * stages.get("other", 0.0) / args.steps}
 
@@ -346,7 +361,7 @@ def main():
             f = h_feats.to(dev, non_blocking=True)
             t = sc.SparseTensor(c, f, 1, boundary, B)  # validated, as a user would
             t = sc.quantize_features(t, sc.PrecisionMode.FP16_STORAGE)
-            o = model.forward(t, sc.ExecOptions(index_kind="hash"))
+            o = model.forward(t, sc.ExecOptions(index_kind="hash", dataflow=args.dataflow))
             h_out.copy_(o.features, non_blocking=True)
             return o
 
