@@ -27,14 +27,19 @@ using namespace ::scb::ptx;
 
 constexpr int BM = 128;
 constexpr int THREADS = 320;
-constexpr int LAG = 2;                  // cp.async groups in flight per producer thread
 constexpr int EPI_BUF = 32 * 64;        // 32 rows x 64 B (32 fp16 columns)
 constexpr int EPI_BYTES = 4 * 2 * EPI_BUF;
+constexpr int MAX_OPS = 8;              // kernel offsets per pipeline stage
 
 struct Params {
   long long n_out, ldf;
   int c_in, c_out, n_pad, kc, n_kchunks, stages, swz, epi_cols, total_tiles, relu;
-  uint32_t idesc, tmem_cols, a_stage_bytes, stage_bytes, b_tx_bytes;
+  int ops;                  // offsets per stage (small C_in -> several)
+  int groups;               // ceil(V / ops) offset groups per tile
+  uint32_t idesc, tmem_cols;
+  uint32_t a_off_bytes;     // one offset's A block [128 rows][kc]
+  uint32_t b_off_bytes;     // one offset's B block [n_pad][kc]
+  uint32_t a_stage_bytes, stage_bytes, b_tx_bytes;
   const int* hits;          // [V][n_out] input row or -1
   const __half* feat;       // [n_in][ldf]
   const float* scale;       // nullable (with shift)
@@ -54,7 +59,10 @@ __device__ __forceinline__ uint32_t pack_half2(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
-template <int V>
+// Pipeline stage = (tile, offset group g, K chunk kk): A = p.ops offsets x
+// [128 rows][kc] gathered rows, B = the matching p.ops weight slices.
+// LAG = cp.async groups (stages) each producer thread keeps in flight.
+template <int V, int LAG>
 __global__ void __launch_bounds__(THREADS, 1)
     implicit_conv_f16_kernel(const __grid_constant__ CUtensorMap tmB,
                              const __grid_constant__ CUtensorMap tmOut,
@@ -62,8 +70,9 @@ __global__ void __launch_bounds__(THREADS, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* epi_base = smem + (size_t)p.stages * p.stage_bytes;
-  uint32_t* flags = (uint32_t*)(epi_base + EPI_BYTES);  // one word per stage, byte per warp
-  uint64_t* full = (uint64_t*)(flags + ((p.stages + 1) & ~1));
+  int* nbr_s = (int*)(epi_base + EPI_BYTES);                      // [128][V] current tile
+  uint32_t* flags = (uint32_t*)(nbr_s + BM * V);                  // [stages][MAX_OPS]
+  uint64_t* full = (uint64_t*)(flags + ((p.stages * MAX_OPS + 1) & ~1));
   uint64_t* empty = full + p.stages;
   uint64_t* tfull = empty + p.stages;
   uint64_t* tempty = tfull + 2;
@@ -98,17 +107,20 @@ __global__ void __launch_bounds__(THREADS, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    // ============ B producer: weight chunk (n, kk) per stage via TMA
+    // ============ B producer: the stage's weight slices via TMA (offsets
+    // past V land out of bounds and are zero-filled)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
       for (int t = t_begin; t < t_end; ++t)
-        for (int n = 0; n < V; ++n)
+        for (int g = 0; g < p.groups; ++g)
           for (int kk = 0; kk < p.n_kchunks; ++kk) {
             mbar_wait(empty + stage, phase ^ 1);
             mbar_expect_tx(full + stage, p.b_tx_bytes);
-            tma_load_2d(smem + (size_t)stage * p.stage_bytes + p.a_stage_bytes, &tmB, full + stage,
-                        kk * p.kc, n * p.n_pad);
+            uint8_t* sb = smem + (size_t)stage * p.stage_bytes + p.a_stage_bytes;
+            for (int o = 0; o < p.ops; ++o)
+              tma_load_2d(sb + o * p.b_off_bytes, &tmB, full + stage, kk * p.kc,
+                          (g * p.ops + o) * p.n_pad);
             if (++stage == p.stages) { stage = 0; phase ^= 1; }
           }
     }
@@ -124,17 +136,21 @@ __global__ void __launch_bounds__(THREADS, 1)
         tc_after();
         const uint32_t d_tmem = tmem_base + (uint32_t)(acc * p.n_pad);
         uint32_t issued = 0;
-        for (int n = 0; n < V; ++n) {
+        for (int g = 0; g < p.groups; ++g) {
           for (int kk = 0; kk < p.n_kchunks; ++kk) {
             mbar_wait(full + stage, phase);
             tc_after();
-            const bool valid = flags[stage] != 0u;
-            if (valid || (!issued && n == V - 1)) {
-              const uint32_t sa = smem_u32(smem + (size_t)stage * p.stage_bytes);
-              const uint32_t sb = sa + p.a_stage_bytes;
+            const uint32_t sa = smem_u32(smem + (size_t)stage * p.stage_bytes);
+            const uint32_t sb = sa + p.a_stage_bytes;
+            for (int o = 0; o < p.ops; ++o) {
+              const int n = g * p.ops + o;
+              if (n >= V) break;
+              const bool valid = flags[stage * MAX_OPS + o] != 0u;
+              if (!(valid || (!issued && n == V - 1))) continue;
+              const uint32_t ao = sa + o * p.a_off_bytes, bo = sb + o * p.b_off_bytes;
               for (int k = 0; k < p.kc / 16; ++k) {
-                mma_f16(d_tmem, make_sdesc(sa + k * 32, sbo, layout),
-                        make_sdesc(sb + k * 32, sbo, layout), p.idesc, issued);
+                mma_f16(d_tmem, make_sdesc(ao + k * 32, sbo, layout),
+                        make_sdesc(bo + k * 32, sbo, layout), p.idesc, issued);
                 issued = 1;
               }
             }
@@ -147,11 +163,14 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
     }
   } else if (warp < 6) {
-    // ============ A producers: row `row` of the tile, all offsets
+    // ============ A producers: thread = row of the tile; its V neighbour rows
+    // come from the hit matrix (prefetched one tile ahead into registers,
+    // parked in smem for runtime indexing) and are copied with cp.async.
     const int row = threadIdx.x - 64;
     const int wbyte = warp - 2;
     const int chunks = p.kc / 8;  // 16-B chunks per row per K chunk
-    int cur[V], nxt[V];
+    int* my_nbr = nbr_s + row * V;
+    int nxt[V];
     {
       const long long k = (long long)t_begin * BM + row;
 #pragma unroll
@@ -162,27 +181,30 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint32_t phase = 0;
     for (int t = t_begin; t < t_end; ++t) {
 #pragma unroll
-      for (int n = 0; n < V; ++n) cur[n] = nxt[n];
-      {  // prefetch the next tile's neighbour rows into registers
+      for (int n = 0; n < V; ++n) my_nbr[n] = nxt[n];
+      {
         const long long k = (long long)(t + 1) * BM + row;
         const bool ok = (t + 1 < t_end) && k < p.n_out;
 #pragma unroll
         for (int n = 0; n < V; ++n) nxt[n] = ok ? __ldg(p.hits + (long long)n * p.n_out + k) : -1;
       }
-#pragma unroll
-      for (int n = 0; n < V; ++n) {
-        const int j = cur[n];
-        const bool any = __any_sync(0xffffffffu, j >= 0);
-        const __half* src_row = p.feat + (j >= 0 ? (long long)j * p.ldf : 0);
+      for (int g = 0; g < p.groups; ++g) {
         for (int kk = 0; kk < p.n_kchunks; ++kk) {
           mbar_wait(empty + stage, phase ^ 1);
-          if (lane == 0) reinterpret_cast<uint8_t*>(flags + stage)[wbyte] = any ? 1 : 0;
           const uint32_t dst = smem_u32(smem + (size_t)stage * p.stage_bytes);
-          for (int c = 0; c < chunks; ++c) {
-            const int col = kk * p.kc + c * 8;
-            const bool ok = j >= 0 && col < p.c_in;
-            cp_async16(dst + swz_off(row, c, p.swz), ok ? (const void*)(src_row + col)
-                                                          : (const void*)p.feat, ok ? 16u : 0u);
+          for (int o = 0; o < p.ops; ++o) {
+            const int n = g * p.ops + o;
+            const int j = n < V ? my_nbr[n] : -1;
+            const bool any = __any_sync(0xffffffffu, j >= 0);
+            if (lane == 0) reinterpret_cast<uint8_t*>(flags + stage * MAX_OPS + o)[wbyte] = any;
+            const __half* src_row = p.feat + (j >= 0 ? (long long)j * p.ldf : 0);
+            const uint32_t d = dst + o * p.a_off_bytes;
+            for (int c = 0; c < chunks; ++c) {
+              const int col = kk * p.kc + c * 8;
+              const bool ok = j >= 0 && col < p.c_in;
+              cp_async16(d + swz_off(row, c, p.swz),
+                         ok ? (const void*)(src_row + col) : (const void*)p.feat, ok ? 16u : 0u);
+            }
           }
           cp_async_commit();
           if (++pending > LAG) {
@@ -348,9 +370,18 @@ extern "C" int32_t scb_conv_implicit(const void* features, int64_t n_in, int32_t
   while (cols < (uint32_t)(2 * n_pad)) cols *= 2;
   p.tmem_cols = cols;
   auto r1024 = [](uint32_t x) { return (x + 1023u) / 1024u * 1024u; };
-  p.a_stage_bytes = r1024((uint32_t)(BM * p.kc * 2));
-  p.stage_bytes = p.a_stage_bytes + r1024((uint32_t)(n_pad * p.kc * 2));
-  p.b_tx_bytes = (uint32_t)(n_pad * p.kc * 2);
+  p.a_off_bytes = r1024((uint32_t)(BM * p.kc * 2));
+  p.b_off_bytes = r1024((uint32_t)(n_pad * p.kc * 2));
+  // several offsets per stage when one offset's chunk is small, so each
+  // barrier round trip moves ~40 KB
+  int ops = (int)(40960u / (p.a_off_bytes + p.b_off_bytes));
+  ops = ops < 1 ? 1 : (ops > MAX_OPS ? MAX_OPS : ops);
+  if (ops > volume) ops = volume;
+  p.ops = ops;
+  p.groups = (volume + ops - 1) / ops;
+  p.a_stage_bytes = ops * p.a_off_bytes;
+  p.stage_bytes = ops * (p.a_off_bytes + p.b_off_bytes);
+  p.b_tx_bytes = (uint32_t)(ops * n_pad * p.kc * 2);
   p.hits = hits;
   p.feat = (const __half*)features;
   p.scale = scale;
@@ -358,12 +389,13 @@ extern "C" int32_t scb_conv_implicit(const void* features, int64_t n_in, int32_t
   p.bias = bias;
   p.residual = (const __half*)residual;
   const int smem_cap = 227 * 1024;
-  const int fixed = 1024 + EPI_BYTES + 64 * 4 + 64 * 8 + 64;
+  const int fixed = 1024 + EPI_BYTES + BM * volume * 4 + 32 * MAX_OPS * 4 + 40 * 8 + 64;
   int stages = (smem_cap - fixed) / (int)p.stage_bytes;
   if (stages > 16) stages = 16;
-  SCB_CHECK_ARG(stages > LAG, "stage does not fit in shared memory");
+  SCB_CHECK_ARG(stages >= 2, "stage does not fit in shared memory");
   p.stages = stages;
   const int smem = fixed + stages * (int)p.stage_bytes;
+  const int lag = stages >= 9 ? 8 : (stages >= 5 ? 4 : (stages >= 3 ? 2 : 1));
 
   CUtensorMap mB, mO;
   std::string err;
@@ -376,23 +408,23 @@ extern "C" int32_t scb_conv_implicit(const void* features, int64_t n_in, int32_t
   }
   cudaStream_t s = as_stream(stream);
   const int grid = p.total_tiles < device_sms() ? p.total_tiles : device_sms();
-  if (volume == 27) {
-    static bool cfg = false;
-    if (!cfg) {
-      SCB_CUDA(cudaFuncSetAttribute(implicit_conv_f16_kernel<27>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem_cap));
-      cfg = true;
-    }
-    implicit_conv_f16_kernel<27><<<grid, THREADS, smem, s>>>(mB, mO, p);
-  } else {
-    static bool cfg = false;
-    if (!cfg) {
-      SCB_CUDA(cudaFuncSetAttribute(implicit_conv_f16_kernel<8>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem_cap));
-      cfg = true;
-    }
-    implicit_conv_f16_kernel<8><<<grid, THREADS, smem, s>>>(mB, mO, p);
-  }
+  auto launch = [&](auto kernel) -> int {
+    SCB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_cap));
+    kernel<<<grid, THREADS, smem, s>>>(mB, mO, p);
+    return SCB_OK;
+  };
+  int rc;
+  if (volume == 27)
+    rc = lag == 8 ? launch(implicit_conv_f16_kernel<27, 8>)
+         : lag == 4 ? launch(implicit_conv_f16_kernel<27, 4>)
+         : lag == 2 ? launch(implicit_conv_f16_kernel<27, 2>)
+                    : launch(implicit_conv_f16_kernel<27, 1>);
+  else
+    rc = lag == 8 ? launch(implicit_conv_f16_kernel<8, 8>)
+         : lag == 4 ? launch(implicit_conv_f16_kernel<8, 4>)
+         : lag == 2 ? launch(implicit_conv_f16_kernel<8, 2>)
+                    : launch(implicit_conv_f16_kernel<8, 1>);
+  if (rc != SCB_OK) return rc;
   SCB_LAUNCHED();
   return SCB_OK;
 }
