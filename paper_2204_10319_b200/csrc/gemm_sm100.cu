@@ -340,6 +340,27 @@ bool encode_map_2d(CUtensorMap* m, CUtensorMapDataType dt, int esize, const void
   return true;
 }
 
+bool encode_map_1d(CUtensorMap* m, CUtensorMapDataType dt, const void* base, long long n, int box,
+                   std::string& err) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) {
+    err = "cuTensorMapEncodeTiled unavailable";
+    return false;
+  }
+  cuuint64_t dims[1] = {(cuuint64_t)(n > 0 ? n : 1)};
+  cuuint64_t strides[1] = {0};
+  cuuint32_t boxd[1] = {(cuuint32_t)box};
+  cuuint32_t estr[1] = {1};
+  CUresult r = fn(m, dt, 1, const_cast<void*>(base), dims, strides, boxd, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    err = "cuTensorMapEncodeTiled (1-D) failed (" + std::to_string((int)r) + ")";
+    return false;
+  }
+  return true;
+}
+
 int device_sms() {
   static int n = [] {
     int dev = 0, v = 148;

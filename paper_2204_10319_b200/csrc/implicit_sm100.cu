@@ -4,17 +4,21 @@
 //   out[k] = epilogue( sum_n  features[hits[n][k]] . W[n] )      (absent -> 0)
 //
 // for 128-row output tiles, accumulating all V offsets in TMEM.  The gather is
-// fused into the MMA operand load (cp.async 16-B row chunks straight into the
-// swizzled UMMA layout, zero-filled for absent neighbours), so neither the
-// gather buffer nor the f32 partials ever reach HBM; each output row is
-// written once (fp16) with BN / bias / residual / ReLU applied in registers.
-// Offsets with no neighbour anywhere in a tile skip their MMAs.
+// done by the TMA engine itself (cp.async.bulk.tensor ... tile::gather4: four
+// arbitrary feature rows per instruction, straight into the 128/64/32-B
+// swizzled UMMA operand layout; absent neighbours are out-of-bounds rows and
+// are zero-filled without a memory read), so neither the gather buffer nor
+// the f32 partials ever reach HBM.  Each output row is written once (fp16)
+// with BN / bias / residual / ReLU applied in registers.  Offsets with no
+// neighbour anywhere in a tile skip their MMAs.
 //
-// Warp roles (320 threads, 1 CTA / SM):
-//   warp 0     TMA producer of the weight chunks (B, K-major fp16)
+// Warp roles (192 threads, 1 CTA / SM, persistent over contiguous tile ranges):
+//   warp 0     producer: per tile one 1-D TMA per offset brings the tile's
+//              neighbour rows (hits[n][tile]) into smem (double-buffered, one
+//              tile ahead); per stage each lane issues one gather4 per offset
+//              for its 4 rows, lane 0 the weight-slice TMA loads
 //   warp 1     TMEM allocator + single-thread tcgen05.mma issuer
-//   warps 2-5  A producers: one output row each, cp.async gather
-//   warps 6-9  epilogue: tcgen05.ld -> epilogue -> swizzled smem -> TMA store
+//   warps 2-5  epilogue: tcgen05.ld -> epilogue -> swizzled smem -> TMA store
 #include <cuda.h>
 
 #include "common.cuh"
@@ -26,22 +30,22 @@ namespace ic {
 using namespace ::scb::ptx;
 
 constexpr int BM = 128;
-constexpr int THREADS = 320;
+constexpr int THREADS = 192;
 constexpr int EPI_BUF = 32 * 64;        // 32 rows x 64 B (32 fp16 columns)
 constexpr int EPI_BYTES = 4 * 2 * EPI_BUF;
 constexpr int MAX_OPS = 8;              // kernel offsets per pipeline stage
+constexpr int MAX_V = 27;
 
 struct Params {
-  long long n_out, ldf;
-  int c_in, c_out, n_pad, kc, n_kchunks, stages, swz, epi_cols, total_tiles, relu;
+  long long n_out;
+  int n_in, c_in, c_out, V, n_pad, kc, n_kchunks, stages, swz, epi_cols, total_tiles, relu;
   int ops;                  // offsets per stage (small C_in -> several)
   int groups;               // ceil(V / ops) offset groups per tile
   uint32_t idesc, tmem_cols;
-  uint32_t a_off_bytes;     // one offset's A block [128 rows][kc]
-  uint32_t b_off_bytes;     // one offset's B block [n_pad][kc]
-  uint32_t a_stage_bytes, stage_bytes, b_tx_bytes;
-  const int* hits;          // [V][n_out] input row or -1
-  const __half* feat;       // [n_in][ldf]
+  uint32_t a_off_bytes;     // one offset's A block [128 rows][kc] (1024-aligned)
+  uint32_t b_off_bytes;     // one offset's B block [n_pad][kc]   (1024-aligned)
+  uint32_t a_stage_bytes, stage_bytes;
+  uint32_t a_tx, b_tx;      // bytes one offset's A / B loads deliver
   const float* scale;       // nullable (with shift)
   const float* shift;
   const float* bias;        // nullable
@@ -59,24 +63,23 @@ __device__ __forceinline__ uint32_t pack_half2(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
-// Pipeline stage = (tile, offset group g, K chunk kk): A = p.ops offsets x
-// [128 rows][kc] gathered rows, B = the matching p.ops weight slices.
-// LAG = cp.async groups (stages) each producer thread keeps in flight.
-template <int V, int LAG>
 __global__ void __launch_bounds__(THREADS, 1)
-    implicit_conv_f16_kernel(const __grid_constant__ CUtensorMap tmB,
+    implicit_conv_f16_kernel(const __grid_constant__ CUtensorMap tmFeat,
+                             const __grid_constant__ CUtensorMap tmHits,
+                             const __grid_constant__ CUtensorMap tmB,
                              const __grid_constant__ CUtensorMap tmOut,
                              const __grid_constant__ Params p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* epi_base = smem + (size_t)p.stages * p.stage_bytes;
-  int* nbr_s = (int*)(epi_base + EPI_BYTES);                      // [128][V] current tile
-  uint32_t* flags = (uint32_t*)(nbr_s + BM * V);                  // [stages][MAX_OPS]
-  uint64_t* full = (uint64_t*)(flags + ((p.stages * MAX_OPS + 1) & ~1));
+  int* nbr_s = (int*)(epi_base + EPI_BYTES);                      // [2][MAX_V][128]
+  uint32_t* flags = (uint32_t*)(nbr_s + 2 * MAX_V * BM);          // [stages][MAX_OPS]
+  uint64_t* full = (uint64_t*)(flags + p.stages * MAX_OPS);
   uint64_t* empty = full + p.stages;
   uint64_t* tfull = empty + p.stages;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+  uint64_t* idx_full = tempty + 2;
+  uint32_t* tmem_slot = (uint32_t*)(idx_full + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int t_begin = (int)((long long)p.total_tiles * blockIdx.x / gridDim.x);
@@ -84,14 +87,17 @@ __global__ void __launch_bounds__(THREADS, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < p.stages; ++s) {
-      mbar_init(full + s, 4 * 32 + 1);  // 128 gather threads + the B expect_tx arrive
+      mbar_init(full + s, 1);
       mbar_init(empty + s, 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull + a, 1);
       mbar_init(tempty + a, 4);
+      mbar_init(idx_full + a, 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmFeat) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmHits) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmOut) : "memory");
   }
@@ -107,28 +113,74 @@ __global__ void __launch_bounds__(THREADS, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    // ============ B producer: the stage's weight slices via TMA (offsets
-    // past V land out of bounds and are zero-filled)
-    if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int t = t_begin; t < t_end; ++t)
-        for (int g = 0; g < p.groups; ++g)
-          for (int kk = 0; kk < p.n_kchunks; ++kk) {
-            mbar_wait(empty + stage, phase ^ 1);
-            mbar_expect_tx(full + stage, p.b_tx_bytes);
-            uint8_t* sb = smem + (size_t)stage * p.stage_bytes + p.a_stage_bytes;
-            for (int o = 0; o < p.ops; ++o)
-              tma_load_2d(sb + o * p.b_off_bytes, &tmB, full + stage, kk * p.kc,
-                          (g * p.ops + o) * p.n_pad);
-            if (++stage == p.stages) { stage = 0; phase ^= 1; }
+    // ============ producer warp
+    const int V = p.V;
+    auto load_idx = [&](int t, int buf) {  // hits[n][t*128 .. +128) for every n
+      if (lane == 0) {
+        mbar_expect_tx(idx_full + buf, (uint32_t)(V * BM * 4));
+        for (int n = 0; n < V; ++n)
+          tma_load_1d(nbr_s + (buf * MAX_V + n) * BM, &tmHits, idx_full + buf,
+                      (int)((long long)n * p.n_out + (long long)t * BM));
+      }
+    };
+    if (t_begin < t_end) load_idx(t_begin, 0);
+    int stage = 0;
+    uint32_t phase = 0, idx_phase0 = 0, idx_phase1 = 0;
+    for (int t = t_begin, buf = 0; t < t_end; ++t, buf ^= 1) {
+      fence_async_smem();  // our generic reads of the other buffer precede its TMA refill
+      __syncwarp();
+      if (t + 1 < t_end) load_idx(t + 1, buf ^ 1);
+      mbar_wait(idx_full + buf, buf ? idx_phase1 : idx_phase0);
+      if (buf) idx_phase1 ^= 1; else idx_phase0 ^= 1;
+      const int* nb = nbr_s + buf * MAX_V * BM;
+      for (int g = 0; g < p.groups; ++g) {
+        int4 rows[MAX_OPS];
+        uint32_t n_valid = 0, anymask = 0;
+#pragma unroll
+        for (int o = 0; o < MAX_OPS; ++o) {
+          if (o >= p.ops) break;
+          const int n = g * p.ops + o;
+          int4 r = make_int4(-1, -1, -1, -1);
+          if (n < V) {
+            r = *reinterpret_cast<const int4*>(nb + n * BM + 4 * lane);
+            ++n_valid;
           }
+          if (__any_sync(0xffffffffu, r.x >= 0 || r.y >= 0 || r.z >= 0 || r.w >= 0))
+            anymask |= 1u << o;
+          // absent neighbours -> row n_in (out of bounds -> zero fill, no read)
+          r.x = r.x < 0 ? p.n_in : r.x;
+          r.y = r.y < 0 ? p.n_in : r.y;
+          r.z = r.z < 0 ? p.n_in : r.z;
+          r.w = r.w < 0 ? p.n_in : r.w;
+          rows[o] = r;
+        }
+        for (int kk = 0; kk < p.n_kchunks; ++kk) {
+          if (lane == 0) {
+            mbar_wait(empty + stage, phase ^ 1);
+            for (int o = 0; o < p.ops; ++o) flags[stage * MAX_OPS + o] = (anymask >> o) & 1u;
+            mbar_expect_tx(full + stage, n_valid * (p.a_tx + p.b_tx));
+          }
+          __syncwarp();
+          uint8_t* sa = smem + (size_t)stage * p.stage_bytes;
+#pragma unroll
+          for (int o = 0; o < MAX_OPS; ++o) {
+            if (o >= (int)n_valid) break;
+            tma_gather4(sa + o * p.a_off_bytes + 4 * lane * (p.kc * 2), &tmFeat, full + stage,
+                        kk * p.kc, rows[o].x, rows[o].y, rows[o].z, rows[o].w);
+            if (lane == 0)
+              tma_load_2d(sa + p.a_stage_bytes + o * p.b_off_bytes, &tmB, full + stage, kk * p.kc,
+                          (g * p.ops + o) * p.n_pad);
+          }
+          if (++stage == p.stages) { stage = 0; phase ^= 1; }
+        }
+      }
     }
   } else if (warp == 1) {
     // ============ MMA issuer
     if (lane == 0) {
       const uint32_t layout = p.swz == 128 ? 2u : (p.swz == 64 ? 4u : 6u);
       const uint32_t sbo = 8u * (uint32_t)p.swz;
+      const int V = p.V;
       int stage = 0, acc = 0;
       uint32_t phase = 0, acc_phase = 0;
       for (int t = t_begin; t < t_end; ++t) {
@@ -162,73 +214,10 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
     }
-  } else if (warp < 6) {
-    // ============ A producers: thread = row of the tile; its V neighbour rows
-    // come from the hit matrix (prefetched one tile ahead into registers,
-    // parked in smem for runtime indexing) and are copied with cp.async.
-    const int row = threadIdx.x - 64;
-    const int wbyte = warp - 2;
-    const int chunks = p.kc / 8;  // 16-B chunks per row per K chunk
-    int* my_nbr = nbr_s + row * V;
-    int nxt[V];
-    {
-      const long long k = (long long)t_begin * BM + row;
-#pragma unroll
-      for (int n = 0; n < V; ++n)
-        nxt[n] = (t_begin < t_end && k < p.n_out) ? __ldg(p.hits + (long long)n * p.n_out + k) : -1;
-    }
-    int stage = 0, sig = 0, pending = 0;
-    uint32_t phase = 0;
-    for (int t = t_begin; t < t_end; ++t) {
-#pragma unroll
-      for (int n = 0; n < V; ++n) my_nbr[n] = nxt[n];
-      {
-        const long long k = (long long)(t + 1) * BM + row;
-        const bool ok = (t + 1 < t_end) && k < p.n_out;
-#pragma unroll
-        for (int n = 0; n < V; ++n) nxt[n] = ok ? __ldg(p.hits + (long long)n * p.n_out + k) : -1;
-      }
-      for (int g = 0; g < p.groups; ++g) {
-        for (int kk = 0; kk < p.n_kchunks; ++kk) {
-          mbar_wait(empty + stage, phase ^ 1);
-          const uint32_t dst = smem_u32(smem + (size_t)stage * p.stage_bytes);
-          for (int o = 0; o < p.ops; ++o) {
-            const int n = g * p.ops + o;
-            const int j = n < V ? my_nbr[n] : -1;
-            const bool any = __any_sync(0xffffffffu, j >= 0);
-            if (lane == 0) reinterpret_cast<uint8_t*>(flags + stage * MAX_OPS + o)[wbyte] = any;
-            const __half* src_row = p.feat + (j >= 0 ? (long long)j * p.ldf : 0);
-            const uint32_t d = dst + o * p.a_off_bytes;
-            for (int c = 0; c < chunks; ++c) {
-              const int col = kk * p.kc + c * 8;
-              const bool ok = j >= 0 && col < p.c_in;
-              cp_async16(d + swz_off(row, c, p.swz),
-                         ok ? (const void*)(src_row + col) : (const void*)p.feat, ok ? 16u : 0u);
-            }
-          }
-          cp_async_commit();
-          if (++pending > LAG) {
-            cp_async_wait<LAG>();
-            fence_async_smem();  // generic-proxy smem writes -> visible to tcgen05 (async proxy)
-            mbar_arrive(full + sig);
-            if (++sig == p.stages) sig = 0;
-            --pending;
-          }
-          if (++stage == p.stages) { stage = 0; phase ^= 1; }
-        }
-      }
-    }
-    cp_async_wait<0>();
-    fence_async_smem();
-    while (pending > 0) {
-      mbar_arrive(full + sig);
-      if (++sig == p.stages) sig = 0;
-      --pending;
-    }
   } else {
     // ============ epilogue
     const int q = warp & 3;
-    uint8_t* bufs = epi_base + (warp - 6) * 2 * EPI_BUF;
+    uint8_t* bufs = epi_base + (warp - 2) * 2 * EPI_BUF;
     int acc = 0, nbuf = 0;
     uint32_t acc_phase = 0;
     const int chunks = p.n_pad / p.epi_cols;
@@ -330,6 +319,8 @@ __global__ void __launch_bounds__(THREADS, 1)
 bool encode_map_2d(CUtensorMap* m, CUtensorMapDataType dt, int esize, const void* base,
                    long long inner, long long rows, long long ld, int box_inner, int box_rows,
                    int swz_bytes, std::string& err);
+bool encode_map_1d(CUtensorMap* m, CUtensorMapDataType dt, const void* base, long long n, int box,
+                   std::string& err);
 int device_sms();
 
 }  // namespace scb
@@ -343,21 +334,23 @@ extern "C" int32_t scb_conv_implicit(const void* features, int64_t n_in, int32_t
                                      const float* bias, const void* residual, int32_t relu,
                                      scb_stream_t stream) {
   using namespace ic;
-  SCB_CHECK_ARG(volume == 8 || volume == 27, "implicit conv supports K^3 = 8 or 27 offsets");
+  SCB_CHECK_ARG(volume >= 1 && volume <= MAX_V, "implicit conv supports up to 27 offsets");
   SCB_CHECK_ARG(c_in % 8 == 0 && ldf % 8 == 0, "C_in and its row stride must be multiples of 8");
   SCB_CHECK_ARG(c_out % 8 == 0, "C_out must be a multiple of 8");
   SCB_CHECK_ARG((scale == nullptr) == (shift == nullptr), "scale and shift go together");
+  SCB_CHECK_ARG(n_in < (1LL << 31) - 1 && (long long)volume * n_out < (1LL << 31),
+                "too many rows for 32-bit TMA coordinates");
   const int n_pad = (c_out + 15) / 16 * 16;
   const int k_pad = (c_in + 15) / 16 * 16;
   SCB_CHECK_ARG(n_pad <= 256, "C_out > 256 not supported by the implicit conv");
-  (void)n_in;
   if (n_out == 0) return SCB_OK;
   Params p;
   memset(&p, 0, sizeof(p));
   p.n_out = n_out;
-  p.ldf = ldf;
+  p.n_in = (int)n_in;
   p.c_in = c_in;
   p.c_out = c_out;
+  p.V = volume;
   p.n_pad = n_pad;
   p.kc = (k_pad % 64 == 0) ? 64 : ((k_pad % 32 == 0) ? 32 : 16);
   p.swz = p.kc * 2;
@@ -370,61 +363,50 @@ extern "C" int32_t scb_conv_implicit(const void* features, int64_t n_in, int32_t
   while (cols < (uint32_t)(2 * n_pad)) cols *= 2;
   p.tmem_cols = cols;
   auto r1024 = [](uint32_t x) { return (x + 1023u) / 1024u * 1024u; };
-  p.a_off_bytes = r1024((uint32_t)(BM * p.kc * 2));
-  p.b_off_bytes = r1024((uint32_t)(n_pad * p.kc * 2));
-  // several offsets per stage when one offset's chunk is small, so each
-  // barrier round trip moves ~40 KB
-  int ops = (int)(40960u / (p.a_off_bytes + p.b_off_bytes));
+  p.a_tx = (uint32_t)(BM * p.kc * 2);
+  p.b_tx = (uint32_t)(n_pad * p.kc * 2);
+  p.a_off_bytes = r1024(p.a_tx);
+  p.b_off_bytes = r1024(p.b_tx);
+  // several offsets per stage when one offset's chunk is small (~48 KB/stage)
+  int ops = (int)(49152u / (p.a_off_bytes + p.b_off_bytes));
   ops = ops < 1 ? 1 : (ops > MAX_OPS ? MAX_OPS : ops);
   if (ops > volume) ops = volume;
   p.ops = ops;
   p.groups = (volume + ops - 1) / ops;
   p.a_stage_bytes = ops * p.a_off_bytes;
   p.stage_bytes = ops * (p.a_off_bytes + p.b_off_bytes);
-  p.b_tx_bytes = (uint32_t)(ops * n_pad * p.kc * 2);
-  p.hits = hits;
-  p.feat = (const __half*)features;
   p.scale = scale;
   p.shift = shift;
   p.bias = bias;
   p.residual = (const __half*)residual;
   const int smem_cap = 227 * 1024;
-  const int fixed = 1024 + EPI_BYTES + BM * volume * 4 + 32 * MAX_OPS * 4 + 40 * 8 + 64;
+  const int fixed = 1024 + EPI_BYTES + 2 * MAX_V * BM * 4 + 16 * MAX_OPS * 4 + 40 * 8 + 64;
   int stages = (smem_cap - fixed) / (int)p.stage_bytes;
   if (stages > 16) stages = 16;
   SCB_CHECK_ARG(stages >= 2, "stage does not fit in shared memory");
   p.stages = stages;
   const int smem = fixed + stages * (int)p.stage_bytes;
-  const int lag = stages >= 9 ? 8 : (stages >= 5 ? 4 : (stages >= 3 ? 2 : 1));
 
-  CUtensorMap mB, mO;
+  CUtensorMap mF, mH, mB, mO;
   std::string err;
-  if (!encode_map_2d(&mB, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, weights_packed, k_pad,
+  if (!encode_map_2d(&mF, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, features, c_in, n_in, ldf, p.kc, 1,
+                     p.swz, err) ||
+      !encode_map_1d(&mH, CU_TENSOR_MAP_DATA_TYPE_INT32, hits, (long long)volume * n_out, BM, err) ||
+      !encode_map_2d(&mB, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, weights_packed, k_pad,
                      (long long)volume * n_pad, k_pad, p.kc, n_pad, p.swz, err) ||
       !encode_map_2d(&mO, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, out, c_out, n_out, c_out,
                      p.epi_cols, 32, p.epi_cols * 2, err)) {
     set_error(std::string("scb_conv_implicit: ") + err);
     return SCB_ECUDA;
   }
-  cudaStream_t s = as_stream(stream);
+  static bool configured = false;
+  if (!configured) {
+    SCB_CUDA(cudaFuncSetAttribute(implicit_conv_f16_kernel,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem_cap));
+    configured = true;
+  }
   const int grid = p.total_tiles < device_sms() ? p.total_tiles : device_sms();
-  auto launch = [&](auto kernel) -> int {
-    SCB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_cap));
-    kernel<<<grid, THREADS, smem, s>>>(mB, mO, p);
-    return SCB_OK;
-  };
-  int rc;
-  if (volume == 27)
-    rc = lag == 8 ? launch(implicit_conv_f16_kernel<27, 8>)
-         : lag == 4 ? launch(implicit_conv_f16_kernel<27, 4>)
-         : lag == 2 ? launch(implicit_conv_f16_kernel<27, 2>)
-                    : launch(implicit_conv_f16_kernel<27, 1>);
-  else
-    rc = lag == 8 ? launch(implicit_conv_f16_kernel<8, 8>)
-         : lag == 4 ? launch(implicit_conv_f16_kernel<8, 4>)
-         : lag == 2 ? launch(implicit_conv_f16_kernel<8, 2>)
-                    : launch(implicit_conv_f16_kernel<8, 1>);
-  if (rc != SCB_OK) return rc;
+  implicit_conv_f16_kernel<<<grid, THREADS, smem, as_stream(stream)>>>(mF, mH, mB, mO, p);
   SCB_LAUNCHED();
   return SCB_OK;
 }
