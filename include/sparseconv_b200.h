@@ -112,7 +112,10 @@ int32_t scb_unflatten(const int64_t* keys, int64_t n, const scb_grid_t* grid, in
  * hit matrix hits[V][n_out] (input row or -1).  With `symmetric` (stride 1,
  * odd K) only offsets 0..centre are probed and the mirror entry
  * hits[V-1-n][j] = k is filled directly, which is exactly the order the
- * reference's stable re-sort produces. */
+ * reference's stable re-sort produces.
+ * Every hit matrix over n rows has row stride scb_hits_ld(n) = roundup(n, 4)
+ * (16-byte aligned rows); allocate V * scb_hits_ld(n) int32. */
+int64_t scb_hits_ld(int64_t n);
 int32_t scb_map_search(int32_t kind, const int32_t* out_coords, int64_t n_out,
                        const scb_grid_t* in_grid, int32_t kernel_size, int32_t offset_base,
                        int32_t stride, int32_t symmetric, const int64_t* table_keys, const int32_t* table_rows,

@@ -48,6 +48,7 @@ _SIGS = {
     "scb_device_sm_count": (_I32, []),
     "scb_launch_count": (_I64, []),
     "scb_hash_slots": (_I64, [_I64]),
+    "scb_hits_ld": (_I64, [_I64]),
     "scb_index_build": (_I32, [_I32, _P, _I64, _GP, _P, _P, _I64, _P, _P]),
     "scb_index_query": (_I32, [_I32, _P, _I64, _GP, _P, _P, _I64, _P, _P]),
     "scb_output_coords_capacity": (_I64, [_I64, _I32, _I32, _I32]),

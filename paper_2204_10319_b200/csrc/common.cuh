@@ -128,6 +128,10 @@ __device__ __forceinline__ int index_lookup(int kind, const int* c, const Grid& 
 
 inline int ceil_div_i(long long a, long long b) { return (int)((a + b - 1) / b); }
 
+// Row stride of a [V][n] hit matrix: n rounded up to 4 entries so every row
+// starts 16-byte aligned (1-D TMA loads of a tile's neighbour rows need it).
+__host__ __device__ __forceinline__ long long hits_ld(long long n) { return (n + 3) & ~3LL; }
+
 // Dispatch on the spatial rank.
 #define SCB_DISPATCH_DIM(dim, ...)          \
   switch (dim) {                            \

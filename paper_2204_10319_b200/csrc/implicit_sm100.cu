@@ -120,7 +120,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         mbar_expect_tx(idx_full + buf, (uint32_t)(V * BM * 4));
         for (int n = 0; n < V; ++n)
           tma_load_1d(nbr_s + (buf * MAX_V + n) * BM, &tmHits, idx_full + buf,
-                      (int)((long long)n * p.n_out + (long long)t * BM));
+                      (int)((long long)n * hits_ld(p.n_out) + (long long)t * BM));
       }
     };
     if (t_begin < t_end) load_idx(t_begin, 0);
@@ -338,7 +338,7 @@ extern "C" int32_t scb_conv_implicit(const void* features, int64_t n_in, int32_t
   SCB_CHECK_ARG(c_in % 8 == 0 && ldf % 8 == 0, "C_in and its row stride must be multiples of 8");
   SCB_CHECK_ARG(c_out % 8 == 0, "C_out must be a multiple of 8");
   SCB_CHECK_ARG((scale == nullptr) == (shift == nullptr), "scale and shift go together");
-  SCB_CHECK_ARG(n_in < (1LL << 31) - 1 && (long long)volume * n_out < (1LL << 31),
+  SCB_CHECK_ARG(n_in < (1LL << 31) - 1 && (long long)volume * hits_ld(n_out) < (1LL << 31),
                 "too many rows for 32-bit TMA coordinates");
   const int n_pad = (c_out + 15) / 16 * 16;
   const int k_pad = (c_in + 15) / 16 * 16;
@@ -391,7 +391,8 @@ extern "C" int32_t scb_conv_implicit(const void* features, int64_t n_in, int32_t
   std::string err;
   if (!encode_map_2d(&mF, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, features, c_in, n_in, ldf, p.kc, 1,
                      p.swz, err) ||
-      !encode_map_1d(&mH, CU_TENSOR_MAP_DATA_TYPE_INT32, hits, (long long)volume * n_out, BM, err) ||
+      !encode_map_1d(&mH, CU_TENSOR_MAP_DATA_TYPE_INT32, hits, (long long)volume * hits_ld(n_out),
+                     BM, err) ||
       !encode_map_2d(&mB, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, weights_packed, k_pad,
                      (long long)volume * n_pad, k_pad, p.kc, n_pad, p.swz, err) ||
       !encode_map_2d(&mO, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, out, c_out, n_out, c_out,

@@ -80,6 +80,8 @@ static int grid_blocks(long long n, int threads, int cap = 148 * 16) {
 
 using namespace scb;
 
+extern "C" int64_t scb_hits_ld(int64_t n) { return hits_ld(n); }
+
 extern "C" int64_t scb_hash_slots(int64_t n) {
   int64_t t = 2;
   while (t < 2 * (n > 1 ? n : 1)) t *= 2;
@@ -295,11 +297,11 @@ __global__ void map_search_kernel(int kind, const int* __restrict__ out_coords, 
 #pragma unroll
     for (int d = 0; d < D; ++d) p[d + 1] = s * out_coords[k * (D + 1) + d + 1] + delta[d];
     const int j = index_lookup<D>(kind, p, gin, keys, rows, mask);
-    hits[(long long)n * n_out + k] = j;
+    hits[(long long)n * hits_ld(n_out) + k] = j;
     // derive_symmetric_maps (mapping.py:322-339): M[V-1-n] holds (k, j) for
     // every (j, k) in M[n]; writing it at row j of the mirror column yields
     // the reference's "sorted by new output row" order for free.
-    if (symmetric && n < center && j >= 0) hits[(long long)(V - 1 - n) * n_out + j] = (int)k;
+    if (symmetric && n < center && j >= 0) hits[(long long)(V - 1 - n) * hits_ld(n_out) + j] = (int)k;
   }
 }
 
@@ -311,7 +313,7 @@ __global__ void __launch_bounds__(CHUNK_THREADS) map_count_kernel(const int* __r
                                                                   long long n_out, int nchunks,
                                                                   int* __restrict__ counts) {
   const int n = blockIdx.y, c = blockIdx.x;
-  const int* col = hits + (long long)n * n_out;
+  const int* col = hits + (long long)n * hits_ld(n_out);
   const long long base = (long long)c * CHUNK;
   int cnt = 0;
 #pragma unroll
@@ -356,7 +358,7 @@ __global__ void __launch_bounds__(CHUNK_THREADS) map_compact_kernel(
     const int* __restrict__ hits, long long n_out, int nchunks, const long long* __restrict__ bases,
     int* __restrict__ in_idx, int* __restrict__ out_idx) {
   const int n = blockIdx.y, c = blockIdx.x;
-  const int* col = hits + (long long)n * n_out;
+  const int* col = hits + (long long)n * hits_ld(n_out);
   const long long base = (long long)c * CHUNK;
   long long out_base = bases[(long long)n * nchunks + c];
   __shared__ int warp_tot[CHUNK_THREADS / 32];
@@ -402,7 +404,7 @@ __global__ void map_transpose_kernel(const long long* __restrict__ offset_ptr,
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
        e += (long long)gridDim.x * blockDim.x) {
     const int n = find_offset(ptr_s, V, e);
-    hits_t[(long long)n * n_in + in_idx[e]] = out_idx[e];
+    hits_t[(long long)n * hits_ld(n_in) + in_idx[e]] = out_idx[e];
   }
 }
 
@@ -412,11 +414,9 @@ __global__ void hits_transpose_kernel(const int* __restrict__ hits, long long to
                                       long long n_out, long long n_in, int* __restrict__ hits_t) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
        i += (long long)gridDim.x * blockDim.x) {
-    const int j = hits[i];
-    if (j >= 0) {
-      const long long n = i / n_out;
-      hits_t[n * n_in + j] = (int)(i - n * n_out);
-    }
+    const long long n = i / n_out, k = i - n * n_out;
+    const int j = hits[n * hits_ld(n_out) + k];
+    if (j >= 0) hits_t[n * hits_ld(n_in) + j] = (int)k;
   }
 }
 
@@ -477,7 +477,8 @@ extern "C" int32_t scb_map_search(int32_t kind, const int32_t* out_coords, int64
   const int searched = sym ? (V - 1) / 2 + 1 : V;
   if (sym && V > 1) {
     const long long c = (V - 1) / 2;
-    SCB_CUDA(cudaMemsetAsync(hits + (c + 1) * n_out, 0xFF, (V - 1 - c) * n_out * sizeof(int32_t), s));
+    SCB_CUDA(cudaMemsetAsync(hits + (c + 1) * hits_ld(n_out), 0xFF,
+                             (V - 1 - c) * hits_ld(n_out) * sizeof(int32_t), s));
   }
   dim3 grid(grid_blocks(n_out, 256, 4096), searched);
   SCB_DISPATCH_DIM(g.dim, map_search_kernel<D><<<grid, 256, 0, s>>>(
@@ -533,7 +534,7 @@ extern "C" int32_t scb_map_transpose(const int64_t* offset_ptr, const int32_t* i
                                      const int32_t* out_idx, int32_t volume, int64_t total,
                                      int64_t n_in, int32_t* hits_t, scb_stream_t stream) {
   cudaStream_t s = as_stream(stream);
-  SCB_CUDA(cudaMemsetAsync(hits_t, 0xFF, (size_t)volume * n_in * sizeof(int32_t), s));
+  SCB_CUDA(cudaMemsetAsync(hits_t, 0xFF, (size_t)volume * hits_ld(n_in) * sizeof(int32_t), s));
   if (total == 0) return SCB_OK;
   map_transpose_kernel<<<grid_blocks(total, 256), 256, (volume + 1) * sizeof(long long), s>>>(
       (const long long*)offset_ptr, in_idx, out_idx, volume, total, n_in, hits_t);
@@ -544,7 +545,7 @@ extern "C" int32_t scb_map_transpose(const int64_t* offset_ptr, const int32_t* i
 extern "C" int32_t scb_hits_transpose(const int32_t* hits, int32_t volume, int64_t n_out,
                                       int64_t n_in, int32_t* hits_t, scb_stream_t stream) {
   cudaStream_t s = as_stream(stream);
-  if (n_in) SCB_CUDA(cudaMemsetAsync(hits_t, 0xFF, (size_t)volume * n_in * sizeof(int32_t), s));
+  if (n_in) SCB_CUDA(cudaMemsetAsync(hits_t, 0xFF, (size_t)volume * hits_ld(n_in) * sizeof(int32_t), s));
   const long long total = (long long)volume * n_out;
   if (total == 0) return SCB_OK;
   hits_transpose_kernel<<<grid_blocks(total, 256), 256, 0, s>>>(hits, total, n_out, n_in, hits_t);

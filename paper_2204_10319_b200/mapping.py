@@ -188,6 +188,12 @@ def compute_output_coords(in_coords, offsets: KernelOffsets, stride: int, out_bo
     return out
 
 
+def _hit_matrix(volume: int, n: int, device) -> torch.Tensor:
+    """Uninitialised [V][ld] int32 hit matrix; ld = n rounded up to 4
+    (scb_hits_ld) so each row is 16-byte aligned."""
+    return torch.empty((volume, max((n + 3) // 4 * 4, 4)), dtype=torch.int32, device=device)
+
+
 def _compact(hits: torch.Tensor, volume: int, n_out: int):
     """Hit matrix [V][n_out] -> CSR map (offset_ptr device, sizes host,
     in_idx, out_idx).  One D2H of V+1 int64 (the map sizes)."""
@@ -251,7 +257,7 @@ class KernelMap:
         if self._hits is None:
             ptr, _, ii, oi = self._ensure_csr()
             V = self.offsets.volume
-            h = torch.empty((V, max(self.n_out, 1)), dtype=torch.int32, device=ii.device)
+            h = _hit_matrix(V, self.n_out, ii.device)
             # hits[n][out_idx[e]] = in_idx[e]: the transpose kernel with roles exchanged
             nat.call("scb_map_transpose", nat.ptr(ptr), nat.ptr(oi), nat.ptr(ii), V,
                      self.total, self.n_out, nat.ptr(h), nat.stream_handle())
@@ -298,7 +304,7 @@ class KernelMap:
         re-sorted order directly: the new hit matrix is indexed by new output row."""
         if self._swapped is None:
             V = self.offsets.volume
-            ht = torch.empty((V, max(self.n_in, 1)), dtype=torch.int32, device=self.device)
+            ht = _hit_matrix(V, self.n_in, self.device)
             if self._hits is not None:
                 nat.call("scb_hits_transpose", nat.ptr(self._hits), V, self.n_out, self.n_in,
                          nat.ptr(ht), nat.stream_handle())
@@ -327,7 +333,7 @@ def map_search(in_index: CoordinateIndex, out_coords, offsets: KernelOffsets, st
     n_out = oc.shape[0]
     if use_symmetry and n_out != in_index.size:
         raise ValueError("symmetric search needs the output set to equal the input set")
-    hits = torch.empty((volume, max(n_out, 1)), dtype=torch.int32, device=oc.device)
+    hits = _hit_matrix(volume, n_out, oc.device)
     grid = nat.make_grid(in_index.boundary, in_index.batch_size)
     nat.call("scb_map_search", in_index.code, nat.ptr(oc), n_out, grid, offsets.kernel_size,
              offsets.base, stride, int(bool(use_symmetry)), nat.ptr(in_index.keys),
