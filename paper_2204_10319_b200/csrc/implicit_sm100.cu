@@ -30,7 +30,7 @@ namespace ic {
 using namespace ::scb::ptx;
 
 constexpr int BM = 128;
-constexpr int THREADS = 192;
+constexpr int THREADS = 320;
 constexpr int EPI_BUF = 32 * 64;        // 32 rows x 64 B (32 fp16 columns)
 constexpr int EPI_BYTES = 4 * 2 * EPI_BUF;
 constexpr int MAX_OPS = 8;              // kernel offsets per pipeline stage
@@ -46,6 +46,9 @@ struct Params {
   uint32_t b_off_bytes;     // one offset's B block [n_pad][kc]   (1024-aligned)
   uint32_t a_stage_bytes, stage_bytes;
   uint32_t a_tx, b_tx;      // bytes one offset's A / B loads deliver
+  long long ldf, ldh;       // feature row stride, hit-matrix row stride
+  const __half* feat;       // [n_in][ldf]
+  const int* hits;          // [V][ldh] input row or -1
   const float* scale;       // nullable (with shift)
   const float* shift;
   const float* bias;        // nullable
@@ -63,23 +66,21 @@ __device__ __forceinline__ uint32_t pack_half2(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
+template <int V, int LAG>
 __global__ void __launch_bounds__(THREADS, 1)
-    implicit_conv_f16_kernel(const __grid_constant__ CUtensorMap tmFeat,
-                             const __grid_constant__ CUtensorMap tmHits,
-                             const __grid_constant__ CUtensorMap tmB,
+    implicit_conv_f16_kernel(const __grid_constant__ CUtensorMap tmB,
                              const __grid_constant__ CUtensorMap tmOut,
                              const __grid_constant__ Params p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* epi_base = smem + (size_t)p.stages * p.stage_bytes;
-  int* nbr_s = (int*)(epi_base + EPI_BYTES);                      // [2][MAX_V][128]
-  uint32_t* flags = (uint32_t*)(nbr_s + 2 * MAX_V * BM);          // [stages][MAX_OPS]
+  int* nbr_s = (int*)(epi_base + EPI_BYTES);                      // [2][V][128]
+  uint32_t* flags = (uint32_t*)(nbr_s + 2 * V * BM);              // [stages][MAX_OPS]
   uint64_t* full = (uint64_t*)(flags + p.stages * MAX_OPS);
   uint64_t* empty = full + p.stages;
   uint64_t* tfull = empty + p.stages;
   uint64_t* tempty = tfull + 2;
-  uint64_t* idx_full = tempty + 2;
-  uint32_t* tmem_slot = (uint32_t*)(idx_full + 2);
+  uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int t_begin = (int)((long long)p.total_tiles * blockIdx.x / gridDim.x);
@@ -87,17 +88,14 @@ __global__ void __launch_bounds__(THREADS, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < p.stages; ++s) {
-      mbar_init(full + s, 1);
+      mbar_init(full + s, 4 * 32 + 1);  // 128 A-producer threads + the B expect_tx arrive
       mbar_init(empty + s, 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull + a, 1);
       mbar_init(tempty + a, 4);
-      mbar_init(idx_full + a, 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmFeat) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmHits) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmOut) : "memory");
   }
@@ -113,74 +111,109 @@ __global__ void __launch_bounds__(THREADS, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    // ============ producer warp
-    const int V = p.V;
-    auto load_idx = [&](int t, int buf) {  // hits[n][t*128 .. +128) for every n
-      if (lane == 0) {
-        mbar_expect_tx(idx_full + buf, (uint32_t)(V * BM * 4));
-        for (int n = 0; n < V; ++n)
-          tma_load_1d(nbr_s + (buf * MAX_V + n) * BM, &tmHits, idx_full + buf,
-                      (int)((long long)n * hits_ld(p.n_out) + (long long)t * BM));
-      }
-    };
-    if (t_begin < t_end) load_idx(t_begin, 0);
-    int stage = 0;
-    uint32_t phase = 0, idx_phase0 = 0, idx_phase1 = 0;
-    for (int t = t_begin, buf = 0; t < t_end; ++t, buf ^= 1) {
-      fence_async_smem();  // our generic reads of the other buffer precede its TMA refill
-      __syncwarp();
-      if (t + 1 < t_end) load_idx(t + 1, buf ^ 1);
-      mbar_wait(idx_full + buf, buf ? idx_phase1 : idx_phase0);
-      if (buf) idx_phase1 ^= 1; else idx_phase0 ^= 1;
-      const int* nb = nbr_s + buf * MAX_V * BM;
-      for (int g = 0; g < p.groups; ++g) {
-        int4 rows[MAX_OPS];
-        uint32_t n_valid = 0, anymask = 0;
-#pragma unroll
-        for (int o = 0; o < MAX_OPS; ++o) {
-          if (o >= p.ops) break;
-          const int n = g * p.ops + o;
-          int4 r = make_int4(-1, -1, -1, -1);
-          if (n < V) {
-            r = *reinterpret_cast<const int4*>(nb + n * BM + 4 * lane);
-            ++n_valid;
-          }
-          if (__any_sync(0xffffffffu, r.x >= 0 || r.y >= 0 || r.z >= 0 || r.w >= 0))
-            anymask |= 1u << o;
-          // absent neighbours -> row n_in (out of bounds -> zero fill, no read)
-          r.x = r.x < 0 ? p.n_in : r.x;
-          r.y = r.y < 0 ? p.n_in : r.y;
-          r.z = r.z < 0 ? p.n_in : r.z;
-          r.w = r.w < 0 ? p.n_in : r.w;
-          rows[o] = r;
-        }
-        for (int kk = 0; kk < p.n_kchunks; ++kk) {
-          if (lane == 0) {
+    // ============ B producer: the stage's weight slices via TMA
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = t_begin; t < t_end; ++t)
+        for (int g = 0; g < p.groups; ++g) {
+          const int nv = min(p.ops, p.V - g * p.ops);
+          for (int kk = 0; kk < p.n_kchunks; ++kk) {
             mbar_wait(empty + stage, phase ^ 1);
-            for (int o = 0; o < p.ops; ++o) flags[stage * MAX_OPS + o] = (anymask >> o) & 1u;
-            mbar_expect_tx(full + stage, n_valid * (p.a_tx + p.b_tx));
-          }
-          __syncwarp();
-          uint8_t* sa = smem + (size_t)stage * p.stage_bytes;
-#pragma unroll
-          for (int o = 0; o < MAX_OPS; ++o) {
-            if (o >= (int)n_valid) break;
-            tma_gather4(sa + o * p.a_off_bytes + 4 * lane * (p.kc * 2), &tmFeat, full + stage,
-                        kk * p.kc, rows[o].x, rows[o].y, rows[o].z, rows[o].w);
-            if (lane == 0)
-              tma_load_2d(sa + p.a_stage_bytes + o * p.b_off_bytes, &tmB, full + stage, kk * p.kc,
+            mbar_expect_tx(full + stage, nv * p.b_tx);
+            uint8_t* sb = smem + (size_t)stage * p.stage_bytes + p.a_stage_bytes;
+            for (int o = 0; o < nv; ++o)
+              tma_load_2d(sb + o * p.b_off_bytes, &tmB, full + stage, kk * p.kc,
                           (g * p.ops + o) * p.n_pad);
+            if (++stage == p.stages) { stage = 0; phase ^= 1; }
+          }
+        }
+    }
+  } else if (warp >= 2 && warp < 6) {
+    // ============ A producers (128 threads).  Thread r owns output row r of
+    // the tile for index bookkeeping: it prefetches that row's V neighbour
+    // rows one tile ahead (registers), parks them in the shared table and
+    // computes the per-offset "any neighbour" flags.  The copies themselves
+    // are spread along rows: consecutive lanes move consecutive 16-B chunks
+    // of consecutive rows, so every warp-wide cp.async reads whole 64/128-B
+    // feature rows (fully used sectors) and writes a contiguous swizzled span.
+    const int row = threadIdx.x - 64;
+    const int wbyte = warp - 2;
+    const int cpr = p.kc / 8;                 // 16-B chunks per row per K chunk
+    const int rows_per_pass = 128 / cpr;
+    int nxt[V];
+    {
+      const long long k = (long long)t_begin * BM + row;
+#pragma unroll
+      for (int n = 0; n < V; ++n)
+        nxt[n] = (t_begin < t_end && k < p.n_out) ? __ldg(p.hits + (long long)n * p.ldh + k) : -1;
+    }
+    int stage = 0, sig = 0, pending = 0;
+    uint32_t phase = 0;
+    for (int t = t_begin, buf = 0; t < t_end; ++t, buf ^= 1) {
+      int* nb = nbr_s + buf * V * BM;
+      uint32_t anymask = 0;
+#pragma unroll
+      for (int n = 0; n < V; ++n) {
+        nb[n * BM + row] = nxt[n];
+        if (__any_sync(0xffffffffu, nxt[n] >= 0)) anymask |= 1u << n;
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");  // the tile's index table is complete
+      {
+        const long long k = (long long)(t + 1) * BM + row;
+        const bool ok = (t + 1 < t_end) && k < p.n_out;
+#pragma unroll
+        for (int n = 0; n < V; ++n) nxt[n] = ok ? __ldg(p.hits + (long long)n * p.ldh + k) : -1;
+      }
+      for (int g = 0; g < p.groups; ++g) {
+        const int nv = min(p.ops, V - g * p.ops);
+        for (int kk = 0; kk < p.n_kchunks; ++kk) {
+          mbar_wait(empty + stage, phase ^ 1);
+          if (lane == 0)
+            for (int o = 0; o < nv; ++o)
+              reinterpret_cast<uint8_t*>(flags + stage * MAX_OPS + o)[wbyte] =
+                  (anymask >> (g * p.ops + o)) & 1u;
+          const uint32_t dst = smem_u32(smem + (size_t)stage * p.stage_bytes);
+          for (int o = 0; o < nv; ++o) {
+            const int* nrow = nb + (g * p.ops + o) * BM;
+            const uint32_t d = dst + o * p.a_off_bytes;
+            for (int pass = 0; pass < cpr; ++pass) {
+              const int q = pass * 128 + row;           // chunk id within the offset block
+              const int r = q / cpr, c = q - r * cpr;   // its row and 16-B chunk
+              const int j = nrow[r];
+              const int col = kk * p.kc + c * 8;
+              const bool ok = j >= 0 && col < p.c_in;
+              cp_async16(d + swz_off(r, c, p.swz),
+                         ok ? (const void*)(p.feat + (long long)j * p.ldf + col)
+                            : (const void*)p.feat,
+                         ok ? 16u : 0u);
+            }
+          }
+          cp_async_commit();
+          if (++pending > LAG) {
+            cp_async_wait<LAG>();
+            fence_async_smem();  // generic-proxy smem writes -> visible to tcgen05 (async proxy)
+            mbar_arrive(full + sig);
+            if (++sig == p.stages) sig = 0;
+            --pending;
           }
           if (++stage == p.stages) { stage = 0; phase ^= 1; }
         }
       }
+      (void)rows_per_pass;
+    }
+    cp_async_wait<0>();
+    fence_async_smem();
+    while (pending > 0) {
+      mbar_arrive(full + sig);
+      if (++sig == p.stages) sig = 0;
+      --pending;
     }
   } else if (warp == 1) {
     // ============ MMA issuer
     if (lane == 0) {
       const uint32_t layout = p.swz == 128 ? 2u : (p.swz == 64 ? 4u : 6u);
       const uint32_t sbo = 8u * (uint32_t)p.swz;
-      const int V = p.V;
       int stage = 0, acc = 0;
       uint32_t phase = 0, acc_phase = 0;
       for (int t = t_begin; t < t_end; ++t) {
@@ -214,10 +247,10 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
     }
-  } else {
+  } else if (warp >= 6) {
     // ============ epilogue
     const int q = warp & 3;
-    uint8_t* bufs = epi_base + (warp - 2) * 2 * EPI_BUF;
+    uint8_t* bufs = epi_base + (warp - 6) * 2 * EPI_BUF;
     int acc = 0, nbuf = 0;
     uint32_t acc_phase = 0;
     const int chunks = p.n_pad / p.epi_cols;
@@ -319,8 +352,6 @@ __global__ void __launch_bounds__(THREADS, 1)
 bool encode_map_2d(CUtensorMap* m, CUtensorMapDataType dt, int esize, const void* base,
                    long long inner, long long rows, long long ld, int box_inner, int box_rows,
                    int swz_bytes, std::string& err);
-bool encode_map_1d(CUtensorMap* m, CUtensorMapDataType dt, const void* base, long long n, int box,
-                   std::string& err);
 int device_sms();
 
 }  // namespace scb
@@ -334,7 +365,7 @@ extern "C" int32_t scb_conv_implicit(const void* features, int64_t n_in, int32_t
                                      const float* bias, const void* residual, int32_t relu,
                                      scb_stream_t stream) {
   using namespace ic;
-  SCB_CHECK_ARG(volume >= 1 && volume <= MAX_V, "implicit conv supports up to 27 offsets");
+  SCB_CHECK_ARG(volume == 8 || volume == 27, "implicit conv supports K^3 = 8 or 27 offsets");
   SCB_CHECK_ARG(c_in % 8 == 0 && ldf % 8 == 0, "C_in and its row stride must be multiples of 8");
   SCB_CHECK_ARG(c_out % 8 == 0, "C_out must be a multiple of 8");
   SCB_CHECK_ARG((scale == nullptr) == (shift == nullptr), "scale and shift go together");
@@ -375,39 +406,54 @@ extern "C" int32_t scb_conv_implicit(const void* features, int64_t n_in, int32_t
   p.groups = (volume + ops - 1) / ops;
   p.a_stage_bytes = ops * p.a_off_bytes;
   p.stage_bytes = ops * (p.a_off_bytes + p.b_off_bytes);
+  p.ldf = ldf;
+  p.ldh = hits_ld(n_out);
+  p.feat = (const __half*)features;
+  p.hits = hits;
   p.scale = scale;
   p.shift = shift;
   p.bias = bias;
   p.residual = (const __half*)residual;
   const int smem_cap = 227 * 1024;
-  const int fixed = 1024 + EPI_BYTES + 2 * MAX_V * BM * 4 + 16 * MAX_OPS * 4 + 40 * 8 + 64;
+  const int fixed = 1024 + EPI_BYTES + 2 * volume * BM * 4 + 16 * MAX_OPS * 4 + 40 * 8 + 64;
   int stages = (smem_cap - fixed) / (int)p.stage_bytes;
   if (stages > 16) stages = 16;
   SCB_CHECK_ARG(stages >= 2, "stage does not fit in shared memory");
   p.stages = stages;
   const int smem = fixed + stages * (int)p.stage_bytes;
+  const int lag = stages >= 9 ? 8 : (stages >= 5 ? 4 : (stages >= 3 ? 2 : 1));
 
-  CUtensorMap mF, mH, mB, mO;
+  CUtensorMap mB, mO;
   std::string err;
-  if (!encode_map_2d(&mF, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, features, c_in, n_in, ldf, p.kc, 1,
-                     p.swz, err) ||
-      !encode_map_1d(&mH, CU_TENSOR_MAP_DATA_TYPE_INT32, hits, (long long)volume * hits_ld(n_out),
-                     BM, err) ||
-      !encode_map_2d(&mB, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, weights_packed, k_pad,
+  if (!encode_map_2d(&mB, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, weights_packed, k_pad,
                      (long long)volume * n_pad, k_pad, p.kc, n_pad, p.swz, err) ||
       !encode_map_2d(&mO, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, out, c_out, n_out, c_out,
                      p.epi_cols, 32, p.epi_cols * 2, err)) {
     set_error(std::string("scb_conv_implicit: ") + err);
     return SCB_ECUDA;
   }
-  static bool configured = false;
-  if (!configured) {
-    SCB_CUDA(cudaFuncSetAttribute(implicit_conv_f16_kernel,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem_cap));
-    configured = true;
-  }
   const int grid = p.total_tiles < device_sms() ? p.total_tiles : device_sms();
-  implicit_conv_f16_kernel<<<grid, THREADS, smem, as_stream(stream)>>>(mF, mH, mB, mO, p);
+  cudaStream_t s = as_stream(stream);
+  auto launch = [&](auto kernel) -> int {
+    SCB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_cap));
+    kernel<<<grid, THREADS, smem, s>>>(mB, mO, p);
+    return SCB_OK;
+  };
+  int rc;
+  if (volume == 27)
+    rc = lag == 8 ? launch(implicit_conv_f16_kernel<27, 8>)
+         : lag == 4 ? launch(implicit_conv_f16_kernel<27, 4>)
+         : lag == 2 ? launch(implicit_conv_f16_kernel<27, 2>)
+                    : launch(implicit_conv_f16_kernel<27, 1>);
+  else if (volume == 8)
+    rc = lag == 8 ? launch(implicit_conv_f16_kernel<8, 8>)
+         : lag == 4 ? launch(implicit_conv_f16_kernel<8, 4>)
+         : lag == 2 ? launch(implicit_conv_f16_kernel<8, 2>)
+                    : launch(implicit_conv_f16_kernel<8, 1>);
+  else
+    rc = SCB_EINVAL;
+  if (rc == SCB_EINVAL) set_error("scb_conv_implicit: V must be 8 or 27");
+  if (rc != SCB_OK) return rc;
   SCB_LAUNCHED();
   return SCB_OK;
 }
