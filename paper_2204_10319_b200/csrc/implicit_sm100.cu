@@ -182,11 +182,15 @@ __global__ void __launch_bounds__(THREADS, 1)
               const int r = q / cpr, c = q - r * cpr;   // its row and 16-B chunk
               const int j = nrow[r];
               const int col = kk * p.kc + c * 8;
-              const bool ok = j >= 0 && col < p.c_in;
-              cp_async16(d + swz_off(r, c, p.swz),
-                         ok ? (const void*)(p.feat + (long long)j * p.ldf + col)
-                            : (const void*)p.feat,
-                         ok ? 16u : 0u);
+              const uint32_t sdst = d + swz_off(r, c, p.swz);
+              if (j >= 0 && col < p.c_in) {
+                cp_async16(sdst, p.feat + (long long)j * p.ldf + col, 16u);
+              } else {
+                // absent neighbour: zero the chunk with a plain shared store (a
+                // zero-size cp.async still sends a request — all to one line)
+                asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(sdst), "r"(0)
+                             : "memory");
+              }
             }
           }
           cp_async_commit();
