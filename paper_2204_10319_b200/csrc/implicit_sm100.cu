@@ -21,6 +21,8 @@
 //   warps 2-5  epilogue: tcgen05.ld -> epilogue -> swizzled smem -> TMA store
 #include <cuda.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "sm100_ptx.cuh"
 
@@ -40,6 +42,7 @@ struct Params {
   long long n_out;
   int n_in, c_in, c_out, V, n_pad, kc, n_kchunks, stages, swz, epi_cols, total_tiles, relu;
   int ops;                  // offsets per stage (small C_in -> several)
+  int debug;                // SCB_IMPLICIT_DEBUG: bit0 no A loads, bit1 no MMAs
   int groups;               // ceil(V / ops) offset groups per tile
   uint32_t idesc, tmem_cols;
   uint32_t a_off_bytes;     // one offset's A block [128 rows][kc] (1024-aligned)
@@ -183,7 +186,7 @@ __global__ void __launch_bounds__(THREADS, 1)
               const int j = nrow[r];
               const int col = kk * p.kc + c * 8;
               const uint32_t sdst = d + swz_off(r, c, p.swz);
-              if (j >= 0 && col < p.c_in) {
+              if (j >= 0 && col < p.c_in && !(p.debug & 1)) {
                 cp_async16(sdst, p.feat + (long long)j * p.ldf + col, 16u);
               } else {
                 // absent neighbour: zero the chunk with a plain shared store (a
@@ -236,6 +239,7 @@ __global__ void __launch_bounds__(THREADS, 1)
               if (n >= V) break;
               const bool valid = flags[stage * MAX_OPS + o] != 0u;
               if (!(valid || (!issued && n == V - 1))) continue;
+              if ((p.debug & 2) && issued) continue;
               const uint32_t ao = sa + o * p.a_off_bytes, bo = sb + o * p.b_off_bytes;
               for (int k = 0; k < p.kc / 16; ++k) {
                 mma_f16(d_tmem, make_sdesc(ao + k * 32, sbo, layout),
@@ -418,6 +422,7 @@ extern "C" int32_t scb_conv_implicit(const void* features, int64_t n_in, int32_t
   p.shift = shift;
   p.bias = bias;
   p.residual = (const __half*)residual;
+  if (const char* dbg = getenv("SCB_IMPLICIT_DEBUG")) p.debug = atoi(dbg);
   const int smem_cap = 227 * 1024;
   const int fixed = 1024 + EPI_BYTES + 2 * volume * BM * 4 + 16 * MAX_OPS * 4 + 40 * 8 + 64;
   int stages = (smem_cap - fixed) / (int)p.stage_bytes;
