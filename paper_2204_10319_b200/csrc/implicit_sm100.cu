@@ -21,6 +21,7 @@
 //   warps 2-5  epilogue: tcgen05.ld -> epilogue -> swizzled smem -> TMA store
 #include <cuda.h>
 
+#include <cstdio>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -64,12 +65,25 @@ __device__ __forceinline__ uint32_t swz_off(int row, int chunk, int swz) {
   return row * 32 + ((chunk ^ ((row >> 2) & 1)) << 4);
 }
 
+// SCB_IMPLICIT_DEBUG bit 16: per-role wait-cycle counters of CTA 0.
+__device__ unsigned long long g_ic_prof[16];
+#define IC_PROF(idx, cond, ...)                                                       \
+  do {                                                                                \
+    if ((p.debug & 16) && blockIdx.x == 0 && (cond)) {                                \
+      const long long t0_ = clock64();                                                \
+      __VA_ARGS__;                                                                    \
+      atomicAdd(&g_ic_prof[idx], (unsigned long long)(clock64() - t0_));              \
+    } else {                                                                          \
+      __VA_ARGS__;                                                                    \
+    }                                                                                 \
+  } while (0)
+
 __device__ __forceinline__ uint32_t pack_half2(float a, float b) {
   __half2 h = __floats2half2_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
-template <int V, int LAG>
+template <int V, int LAG, int KC>
 __global__ void __launch_bounds__(THREADS, 1)
     implicit_conv_f16_kernel(const __grid_constant__ CUtensorMap tmB,
                              const __grid_constant__ CUtensorMap tmOut,
@@ -85,6 +99,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
 
+  const long long k_t0 = clock64();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int t_begin = (int)((long long)p.total_tiles * blockIdx.x / gridDim.x);
   const int t_end = (int)((long long)p.total_tiles * (blockIdx.x + 1) / gridDim.x);
@@ -122,7 +137,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int g = 0; g < p.groups; ++g) {
           const int nv = min(p.ops, p.V - g * p.ops);
           for (int kk = 0; kk < p.n_kchunks; ++kk) {
-            mbar_wait(empty + stage, phase ^ 1);
+            IC_PROF(2, true, mbar_wait(empty + stage, phase ^ 1));
             mbar_expect_tx(full + stage, nv * p.b_tx);
             uint8_t* sb = smem + (size_t)stage * p.stage_bytes + p.a_stage_bytes;
             for (int o = 0; o < nv; ++o)
@@ -142,8 +157,20 @@ __global__ void __launch_bounds__(THREADS, 1)
     // feature rows (fully used sectors) and writes a contiguous swizzled span.
     const int row = threadIdx.x - 64;
     const int wbyte = warp - 2;
-    const int cpr = p.kc / 8;                 // 16-B chunks per row per K chunk
-    const int rows_per_pass = 128 / cpr;
+    constexpr int CPR = KC / 8;               // 16-B chunks per row per K chunk
+    constexpr int SWZ = KC * 2;               // swizzle span = row bytes
+    // this thread's fixed (row, chunk) slots of an offset block: chunk id
+    // q = pass*128 + row  ->  row q / CPR, chunk q % CPR (compile-time CPR)
+    int r_of[CPR];
+    uint32_t off_of[CPR], col_of[CPR];
+#pragma unroll
+    for (int pass = 0; pass < CPR; ++pass) {
+      const int q = pass * 128 + row;
+      const int r = q / CPR, c = q % CPR;
+      r_of[pass] = r;
+      col_of[pass] = c * 8;
+      off_of[pass] = swz_off(r, c, SWZ);
+    }
     int nxt[V];
     {
       const long long k = (long long)t_begin * BM + row;
@@ -153,8 +180,10 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     int stage = 0, sig = 0, pending = 0;
     uint32_t phase = 0;
+    const uint32_t nbr_base = smem_u32(nbr_s);
     for (int t = t_begin, buf = 0; t < t_end; ++t, buf ^= 1) {
       int* nb = nbr_s + buf * V * BM;
+      const uint32_t nb_s = nbr_base + (uint32_t)(buf * V * BM * 4);
       uint32_t anymask = 0;
 #pragma unroll
       for (int n = 0; n < V; ++n) {
@@ -171,35 +200,38 @@ __global__ void __launch_bounds__(THREADS, 1)
       for (int g = 0; g < p.groups; ++g) {
         const int nv = min(p.ops, V - g * p.ops);
         for (int kk = 0; kk < p.n_kchunks; ++kk) {
-          mbar_wait(empty + stage, phase ^ 1);
+          IC_PROF(0, row == 0, mbar_wait(empty + stage, phase ^ 1));
           if (lane == 0)
             for (int o = 0; o < nv; ++o)
               reinterpret_cast<uint8_t*>(flags + stage * MAX_OPS + o)[wbyte] =
                   (anymask >> (g * p.ops + o)) & 1u;
           const uint32_t dst = smem_u32(smem + (size_t)stage * p.stage_bytes);
+          const int col0 = kk * KC;
           for (int o = 0; o < nv; ++o) {
-            const int* nrow = nb + (g * p.ops + o) * BM;
+            const uint32_t nrow = nb_s + (uint32_t)((g * p.ops + o) * BM * 4);
             const uint32_t d = dst + o * p.a_off_bytes;
-            for (int pass = 0; pass < cpr; ++pass) {
-              const int q = pass * 128 + row;           // chunk id within the offset block
-              const int r = q / cpr, c = q - r * cpr;   // its row and 16-B chunk
-              const int j = nrow[r];
-              const int col = kk * p.kc + c * 8;
-              const uint32_t sdst = d + swz_off(r, c, p.swz);
-              if (j >= 0 && col < p.c_in && !(p.debug & 1)) {
-                cp_async16(sdst, p.feat + (long long)j * p.ldf + col, 16u);
-              } else {
+            int j[CPR];
+#pragma unroll
+            for (int pass = 0; pass < CPR; ++pass)
+              asm volatile("ld.shared.b32 %0, [%1];" : "=r"(j[pass]) : "r"(nrow + r_of[pass] * 4));
+#pragma unroll
+            for (int pass = 0; pass < CPR; ++pass) {
+              const int col = col0 + (int)col_of[pass];
+              if (j[pass] >= 0 && col < p.c_in && !(p.debug & 1)) {
+                cp_async16(d + off_of[pass], p.feat + (long long)j[pass] * p.ldf + col, 16u);
+              } else if (!(p.debug & 8)) {
                 // absent neighbour: zero the chunk with a plain shared store (a
                 // zero-size cp.async still sends a request — all to one line)
-                asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(sdst), "r"(0)
+                asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(d + off_of[pass]),
+                             "r"(0)
                              : "memory");
               }
             }
           }
           cp_async_commit();
           if (++pending > LAG) {
-            cp_async_wait<LAG>();
-            fence_async_smem();  // generic-proxy smem writes -> visible to tcgen05 (async proxy)
+            IC_PROF(1, row == 0, cp_async_wait<LAG>());
+            if (!(p.debug & 4)) fence_async_smem();  // generic-proxy smem writes -> async proxy
             mbar_arrive(full + sig);
             if (++sig == p.stages) sig = 0;
             --pending;
@@ -207,7 +239,6 @@ __global__ void __launch_bounds__(THREADS, 1)
           if (++stage == p.stages) { stage = 0; phase ^= 1; }
         }
       }
-      (void)rows_per_pass;
     }
     cp_async_wait<0>();
     fence_async_smem();
@@ -224,13 +255,13 @@ __global__ void __launch_bounds__(THREADS, 1)
       int stage = 0, acc = 0;
       uint32_t phase = 0, acc_phase = 0;
       for (int t = t_begin; t < t_end; ++t) {
-        mbar_wait(tempty + acc, acc_phase ^ 1);
+        IC_PROF(4, true, mbar_wait(tempty + acc, acc_phase ^ 1));
         tc_after();
         const uint32_t d_tmem = tmem_base + (uint32_t)(acc * p.n_pad);
         uint32_t issued = 0;
         for (int g = 0; g < p.groups; ++g) {
           for (int kk = 0; kk < p.n_kchunks; ++kk) {
-            mbar_wait(full + stage, phase);
+            IC_PROF(3, true, mbar_wait(full + stage, phase));
             tc_after();
             const uint32_t sa = smem_u32(smem + (size_t)stage * p.stage_bytes);
             const uint32_t sb = sa + p.a_stage_bytes;
@@ -266,7 +297,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int row0 = t * BM + 32 * q;
       const long long k = (long long)row0 + lane;
       const bool row_ok = k < p.n_out;
-      mbar_wait(tfull + acc, acc_phase);
+      IC_PROF(5, warp == 6 && lane == 0, mbar_wait(tfull + acc, acc_phase));
       tc_after();
       for (int j = 0; j < chunks; ++j) {
         const int c0 = j * p.epi_cols;
@@ -312,7 +343,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
         }
         uint8_t* buf = bufs + nbuf * EPI_BUF;
-        if (lane == 0) bulk_wait_read1();
+        if (lane == 0) IC_PROF(6, warp == 6, bulk_wait_read1());
         __syncwarp();
         if (ncol == 32) {
 #pragma unroll
@@ -351,6 +382,10 @@ __global__ void __launch_bounds__(THREADS, 1)
     tc_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
                  "r"(p.tmem_cols));
+  }
+  if ((p.debug & 16) && blockIdx.x == 0 && threadIdx.x == 0) {
+    atomicAdd(&g_ic_prof[7], (unsigned long long)(clock64() - k_t0));
+    atomicAdd(&g_ic_prof[9], (unsigned long long)(t_end - t_begin));
   }
 }
 
@@ -448,21 +483,31 @@ extern "C" int32_t scb_conv_implicit(const void* features, int64_t n_in, int32_t
     kernel<<<grid, THREADS, smem, s>>>(mB, mO, p);
     return SCB_OK;
   };
-  int rc;
-  if (volume == 27)
-    rc = lag == 8 ? launch(implicit_conv_f16_kernel<27, 8>)
-         : lag == 4 ? launch(implicit_conv_f16_kernel<27, 4>)
-         : lag == 2 ? launch(implicit_conv_f16_kernel<27, 2>)
-                    : launch(implicit_conv_f16_kernel<27, 1>);
-  else if (volume == 8)
-    rc = lag == 8 ? launch(implicit_conv_f16_kernel<8, 8>)
-         : lag == 4 ? launch(implicit_conv_f16_kernel<8, 4>)
-         : lag == 2 ? launch(implicit_conv_f16_kernel<8, 2>)
-                    : launch(implicit_conv_f16_kernel<8, 1>);
-  else
-    rc = SCB_EINVAL;
+  int rc = SCB_EINVAL;
+#define SCB_IC_LAUNCH(VV, KK)                                                               \
+  rc = lag == 8 ? launch(implicit_conv_f16_kernel<VV, 8, KK>)                             \
+       : lag == 4 ? launch(implicit_conv_f16_kernel<VV, 4, KK>)                           \
+       : lag == 2 ? launch(implicit_conv_f16_kernel<VV, 2, KK>)                           \
+                  : launch(implicit_conv_f16_kernel<VV, 1, KK>)
+  if (volume == 27) {
+    if (p.kc == 64) SCB_IC_LAUNCH(27, 64); else if (p.kc == 32) SCB_IC_LAUNCH(27, 32); else SCB_IC_LAUNCH(27, 16);
+  } else if (volume == 8) {
+    if (p.kc == 64) SCB_IC_LAUNCH(8, 64); else if (p.kc == 32) SCB_IC_LAUNCH(8, 32); else SCB_IC_LAUNCH(8, 16);
+  }
+#undef SCB_IC_LAUNCH
   if (rc == SCB_EINVAL) set_error("scb_conv_implicit: V must be 8 or 27");
   if (rc != SCB_OK) return rc;
+  if (p.debug & 16) {
+    unsigned long long prof[16];
+    cudaStreamSynchronize(s);
+    cudaMemcpyFromSymbol(prof, g_ic_prof, sizeof(prof));
+    fprintf(stderr, "[ic prof cta0] tiles=%llu total=%llu Aempty=%llu Await=%llu Bempty=%llu "
+            "MMAfull=%llu MMAtempty=%llu EPItfull=%llu EPIbulk=%llu Abar=%llu (stages=%d ops=%d)\n",
+            prof[9], prof[7], prof[0], prof[1], prof[2], prof[3], prof[4], prof[5], prof[6], prof[8],
+            p.stages, p.ops);
+    static const unsigned long long zero[16] = {0};
+    cudaMemcpyToSymbol(g_ic_prof, zero, sizeof(zero));
+  }
   SCB_LAUNCHED();
   return SCB_OK;
 }
