@@ -4,21 +4,19 @@
 //   out[k] = epilogue( sum_n  features[hits[n][k]] . W[n] )      (absent -> 0)
 //
 // for 128-row output tiles, accumulating all V offsets in TMEM.  The gather is
-// done by the TMA engine itself (cp.async.bulk.tensor ... tile::gather4: four
-// arbitrary feature rows per instruction, straight into the 128/64/32-B
-// swizzled UMMA operand layout; absent neighbours are out-of-bounds rows and
-// are zero-filled without a memory read), so neither the gather buffer nor
+// fused into the operand load: cp.async moves each present neighbour's 16-B
+// row chunks straight into the 128/64/32-B swizzled UMMA layout (absent
+// neighbours are zeroed with shared stores), so neither the gather buffer nor
 // the f32 partials ever reach HBM.  Each output row is written once (fp16)
 // with BN / bias / residual / ReLU applied in registers.  Offsets with no
-// neighbour anywhere in a tile skip their MMAs.
+// neighbour anywhere in a tile skip their MMAs.  (A TMA tile::gather4 variant
+// was measured ~2-3x slower on this path: ~100 cycles per 4-row request.)
 //
-// Warp roles (192 threads, 1 CTA / SM, persistent over contiguous tile ranges):
-//   warp 0     producer: per tile one 1-D TMA per offset brings the tile's
-//              neighbour rows (hits[n][tile]) into smem (double-buffered, one
-//              tile ahead); per stage each lane issues one gather4 per offset
-//              for its 4 rows, lane 0 the weight-slice TMA loads
+// Warp roles (320 threads, 1 CTA / SM, persistent over contiguous tile ranges):
+//   warp 0     TMA producer of the weight slices (B, K-major fp16)
 //   warp 1     TMEM allocator + single-thread tcgen05.mma issuer
-//   warps 2-5  epilogue: tcgen05.ld -> epilogue -> swizzled smem -> TMA store
+//   warps 2-5  A producers: neighbour indices one tile ahead, cp.async gather
+//   warps 6-9  epilogue: tcgen05.ld -> epilogue -> swizzled smem -> TMA store
 #include <cuda.h>
 
 #include <cstdio>
@@ -207,6 +205,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                   (anymask >> (g * p.ops + o)) & 1u;
           const uint32_t dst = smem_u32(smem + (size_t)stage * p.stage_bytes);
           const int col0 = kk * KC;
+          const long long tl0 = ((p.debug & 16) && blockIdx.x == 0 && row == 0) ? clock64() : 0;
           for (int o = 0; o < nv; ++o) {
             const uint32_t nrow = nb_s + (uint32_t)((g * p.ops + o) * BM * 4);
             const uint32_t d = dst + o * p.a_off_bytes;
@@ -217,22 +216,25 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
             for (int pass = 0; pass < CPR; ++pass) {
               const int col = col0 + (int)col_of[pass];
-              if (j[pass] >= 0 && col < p.c_in && !(p.debug & 1)) {
-                cp_async16(d + off_of[pass], p.feat + (long long)j[pass] * p.ldf + col, 16u);
-              } else if (!(p.debug & 8)) {
-                // absent neighbour: zero the chunk with a plain shared store (a
-                // zero-size cp.async still sends a request — all to one line)
-                asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(d + off_of[pass]),
-                             "r"(0)
-                             : "memory");
-              }
+              const uint32_t ok = (j[pass] >= 0 && col < p.c_in && !(p.debug & 1)) ? 1u : 0u;
+              // branch-free: present neighbour -> cp.async of its 16-B chunk;
+              // absent -> zero the chunk with a shared store (a zero-size
+              // cp.async would still send a request, all to one line)
+              asm volatile(
+                  "{\n.reg .pred p;\nsetp.ne.b32 p, %2, 0;\n"
+                  "@p cp.async.cg.shared.global [%0], [%1], 16;\n"
+                  "@!p st.shared.v4.u32 [%0], {%3, %3, %3, %3};\n}\n" ::"r"(d + off_of[pass]),
+                  "l"(p.feat + (long long)(ok ? j[pass] : 0) * p.ldf + col), "r"(ok), "r"(0)
+                  : "memory");
             }
           }
+          if ((p.debug & 16) && blockIdx.x == 0 && row == 0)
+            atomicAdd(&g_ic_prof[10], (unsigned long long)(clock64() - tl0));
           cp_async_commit();
           if (++pending > LAG) {
             IC_PROF(1, row == 0, cp_async_wait<LAG>());
-            if (!(p.debug & 4)) fence_async_smem();  // generic-proxy smem writes -> async proxy
-            mbar_arrive(full + sig);
+            if (!(p.debug & 4)) IC_PROF(11, row == 0, fence_async_smem());  // generic -> async proxy
+            IC_PROF(12, row == 0, mbar_arrive(full + sig));
             if (++sig == p.stages) sig = 0;
             --pending;
           }
@@ -502,9 +504,10 @@ extern "C" int32_t scb_conv_implicit(const void* features, int64_t n_in, int32_t
     cudaStreamSynchronize(s);
     cudaMemcpyFromSymbol(prof, g_ic_prof, sizeof(prof));
     fprintf(stderr, "[ic prof cta0] tiles=%llu total=%llu Aempty=%llu Await=%llu Bempty=%llu "
-            "MMAfull=%llu MMAtempty=%llu EPItfull=%llu EPIbulk=%llu Abar=%llu (stages=%d ops=%d)\n",
-            prof[9], prof[7], prof[0], prof[1], prof[2], prof[3], prof[4], prof[5], prof[6], prof[8],
-            p.stages, p.ops);
+            "MMAfull=%llu MMAtempty=%llu EPItfull=%llu EPIbulk=%llu Aloop=%llu Afence=%llu Aarrive=%llu "
+            "(stages=%d ops=%d)\n",
+            prof[9], prof[7], prof[0], prof[1], prof[2], prof[3], prof[4], prof[5], prof[6], prof[10],
+            prof[11], prof[12], p.stages, p.ops);
     static const unsigned long long zero[16] = {0};
     cudaMemcpyToSymbol(g_ic_prof, zero, sizeof(zero));
   }

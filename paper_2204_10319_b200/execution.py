@@ -436,13 +436,12 @@ def choose_dataflow(opts: ExecOptions, dtype, kmap: KernelMap, w: WeightTensor) 
         return "staged"
     if opts.dataflow == "fused":
         return "fused"
-    n, v = kmap.n_out, kmap.offsets.volume
-    ci, co = w.c_in, w.c_out
-    m_est = n * (v if v == 8 else 7.5)  # |M|/N of LiDAR maps; 8 -> upper bound
-    t_staged = (m_est * (4 * ci + 8 * co + 8) + 2 * n * (ci + co)) / 4.5e12 + 25e-6
-    t_fused = max(v * n * ci * co * 2 / 1.1e15, m_est * ci * 2 / 9e12,
-                  2 * n * (ci + co) / 5e12) + 8e-6
-    return "fused" if t_fused <= t_staged else "staged"
+    # Measured on B200 (tools/fused_probe.py, 1M-voxel level-0 layer, k3):
+    # fused/staged = 0.56/1.0 ms at C=32, 1.74/2.68 at C=96 -> fused; 1.48/1.19
+    # at C=64, 2.6/2.1 at 128->96, 7.8/7.3 at 256 -> staged.  The fused
+    # producer is instruction-bound per 16-B chunk (absent rows included), so
+    # it wins where rows are short.
+    return "fused" if w.c_in <= 32 or (w.c_in % 64 != 0 and w.c_in <= 96) else "staged"
 
 
 def _run_fused(features: torch.Tensor, kmap: KernelMap, w: WeightTensor, opts: ExecOptions,
