@@ -34,9 +34,6 @@ import numpy as np
 
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
-# per-layer buffers change size every layer: let the caching allocator grow
-# segments instead of cudaFree/cudaMalloc churn inside the timed steps
-os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "expandable_segments:True")
 
 METRIC = "MinkUNet scans/sec (SemanticKITTI shape)"
 UNIT = "scans/s"

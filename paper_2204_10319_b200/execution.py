@@ -195,9 +195,35 @@ def _ld(t: torch.Tensor | None) -> int:
     return t.stride(0) if t.shape[0] > 1 else t.shape[1]
 
 
+class _Arena:
+    """Per-(device, stream) scratch slots for the per-layer gather buffer and
+    f32 partials.  Layers run in stream order, so one slot serves every layer
+    of a forward pass; slots only grow (by >= 25%), which keeps multi-GB
+    cudaMalloc/cudaFree churn out of the forward."""
+
+    def __init__(self):
+        self.slots = {}
+
+    def tensor(self, name: str, shape, dtype, device) -> torch.Tensor:
+        n = 1
+        for s in shape:
+            n *= int(s)
+        nbytes = n * torch.empty((), dtype=dtype).element_size()
+        key = (str(device), torch.cuda.current_stream(device).cuda_stream, name)
+        raw = self.slots.get(key)
+        if raw is None or raw.numel() < nbytes:
+            grow = 0 if raw is None else raw.numel() + raw.numel() // 4
+            raw = torch.empty(max(nbytes, grow, 256), dtype=torch.uint8, device=device)
+            self.slots[key] = raw
+        return raw[:nbytes].view(dtype).view(tuple(int(s) for s in shape))
+
+
+_ARENA = _Arena()
+
+
 def _gather_padded(features: torch.Tensor, plan: GatherScatterPlan, c: int) -> torch.Tensor:
     ld = _buffer_ld(features.dtype, c)
-    buf = torch.empty((max(plan.rows_pad, 1), ld), dtype=features.dtype, device=features.device)
+    buf = _ARENA.tensor("gather", (max(plan.rows_pad, 1), ld), features.dtype, features.device)
     nat.call("scb_gather", nat.dtype_code(features.dtype), nat.ptr(features), features.shape[0], c,
              _ld(features), nat.ptr(plan.buf_in), plan.rows_pad, nat.ptr(buf), ld,
              nat.stream_handle())
@@ -362,7 +388,7 @@ def _weights_for(w: WeightTensor, dtype):
 
 def _grouped_gemm(dtype, buffer, rows_pad, features, w: WeightTensor, segs, nseg, c_rows):
     wt, ldc = _weights_for(w, dtype)
-    partial = torch.empty((max(c_rows, 1), ldc), dtype=torch.float32, device=wt.device)
+    partial = _ARENA.tensor("partial", (max(c_rows, 1), ldc), torch.float32, wt.device)
     nat.call("scb_grouped_gemm", nat.dtype_code(dtype), nat.ptr(buffer), max(rows_pad, 1),
              _ld(buffer), nat.ptr(features), 0 if features is None else features.shape[0],
              0 if features is None else _ld(features), w.c_in, nat.ptr(wt), w.weights.shape[0],
