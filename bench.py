@@ -23,6 +23,7 @@ FP16 feature storage, B = 8 scans per GPU per step (64 scans at N = 8).
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import subprocess
@@ -287,14 +288,20 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     launches0 = nat.load().scb_launch_count()
+    host_ms = []
+    gc.collect()
+    gc.disable()  # no collector pauses inside the timed steps
     for i in range(args.steps):
         flush.fill_(i & 0xFF)  # L2 flush, outside the step's events
         evs[i][0].record()
+        h0 = time.perf_counter()
         out = step(timer, traffic)
+        host_ms.append(1e3 * (time.perf_counter() - h0))
         evs[i][1].record()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    gc.enable()
     launches = nat.load().scb_launch_count() - launches0
     clk = clocks.stop(local)
     step_ms = [a.elapsed_time(b) for a, b in evs]
@@ -371,11 +378,14 @@ def main():
         if world > 1:
             dist.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        gc.collect()
+        gc.disable()
         e0.record()
         for _ in range(args.steps):
             e2e_step()
         e1.record()
         torch.cuda.synchronize()
+        gc.enable()
         es = torch.tensor(e0.elapsed_time(e1) / 1e3, device=dev, dtype=torch.float64)
         if world > 1:
             dist.all_reduce(es, op=dist.ReduceOp.MAX)
@@ -413,7 +423,7 @@ def main():
             "data": "synthetic (raycast LiDAR scans, random-init weights)",
             "config": dict(workload_config(args, world), voxels_per_gpu=n_vox),
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
-            "clocks": clk, "step_ms": step_ms,
+            "clocks": clk, "step_ms": step_ms, "host_issue_ms": host_ms,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
