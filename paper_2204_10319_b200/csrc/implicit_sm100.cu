@@ -41,7 +41,7 @@ struct Params {
   long long n_out;
   int n_in, c_in, c_out, V, n_pad, kc, n_kchunks, stages, swz, epi_cols, total_tiles, relu;
   int ops;                  // offsets per stage (small C_in -> several)
-  int debug;                // SCB_IMPLICIT_DEBUG: bit0 no A loads, bit1 no MMAs
+  int debug;                // SCB_IMPLICIT_DEBUG: 1 no A loads, 2 no MMAs, 16 wait counters
   int groups;               // ceil(V / ops) offset groups per tile
   uint32_t idesc, tmem_cols;
   uint32_t a_off_bytes;     // one offset's A block [128 rows][kc] (1024-aligned)
@@ -149,26 +149,15 @@ __global__ void __launch_bounds__(THREADS, 1)
     // ============ A producers (128 threads).  Thread r owns output row r of
     // the tile for index bookkeeping: it prefetches that row's V neighbour
     // rows one tile ahead (registers), parks them in the shared table and
-    // computes the per-offset "any neighbour" flags.  The copies themselves
-    // are spread along rows: consecutive lanes move consecutive 16-B chunks
-    // of consecutive rows, so every warp-wide cp.async reads whole 64/128-B
-    // feature rows (fully used sectors) and writes a contiguous swizzled span.
+    // computes the per-offset "any neighbour" flags, then copies its own row
+    // of every offset block: one index read and one 64-bit address per row,
+    // CPR predicated 16-B cp.async (present) or zero stores (absent) with
+    // immediate chunk offsets.  (Spreading a row's chunks over consecutive
+    // lanes coalesces better but costs ~4x the instructions; measured slower.)
     const int row = threadIdx.x - 64;
     const int wbyte = warp - 2;
     constexpr int CPR = KC / 8;               // 16-B chunks per row per K chunk
     constexpr int SWZ = KC * 2;               // swizzle span = row bytes
-    // this thread's fixed (row, chunk) slots of an offset block: chunk id
-    // q = pass*128 + row  ->  row q / CPR, chunk q % CPR (compile-time CPR)
-    int r_of[CPR];
-    uint32_t off_of[CPR], col_of[CPR];
-#pragma unroll
-    for (int pass = 0; pass < CPR; ++pass) {
-      const int q = pass * 128 + row;
-      const int r = q / CPR, c = q % CPR;
-      r_of[pass] = r;
-      col_of[pass] = c * 8;
-      off_of[pass] = swz_off(r, c, SWZ);
-    }
     int nxt[V];
     {
       const long long k = (long long)t_begin * BM + row;
@@ -180,6 +169,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint32_t phase = 0;
     const uint32_t nbr_base = smem_u32(nbr_s);
     for (int t = t_begin, buf = 0; t < t_end; ++t, buf ^= 1) {
+      const long long tp0 = ((p.debug & 16) && blockIdx.x == 0 && row == 0) ? clock64() : 0;
       int* nb = nbr_s + buf * V * BM;
       const uint32_t nb_s = nbr_base + (uint32_t)(buf * V * BM * 4);
       uint32_t anymask = 0;
@@ -188,13 +178,18 @@ __global__ void __launch_bounds__(THREADS, 1)
         nb[n * BM + row] = nxt[n];
         if (__any_sync(0xffffffffu, nxt[n] >= 0)) anymask |= 1u << n;
       }
+      const long long tb0 = ((p.debug & 16) && blockIdx.x == 0 && row == 0) ? clock64() : 0;
       asm volatile("bar.sync 1, 128;" ::: "memory");  // the tile's index table is complete
+      if ((p.debug & 16) && blockIdx.x == 0 && row == 0)
+        atomicAdd(&g_ic_prof[14], (unsigned long long)(clock64() - tb0));
       {
         const long long k = (long long)(t + 1) * BM + row;
         const bool ok = (t + 1 < t_end) && k < p.n_out;
 #pragma unroll
         for (int n = 0; n < V; ++n) nxt[n] = ok ? __ldg(p.hits + (long long)n * p.ldh + k) : -1;
       }
+      if ((p.debug & 16) && blockIdx.x == 0 && row == 0)
+        atomicAdd(&g_ic_prof[13], (unsigned long long)(clock64() - tp0));
       for (int g = 0; g < p.groups; ++g) {
         const int nv = min(p.ops, V - g * p.ops);
         for (int kk = 0; kk < p.n_kchunks; ++kk) {
@@ -206,25 +201,27 @@ __global__ void __launch_bounds__(THREADS, 1)
           const uint32_t dst = smem_u32(smem + (size_t)stage * p.stage_bytes);
           const int col0 = kk * KC;
           const long long tl0 = ((p.debug & 16) && blockIdx.x == 0 && row == 0) ? clock64() : 0;
+          // thread = row: one index read and one 64-bit address per row,
+          // then CPR predicated 16-B copies (or zero stores) with immediate
+          // chunk offsets
+          const int rx = SWZ == 128 ? (row & 7) : (SWZ == 64 ? ((row >> 1) & 3) : ((row >> 2) & 1));
+          const int live = min(CPR, (p.c_in - col0) / 8);  // chunks inside C_in
           for (int o = 0; o < nv; ++o) {
-            const uint32_t nrow = nb_s + (uint32_t)((g * p.ops + o) * BM * 4);
-            const uint32_t d = dst + o * p.a_off_bytes;
-            int j[CPR];
+            int j;
+            asm volatile("ld.shared.b32 %0, [%1];"
+                         : "=r"(j)
+                         : "r"(nb_s + (uint32_t)(((g * p.ops + o) * BM + row) * 4)));
+            const uint32_t base = dst + o * p.a_off_bytes + row * (KC * 2);
+            const __half* src = p.feat + (long long)(j >= 0 ? j : 0) * p.ldf + col0;
 #pragma unroll
-            for (int pass = 0; pass < CPR; ++pass)
-              asm volatile("ld.shared.b32 %0, [%1];" : "=r"(j[pass]) : "r"(nrow + r_of[pass] * 4));
-#pragma unroll
-            for (int pass = 0; pass < CPR; ++pass) {
-              const int col = col0 + (int)col_of[pass];
-              const uint32_t ok = (j[pass] >= 0 && col < p.c_in && !(p.debug & 1)) ? 1u : 0u;
-              // branch-free: present neighbour -> cp.async of its 16-B chunk;
-              // absent -> zero the chunk with a shared store (a zero-size
-              // cp.async would still send a request, all to one line)
+            for (int c = 0; c < CPR; ++c) {
+              const uint32_t ok = (j >= 0 && c < live) ? 1u : 0u;
               asm volatile(
                   "{\n.reg .pred p;\nsetp.ne.b32 p, %2, 0;\n"
                   "@p cp.async.cg.shared.global [%0], [%1], 16;\n"
-                  "@!p st.shared.v4.u32 [%0], {%3, %3, %3, %3};\n}\n" ::"r"(d + off_of[pass]),
-                  "l"(p.feat + (long long)(ok ? j[pass] : 0) * p.ldf + col), "r"(ok), "r"(0)
+                  "@!p st.shared.v4.u32 [%0], {%3, %3, %3, %3};\n}\n" ::"r"(
+                      base + ((uint32_t)(c ^ rx) << 4)),
+                  "l"(src + c * 8), "r"(ok), "r"(0)
                   : "memory");
             }
           }
@@ -505,9 +502,9 @@ extern "C" int32_t scb_conv_implicit(const void* features, int64_t n_in, int32_t
     cudaMemcpyFromSymbol(prof, g_ic_prof, sizeof(prof));
     fprintf(stderr, "[ic prof cta0] tiles=%llu total=%llu Aempty=%llu Await=%llu Bempty=%llu "
             "MMAfull=%llu MMAtempty=%llu EPItfull=%llu EPIbulk=%llu Aloop=%llu Afence=%llu Aarrive=%llu "
-            "(stages=%d ops=%d)\n",
+            "prologue=%llu bar=%llu (stages=%d ops=%d)\n",
             prof[9], prof[7], prof[0], prof[1], prof[2], prof[3], prof[4], prof[5], prof[6], prof[10],
-            prof[11], prof[12], p.stages, p.ops);
+            prof[11], prof[12], prof[13], prof[14], p.stages, p.ops);
     static const unsigned long long zero[16] = {0};
     cudaMemcpyToSymbol(g_ic_prof, zero, sizeof(zero));
   }
