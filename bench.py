@@ -53,6 +53,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--dataflow", choices=("staged", "fused", "auto"), default="auto")
+    ap.add_argument("--clock-ms", type=int, default=100, help="nvidia-smi sampling period (0: off)")
     return ap.parse_args()
 
 
@@ -201,14 +202,14 @@ class Clocks:
         self.path = path
         self.proc = None
 
-    def start(self):
+    def start(self, period_ms=100):
         try:
             self.fh = open(self.path, "w")
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "--query-gpu=index,clocks.sm,clocks.max.sm,power.draw,"
                  "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
                  "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "100"],
+                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", str(period_ms)],
                 stdout=self.fh, stderr=subprocess.DEVNULL)
         except (OSError, FileNotFoundError):
             self.proc = None
@@ -283,7 +284,8 @@ def main():
                     if (ROOT / "gpurun_out").exists() else f"/tmp/clocks_rank{rank}.csv")
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(args.steps)]
-    clocks.start()
+    if args.clock_ms > 0:
+        clocks.start(args.clock_ms)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -303,7 +305,7 @@ def main():
         dist.barrier()
     gc.enable()
     launches = nat.load().scb_launch_count() - launches0
-    clk = clocks.stop(local)
+    clk = clocks.stop(local) if args.clock_ms > 0 else {"sm_mhz": None, "reasons": ["not sampled"]}
     step_ms = [a.elapsed_time(b) for a, b in evs]
     total_s = torch.tensor(sum(step_ms) / 1e3, device=dev, dtype=torch.float64)
     if world > 1:
