@@ -290,6 +290,7 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     launches0 = nat.load().scb_launch_count()
+    seg0 = torch.cuda.memory_stats(dev).get("segment.all.allocated", 0)
     host_ms = []
     gc.collect()
     gc.disable()  # no collector pauses inside the timed steps
@@ -304,6 +305,7 @@ def main():
     if world > 1:
         dist.barrier()
     gc.enable()
+    seg_allocs = torch.cuda.memory_stats(dev).get("segment.all.allocated", 0) - seg0
     launches = nat.load().scb_launch_count() - launches0
     clk = clocks.stop(local) if args.clock_ms > 0 else {"sm_mhz": None, "reasons": ["not sampled"]}
     step_ms = [a.elapsed_time(b) for a, b in evs]
@@ -426,6 +428,7 @@ def main():
             "config": dict(workload_config(args, world), voxels_per_gpu=n_vox),
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clk, "step_ms": step_ms, "host_issue_ms": host_ms,
+            "cuda_mallocs_in_timed_steps": seg_allocs,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
