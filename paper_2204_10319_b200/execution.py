@@ -596,7 +596,7 @@ def _record_traffic(opts, plan, c_in, c_out, dtype, n_in, n_out, n_center, m_tot
     excluded.  |M'| = plan.total (buffer rows), centre rows read in place."""
     e = 2 if dtype == torch.float16 else 4
     m = plan.total
-    v = plan.kmap.offsets.volume
+    v = plan.volume
     opts.traffic_log.append((opts.layer_label, {
         "gather_bytes": e * n_in * c_in + e * m * c_in + 4 * m,
         "gemm_bytes": e * m * c_in + 4 * m * c_out + e * n_center * c_in
@@ -652,10 +652,13 @@ def sparse_conv_forward(t: SparseTensor, w: WeightTensor, spec: LayerSpec,
                 out_cset = CoordinateSet(oc, out_boundary, t.batch_size)
             index = build_index(cset, kind, cell_cap=opts.grid_cell_cap)
             kmap = map_search(index, out_cset.coords, offsets, spec.stride)
-            hit = (out_cset, kmap)
+            # stride 1: the output set IS this set; store None, not a
+            # self-reference (a cycle would pin the maps until the cyclic GC)
+            hit = (None if out_cset is cset else out_cset, kmap)
             if opts.map_reuse:
                 cset.maps[key] = hit
         out_cset, kmap = hit
+        out_cset = cset if out_cset is None else out_cset
         if map_cache is not None and spec.reuse_key:
             map_cache[spec.reuse_key] = CachedMap(kmap, t.coords, t.boundary, t.stride, cset)
     schedule, symmetric = schedule_for(offsets, spec.stride)

@@ -11,6 +11,7 @@ entries are sorted by output row ``k`` (mapping.py:289-319).
 
 from __future__ import annotations
 
+import weakref
 from dataclasses import dataclass
 from itertools import product
 
@@ -376,7 +377,10 @@ class GatherScatterPlan:
             skipped = kmap.offsets.center
             if skipped is None or kmap.stride != 1:
                 raise ValueError("skip_center requires a stride-1 odd-K map")
-        self.kmap = kmap
+        # weak: the map caches its plans, a strong back-reference would form a
+        # cycle that only the cyclic GC frees (multi-100-MB device buffers)
+        self._kmap = weakref.ref(kmap)
+        self.volume = kmap.offsets.volume
         self.n_in, self.n_out = kmap.n_in, kmap.n_out
         self.skipped_offset = skipped
         self.tile_rows = int(tile_rows)
@@ -407,6 +411,13 @@ class GatherScatterPlan:
     @property
     def sizes(self) -> np.ndarray:
         return self._sizes.copy()
+
+    @property
+    def kmap(self) -> KernelMap:
+        k = self._kmap()
+        if k is None:
+            raise RuntimeError("the kernel map of this plan has been released")
+        return k
 
     # ---- reference CSR views (host numpy, computed on demand) -------------
     def _views(self):
