@@ -159,13 +159,31 @@ int32_t scb_plan_build(const int64_t* offset_ptr, const int32_t* in_idx, const i
                        int32_t tile_rows, int32_t* buf_in, int64_t rows_pad, int32_t* pos,
                        int32_t* status, scb_stream_t stream);
 
+/* Sync-free plan: the same layout built straight from a hit matrix on the
+ * device (count + scan + placement), so the staged layer never reads map
+ * sizes on the host.  Also writes the layer's GEMM problem table (`table`,
+ * scb_segtable_bytes(); consumed by scb_grouped_gemm_table) with an optional
+ * centre segment (a_src = 1, rows = center_rows, weight center_seg) placed at
+ * partial rows [0, c_base); offset slabs go to partial rows slab + c_base.
+ * `gemm_bm`/`gemm_ntn` are the GEMM's tile height and column tiles.
+ * buf_in needs scb_plan_rows_cap() entries, workspace scb_map_workspace(). */
+int64_t scb_plan_rows_cap(int32_t volume, int64_t n_out, int32_t tile_rows);
+int64_t scb_segtable_bytes(void);
+int32_t scb_plan_from_hits(const int32_t* hits, int32_t volume, int64_t n_out,
+                           int32_t skip_offset, int32_t tile_rows, int64_t c_base,
+                           int32_t gemm_bm, int32_t gemm_ntn, int32_t center_seg,
+                           int64_t center_rows, void* workspace, int64_t* offset_ptr,
+                           int32_t* buf_in, int32_t* pos, void* table, scb_stream_t stream);
+
 /* ---------------------------------------------------------------- movement
  * gather (execution.py:159-180, kernels.py:28-35): buffer[r] =
  * features[buf_in[r]] (zero row when buf_in[r] < 0), 128-bit vector copies,
- * bit-exact.  `ld_*` are row strides in elements. */
+ * bit-exact.  `ld_*` are row strides in elements.  With `rows_dev`
+ * (nullable, device int64 — a device-built SegTable's rows_pad) only
+ * min(rows, *rows_dev) rows are moved; `rows` is then the capacity. */
 int32_t scb_gather(int32_t dtype, const void* features, int64_t n_in, int32_t channels,
                    int64_t ld_feat, const int32_t* buf_in, int64_t rows, void* buffer,
-                   int64_t ld_buf, scb_stream_t stream);
+                   int64_t ld_buf, const int64_t* rows_dev, scb_stream_t stream);
 /* scatter_accumulate, output-stationary (execution.py:183-218,
  * kernels.py:38-50) fused with the centre-offset add (execution.py:423-428)
  * and an optional pointwise epilogue (execution.py:554-576):
@@ -213,6 +231,17 @@ int32_t scb_grouped_gemm(int32_t dtype, const void* a_buffer, int64_t a_rows, in
                          const void* weights, int32_t volume, int32_t c_out, float* partial,
                          int64_t c_rows, int64_t ldc, const scb_segment_t* segments,
                          int32_t n_segments, scb_stream_t stream);
+/* Same GEMM driven by a device-built problem table (scb_plan_from_hits):
+ * a_rows / c_rows are capacities, the kernel reads the segments and tile
+ * count from `table`, one persistent CTA per SM.  No host sync anywhere. */
+int32_t scb_grouped_gemm_table(int32_t dtype, const void* a_buffer, int64_t a_rows, int64_t lda,
+                               const void* a_features, int64_t f_rows, int64_t ldf, int32_t c_in,
+                               const void* weights, int32_t volume, int32_t c_out, float* partial,
+                               int64_t c_rows, int64_t ldc, const void* table,
+                               scb_stream_t stream);
+/* Tile height and column-tile count the GEMM of `dtype` uses (for
+ * scb_plan_from_hits' gemm_bm / gemm_ntn). */
+int32_t scb_gemm_tile_geometry(int32_t dtype, int32_t c_out, int32_t* bm, int32_t* ntn);
 
 /* ---------------------------------------------------------------- fused dataflow
  * gather -> GEMM -> scatter of one layer (the whole of _run_dataflow,

@@ -175,10 +175,14 @@ class SparseTensor:
 
     # -- host views (tests, I/O) ------------------------------------------
     def coords_numpy(self) -> np.ndarray:
-        return self.coords.cpu().numpy().astype(np.int64)
+        out = self.coords.cpu().numpy().astype(np.int64)
+        flush_saturation_warnings(block=True)
+        return out
 
     def features_numpy(self) -> np.ndarray:
-        return self.features.cpu().numpy()
+        out = self.features.cpu().numpy()
+        flush_saturation_warnings(block=True)
+        return out
 
     @property
     def coordset(self) -> CoordinateSet:
@@ -264,7 +268,31 @@ def quantize_features(t: SparseTensor, mode: PrecisionMode) -> SparseTensor:
     sat = torch.zeros(1, dtype=torch.int64, device=src.device)
     nat.call("scb_quantize_f16", nat.ptr(src), nat.ptr(out), src.numel(), nat.ptr(sat),
              nat.stream_handle())
-    n_sat = int(sat.item())
-    if n_sat:
-        warnings.warn(f"{n_sat} feature element(s) saturated to the fp16 range")
+    # The saturation count comes back asynchronously (pinned copy + event) so
+    # quantising a network input does not stall the stream; the warning is
+    # raised as soon as the count is known (next engine call, or any host read).
+    host = torch.empty(1, dtype=torch.int64, pin_memory=True)
+    host.copy_(sat, non_blocking=True)
+    ev = torch.cuda.Event()
+    ev.record()
+    _PENDING_SATURATION.append((ev, host))
     return t.replace_features(out)
+
+
+_PENDING_SATURATION: list = []
+
+
+def flush_saturation_warnings(block: bool = False) -> None:
+    """Emit the fp16 saturation warnings of finished quantisations
+    (reference core.py:232-237)."""
+    keep = []
+    for ev, host in _PENDING_SATURATION:
+        if block:
+            ev.synchronize()
+        if block or ev.query():
+            n_sat = int(host.item())
+            if n_sat:
+                warnings.warn(f"{n_sat} feature element(s) saturated to the fp16 range")
+        else:
+            keep.append((ev, host))
+    _PENDING_SATURATION[:] = keep

@@ -132,6 +132,21 @@ inline int ceil_div_i(long long a, long long b) { return (int)((a + b - 1) / b);
 // starts 16-byte aligned (1-D TMA loads of a tile's neighbour rows need it).
 __host__ __device__ __forceinline__ long long hits_ld(long long n) { return (n + 3) & ~3LL; }
 
+// GEMM problem table of one layer (segments = scheduled offsets + centre).
+// Built on the host (scb_grouped_gemm) or on the device straight from a hit
+// matrix (scb_plan_from_hits), in which case the GEMM reads it from global
+// memory and no map size ever crosses to the host.
+struct SegDesc {
+  long long a_row, c_row;
+  int rows, b_index, a_src, _pad;
+};
+struct SegTable {
+  int n_segs, total_tiles;
+  long long rows_pad;  // gather-buffer rows in use (device-built tables)
+  int tile_start[SCB_MAX_SEGMENTS + 1];
+  SegDesc seg[SCB_MAX_SEGMENTS];
+};
+
 // Dispatch on the spatial rank.
 #define SCB_DISPATCH_DIM(dim, ...)          \
   switch (dim) {                            \

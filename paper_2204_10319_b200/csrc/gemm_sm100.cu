@@ -28,27 +28,22 @@ constexpr int MAX_SEG = SCB_MAX_SEGMENTS;
 constexpr int EPI_BUF_BYTES = 4096;  // 32 rows x 128 B
 constexpr int EPI_BYTES = 4 * 2 * EPI_BUF_BYTES;
 
-struct Seg {
-  long long a_row, c_row;
-  int rows, b_index, a_src, _pad;
-};
+using Seg = SegDesc;
 
 struct Params {
-  int n_segs, total_tiles;
   int n_pad, kc, n_kchunks, epi_cols, stages, swz;
   uint32_t idesc, tmem_cols, a_stage_bytes, b_stage_bytes, stage_bytes, tx_bytes;
-  int tile_start[MAX_SEG + 1];
-  Seg seg[MAX_SEG];
+  const SegTable* dtab;  // device-built problem table (scb_plan_from_hits), else null
+  SegTable tab;          // host-built table (by value in parameter space)
 };
 
 using namespace ::scb::ptx;
 
-
-__device__ __forceinline__ int find_seg(const Params& p, int t) {
-  int lo = 0, hi = p.n_segs;  // largest s with tile_start[s] <= t
+__device__ __forceinline__ int find_seg(const SegTable& T, int t) {
+  int lo = 0, hi = T.n_segs;  // largest s with tile_start[s] <= t
   while (hi - lo > 1) {
     const int mid = (lo + hi) >> 1;
-    if (p.tile_start[mid] <= t) lo = mid; else hi = mid;
+    if (T.tile_start[mid] <= t) lo = mid; else hi = mid;
   }
   return lo;
 }
@@ -70,9 +65,10 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const SegTable& T = p.dtab ? *p.dtab : p.tab;
   // contiguous tile range per CTA: consecutive tiles share an offset's weights
-  const int t_begin = (int)((long long)p.total_tiles * blockIdx.x / gridDim.x);
-  const int t_end = (int)((long long)p.total_tiles * (blockIdx.x + 1) / gridDim.x);
+  const int t_begin = (int)((long long)T.total_tiles * blockIdx.x / gridDim.x);
+  const int t_end = (int)((long long)T.total_tiles * (blockIdx.x + 1) / gridDim.x);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < p.stages; ++s) {
@@ -106,9 +102,9 @@ __global__ void __launch_bounds__(THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int t = t_begin; t < t_end; ++t) {
-        const int s = find_seg(p, t);
-        const Seg& sg = p.seg[s];
-        const int a_row = (int)(sg.a_row + (long long)(t - p.tile_start[s]) * BM);
+        const int s = find_seg(T, t);
+        const Seg& sg = T.seg[s];
+        const int a_row = (int)(sg.a_row + (long long)(t - T.tile_start[s]) * BM);
         const int b_row = sg.b_index * p.n_pad;
         const CUtensorMap* ma = sg.a_src ? &tmA1 : &tmA0;
         for (int kk = 0; kk < p.n_kchunks; ++kk) {
@@ -159,9 +155,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint32_t acc_phase = 0;
     const int chunks = p.n_pad / p.epi_cols;
     for (int t = t_begin; t < t_end; ++t) {
-      const int s = find_seg(p, t);
-      const Seg& sg = p.seg[s];
-      const int c_row = (int)(sg.c_row + (long long)(t - p.tile_start[s]) * BM) + 32 * q;
+      const int s = find_seg(T, t);
+      const Seg& sg = T.seg[s];
+      const int c_row = (int)(sg.c_row + (long long)(t - T.tile_start[s]) * BM) + 32 * q;
       mbar_wait(tfull + acc, acc_phase);
       tc_after();
       for (int j = 0; j < chunks; ++j) {
@@ -220,14 +216,11 @@ namespace simt {
 constexpr int BM = 64, BN = 64, BK = 16;
 constexpr int MAX_SEG = SCB_MAX_SEGMENTS;
 
-struct Seg {
-  long long a_row, c_row;
-  int rows, b_index, a_src, mtiles;
-};
+using Seg = SegDesc;
 struct Params {
-  int n_segs, total_tiles, ntn;
-  int tile_start[MAX_SEG + 1];
-  Seg seg[MAX_SEG];
+  int ntn;
+  const SegTable* dtab;  // device-built table (tiles = m-tiles of 64 x ntn), else null
+  SegTable tab;
 };
 
 __global__ void __launch_bounds__(256) grouped_gemm_f32_kernel(
@@ -237,14 +230,15 @@ __global__ void __launch_bounds__(256) grouped_gemm_f32_kernel(
   __shared__ float As[BK][BM + 4];
   __shared__ float Bs[BK][BN];
   const int tid = threadIdx.x, ty = tid / 16, tx = tid % 16;
-  for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
-    int lo = 0, hi = p.n_segs;
+  const SegTable& T = p.dtab ? *p.dtab : p.tab;
+  for (int t = blockIdx.x; t < T.total_tiles; t += gridDim.x) {
+    int lo = 0, hi = T.n_segs;
     while (hi - lo > 1) {
       int mid = (lo + hi) >> 1;
-      if (p.tile_start[mid] <= t) lo = mid; else hi = mid;
+      if (T.tile_start[mid] <= t) lo = mid; else hi = mid;
     }
-    const Seg& sg = p.seg[lo];
-    const int local = t - p.tile_start[lo];
+    const Seg& sg = T.seg[lo];
+    const int local = t - T.tile_start[lo];
     const int mt = local / p.ntn, nt = local % p.ntn;
     const int m0 = mt * BM, n0 = nt * BN;
     const float* A = sg.a_src ? A1 : A0;
@@ -370,10 +364,40 @@ int device_sms() {
   return n;
 }
 
+// Host-built table from a segment list (tile = `bm` rows x `ntn` column tiles).
+static int build_table(SegTable& T, const scb_segment_t* segs, int n_segs, int volume,
+                       const void* a_features, long long c_rows, int bm, int ntn, bool pad_rows) {
+  SCB_CHECK_ARG(n_segs <= SCB_MAX_SEGMENTS, "too many GEMM segments");
+  memset(&T, 0, sizeof(T));
+  int tiles = 0, used = 0;
+  for (int i = 0; i < n_segs; ++i) {
+    if (segs[i].rows <= 0) continue;
+    SCB_CHECK_ARG(segs[i].b_index >= 0 && segs[i].b_index < volume, "segment weight index");
+    SCB_CHECK_ARG(segs[i].a_src == 0 || a_features != nullptr, "centre segment needs features");
+    const int mt = (segs[i].rows + bm - 1) / bm;
+    SCB_CHECK_ARG(segs[i].c_row + (pad_rows ? (long long)mt * bm : segs[i].rows) <= c_rows,
+                  "partial buffer too small");
+    SegDesc& d = T.seg[used];
+    d.a_row = segs[i].a_row;
+    d.c_row = segs[i].c_row;
+    d.rows = segs[i].rows;
+    d.b_index = segs[i].b_index;
+    d.a_src = segs[i].a_src;
+    T.tile_start[used] = tiles;
+    tiles += mt * ntn;
+    ++used;
+  }
+  T.n_segs = used;
+  T.tile_start[used] = tiles;
+  T.total_tiles = tiles;
+  return SCB_OK;
+}
+
 static int gemm_f16(const void* a_buffer, long long a_rows, long long lda, const void* a_features,
                     long long f_rows, long long ldf, int c_in, const void* w_packed, int volume,
                     int c_out, float* partial, long long c_rows, long long ldc,
-                    const scb_segment_t* segs, int n_segs, cudaStream_t stream) {
+                    const scb_segment_t* segs, int n_segs, const SegTable* dtab,
+                    cudaStream_t stream) {
   using namespace tc;
   const int n_pad = (c_out + 15) / 16 * 16;
   const int k_pad = (c_in + 15) / 16 * 16;
@@ -405,29 +429,15 @@ static int gemm_f16(const void* a_buffer, long long a_rows, long long lda, const
   p.stages = stages;
   const int smem = fixed + stages * (int)p.stage_bytes;
 
-  SCB_CHECK_ARG(n_segs <= MAX_SEG, "too many GEMM segments");
-  int tiles = 0;
-  int used = 0;
-  for (int i = 0; i < n_segs; ++i) {
-    if (segs[i].rows <= 0) continue;
-    SCB_CHECK_ARG(segs[i].b_index >= 0 && segs[i].b_index < volume, "segment weight index");
-    SCB_CHECK_ARG(segs[i].a_src == 0 || a_features != nullptr, "centre segment needs features");
-    Seg& s = p.seg[used];
-    s.a_row = segs[i].a_row;
-    s.c_row = segs[i].c_row;
-    s.rows = segs[i].rows;
-    s.b_index = segs[i].b_index;
-    s.a_src = segs[i].a_src;
-    p.tile_start[used] = tiles;
-    const int nt = (segs[i].rows + BM - 1) / BM;
-    SCB_CHECK_ARG(segs[i].c_row + (long long)nt * BM <= c_rows, "partial buffer too small");
-    tiles += nt;
-    ++used;
+  int grid = device_sms();
+  if (dtab) {
+    p.dtab = dtab;  // tile count known on the device only: one persistent CTA per SM
+  } else {
+    const int rc = build_table(p.tab, segs, n_segs, volume, a_features, c_rows, BM, 1, true);
+    if (rc != SCB_OK) return rc;
+    if (p.tab.total_tiles == 0) return SCB_OK;
+    if (p.tab.total_tiles < grid) grid = p.tab.total_tiles;
   }
-  p.n_segs = used;
-  p.tile_start[used] = tiles;
-  p.total_tiles = tiles;
-  if (tiles == 0) return SCB_OK;
 
   CUtensorMap mA0, mA1, mB, mC;
   std::string err;
@@ -451,7 +461,6 @@ static int gemm_f16(const void* a_buffer, long long a_rows, long long lda, const
                                   smem_cap));
     configured = 1;
   }
-  const int grid = tiles < device_sms() ? tiles : device_sms();
   grouped_gemm_f16_kernel<<<grid, THREADS, smem, stream>>>(mA0, mA1, mB, mC, p);
   SCB_LAUNCHED();
   return SCB_OK;
@@ -460,35 +469,21 @@ static int gemm_f16(const void* a_buffer, long long a_rows, long long lda, const
 static int gemm_f32(const void* a_buffer, long long lda, const void* a_features, long long ldf,
                     int c_in, const void* w, int volume, int c_out, float* partial,
                     long long c_rows, long long ldc, const scb_segment_t* segs, int n_segs,
-                    cudaStream_t stream) {
+                    const SegTable* dtab, cudaStream_t stream) {
   using namespace simt;
-  SCB_CHECK_ARG(n_segs <= MAX_SEG, "too many GEMM segments");
   SCB_CHECK_ARG(ldc >= c_out, "partial stride smaller than c_out");
   Params p;
   memset(&p, 0, sizeof(p));
   p.ntn = (c_out + BN - 1) / BN;
-  int tiles = 0, used = 0;
-  for (int i = 0; i < n_segs; ++i) {
-    if (segs[i].rows <= 0) continue;
-    SCB_CHECK_ARG(segs[i].b_index >= 0 && segs[i].b_index < volume, "segment weight index");
-    SCB_CHECK_ARG(segs[i].a_src == 0 || a_features != nullptr, "centre segment needs features");
-    SCB_CHECK_ARG(segs[i].c_row + segs[i].rows <= c_rows, "partial buffer too small");
-    Seg& s = p.seg[used];
-    s.a_row = segs[i].a_row;
-    s.c_row = segs[i].c_row;
-    s.rows = segs[i].rows;
-    s.b_index = segs[i].b_index;
-    s.a_src = segs[i].a_src;
-    s.mtiles = (segs[i].rows + BM - 1) / BM;
-    p.tile_start[used] = tiles;
-    tiles += s.mtiles * p.ntn;
-    ++used;
+  int grid = device_sms() * 8;
+  if (dtab) {
+    p.dtab = dtab;
+  } else {
+    const int rc = build_table(p.tab, segs, n_segs, volume, a_features, c_rows, BM, p.ntn, false);
+    if (rc != SCB_OK) return rc;
+    if (p.tab.total_tiles == 0) return SCB_OK;
+    if (p.tab.total_tiles < grid) grid = p.tab.total_tiles;
   }
-  p.n_segs = used;
-  p.tile_start[used] = tiles;
-  p.total_tiles = tiles;
-  if (tiles == 0) return SCB_OK;
-  const int grid = tiles < device_sms() * 8 ? tiles : device_sms() * 8;
   grouped_gemm_f32_kernel<<<grid, 256, 0, stream>>>((const float*)a_buffer, lda,
                                                     (const float*)a_features, ldf, c_in,
                                                     (const float*)w, c_out, partial, ldc, p);
@@ -497,6 +492,18 @@ static int gemm_f32(const void* a_buffer, long long lda, const void* a_features,
 }
 
 }  // namespace scb
+
+extern "C" int32_t scb_gemm_tile_geometry(int32_t dtype, int32_t c_out, int32_t* bm,
+                                          int32_t* ntn) {
+  if (dtype == SCB_F16) {
+    *bm = scb::tc::BM;
+    *ntn = 1;
+  } else {
+    *bm = scb::simt::BM;
+    *ntn = (c_out + scb::simt::BN - 1) / scb::simt::BN;
+  }
+  return SCB_OK;
+}
 
 extern "C" int32_t scb_grouped_gemm(int32_t dtype, const void* a_buffer, int64_t a_rows,
                                     int64_t lda, const void* a_features, int64_t f_rows,
@@ -509,10 +516,30 @@ extern "C" int32_t scb_grouped_gemm(int32_t dtype, const void* a_buffer, int64_t
   cudaStream_t s = scb::as_stream(stream);
   if (dtype == SCB_F16)
     return scb::gemm_f16(a_buffer, a_rows, lda, a_features, f_rows, ldf, c_in, weights, volume,
-                         c_out, partial, c_rows, ldc, segments, n_segments, s);
+                         c_out, partial, c_rows, ldc, segments, n_segments, nullptr, s);
   if (dtype == SCB_F32)
     return scb::gemm_f32(a_buffer, lda, a_features, ldf, c_in, weights, volume, c_out, partial,
-                         c_rows, ldc, segments, n_segments, s);
+                         c_rows, ldc, segments, n_segments, nullptr, s);
   scb::set_error("scb_grouped_gemm: dtype must be f32 or f16");
+  return SCB_EINVAL;
+}
+
+extern "C" int32_t scb_grouped_gemm_table(int32_t dtype, const void* a_buffer, int64_t a_rows,
+                                          int64_t lda, const void* a_features, int64_t f_rows,
+                                          int64_t ldf, int32_t c_in, const void* weights,
+                                          int32_t volume, int32_t c_out, float* partial,
+                                          int64_t c_rows, int64_t ldc, const void* table,
+                                          scb_stream_t stream) {
+  SCB_CHECK_ARG(c_in >= 1 && c_out >= 1 && volume >= 1, "bad GEMM shape");
+  SCB_CHECK_ARG(table != nullptr, "missing device problem table");
+  cudaStream_t s = scb::as_stream(stream);
+  const auto* t = (const scb::SegTable*)table;
+  if (dtype == SCB_F16)
+    return scb::gemm_f16(a_buffer, a_rows, lda, a_features, f_rows, ldf, c_in, weights, volume,
+                         c_out, partial, c_rows, ldc, nullptr, 0, t, s);
+  if (dtype == SCB_F32)
+    return scb::gemm_f32(a_buffer, lda, a_features, ldf, c_in, weights, volume, c_out, partial,
+                         c_rows, ldc, nullptr, 0, t, s);
+  scb::set_error("scb_grouped_gemm_table: dtype must be f32 or f16");
   return SCB_EINVAL;
 }

@@ -385,6 +385,94 @@ __global__ void __launch_bounds__(CHUNK_THREADS) map_compact_kernel(
   }
 }
 
+// The whole gather/scatter plan straight from a hit matrix, after
+// map_count_kernel + map_scan_kernel (bases / offset_ptr): entry (j, k) of
+// offset n with rank r among the offset's entries (output order) goes to
+// buffer row slab[n] + r.  Writes buf_in, the full pos[n_out][V] (-1 where
+// absent, so no memset), the padding rows of every slab, and — block (0,0) —
+// the GEMM SegTable.  No host round trip.
+__global__ void __launch_bounds__(CHUNK_THREADS) plan_from_hits_kernel(
+    const int* __restrict__ hits, long long ld, int V, long long n_out, int nchunks,
+    const long long* __restrict__ bases, const long long* __restrict__ offset_ptr, int skip,
+    int tile, long long c_base, int gemm_bm, int gemm_ntn, int center_seg, long long center_rows,
+    int* __restrict__ buf_in, int* __restrict__ pos, SegTable* __restrict__ table) {
+  __shared__ long long ptr_s[SCB_MAX_SEGMENTS + 1];
+  __shared__ long long slab_s[SCB_MAX_SEGMENTS + 1];
+  __shared__ int warp_tot[CHUNK_THREADS / 32];
+  const int n = blockIdx.y, c = blockIdx.x;
+  for (int i = threadIdx.x; i <= V; i += blockDim.x) ptr_s[i] = offset_ptr[i];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long acc = 0;
+    for (int m = 0; m < V; ++m) {
+      slab_s[m] = acc;
+      const long long sz = (m == skip) ? 0 : ptr_s[m + 1] - ptr_s[m];
+      acc += (sz + tile - 1) / tile * tile;
+    }
+    slab_s[V] = acc;
+  }
+  __syncthreads();
+  if (c == 0 && n == 0) {
+    // padding rows of every slab -> -1 (zero rows in the gather)
+    for (int m = 0; m < V; ++m) {
+      const long long sz = (m == skip) ? 0 : ptr_s[m + 1] - ptr_s[m];
+      for (long long r = slab_s[m] + sz + threadIdx.x; r < slab_s[m + 1]; r += blockDim.x)
+        buf_in[r] = -1;
+    }
+    if (threadIdx.x == 0) {
+      int s = 0, tiles = 0;
+      if (center_seg >= 0 && center_rows > 0) {
+        SegDesc& d = table->seg[s];
+        d.a_row = 0; d.c_row = 0; d.rows = (int)center_rows; d.b_index = center_seg; d.a_src = 1;
+        table->tile_start[s++] = tiles;
+        tiles += (int)((center_rows + gemm_bm - 1) / gemm_bm) * gemm_ntn;
+      }
+      for (int m = 0; m < V; ++m) {
+        const long long sz = (m == skip) ? 0 : ptr_s[m + 1] - ptr_s[m];
+        if (sz == 0 || s >= SCB_MAX_SEGMENTS) continue;
+        SegDesc& d = table->seg[s];
+        d.a_row = slab_s[m]; d.c_row = slab_s[m] + c_base; d.rows = (int)sz; d.b_index = m;
+        d.a_src = 0;
+        table->tile_start[s++] = tiles;
+        tiles += (int)((sz + gemm_bm - 1) / gemm_bm) * gemm_ntn;
+      }
+      table->tile_start[s] = tiles;
+      table->n_segs = s;
+      table->total_tiles = tiles;
+      table->rows_pad = slab_s[V];
+    }
+  }
+  const int* col = hits + (long long)n * ld;
+  const long long base = (long long)c * CHUNK;
+  long long out_base = bases[(long long)n * nchunks + c] - ptr_s[n] + slab_s[n];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int i = 0; i < CHUNK_ITEMS; ++i) {
+    const long long k = base + i * CHUNK_THREADS + threadIdx.x;
+    const int j = k < n_out ? col[k] : -1;
+    const bool take = j >= 0 && n != skip;
+    const unsigned ballot = __ballot_sync(0xffffffffu, take);
+    if (lane == 0) warp_tot[warp] = __popc(ballot);
+    __syncthreads();
+    int before = 0, all = 0;
+#pragma unroll
+    for (int w = 0; w < CHUNK_THREADS / 32; ++w) {
+      before += (w < warp) ? warp_tot[w] : 0;
+      all += warp_tot[w];
+    }
+    if (k < n_out) {
+      int r = -1;
+      if (take) {
+        const long long row = out_base + before + __popc(ballot & ((1u << lane) - 1));
+        buf_in[row] = j;
+        r = (int)(row + c_base);
+      }
+      pos[k * V + n] = r;
+    }
+    out_base += all;
+    __syncthreads();
+  }
+}
+
 __device__ __forceinline__ int find_offset(const long long* ptr_s, int V, long long e) {
   int lo = 0, hi = V;  // largest n with ptr[n] <= e
   while (hi - lo > 1) {
@@ -538,6 +626,39 @@ extern "C" int32_t scb_map_transpose(const int64_t* offset_ptr, const int32_t* i
   if (total == 0) return SCB_OK;
   map_transpose_kernel<<<grid_blocks(total, 256), 256, (volume + 1) * sizeof(long long), s>>>(
       (const long long*)offset_ptr, in_idx, out_idx, volume, total, n_in, hits_t);
+  SCB_LAUNCHED();
+  return SCB_OK;
+}
+
+extern "C" int64_t scb_plan_rows_cap(int32_t volume, int64_t n_out, int32_t tile_rows) {
+  return (int64_t)volume * (n_out + tile_rows);
+}
+
+extern "C" int64_t scb_segtable_bytes(void) { return (int64_t)sizeof(SegTable); }
+
+extern "C" int32_t scb_plan_from_hits(const int32_t* hits, int32_t volume, int64_t n_out,
+                                      int32_t skip_offset, int32_t tile_rows, int64_t c_base,
+                                      int32_t gemm_bm, int32_t gemm_ntn, int32_t center_seg,
+                                      int64_t center_rows, void* workspace, int64_t* offset_ptr,
+                                      int32_t* buf_in, int32_t* pos, void* table,
+                                      scb_stream_t stream) {
+  SCB_CHECK_ARG(volume >= 1 && volume <= SCB_MAX_SEGMENTS - 1, "kernel volume too large");
+  SCB_CHECK_ARG(tile_rows >= 1 && gemm_bm >= 1 && gemm_ntn >= 1, "bad tile sizes");
+  cudaStream_t s = as_stream(stream);
+  const long long nchunks = (n_out + CHUNK - 1) / CHUNK;
+  if (nchunks == 0) {
+    SCB_CUDA(cudaMemsetAsync(table, 0, sizeof(SegTable), s));
+    SCB_CUDA(cudaMemsetAsync(offset_ptr, 0, (volume + 1) * sizeof(int64_t), s));
+    return SCB_OK;
+  }
+  const int32_t rc = scb_map_count(hits, volume, n_out, workspace, offset_ptr, stream);
+  if (rc != SCB_OK) return rc;
+  const long long m = volume * nchunks;
+  const long long* bases = (const long long*)((const char*)workspace + (m * 4 + 255) / 256 * 256);
+  plan_from_hits_kernel<<<dim3((unsigned)nchunks, volume), CHUNK_THREADS, 0, s>>>(
+      hits, hits_ld(n_out), volume, n_out, (int)nchunks, bases, (const long long*)offset_ptr,
+      skip_offset, tile_rows, c_base, gemm_bm, gemm_ntn, center_seg, center_rows, buf_in, pos,
+      (SegTable*)table);
   SCB_LAUNCHED();
   return SCB_OK;
 }

@@ -33,7 +33,9 @@ template <typename VT, int UNROLL = 4>
 __global__ void __launch_bounds__(256) gather_kernel(const VT* __restrict__ feat, long long ldf_v,
                                                      const int* __restrict__ buf_in,
                                                      long long rows, int vecs_per_row,
-                                                     VT* __restrict__ buf, long long ldb_v) {
+                                                     VT* __restrict__ buf, long long ldb_v,
+                                                     const long long* __restrict__ rows_dev) {
+  if (rows_dev) rows = min(rows, *rows_dev);  // device-built plans: rows in use
   const long long total = rows * vecs_per_row;
   const long long stride = (long long)gridDim.x * blockDim.x;
   // UNROLL independent (index load -> row load -> store) chains per thread so
@@ -63,11 +65,12 @@ __global__ void __launch_bounds__(256) gather_kernel(const VT* __restrict__ feat
 
 template <typename VT>
 static void launch_gather(const void* f, long long ldf_b, const int* buf_in, long long rows,
-                          long long row_b, void* buf, long long ldb_b, cudaStream_t s) {
+                          long long row_b, void* buf, long long ldb_b, const long long* rows_dev,
+                          cudaStream_t s) {
   const int vpr = (int)(row_b / sizeof(VT));
   gather_kernel<VT><<<blocks_for(rows * vpr, 256), 256, 0, s>>>(
       (const VT*)f, ldf_b / (long long)sizeof(VT), buf_in, rows, vpr, (VT*)buf,
-      ldb_b / (long long)sizeof(VT));
+      ldb_b / (long long)sizeof(VT), rows_dev);
 }
 
 // ------------------------------------------------------------------ scatter
@@ -228,7 +231,7 @@ using namespace scb;
 
 extern "C" int32_t scb_gather(int32_t dtype, const void* features, int64_t n_in, int32_t channels,
                               int64_t ld_feat, const int32_t* buf_in, int64_t rows, void* buffer,
-                              int64_t ld_buf, scb_stream_t stream) {
+                              int64_t ld_buf, const int64_t* rows_dev, scb_stream_t stream) {
   (void)n_in;
   SCB_CHECK_ARG(dtype == SCB_F32 || dtype == SCB_F16, "dtype must be f32 or f16");
   SCB_CHECK_ARG(channels >= 1 && ld_feat >= channels && ld_buf >= channels, "bad strides");
@@ -240,10 +243,11 @@ extern "C" int32_t scb_gather(int32_t dtype, const void* features, int64_t n_in,
     return row_b % w == 0 && ldf_b % w == 0 && ldb_b % w == 0 && align % w == 0;
   };
   cudaStream_t s = as_stream(stream);
-  if (fits(16)) launch_gather<int4>(features, ldf_b, buf_in, rows, row_b, buffer, ldb_b, s);
-  else if (fits(8)) launch_gather<int2>(features, ldf_b, buf_in, rows, row_b, buffer, ldb_b, s);
-  else if (fits(4)) launch_gather<int>(features, ldf_b, buf_in, rows, row_b, buffer, ldb_b, s);
-  else launch_gather<short>(features, ldf_b, buf_in, rows, row_b, buffer, ldb_b, s);
+  const long long* rd = (const long long*)rows_dev;
+  if (fits(16)) launch_gather<int4>(features, ldf_b, buf_in, rows, row_b, buffer, ldb_b, rd, s);
+  else if (fits(8)) launch_gather<int2>(features, ldf_b, buf_in, rows, row_b, buffer, ldb_b, rd, s);
+  else if (fits(4)) launch_gather<int>(features, ldf_b, buf_in, rows, row_b, buffer, ldb_b, rd, s);
+  else launch_gather<short>(features, ldf_b, buf_in, rows, row_b, buffer, ldb_b, rd, s);
   SCB_LAUNCHED();
   return SCB_OK;
 }

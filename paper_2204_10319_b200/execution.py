@@ -28,7 +28,8 @@ import numpy as np
 import torch
 
 from . import _native as nat
-from .core import CoordinateSet, PrecisionMode, SparseTensor, WeightTensor
+from .core import (CoordinateSet, PrecisionMode, SparseTensor, WeightTensor,
+                   flush_saturation_warnings)
 from .mapping import (DEFAULT_GRID_CELL_CAP, GatherScatterPlan, GridCapacityError, KernelMap,
                       KernelOffsets, build_gather_scatter_plan, build_index,
                       compute_output_coords, downsample_boundary, enumerate_offsets, map_search,
@@ -162,6 +163,7 @@ class ExecOptions:
     plan_log: list | None = None
     map_reuse: bool = True
     dataflow: str = "staged"
+    sync_free: bool = True
 
 
     def __post_init__(self):
@@ -209,7 +211,7 @@ class _Arena:
         for s in shape:
             n *= int(s)
         nbytes = n * torch.empty((), dtype=dtype).element_size()
-        key = (str(device), torch.cuda.current_stream(device).cuda_stream, name)
+        key = (device.index, nat.stream_handle(), name)
         raw = self.slots.get(key)
         if raw is None or raw.numel() < nbytes:
             grow = 0 if raw is None else raw.numel() + raw.numel() // 4
@@ -225,9 +227,45 @@ def _gather_padded(features: torch.Tensor, plan: GatherScatterPlan, c: int) -> t
     ld = _buffer_ld(features.dtype, c)
     buf = _ARENA.tensor("gather", (max(plan.rows_pad, 1), ld), features.dtype, features.device)
     nat.call("scb_gather", nat.dtype_code(features.dtype), nat.ptr(features), features.shape[0], c,
-             _ld(features), nat.ptr(plan.buf_in), plan.rows_pad, nat.ptr(buf), ld,
+             _ld(features), nat.ptr(plan.buf_in), plan.rows_pad, nat.ptr(buf), ld, None,
              nat.stream_handle())
     return buf
+
+
+class DevicePlan:
+    """Sync-free plan of one layer (scb_plan_from_hits): buffer rows,
+    output positions and the GEMM problem table all built on the device from
+    the hit matrix; sizes are capacities (upper bounds), the real row count
+    lives in the device table."""
+
+    __slots__ = ("pos", "buf_in", "table", "rows_cap", "c_base", "offset_ptr")
+
+    def __init__(self, kmap: KernelMap, skip: int | None, dtype, c_out: int,
+                 center_rows: int, center_seg: int | None):
+        import ctypes
+        lib = nat.load()
+        dev = kmap.device
+        V, n_out = kmap.offsets.volume, kmap.n_out
+        bm, ntn = ctypes.c_int32(), ctypes.c_int32()
+        lib.scb_gemm_tile_geometry(nat.dtype_code(dtype), c_out, ctypes.byref(bm),
+                                   ctypes.byref(ntn))
+        self.rows_cap = int(lib.scb_plan_rows_cap(V, n_out, nat.TILE_ROWS))
+        self.c_base = (center_rows + nat.TILE_ROWS - 1) // nat.TILE_ROWS * nat.TILE_ROWS
+        ws = _ARENA.tensor("map_ws", (max(int(lib.scb_map_workspace(V, n_out)), 8),),
+                           torch.uint8, dev)
+        self.offset_ptr = torch.empty(V + 1, dtype=torch.int64, device=dev)
+        self.buf_in = torch.empty(max(self.rows_cap, 1), dtype=torch.int32, device=dev)
+        self.pos = torch.empty((max(n_out, 1), V), dtype=torch.int32, device=dev)
+        self.table = torch.empty(int(lib.scb_segtable_bytes()), dtype=torch.uint8, device=dev)
+        nat.call("scb_plan_from_hits", nat.ptr(kmap.hits), V, n_out,
+                 -1 if skip is None else skip, nat.TILE_ROWS, self.c_base, bm.value, ntn.value,
+                 -1 if center_seg is None else center_seg, center_rows, nat.ptr(ws),
+                 nat.ptr(self.offset_ptr), nat.ptr(self.buf_in), nat.ptr(self.pos),
+                 nat.ptr(self.table), nat.stream_handle())
+
+    @property
+    def rows_pad_ptr(self) -> int:
+        return self.table.data_ptr() + 8  # SegTable.rows_pad
 
 
 def gather(features, plan: GatherScatterPlan, order: str = "weight_stationary") -> torch.Tensor:
@@ -492,6 +530,46 @@ def _run_fused(features: torch.Tensor, kmap: KernelMap, w: WeightTensor, opts: E
     return out
 
 
+def _run_staged_device(features: torch.Tensor, kmap: KernelMap, w: WeightTensor,
+                       opts: ExecOptions, center: int | None, epilogue: dict | None):
+    """Staged gather -> grouped GEMM -> scatter without any host sync: the
+    plan and GEMM problem table come from scb_plan_from_hits, buffers are
+    arena capacities, kernels read the live row/tile counts on the device.
+    Same buffer layout and fold order as the host-planned path."""
+    label, timer = opts.layer_label, opts.timer
+    dt = features.dtype
+    c_in, c_out = w.c_in, w.c_out
+    direct = center is not None and _direct_center(dt, c_in)
+    center_rows = features.shape[0] if direct else 0
+    key = ("device", center if direct else None, nat.dtype_code(dt), c_out if dt == torch.float32
+           else 0, center_rows)
+    dp = kmap._plans.get(key)
+    if dp is None:
+        dp = DevicePlan(kmap, center if direct else None, dt, c_out, center_rows,
+                        center if direct else None)
+        kmap._plans[key] = dp
+    ld = _buffer_ld(dt, c_in)
+    with _timed(timer, label, "gather"):
+        buf = _ARENA.tensor("gather", (max(dp.rows_cap, 1), ld), dt, features.device)
+        nat.call("scb_gather", nat.dtype_code(dt), nat.ptr(features), features.shape[0], c_in,
+                 _ld(features), nat.ptr(dp.buf_in), dp.rows_cap, nat.ptr(buf), ld,
+                 dp.rows_pad_ptr, nat.stream_handle())
+    wt, ldc = _weights_for(w, dt)
+    c_rows = dp.c_base + dp.rows_cap
+    with _timed(timer, label, "matmul"):
+        partial = _ARENA.tensor("partial", (max(c_rows, 1), ldc), torch.float32, features.device)
+        nat.call("scb_grouped_gemm_table", nat.dtype_code(dt), nat.ptr(buf), max(dp.rows_cap, 1),
+                 ld, nat.ptr(features) if direct else None, features.shape[0] if direct else 0,
+                 _ld(features) if direct else 0, c_in, nat.ptr(wt), w.weights.shape[0], c_out,
+                 nat.ptr(partial), max(c_rows, 1), ldc, nat.ptr(dp.table), nat.stream_handle())
+    out = torch.empty((kmap.n_out, c_out), dtype=dt, device=features.device)
+    with _timed(timer, label, "scatter"):
+        nat.call("scb_scatter", nat.ptr(partial), ldc, nat.ptr(dp.pos), kmap.offsets.volume,
+                 kmap.n_out, c_out, 0 if direct else -1, nat.dtype_code(dt), nat.ptr(out), c_out,
+                 *_epi_args(epilogue), nat.stream_handle())
+    return out
+
+
 def _run_dataflow(features: torch.Tensor, kmap: KernelMap, w: WeightTensor,
                   strat: LayerStrategy, schedule, symmetric: bool, opts: ExecOptions,
                   center: int | None, epilogue: dict | None = None, record=None) -> torch.Tensor:
@@ -500,6 +578,9 @@ def _run_dataflow(features: torch.Tensor, kmap: KernelMap, w: WeightTensor,
         if record is not None and opts.workload_log is not None:
             record(kmap.sizes)
         return _run_fused(features, kmap, w, opts, epilogue)
+    if opts.sync_free and opts.workload_log is None and opts.plan_log is None \
+            and opts.traffic_log is None:
+        return _run_staged_device(features, kmap, w, opts, center, epilogue)
     sizes = kmap.sizes
     if center is not None:
         sizes[center] = 0
@@ -621,6 +702,7 @@ def sparse_conv_forward(t: SparseTensor, w: WeightTensor, spec: LayerSpec,
 
     ``epilogue`` (B200 extension) fuses
     ``{"scale", "shift", "bias", "relu"}`` into the scatter's single write."""
+    flush_saturation_warnings()
     opts = options or ExecOptions()
     _check_channels(t, w, spec)
     label, timer = opts.layer_label, opts.timer

@@ -456,3 +456,41 @@ def test_lazy_map_needs_no_compaction_for_fused(sc, rng):
     (_, kmap), = t.coordset.maps.values()
     assert kmap._csr is None  # the fused path consumed the hit matrix only
     assert kmap.total > 0 and kmap._csr is not None  # CSR on demand
+
+
+@pytest.mark.parametrize("prec", ["fp32", "fp16"])
+@pytest.mark.parametrize("k,s,c_in", [(3, 1, 16), (3, 1, 4), (2, 2, 32), (3, 2, 8)])
+def test_sync_free_staged_is_bit_identical(sc, rng, prec, k, s, c_in):
+    """The device-planned staged path (no host sync) reproduces the
+    host-planned one bit for bit (same layout, same fold order)."""
+    coords = random_coords(rng, (24, 22, 20), 0.08)
+    f = O.quantize(rng.standard_normal((coords.shape[0], c_in)).astype(np.float32), prec)
+    w = sc.WeightTensor(rng.normal(0, 0.1, (k ** 3, c_in, 24)).astype(np.float32), k, 3)
+    outs = []
+    for sync_free in (True, False):
+        t = sc.SparseTensor(coords, f, 1, (24, 22, 20))
+        cache = {}
+        o = sc.sparse_conv_forward(t, w, sc.LayerSpec(k, s, c_in, 24, reuse_key="d"), None, cache,
+                                   sc.ExecOptions(sync_free=sync_free, dataflow="staged"))
+        outs.append(o.features_numpy())
+        if s == 2:
+            w2 = sc.WeightTensor(rng.normal(0, 0.1, (k ** 3, 24, 8)).astype(np.float32), k, 3) \
+                if not outs[1:] else w2
+            u = sc.inverse_conv_forward(o, w2, sc.LayerSpec(k, 1, 24, 8, transposed=True,
+                                                            reuse_key="d"), cache, None,
+                                        sc.ExecOptions(sync_free=sync_free, dataflow="staged"))
+            outs.append(u.features_numpy())
+    half = len(outs) // 2
+    for a, b in zip(outs[:half], outs[half:]):
+        np.testing.assert_array_equal(a, b)
+    _, ref, _ = O.conv_forward(coords, f, (24, 22, 20), w.weights, k, s)
+    assert rel_l2(outs[0], ref) <= TOL[prec]
+
+
+def test_fp16_saturation_warns(sc):
+    t = sc.SparseTensor(np.array([[0, 1, 1, 1]]), np.array([[1e6, -1e6, 1.0]], np.float32), 1,
+                        (4, 4, 4))
+    with pytest.warns(UserWarning, match="saturated"):
+        q = sc.quantize_features(t, sc.PrecisionMode.FP16_STORAGE)
+        f = q.features_numpy()
+    assert f[0, 0] == 65504 and f[0, 1] == -65504 and f[0, 2] == 1.0
