@@ -43,7 +43,6 @@ struct Params {
   int ops;                  // offsets per stage (small C_in -> several)
   int debug;                // SCB_IMPLICIT_DEBUG: 1 no A loads, 2 no MMAs, 16 wait counters
   int groups;               // ceil(V / ops) offset groups per tile
-  int nacc;                 // independent TMEM sub-accumulators per tile
   uint32_t idesc, tmem_cols;
   uint32_t a_off_bytes;     // one offset's A block [128 rows][kc] (1024-aligned)
   uint32_t b_off_bytes;     // one offset's B block [n_pad][kc]   (1024-aligned)
@@ -282,11 +281,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       for (int t = t_begin; t < t_end; ++t) {
         IC_PROF(4, true, mbar_wait(tempty + acc, acc_phase ^ 1));
         tc_after();
-        // offset n accumulates into sub-accumulator n % nacc: nacc independent
-        // MMA chains instead of one (a small-N MMA waits on its predecessor);
-        // the epilogue sums them.  Offsets n < nacc always issue (their first
-        // MMA zero-initialises the sub-accumulator; absent rows are zeros).
-        const uint32_t d_base = tmem_base + (uint32_t)(acc * p.nacc * p.n_pad);
+        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * p.n_pad);
+        uint32_t issued = 0;
         for (int g = 0; g < p.groups; ++g) {
           for (int kk = 0; kk < p.n_kchunks; ++kk) {
             IC_PROF(3, true, mbar_wait(full + stage, phase));
@@ -296,14 +292,15 @@ __global__ void __launch_bounds__(THREADS, 1)
             for (int o = 0; o < p.ops; ++o) {
               const int n = g * p.ops + o;
               if (n >= V) break;
-              const bool init = n < p.nacc;
-              if (!init && (flags[stage * MAX_OPS + o] == 0u || (p.debug & 2))) continue;
-              const uint32_t d_tmem = d_base + (uint32_t)((n % p.nacc) * p.n_pad);
+              const bool valid = flags[stage * MAX_OPS + o] != 0u;
+              if (!(valid || (!issued && n == V - 1))) continue;
+              if ((p.debug & 2) && issued) continue;
               const uint32_t ao = sa + o * p.a_off_bytes, bo = sb + o * p.b_off_bytes;
-              for (int k = 0; k < p.kc / 16; ++k)
+              for (int k = 0; k < p.kc / 16; ++k) {
                 mma_f16(d_tmem, make_sdesc(ao + k * 32, sbo, layout),
-                        make_sdesc(bo + k * 32, sbo, layout), p.idesc,
-                        (init && kk == 0 && k == 0) ? 0u : 1u);
+                        make_sdesc(bo + k * 32, sbo, layout), p.idesc, issued);
+                issued = 1;
+              }
             }
             mma_commit(empty + stage);
             if (++stage == p.stages) { stage = 0; phase ^= 1; }
@@ -328,19 +325,15 @@ __global__ void __launch_bounds__(THREADS, 1)
       tc_after();
       for (int j = 0; j < chunks; ++j) {
         const int c0 = j * p.epi_cols;
-        const uint32_t taddr = tmem_base + ((uint32_t)(32 * q) << 16) +
-                               (uint32_t)(acc * p.nacc * p.n_pad + c0);
+        const uint32_t taddr =
+            tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * p.n_pad + c0);
+        uint32_t r[32];
+        TMEM_LD_X16(taddr, r);
+        if (p.epi_cols == 32) TMEM_LD_X16(taddr + 16, (r + 16));
+        tmem_wait_ld();
         float v[32];
 #pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] = 0.f;
-        for (int a = 0; a < p.nacc; ++a) {  // sum the sub-accumulators in a fixed order
-          uint32_t r[32];
-          TMEM_LD_X16(taddr + a * p.n_pad, r);
-          if (p.epi_cols == 32) TMEM_LD_X16(taddr + a * p.n_pad + 16, (r + 16));
-          tmem_wait_ld();
-#pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] += __uint_as_float(r[i]);
-        }
+        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
         const int ncol = p.epi_cols;
         if (p.scale) {
 #pragma unroll
@@ -465,12 +458,7 @@ extern "C" int32_t scb_conv_implicit(const void* features, int64_t n_in, int32_t
   p.relu = relu;
   p.idesc = (1u << 4) | ((uint32_t)(n_pad >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
   uint32_t cols = 32;
-  // independent sub-accumulators: 2 (double buffer) x nacc x n_pad <= 512 columns
-  int nacc = 256 / n_pad;
-  nacc = nacc > 8 ? 8 : (nacc < 1 ? 1 : nacc);
-  if (nacc > volume) nacc = volume;
-  p.nacc = nacc;
-  while (cols < (uint32_t)(2 * nacc * n_pad)) cols *= 2;
+  while (cols < (uint32_t)(2 * n_pad)) cols *= 2;
   p.tmem_cols = cols;
   auto r1024 = [](uint32_t x) { return (x + 1023u) / 1024u * 1024u; };
   p.a_tx = (uint32_t)(BM * p.kc * 2);
