@@ -12,15 +12,17 @@
 // neighbour anywhere in a tile skip their MMAs.  (A TMA tile::gather4 variant
 // was measured ~2-3x slower on this path: ~100 cycles per 4-row request.)
 //
-// Warp roles (320 threads, 1 CTA / SM, persistent over contiguous tile ranges):
-//   warp 0     TMA producer of the weight slices (B, K-major fp16)
-//   warp 1     TMEM allocator + single-thread tcgen05.mma issuer
-//   warps 2-5  A producers: neighbour indices one tile ahead, cp.async gather
-//   warps 6-9  epilogue: tcgen05.ld -> epilogue -> swizzled smem -> TMA store
+// Warp roles (64 + 128 P + 128 threads, 1 CTA / SM, persistent over
+// contiguous tile ranges; P = 1 A-producer group):
+//   warp 0        TMA producer of the weight slices (B, K-major fp16)
+//   warp 1        TMEM allocator + single-thread tcgen05.mma issuer
+//   warps 2..     A producers: neighbour indices one tile ahead, cp.async gather
+//   last 4 warps  epilogue: tcgen05.ld -> epilogue -> swizzled smem -> TMA store
 #include <cuda.h>
 
 #include <cstdio>
 #include <cstdlib>
+#include <algorithm>
 
 #include "common.cuh"
 #include "sm100_ptx.cuh"
@@ -31,7 +33,7 @@ namespace ic {
 using namespace ::scb::ptx;
 
 constexpr int BM = 128;
-constexpr int THREADS = 320;
+constexpr int MAX_P = 1;                // A-producer groups
 constexpr int EPI_BUF = 32 * 64;        // 32 rows x 64 B (32 fp16 columns)
 constexpr int EPI_BYTES = 4 * 2 * EPI_BUF;
 constexpr int MAX_OPS = 8;              // kernel offsets per pipeline stage
@@ -81,11 +83,14 @@ __device__ __forceinline__ uint32_t pack_half2(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
-template <int V, int LAG, int KC>
-__global__ void __launch_bounds__(THREADS, 1)
+template <int V, int LAG, int KC, int P, int MINB>
+__global__ void __launch_bounds__(64 + 128 * P + 128, MINB)
     implicit_conv_f16_kernel(const __grid_constant__ CUtensorMap tmB,
                              const __grid_constant__ CUtensorMap tmOut,
                              const __grid_constant__ Params p) {
+  constexpr int NPROD = 128 * P;           // A-producer threads
+  constexpr int EPI0 = 2 + 4 * P;          // first epilogue warp
+  constexpr int NT = (V + P - 1) / P;      // offsets per producer thread
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* epi_base = smem + (size_t)p.stages * p.stage_bytes;
@@ -96,7 +101,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint64_t* tfull = empty + p.stages;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
-  uint8_t* wmask = (uint8_t*)(tmem_slot + 4);  // [stages][128]: blocks each row holds data in
+  uint8_t* wmask = (uint8_t*)(tmem_slot + 4);  // [stages][P][128]: blocks each row holds data in
 
   const long long k_t0 = clock64();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -105,7 +110,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < p.stages; ++s) {
-      mbar_init(full + s, 4 * 32 + 1);  // 128 A-producer threads + the B expect_tx arrive
+      mbar_init(full + s, NPROD + 1);  // A-producer threads + the B expect_tx arrive
       mbar_init(empty + s, 1);
     }
     for (int a = 0; a < 2; ++a) {
@@ -146,117 +151,109 @@ __global__ void __launch_bounds__(THREADS, 1)
           }
         }
     }
-  } else if (warp >= 2 && warp < 6) {
-    // ============ A producers (128 threads).  Thread r owns output row r of
-    // the tile for index bookkeeping: it prefetches that row's V neighbour
-    // rows one tile ahead (registers), parks them in the shared table and
-    // computes the per-offset "any neighbour" flags, then copies its own row
-    // of every offset block: one index read and one 64-bit address per row,
-    // CPR predicated 16-B cp.async (present) or zero stores (absent) with
-    // immediate chunk offsets.  (Spreading a row's chunks over consecutive
+  } else if (warp >= 2 && warp < EPI0) {
+    // ============ A producers (P groups of 128 threads).  Thread (h, r) owns
+    // output row r of the tile for the offsets n = h (mod P): it prefetches
+    // those neighbour rows one tile ahead (registers), parks them in the
+    // shared table and computes the per-offset "any neighbour" flags, then
+    // copies its row of each of its offset blocks: one index read and one
+    // 64-bit address per row, CPR predicated 16-B cp.async (present) or zero
+    // stores (absent) with immediate chunk offsets.  Two groups put two
+    // producer warps on every scheduler: the copy loop is latency-bound per
+    // warp, not bandwidth-bound.  (Spreading a row's chunks over consecutive
     // lanes coalesces better but costs ~4x the instructions; measured slower.)
-    const int row = threadIdx.x - 64;
-    const int wbyte = warp - 2;
+    const int pt = threadIdx.x - 64;
+    const int row = pt & (BM - 1);
+    const int h = pt >> 7;
+    const int wbyte = (pt >> 5) & 3;
     constexpr int CPR = KC / 8;               // 16-B chunks per row per K chunk
     constexpr int SWZ = KC * 2;               // swizzle span = row bytes
-    int nxt[V];
+    int nxt[NT];
     {
       const long long k = (long long)t_begin * BM + row;
 #pragma unroll
-      for (int n = 0; n < V; ++n)
-        nxt[n] = (t_begin < t_end && k < p.n_out) ? __ldg(p.hits + (long long)n * p.ldh + k) : -1;
-    }
-    // zero this thread's row of every A block once; afterwards only changed
-    // rows are rewritten (see the stage loop)
-    for (int s = 0; s < p.stages; ++s) {
-      for (int o = 0; o < p.ops; ++o) {
-        const uint32_t base = smem_u32(smem + (size_t)s * p.stage_bytes) + o * p.a_off_bytes +
-                              row * (KC * 2);
-#pragma unroll
-        for (int c = 0; c < CPR; ++c)
-          asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(base + c * 16), "r"(0)
-                       : "memory");
+      for (int i = 0; i < NT; ++i) {
+        const int n = h + i * P;
+        nxt[i] = (n < V && t_begin < t_end && k < p.n_out) ? __ldg(p.hits + (long long)n * p.ldh + k) : -1;
       }
-      wmask[s * BM + row] = 0;
     }
+    // zero every A block once; afterwards only rows whose presence changed
+    // are rewritten (see the stage loop)
+    for (int s = 0; s < p.stages; ++s) {
+      const uint32_t base = smem_u32(smem + (size_t)s * p.stage_bytes);
+      for (uint32_t b = (uint32_t)pt * 16u; b < p.a_stage_bytes; b += NPROD * 16u)
+        asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(base + b), "r"(0) : "memory");
+      wmask[(s * P + h) * BM + row] = 0;
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(NPROD) : "memory");
     int stage = 0, sig = 0, pending = 0;
     uint32_t phase = 0;
     const uint32_t nbr_base = smem_u32(nbr_s);
+    const int rx = SWZ == 128 ? (row & 7) : (SWZ == 64 ? ((row >> 1) & 3) : ((row >> 2) & 1));
     for (int t = t_begin, buf = 0; t < t_end; ++t, buf ^= 1) {
-      const long long tp0 = ((p.debug & 16) && blockIdx.x == 0 && row == 0) ? clock64() : 0;
       int* nb = nbr_s + buf * V * BM;
       const uint32_t nb_s = nbr_base + (uint32_t)(buf * V * BM * 4);
       uint32_t anymask = 0;
 #pragma unroll
-      for (int n = 0; n < V; ++n) {
-        nb[n * BM + row] = nxt[n];
-        if (__any_sync(0xffffffffu, nxt[n] >= 0)) anymask |= 1u << n;
+      for (int i = 0; i < NT; ++i) {
+        const int n = h + i * P;
+        if (n < V) {
+          nb[n * BM + row] = nxt[i];
+          if (__any_sync(0xffffffffu, nxt[i] >= 0)) anymask |= 1u << n;
+        }
       }
-      const long long tb0 = ((p.debug & 16) && blockIdx.x == 0 && row == 0) ? clock64() : 0;
-      asm volatile("bar.sync 1, 128;" ::: "memory");  // the tile's index table is complete
-      if ((p.debug & 16) && blockIdx.x == 0 && row == 0)
-        atomicAdd(&g_ic_prof[14], (unsigned long long)(clock64() - tb0));
+      asm volatile("bar.sync 1, %0;" ::"n"(NPROD) : "memory");  // the tile's index table is complete
       {
         const long long k = (long long)(t + 1) * BM + row;
         const bool ok = (t + 1 < t_end) && k < p.n_out;
 #pragma unroll
-        for (int n = 0; n < V; ++n) nxt[n] = ok ? __ldg(p.hits + (long long)n * p.ldh + k) : -1;
+        for (int i = 0; i < NT; ++i) {
+          const int n = h + i * P;
+          nxt[i] = (ok && n < V) ? __ldg(p.hits + (long long)n * p.ldh + k) : -1;
+        }
       }
-      if ((p.debug & 16) && blockIdx.x == 0 && row == 0)
-        atomicAdd(&g_ic_prof[13], (unsigned long long)(clock64() - tp0));
       for (int g = 0; g < p.groups; ++g) {
         const int nv = min(p.ops, V - g * p.ops);
         for (int kk = 0; kk < p.n_kchunks; ++kk) {
-          IC_PROF(0, row == 0, mbar_wait(empty + stage, phase ^ 1));
+          IC_PROF(0, pt == 0, mbar_wait(empty + stage, phase ^ 1));
           if (lane == 0)
             for (int o = 0; o < nv; ++o)
-              reinterpret_cast<uint8_t*>(flags + stage * MAX_OPS + o)[wbyte] =
-                  (anymask >> (g * p.ops + o)) & 1u;
+              if ((g * p.ops + o) % P == h)
+                reinterpret_cast<uint8_t*>(flags + stage * MAX_OPS + o)[wbyte] =
+                    (anymask >> (g * p.ops + o)) & 1u;
           const uint32_t dst = smem_u32(smem + (size_t)stage * p.stage_bytes);
           const int col0 = kk * KC;
-          const long long tl0 = ((p.debug & 16) && blockIdx.x == 0 && row == 0) ? clock64() : 0;
-          // thread = row: one index read and one 64-bit address per row,
-          // then CPR predicated 16-B copies (or zero stores) with immediate
-          // chunk offsets
-          const int rx = SWZ == 128 ? (row & 7) : (SWZ == 64 ? ((row >> 1) & 3) : ((row >> 2) & 1));
           const int live = min(CPR, (p.c_in - col0) / 8);  // chunks inside C_in
           // Stage buffers start zeroed and this thread alone owns row `row` of
-          // every block, so it only writes what changes: present -> copy;
+          // its blocks, so it only writes what changes: present -> copy;
           // absent but written by the slot's previous use -> re-zero;
           // absent and already zero -> nothing (most rows: |M|/(V*N) ~ 0.28).
           // Chunks past C_in are never written, so they stay zero.
-          const uint32_t prev = wmask[stage * BM + row];
-          uint32_t now = prev & ~((1u << nv) - 1u);
+          uint8_t* wm = wmask + (stage * P + h) * BM + row;
+          uint32_t now = *wm;
           for (int o = 0; o < nv; ++o) {
+            const int n = g * p.ops + o;
+            if (n % P != h) continue;
             int j;
-            asm volatile("ld.shared.b32 %0, [%1];"
-                         : "=r"(j)
-                         : "r"(nb_s + (uint32_t)(((g * p.ops + o) * BM + row) * 4)));
+            asm volatile("ld.shared.b32 %0, [%1];" : "=r"(j) : "r"(nb_s + (uint32_t)((n * BM + row) * 4)));
+            const bool present = j >= 0 && !(p.debug & 1);
+            const bool rezero = !present && ((now >> o) & 1u);
             const uint32_t base = dst + o * p.a_off_bytes + row * (KC * 2);
-            if (j >= 0 && !(p.debug & 1)) {
-              now |= 1u << o;
-              const __half* src = p.feat + (long long)j * p.ldf + col0;
+            const __half* src = p.feat + (long long)max(j, 0) * p.ldf + col0;
 #pragma unroll
-              for (int c = 0; c < CPR; ++c)
-                if (c < live) cp_async16(base + ((uint32_t)(c ^ rx) << 4), src + c * 8, 16u);
-            } else if (prev & (1u << o)) {
-#pragma unroll
-              for (int c = 0; c < CPR; ++c)
-                if (c < live)
-                  asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(
-                                   base + ((uint32_t)(c ^ rx) << 4)),
-                               "r"(0)
-                               : "memory");
+            for (int c = 0; c < CPR; ++c) {
+              const uint32_t d = base + ((uint32_t)(c ^ rx) << 4);
+              cp_async16_if(d, src + c * 8, present && c < live);
+              st_zero16_if(d, rezero && c < live);
             }
+            now = (now & ~(1u << o)) | ((uint32_t)present << o);
           }
-          wmask[stage * BM + row] = (uint8_t)now;
-          if ((p.debug & 16) && blockIdx.x == 0 && row == 0)
-            atomicAdd(&g_ic_prof[10], (unsigned long long)(clock64() - tl0));
+          *wm = (uint8_t)now;
           cp_async_commit();
           if (++pending > LAG) {
-            IC_PROF(1, row == 0, cp_async_wait<LAG>());
-            if (!(p.debug & 4)) IC_PROF(11, row == 0, fence_async_smem());  // generic -> async proxy
-            IC_PROF(12, row == 0, mbar_arrive(full + sig));
+            IC_PROF(1, pt == 0, cp_async_wait<LAG>());
+            if (!(p.debug & 4)) fence_async_smem();  // generic -> async proxy
+            mbar_arrive(full + sig);
             if (++sig == p.stages) sig = 0;
             --pending;
           }
@@ -310,10 +307,10 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
     }
-  } else if (warp >= 6) {
+  } else if (warp >= EPI0) {
     // ============ epilogue
     const int q = warp & 3;
-    uint8_t* bufs = epi_base + (warp - 6) * 2 * EPI_BUF;
+    uint8_t* bufs = epi_base + (warp - EPI0) * 2 * EPI_BUF;
     int acc = 0, nbuf = 0;
     uint32_t acc_phase = 0;
     const int chunks = p.n_pad / p.epi_cols;
@@ -321,7 +318,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int row0 = t * BM + 32 * q;
       const long long k = (long long)row0 + lane;
       const bool row_ok = k < p.n_out;
-      IC_PROF(5, warp == 6 && lane == 0, mbar_wait(tfull + acc, acc_phase));
+      IC_PROF(5, warp == EPI0 && lane == 0, mbar_wait(tfull + acc, acc_phase));
       tc_after();
       for (int j = 0; j < chunks; ++j) {
         const int c0 = j * p.epi_cols;
@@ -367,7 +364,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
         }
         uint8_t* buf = bufs + nbuf * EPI_BUF;
-        if (lane == 0) IC_PROF(6, warp == 6, bulk_wait_read1());
+        if (lane == 0) IC_PROF(6, warp == EPI0, bulk_wait_read1());
         __syncwarp();
         if (ncol == 32) {
 #pragma unroll
@@ -465,10 +462,18 @@ extern "C" int32_t scb_conv_implicit(const void* features, int64_t n_in, int32_t
   p.b_tx = (uint32_t)(n_pad * p.kc * 2);
   p.a_off_bytes = r1024(p.a_tx);
   p.b_off_bytes = r1024(p.b_tx);
-  // several offsets per stage when one offset's chunk is small (~48 KB/stage)
-  int ops = (int)(49152u / (p.a_off_bytes + p.b_off_bytes));
+  // Launch shape (swept on the MinkUNet level-0 map, tools/ic_sweep.py): two
+  // CTAs per SM whenever both fit in TMEM (C_out <= 128) -- the producer loop
+  // is latency-bound, so a second CTA's pipeline fills the gaps -- with ~32 KB
+  // stages; a single CTA with ~48 KB stages otherwise.
+  int ctas = cols <= 256 ? 2 : 1;
+  if (const char* e = getenv("SCB_IMPLICIT_CTAS")) ctas = atoi(e) == 2 ? 2 : 1;
+  if (cols > 256) ctas = 1;                   // two CTAs must both fit in TMEM
+  // several offsets per stage when one offset's chunk is small
+  int ops = (int)((ctas == 2 ? 32768u : 49152u) / (p.a_off_bytes + p.b_off_bytes));
   ops = ops < 1 ? 1 : (ops > MAX_OPS ? MAX_OPS : ops);
   if (ops > volume) ops = volume;
+  if (const char* e = getenv("SCB_IMPLICIT_OPS")) ops = std::max(1, std::min(atoi(e), std::min(MAX_OPS, volume)));
   p.ops = ops;
   p.groups = (volume + ops - 1) / ops;
   p.a_stage_bytes = ops * p.a_off_bytes;
@@ -482,15 +487,23 @@ extern "C" int32_t scb_conv_implicit(const void* features, int64_t n_in, int32_t
   p.bias = bias;
   p.residual = (const __half*)residual;
   if (const char* dbg = getenv("SCB_IMPLICIT_DEBUG")) p.debug = atoi(dbg);
-  const int smem_cap = 227 * 1024;
+  const int smem_cap = ctas == 2 ? 113 * 1024 : 227 * 1024;
   const int fixed = 1024 + EPI_BYTES + 2 * volume * BM * 4 + 16 * MAX_OPS * 4 + 40 * 8 + 64 +
-                    16 * BM;  // wmask
+                    16 * MAX_P * BM;  // wmask
   int stages = (smem_cap - fixed) / (int)p.stage_bytes;
   if (stages > 16) stages = 16;
   SCB_CHECK_ARG(stages >= 2, "stage does not fit in shared memory");
   p.stages = stages;
   const int smem = fixed + stages * (int)p.stage_bytes;
-  const int lag = stages >= 9 ? 8 : (stages >= 5 ? 4 : (stages >= 3 ? 2 : 1));
+  // cp.async groups a producer leaves in flight before signalling a stage
+  // full: arriving as early as possible measured best (the other CTA / later
+  // stages keep loads in flight)
+  int lag = ctas == 2 ? 0 : 1;
+  if (const char* e = getenv("SCB_IMPLICIT_LAG")) {
+    const int l = atoi(e);
+    lag = l >= 8 ? 8 : (l >= 4 ? 4 : (l >= 2 ? 2 : (l >= 1 ? 1 : 0)));
+    while (lag >= stages) lag = lag / 2;
+  }
 
   CUtensorMap mB, mO;
   std::string err;
@@ -501,25 +514,29 @@ extern "C" int32_t scb_conv_implicit(const void* features, int64_t n_in, int32_t
     set_error(std::string("scb_conv_implicit: ") + err);
     return SCB_ECUDA;
   }
-  const int grid = p.total_tiles < device_sms() ? p.total_tiles : device_sms();
+  const int grid = p.total_tiles < ctas * device_sms() ? p.total_tiles : ctas * device_sms();
   cudaStream_t s = as_stream(stream);
-  auto launch = [&](auto kernel) -> int {
+  auto launch = [&](auto kernel, int threads) -> int {
     SCB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_cap));
-    kernel<<<grid, THREADS, smem, s>>>(mB, mO, p);
+    kernel<<<grid, threads, smem, s>>>(mB, mO, p);
     return SCB_OK;
   };
   int rc = SCB_EINVAL;
+#define SCB_IC_LAUNCH_P(VV, KK, MB)                                                         \
+  rc = lag == 8 ? launch(implicit_conv_f16_kernel<VV, 8, KK, 1, MB>, 320)                 \
+       : lag == 4 ? launch(implicit_conv_f16_kernel<VV, 4, KK, 1, MB>, 320)               \
+       : lag == 2 ? launch(implicit_conv_f16_kernel<VV, 2, KK, 1, MB>, 320)               \
+       : lag == 1 ? launch(implicit_conv_f16_kernel<VV, 1, KK, 1, MB>, 320)               \
+                  : launch(implicit_conv_f16_kernel<VV, 0, KK, 1, MB>, 320)
 #define SCB_IC_LAUNCH(VV, KK)                                                               \
-  rc = lag == 8 ? launch(implicit_conv_f16_kernel<VV, 8, KK>)                             \
-       : lag == 4 ? launch(implicit_conv_f16_kernel<VV, 4, KK>)                           \
-       : lag == 2 ? launch(implicit_conv_f16_kernel<VV, 2, KK>)                           \
-                  : launch(implicit_conv_f16_kernel<VV, 1, KK>)
+  if (ctas == 2) SCB_IC_LAUNCH_P(VV, KK, 2); else SCB_IC_LAUNCH_P(VV, KK, 1)
   if (volume == 27) {
     if (p.kc == 64) SCB_IC_LAUNCH(27, 64); else if (p.kc == 32) SCB_IC_LAUNCH(27, 32); else SCB_IC_LAUNCH(27, 16);
   } else if (volume == 8) {
     if (p.kc == 64) SCB_IC_LAUNCH(8, 64); else if (p.kc == 32) SCB_IC_LAUNCH(8, 32); else SCB_IC_LAUNCH(8, 16);
   }
 #undef SCB_IC_LAUNCH
+#undef SCB_IC_LAUNCH_P
   if (rc == SCB_EINVAL) set_error("scb_conv_implicit: V must be 8 or 27");
   if (rc != SCB_OK) return rc;
   if (p.debug & 16) {

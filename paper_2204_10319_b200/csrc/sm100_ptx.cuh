@@ -117,6 +117,21 @@ __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32
                "r"(src_size)
                : "memory");
 }
+// Predicated forms (no branch / reconvergence around each copy).
+__device__ __forceinline__ void cp_async16_if(uint32_t dst, const void* src, bool p) {
+  asm volatile(
+      "{ .reg .pred q; setp.ne.b32 q, %2, 0;\n"
+      "  @q cp.async.cg.shared.global [%0], [%1], 16; }" ::"r"(dst),
+      "l"(src), "r"((int)p)
+      : "memory");
+}
+__device__ __forceinline__ void st_zero16_if(uint32_t dst, bool p) {
+  asm volatile(
+      "{ .reg .pred q; setp.ne.b32 q, %1, 0;\n"
+      "  @q st.shared.v4.u32 [%0], {%2, %2, %2, %2}; }" ::"r"(dst),
+      "r"((int)p), "r"(0)
+      : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {

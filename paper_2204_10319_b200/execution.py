@@ -500,12 +500,12 @@ def choose_dataflow(opts: ExecOptions, dtype, kmap: KernelMap, w: WeightTensor) 
         return "staged"
     if opts.dataflow == "fused":
         return "fused"
-    # Measured on B200 (tools/fused_probe.py, 1M-voxel level-0 layer, k3):
-    # fused/staged = 0.56/1.0 ms at C=32, 1.74/2.68 at C=96 -> fused; 1.48/1.19
-    # at C=64, 2.6/2.1 at 128->96, 7.8/7.3 at 256 -> staged.  The fused
-    # producer is instruction-bound per 16-B chunk (absent rows included), so
-    # it wins where rows are short.
-    return "fused" if w.c_in <= 32 or (w.c_in % 64 != 0 and w.c_in <= 96) else "staged"
+    # Measured on B200 per MinkUNet layer (tools/layer_compare.py, 8 packed
+    # scans): fused wins every layer with C_out <= 128 (two CTAs per SM fit
+    # in TMEM), e.g. 32->32 0.17/0.27 ms, 96->96 1.33/1.77, 192->128
+    # 0.49/0.52; staged wins at C_out = 256 (0.35/0.43) and for 256->128
+    # (0.14/0.19), where the staged GEMM's wide tiles amortise better.
+    return "fused" if w.c_out <= 128 and w.c_in <= 192 else "staged"
 
 
 def _run_fused(features: torch.Tensor, kmap: KernelMap, w: WeightTensor, opts: ExecOptions,

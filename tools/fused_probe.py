@@ -25,16 +25,19 @@ def main():
     spec = sc.LayerSpec(k, s, cin, cout)
     for df in os.environ.get("DATAFLOWS", "staged,fused").split(","):
         opts = sc.ExecOptions(dataflow=df, index_kind="hash")
-        out = sc.sparse_conv_forward(t, w, spec, None, None, opts)  # warm + build map
-        torch.cuda.synchronize()
+        # warm (map build + clock ramp: >= 0.5 s of back-to-back launches)
+        t_end = time.time() + 0.5
+        while time.time() < t_end:
+            out = sc.sparse_conv_forward(t, w, spec, None, None, opts)
+            torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        for _ in range(5):
+        for _ in range(20):
             out = sc.sparse_conv_forward(t, w, spec, None, None, opts)
         e1.record()
         torch.cuda.synchronize()
         print(f"{df:7s} dbg={os.environ.get('SCB_IMPLICIT_DEBUG', '0')} N={c.shape[0]} "
-              f"C={cin}->{cout} K={k}: {e0.elapsed_time(e1) / 5:.3f} ms/layer", flush=True)
+              f"C={cin}->{cout} K={k}: {e0.elapsed_time(e1) / 20:.3f} ms/layer", flush=True)
 
 
 if __name__ == "__main__":
