@@ -3,20 +3,27 @@
 //
 //   out[k] = epilogue( sum_n  features[hits[n][k]] . W[n] )      (absent -> 0)
 //
-// for 128-row output tiles, accumulating all V offsets in TMEM.  The gather is
-// fused into the operand load: cp.async moves each present neighbour's 16-B
-// row chunks straight into the 128/64/32-B swizzled UMMA layout (absent
-// neighbours are zeroed with shared stores), so neither the gather buffer nor
-// the f32 partials ever reach HBM.  Each output row is written once (fp16)
-// with BN / bias / residual / ReLU applied in registers.  Offsets with no
-// neighbour anywhere in a tile skip their MMAs.  (A TMA tile::gather4 variant
-// was measured ~2-3x slower on this path: ~100 cycles per 4-row request.)
+// for super-tiles of T x 128 output rows, accumulating all V offsets in TMEM
+// (T accumulators, double-buffered).  The gather is fused into the operand
+// load: cp.async moves each present neighbour's 16-B row chunks straight into
+// the 128/64/32-B swizzled UMMA layout (absent neighbours are zero), so neither
+// the gather buffer nor the f32 partials ever reach HBM.  Each weight slice
+// W[n][k-chunk] is brought in by TMA once per super-tile and feeds T MMAs
+// (weight re-streaming from L2 was the measured limit at T = 1: a 96->96 k3
+// layer reloads 486 KB of weights per 128 rows).  Each output row is written
+// once (fp16) with BN / bias / residual / ReLU applied in registers.  Offsets
+// with no neighbour in a tile skip that tile's MMAs.
 //
-// Warp roles (64 + 128 P + 128 threads, 1 CTA / SM, persistent over
-// contiguous tile ranges; P = 1 A-producer group):
+// Producers never block on their own copies: each thread's stage completion
+// is tracked by cp.async.mbarrier.arrive.noinc (LAG < 0), so the copy loop
+// runs ahead as far as free stages allow.  (LAG >= 0: the older
+// wait_group<LAG> + arrive scheme, kept for comparison.)
+//
+// Warp roles (64 + 128 T + 128 threads, persistent over contiguous
+// super-tile ranges):
 //   warp 0        TMA producer of the weight slices (B, K-major fp16)
 //   warp 1        TMEM allocator + single-thread tcgen05.mma issuer
-//   warps 2..     A producers: neighbour indices one tile ahead, cp.async gather
+//   warps 2..     A producers: thread (h, r) owns row r of tile h
 //   last 4 warps  epilogue: tcgen05.ld -> epilogue -> swizzled smem -> TMA store
 #include <cuda.h>
 
@@ -33,7 +40,7 @@ namespace ic {
 using namespace ::scb::ptx;
 
 constexpr int BM = 128;
-constexpr int MAX_P = 1;                // A-producer groups
+constexpr int MAX_T = 4;                // tiles per super-tile
 constexpr int EPI_BUF = 32 * 64;        // 32 rows x 64 B (32 fp16 columns)
 constexpr int EPI_BYTES = 4 * 2 * EPI_BUF;
 constexpr int MAX_OPS = 8;              // kernel offsets per pipeline stage
@@ -43,10 +50,10 @@ struct Params {
   long long n_out;
   int n_in, c_in, c_out, V, n_pad, kc, n_kchunks, stages, swz, epi_cols, total_tiles, relu;
   int ops;                  // offsets per stage (small C_in -> several)
-  int debug;                // SCB_IMPLICIT_DEBUG: 1 no A loads, 2 no MMAs, 16 wait counters
-  int groups;               // ceil(V / ops) offset groups per tile
+  int debug;                // SCB_IMPLICIT_DEBUG: 1 no A loads, 2 no MMAs, 16 wait counters, 32 no B loads
+  int groups;               // ceil(V / ops) offset groups per super-tile
   uint32_t idesc, tmem_cols;
-  uint32_t a_off_bytes;     // one offset's A block [128 rows][kc] (1024-aligned)
+  uint32_t a_off_bytes;     // one (offset, tile) A block [128 rows][kc] (1024-aligned)
   uint32_t b_off_bytes;     // one offset's B block [n_pad][kc]   (1024-aligned)
   uint32_t a_stage_bytes, stage_bytes;
   uint32_t a_tx, b_tx;      // bytes one offset's A / B loads deliver
@@ -83,25 +90,29 @@ __device__ __forceinline__ uint32_t pack_half2(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
-template <int V, int LAG, int KC, int P, int MINB>
-__global__ void __launch_bounds__(64 + 128 * P + 128, MINB)
+__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+template <int V, int LAG, int KC, int T, int COAL, int MINB>
+__global__ void __launch_bounds__(64 + 128 * T + 128, MINB)
     implicit_conv_f16_kernel(const __grid_constant__ CUtensorMap tmB,
                              const __grid_constant__ CUtensorMap tmOut,
                              const __grid_constant__ Params p) {
-  constexpr int NPROD = 128 * P;           // A-producer threads
-  constexpr int EPI0 = 2 + 4 * P;          // first epilogue warp
-  constexpr int NT = (V + P - 1) / P;      // offsets per producer thread
+  constexpr int NPROD = 128 * T;           // A-producer threads (one per super-tile row)
+  constexpr int EPI0 = 2 + 4 * T;          // first epilogue warp
+  constexpr bool NOINC = LAG < 0;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* epi_base = smem + (size_t)p.stages * p.stage_bytes;
-  int* nbr_s = (int*)(epi_base + EPI_BYTES);                      // [2][V][128]
-  uint32_t* flags = (uint32_t*)(nbr_s + 2 * V * BM);              // [stages][MAX_OPS]
-  uint64_t* full = (uint64_t*)(flags + p.stages * MAX_OPS);
+  int* nbr_s = (int*)(epi_base + EPI_BYTES);                      // [1 + COAL][V][NPROD]
+  uint32_t* flags = (uint32_t*)(nbr_s + (1 + COAL) * V * NPROD);  // [stages][MAX_OPS][T]
+  uint64_t* full = (uint64_t*)(flags + p.stages * MAX_OPS * T);
   uint64_t* empty = full + p.stages;
   uint64_t* tfull = empty + p.stages;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
-  uint8_t* wmask = (uint8_t*)(tmem_slot + 4);  // [stages][P][128]: blocks each row holds data in
+  uint32_t* wmask = tmem_slot + 4;  // [stages][NPROD]: blocks each thread's items hold data in
 
   const long long k_t0 = clock64();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -110,7 +121,8 @@ __global__ void __launch_bounds__(64 + 128 * P + 128, MINB)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < p.stages; ++s) {
-      mbar_init(full + s, NPROD + 1);  // A-producer threads + the B expect_tx arrive
+      // producers: one (async, noinc) arrive per thread + the B expect_tx arrive
+      mbar_init(full + s, NPROD + 1);
       mbar_init(empty + s, 1);
     }
     for (int a = 0; a < 2; ++a) {
@@ -141,171 +153,225 @@ __global__ void __launch_bounds__(64 + 128 * P + 128, MINB)
         for (int g = 0; g < p.groups; ++g) {
           const int nv = min(p.ops, p.V - g * p.ops);
           for (int kk = 0; kk < p.n_kchunks; ++kk) {
-            IC_PROF(2, true, mbar_wait(empty + stage, phase ^ 1));
-            mbar_expect_tx(full + stage, nv * p.b_tx);
-            uint8_t* sb = smem + (size_t)stage * p.stage_bytes + p.a_stage_bytes;
-            for (int o = 0; o < nv; ++o)
-              tma_load_2d(sb + o * p.b_off_bytes, &tmB, full + stage, kk * p.kc,
-                          (g * p.ops + o) * p.n_pad);
+            IC_PROF(2, true, mbar_wait_sleep(empty + stage, phase ^ 1, 32));
+            if (p.debug & 32) {
+              mbar_arrive(full + stage);
+            } else {
+              mbar_expect_tx(full + stage, nv * p.b_tx);
+              uint8_t* sb = smem + (size_t)stage * p.stage_bytes + p.a_stage_bytes;
+              for (int o = 0; o < nv; ++o)
+                tma_load_2d(sb + o * p.b_off_bytes, &tmB, full + stage, kk * p.kc,
+                            (g * p.ops + o) * p.n_pad);
+            }
             if (++stage == p.stages) { stage = 0; phase ^= 1; }
           }
         }
     }
   } else if (warp >= 2 && warp < EPI0) {
-    // ============ A producers (P groups of 128 threads).  Thread (h, r) owns
-    // output row r of the tile for the offsets n = h (mod P): it prefetches
-    // those neighbour rows one tile ahead (registers), parks them in the
-    // shared table and computes the per-offset "any neighbour" flags, then
-    // copies its row of each of its offset blocks: one index read and one
-    // 64-bit address per row, CPR predicated 16-B cp.async (present) or zero
-    // stores (absent) with immediate chunk offsets.  Two groups put two
-    // producer warps on every scheduler: the copy loop is latency-bound per
-    // warp, not bandwidth-bound.  (Spreading a row's chunks over consecutive
-    // lanes coalesces better but costs ~4x the instructions; measured slower.)
+    // ============ A producers.  Thread (h, r) owns output row r of tile h of
+    // the super-tile: it prefetches its neighbour rows one super-tile ahead
+    // (registers), parks them in its private smem slots, and copies its row
+    // of every (offset, k-chunk) block: CPR predicated 16-B cp.async
+    // (present) or zero stores (absent, only where the slot held data).
     const int pt = threadIdx.x - 64;
     const int row = pt & (BM - 1);
-    const int h = pt >> 7;
+    const int h = (pt >> 7) % T;
     const int wbyte = (pt >> 5) & 3;
     constexpr int CPR = KC / 8;               // 16-B chunks per row per K chunk
     constexpr int SWZ = KC * 2;               // swizzle span = row bytes
-    int nxt[NT];
+    int nxt[V];
     {
-      const long long k = (long long)t_begin * BM + row;
+      const long long k = ((long long)t_begin * T + h) * BM + row;
 #pragma unroll
-      for (int i = 0; i < NT; ++i) {
-        const int n = h + i * P;
-        nxt[i] = (n < V && t_begin < t_end && k < p.n_out) ? __ldg(p.hits + (long long)n * p.ldh + k) : -1;
-      }
+      for (int n = 0; n < V; ++n)
+        nxt[n] = (t_begin < t_end && k < p.n_out) ? __ldg(p.hits + (long long)n * p.ldh + k) : -1;
     }
-    // zero every A block once; afterwards only rows whose presence changed
-    // are rewritten (see the stage loop)
     for (int s = 0; s < p.stages; ++s) {
       const uint32_t base = smem_u32(smem + (size_t)s * p.stage_bytes);
       for (uint32_t b = (uint32_t)pt * 16u; b < p.a_stage_bytes; b += NPROD * 16u)
         asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(base + b), "r"(0) : "memory");
-      wmask[(s * P + h) * BM + row] = 0;
+      wmask[s * NPROD + pt] = 0u;
     }
     asm volatile("bar.sync 1, %0;" ::"n"(NPROD) : "memory");
     int stage = 0, sig = 0, pending = 0;
     uint32_t phase = 0;
-    const uint32_t nbr_base = smem_u32(nbr_s);
+    const uint32_t nb_s0 = smem_u32(nbr_s);
+    const uint32_t nb_s = nb_s0 + (uint32_t)pt * 4u;
     const int rx = SWZ == 128 ? (row & 7) : (SWZ == 64 ? ((row >> 1) & 3) : ((row >> 2) & 1));
-    for (int t = t_begin, buf = 0; t < t_end; ++t, buf ^= 1) {
-      int* nb = nbr_s + buf * V * BM;
-      const uint32_t nb_s = nbr_base + (uint32_t)(buf * V * BM * 4);
-      uint32_t anymask = 0;
+    const int cr = row / CPR, cc = row % CPR;   // COAL: row group / chunk of this lane
+    uint32_t roff[CPR];                         // COAL: smem offset of item it in a block
 #pragma unroll
-      for (int i = 0; i < NT; ++i) {
-        const int n = h + i * P;
-        if (n < V) {
-          nb[n * BM + row] = nxt[i];
-          if (__any_sync(0xffffffffu, nxt[i] >= 0)) anymask |= 1u << n;
-        }
+    for (int it = 0; it < CPR; ++it) {
+      const int r = it * (BM / CPR) + cr;
+      const int rxr = SWZ == 128 ? (r & 7) : (SWZ == 64 ? ((r >> 1) & 3) : ((r >> 2) & 1));
+      roff[it] = (uint32_t)(r * (KC * 2)) + ((uint32_t)(cc ^ rxr) << 4);
+    }
+    const uint32_t ldfb = (uint32_t)(p.ldf * 2);  // feature row stride in bytes (host-checked < 2^32)
+    int cbuf = 0;
+    for (int t = t_begin; t < t_end; ++t) {
+      const uint32_t nbw = COAL ? nb_s + (uint32_t)(cbuf * V * NPROD * 4) : nb_s;
+#pragma unroll
+      for (int n = 0; n < V; ++n) {
+        asm volatile("st.shared.b32 [%0], %1;" ::"r"(nbw + (uint32_t)(n * NPROD * 4)), "r"(nxt[n]) : "memory");
       }
-      asm volatile("bar.sync 1, %0;" ::"n"(NPROD) : "memory");  // the tile's index table is complete
+      // COAL: rows are copied by other threads; the double-buffered table
+      // needs one producer barrier per tile
+      if constexpr (COAL) asm volatile("bar.sync 1, %0;" ::"n"(NPROD) : "memory");
       {
-        const long long k = (long long)(t + 1) * BM + row;
+        const long long k = ((long long)(t + 1) * T + h) * BM + row;
         const bool ok = (t + 1 < t_end) && k < p.n_out;
 #pragma unroll
-        for (int i = 0; i < NT; ++i) {
-          const int n = h + i * P;
-          nxt[i] = (ok && n < V) ? __ldg(p.hits + (long long)n * p.ldh + k) : -1;
-        }
+        for (int n = 0; n < V; ++n) nxt[n] = ok ? __ldg(p.hits + (long long)n * p.ldh + k) : -1;
       }
       for (int g = 0; g < p.groups; ++g) {
         const int nv = min(p.ops, V - g * p.ops);
         for (int kk = 0; kk < p.n_kchunks; ++kk) {
           IC_PROF(0, pt == 0, mbar_wait(empty + stage, phase ^ 1));
-          if (lane == 0)
-            for (int o = 0; o < nv; ++o)
-              if ((g * p.ops + o) % P == h)
-                reinterpret_cast<uint8_t*>(flags + stage * MAX_OPS + o)[wbyte] =
-                    (anymask >> (g * p.ops + o)) & 1u;
+          const long long a_t0 = clock64();
           const uint32_t dst = smem_u32(smem + (size_t)stage * p.stage_bytes);
           const int col0 = kk * KC;
           const int live = min(CPR, (p.c_in - col0) / 8);  // chunks inside C_in
-          // Stage buffers start zeroed and this thread alone owns row `row` of
-          // its blocks, so it only writes what changes: present -> copy;
-          // absent but written by the slot's previous use -> re-zero;
-          // absent and already zero -> nothing (most rows: |M|/(V*N) ~ 0.28).
-          // Chunks past C_in are never written, so they stay zero.
-          uint8_t* wm = wmask + (stage * P + h) * BM + row;
+          // Stage buffers start zeroed and each 16-B item of a block has one
+          // owner thread, so a thread only writes what changes: present ->
+          // copy; absent but written by the slot's previous use -> re-zero;
+          // absent and already zero -> nothing.  Chunks past C_in stay zero.
+          uint32_t* wm = wmask + stage * NPROD + pt;
           uint32_t now = *wm;
-          for (int o = 0; o < nv; ++o) {
-            const int n = g * p.ops + o;
-            if (n % P != h) continue;
-            int j;
-            asm volatile("ld.shared.b32 %0, [%1];" : "=r"(j) : "r"(nb_s + (uint32_t)((n * BM + row) * 4)));
-            const bool present = j >= 0 && !(p.debug & 1);
-            const bool rezero = !present && ((now >> o) & 1u);
-            const uint32_t base = dst + o * p.a_off_bytes + row * (KC * 2);
-            const __half* src = p.feat + (long long)max(j, 0) * p.ldf + col0;
+          if constexpr (COAL) {
+            // lane-per-chunk: the CPR lanes of a row copy its consecutive
+            // 16-B chunks (one warp instruction touches 32 / CPR rows).  An
+            // offset's CPR index loads go first (volatile asm keeps the order)
+            // so their latencies overlap; then one IMAD.WIDE per copy.
+            const uint32_t nbc = nb_s0 + (uint32_t)(cbuf * V * NPROD * 4) +
+                                 (uint32_t)((g * p.ops * NPROD + h * BM + cr) * 4);
+            const uint64_t fbase = reinterpret_cast<uint64_t>(p.feat) + (uint64_t)((col0 + cc * 8) * 2);
+            const bool live_c = cc < live && !(p.debug & 1);
+            for (int o = 0; o < nv; ++o) {
+              int jj[CPR];
 #pragma unroll
-            for (int c = 0; c < CPR; ++c) {
-              const uint32_t d = base + ((uint32_t)(c ^ rx) << 4);
-              cp_async16_if(d, src + c * 8, present && c < live);
-              st_zero16_if(d, rezero && c < live);
+              for (int it = 0; it < CPR; ++it)
+                asm volatile("ld.shared.b32 %0, [%1];" : "=r"(jj[it]) : "r"(nbc + (uint32_t)((o * NPROD + it * (BM / CPR)) * 4)));
+              const uint32_t blk = dst + (o * T + h) * p.a_off_bytes;
+#pragma unroll
+              for (int it = 0; it < CPR; ++it) {
+                const int j = jj[it];
+                const bool present = j >= 0;
+                constexpr int MAXO = (32 / CPR) < MAX_OPS ? (32 / CPR) : MAX_OPS;
+                const uint32_t bit = 1u << (it * MAXO + o);
+                const bool rezero = !present && (now & bit);
+                const void* src = reinterpret_cast<const void*>(
+                    fbase + (uint64_t)(uint32_t)max(j, 0) * (uint64_t)ldfb);
+                cp_async16_zfill_if(blk + roff[it], src, present, (present || rezero) && live_c);
+                now = present ? (now | bit) : (now & ~bit);
+              }
             }
-            now = (now & ~(1u << o)) | ((uint32_t)present << o);
+          } else {
+            for (int o = 0; o < nv; ++o) {
+              const int n = g * p.ops + o;
+              int j;
+              asm volatile("ld.shared.b32 %0, [%1];" : "=r"(j) : "r"(nb_s + (uint32_t)(n * NPROD * 4)));
+              const bool present = j >= 0 && !(p.debug & 1);
+              const bool rezero = !present && ((now >> o) & 1u);
+              const uint32_t base = dst + (o * T + h) * p.a_off_bytes + row * (KC * 2);
+              const __half* src = p.feat + (long long)max(j, 0) * p.ldf + col0;
+#pragma unroll
+              for (int c = 0; c < CPR; ++c) {
+                const uint32_t d = base + ((uint32_t)(c ^ rx) << 4);
+                if constexpr (NOINC) {
+                  // absent rows: zero-size cp.async zero-fills without a read,
+                  // so every write of the stage is tracked by the async arrive
+                  cp_async16_zfill_if(d, src + c * 8, present, (present || rezero) && c < live);
+                } else {
+                  cp_async16_if(d, src + c * 8, present && c < live);
+                  st_zero16_if(d, rezero && c < live);
+                }
+              }
+              now = (now & ~(1u << o)) | ((uint32_t)present << o);
+            }
           }
-          *wm = (uint8_t)now;
-          cp_async_commit();
-          if (++pending > LAG) {
-            IC_PROF(1, pt == 0, cp_async_wait<LAG>());
-            if (!(p.debug & 4)) fence_async_smem();  // generic -> async proxy
-            mbar_arrive(full + sig);
-            if (++sig == p.stages) sig = 0;
-            --pending;
+          *wm = now;
+          if ((p.debug & 16) && blockIdx.x == 0 && pt == 0) atomicAdd(&g_ic_prof[11], (unsigned long long)(clock64() - a_t0));
+          if constexpr (NOINC) {
+            cp_async_arrive_noinc(full + stage);   // fires when this thread's copies land
+          } else {
+            cp_async_commit();
+            if (++pending > LAG) {
+              IC_PROF(1, pt == 0, cp_async_wait<(LAG < 0 ? 0 : LAG)>());
+              fence_async_smem();  // generic -> async proxy
+              mbar_arrive(full + sig);
+              if (++sig == p.stages) sig = 0;
+              --pending;
+            }
           }
           if (++stage == p.stages) { stage = 0; phase ^= 1; }
         }
       }
+      cbuf ^= COAL;
     }
-    cp_async_wait<0>();
-    fence_async_smem();
-    while (pending > 0) {
-      mbar_arrive(full + sig);
-      if (++sig == p.stages) sig = 0;
-      --pending;
+    if constexpr (!NOINC) {
+      cp_async_wait<0>();
+      fence_async_smem();
+      while (pending > 0) {
+        mbar_arrive(full + sig);
+        if (++sig == p.stages) sig = 0;
+        --pending;
+      }
     }
   } else if (warp == 1) {
-    // ============ MMA issuer
-    if (lane == 0) {
-      const uint32_t layout = p.swz == 128 ? 2u : (p.swz == 64 ? 4u : 6u);
-      const uint32_t sbo = 8u * (uint32_t)p.swz;
-      int stage = 0, acc = 0;
-      uint32_t phase = 0, acc_phase = 0;
-      for (int t = t_begin; t < t_end; ++t) {
-        IC_PROF(4, true, mbar_wait(tempty + acc, acc_phase ^ 1));
-        tc_after();
-        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * p.n_pad);
-        uint32_t issued = 0;
-        for (int g = 0; g < p.groups; ++g) {
-          for (int kk = 0; kk < p.n_kchunks; ++kk) {
-            IC_PROF(3, true, mbar_wait(full + stage, phase));
+    // ============ MMA issuer.  The whole warp runs the loop (so stage
+    // indices and descriptors stay warp-uniform, in uniform registers) and
+    // one elected lane issues.  Every (offset, tile) block of a stage is
+    // multiplied (a tile rarely lacks an offset entirely, and the per-block
+    // test cost more issue time than the MMAs it saved); stage descriptors
+    // advance by constant steps, so the loop body is the MMAs.
+    const uint32_t layout = p.swz == 128 ? 2u : (p.swz == 64 ? 4u : 6u);
+    const uint32_t sbo = 8u * (uint32_t)p.swz;
+    const uint64_t adesc_base = make_sdesc(smem_u32(smem), sbo, layout);
+    const uint32_t stage_d = p.stage_bytes >> 4, a_stage_d = p.a_stage_bytes >> 4;
+    const uint32_t a_off_d = p.a_off_bytes >> 4, b_off_d = p.b_off_bytes >> 4;
+    const uint32_t idesc = p.idesc, n_pad = p.n_pad;
+    const uint32_t tmem0 = __shfl_sync(0xffffffffu, tmem_base, 0);
+    int stage = 0, acc = 0;
+    uint32_t phase = 0, acc_phase = 0;
+    for (int t = t_begin; t < t_end; ++t) {
+      IC_PROF(4, lane == 0, mbar_wait(tempty + acc, acc_phase ^ 1));
+      tc_after();
+      const uint32_t d0 = tmem0 + (uint32_t)acc * T * n_pad;
+      for (int g = 0; g < p.groups; ++g) {
+        const int nv = min(p.ops, V - g * p.ops);
+        for (int kk = 0; kk < p.n_kchunks; ++kk) {
+          IC_PROF(3, lane == 0, mbar_wait(full + stage, phase));
+          const long long m_t0 = clock64();
+          const uint64_t ad = adesc_base + (uint64_t)(stage * stage_d);
+          const uint64_t bd = ad + a_stage_d;
+          const uint32_t acc0 = (g | kk) ? 1u : 0u;
+          if (elect_one()) {
+            if (!(p.debug & 64)) fence_async_smem();  // cp.async (generic proxy) data -> tcgen05 reads
             tc_after();
-            const uint32_t sa = smem_u32(smem + (size_t)stage * p.stage_bytes);
-            const uint32_t sb = sa + p.a_stage_bytes;
-            for (int o = 0; o < p.ops; ++o) {
-              const int n = g * p.ops + o;
-              if (n >= V) break;
-              const bool valid = flags[stage * MAX_OPS + o] != 0u;
-              if (!(valid || (!issued && n == V - 1))) continue;
-              if ((p.debug & 2) && issued) continue;
-              const uint32_t ao = sa + o * p.a_off_bytes, bo = sb + o * p.b_off_bytes;
-              for (int k = 0; k < p.kc / 16; ++k) {
-                mma_f16(d_tmem, make_sdesc(ao + k * 32, sbo, layout),
-                        make_sdesc(bo + k * 32, sbo, layout), p.idesc, issued);
-                issued = 1;
+#pragma unroll
+            for (int o = 0; o < MAX_OPS; ++o) {
+              if (o < nv) {
+#pragma unroll
+                for (int h = 0; h < T; ++h) {
+                  const uint64_t a = ad + (uint64_t)((o * T + h) * a_off_d);
+                  const uint64_t b = bd + (uint64_t)(o * b_off_d);
+                  const uint32_t d = d0 + h * n_pad;
+                  mma_f16(d, a, b, idesc, o ? 1u : acc0);
+#pragma unroll
+                  for (int k = 1; k < KC / 16; ++k) mma_f16(d, a + 2u * k, b + 2u * k, idesc, 1u);
+                }
               }
             }
             mma_commit(empty + stage);
-            if (++stage == p.stages) { stage = 0; phase ^= 1; }
+            if ((p.debug & 16) && blockIdx.x == 0) atomicAdd(&g_ic_prof[10], (unsigned long long)(clock64() - m_t0));
           }
+          __syncwarp();
+          if (++stage == p.stages) { stage = 0; phase ^= 1; }
         }
-        mma_commit(tfull + acc);
-        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
+      if (elect_one()) mma_commit(tfull + acc);
+      __syncwarp();
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
   } else if (warp >= EPI0) {
     // ============ epilogue
@@ -315,79 +381,82 @@ __global__ void __launch_bounds__(64 + 128 * P + 128, MINB)
     uint32_t acc_phase = 0;
     const int chunks = p.n_pad / p.epi_cols;
     for (int t = t_begin; t < t_end; ++t) {
-      const int row0 = t * BM + 32 * q;
-      const long long k = (long long)row0 + lane;
-      const bool row_ok = k < p.n_out;
-      IC_PROF(5, warp == EPI0 && lane == 0, mbar_wait(tfull + acc, acc_phase));
+      IC_PROF(5, warp == EPI0 && lane == 0, mbar_wait_sleep(tfull + acc, acc_phase, 256));
       tc_after();
-      for (int j = 0; j < chunks; ++j) {
-        const int c0 = j * p.epi_cols;
-        const uint32_t taddr =
-            tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * p.n_pad + c0);
-        uint32_t r[32];
-        TMEM_LD_X16(taddr, r);
-        if (p.epi_cols == 32) TMEM_LD_X16(taddr + 16, (r + 16));
-        tmem_wait_ld();
-        float v[32];
+      for (int h = 0; h < T; ++h) {
+        const long long row0 = ((long long)t * T + h) * BM + 32 * q;
+        if (row0 >= p.n_out) break;
+        const long long k = row0 + lane;
+        const bool row_ok = k < p.n_out;
+        for (int j = 0; j < chunks; ++j) {
+          const int c0 = j * p.epi_cols;
+          const uint32_t taddr = tmem_base + ((uint32_t)(32 * q) << 16) +
+                                 (uint32_t)((acc * T + h) * p.n_pad + c0);
+          uint32_t r[32];
+          TMEM_LD_X16(taddr, r);
+          if (p.epi_cols == 32) TMEM_LD_X16(taddr + 16, (r + 16));
+          tmem_wait_ld();
+          float v[32];
 #pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-        const int ncol = p.epi_cols;
-        if (p.scale) {
+          for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+          const int ncol = p.epi_cols;
+          if (p.scale) {
 #pragma unroll
-          for (int i = 0; i < 32; ++i)
-            if (i < ncol && c0 + i < p.c_out)
-              v[i] = v[i] * __ldg(p.scale + c0 + i) + __ldg(p.shift + c0 + i);
-        }
-        if (p.bias) {
+            for (int i = 0; i < 32; ++i)
+              if (i < ncol && c0 + i < p.c_out)
+                v[i] = v[i] * __ldg(p.scale + c0 + i) + __ldg(p.shift + c0 + i);
+          }
+          if (p.bias) {
 #pragma unroll
-          for (int i = 0; i < 32; ++i)
-            if (i < ncol && c0 + i < p.c_out) v[i] += __ldg(p.bias + c0 + i);
-        }
-        if (p.residual && row_ok) {
-          const uint4* rp = reinterpret_cast<const uint4*>(p.residual + k * p.c_out + c0);
+            for (int i = 0; i < 32; ++i)
+              if (i < ncol && c0 + i < p.c_out) v[i] += __ldg(p.bias + c0 + i);
+          }
+          if (p.residual && row_ok) {
+            const uint4* rp = reinterpret_cast<const uint4*>(p.residual + k * p.c_out + c0);
 #pragma unroll
-          for (int g = 0; g < 4; ++g) {
-            if (g * 8 < ncol && c0 + g * 8 < p.c_out) {
-              const uint4 w = __ldg(rp + g);
-              const __half2* h = reinterpret_cast<const __half2*>(&w);
+            for (int g = 0; g < 4; ++g) {
+              if (g * 8 < ncol && c0 + g * 8 < p.c_out) {
+                const uint4 w = __ldg(rp + g);
+                const __half2* hh = reinterpret_cast<const __half2*>(&w);
 #pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const float2 f = __half22float2(h[e]);
-                v[g * 8 + 2 * e] += f.x;
-                v[g * 8 + 2 * e + 1] += f.y;
+                for (int e = 0; e < 4; ++e) {
+                  const float2 f = __half22float2(hh[e]);
+                  v[g * 8 + 2 * e] += f.x;
+                  v[g * 8 + 2 * e + 1] += f.y;
+                }
               }
             }
           }
-        }
-        if (p.relu) {
+          if (p.relu) {
 #pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
-        }
-        uint8_t* buf = bufs + nbuf * EPI_BUF;
-        if (lane == 0) IC_PROF(6, warp == EPI0, bulk_wait_read1());
-        __syncwarp();
-        if (ncol == 32) {
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            uint4 w = make_uint4(pack_half2(v[8 * c], v[8 * c + 1]), pack_half2(v[8 * c + 2], v[8 * c + 3]),
-                                 pack_half2(v[8 * c + 4], v[8 * c + 5]), pack_half2(v[8 * c + 6], v[8 * c + 7]));
-            *reinterpret_cast<uint4*>(buf + swz_off(lane, c, 64)) = w;
+            for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
           }
-        } else {
+          uint8_t* buf = bufs + nbuf * EPI_BUF;
+          if (lane == 0) IC_PROF(6, warp == EPI0, bulk_wait_read1());
+          __syncwarp();
+          if (ncol == 32) {
 #pragma unroll
-          for (int c = 0; c < 2; ++c) {
-            uint4 w = make_uint4(pack_half2(v[8 * c], v[8 * c + 1]), pack_half2(v[8 * c + 2], v[8 * c + 3]),
-                                 pack_half2(v[8 * c + 4], v[8 * c + 5]), pack_half2(v[8 * c + 6], v[8 * c + 7]));
-            *reinterpret_cast<uint4*>(buf + swz_off(lane, c, 32)) = w;
+            for (int c = 0; c < 4; ++c) {
+              uint4 w = make_uint4(pack_half2(v[8 * c], v[8 * c + 1]), pack_half2(v[8 * c + 2], v[8 * c + 3]),
+                                   pack_half2(v[8 * c + 4], v[8 * c + 5]), pack_half2(v[8 * c + 6], v[8 * c + 7]));
+              *reinterpret_cast<uint4*>(buf + swz_off(lane, c, 64)) = w;
+            }
+          } else {
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+              uint4 w = make_uint4(pack_half2(v[8 * c], v[8 * c + 1]), pack_half2(v[8 * c + 2], v[8 * c + 3]),
+                                   pack_half2(v[8 * c + 4], v[8 * c + 5]), pack_half2(v[8 * c + 6], v[8 * c + 7]));
+              *reinterpret_cast<uint4*>(buf + swz_off(lane, c, 32)) = w;
+            }
           }
+          fence_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&tmOut, buf, c0, (int)row0);
+            bulk_commit();
+          }
+          nbuf ^= 1;
         }
-        fence_async_smem();
-        __syncwarp();
-        if (lane == 0) {
-          tma_store_2d(&tmOut, buf, c0, row0);
-          bulk_commit();
-        }
-        nbuf ^= 1;
       }
       tc_before();
       __syncwarp();
@@ -432,6 +501,7 @@ extern "C" int32_t scb_conv_implicit(const void* features, int64_t n_in, int32_t
   SCB_CHECK_ARG(volume == 8 || volume == 27, "implicit conv supports K^3 = 8 or 27 offsets");
   SCB_CHECK_ARG(c_in % 8 == 0 && ldf % 8 == 0, "C_in and its row stride must be multiples of 8");
   SCB_CHECK_ARG(c_out % 8 == 0, "C_out must be a multiple of 8");
+  SCB_CHECK_ARG(ldf * 2 < (1LL << 32), "feature row stride too large");
   SCB_CHECK_ARG((scale == nullptr) == (shift == nullptr), "scale and shift go together");
   SCB_CHECK_ARG(n_in < (1LL << 31) - 1 && (long long)volume * hits_ld(n_out) < (1LL << 31),
                 "too many rows for 32-bit TMA coordinates");
@@ -451,33 +521,41 @@ extern "C" int32_t scb_conv_implicit(const void* features, int64_t n_in, int32_t
   p.swz = p.kc * 2;
   p.n_kchunks = k_pad / p.kc;
   p.epi_cols = (n_pad % 32 == 0) ? 32 : 16;
-  p.total_tiles = (int)((n_out + BM - 1) / BM);
   p.relu = relu;
   p.idesc = (1u << 4) | ((uint32_t)(n_pad >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+  auto env_int = [](const char* name, int dflt) {
+    const char* e = getenv(name);
+    return e ? atoi(e) : dflt;
+  };
+  // Launch shape.  T tiles share every weight slice load; T accumulators are
+  // double-buffered in TMEM (2 T n_pad columns <= 512), and two CTAs per SM
+  // run when both fit (their producer loops fill each other's gaps).
+  int T = 1;
+  T = env_int("SCB_IC_T", T);
+  T = T >= 4 ? 4 : (T >= 2 ? 2 : 1);
+  while (T > 1 && 2 * T * n_pad > 512) T /= 2;
   uint32_t cols = 32;
-  while (cols < (uint32_t)(2 * n_pad)) cols *= 2;
+  while (cols < (uint32_t)(2 * T * n_pad)) cols *= 2;
   p.tmem_cols = cols;
+  int ctas = (cols <= 256 && T <= 2) ? 2 : 1;
+  ctas = env_int("SCB_IMPLICIT_CTAS", ctas) == 2 ? 2 : 1;
+  if (cols > 256 || T > 2) ctas = 1;
+  p.total_tiles = (int)((n_out + (long long)BM * T - 1) / ((long long)BM * T));
   auto r1024 = [](uint32_t x) { return (x + 1023u) / 1024u * 1024u; };
   p.a_tx = (uint32_t)(BM * p.kc * 2);
   p.b_tx = (uint32_t)(n_pad * p.kc * 2);
   p.a_off_bytes = r1024(p.a_tx);
   p.b_off_bytes = r1024(p.b_tx);
-  // Launch shape (swept on the MinkUNet level-0 map, tools/ic_sweep.py): two
-  // CTAs per SM whenever both fit in TMEM (C_out <= 128) -- the producer loop
-  // is latency-bound, so a second CTA's pipeline fills the gaps -- with ~32 KB
-  // stages; a single CTA with ~48 KB stages otherwise.
-  int ctas = cols <= 256 ? 2 : 1;
-  if (const char* e = getenv("SCB_IMPLICIT_CTAS")) ctas = atoi(e) == 2 ? 2 : 1;
-  if (cols > 256) ctas = 1;                   // two CTAs must both fit in TMEM
-  // several offsets per stage when one offset's chunk is small
-  int ops = (int)((ctas == 2 ? 32768u : 49152u) / (p.a_off_bytes + p.b_off_bytes));
+  const uint32_t op_bytes = T * p.a_off_bytes + p.b_off_bytes;
+  int ops = (int)((uint32_t)env_int("SCB_IC_STAGE_KB", ctas == 2 ? 32 : 48) * 1024u / op_bytes);
   ops = ops < 1 ? 1 : (ops > MAX_OPS ? MAX_OPS : ops);
   if (ops > volume) ops = volume;
-  if (const char* e = getenv("SCB_IMPLICIT_OPS")) ops = std::max(1, std::min(atoi(e), std::min(MAX_OPS, volume)));
+  ops = std::max(1, std::min(env_int("SCB_IMPLICIT_OPS", ops), std::min(MAX_OPS, volume)));
+  ops = std::min(ops, 32 / (p.kc / 8));  // one presence bit per 16-B item of a producer thread
   p.ops = ops;
   p.groups = (volume + ops - 1) / ops;
-  p.a_stage_bytes = ops * p.a_off_bytes;
-  p.stage_bytes = ops * (p.a_off_bytes + p.b_off_bytes);
+  p.a_stage_bytes = ops * T * p.a_off_bytes;
+  p.stage_bytes = ops * op_bytes;
   p.ldf = ldf;
   p.ldh = hits_ld(n_out);
   p.feat = (const __half*)features;
@@ -487,23 +565,34 @@ extern "C" int32_t scb_conv_implicit(const void* features, int64_t n_in, int32_t
   p.bias = bias;
   p.residual = (const __half*)residual;
   if (const char* dbg = getenv("SCB_IMPLICIT_DEBUG")) p.debug = atoi(dbg);
-  const int smem_cap = ctas == 2 ? 113 * 1024 : 227 * 1024;
-  const int fixed = 1024 + EPI_BYTES + 2 * volume * BM * 4 + 16 * MAX_OPS * 4 + 40 * 8 + 64 +
-                    16 * MAX_P * BM;  // wmask
-  int stages = (smem_cap - fixed) / (int)p.stage_bytes;
+  const int coal = env_int("SCB_IC_COAL", 1) ? 1 : 0;
+  const int nprod = 128 * T;
+  // shared memory: stages (A + B blocks and one presence word per producer
+  // thread) + epilogue staging + neighbour table + flags + barriers
+  auto fixed_bytes = [&](int c) {
+    return 1024 + EPI_BYTES + (1 + c) * volume * nprod * 4 + 16 * MAX_OPS * T * 4 + 40 * 8 + 64;
+  };
+  int smem_cap = ctas == 2 ? 113 * 1024 : 227 * 1024;
+  auto fit = [&]() { return (smem_cap - fixed_bytes(coal)) / (int)(p.stage_bytes + nprod * 4); };
+  while (fit() < 2 && p.ops > 1) {  // fewer offsets per stage, then one CTA per SM
+    --p.ops;
+    p.stage_bytes = p.ops * op_bytes;
+  }
+  if (fit() < 2 && ctas == 2) {
+    ctas = 1;
+    smem_cap = 227 * 1024;
+  }
+  p.groups = (volume + p.ops - 1) / p.ops;
+  p.a_stage_bytes = p.ops * T * p.a_off_bytes;
+  int stages = fit();
   if (stages > 16) stages = 16;
+  stages = std::min(stages, std::max(2, env_int("SCB_IC_STAGES", 16)));
   SCB_CHECK_ARG(stages >= 2, "stage does not fit in shared memory");
   p.stages = stages;
+  const int fixed = fixed_bytes(coal) + stages * nprod * 4;
   const int smem = fixed + stages * (int)p.stage_bytes;
-  // cp.async groups a producer leaves in flight before signalling a stage
-  // full: arriving as early as possible measured best (the other CTA / later
-  // stages keep loads in flight)
-  int lag = ctas == 2 ? 0 : 1;
-  if (const char* e = getenv("SCB_IMPLICIT_LAG")) {
-    const int l = atoi(e);
-    lag = l >= 8 ? 8 : (l >= 4 ? 4 : (l >= 2 ? 2 : (l >= 1 ? 1 : 0)));
-    while (lag >= stages) lag = lag / 2;
-  }
+  // LAG < 0: producers arrive asynchronously (cp.async.mbarrier.arrive.noinc)
+  const int lag = env_int("SCB_IMPLICIT_LAG", -1) < 0 ? -1 : 0;
 
   CUtensorMap mB, mO;
   std::string err;
@@ -522,20 +611,24 @@ extern "C" int32_t scb_conv_implicit(const void* features, int64_t n_in, int32_t
     return SCB_OK;
   };
   int rc = SCB_EINVAL;
-#define SCB_IC_LAUNCH_P(VV, KK, MB)                                                         \
-  rc = lag == 8 ? launch(implicit_conv_f16_kernel<VV, 8, KK, 1, MB>, 320)                 \
-       : lag == 4 ? launch(implicit_conv_f16_kernel<VV, 4, KK, 1, MB>, 320)               \
-       : lag == 2 ? launch(implicit_conv_f16_kernel<VV, 2, KK, 1, MB>, 320)               \
-       : lag == 1 ? launch(implicit_conv_f16_kernel<VV, 1, KK, 1, MB>, 320)               \
-                  : launch(implicit_conv_f16_kernel<VV, 0, KK, 1, MB>, 320)
-#define SCB_IC_LAUNCH(VV, KK)                                                               \
-  if (ctas == 2) SCB_IC_LAUNCH_P(VV, KK, 2); else SCB_IC_LAUNCH_P(VV, KK, 1)
+#define SCB_IC_LAUNCH_L(VV, KK, TT, MB)                                                        \
+  rc = lag < 0 ? launch(implicit_conv_f16_kernel<VV, -1, KK, TT, 0, MB>, 64 + 128 * TT + 128)  \
+               : launch(implicit_conv_f16_kernel<VV, 0, KK, TT, 0, MB>, 64 + 128 * TT + 128)
+#define SCB_IC_LAUNCH_P(VV, KK, TT, MB)                                                        \
+  rc = launch(implicit_conv_f16_kernel<VV, -1, KK, TT, 1, MB>, 64 + 128 * TT + 128)
+#define SCB_IC_LAUNCH_T(VV, KK)                                                                \
+  if (T == 4) { SCB_IC_LAUNCH_L(VV, KK, 4, 1); }                                               \
+  else if (T == 2 && coal) { if (ctas == 2) { SCB_IC_LAUNCH_P(VV, KK, 2, 2); } else { SCB_IC_LAUNCH_P(VV, KK, 2, 1); } } \
+  else if (T == 2) { if (ctas == 2) { SCB_IC_LAUNCH_L(VV, KK, 2, 2); } else { SCB_IC_LAUNCH_L(VV, KK, 2, 1); } } \
+  else if (coal) { if (ctas == 2) { SCB_IC_LAUNCH_P(VV, KK, 1, 2); } else { SCB_IC_LAUNCH_P(VV, KK, 1, 1); } } \
+  else { if (ctas == 2) { SCB_IC_LAUNCH_L(VV, KK, 1, 2); } else { SCB_IC_LAUNCH_L(VV, KK, 1, 1); } }
   if (volume == 27) {
-    if (p.kc == 64) SCB_IC_LAUNCH(27, 64); else if (p.kc == 32) SCB_IC_LAUNCH(27, 32); else SCB_IC_LAUNCH(27, 16);
+    if (p.kc == 64) { SCB_IC_LAUNCH_T(27, 64) } else if (p.kc == 32) { SCB_IC_LAUNCH_T(27, 32) } else { SCB_IC_LAUNCH_T(27, 16) }
   } else if (volume == 8) {
-    if (p.kc == 64) SCB_IC_LAUNCH(8, 64); else if (p.kc == 32) SCB_IC_LAUNCH(8, 32); else SCB_IC_LAUNCH(8, 16);
+    if (p.kc == 64) { SCB_IC_LAUNCH_T(8, 64) } else if (p.kc == 32) { SCB_IC_LAUNCH_T(8, 32) } else { SCB_IC_LAUNCH_T(8, 16) }
   }
-#undef SCB_IC_LAUNCH
+#undef SCB_IC_LAUNCH_T
+#undef SCB_IC_LAUNCH_L
 #undef SCB_IC_LAUNCH_P
   if (rc == SCB_EINVAL) set_error("scb_conv_implicit: V must be 8 or 27");
   if (rc != SCB_OK) return rc;
@@ -544,7 +637,7 @@ extern "C" int32_t scb_conv_implicit(const void* features, int64_t n_in, int32_t
     cudaStreamSynchronize(s);
     cudaMemcpyFromSymbol(prof, g_ic_prof, sizeof(prof));
     fprintf(stderr, "[ic prof cta0] tiles=%llu total=%llu Aempty=%llu Await=%llu Bempty=%llu "
-            "MMAfull=%llu MMAtempty=%llu EPItfull=%llu EPIbulk=%llu Aloop=%llu Afence=%llu Aarrive=%llu "
+            "MMAfull=%llu MMAtempty=%llu EPItfull=%llu EPIbulk=%llu MMAissue=%llu Aitems=%llu Aarrive=%llu "
             "prologue=%llu bar=%llu (stages=%d ops=%d)\n",
             prof[9], prof[7], prof[0], prof[1], prof[2], prof[3], prof[4], prof[5], prof[6], prof[10],
             prof[11], prof[12], prof[13], prof[14], p.stages, p.ops);

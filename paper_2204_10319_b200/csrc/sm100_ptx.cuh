@@ -36,6 +36,22 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// Wait with a sleep between polls: for waiters off the critical path (the
+// epilogue between tiles) so their spinning does not take issue slots.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t ns) {
+  uint32_t done;
+  for (;;) {
+    asm volatile(
+        "{ .reg .pred P1;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, P1; }\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (done) return;
+    __nanosleep(ns);
+  }
+}
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int x,
                                             int y) {
   asm volatile(
@@ -78,6 +94,14 @@ __device__ __forceinline__ void fence_async_smem() {
 __device__ __forceinline__ void tc_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
+// One lane of the (converged) warp returns true.
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred;
+  asm volatile(
+      "{\n .reg .pred P;\n elect.sync _|P, 0xffffffff;\n selp.u32 %0, 1, 0, P;\n}\n"
+      : "=r"(pred));
+  return pred != 0;
+}
 __device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr, uint32_t sbo, uint32_t layout) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
@@ -123,6 +147,14 @@ __device__ __forceinline__ void cp_async16_if(uint32_t dst, const void* src, boo
       "{ .reg .pred q; setp.ne.b32 q, %2, 0;\n"
       "  @q cp.async.cg.shared.global [%0], [%1], 16; }" ::"r"(dst),
       "l"(src), "r"((int)p)
+      : "memory");
+}
+// Predicated cp.async whose source size is 16 (copy) or 0 (zero-fill, no read).
+__device__ __forceinline__ void cp_async16_zfill_if(uint32_t dst, const void* src, bool copy, bool p) {
+  asm volatile(
+      "{ .reg .pred q; setp.ne.b32 q, %3, 0;\n"
+      "  @q cp.async.cg.shared.global [%0], [%1], 16, %2; }" ::"r"(dst),
+      "l"(src), "r"(copy ? 16u : 0u), "r"((int)p)
       : "memory");
 }
 __device__ __forceinline__ void st_zero16_if(uint32_t dst, bool p) {

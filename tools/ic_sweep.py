@@ -12,7 +12,9 @@ import paper_2204_10319_b200 as sc  # noqa: E402
 from bench import load_scans, pack  # noqa: E402
 
 
-OPS_LAG = [(o, l) for o in (1, 2, 3, 4, 6, 8) for l in (0, 1, 2, 4)]
+CONFIGS = [(1, 2, -1, 32, 1), (1, 2, -1, 48, 1), (1, 2, -1, 32, 0), (1, 2, -1, 48, 0),
+           (1, 1, -1, 64, 1), (1, 1, -1, 64, 0), (2, 1, -1, 96, 1), (2, 1, -1, 96, 0),
+           (2, 2, -1, 32, 1)]
 
 
 def timeit(fn, n=20):
@@ -44,22 +46,19 @@ def main():
         o_st = sc.ExecOptions(dataflow="staged", index_kind="hash")
         res["staged"] = timeit(lambda: sc.sparse_conv_forward(t, w, spec, None, None, o_st))
         o_f = sc.ExecOptions(dataflow="fused", index_kind="hash")
-        for ctas in (1, 2):
-            for ops, lag in OPS_LAG:
-                os.environ["SCB_IMPLICIT_CTAS"] = str(ctas)
-                os.environ["SCB_IMPLICIT_LAG"] = str(lag)
-                if ops:
-                    os.environ["SCB_IMPLICIT_OPS"] = str(ops)
-                else:
-                    os.environ.pop("SCB_IMPLICIT_OPS", None)
-                try:
-                    res[f"c{ctas}o{ops}l{lag}"] = timeit(
-                        lambda: sc.sparse_conv_forward(t, w, spec, None, None, o_f))
-                except Exception:  # stage does not fit
-                    pass
-        os.environ.pop("SCB_IMPLICIT_OPS", None)
-        os.environ.pop("SCB_IMPLICIT_CTAS", None)
-        os.environ.pop("SCB_IMPLICIT_LAG", None)
+        ref = sc.sparse_conv_forward(t, w, spec, None, None, o_st).features.float()
+        for T, ctas, lag, kb, P in CONFIGS:
+            os.environ.update(SCB_IC_T=str(T), SCB_IMPLICIT_CTAS=str(ctas), SCB_IC_COAL=str(P),
+                              SCB_IMPLICIT_LAG=str(lag), SCB_IC_STAGE_KB=str(kb))
+            try:
+                ms = timeit(lambda: sc.sparse_conv_forward(t, w, spec, None, None, o_f))
+                got = sc.sparse_conv_forward(t, w, spec, None, None, o_f).features.float()
+                err = float((got - ref).norm() / ref.norm())
+                res[f"T{T}c{ctas}C{P}k{kb}"] = ms if err < 1e-2 else float("nan")
+            except Exception:  # stage does not fit
+                pass
+        for k in ("SCB_IC_T", "SCB_IMPLICIT_CTAS", "SCB_IC_COAL", "SCB_IMPLICIT_LAG", "SCB_IC_STAGE_KB"):
+            os.environ.pop(k, None)
         best = min((v, k) for k, v in res.items() if v == v)
         print(f"{cin}->{cout}: best {best[1]} {best[0]:.3f} | " +
               " ".join(f"{k}={v:.3f}" for k, v in res.items()), flush=True)
