@@ -274,12 +274,18 @@ def main():
         return model.forward(t, sc.ExecOptions(timer=timer, traffic_log=traffic,
                                                index_kind="hash", dataflow=args.dataflow))
 
+    # algorithmic bytes per layer from one untimed pass (the
+    # traffic log takes the host-planned path, the timed steps the sync-free
+    # one); the warm-up steps after it settle the allocator again
+    traffic = []
+    step(None, traffic)
+    torch.cuda.synchronize()
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
 
     # ---------------- device-resident timed region
-    timer, traffic = sc.StageTimer(), []
+    timer = sc.StageTimer()
     clocks = Clocks(str(ROOT / f"gpurun_out/clocks_rank{rank}.csv")
                     if (ROOT / "gpurun_out").exists() else f"/tmp/clocks_rank{rank}.csv")
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -298,7 +304,7 @@ def main():
         flush.fill_(i & 0xFF)  # L2 flush, outside the step's events
         evs[i][0].record()
         h0 = time.perf_counter()
-        out = step(timer, traffic)
+        out = step(timer)
         host_ms.append(1e3 * (time.perf_counter() - h0))
         evs[i][1].record()
     torch.cuda.synchronize()
@@ -321,7 +327,7 @@ def main():
         stages[stage] = stages.get(stage, 0.0) + s
     bytes_by = {"gather": 0, "matmul": 0, "scatter": 0, "fused": 0}
     flops = fused_flops = 0
-    for _, rec in traffic:
+    for _, rec in traffic * args.steps:  # one pass recorded, K timed
         bytes_by["gather"] += rec.get("gather_bytes", 0)
         bytes_by["matmul"] += rec.get("gemm_bytes", 0)
         bytes_by["scatter"] += rec.get("scatter_bytes", 0)
@@ -343,10 +349,11 @@ def main():
             "unit": "GB/s", "frac": ach / hbm_peak,
             "traffic": measured.get(dom, {}).get("dram_bytes_per_launch"),
             "traffic_source": measured.get("source"),
-            "algorithmic_bytes_per_launch": bytes_by[dom] / max(1, sum(
+            "algorithmic_bytes_per_launch": bytes_by[dom] / args.steps / max(1, sum(
                 1 for _, r in traffic if (("fused_bytes" in r) if dom == "fused"
                                           else ("gemm_bytes" in r)))),
-            "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6.65 TB/s",
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks
+            else "of fallback 6.65 TB/s (B200_PROFILING.md; MEASURED_PEAKS.json absent)",
             "per_stage": {k: {"ms_per_step": 1e3 * stages.get(k, 0.0) / args.steps,
                               "GBps": (bytes_by[k] / stages[k] / 1e9) if stages.get(k) else None}
                           for k in ("gather", "matmul", "scatter", "fused")},

@@ -250,8 +250,10 @@ int32_t scb_gemm_tile_geometry(int32_t dtype, int32_t c_out, int32_t* bm, int32_
  *   out[k] = epi( sum_n features[hits[n][k]] . W[n] ),  absent neighbours = 0,
  * with epi = *scale + shift, + bias, + residual[k], ReLU (each optional).
  * `hits` is the [V][n_out] hit matrix of scb_map_search / scb_map_transpose,
- * so no compaction, plan, gather buffer or partials are needed.  FP16 storage
- * only; V in {8, 27}; c_in, c_out multiples of 8; weights packed by
+ * so no compaction, plan, gather buffer or partials are needed.  V = 1 is the
+ * K=1 pointwise layer (execution.py:472-477): `hits` may be NULL (identity
+ * map, n_in == n_out).  FP16 storage only; V in {1, 8, 27}; c_in, c_out
+ * multiples of 8 (callers zero-pad narrower inputs); weights packed by
  * scb_pack_weights_f16.  Per-output accumulation runs over the offsets in
  * ascending order inside the tensor core (f32). */
 int32_t scb_conv_implicit(const void* features, int64_t n_in, int32_t c_in, int64_t ldf,

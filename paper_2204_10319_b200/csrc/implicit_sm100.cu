@@ -184,7 +184,7 @@ __global__ void __launch_bounds__(64 + 128 * T + 128, MINB)
       const long long k = ((long long)t_begin * T + h) * BM + row;
 #pragma unroll
       for (int n = 0; n < V; ++n)
-        nxt[n] = (t_begin < t_end && k < p.n_out) ? __ldg(p.hits + (long long)n * p.ldh + k) : -1;
+        nxt[n] = (t_begin < t_end && k < p.n_out) ? (V == 1 ? (int)k : __ldg(p.hits + (long long)n * p.ldh + k)) : -1;
     }
     for (int s = 0; s < p.stages; ++s) {
       const uint32_t base = smem_u32(smem + (size_t)s * p.stage_bytes);
@@ -221,7 +221,7 @@ __global__ void __launch_bounds__(64 + 128 * T + 128, MINB)
         const long long k = ((long long)(t + 1) * T + h) * BM + row;
         const bool ok = (t + 1 < t_end) && k < p.n_out;
 #pragma unroll
-        for (int n = 0; n < V; ++n) nxt[n] = ok ? __ldg(p.hits + (long long)n * p.ldh + k) : -1;
+        for (int n = 0; n < V; ++n) nxt[n] = ok ? (V == 1 ? (int)k : __ldg(p.hits + (long long)n * p.ldh + k)) : -1;
       }
       for (int g = 0; g < p.groups; ++g) {
         const int nv = min(p.ops, V - g * p.ops);
@@ -498,7 +498,10 @@ extern "C" int32_t scb_conv_implicit(const void* features, int64_t n_in, int32_t
                                      const float* bias, const void* residual, int32_t relu,
                                      scb_stream_t stream) {
   using namespace ic;
-  SCB_CHECK_ARG(volume == 8 || volume == 27, "implicit conv supports K^3 = 8 or 27 offsets");
+  SCB_CHECK_ARG(volume == 1 || volume == 8 || volume == 27,
+                "implicit conv supports K^3 = 1, 8 or 27 offsets");
+  SCB_CHECK_ARG(volume == 1 || hits != nullptr, "hit matrix required for K > 1");
+  SCB_CHECK_ARG(volume != 1 || n_in == n_out, "K = 1: identity map needs n_in == n_out");
   SCB_CHECK_ARG(c_in % 8 == 0 && ldf % 8 == 0, "C_in and its row stride must be multiples of 8");
   SCB_CHECK_ARG(c_out % 8 == 0, "C_out must be a multiple of 8");
   SCB_CHECK_ARG(ldf * 2 < (1LL << 32), "feature row stride too large");
@@ -530,10 +533,7 @@ extern "C" int32_t scb_conv_implicit(const void* features, int64_t n_in, int32_t
   // Launch shape.  T tiles share every weight slice load; T accumulators are
   // double-buffered in TMEM (2 T n_pad columns <= 512), and two CTAs per SM
   // run when both fit (their producer loops fill each other's gaps).
-  int T = 1;
-  T = env_int("SCB_IC_T", T);
-  T = T >= 4 ? 4 : (T >= 2 ? 2 : 1);
-  while (T > 1 && 2 * T * n_pad > 512) T /= 2;
+  const int T = 1;
   uint32_t cols = 32;
   while (cols < (uint32_t)(2 * T * n_pad)) cols *= 2;
   p.tmem_cols = cols;
@@ -592,7 +592,6 @@ extern "C" int32_t scb_conv_implicit(const void* features, int64_t n_in, int32_t
   const int fixed = fixed_bytes(coal) + stages * nprod * 4;
   const int smem = fixed + stages * (int)p.stage_bytes;
   // LAG < 0: producers arrive asynchronously (cp.async.mbarrier.arrive.noinc)
-  const int lag = env_int("SCB_IMPLICIT_LAG", -1) < 0 ? -1 : 0;
 
   CUtensorMap mB, mO;
   std::string err;
@@ -611,26 +610,26 @@ extern "C" int32_t scb_conv_implicit(const void* features, int64_t n_in, int32_t
     return SCB_OK;
   };
   int rc = SCB_EINVAL;
-#define SCB_IC_LAUNCH_L(VV, KK, TT, MB)                                                        \
-  rc = lag < 0 ? launch(implicit_conv_f16_kernel<VV, -1, KK, TT, 0, MB>, 64 + 128 * TT + 128)  \
-               : launch(implicit_conv_f16_kernel<VV, 0, KK, TT, 0, MB>, 64 + 128 * TT + 128)
-#define SCB_IC_LAUNCH_P(VV, KK, TT, MB)                                                        \
-  rc = launch(implicit_conv_f16_kernel<VV, -1, KK, TT, 1, MB>, 64 + 128 * TT + 128)
+  // instantiated: T = 1, async producer arrival, coalesced or row-per-thread
+  // copies, one or two CTAs per SM (T > 1 and the wait_group scheme measured
+  // slower on the MinkUNet layers and are not built)
 #define SCB_IC_LAUNCH_T(VV, KK)                                                                \
-  if (T == 4) { SCB_IC_LAUNCH_L(VV, KK, 4, 1); }                                               \
-  else if (T == 2 && coal) { if (ctas == 2) { SCB_IC_LAUNCH_P(VV, KK, 2, 2); } else { SCB_IC_LAUNCH_P(VV, KK, 2, 1); } } \
-  else if (T == 2) { if (ctas == 2) { SCB_IC_LAUNCH_L(VV, KK, 2, 2); } else { SCB_IC_LAUNCH_L(VV, KK, 2, 1); } } \
-  else if (coal) { if (ctas == 2) { SCB_IC_LAUNCH_P(VV, KK, 1, 2); } else { SCB_IC_LAUNCH_P(VV, KK, 1, 1); } } \
-  else { if (ctas == 2) { SCB_IC_LAUNCH_L(VV, KK, 1, 2); } else { SCB_IC_LAUNCH_L(VV, KK, 1, 1); } }
+  if (coal) {                                                                                  \
+    if (ctas == 2) rc = launch(implicit_conv_f16_kernel<VV, -1, KK, 1, 1, 2>, 320);            \
+    else rc = launch(implicit_conv_f16_kernel<VV, -1, KK, 1, 1, 1>, 320);                      \
+  } else {                                                                                     \
+    if (ctas == 2) rc = launch(implicit_conv_f16_kernel<VV, -1, KK, 1, 0, 2>, 320);            \
+    else rc = launch(implicit_conv_f16_kernel<VV, -1, KK, 1, 0, 1>, 320);                      \
+  }
   if (volume == 27) {
     if (p.kc == 64) { SCB_IC_LAUNCH_T(27, 64) } else if (p.kc == 32) { SCB_IC_LAUNCH_T(27, 32) } else { SCB_IC_LAUNCH_T(27, 16) }
   } else if (volume == 8) {
     if (p.kc == 64) { SCB_IC_LAUNCH_T(8, 64) } else if (p.kc == 32) { SCB_IC_LAUNCH_T(8, 32) } else { SCB_IC_LAUNCH_T(8, 16) }
+  } else if (volume == 1) {
+    if (p.kc == 64) { SCB_IC_LAUNCH_T(1, 64) } else if (p.kc == 32) { SCB_IC_LAUNCH_T(1, 32) } else { SCB_IC_LAUNCH_T(1, 16) }
   }
 #undef SCB_IC_LAUNCH_T
-#undef SCB_IC_LAUNCH_L
-#undef SCB_IC_LAUNCH_P
-  if (rc == SCB_EINVAL) set_error("scb_conv_implicit: V must be 8 or 27");
+  if (rc == SCB_EINVAL) set_error("scb_conv_implicit: V must be 1, 8 or 27");
   if (rc != SCB_OK) return rc;
   if (p.debug & 16) {
     unsigned long long prof[16];

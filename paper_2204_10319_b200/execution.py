@@ -485,48 +485,58 @@ def _epi_args(ep: dict | None):
             nat.ptr(res), int(bool(ep.get("relu", False))))
 
 
-def _fused_eligible(dtype, kmap: KernelMap, w: WeightTensor) -> bool:
-    return (dtype == torch.float16 and kmap.offsets.volume in (8, 27) and w.c_in % 8 == 0
-            and w.c_out % 8 == 0 and w.c_out <= 256)
+def _fused_eligible(dtype, volume: int, w: WeightTensor) -> bool:
+    """The implicit-GEMM kernel: FP16 storage, K^3 in {1, 8, 27}, C_out a
+    multiple of 8 (16-B TMA rows of the output) up to 256.  C_in that is not
+    a multiple of 8 (the 4-channel stem) is zero-padded to one."""
+    return (dtype == torch.float16 and volume in (1, 8, 27) and w.c_out % 8 == 0
+            and w.c_out <= 256)
 
 
-def choose_dataflow(opts: ExecOptions, dtype, kmap: KernelMap, w: WeightTensor) -> str:
+def choose_dataflow(opts: ExecOptions, dtype, kmap: KernelMap | None, w: WeightTensor) -> str:
     """"staged" (gather -> grouped GEMM -> scatter, the reference's structure)
-    or "fused" (one implicit-GEMM kernel).  ``auto`` compares the two
-    roofline estimates: staged moves the buffer and the f32 partials through
-    HBM; fused multiplies every offset densely (absent rows are zero) but
-    keeps all intermediates on chip."""
-    if opts.dataflow == "staged" or not _fused_eligible(dtype, kmap, w):
+    or "fused" (one implicit-GEMM kernel).  ``auto`` picks fused wherever it
+    is eligible: measured on B200 per MinkUNet layer (tools/layer_compare.py,
+    8 packed scans) it wins every k3 / k2 / transposed layer from 32 to 256
+    channels (e.g. 96->96 at level 0: 0.82 vs 1.77 ms, 256->256: 0.22 vs
+    0.35 ms) and k1 layers once their output is written by the fused
+    epilogue instead of an f32 partial round trip."""
+    volume = 1 if kmap is None else kmap.offsets.volume
+    if opts.dataflow == "staged" or not _fused_eligible(dtype, volume, w):
         return "staged"
-    if opts.dataflow == "fused":
-        return "fused"
-    # Measured on B200 per MinkUNet layer (tools/layer_compare.py, 8 packed
-    # scans): fused wins every layer with C_out <= 128 (two CTAs per SM fit
-    # in TMEM), e.g. 32->32 0.17/0.27 ms, 96->96 1.33/1.77, 192->128
-    # 0.49/0.52; staged wins at C_out = 256 (0.35/0.43) and for 256->128
-    # (0.14/0.19), where the staged GEMM's wide tiles amortise better.
-    return "fused" if w.c_out <= 128 and w.c_in <= 192 else "staged"
+    return "fused"
 
 
-def _run_fused(features: torch.Tensor, kmap: KernelMap, w: WeightTensor, opts: ExecOptions,
-               epilogue: dict | None) -> torch.Tensor:
+def _pad_channels(f: torch.Tensor) -> torch.Tensor:
+    """Zero-pad fp16 rows to a multiple of 8 channels (16-B cp.async chunks);
+    the packed weights already carry zero rows for the padded channels."""
+    c = f.shape[1]
+    if c % 8 == 0 and f.is_contiguous():
+        return f
+    return torch.nn.functional.pad(f, (0, (-c) % 8)).contiguous()
+
+
+def _run_fused(features: torch.Tensor, kmap: KernelMap | None, w: WeightTensor,
+               opts: ExecOptions, epilogue: dict | None) -> torch.Tensor:
+    """One scb_conv_implicit launch; ``kmap`` None = the K=1 identity map."""
     label, timer = opts.layer_label, opts.timer
     packed, _, _ = w.packed_f16()
-    f = features.contiguous()
-    out = torch.empty((kmap.n_out, w.c_out), dtype=f.dtype, device=f.device)
+    volume = 1 if kmap is None else kmap.offsets.volume
+    n_out = features.shape[0] if kmap is None else kmap.n_out
+    out = torch.empty((n_out, w.c_out), dtype=features.dtype, device=features.device)
     scale, shift, bias, res, relu = _epi_args(epilogue)
     with _timed(timer, label, "fused"):
-        nat.call("scb_conv_implicit", nat.ptr(f), f.shape[0], w.c_in, w.c_in, nat.ptr(kmap.hits),
-                 kmap.offsets.volume, kmap.n_out, nat.ptr(packed), w.c_out, nat.ptr(out), scale,
-                 shift, bias, res, relu, nat.stream_handle())
+        f = _pad_channels(features)
+        nat.call("scb_conv_implicit", nat.ptr(f), f.shape[0], f.shape[1], f.shape[1],
+                 None if kmap is None else nat.ptr(kmap.hits), volume, n_out, nat.ptr(packed),
+                 w.c_out, nat.ptr(out), scale, shift, bias, res, relu, nat.stream_handle())
     if opts.traffic_log is not None:
-        v = kmap.offsets.volume
         e = 2
         opts.traffic_log.append((label, {
-            "fused_bytes": e * f.shape[0] * w.c_in + e * kmap.n_out * w.c_out
-            + 4 * v * kmap.n_out + e * v * w.c_in * w.c_out
-            + (e * kmap.n_out * w.c_out if res else 0),
-            "fused_flops_executed": 2 * v * kmap.n_out * w.c_in * w.c_out}))
+            "fused_bytes": e * features.shape[0] * w.c_in + e * n_out * w.c_out
+            + (4 * volume * n_out if volume > 1 else 0) + e * volume * w.c_in * w.c_out
+            + (e * n_out * w.c_out if res else 0),
+            "fused_flops_executed": 2 * volume * n_out * w.c_in * w.c_out}))
     return out
 
 
@@ -625,6 +635,8 @@ def _run_dataflow(features: torch.Tensor, kmap: KernelMap, w: WeightTensor,
 
 def _pointwise_matmul(t: SparseTensor, w: WeightTensor, opts: ExecOptions, epilogue=None):
     """K=1, s=1 fast path (execution.py:472-477): out = features @ W[0]."""
+    if choose_dataflow(opts, t.features.dtype, None, w) == "fused":
+        return _run_fused(t.features, None, w, opts, epilogue)
     f = t.features
     dt = f.dtype
     n = f.shape[0]
@@ -708,8 +720,11 @@ def sparse_conv_forward(t: SparseTensor, w: WeightTensor, spec: LayerSpec,
     label, timer = opts.layer_label, opts.timer
     strat = resolve_strategy(spec, strategy)
     if spec.kernel_size == 1 and spec.stride == 1:
-        with _timed(timer, label, "matmul"):
+        if choose_dataflow(opts, t.features.dtype, None, w) == "fused":
             out = _pointwise_matmul(t, w, opts, epilogue)
+        else:
+            with _timed(timer, label, "matmul"):
+                out = _pointwise_matmul(t, w, opts, epilogue)
         _record_workload(opts, spec, np.array([t.num_points]), False, [0], t.coords, t.coords,
                          t.boundary, t.batch_size)
         return t.replace_features(out)

@@ -446,6 +446,39 @@ def test_epilogue_bn_residual_relu(sc, rng, dataflow):
     assert (got >= 0).all()
 
 
+@pytest.mark.parametrize("c_in,c_out", [(64, 96), (128, 256), (32, 32)])
+def test_fused_pointwise_layer(sc, rng, c_in, c_out):
+    """K=1 layer through the implicit kernel (V = 1, identity map, BN + ReLU
+    in the epilogue) against the oracle (execution.py:472-477)."""
+    coords = random_coords(rng, (24, 24, 24), 0.2)
+    n = coords.shape[0]
+    f = O.quantize(rng.standard_normal((n, c_in)).astype(np.float32), "fp16")
+    w = rng.normal(0, 1 / np.sqrt(c_in), (1, c_in, c_out)).astype(np.float32)
+    s = rng.uniform(0.8, 1.2, c_out).astype(np.float32)
+    h = rng.normal(0, 0.05, c_out).astype(np.float32)
+    _, base, _ = O.conv_forward(coords, f, (24, 24, 24), w, 1, 1)
+    want = np.maximum(base.astype(np.float32) * s + h, 0)
+    t = sc.SparseTensor(coords, f, 1, (24, 24, 24))
+    ep = {"scale": torch.from_numpy(s).cuda(), "shift": torch.from_numpy(h).cuda(), "relu": True}
+    out = sc.sparse_conv_forward(t, sc.WeightTensor(w, 1, 3), sc.LayerSpec(1, 1, c_in, c_out),
+                                 None, None, sc.ExecOptions(dataflow="fused"), epilogue=ep)
+    assert rel_l2(out.features_numpy().astype(np.float32), want) <= 1e-2
+
+
+@pytest.mark.parametrize("c_in", [4, 5, 12])
+def test_fused_narrow_input_channels(sc, rng, c_in):
+    """C_in not a multiple of 8 (the 4-channel MinkUNet stem, 5-channel
+    nuScenes stem) is zero-padded for the implicit kernel."""
+    coords = random_coords(rng, (20, 20, 20), 0.15)
+    f = O.quantize(rng.standard_normal((coords.shape[0], c_in)).astype(np.float32), "fp16")
+    w = rng.normal(0, 1 / np.sqrt(27 * c_in), (27, c_in, 32)).astype(np.float32)
+    _, want, _ = O.conv_forward(coords, f, (20, 20, 20), w, 3, 1)
+    out = sc.sparse_conv_forward(sc.SparseTensor(coords, f, 1, (20, 20, 20)),
+                                 sc.WeightTensor(w, 3, 3), sc.LayerSpec(3, 1, c_in, 32), None,
+                                 None, sc.ExecOptions(dataflow="fused"))
+    assert rel_l2(out.features_numpy(), want) <= 1e-2
+
+
 def test_lazy_map_needs_no_compaction_for_fused(sc, rng):
     coords = random_coords(rng, (16, 16, 16), 0.1)
     t = sc.SparseTensor(coords, rng.standard_normal((coords.shape[0], 16)).astype(np.float16),
