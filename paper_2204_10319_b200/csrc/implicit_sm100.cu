@@ -42,7 +42,7 @@ using namespace ::scb::ptx;
 constexpr int BM = 128;
 constexpr int MAX_T = 4;                // tiles per super-tile
 constexpr int EPI_BUF = 32 * 64;        // 32 rows x 64 B (32 fp16 columns)
-constexpr int EPI_BYTES = 4 * 2 * EPI_BUF;
+constexpr int EPI_MAX_BYTES = 4 * 2 * EPI_BUF;  // epilogue staging: 4 warps x (1 or 2) buffers
 constexpr int MAX_OPS = 8;              // kernel offsets per pipeline stage
 constexpr int MAX_V = 27;
 
@@ -50,6 +50,7 @@ struct Params {
   long long n_out;
   int n_in, c_in, c_out, V, n_pad, kc, n_kchunks, stages, swz, epi_cols, total_tiles, relu;
   int ops;                  // offsets per stage (small C_in -> several)
+  int epi_bufs;             // epilogue staging buffers per warp (1 or 2)
   int debug;                // SCB_IMPLICIT_DEBUG: 1 no A loads, 2 no MMAs, 16 wait counters, 32 no B loads
   int groups;               // ceil(V / ops) offset groups per super-tile
   uint32_t idesc, tmem_cols;
@@ -105,9 +106,8 @@ __global__ void __launch_bounds__(64 + 128 * T + 128, MINB)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* epi_base = smem + (size_t)p.stages * p.stage_bytes;
-  int* nbr_s = (int*)(epi_base + EPI_BYTES);                      // [1 + COAL][V][NPROD]
-  uint32_t* flags = (uint32_t*)(nbr_s + (1 + COAL) * V * NPROD);  // [stages][MAX_OPS][T]
-  uint64_t* full = (uint64_t*)(flags + p.stages * MAX_OPS * T);
+  int* nbr_s = (int*)(epi_base + 4 * p.epi_bufs * EPI_BUF);      // [V][NPROD] neighbour rows
+  uint64_t* full = (uint64_t*)(nbr_s + V * NPROD);
   uint64_t* empty = full + p.stages;
   uint64_t* tfull = empty + p.stages;
   uint64_t* tempty = tfull + 2;
@@ -207,15 +207,15 @@ __global__ void __launch_bounds__(64 + 128 * T + 128, MINB)
       roff[it] = (uint32_t)(r * (KC * 2)) + ((uint32_t)(cc ^ rxr) << 4);
     }
     const uint32_t ldfb = (uint32_t)(p.ldf * 2);  // feature row stride in bytes (host-checked < 2^32)
-    int cbuf = 0;
     for (int t = t_begin; t < t_end; ++t) {
-      const uint32_t nbw = COAL ? nb_s + (uint32_t)(cbuf * V * NPROD * 4) : nb_s;
+      // COAL: rows are copied by other threads, so the (single) table is
+      // rewritten only after every producer finished the previous tile
+      if constexpr (COAL) asm volatile("bar.sync 1, %0;" ::"n"(NPROD) : "memory");
+      const uint32_t nbw = nb_s;
 #pragma unroll
       for (int n = 0; n < V; ++n) {
         asm volatile("st.shared.b32 [%0], %1;" ::"r"(nbw + (uint32_t)(n * NPROD * 4)), "r"(nxt[n]) : "memory");
       }
-      // COAL: rows are copied by other threads; the double-buffered table
-      // needs one producer barrier per tile
       if constexpr (COAL) asm volatile("bar.sync 1, %0;" ::"n"(NPROD) : "memory");
       {
         const long long k = ((long long)(t + 1) * T + h) * BM + row;
@@ -242,7 +242,7 @@ __global__ void __launch_bounds__(64 + 128 * T + 128, MINB)
             // 16-B chunks (one warp instruction touches 32 / CPR rows).  An
             // offset's CPR index loads go first (volatile asm keeps the order)
             // so their latencies overlap; then one IMAD.WIDE per copy.
-            const uint32_t nbc = nb_s0 + (uint32_t)(cbuf * V * NPROD * 4) +
+            const uint32_t nbc = nb_s0 +
                                  (uint32_t)((g * p.ops * NPROD + h * BM + cr) * 4);
             const uint64_t fbase = reinterpret_cast<uint64_t>(p.feat) + (uint64_t)((col0 + cc * 8) * 2);
             const bool live_c = cc < live && !(p.debug & 1);
@@ -306,7 +306,6 @@ __global__ void __launch_bounds__(64 + 128 * T + 128, MINB)
           if (++stage == p.stages) { stage = 0; phase ^= 1; }
         }
       }
-      cbuf ^= COAL;
     }
     if constexpr (!NOINC) {
       cp_async_wait<0>();
@@ -376,7 +375,7 @@ __global__ void __launch_bounds__(64 + 128 * T + 128, MINB)
   } else if (warp >= EPI0) {
     // ============ epilogue
     const int q = warp & 3;
-    uint8_t* bufs = epi_base + (warp - EPI0) * 2 * EPI_BUF;
+    uint8_t* bufs = epi_base + (warp - EPI0) * p.epi_bufs * EPI_BUF;
     int acc = 0, nbuf = 0;
     uint32_t acc_phase = 0;
     const int chunks = p.n_pad / p.epi_cols;
@@ -432,7 +431,10 @@ __global__ void __launch_bounds__(64 + 128 * T + 128, MINB)
             for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
           }
           uint8_t* buf = bufs + nbuf * EPI_BUF;
-          if (lane == 0) IC_PROF(6, warp == EPI0, bulk_wait_read1());
+          if (lane == 0) {
+            if (p.epi_bufs == 2) IC_PROF(6, warp == EPI0, bulk_wait_read1());
+            else bulk_wait_read0();
+          }
           __syncwarp();
           if (ncol == 32) {
 #pragma unroll
@@ -455,7 +457,7 @@ __global__ void __launch_bounds__(64 + 128 * T + 128, MINB)
             tma_store_2d(&tmOut, buf, c0, (int)row0);
             bulk_commit();
           }
-          nbuf ^= 1;
+          nbuf ^= p.epi_bufs - 1;
         }
       }
       tc_before();
@@ -569,27 +571,30 @@ extern "C" int32_t scb_conv_implicit(const void* features, int64_t n_in, int32_t
   const int nprod = 128 * T;
   // shared memory: stages (A + B blocks and one presence word per producer
   // thread) + epilogue staging + neighbour table + flags + barriers
-  auto fixed_bytes = [&](int c) {
-    return 1024 + EPI_BYTES + (1 + c) * volume * nprod * 4 + 16 * MAX_OPS * T * 4 + 40 * 8 + 64;
+  auto fixed_bytes = [&](int epi_bufs) {
+    return 1024 + 4 * epi_bufs * EPI_BUF + volume * nprod * 4 + 40 * 8 + 64;
   };
   int smem_cap = ctas == 2 ? 113 * 1024 : 227 * 1024;
-  auto fit = [&]() { return (smem_cap - fixed_bytes(coal)) / (int)(p.stage_bytes + nprod * 4); };
-  while (fit() < 2 && p.ops > 1) {  // fewer offsets per stage, then one CTA per SM
+  auto fit = [&](int e) { return (smem_cap - fixed_bytes(e)) / (int)(p.stage_bytes + nprod * 4); };
+  while (fit(1) < 2 && p.ops > 1) {  // fewer offsets per stage, then one CTA per SM
     --p.ops;
     p.stage_bytes = p.ops * op_bytes;
   }
-  if (fit() < 2 && ctas == 2) {
+  if (fit(1) < 2 && ctas == 2) {
     ctas = 1;
     smem_cap = 227 * 1024;
   }
+  // double-buffered epilogue staging unless the second buffer costs a stage
+  p.epi_bufs = fit(2) >= fit(1) ? 2 : 1;
+  if (const char* e = getenv("SCB_IC_EPI_BUFS")) p.epi_bufs = atoi(e) == 1 ? 1 : 2;
   p.groups = (volume + p.ops - 1) / p.ops;
   p.a_stage_bytes = p.ops * T * p.a_off_bytes;
-  int stages = fit();
+  int stages = fit(p.epi_bufs);
   if (stages > 16) stages = 16;
   stages = std::min(stages, std::max(2, env_int("SCB_IC_STAGES", 16)));
   SCB_CHECK_ARG(stages >= 2, "stage does not fit in shared memory");
   p.stages = stages;
-  const int fixed = fixed_bytes(coal) + stages * nprod * 4;
+  const int fixed = fixed_bytes(p.epi_bufs) + stages * nprod * 4;
   const int smem = fixed + stages * (int)p.stage_bytes;
   // LAG < 0: producers arrive asynchronously (cp.async.mbarrier.arrive.noinc)
 

@@ -706,6 +706,54 @@ def _check_channels(t, w, spec, msg=None):
             f"weights {w.c_in}->{w.c_out}"))
 
 
+def _layer_maps(cset: CoordinateSet, spec: LayerSpec, strat: LayerStrategy,
+                opts: ExecOptions) -> tuple[CoordinateSet, KernelMap]:
+    """Output coordinate set and kernel map of a (non-transposed) layer over
+    ``cset``, cached on the set under (K, stride, offset base) when
+    ``opts.map_reuse`` (result-identical: maps depend on coordinates only)."""
+    offsets = enumerate_offsets(len(cset.boundary), spec.kernel_size)
+    kind = opts.index_kind or strat.index_kind or spec.index_kind or "auto"
+    if kind == "grid" and _cells(cset.boundary, cset.batch_size) > opts.grid_cell_cap:
+        raise GridCapacityError(
+            f"grid index needs {_cells(cset.boundary, cset.batch_size)} cells "
+            f"(cap {opts.grid_cell_cap}); use the hash index")
+    key = (spec.kernel_size, spec.stride, offsets.base)
+    hit = cset.maps.get(key) if opts.map_reuse else None
+    if hit is None:
+        if spec.stride == 1:
+            out_cset = cset
+        else:
+            out_boundary = downsample_boundary(cset.boundary, spec.stride)
+            oc = compute_output_coords(cset, offsets, spec.stride, out_boundary,
+                                       cset.batch_size)
+            out_cset = CoordinateSet(oc, out_boundary, cset.batch_size)
+        index = build_index(cset, kind, cell_cap=opts.grid_cell_cap)
+        kmap = map_search(index, out_cset.coords, offsets, spec.stride)
+        # stride 1: the output set IS this set; store None, not a
+        # self-reference (a cycle would pin the maps until the cyclic GC)
+        hit = (None if out_cset is cset else out_cset, kmap)
+        if opts.map_reuse:
+            cset.maps[key] = hit
+    out_cset, kmap = hit
+    return (cset if out_cset is None else out_cset), kmap
+
+
+def prepare_layer_maps(t, spec: LayerSpec, options: ExecOptions | None = None) -> CoordinateSet:
+    """Build (and cache on the coordinate set) the maps a layer will use,
+    without running it; returns the layer's output coordinate set.  B200
+    extension: a model calls this for its strided layers before queueing any
+    convolution, so the one host read per strided layer (the output
+    coordinate count) happens while the GPU queue is empty and the forward
+    itself issues without a host sync.  Result-identical."""
+    opts = options or ExecOptions()
+    if not opts.map_reuse:
+        raise ValueError("prepared maps are kept in the map-reuse cache")
+    cset = t.coordset if isinstance(t, SparseTensor) else t
+    if spec.kernel_size == 1 and spec.stride == 1:
+        return cset
+    return _layer_maps(cset, spec, resolve_strategy(spec, None), opts)[0]
+
+
 def sparse_conv_forward(t: SparseTensor, w: WeightTensor, spec: LayerSpec,
                         strategy: LayerStrategy | None = None, map_cache: dict | None = None,
                         options: ExecOptions | None = None, *,
@@ -732,30 +780,7 @@ def sparse_conv_forward(t: SparseTensor, w: WeightTensor, spec: LayerSpec,
     offsets = enumerate_offsets(t.spatial_dims, spec.kernel_size)
     cset = t.coordset
     with _timed(timer, label, "mapping"):
-        kind = opts.index_kind or strat.index_kind or spec.index_kind or "auto"
-        if kind == "grid" and _cells(t.boundary, t.batch_size) > opts.grid_cell_cap:
-            raise GridCapacityError(
-                f"grid index needs {_cells(t.boundary, t.batch_size)} cells "
-                f"(cap {opts.grid_cell_cap}); use the hash index")
-        key = (spec.kernel_size, spec.stride, offsets.base)
-        hit = cset.maps.get(key) if opts.map_reuse else None
-        if hit is None:
-            if spec.stride == 1:
-                out_boundary = t.boundary
-                out_cset = cset
-            else:
-                out_boundary = downsample_boundary(t.boundary, spec.stride)
-                oc = compute_output_coords(t, offsets, spec.stride, out_boundary, t.batch_size)
-                out_cset = CoordinateSet(oc, out_boundary, t.batch_size)
-            index = build_index(cset, kind, cell_cap=opts.grid_cell_cap)
-            kmap = map_search(index, out_cset.coords, offsets, spec.stride)
-            # stride 1: the output set IS this set; store None, not a
-            # self-reference (a cycle would pin the maps until the cyclic GC)
-            hit = (None if out_cset is cset else out_cset, kmap)
-            if opts.map_reuse:
-                cset.maps[key] = hit
-        out_cset, kmap = hit
-        out_cset = cset if out_cset is None else out_cset
+        out_cset, kmap = _layer_maps(cset, spec, strat, opts)
         if map_cache is not None and spec.reuse_key:
             map_cache[spec.reuse_key] = CachedMap(kmap, t.coords, t.boundary, t.stride, cset)
     schedule, symmetric = schedule_for(offsets, spec.stride)

@@ -133,6 +133,15 @@ class EngineMinkUNet:
             return a.replace_features(torch.cat([a.features, b.features], dim=1))
 
         names = {l["name"] for l in self.table}
+        # the coordinate pyramid first: each strided level needs one host
+        # read (its output count), done while nothing else is queued, so the
+        # convolutions below are issued without a host sync
+        from .execution import prepare_layer_maps
+        cs = t.coordset
+        if base.map_reuse:
+            for i in range(1, 5):
+                w = self.w[f"down{i}"]
+                cs = prepare_layer_maps(cs, LayerSpec(2, 2, w.c_in, w.c_out), base)
         x = conv(t, "stem.0", 3, 1)
         x = conv(x, "stem.1", 3, 1)
         skips = [x]
