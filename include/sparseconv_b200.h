@@ -103,6 +103,15 @@ int32_t scb_output_coords(const int32_t* in_coords, int64_t n_in, const scb_grid
                           int32_t kernel_size, int32_t offset_base, int32_t stride,
                           void* workspace, int64_t ws_bytes, int64_t* out_keys, int64_t* n_out,
                           scb_stream_t stream);
+/* The next strided level straight from the previous level's output keys
+ * (grid `in_grid`), whose count stays on the device (`n_in_dev`, at most
+ * `n_cap`): a chain of strided levels costs one host read instead of one per
+ * level.  Same output as scb_output_coords on the unflattened coordinates. */
+int32_t scb_output_keys_next(const int64_t* in_keys, const int64_t* n_in_dev, int64_t n_cap,
+                             const scb_grid_t* in_grid, const scb_grid_t* out_grid,
+                             int32_t kernel_size, int32_t offset_base, int32_t stride,
+                             void* workspace, int64_t ws_bytes, int64_t* out_keys, int64_t* n_out,
+                             scb_stream_t stream);
 int32_t scb_unflatten(const int64_t* keys, int64_t n, const scb_grid_t* grid, int32_t* coords,
                       scb_stream_t stream);
 

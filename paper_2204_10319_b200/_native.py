@@ -54,6 +54,8 @@ _SIGS = {
     "scb_output_coords_capacity": (_I64, [_I64, _I32, _I32, _I32]),
     "scb_output_coords_workspace": (_I64, [_I64, _I32, _I32, _I32]),
     "scb_output_coords": (_I32, [_P, _I64, _GP, _I32, _I32, _I32, _P, _I64, _P, _P, _P]),
+    "scb_output_keys_next": (_I32, [_P, _P, _I64, _GP, _GP, _I32, _I32, _I32, _P, _I64, _P, _P,
+                                    _P]),
     "scb_unflatten": (_I32, [_P, _I64, _GP, _P, _P]),
     "scb_map_search": (_I32, [_I32, _P, _I64, _GP, _I32, _I32, _I32, _I32, _P, _P, _I64, _P, _P]),
     "scb_map_workspace": (_I64, [_I32, _I64]),
@@ -128,13 +130,20 @@ def ptr(t) -> int | None:
     return t.data_ptr()
 
 
+_FN: dict = {}
+_NO_STATUS = ("scb_abi_version", "scb_device_sm_count")
+
+
 def call(name: str, *args) -> int:
     """Invoke an ABI function, raising NativeError with the library's
     message on a non-zero status."""
-    lib = load()
-    fn = getattr(lib, name)
+    fn = _FN.get(name)
+    if fn is None:
+        fn = getattr(load(), name)
+        _FN[name] = fn
     status = fn(*args)
-    if fn.restype is _I32 and name not in ("scb_abi_version", "scb_device_sm_count") and status != 0:
+    if status and fn.restype is _I32 and name not in _NO_STATUS:
+        lib = load()
         msg = lib.scb_last_error().decode(errors="replace")
         if status == 1:
             raise ValueError(msg)

@@ -107,7 +107,7 @@ class CoordinateSet:
     indexes by kind and kernel maps by (kernel_size, stride) — the
     level-keyed map cache."""
 
-    __slots__ = ("coords", "boundary", "batch_size", "indexes", "maps", "__weakref__")
+    __slots__ = ("coords", "boundary", "batch_size", "indexes", "maps", "stream", "__weakref__")
 
     def __init__(self, coords: torch.Tensor, boundary, batch_size: int):
         self.coords = coords
@@ -115,6 +115,20 @@ class CoordinateSet:
         self.batch_size = int(batch_size)
         self.indexes = {}
         self.maps = {}
+        # the stream the coordinates were produced on (a model may continue
+        # the mapping work there, off its compute stream)
+        self.stream = torch.cuda.current_stream() if torch.cuda.is_available() else None
+
+    def device_tensors(self):
+        """Every device tensor owned by this set, its indexes and its maps
+        (for Tensor.record_stream when another stream consumes them)."""
+        out = [self.coords]
+        for idx in self.indexes.values():
+            out += [t for t in (getattr(idx, "keys", None), getattr(idx, "rows", None),
+                                getattr(idx, "_status", None)) if isinstance(t, torch.Tensor)]
+        for _, kmap in self.maps.values():
+            out += kmap.device_tensors()
+        return out
 
     @property
     def num_points(self) -> int:
@@ -155,6 +169,21 @@ class SparseTensor:
         self.batch_size = int(batch_size)
         self._cset = coordset
 
+    @classmethod
+    def _wrap(cls, features: torch.Tensor, stride: int, boundary: tuple, batch_size: int,
+              coordset: CoordinateSet) -> "SparseTensor":
+        """Engine-internal constructor for layer outputs: the features are a
+        fresh device tensor with one row per coordinate of ``coordset`` (no
+        checks, no copies)."""
+        t = object.__new__(cls)
+        t.coords = coordset.coords
+        t.features = features
+        t.stride = stride
+        t.boundary = boundary
+        t.batch_size = batch_size
+        t._cset = coordset
+        return t
+
     # -- reference API --------------------------------------------------
     @property
     def num_points(self) -> int:
@@ -170,6 +199,11 @@ class SparseTensor:
 
     def replace_features(self, features) -> "SparseTensor":
         """Same coordinates (and coordinate set), new feature matrix."""
+        if (isinstance(features, torch.Tensor) and features.is_cuda and features.ndim == 2
+                and features.dtype in (torch.float16, torch.float32)
+                and features.shape[0] == self.coords.shape[0] and features.is_contiguous()):
+            return SparseTensor._wrap(features, self.stride, self.boundary, self.batch_size,
+                                      self._cset)
         return SparseTensor(None, features, self.stride, self.boundary, self.batch_size,
                             coordset=self._cset)
 

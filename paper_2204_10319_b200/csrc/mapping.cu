@@ -174,6 +174,48 @@ __global__ void out_candidates_kernel(const int* __restrict__ coords, long long 
   }
 }
 
+// The same candidates from the previous level's sorted unique keys (input
+// grid `gin`), for the first *n_dev of n_cap rows; rows past the live count
+// propose only sentinels.  Lets a chain of strided levels run with the
+// counts on the device (one host read for the whole chain).
+template <int D>
+__global__ void out_candidates_keys_kernel(const unsigned long long* __restrict__ keys,
+                                           const long long* __restrict__ n_dev, long long n_cap,
+                                           Grid gin, Grid gout, int K, int lo, int s, int cap,
+                                           unsigned long long sentinel,
+                                           unsigned long long* __restrict__ cand) {
+  const int V = [&] { int v = 1; for (int d = 0; d < D; ++d) v *= K; return v; }();
+  const long long n = *n_dev;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n_cap;
+       i += (long long)gridDim.x * blockDim.x) {
+    int w = 0;
+    if (i < n) {
+      long long r = (long long)keys[i];
+      int p[D + 1];
+#pragma unroll
+      for (int d = D - 1; d >= 0; --d) {
+        p[d + 1] = (int)(r % gin.ext[d]);
+        r /= gin.ext[d];
+      }
+      p[0] = (int)r;
+      for (int o = 0; o < V; ++o) {
+        int delta[D];
+        offset_of<D>(o, K, lo, delta);
+        bool keep = true;
+        long long key = p[0];
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+          const int u = p[d + 1] - delta[d];
+          keep = keep && u >= 0 && (u % s) == 0 && u < s * gout.ext[d];
+          key = key * gout.ext[d] + (u >= 0 ? u / s : 0);
+        }
+        if (keep && w < cap) cand[i * cap + (w++)] = (unsigned long long)key;
+      }
+    }
+    for (; w < cap; ++w) cand[i * cap + w] = sentinel;
+  }
+}
+
 __global__ void drop_sentinel_kernel(const unsigned long long* uniq, long long* count,
                                      unsigned long long sentinel) {
   long long c = *count;
@@ -251,6 +293,47 @@ extern "C" int32_t scb_output_coords(const int32_t* in_coords, int64_t n_in,
   void* tmp = base + 2 * w.cand_bytes;
   SCB_DISPATCH_DIM(g.dim, out_candidates_kernel<D><<<grid_blocks(n_in, 256), 256, 0, s>>>(
                               in_coords, n_in, g, kernel_size, offset_base, stride, cap, sentinel, cand));
+  SCB_LAUNCHED();
+  size_t tb = w.sort_tmp;
+  SCB_CUDA(cub::DeviceRadixSort::SortKeys(tmp, tb, cand, sorted, (int64_t)items, 0, end_bit, s));
+  tb = w.uniq_tmp;
+  SCB_CUDA(cub::DeviceSelect::Unique(tmp, tb, sorted, (unsigned long long*)out_keys,
+                                     (long long*)n_out, (int64_t)items, s));
+  drop_sentinel_kernel<<<1, 1, 0, s>>>((const unsigned long long*)out_keys, (long long*)n_out,
+                                       sentinel);
+  SCB_LAUNCHED();
+  return SCB_OK;
+}
+
+extern "C" int32_t scb_output_keys_next(const int64_t* in_keys, const int64_t* n_in_dev,
+                                        int64_t n_cap, const scb_grid_t* in_grid,
+                                        const scb_grid_t* out_grid, int32_t kernel_size,
+                                        int32_t offset_base, int32_t stride, void* workspace,
+                                        int64_t ws_bytes, int64_t* out_keys, int64_t* n_out,
+                                        scb_stream_t stream) {
+  SCB_CHECK_ARG(in_grid && out_grid && in_grid->dim == out_grid->dim && out_grid->dim >= 1 &&
+                    out_grid->dim <= 4, "bad grids");
+  SCB_CHECK_ARG(stride >= 1 && kernel_size >= 1, "bad kernel size / stride");
+  cudaStream_t s = as_stream(stream);
+  Grid gi = to_grid(in_grid), g = to_grid(out_grid);
+  OutCoordWs w = out_coord_ws(n_cap, g.dim, kernel_size, stride);
+  SCB_CHECK_ARG(ws_bytes >= (int64_t)w.total, "workspace too small");
+  if (n_cap == 0) {
+    SCB_CUDA(cudaMemsetAsync(n_out, 0, sizeof(int64_t), s));
+    return SCB_OK;
+  }
+  const int cap = cand_per_input(g.dim, kernel_size, stride);
+  const long long items = n_cap * cap;
+  const unsigned long long sentinel = (unsigned long long)total_cells(g);
+  int end_bit = 1;
+  while (end_bit < 64 && (sentinel >> end_bit) != 0) ++end_bit;
+  char* base = (char*)workspace;
+  auto* cand = (unsigned long long*)base;
+  auto* sorted = (unsigned long long*)(base + w.cand_bytes);
+  void* tmp = base + 2 * w.cand_bytes;
+  SCB_DISPATCH_DIM(g.dim, out_candidates_keys_kernel<D><<<grid_blocks(n_cap, 256), 256, 0, s>>>(
+                              (const unsigned long long*)in_keys, (const long long*)n_in_dev,
+                              n_cap, gi, g, kernel_size, offset_base, stride, cap, sentinel, cand));
   SCB_LAUNCHED();
   size_t tb = w.sort_tmp;
   SCB_CUDA(cub::DeviceRadixSort::SortKeys(tmp, tb, cand, sorted, (int64_t)items, 0, end_bit, s));

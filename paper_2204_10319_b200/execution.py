@@ -32,8 +32,8 @@ from .core import (CoordinateSet, PrecisionMode, SparseTensor, WeightTensor,
                    flush_saturation_warnings)
 from .mapping import (DEFAULT_GRID_CELL_CAP, GatherScatterPlan, GridCapacityError, KernelMap,
                       KernelOffsets, build_gather_scatter_plan, build_index,
-                      compute_output_coords, downsample_boundary, enumerate_offsets, map_search,
-                      _cells)
+                      compute_output_coords, compute_output_coords_chain, downsample_boundary,
+                      enumerate_offsets, map_search, _cells)
 
 GATHER_ORDERS = ("weight_stationary", "input_stationary")
 SCATTER_ORDERS = ("weight_stationary", "output_stationary")
@@ -48,17 +48,13 @@ class StageTimer:
     def __init__(self):
         self._events: list[tuple[str, str, torch.cuda.Event, torch.cuda.Event]] = []
         self._samples: dict[tuple[str, str], float] = {}
+        self._pool: list[torch.cuda.Event] = []
 
-    @contextmanager
-    def section(self, layer: str, stage: str):
-        start = torch.cuda.Event(enable_timing=True)
-        end = torch.cuda.Event(enable_timing=True)
-        start.record()
-        try:
-            yield
-        finally:
-            end.record()
-            self._events.append((layer, stage, start, end))
+    def _event(self) -> torch.cuda.Event:
+        return self._pool.pop() if self._pool else torch.cuda.Event(enable_timing=True)
+
+    def section(self, layer: str, stage: str) -> "_Section":
+        return _Section(self, layer, stage)
 
     @property
     def samples(self) -> dict[tuple[str, str], float]:
@@ -67,8 +63,29 @@ class StageTimer:
             for layer, stage, s, e in self._events:
                 key = (layer, stage)
                 self._samples[key] = self._samples.get(key, 0.0) + s.elapsed_time(e) / 1e3
+                self._pool += (s, e)  # events are reusable once read
             self._events.clear()
         return dict(self._samples)
+
+
+class _Section:
+    """CUDA-event bracket of one (layer, stage) on the current stream."""
+
+    __slots__ = ("timer", "layer", "stage", "start")
+
+    def __init__(self, timer: StageTimer, layer: str, stage: str):
+        self.timer, self.layer, self.stage = timer, layer, stage
+
+    def __enter__(self):
+        self.start = self.timer._event()
+        self.start.record()
+        return self
+
+    def __exit__(self, *exc):
+        end = self.timer._event()
+        end.record()
+        self.timer._events.append((self.layer, self.stage, self.start, end))
+        return False
 
 
 def _timed(timer, layer, stage):
@@ -754,6 +771,47 @@ def prepare_layer_maps(t, spec: LayerSpec, options: ExecOptions | None = None) -
     return _layer_maps(cset, spec, resolve_strategy(spec, None), opts)[0]
 
 
+def prepare_strided_chain(t, specs, options: ExecOptions | None = None) -> list[CoordinateSet]:
+    """prepare_layer_maps for a chain of strided layers applied one after
+    another (an encoder's downsampling path), with ONE host read for all
+    output counts when every window proposes one candidate per input (K = s);
+    otherwise level by level.  Returns the output coordinate set of each
+    layer; maps are cached on the input sets as sparse_conv_forward would.
+    Result-identical to running the layers."""
+    opts = options or ExecOptions()
+    if not opts.map_reuse:
+        raise ValueError("prepared maps are kept in the map-reuse cache")
+    cset = t.coordset if isinstance(t, SparseTensor) else t
+    dim = len(cset.boundary)
+    steps = [(enumerate_offsets(dim, sp.kernel_size), sp.stride) for sp in specs]
+    chainable = all(sp.stride > 1 and sp.kernel_size == sp.stride for sp in specs)
+    if not chainable or not specs:
+        out, cs = [], cset
+        for sp in specs:
+            cs = prepare_layer_maps(cs, sp, opts)
+            out.append(cs)
+        return out
+    # already prepared (same coordinate set): nothing to do
+    hit = cset.maps.get((specs[0].kernel_size, specs[0].stride, steps[0][0].base))
+    if hit is not None and len(specs) == 1:
+        return [hit[0]]
+    levels = compute_output_coords_chain(cset, steps)
+    out, cs = [], cset
+    for sp, (off, stride), (oc, ob) in zip(specs, steps, levels):
+        key = (sp.kernel_size, stride, off.base)
+        hit = cs.maps.get(key)
+        if hit is None:
+            nxt = CoordinateSet(oc, ob, cs.batch_size)
+            kind = (opts.index_kind or (sp.strategy.index_kind if sp.strategy else None)
+                    or sp.index_kind or "auto")
+            index = build_index(cs, kind, cell_cap=opts.grid_cell_cap)
+            cs.maps[key] = (nxt, map_search(index, nxt.coords, off, stride))
+            hit = cs.maps[key]
+        cs = hit[0]
+        out.append(cs)
+    return out
+
+
 def sparse_conv_forward(t: SparseTensor, w: WeightTensor, spec: LayerSpec,
                         strategy: LayerStrategy | None = None, map_cache: dict | None = None,
                         options: ExecOptions | None = None, *,
@@ -789,11 +847,8 @@ def sparse_conv_forward(t: SparseTensor, w: WeightTensor, spec: LayerSpec,
                                             out_cset.coords, t.boundary, t.batch_size)
     out = _run_dataflow(t.features, kmap, w, strat, schedule, symmetric, opts, center, epilogue,
                         record)
-    with _timed(timer, label, "other"):
-        result = SparseTensor(None, out, stride=t.stride * spec.stride,
-                              boundary=out_cset.boundary, batch_size=t.batch_size,
-                              coordset=out_cset)
-    return result
+    return SparseTensor._wrap(out, t.stride * spec.stride, out_cset.boundary, t.batch_size,
+                              out_cset)
 
 
 def inverse_conv_forward(t: SparseTensor, w: WeightTensor, spec: LayerSpec, map_cache: dict,
@@ -820,11 +875,8 @@ def inverse_conv_forward(t: SparseTensor, w: WeightTensor, spec: LayerSpec, map_
                                             entry.in_coords, entry.in_boundary, t.batch_size)
     out = _run_dataflow(t.features, swapped, w, strat, schedule, False, opts, None, epilogue,
                         record)
-    with _timed(timer, label, "other"):
-        cset = entry.in_coordset or CoordinateSet(entry.in_coords, entry.in_boundary, t.batch_size)
-        result = SparseTensor(None, out, stride=entry.in_stride, boundary=entry.in_boundary,
-                              batch_size=t.batch_size, coordset=cset)
-    return result
+    cset = entry.in_coordset or CoordinateSet(entry.in_coords, entry.in_boundary, t.batch_size)
+    return SparseTensor._wrap(out, entry.in_stride, tuple(entry.in_boundary), t.batch_size, cset)
 
 
 _POINTWISE = {"relu": 0, "bias_add": 1, "bn_fold": 2}

@@ -65,8 +65,22 @@ class KernelOffsets:
         return int(self.offsets[0, 0]) if self.volume else 0
 
 
+_OFFSETS_CACHE: dict = {}
+
+
 def enumerate_offsets(dim: int, kernel_size: int) -> KernelOffsets:
-    """All K**D offsets in lexicographic order (mapping.py:63-79)."""
+    """All K**D offsets in lexicographic order (mapping.py:63-79).  Cached
+    (immutable) per (dim, K, even-K base)."""
+    key = (dim, kernel_size, EVEN_KERNEL_OFFSET_BASE)
+    hit = _OFFSETS_CACHE.get(key)
+    if hit is not None:
+        return hit
+    hit = _enumerate_offsets(dim, kernel_size)
+    _OFFSETS_CACHE[key] = hit
+    return hit
+
+
+def _enumerate_offsets(dim: int, kernel_size: int) -> KernelOffsets:
     if not 1 <= dim <= 4:
         raise ValueError("dim must be between 1 and 4")
     if kernel_size < 1:
@@ -189,6 +203,53 @@ def compute_output_coords(in_coords, offsets: KernelOffsets, stride: int, out_bo
     return out
 
 
+def compute_output_coords_chain(cset, steps) -> list[torch.Tensor]:
+    """Output coordinates of successive strided levels, ``steps`` = [(offsets,
+    stride), ...] applied one after the other starting from ``cset``.  Level
+    i+1 is generated from level i's keys with its count on the device
+    (scb_output_keys_next), so the whole chain costs ONE host read.  Each
+    level equals compute_output_coords of the previous one.  Only for windows
+    that propose one candidate per input (K = s, e.g. k2 s2), where the
+    capacity does not grow along the chain."""
+    lib = nat.load()
+    c = cset.coords
+    dev = c.device
+    dim = c.shape[1] - 1
+    n_cap = c.shape[0]
+    counts = torch.zeros(max(len(steps), 1), dtype=torch.int64, device=dev)
+    boundary, prev = cset.boundary, None
+    levels = []
+    for i, (offsets, stride) in enumerate(steps):
+        out_b = downsample_boundary(boundary, stride)
+        g = nat.make_grid(out_b, cset.batch_size)
+        cap = int(lib.scb_output_coords_capacity(n_cap, dim, offsets.kernel_size, stride))
+        if cap > n_cap and i:
+            raise ValueError("chained output coordinates need one candidate per input")
+        ws_bytes = int(lib.scb_output_coords_workspace(n_cap, dim, offsets.kernel_size, stride))
+        ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
+        keys = torch.empty(max(cap, 1), dtype=torch.int64, device=dev)
+        cnt = counts.data_ptr() + 8 * i
+        if prev is None:
+            nat.call("scb_output_coords", nat.ptr(c), n_cap, g, offsets.kernel_size,
+                     offsets.base, stride, nat.ptr(ws), ws_bytes, nat.ptr(keys), cnt,
+                     nat.stream_handle())
+        else:
+            pkeys, pcnt, pgrid = prev
+            nat.call("scb_output_keys_next", nat.ptr(pkeys), pcnt, n_cap, pgrid, g,
+                     offsets.kernel_size, offsets.base, stride, nat.ptr(ws), ws_bytes,
+                     nat.ptr(keys), cnt, nat.stream_handle())
+        levels.append((keys, g, out_b, ws))
+        prev = (keys, cnt, g)
+        boundary, n_cap = out_b, cap
+    host = counts.cpu().tolist()  # the chain's one host read
+    out = []
+    for (keys, g, out_b, _), n in zip(levels, host):
+        co = torch.empty((n, dim + 1), dtype=torch.int32, device=dev)
+        nat.call("scb_unflatten", nat.ptr(keys), n, g, nat.ptr(co), nat.stream_handle())
+        out.append((co, out_b))
+    return out
+
+
 def _hit_matrix(volume: int, n: int, device) -> torch.Tensor:
     """Uninitialised [V][ld] int32 hit matrix; ld = n rounded up to 4
     (scb_hits_ld) so each row is 16-byte aligned."""
@@ -245,6 +306,12 @@ class KernelMap:
     def from_hits(cls, hits, offsets, stride, n_in, n_out, symmetric=False) -> "KernelMap":
         return cls(None, None, None, None, offsets, stride, n_in, n_out, symmetric,
                    trusted=True, hits=hits)
+
+    def device_tensors(self):
+        out = [t for t in (self._hits,) if t is not None]
+        if self._csr is not None:
+            out += [self._csr[0], self._csr[2], self._csr[3]]
+        return out
 
     # ---- representations ------------------------------------------------
     def _ensure_csr(self):

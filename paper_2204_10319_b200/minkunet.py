@@ -101,17 +101,46 @@ class EngineMinkUNet:
         # materialise device weights now (not inside a timed step)
         for name, w in self.w.items():
             w.packed_f16()
+        # mapping work (coordinate pyramid, hash indexes, kernel maps) runs
+        # here, off the compute stream: it depends on coordinates only, so
+        # the next batch's maps overlap this batch's convolutions
+        self.mapping_stream = torch.cuda.Stream(priority=-1)
+
+    def _prepare_maps(self, t, opts):
+        """The coordinate pyramid and every level's k3 map, on the mapping
+        stream.  Each strided level needs one host read (its output count);
+        it waits for mapping work only, never for queued convolutions, and
+        the convolutions are then issued without any host sync."""
+        import torch
+        from .execution import LayerSpec, prepare_layer_maps, prepare_strided_chain
+        cur = torch.cuda.current_stream()
+        ms = self.mapping_stream
+        cs = t.coordset
+        if cs.stream is None or cs.stream != ms:
+            ms.wait_stream(cur)  # coordinates produced elsewhere: order after them
+        levels = [cs]
+        with torch.cuda.stream(ms):
+            downs = [LayerSpec(2, 2, self.w[f"down{i}"].c_in, self.w[f"down{i}"].c_out)
+                     for i in range(1, 5)]
+            levels += prepare_strided_chain(cs, downs, opts)
+            for cs in levels:
+                prepare_layer_maps(cs, LayerSpec(3, 1, 1, 1), opts)
+        cur.wait_stream(ms)
+        for cs in levels:  # allocated on the mapping stream, read on this one
+            for x in cs.device_tensors():
+                x.record_stream(cur)
 
     def forward(self, t, options=None):
         from .execution import (ExecOptions, LayerSpec, inverse_conv_forward,
                                 sparse_conv_forward)
         from dataclasses import replace
-        base = options or ExecOptions()
+        base = replace(options) if options is not None else ExecOptions()  # private copy
         cache = {}
 
         def conv(x, name, k, s, relu=True, reuse=None, kind="conv", residual=None):
             w = self.w[name]
-            opts = replace(base, layer_label=name)
+            opts = base
+            opts.layer_label = name
             ep = {"relu": relu, "residual": residual}
             if name in self.bn:
                 ep.update(scale=self.bn[name][0], shift=self.bn[name][1])
@@ -133,15 +162,8 @@ class EngineMinkUNet:
             return a.replace_features(torch.cat([a.features, b.features], dim=1))
 
         names = {l["name"] for l in self.table}
-        # the coordinate pyramid first: each strided level needs one host
-        # read (its output count), done while nothing else is queued, so the
-        # convolutions below are issued without a host sync
-        from .execution import prepare_layer_maps
-        cs = t.coordset
         if base.map_reuse:
-            for i in range(1, 5):
-                w = self.w[f"down{i}"]
-                cs = prepare_layer_maps(cs, LayerSpec(2, 2, w.c_in, w.c_out), base)
+            self._prepare_maps(t, base)
         x = conv(t, "stem.0", 3, 1)
         x = conv(x, "stem.1", 3, 1)
         skips = [x]

@@ -527,3 +527,25 @@ def test_fp16_saturation_warns(sc):
         q = sc.quantize_features(t, sc.PrecisionMode.FP16_STORAGE)
         f = q.features_numpy()
     assert f[0, 0] == 65504 and f[0, 1] == -65504 and f[0, 2] == 1.0
+
+
+def test_strided_chain_equals_level_by_level(sc):
+    """compute_output_coords_chain (device counts, one host read) gives the
+    coordinates and maps of running each k2 s2 level on its own, bit-exact
+    against the oracle (mapping.py:216-248)."""
+    from paper_2204_10319_b200 import workloads
+    coords, _, boundary = workloads.config1_cloud()
+    t = sc.SparseTensor(coords, np.zeros((coords.shape[0], 8), np.float16), 1, boundary, 1)
+    specs = [sc.LayerSpec(2, 2, 8, 8)] * 4
+    levels = sc.prepare_strided_chain(t, specs, sc.ExecOptions())
+    c, b = np.asarray(coords, np.int64), tuple(boundary)
+    cs = t.coordset
+    for lvl in levels:
+        ob = O.downsample_boundary(b, 2)
+        want = O.output_coords(c, 2, 2, ob, 1)
+        np.testing.assert_array_equal(lvl.coords.cpu().numpy().astype(np.int64), want)
+        kmap = cs.maps[(2, 2, 0)][1]
+        pairs = O.kernel_map(c, b, want, 2, 2, 1)
+        for got, ref in zip(kmap.pairs, pairs):
+            np.testing.assert_array_equal(got, ref)
+        c, b, cs = want, ob, lvl
