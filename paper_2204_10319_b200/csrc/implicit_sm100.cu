@@ -3,27 +3,32 @@
 //
 //   out[k] = epilogue( sum_n  features[hits[n][k]] . W[n] )      (absent -> 0)
 //
-// for super-tiles of T x 128 output rows, accumulating all V offsets in TMEM
-// (T accumulators, double-buffered).  The gather is fused into the operand
-// load: cp.async moves each present neighbour's 16-B row chunks straight into
-// the 128/64/32-B swizzled UMMA layout (absent neighbours are zero), so neither
-// the gather buffer nor the f32 partials ever reach HBM.  Each weight slice
-// W[n][k-chunk] is brought in by TMA once per super-tile and feeds T MMAs
-// (weight re-streaming from L2 was the measured limit at T = 1: a 96->96 k3
-// layer reloads 486 KB of weights per 128 rows).  Each output row is written
-// once (fp16) with BN / bias / residual / ReLU applied in registers.  Offsets
-// with no neighbour in a tile skip that tile's MMAs.
+// for 128-row output tiles, accumulating all V offsets in TMEM (double-
+// buffered accumulators, so the epilogue of tile i overlaps tile i+1).  The
+// gather is fused into the operand load: cp.async moves each present
+// neighbour's 16-B row chunks straight into the 128/64/32-B swizzled UMMA
+// layout (absent neighbours are zero), so neither the gather buffer nor the
+// f32 partials ever reach HBM.  Each output row is written once (fp16) with
+// BN / bias / residual / ReLU applied in registers.  V = 1 is the K=1 layer
+// (identity map, no hit matrix).
 //
-// Producers never block on their own copies: each thread's stage completion
-// is tracked by cp.async.mbarrier.arrive.noinc (LAG < 0), so the copy loop
-// runs ahead as far as free stages allow.  (LAG >= 0: the older
-// wait_group<LAG> + arrive scheme, kept for comparison.)
+// Pipeline (per stage: `ops` offsets x one K chunk of A and B):
+//   * producers never block on their own copies: each thread's completion is
+//     tracked by cp.async.mbarrier.arrive.noinc, absent rows are zero-filled
+//     by zero-size cp.async, so every write of a stage is async-tracked;
+//   * copies are lane-per-chunk (the CPR lanes of a row copy its consecutive
+//     16-B chunks), P threads per row split the chunks;
+//   * the MMA warp runs converged (stage indices and descriptors in uniform
+//     registers) and one elected lane issues; descriptors advance by
+//     constant steps.
+// (Measured on the MinkUNet level-0 96->96 layer: 1.27 ms for the first
+// row-per-thread / wait_group version, 0.73 ms with the above.)
 //
-// Warp roles (64 + 128 T + 128 threads, persistent over contiguous
-// super-tile ranges):
+// Warp roles (64 + 128 P + 128 threads, persistent over contiguous tile
+// ranges, 1 or 2 CTAs per SM):
 //   warp 0        TMA producer of the weight slices (B, K-major fp16)
-//   warp 1        TMEM allocator + single-thread tcgen05.mma issuer
-//   warps 2..     A producers: thread (h, r) owns row r of tile h
+//   warp 1        TMEM allocator + MMA issuer
+//   warps 2..     A producers (P per output row)
 //   last 4 warps  epilogue: tcgen05.ld -> epilogue -> swizzled smem -> TMA store
 #include <cuda.h>
 
@@ -40,27 +45,24 @@ namespace ic {
 using namespace ::scb::ptx;
 
 constexpr int BM = 128;
-constexpr int MAX_T = 4;                // tiles per super-tile
 constexpr int EPI_BUF = 32 * 64;        // 32 rows x 64 B (32 fp16 columns)
-constexpr int EPI_MAX_BYTES = 4 * 2 * EPI_BUF;  // epilogue staging: 4 warps x (1 or 2) buffers
 constexpr int MAX_OPS = 8;              // kernel offsets per pipeline stage
-constexpr int MAX_V = 27;
 
 struct Params {
   long long n_out;
   int n_in, c_in, c_out, V, n_pad, kc, n_kchunks, stages, swz, epi_cols, total_tiles, relu;
   int ops;                  // offsets per stage (small C_in -> several)
   int epi_bufs;             // epilogue staging buffers per warp (1 or 2)
-  int debug;                // SCB_IMPLICIT_DEBUG: 1 no A loads, 2 no MMAs, 16 wait counters, 32 no B loads
-  int groups;               // ceil(V / ops) offset groups per super-tile
+  int debug;                // SCB_IMPLICIT_DEBUG: 1 no A loads, 16 wait counters, 32 no B loads
+  int groups;               // ceil(V / ops) offset groups per tile
   uint32_t idesc, tmem_cols;
-  uint32_t a_off_bytes;     // one (offset, tile) A block [128 rows][kc] (1024-aligned)
+  uint32_t a_off_bytes;     // one offset's A block [128 rows][kc] (1024-aligned)
   uint32_t b_off_bytes;     // one offset's B block [n_pad][kc]   (1024-aligned)
   uint32_t a_stage_bytes, stage_bytes;
-  uint32_t a_tx, b_tx;      // bytes one offset's A / B loads deliver
+  uint32_t b_tx;            // bytes one offset's B load delivers
   long long ldf, ldh;       // feature row stride, hit-matrix row stride
   const __half* feat;       // [n_in][ldf]
-  const int* hits;          // [V][ldh] input row or -1
+  const int* hits;          // [V][ldh] input row or -1 (unused for V = 1)
   const float* scale;       // nullable (with shift)
   const float* shift;
   const float* bias;        // nullable
@@ -73,7 +75,7 @@ __device__ __forceinline__ uint32_t swz_off(int row, int chunk, int swz) {
   return row * 32 + ((chunk ^ ((row >> 2) & 1)) << 4);
 }
 
-// SCB_IMPLICIT_DEBUG bit 16: per-role wait-cycle counters of CTA 0.
+// SCB_IMPLICIT_DEBUG bit 16: per-role cycle counters of CTA 0.
 __device__ unsigned long long g_ic_prof[16];
 #define IC_PROF(idx, cond, ...)                                                       \
   do {                                                                                \
@@ -95,24 +97,29 @@ __device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-template <int V, int LAG, int KC, int T, int COAL, int MINB>
-__global__ void __launch_bounds__(64 + 128 * T + 128, MINB)
+template <int V, int KC, int P, int MINB>
+__global__ void __launch_bounds__(64 + 128 * P + 128, MINB)
     implicit_conv_f16_kernel(const __grid_constant__ CUtensorMap tmB,
                              const __grid_constant__ CUtensorMap tmOut,
                              const __grid_constant__ Params p) {
-  constexpr int NPROD = 128 * T;           // A-producer threads (one per super-tile row)
-  constexpr int EPI0 = 2 + 4 * T;          // first epilogue warp
-  constexpr bool NOINC = LAG < 0;
+  constexpr int NPROD = 128 * P;           // A-producer threads
+  constexpr int EPI0 = 2 + 4 * P;          // first epilogue warp
+  constexpr int CPR = KC / 8;              // 16-B chunks per row per K chunk
+  constexpr int IT = CPR / P;              // chunks a producer thread copies per offset
+  constexpr int SWZ = KC * 2;              // swizzle span = row bytes
+  constexpr int MAXO = (32 / IT) < MAX_OPS ? (32 / IT) : MAX_OPS;
+  constexpr int NT = (V + P - 1) / P;      // offsets whose index a thread prefetches
+  static_assert(IT >= 1 && IT * P == CPR, "P must divide the chunks per row");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* epi_base = smem + (size_t)p.stages * p.stage_bytes;
-  int* nbr_s = (int*)(epi_base + 4 * p.epi_bufs * EPI_BUF);      // [V][NPROD] neighbour rows
-  uint64_t* full = (uint64_t*)(nbr_s + V * NPROD);
+  int* nbr_s = (int*)(epi_base + 4 * p.epi_bufs * EPI_BUF);      // [V][BM] neighbour rows of the tile
+  uint64_t* full = (uint64_t*)(nbr_s + V * BM);
   uint64_t* empty = full + p.stages;
   uint64_t* tfull = empty + p.stages;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
-  uint32_t* wmask = tmem_slot + 4;  // [stages][NPROD]: blocks each thread's items hold data in
+  uint32_t* wmask = tmem_slot + 4;  // [stages][NPROD]: which of a thread's items hold data
 
   const long long k_t0 = clock64();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -121,8 +128,7 @@ __global__ void __launch_bounds__(64 + 128 * T + 128, MINB)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < p.stages; ++s) {
-      // producers: one (async, noinc) arrive per thread + the B expect_tx arrive
-      mbar_init(full + s, NPROD + 1);
+      mbar_init(full + s, NPROD + 1);  // one async (noinc) arrive per producer + the B expect_tx
       mbar_init(empty + s, 1);
     }
     for (int a = 0; a < 2; ++a) {
@@ -168,23 +174,23 @@ __global__ void __launch_bounds__(64 + 128 * T + 128, MINB)
         }
     }
   } else if (warp >= 2 && warp < EPI0) {
-    // ============ A producers.  Thread (h, r) owns output row r of tile h of
-    // the super-tile: it prefetches its neighbour rows one super-tile ahead
-    // (registers), parks them in its private smem slots, and copies its row
-    // of every (offset, k-chunk) block: CPR predicated 16-B cp.async
-    // (present) or zero stores (absent, only where the slot held data).
+    // ============ A producers.  Thread (h, row) prefetches the neighbour
+    // rows of output row `row` for the offsets n = h (mod P) one tile ahead
+    // and parks them in the tile's index table.  Copies are lane-per-chunk:
+    // item `it` of thread pt is chunk (pt % CPR) of row it * (NPROD / CPR) +
+    // pt / CPR, so consecutive lanes copy consecutive 16-B chunks of a row.
     const int pt = threadIdx.x - 64;
     const int row = pt & (BM - 1);
-    const int h = (pt >> 7) % T;
-    const int wbyte = (pt >> 5) & 3;
-    constexpr int CPR = KC / 8;               // 16-B chunks per row per K chunk
-    constexpr int SWZ = KC * 2;               // swizzle span = row bytes
-    int nxt[V];
+    const int h = pt >> 7;
+    int nxt[NT];
     {
-      const long long k = ((long long)t_begin * T + h) * BM + row;
+      const long long k = (long long)t_begin * BM + row;
 #pragma unroll
-      for (int n = 0; n < V; ++n)
-        nxt[n] = (t_begin < t_end && k < p.n_out) ? (V == 1 ? (int)k : __ldg(p.hits + (long long)n * p.ldh + k)) : -1;
+      for (int i = 0; i < NT; ++i) {
+        const int n = h + i * P;
+        nxt[i] = (n < V && t_begin < t_end && k < p.n_out)
+                     ? (V == 1 ? (int)k : __ldg(p.hits + (long long)n * p.ldh + k)) : -1;
+      }
     }
     for (int s = 0; s < p.stages; ++s) {
       const uint32_t base = smem_u32(smem + (size_t)s * p.stage_bytes);
@@ -192,36 +198,38 @@ __global__ void __launch_bounds__(64 + 128 * T + 128, MINB)
         asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(base + b), "r"(0) : "memory");
       wmask[s * NPROD + pt] = 0u;
     }
-    asm volatile("bar.sync 1, %0;" ::"n"(NPROD) : "memory");
-    int stage = 0, sig = 0, pending = 0;
+    int stage = 0;
     uint32_t phase = 0;
     const uint32_t nb_s0 = smem_u32(nbr_s);
-    const uint32_t nb_s = nb_s0 + (uint32_t)pt * 4u;
-    const int rx = SWZ == 128 ? (row & 7) : (SWZ == 64 ? ((row >> 1) & 3) : ((row >> 2) & 1));
-    const int cr = row / CPR, cc = row % CPR;   // COAL: row group / chunk of this lane
-    uint32_t roff[CPR];                         // COAL: smem offset of item it in a block
+    const int cr = pt / CPR, cc = pt % CPR;   // row group / chunk of this lane
+    uint32_t roff[IT];                        // smem offset of item it inside a block
 #pragma unroll
-    for (int it = 0; it < CPR; ++it) {
-      const int r = it * (BM / CPR) + cr;
+    for (int it = 0; it < IT; ++it) {
+      const int r = it * (NPROD / CPR) + cr;
       const int rxr = SWZ == 128 ? (r & 7) : (SWZ == 64 ? ((r >> 1) & 3) : ((r >> 2) & 1));
       roff[it] = (uint32_t)(r * (KC * 2)) + ((uint32_t)(cc ^ rxr) << 4);
     }
     const uint32_t ldfb = (uint32_t)(p.ldf * 2);  // feature row stride in bytes (host-checked < 2^32)
     for (int t = t_begin; t < t_end; ++t) {
-      // COAL: rows are copied by other threads, so the (single) table is
-      // rewritten only after every producer finished the previous tile
-      if constexpr (COAL) asm volatile("bar.sync 1, %0;" ::"n"(NPROD) : "memory");
-      const uint32_t nbw = nb_s;
+      // the table is read by other threads: rewrite it only after every
+      // producer finished the previous tile (the first barrier also orders
+      // the zeroed stage buffers before any copy)
+      asm volatile("bar.sync 1, %0;" ::"n"(NPROD) : "memory");
 #pragma unroll
-      for (int n = 0; n < V; ++n) {
-        asm volatile("st.shared.b32 [%0], %1;" ::"r"(nbw + (uint32_t)(n * NPROD * 4)), "r"(nxt[n]) : "memory");
+      for (int i = 0; i < NT; ++i) {
+        const int n = h + i * P;
+        if (n < V)
+          asm volatile("st.shared.b32 [%0], %1;" ::"r"(nb_s0 + (uint32_t)((n * BM + row) * 4)), "r"(nxt[i]) : "memory");
       }
-      if constexpr (COAL) asm volatile("bar.sync 1, %0;" ::"n"(NPROD) : "memory");
+      asm volatile("bar.sync 1, %0;" ::"n"(NPROD) : "memory");
       {
-        const long long k = ((long long)(t + 1) * T + h) * BM + row;
+        const long long k = (long long)(t + 1) * BM + row;
         const bool ok = (t + 1 < t_end) && k < p.n_out;
 #pragma unroll
-        for (int n = 0; n < V; ++n) nxt[n] = ok ? (V == 1 ? (int)k : __ldg(p.hits + (long long)n * p.ldh + k)) : -1;
+        for (int i = 0; i < NT; ++i) {
+          const int n = h + i * P;
+          nxt[i] = (ok && n < V) ? (V == 1 ? (int)k : __ldg(p.hits + (long long)n * p.ldh + k)) : -1;
+        }
       }
       for (int g = 0; g < p.groups; ++g) {
         const int nv = min(p.ops, V - g * p.ops);
@@ -231,98 +239,46 @@ __global__ void __launch_bounds__(64 + 128 * T + 128, MINB)
           const uint32_t dst = smem_u32(smem + (size_t)stage * p.stage_bytes);
           const int col0 = kk * KC;
           const int live = min(CPR, (p.c_in - col0) / 8);  // chunks inside C_in
-          // Stage buffers start zeroed and each 16-B item of a block has one
-          // owner thread, so a thread only writes what changes: present ->
-          // copy; absent but written by the slot's previous use -> re-zero;
+          // Stage buffers start zeroed and each 16-B item has one owner
+          // thread, so a thread only writes what changes: present -> copy;
+          // absent but written by the slot's previous use -> zero-fill;
           // absent and already zero -> nothing.  Chunks past C_in stay zero.
           uint32_t* wm = wmask + stage * NPROD + pt;
           uint32_t now = *wm;
-          if constexpr (COAL) {
-            // lane-per-chunk: the CPR lanes of a row copy its consecutive
-            // 16-B chunks (one warp instruction touches 32 / CPR rows).  An
-            // offset's CPR index loads go first (volatile asm keeps the order)
-            // so their latencies overlap; then one IMAD.WIDE per copy.
-            const uint32_t nbc = nb_s0 +
-                                 (uint32_t)((g * p.ops * NPROD + h * BM + cr) * 4);
-            const uint64_t fbase = reinterpret_cast<uint64_t>(p.feat) + (uint64_t)((col0 + cc * 8) * 2);
-            const bool live_c = cc < live && !(p.debug & 1);
-            for (int o = 0; o < nv; ++o) {
-              int jj[CPR];
+          const uint32_t nbc = nb_s0 + (uint32_t)((g * p.ops * BM + cr) * 4);
+          const uint64_t fbase = reinterpret_cast<uint64_t>(p.feat) + (uint64_t)((col0 + cc * 8) * 2);
+          const bool live_c = cc < live && !(p.debug & 1);
+          for (int o = 0; o < nv; ++o) {
+            int jj[IT];  // index loads first (volatile asm keeps the order): latencies overlap
 #pragma unroll
-              for (int it = 0; it < CPR; ++it)
-                asm volatile("ld.shared.b32 %0, [%1];" : "=r"(jj[it]) : "r"(nbc + (uint32_t)((o * NPROD + it * (BM / CPR)) * 4)));
-              const uint32_t blk = dst + (o * T + h) * p.a_off_bytes;
+            for (int it = 0; it < IT; ++it)
+              asm volatile("ld.shared.b32 %0, [%1];" : "=r"(jj[it]) : "r"(nbc + (uint32_t)((o * BM + it * (NPROD / CPR)) * 4)));
+            const uint32_t blk = dst + o * p.a_off_bytes;
 #pragma unroll
-              for (int it = 0; it < CPR; ++it) {
-                const int j = jj[it];
-                const bool present = j >= 0;
-                constexpr int MAXO = (32 / CPR) < MAX_OPS ? (32 / CPR) : MAX_OPS;
-                const uint32_t bit = 1u << (it * MAXO + o);
-                const bool rezero = !present && (now & bit);
-                const void* src = reinterpret_cast<const void*>(
-                    fbase + (uint64_t)(uint32_t)max(j, 0) * (uint64_t)ldfb);
-                cp_async16_zfill_if(blk + roff[it], src, present, (present || rezero) && live_c);
-                now = present ? (now | bit) : (now & ~bit);
-              }
-            }
-          } else {
-            for (int o = 0; o < nv; ++o) {
-              const int n = g * p.ops + o;
-              int j;
-              asm volatile("ld.shared.b32 %0, [%1];" : "=r"(j) : "r"(nb_s + (uint32_t)(n * NPROD * 4)));
-              const bool present = j >= 0 && !(p.debug & 1);
-              const bool rezero = !present && ((now >> o) & 1u);
-              const uint32_t base = dst + (o * T + h) * p.a_off_bytes + row * (KC * 2);
-              const __half* src = p.feat + (long long)max(j, 0) * p.ldf + col0;
-#pragma unroll
-              for (int c = 0; c < CPR; ++c) {
-                const uint32_t d = base + ((uint32_t)(c ^ rx) << 4);
-                if constexpr (NOINC) {
-                  // absent rows: zero-size cp.async zero-fills without a read,
-                  // so every write of the stage is tracked by the async arrive
-                  cp_async16_zfill_if(d, src + c * 8, present, (present || rezero) && c < live);
-                } else {
-                  cp_async16_if(d, src + c * 8, present && c < live);
-                  st_zero16_if(d, rezero && c < live);
-                }
-              }
-              now = (now & ~(1u << o)) | ((uint32_t)present << o);
+            for (int it = 0; it < IT; ++it) {
+              const int j = jj[it];
+              const bool present = j >= 0;
+              const uint32_t bit = 1u << (it * MAXO + o);
+              const bool rezero = !present && (now & bit);
+              const void* src = reinterpret_cast<const void*>(
+                  fbase + (uint64_t)(uint32_t)max(j, 0) * (uint64_t)ldfb);
+              cp_async16_zfill_if(blk + roff[it], src, present, (present || rezero) && live_c);
+              now = present ? (now | bit) : (now & ~bit);
             }
           }
           *wm = now;
           if ((p.debug & 16) && blockIdx.x == 0 && pt == 0) atomicAdd(&g_ic_prof[11], (unsigned long long)(clock64() - a_t0));
-          if constexpr (NOINC) {
-            cp_async_arrive_noinc(full + stage);   // fires when this thread's copies land
-          } else {
-            cp_async_commit();
-            if (++pending > LAG) {
-              IC_PROF(1, pt == 0, cp_async_wait<(LAG < 0 ? 0 : LAG)>());
-              fence_async_smem();  // generic -> async proxy
-              mbar_arrive(full + sig);
-              if (++sig == p.stages) sig = 0;
-              --pending;
-            }
-          }
+          cp_async_arrive_noinc(full + stage);   // fires when this thread's copies land
           if (++stage == p.stages) { stage = 0; phase ^= 1; }
         }
-      }
-    }
-    if constexpr (!NOINC) {
-      cp_async_wait<0>();
-      fence_async_smem();
-      while (pending > 0) {
-        mbar_arrive(full + sig);
-        if (++sig == p.stages) sig = 0;
-        --pending;
       }
     }
   } else if (warp == 1) {
     // ============ MMA issuer.  The whole warp runs the loop (so stage
     // indices and descriptors stay warp-uniform, in uniform registers) and
-    // one elected lane issues.  Every (offset, tile) block of a stage is
-    // multiplied (a tile rarely lacks an offset entirely, and the per-block
-    // test cost more issue time than the MMAs it saved); stage descriptors
-    // advance by constant steps, so the loop body is the MMAs.
+    // one elected lane issues.  Every offset block of a stage is multiplied
+    // (a tile rarely lacks an offset entirely, and a per-block test cost more
+    // issue time than the MMAs it saved).
     const uint32_t layout = p.swz == 128 ? 2u : (p.swz == 64 ? 4u : 6u);
     const uint32_t sbo = 8u * (uint32_t)p.swz;
     const uint64_t adesc_base = make_sdesc(smem_u32(smem), sbo, layout);
@@ -335,7 +291,7 @@ __global__ void __launch_bounds__(64 + 128 * T + 128, MINB)
     for (int t = t_begin; t < t_end; ++t) {
       IC_PROF(4, lane == 0, mbar_wait(tempty + acc, acc_phase ^ 1));
       tc_after();
-      const uint32_t d0 = tmem0 + (uint32_t)acc * T * n_pad;
+      const uint32_t d = tmem0 + (uint32_t)acc * n_pad;
       for (int g = 0; g < p.groups; ++g) {
         const int nv = min(p.ops, V - g * p.ops);
         for (int kk = 0; kk < p.n_kchunks; ++kk) {
@@ -345,20 +301,16 @@ __global__ void __launch_bounds__(64 + 128 * T + 128, MINB)
           const uint64_t bd = ad + a_stage_d;
           const uint32_t acc0 = (g | kk) ? 1u : 0u;
           if (elect_one()) {
-            if (!(p.debug & 64)) fence_async_smem();  // cp.async (generic proxy) data -> tcgen05 reads
+            fence_async_smem();  // cp.async (generic proxy) data -> tcgen05 reads
             tc_after();
 #pragma unroll
             for (int o = 0; o < MAX_OPS; ++o) {
               if (o < nv) {
+                const uint64_t a = ad + (uint64_t)(o * a_off_d);
+                const uint64_t b = bd + (uint64_t)(o * b_off_d);
+                mma_f16(d, a, b, idesc, o ? 1u : acc0);
 #pragma unroll
-                for (int h = 0; h < T; ++h) {
-                  const uint64_t a = ad + (uint64_t)((o * T + h) * a_off_d);
-                  const uint64_t b = bd + (uint64_t)(o * b_off_d);
-                  const uint32_t d = d0 + h * n_pad;
-                  mma_f16(d, a, b, idesc, o ? 1u : acc0);
-#pragma unroll
-                  for (int k = 1; k < KC / 16; ++k) mma_f16(d, a + 2u * k, b + 2u * k, idesc, 1u);
-                }
+                for (int k = 1; k < KC / 16; ++k) mma_f16(d, a + 2u * k, b + 2u * k, idesc, 1u);
               }
             }
             mma_commit(empty + stage);
@@ -382,83 +334,79 @@ __global__ void __launch_bounds__(64 + 128 * T + 128, MINB)
     for (int t = t_begin; t < t_end; ++t) {
       IC_PROF(5, warp == EPI0 && lane == 0, mbar_wait_sleep(tfull + acc, acc_phase, 256));
       tc_after();
-      for (int h = 0; h < T; ++h) {
-        const long long row0 = ((long long)t * T + h) * BM + 32 * q;
-        if (row0 >= p.n_out) break;
-        const long long k = row0 + lane;
-        const bool row_ok = k < p.n_out;
-        for (int j = 0; j < chunks; ++j) {
-          const int c0 = j * p.epi_cols;
-          const uint32_t taddr = tmem_base + ((uint32_t)(32 * q) << 16) +
-                                 (uint32_t)((acc * T + h) * p.n_pad + c0);
-          uint32_t r[32];
-          TMEM_LD_X16(taddr, r);
-          if (p.epi_cols == 32) TMEM_LD_X16(taddr + 16, (r + 16));
-          tmem_wait_ld();
-          float v[32];
+      const long long row0 = (long long)t * BM + 32 * q;
+      const long long k = row0 + lane;
+      const bool row_ok = k < p.n_out;
+      for (int j = 0; j < chunks && row0 < p.n_out; ++j) {
+        const int c0 = j * p.epi_cols;
+        const uint32_t taddr = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * p.n_pad + c0);
+        uint32_t r[32];
+        TMEM_LD_X16(taddr, r);
+        if (p.epi_cols == 32) TMEM_LD_X16(taddr + 16, (r + 16));
+        tmem_wait_ld();
+        float v[32];
 #pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-          const int ncol = p.epi_cols;
-          if (p.scale) {
+        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+        const int ncol = p.epi_cols;
+        if (p.scale) {
 #pragma unroll
-            for (int i = 0; i < 32; ++i)
-              if (i < ncol && c0 + i < p.c_out)
-                v[i] = v[i] * __ldg(p.scale + c0 + i) + __ldg(p.shift + c0 + i);
-          }
-          if (p.bias) {
+          for (int i = 0; i < 32; ++i)
+            if (i < ncol && c0 + i < p.c_out)
+              v[i] = v[i] * __ldg(p.scale + c0 + i) + __ldg(p.shift + c0 + i);
+        }
+        if (p.bias) {
 #pragma unroll
-            for (int i = 0; i < 32; ++i)
-              if (i < ncol && c0 + i < p.c_out) v[i] += __ldg(p.bias + c0 + i);
-          }
-          if (p.residual && row_ok) {
-            const uint4* rp = reinterpret_cast<const uint4*>(p.residual + k * p.c_out + c0);
+          for (int i = 0; i < 32; ++i)
+            if (i < ncol && c0 + i < p.c_out) v[i] += __ldg(p.bias + c0 + i);
+        }
+        if (p.residual && row_ok) {
+          const uint4* rp = reinterpret_cast<const uint4*>(p.residual + k * p.c_out + c0);
 #pragma unroll
-            for (int g = 0; g < 4; ++g) {
-              if (g * 8 < ncol && c0 + g * 8 < p.c_out) {
-                const uint4 w = __ldg(rp + g);
-                const __half2* hh = reinterpret_cast<const __half2*>(&w);
+          for (int g = 0; g < 4; ++g) {
+            if (g * 8 < ncol && c0 + g * 8 < p.c_out) {
+              const uint4 w = __ldg(rp + g);
+              const __half2* hh = reinterpret_cast<const __half2*>(&w);
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                  const float2 f = __half22float2(hh[e]);
-                  v[g * 8 + 2 * e] += f.x;
-                  v[g * 8 + 2 * e + 1] += f.y;
-                }
+              for (int e = 0; e < 4; ++e) {
+                const float2 f = __half22float2(hh[e]);
+                v[g * 8 + 2 * e] += f.x;
+                v[g * 8 + 2 * e + 1] += f.y;
               }
             }
           }
-          if (p.relu) {
-#pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
-          }
-          uint8_t* buf = bufs + nbuf * EPI_BUF;
-          if (lane == 0) {
-            if (p.epi_bufs == 2) IC_PROF(6, warp == EPI0, bulk_wait_read1());
-            else bulk_wait_read0();
-          }
-          __syncwarp();
-          if (ncol == 32) {
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              uint4 w = make_uint4(pack_half2(v[8 * c], v[8 * c + 1]), pack_half2(v[8 * c + 2], v[8 * c + 3]),
-                                   pack_half2(v[8 * c + 4], v[8 * c + 5]), pack_half2(v[8 * c + 6], v[8 * c + 7]));
-              *reinterpret_cast<uint4*>(buf + swz_off(lane, c, 64)) = w;
-            }
-          } else {
-#pragma unroll
-            for (int c = 0; c < 2; ++c) {
-              uint4 w = make_uint4(pack_half2(v[8 * c], v[8 * c + 1]), pack_half2(v[8 * c + 2], v[8 * c + 3]),
-                                   pack_half2(v[8 * c + 4], v[8 * c + 5]), pack_half2(v[8 * c + 6], v[8 * c + 7]));
-              *reinterpret_cast<uint4*>(buf + swz_off(lane, c, 32)) = w;
-            }
-          }
-          fence_async_smem();
-          __syncwarp();
-          if (lane == 0) {
-            tma_store_2d(&tmOut, buf, c0, (int)row0);
-            bulk_commit();
-          }
-          nbuf ^= p.epi_bufs - 1;
         }
+        if (p.relu) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
+        }
+        uint8_t* buf = bufs + nbuf * EPI_BUF;
+        if (lane == 0) {
+          if (p.epi_bufs == 2) IC_PROF(6, warp == EPI0, bulk_wait_read1());
+          else bulk_wait_read0();
+        }
+        __syncwarp();
+        if (ncol == 32) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            uint4 w = make_uint4(pack_half2(v[8 * c], v[8 * c + 1]), pack_half2(v[8 * c + 2], v[8 * c + 3]),
+                                 pack_half2(v[8 * c + 4], v[8 * c + 5]), pack_half2(v[8 * c + 6], v[8 * c + 7]));
+            *reinterpret_cast<uint4*>(buf + swz_off(lane, c, 64)) = w;
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            uint4 w = make_uint4(pack_half2(v[8 * c], v[8 * c + 1]), pack_half2(v[8 * c + 2], v[8 * c + 3]),
+                                 pack_half2(v[8 * c + 4], v[8 * c + 5]), pack_half2(v[8 * c + 6], v[8 * c + 7]));
+            *reinterpret_cast<uint4*>(buf + swz_off(lane, c, 32)) = w;
+          }
+        }
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(&tmOut, buf, c0, (int)row0);
+          bulk_commit();
+        }
+        nbuf ^= p.epi_bufs - 1;
       }
       tc_before();
       __syncwarp();
@@ -532,31 +480,29 @@ extern "C" int32_t scb_conv_implicit(const void* features, int64_t n_in, int32_t
     const char* e = getenv(name);
     return e ? atoi(e) : dflt;
   };
-  // Launch shape.  T tiles share every weight slice load; T accumulators are
-  // double-buffered in TMEM (2 T n_pad columns <= 512), and two CTAs per SM
-  // run when both fit (their producer loops fill each other's gaps).
-  const int T = 1;
+  // Launch shape: two CTAs per SM when both accumulator pairs fit in TMEM
+  // (C_out <= 128) -- one CTA's producer / MMA-issue gaps are filled by the
+  // other -- else one; P producer threads per output row.
   uint32_t cols = 32;
-  while (cols < (uint32_t)(2 * T * n_pad)) cols *= 2;
+  while (cols < (uint32_t)(2 * n_pad)) cols *= 2;
   p.tmem_cols = cols;
-  int ctas = (cols <= 256 && T <= 2) ? 2 : 1;
-  ctas = env_int("SCB_IMPLICIT_CTAS", ctas) == 2 ? 2 : 1;
-  if (cols > 256 || T > 2) ctas = 1;
-  p.total_tiles = (int)((n_out + (long long)BM * T - 1) / ((long long)BM * T));
+  int ctas = cols <= 256 ? 2 : 1;
+  ctas = env_int("SCB_IMPLICIT_CTAS", ctas) == 2 && cols <= 256 ? 2 : 1;
+  const int cpr = p.kc / 8;
+  int P = env_int("SCB_IC_P", 1) >= 2 ? 2 : 1;
+  if (cpr < P) P = 1;
+  const int nprod = 128 * P;
+  p.total_tiles = (int)((n_out + BM - 1) / BM);
   auto r1024 = [](uint32_t x) { return (x + 1023u) / 1024u * 1024u; };
-  p.a_tx = (uint32_t)(BM * p.kc * 2);
   p.b_tx = (uint32_t)(n_pad * p.kc * 2);
-  p.a_off_bytes = r1024(p.a_tx);
+  p.a_off_bytes = r1024((uint32_t)(BM * p.kc * 2));
   p.b_off_bytes = r1024(p.b_tx);
-  const uint32_t op_bytes = T * p.a_off_bytes + p.b_off_bytes;
+  const uint32_t op_bytes = p.a_off_bytes + p.b_off_bytes;
   int ops = (int)((uint32_t)env_int("SCB_IC_STAGE_KB", ctas == 2 ? 32 : 48) * 1024u / op_bytes);
-  ops = ops < 1 ? 1 : (ops > MAX_OPS ? MAX_OPS : ops);
-  if (ops > volume) ops = volume;
+  ops = std::max(1, std::min(ops, std::min(MAX_OPS, volume)));
   ops = std::max(1, std::min(env_int("SCB_IMPLICIT_OPS", ops), std::min(MAX_OPS, volume)));
-  ops = std::min(ops, 32 / (p.kc / 8));  // one presence bit per 16-B item of a producer thread
+  ops = std::min(ops, 32 / (cpr / P));  // one presence bit per 16-B item of a producer thread
   p.ops = ops;
-  p.groups = (volume + ops - 1) / ops;
-  p.a_stage_bytes = ops * T * p.a_off_bytes;
   p.stage_bytes = ops * op_bytes;
   p.ldf = ldf;
   p.ldh = hits_ld(n_out);
@@ -567,12 +513,10 @@ extern "C" int32_t scb_conv_implicit(const void* features, int64_t n_in, int32_t
   p.bias = bias;
   p.residual = (const __half*)residual;
   if (const char* dbg = getenv("SCB_IMPLICIT_DEBUG")) p.debug = atoi(dbg);
-  const int coal = env_int("SCB_IC_COAL", 1) ? 1 : 0;
-  const int nprod = 128 * T;
-  // shared memory: stages (A + B blocks and one presence word per producer
-  // thread) + epilogue staging + neighbour table + flags + barriers
+  // shared memory: stages (A + B blocks, one presence word per producer
+  // thread) + epilogue staging + the tile's neighbour table + barriers
   auto fixed_bytes = [&](int epi_bufs) {
-    return 1024 + 4 * epi_bufs * EPI_BUF + volume * nprod * 4 + 40 * 8 + 64;
+    return 1024 + 4 * epi_bufs * EPI_BUF + volume * BM * 4 + 40 * 8 + 64;
   };
   int smem_cap = ctas == 2 ? 113 * 1024 : 227 * 1024;
   auto fit = [&](int e) { return (smem_cap - fixed_bytes(e)) / (int)(p.stage_bytes + nprod * 4); };
@@ -588,15 +532,12 @@ extern "C" int32_t scb_conv_implicit(const void* features, int64_t n_in, int32_t
   p.epi_bufs = fit(2) >= fit(1) ? 2 : 1;
   if (const char* e = getenv("SCB_IC_EPI_BUFS")) p.epi_bufs = atoi(e) == 1 ? 1 : 2;
   p.groups = (volume + p.ops - 1) / p.ops;
-  p.a_stage_bytes = p.ops * T * p.a_off_bytes;
-  int stages = fit(p.epi_bufs);
-  if (stages > 16) stages = 16;
+  p.a_stage_bytes = p.ops * p.a_off_bytes;
+  int stages = std::min(fit(p.epi_bufs), 16);
   stages = std::min(stages, std::max(2, env_int("SCB_IC_STAGES", 16)));
   SCB_CHECK_ARG(stages >= 2, "stage does not fit in shared memory");
   p.stages = stages;
-  const int fixed = fixed_bytes(p.epi_bufs) + stages * nprod * 4;
-  const int smem = fixed + stages * (int)p.stage_bytes;
-  // LAG < 0: producers arrive asynchronously (cp.async.mbarrier.arrive.noinc)
+  const int smem = fixed_bytes(p.epi_bufs) + stages * (nprod * 4 + (int)p.stage_bytes);
 
   CUtensorMap mB, mO;
   std::string err;
@@ -609,42 +550,44 @@ extern "C" int32_t scb_conv_implicit(const void* features, int64_t n_in, int32_t
   }
   const int grid = p.total_tiles < ctas * device_sms() ? p.total_tiles : ctas * device_sms();
   cudaStream_t s = as_stream(stream);
-  auto launch = [&](auto kernel, int threads) -> int {
+  auto launch = [&](auto kernel) -> int {
     SCB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_cap));
-    kernel<<<grid, threads, smem, s>>>(mB, mO, p);
+    kernel<<<grid, 64 + nprod + 128, smem, s>>>(mB, mO, p);
     return SCB_OK;
   };
   int rc = SCB_EINVAL;
-  // instantiated: T = 1, async producer arrival, coalesced or row-per-thread
-  // copies, one or two CTAs per SM (T > 1 and the wait_group scheme measured
-  // slower on the MinkUNet layers and are not built)
-#define SCB_IC_LAUNCH_T(VV, KK)                                                                \
-  if (coal) {                                                                                  \
-    if (ctas == 2) rc = launch(implicit_conv_f16_kernel<VV, -1, KK, 1, 1, 2>, 320);            \
-    else rc = launch(implicit_conv_f16_kernel<VV, -1, KK, 1, 1, 1>, 320);                      \
+#define SCB_IC_LAUNCH_P(VV, KK)                                                                \
+  if (P == 2) {                                                                                \
+    rc = ctas == 2 ? launch(implicit_conv_f16_kernel<VV, KK, 2, 2>)                            \
+                   : launch(implicit_conv_f16_kernel<VV, KK, 2, 1>);                           \
   } else {                                                                                     \
-    if (ctas == 2) rc = launch(implicit_conv_f16_kernel<VV, -1, KK, 1, 0, 2>, 320);            \
-    else rc = launch(implicit_conv_f16_kernel<VV, -1, KK, 1, 0, 1>, 320);                      \
+    rc = ctas == 2 ? launch(implicit_conv_f16_kernel<VV, KK, 1, 2>)                            \
+                   : launch(implicit_conv_f16_kernel<VV, KK, 1, 1>);                           \
   }
+#define SCB_IC_LAUNCH_K(VV)                                                                    \
+  if (p.kc == 64) { SCB_IC_LAUNCH_P(VV, 64) }                                                  \
+  else if (p.kc == 32) { SCB_IC_LAUNCH_P(VV, 32) }                                             \
+  else { SCB_IC_LAUNCH_P(VV, 16) }
   if (volume == 27) {
-    if (p.kc == 64) { SCB_IC_LAUNCH_T(27, 64) } else if (p.kc == 32) { SCB_IC_LAUNCH_T(27, 32) } else { SCB_IC_LAUNCH_T(27, 16) }
+    SCB_IC_LAUNCH_K(27)
   } else if (volume == 8) {
-    if (p.kc == 64) { SCB_IC_LAUNCH_T(8, 64) } else if (p.kc == 32) { SCB_IC_LAUNCH_T(8, 32) } else { SCB_IC_LAUNCH_T(8, 16) }
+    SCB_IC_LAUNCH_K(8)
   } else if (volume == 1) {
-    if (p.kc == 64) { SCB_IC_LAUNCH_T(1, 64) } else if (p.kc == 32) { SCB_IC_LAUNCH_T(1, 32) } else { SCB_IC_LAUNCH_T(1, 16) }
+    SCB_IC_LAUNCH_K(1)
   }
-#undef SCB_IC_LAUNCH_T
+#undef SCB_IC_LAUNCH_K
+#undef SCB_IC_LAUNCH_P
   if (rc == SCB_EINVAL) set_error("scb_conv_implicit: V must be 1, 8 or 27");
   if (rc != SCB_OK) return rc;
   if (p.debug & 16) {
     unsigned long long prof[16];
     cudaStreamSynchronize(s);
     cudaMemcpyFromSymbol(prof, g_ic_prof, sizeof(prof));
-    fprintf(stderr, "[ic prof cta0] tiles=%llu total=%llu Aempty=%llu Await=%llu Bempty=%llu "
-            "MMAfull=%llu MMAtempty=%llu EPItfull=%llu EPIbulk=%llu MMAissue=%llu Aitems=%llu Aarrive=%llu "
-            "prologue=%llu bar=%llu (stages=%d ops=%d)\n",
-            prof[9], prof[7], prof[0], prof[1], prof[2], prof[3], prof[4], prof[5], prof[6], prof[10],
-            prof[11], prof[12], prof[13], prof[14], p.stages, p.ops);
+    fprintf(stderr, "[ic prof cta0] tiles=%llu total=%llu Aempty=%llu Bempty=%llu MMAfull=%llu "
+            "MMAtempty=%llu EPItfull=%llu EPIbulk=%llu MMAissue=%llu Aitems=%llu (stages=%d ops=%d "
+            "P=%d ctas=%d)\n",
+            prof[9], prof[7], prof[0], prof[2], prof[3], prof[4], prof[5], prof[6], prof[10],
+            prof[11], p.stages, p.ops, P, ctas);
     static const unsigned long long zero[16] = {0};
     cudaMemcpyToSymbol(g_ic_prof, zero, sizeof(zero));
   }
