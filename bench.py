@@ -43,6 +43,12 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "MinkUNet scans/sec (SemanticKITTI shape)"
 UNIT = "scans/s"
+CP_METRIC = "CenterPoint-style encoder sweeps/sec (nuScenes shape, config 4)"
+CP_UNIT = "sweeps/s"
+
+
+def metric_unit(args):
+    return (METRIC, UNIT) if args.model == "minkunet" else (CP_METRIC, CP_UNIT)
 SECTORS = 8
 
 
@@ -53,6 +59,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("engine", "reference"), default="engine")
     ap.add_argument("--width", type=float, default=1.0)
+    ap.add_argument("--model", choices=("minkunet", "centerpoint"), default="minkunet",
+                    help="minkunet: the BASELINE metric (configs 3/5); centerpoint: config 4")
     ap.add_argument("--scans-per-gpu", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -64,17 +72,23 @@ def parse():
 
 # ------------------------------------------------------------------ data
 
-def load_scans(seeds):
+CP_AZIMUTHS = 3000  # nuScenes-shaped sweeps of ~200k voxels
+
+
+def load_scans(seeds, model="minkunet"):
     from paper_2204_10319_b200 import workloads
     cache = Path(os.environ.get("SCB_SCAN_CACHE", "/tmp/scb_scans"))
     out = []
     for s in seeds:
-        f = cache / f"scan{s}.npz"
+        f = cache / (f"scan{s}.npz" if model == "minkunet" else f"sweeps{s}_{CP_AZIMUTHS}.npz")
         if f.exists():
             d = np.load(f)
             out.append((d["c"], d["f"], tuple(int(x) for x in d["b"])))
             continue
-        c, fe, b = workloads.semantickitti_scan(s)
+        if model == "minkunet":
+            c, fe, b = workloads.semantickitti_scan(s)
+        else:
+            c, fe, b = workloads.nuscenes_sweeps(s, azimuths=CP_AZIMUTHS)
         try:
             cache.mkdir(parents=True, exist_ok=True)
             np.savez(f, c=c, f=fe, b=np.array(b))
@@ -107,19 +121,27 @@ def sectors(scan, n=SECTORS):
 _W = {}
 
 
-def _cpu_worker_init(width):
+def _cpu_worker_init(width, model="minkunet"):
     os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
-    from paper_2204_10319_b200.minkunet import build_params
-    _W["width"] = width
-    _W["params"] = build_params(width, 4, 0)
+    _W["width"], _W["model"] = width, model
+    if model == "minkunet":
+        from paper_2204_10319_b200.minkunet import build_params
+        _W["params"] = build_params(width, 4, 0)
+    else:
+        from paper_2204_10319_b200.centerpoint import build_params
+        _W["params"] = build_params(5, 0)
 
 
 def _cpu_worker_run(item):
     from oracle import sparseconv_oracle as O
-    from paper_2204_10319_b200.minkunet import forward_oracle
     c, f, b = item
     t0 = time.perf_counter()
-    forward_oracle(_W["params"], _W["width"], c, O.quantize(f, "fp16"), b)
+    if _W["model"] == "minkunet":
+        from paper_2204_10319_b200.minkunet import forward_oracle
+        forward_oracle(_W["params"], _W["width"], c, O.quantize(f, "fp16"), b)
+    else:
+        from paper_2204_10319_b200.centerpoint import forward_oracle
+        forward_oracle(_W["params"], c, O.quantize(f, "fp16"), b)
     return time.perf_counter() - t0
 
 
@@ -127,14 +149,14 @@ class CpuPath:
     """The reference's CPU path (oracle port) over P worker processes, each
     running the full MinkUNet graph on one azimuth sector (1/8 scan) per step."""
 
-    def __init__(self, width, scans, procs):
+    def __init__(self, width, scans, procs, model="minkunet"):
         import multiprocessing as mp
         os.environ["OPENBLAS_NUM_THREADS"] = "1"
         os.environ["OMP_NUM_THREADS"] = "1"
         os.environ["MKL_NUM_THREADS"] = "1"
         self.items = [sec for s in scans for sec in sectors(s)]
         self.procs = max(1, min(procs, len(self.items)))
-        self.pool = mp.get_context("spawn").Pool(self.procs, _cpu_worker_init, (width,))
+        self.pool = mp.get_context("spawn").Pool(self.procs, _cpu_worker_init, (width, model))
         self.cursor = 0
 
     def step(self):
@@ -165,9 +187,10 @@ def run_reference(args):
     if rank != 0:
         return
     n_scans = 2
-    scans = load_scans(range(n_scans))
+    scans = load_scans(range(n_scans), args.model)
+    METRIC, UNIT = metric_unit(args)
     procs = min(os.cpu_count() or 1, 64)
-    cpu = CpuPath(args.width, scans, procs)
+    cpu = CpuPath(args.width, scans, procs, args.model)
     for _ in range(args.warmup):
         cpu.step()
     secs, done = 0.0, 0.0
@@ -193,9 +216,17 @@ def run_reference(args):
 
 
 def workload_config(args, world):
-    return {"workload": f"MinkUNet {args.width}x, {args.scans_per_gpu} SemanticKITTI-shaped "
-                        f"raycast scans per GPU per step (~120k voxels each, 0.05 m), FP16 storage",
-            "model": f"MinkUNet-{args.width}x", "global_batch": args.scans_per_gpu * world,
+    if args.model == "centerpoint":
+        work = (f"CenterPoint-style sparse encoder (21 k3 layers, 4 strided), "
+                f"{args.scans_per_gpu} nuScenes-shaped 10-sweep clouds per GPU per step "
+                f"(~200k voxels each, 0.075 m, 5 channels), FP16 storage")
+        name = "CenterPoint-encoder"
+    else:
+        work = (f"MinkUNet {args.width}x, {args.scans_per_gpu} SemanticKITTI-shaped "
+                f"raycast scans per GPU per step (~120k voxels each, 0.05 m), FP16 storage")
+        name = f"MinkUNet-{args.width}x"
+    return {"workload": work,
+            "model": name, "global_batch": args.scans_per_gpu * world,
             "scans_per_gpu": args.scans_per_gpu, "parallelism": f"scan-sharded x{world}",
             "l2": "flushed (256 MiB write, on the mapping stream ahead of the step's input reads) "
                   "before every timed step; per-step buffers >> L2"}
@@ -255,7 +286,9 @@ def main():
 
     import paper_2204_10319_b200 as sc
     from paper_2204_10319_b200 import _native as nat
+    from paper_2204_10319_b200.centerpoint import EngineCenterPoint
     from paper_2204_10319_b200.minkunet import EngineMinkUNet
+    METRIC, UNIT = metric_unit(args)
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -267,14 +300,17 @@ def main():
     B = args.scans_per_gpu
 
     from paper_2204_10319_b200.sharding import shard_seeds
-    scans = load_scans(shard_seeds(rank, world, B))
+    scans = load_scans(shard_seeds(rank, world, B), args.model)
     coords, feats, boundary = pack(scans)
-    model = EngineMinkUNet(args.width, 4, 0)
+    if args.model == "minkunet":
+        model = EngineMinkUNet(args.width, 4, 0)
+    else:
+        model = EngineCenterPoint(5, 0)
     coords_d = torch.from_numpy(coords.astype(np.int32)).to(dev)
     feats_d = torch.from_numpy(feats).to(dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
-    ms = model.mapping_stream
+    ms = getattr(model, "mapping_stream", None) or torch.cuda.current_stream()
 
     def step(timer=None, traffic=None):
         # the batch's coordinate set lives on the mapping stream (maps of
@@ -393,7 +429,7 @@ def main():
     if not args.no_e2e:
         h_coords = torch.from_numpy(coords.astype(np.int32)).pin_memory()
         h_feats = torch.from_numpy(feats).pin_memory()
-        h_out = torch.empty((coords.shape[0], 19), dtype=torch.float16).pin_memory()
+        h_out = torch.empty(tuple(out.features.shape), dtype=torch.float16).pin_memory()
 
         def e2e_step():
             f = h_feats.to(dev, non_blocking=True)
@@ -432,7 +468,7 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         procs = min(os.cpu_count() or 1, 64)
-        path = CpuPath(args.width, scans[:2], procs)
+        path = CpuPath(args.width, scans[:2], procs, args.model)
         path.step()  # warm (spawn + imports)
         secs, done = 0.0, 0.0
         while secs < args.cpu_seconds:
@@ -443,7 +479,8 @@ def main():
         cpu = {"value": done / secs, "unit": UNIT, "cores": path.procs, "kind": "port",
                "sample": f"{path.procs} processes x 1 azimuth sector (1/{SECTORS} scan) per round,"
                          f" {done:.2f} scans in {secs:.1f} s; oracle port of the same MinkUNet "
-                         "graph (numpy, 1 BLAS thread per process)", "cpu": cpu_model()}
+                         f"graph ({args.model}; numpy, 1 BLAS thread per process)",
+               "cpu": cpu_model()}
 
     if world > 1:
         dist.barrier()

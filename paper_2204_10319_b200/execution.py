@@ -812,6 +812,25 @@ def prepare_strided_chain(t, specs, options: ExecOptions | None = None) -> list[
     return out
 
 
+def prepare_maps_on_stream(t, stream: torch.cuda.Stream, build) -> None:
+    """Run a model's map preparation ``build(coordset) -> [CoordinateSet]``
+    on ``stream`` (B200 extension).  Maps depend on coordinates only, so a
+    model can keep them off its compute stream: the next batch's mapping then
+    overlaps this batch's convolutions, and the host reads it needs wait for
+    mapping work only.  The compute (current) stream waits for the result,
+    and every map tensor is recorded as in use by it."""
+    cur = torch.cuda.current_stream()
+    cs = t.coordset
+    if cs.stream is None or cs.stream != stream:
+        stream.wait_stream(cur)  # coordinates produced on another stream: order after them
+    with torch.cuda.stream(stream):
+        levels = build(cs)
+    cur.wait_stream(stream)
+    for lvl in levels:
+        for x in lvl.device_tensors():
+            x.record_stream(cur)
+
+
 def sparse_conv_forward(t: SparseTensor, w: WeightTensor, spec: LayerSpec,
                         strategy: LayerStrategy | None = None, map_cache: dict | None = None,
                         options: ExecOptions | None = None, *,

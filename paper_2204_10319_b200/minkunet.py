@@ -104,31 +104,23 @@ class EngineMinkUNet:
         # mapping work (coordinate pyramid, hash indexes, kernel maps) runs
         # here, off the compute stream: it depends on coordinates only, so
         # the next batch's maps overlap this batch's convolutions
-        self.mapping_stream = torch.cuda.Stream(priority=-1)
+        self.mapping_stream = torch.cuda.Stream(priority=-1)  # high: its kernels are short and gate the host
 
     def _prepare_maps(self, t, opts):
-        """The coordinate pyramid and every level's k3 map, on the mapping
-        stream.  Each strided level needs one host read (its output count);
-        it waits for mapping work only, never for queued convolutions, and
-        the convolutions are then issued without any host sync."""
-        import torch
-        from .execution import LayerSpec, prepare_layer_maps, prepare_strided_chain
-        cur = torch.cuda.current_stream()
-        ms = self.mapping_stream
-        cs = t.coordset
-        if cs.stream is None or cs.stream != ms:
-            ms.wait_stream(cur)  # coordinates produced elsewhere: order after them
-        levels = [cs]
-        with torch.cuda.stream(ms):
+        """The coordinate pyramid (one host read for the four k2 s2 levels)
+        and every level's k3 map, on the mapping stream."""
+        from .execution import (LayerSpec, prepare_layer_maps, prepare_maps_on_stream,
+                                prepare_strided_chain)
+
+        def build(cs):
             downs = [LayerSpec(2, 2, self.w[f"down{i}"].c_in, self.w[f"down{i}"].c_out)
                      for i in range(1, 5)]
-            levels += prepare_strided_chain(cs, downs, opts)
-            for cs in levels:
-                prepare_layer_maps(cs, LayerSpec(3, 1, 1, 1), opts)
-        cur.wait_stream(ms)
-        for cs in levels:  # allocated on the mapping stream, read on this one
-            for x in cs.device_tensors():
-                x.record_stream(cur)
+            levels = [cs] + prepare_strided_chain(cs, downs, opts)
+            for lvl in levels:
+                prepare_layer_maps(lvl, LayerSpec(3, 1, 1, 1), opts)
+            return levels
+
+        prepare_maps_on_stream(t, self.mapping_stream, build)
 
     def forward(self, t, options=None):
         from .execution import (ExecOptions, LayerSpec, inverse_conv_forward,
