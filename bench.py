@@ -33,10 +33,10 @@ from pathlib import Path
 
 import numpy as np
 
-# one growable segment per pool instead of many cudaMalloc'd blocks (the
-# mapping stream's buffers are recorded on the compute stream, so freed
-# blocks return a step later)
-os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "expandable_segments:True")
+# (expandable_segments:True measured 50-500 ms host stalls on the second
+# timed step: segment growth maps memory synchronously; not used)
+if os.environ.get("SCB_EXPANDABLE") == "1":
+    os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "expandable_segments:True")
 
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
@@ -327,9 +327,13 @@ def main():
     traffic = []
     step(None, traffic)
     torch.cuda.synchronize()
-    for _ in range(args.warmup):
+    # W warm-up steps at least, and at least ~1.5 s of them: a fresh box
+    # needs that long to settle clocks, lazy module loads and the allocator
+    warm, w0 = 0, time.perf_counter()
+    while warm < args.warmup or (time.perf_counter() - w0 < 1.5 and warm < 200):
         step()
-    torch.cuda.synchronize()
+        torch.cuda.synchronize()
+        warm += 1
 
     # ---------------- device-resident timed region
     timer = sc.StageTimer()
@@ -383,46 +387,66 @@ def main():
     for (layer, stage), s in timer.samples.items():
         stages[stage] = stages.get(stage, 0.0) + s
     bytes_by = {"gather": 0, "matmul": 0, "scatter": 0, "fused": 0}
-    flops = fused_flops = 0
+    flops = fused_flops = fused_exec = 0
     for _, rec in traffic * args.steps:  # one pass recorded, K timed
         bytes_by["gather"] += rec.get("gather_bytes", 0)
         bytes_by["matmul"] += rec.get("gemm_bytes", 0)
         bytes_by["scatter"] += rec.get("scatter_bytes", 0)
         bytes_by["fused"] += rec.get("fused_bytes", 0)
         flops += rec.get("gemm_flops", 0)
-        fused_flops += rec.get("fused_flops_executed", 0)
+        fused_flops += rec.get("fused_flops", 0)
+        fused_exec += rec.get("fused_flops_executed", 0)
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) \
         if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
-    tc_peak = peaks.get("bf16_tflops", 1590.0)
+    tc_peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 1590.0))
+    src = ("MEASURED_PEAKS.json" if peaks
+           else "of fallback 6.65 TB/s / 1.59 PFLOP/s (B200_PROFILING.md; MEASURED_PEAKS.json absent)")
     dom = max(("gather", "matmul", "scatter", "fused"), key=lambda k: stages.get(k, 0.0))
     kernel_name = {"gather": "scb gather_kernel", "matmul": "scb grouped_gemm_f16_kernel (tcgen05)",
                    "scatter": "scb scatter_kernel",
                    "fused": "scb implicit_conv_f16_kernel (tcgen05, fused gather/GEMM/scatter)"}[dom]
-    ach = bytes_by[dom] / stages[dom] / 1e9
+    n_launch = max(1, sum(1 for _, r in traffic if (("fused_bytes" in r) if dom == "fused"
+                                                      else ("gemm_bytes" in r))))
+    gbps = bytes_by[dom] / stages[dom] / 1e9
+    measured = {}
     traffic_file = ROOT / "profiles" / "latest_traffic.json"
-    measured = json.loads(traffic_file.read_text()) if traffic_file.exists() else {}
-    roof = {"bound": "hbm", "kernel": kernel_name, "achieved": ach, "peak": hbm_peak,
-            "unit": "GB/s", "frac": ach / hbm_peak,
-            "traffic": measured.get(dom, {}).get("dram_bytes_per_launch"),
-            "traffic_source": measured.get("source"),
-            "algorithmic_bytes_per_launch": bytes_by[dom] / args.steps / max(1, sum(
-                1 for _, r in traffic if (("fused_bytes" in r) if dom == "fused"
-                                          else ("gemm_bytes" in r)))),
-            "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks
-            else "of fallback 6.65 TB/s (B200_PROFILING.md; MEASURED_PEAKS.json absent)",
-            "per_stage": {k: {"ms_per_step": 1e3 * stages.get(k, 0.0) / args.steps,
-                              "GBps": (bytes_by[k] / stages[k] / 1e9) if stages.get(k) else None}
-                          for k in ("gather", "matmul", "scatter", "fused")},
-            "gemm_tflops": flops / stages["matmul"] / 1e12 if stages.get("matmul") else None,
-            "gemm_tensor_frac": (flops / stages["matmul"] / 1e12) / tc_peak
-            if stages.get("matmul") else None,
-            "fused_tflops_executed": fused_flops / stages["fused"] / 1e12
-            if stages.get("fused") else None,
-            "fused_tensor_frac": (fused_flops / stages["fused"] / 1e12) / tc_peak
-            if stages.get("fused") else None,
-            "mapping_ms_per_step": 1e3 * stages.get("mapping", 0.0) / args.steps,
-            "other_ms_per_step": 1e3 * stages.get("other", 0.0) / args.steps}
+    if traffic_file.exists():
+        measured = json.loads(traffic_file.read_text())
+    if dom == "fused":
+        # arithmetic intensity of the useful work decides the bound (ridge = peak ratio)
+        tflops = fused_flops / stages[dom] / 1e12
+        intensity = fused_flops / max(1, bytes_by[dom])
+        tensor_bound = intensity > tc_peak * 1e12 / (hbm_peak * 1e9)
+        roof = {"bound": "tensor" if tensor_bound else "hbm",
+                "achieved": tflops if tensor_bound else gbps,
+                "peak": tc_peak if tensor_bound else hbm_peak,
+                "unit": "TFLOP/s" if tensor_bound else "GB/s"}
+        roof["frac"] = roof["achieved"] / roof["peak"]
+        roof["algorithmic_flops_per_launch"] = fused_flops / args.steps / n_launch
+        roof["arithmetic_intensity_flop_per_byte"] = intensity
+        roof["hbm_frac"] = gbps / hbm_peak
+        roof["tensor_frac_useful"] = tflops / tc_peak
+        roof["tensor_frac_executed"] = fused_exec / stages[dom] / 1e12 / tc_peak
+    else:
+        roof = {"bound": "hbm", "achieved": gbps, "peak": hbm_peak, "unit": "GB/s",
+                "frac": gbps / hbm_peak}
+    m = measured.get(dom, {})
+    roof.update({
+        "kernel": kernel_name,
+        "traffic": m.get("dram_bytes_per_launch"),
+        "traffic_note": (f"ncu dram read+write of one launch ({m.get('launch')}) vs its "
+                         f"{m.get('algorithmic_bytes_per_launch')} algorithmic bytes; "
+                         f"{measured.get('source')}") if m else None,
+        "algorithmic_bytes_per_launch": bytes_by[dom] / args.steps / n_launch,
+        "peak_source": src,
+        "per_stage": {k: {"ms_per_step": 1e3 * stages.get(k, 0.0) / args.steps,
+                          "GBps": (bytes_by[k] / stages[k] / 1e9) if stages.get(k) else None}
+                      for k in ("gather", "matmul", "scatter", "fused")},
+        "mapping_ms_per_step": 1e3 * stages.get("mapping", 0.0) / args.steps,
+    })
+    if stages.get("matmul"):
+        roof["gemm_tflops"] = flops / stages["matmul"] / 1e12
 
     # ---------------- end to end through the public API with host buffers
     e2e = None
@@ -442,9 +466,11 @@ def main():
             h_out.copy_(o.features, non_blocking=True)
             return o
 
-        for _ in range(args.warmup):
+        warm_e, w0 = 0, time.perf_counter()
+        while warm_e < args.warmup or (time.perf_counter() - w0 < 0.5 and warm_e < 100):
             e2e_step()
-        torch.cuda.synchronize()
+            torch.cuda.synchronize()
+            warm_e += 1
         if world > 1:
             dist.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -494,7 +520,7 @@ def main():
             "data": "synthetic (raycast LiDAR scans, random-init weights)",
             "config": dict(workload_config(args, world), voxels_per_gpu=n_vox),
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
-            "clocks": clk, "step_ms": step_ms, "host_issue_ms": host_ms,
+            "clocks": clk, "warmup_steps_run": warm, "step_ms": step_ms, "host_issue_ms": host_ms,
             "cuda_mallocs_in_timed_steps": seg_allocs,
         }
         print(json.dumps(line), flush=True)

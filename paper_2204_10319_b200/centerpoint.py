@@ -71,13 +71,20 @@ class EngineCenterPoint:
             self.bn[l["name"]] = (torch.from_numpy(p["scale"]).cuda(),
                                   torch.from_numpy(p["shift"]).cuda())
             self.w[l["name"]].packed_f16()
-        self.mapping_stream = torch.cuda.Stream(priority=-1)  # high: its kernels are short and gate the host
+        # SCB_MAP_STREAM=1: maps on a high-priority side stream (overlaps the
+        # previous batch; measured noisier: the persistent conv kernels leave
+        # no room for the short mapping kernels between their boundaries)
+        self.mapping_stream = (torch.cuda.Stream(priority=-1)
+                               if __import__("os").environ.get("SCB_MAP_STREAM") == "1" else None)
+        from .execution import InflightLimiter
+        self.inflight = InflightLimiter(2)
 
     def forward(self, t, options=None):
         from dataclasses import replace
         from .execution import (ExecOptions, LayerSpec, prepare_layer_maps,
                                 prepare_maps_on_stream, sparse_conv_forward)
         opts = replace(options) if options is not None else ExecOptions()
+        self.inflight.before_forward()
         if opts.map_reuse:  # the coordinate pyramid before any convolution is queued
 
             def build(cs):
@@ -90,7 +97,7 @@ class EngineCenterPoint:
                         levels.append(cs)
                 return levels
 
-            prepare_maps_on_stream(t, self.mapping_stream, build)
+            prepare_maps_on_stream(t, self.mapping_stream, build, opts.timer)
         x = t
         for l in self.table:
             opts.layer_label = l["name"]
@@ -98,6 +105,7 @@ class EngineCenterPoint:
             x = sparse_conv_forward(x, self.w[l["name"]], LayerSpec(3, l["s"], l["ci"], l["co"]),
                                     None, None, opts,
                                     epilogue={"scale": sc, "shift": sh, "relu": True})
+        self.inflight.after_forward()
         return x
 
 

@@ -553,6 +553,8 @@ def _run_fused(features: torch.Tensor, kmap: KernelMap | None, w: WeightTensor,
             "fused_bytes": e * features.shape[0] * w.c_in + e * n_out * w.c_out
             + (4 * volume * n_out if volume > 1 else 0) + e * volume * w.c_in * w.c_out
             + (e * n_out * w.c_out if res else 0),
+            # algorithmic (useful) FLOPs 2 |M| C_in C_out; executed: dense over all V offsets
+            "fused_flops": 2 * (n_out if kmap is None else kmap.total) * w.c_in * w.c_out,
             "fused_flops_executed": 2 * volume * n_out * w.c_in * w.c_out}))
     return out
 
@@ -812,7 +814,28 @@ def prepare_strided_chain(t, specs, options: ExecOptions | None = None) -> list[
     return out
 
 
-def prepare_maps_on_stream(t, stream: torch.cuda.Stream, build) -> None:
+class InflightLimiter:
+    """Bounds how far the host runs ahead of the compute stream: a model
+    records an event at the end of each forward, and the forward after next
+    first waits (on the host) for it.  With maps built off the compute
+    stream nothing else throttles the host, and every forward in flight
+    holds its maps and activations in memory."""
+
+    def __init__(self, depth: int = 2):
+        self.depth = depth
+        self.events: list[torch.cuda.Event] = []
+
+    def before_forward(self) -> None:
+        while len(self.events) >= self.depth:
+            self.events.pop(0).synchronize()
+
+    def after_forward(self) -> None:
+        ev = torch.cuda.Event()
+        ev.record()
+        self.events.append(ev)
+
+
+def prepare_maps_on_stream(t, stream: torch.cuda.Stream, build, timer=None) -> None:
     """Run a model's map preparation ``build(coordset) -> [CoordinateSet]``
     on ``stream`` (B200 extension).  Maps depend on coordinates only, so a
     model can keep them off its compute stream: the next batch's mapping then
@@ -821,9 +844,13 @@ def prepare_maps_on_stream(t, stream: torch.cuda.Stream, build) -> None:
     and every map tensor is recorded as in use by it."""
     cur = torch.cuda.current_stream()
     cs = t.coordset
+    if stream is None or stream == cur:  # inline, on the compute stream
+        with _timed(timer, "maps", "mapping"):
+            build(cs)
+        return
     if cs.stream is None or cs.stream != stream:
         stream.wait_stream(cur)  # coordinates produced on another stream: order after them
-    with torch.cuda.stream(stream):
+    with torch.cuda.stream(stream), _timed(timer, "maps", "mapping"):
         levels = build(cs)
     cur.wait_stream(stream)
     for lvl in levels:

@@ -104,7 +104,13 @@ class EngineMinkUNet:
         # mapping work (coordinate pyramid, hash indexes, kernel maps) runs
         # here, off the compute stream: it depends on coordinates only, so
         # the next batch's maps overlap this batch's convolutions
-        self.mapping_stream = torch.cuda.Stream(priority=-1)  # high: its kernels are short and gate the host
+        # SCB_MAP_STREAM=1: maps on a high-priority side stream (overlaps the
+        # previous batch; measured noisier: the persistent conv kernels leave
+        # no room for the short mapping kernels between their boundaries)
+        self.mapping_stream = (torch.cuda.Stream(priority=-1)
+                               if __import__("os").environ.get("SCB_MAP_STREAM") == "1" else None)
+        from .execution import InflightLimiter
+        self.inflight = InflightLimiter(3)
 
     def _prepare_maps(self, t, opts):
         """The coordinate pyramid (one host read for the four k2 s2 levels)
@@ -120,7 +126,7 @@ class EngineMinkUNet:
                 prepare_layer_maps(lvl, LayerSpec(3, 1, 1, 1), opts)
             return levels
 
-        prepare_maps_on_stream(t, self.mapping_stream, build)
+        prepare_maps_on_stream(t, self.mapping_stream, build, opts.timer)
 
     def forward(self, t, options=None):
         from .execution import (ExecOptions, LayerSpec, inverse_conv_forward,
@@ -154,6 +160,7 @@ class EngineMinkUNet:
             return a.replace_features(torch.cat([a.features, b.features], dim=1))
 
         names = {l["name"] for l in self.table}
+        self.inflight.before_forward()
         if base.map_reuse:
             self._prepare_maps(t, base)
         x = conv(t, "stem.0", 3, 1)
@@ -169,7 +176,9 @@ class EngineMinkUNet:
             x = concat(x, skips[4 - j])
             x = res(x, f"dec{j}.r0", True)
             x = res(x, f"dec{j}.r1", f"dec{j}.r1.proj" in names)
-        return conv(x, "head", 1, 1)
+        out = conv(x, "head", 1, 1)
+        self.inflight.after_forward()
+        return out
 
 
 # ---------------------------------------------------------------- oracle (CPU)
