@@ -224,18 +224,19 @@ class SparseTensor:
 
 
 def _validate(cset: CoordinateSet) -> None:
-    """Range and uniqueness checks of reference core.py:112-120, on device."""
-    c = cset.coords
-    b = c[:, 0]
-    if int(b.min()) < 0 or int(b.max()) >= cset.batch_size:
-        raise ValueError("batch index out of range")
-    bound = torch.tensor(cset.boundary, device=c.device, dtype=torch.int32)
-    sp = c[:, 1:]
-    if bool((sp < 0).any()) or bool((sp >= bound).any()):
-        raise ValueError("coordinate outside boundary")
+    """Range and uniqueness checks of reference core.py:112-120, on device:
+    building the hash index (which the first layer reuses) counts duplicate
+    and out-of-range rows; one host read of the two counts."""
     from .mapping import build_index  # local import: mapping depends on core
     idx = build_index(cset, "hash")
-    if idx.duplicates:
+    dup, oob = (int(x) for x in idx._status.tolist())
+    if oob:  # rare: find which check failed for the reference's message
+        c = cset.coords
+        b = c[:, 0]
+        if int(b.min()) < 0 or int(b.max()) >= cset.batch_size:
+            raise ValueError("batch index out of range")
+        raise ValueError("coordinate outside boundary")
+    if dup:
         raise ValueError("coordinate rows must be unique")
 
 
