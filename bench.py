@@ -455,28 +455,40 @@ def main():
         h_feats = torch.from_numpy(feats).pin_memory()
         h_out = torch.empty(tuple(out.features.shape), dtype=torch.float16).pin_memory()
 
-        # a serving loop: uploads and the logits download on their own copy
-        # streams, so batch i+1's H2D and batch i's D2H overlap compute
+        # a serving loop: uploads and the output download on their own copy
+        # streams, so batch i+1's H2D and batch i's D2H overlap compute.  Input
+        # buffers are a ring reused once the batch that last used them is done
+        # (no record_stream: its delayed block reuse cost cudaMallocs), and
+        # each output is kept alive until its download finished.
+        import collections
         h2d_s, d2h_s = torch.cuda.Stream(), torch.cuda.Stream()
+        NB = 4
+        c_ring = [torch.empty(h_coords.shape, dtype=h_coords.dtype, device=dev) for _ in range(NB)]
+        f_ring = [torch.empty(h_feats.shape, dtype=h_feats.dtype, device=dev) for _ in range(NB)]
+        done = [None] * NB
+        pending = collections.deque()
+        counter = [0]
 
         def e2e_step():
+            k = counter[0] % NB
+            counter[0] += 1
             cur = torch.cuda.current_stream()
             with torch.cuda.stream(h2d_s):
-                f = h_feats.to(dev, non_blocking=True)
-                c = h_coords.to(dev, non_blocking=True)
+                if done[k] is not None:
+                    h2d_s.wait_event(done[k])
+                c_ring[k].copy_(h_coords, non_blocking=True)
+                f_ring[k].copy_(h_feats, non_blocking=True)
             cur.wait_stream(h2d_s)
-            f.record_stream(cur)
-            c.record_stream(cur)
-            with torch.cuda.stream(ms):  # validation (index build) where the maps are built
-                if ms != cur:
-                    ms.wait_stream(cur)
-                t = sc.SparseTensor(c, f, 1, boundary, B)  # validated, as a user would
+            t = sc.SparseTensor(c_ring[k], f_ring[k], 1, boundary, B)  # validated, as a user would
             t = sc.quantize_features(t, sc.PrecisionMode.FP16_STORAGE)
             o = model.forward(t, sc.ExecOptions(index_kind="hash", dataflow=args.dataflow))
-            d2h_s.wait_stream(cur)
+            done[k] = cur.record_event()
+            d2h_s.wait_event(done[k])
             with torch.cuda.stream(d2h_s):
                 h_out.copy_(o.features, non_blocking=True)
-            o.features.record_stream(d2h_s)
+                pending.append((o, d2h_s.record_event()))
+            while len(pending) > 3:
+                pending.popleft()[1].synchronize()
             return o
 
         warm_e, w0 = 0, time.perf_counter()

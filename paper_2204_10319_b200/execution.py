@@ -33,6 +33,7 @@ from .core import (CoordinateSet, PrecisionMode, SparseTensor, WeightTensor,
 from .mapping import (DEFAULT_GRID_CELL_CAP, GatherScatterPlan, GridCapacityError, KernelMap,
                       KernelOffsets, build_gather_scatter_plan, build_index,
                       compute_output_coords, compute_output_coords_chain, downsample_boundary,
+                      start_output_coords_chain,
                       enumerate_offsets, map_search, _cells)
 
 GATHER_ORDERS = ("weight_stationary", "input_stationary")
@@ -773,31 +774,46 @@ def prepare_layer_maps(t, spec: LayerSpec, options: ExecOptions | None = None) -
     return _layer_maps(cset, spec, resolve_strategy(spec, None), opts)[0]
 
 
-def prepare_strided_chain(t, specs, options: ExecOptions | None = None) -> list[CoordinateSet]:
+def prepare_strided_chain(t, specs, options: ExecOptions | None = None, *,
+                          deferred: bool = False):
     """prepare_layer_maps for a chain of strided layers applied one after
     another (an encoder's downsampling path), with ONE host read for all
     output counts when every window proposes one candidate per input (K = s);
     otherwise level by level.  Returns the output coordinate set of each
     layer; maps are cached on the input sets as sparse_conv_forward would.
-    Result-identical to running the layers."""
+    Result-identical to running the layers.  ``deferred``: issue the chain
+    and return a callable that finishes it (waits for the counts, builds the
+    sets and maps) — queue other work in between so the host read costs no
+    GPU idle time."""
     opts = options or ExecOptions()
     if not opts.map_reuse:
         raise ValueError("prepared maps are kept in the map-reuse cache")
     cset = t.coordset if isinstance(t, SparseTensor) else t
+    if deferred:
+        return _strided_chain(cset, specs, opts, True)
+    return _strided_chain(cset, specs, opts, False)
+
+
+def _strided_chain(cset, specs, opts, deferred):
     dim = len(cset.boundary)
     steps = [(enumerate_offsets(dim, sp.kernel_size), sp.stride) for sp in specs]
     chainable = all(sp.stride > 1 and sp.kernel_size == sp.stride for sp in specs)
     if not chainable or not specs:
-        out, cs = [], cset
-        for sp in specs:
-            cs = prepare_layer_maps(cs, sp, opts)
-            out.append(cs)
-        return out
-    # already prepared (same coordinate set): nothing to do
-    hit = cset.maps.get((specs[0].kernel_size, specs[0].stride, steps[0][0].base))
-    if hit is not None and len(specs) == 1:
-        return [hit[0]]
-    levels = compute_output_coords_chain(cset, steps)
+        def sequential():
+            out, cs = [], cset
+            for sp in specs:
+                cs = prepare_layer_maps(cs, sp, opts)
+                out.append(cs)
+            return out
+        return sequential if deferred else sequential()
+    finish = start_output_coords_chain(cset, steps)
+
+    def build():
+        return _chain_maps(cset, specs, steps, finish(), opts)
+    return build if deferred else build()
+
+
+def _chain_maps(cset, specs, steps, levels, opts):
     out, cs = [], cset
     for sp, (off, stride), (oc, ob) in zip(specs, steps, levels):
         key = (sp.kernel_size, stride, off.base)

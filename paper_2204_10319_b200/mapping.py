@@ -204,8 +204,15 @@ def compute_output_coords(in_coords, offsets: KernelOffsets, stride: int, out_bo
 
 
 def compute_output_coords_chain(cset, steps) -> list[torch.Tensor]:
-    """Output coordinates of successive strided levels, ``steps`` = [(offsets,
-    stride), ...] applied one after the other starting from ``cset``.  Level
+    """See start_output_coords_chain; returns the finished levels."""
+    return start_output_coords_chain(cset, steps)()
+
+
+def start_output_coords_chain(cset, steps):
+    """Issue the output coordinates of successive strided levels, ``steps`` =
+    [(offsets, stride), ...] applied one after the other from ``cset``, and
+    return a finisher that waits for the counts and returns [(coords,
+    boundary), ...] per level.  Level
     i+1 is generated from level i's keys with its count on the device
     (scb_output_keys_next), so the whole chain costs ONE host read.  Each
     level equals compute_output_coords of the previous one.  Only for windows
@@ -241,13 +248,23 @@ def compute_output_coords_chain(cset, steps) -> list[torch.Tensor]:
         levels.append((keys, g, out_b, ws))
         prev = (keys, cnt, g)
         boundary, n_cap = out_b, cap
-    host = counts.cpu().tolist()  # the chain's one host read
-    out = []
-    for (keys, g, out_b, _), n in zip(levels, host):
-        co = torch.empty((n, dim + 1), dtype=torch.int32, device=dev)
-        nat.call("scb_unflatten", nat.ptr(keys), n, g, nat.ptr(co), nat.stream_handle())
-        out.append((co, out_b))
-    return out
+    # the chain's one host read, asynchronous: the caller can queue other work
+    # (e.g. the first convolutions) before calling the returned finisher
+    host = torch.empty(counts.shape, dtype=torch.int64, pin_memory=True)
+    host.copy_(counts, non_blocking=True)
+    ready = torch.cuda.Event()
+    ready.record()
+
+    def finish():
+        ready.synchronize()
+        out = []
+        for (keys, g, out_b, _), n in zip(levels, host.tolist()):
+            co = torch.empty((n, dim + 1), dtype=torch.int32, device=dev)
+            nat.call("scb_unflatten", nat.ptr(keys), n, g, nat.ptr(co), nat.stream_handle())
+            out.append((co, out_b))
+        return out
+
+    return finish
 
 
 def _hit_matrix(volume: int, n: int, device) -> torch.Tensor:

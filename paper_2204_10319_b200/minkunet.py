@@ -112,6 +112,11 @@ class EngineMinkUNet:
         from .execution import InflightLimiter
         self.inflight = InflightLimiter(3)
 
+    def _down_specs(self):
+        from .execution import LayerSpec
+        return [LayerSpec(2, 2, self.w[f"down{i}"].c_in, self.w[f"down{i}"].c_out)
+                for i in range(1, 5)]
+
     def _prepare_maps(self, t, opts):
         """The coordinate pyramid (one host read for the four k2 s2 levels)
         and every level's k3 map, on the mapping stream."""
@@ -119,9 +124,7 @@ class EngineMinkUNet:
                                 prepare_strided_chain)
 
         def build(cs):
-            downs = [LayerSpec(2, 2, self.w[f"down{i}"].c_in, self.w[f"down{i}"].c_out)
-                     for i in range(1, 5)]
-            levels = [cs] + prepare_strided_chain(cs, downs, opts)
+            levels = [cs] + prepare_strided_chain(cs, self._down_specs(), opts)
             for lvl in levels:
                 prepare_layer_maps(lvl, LayerSpec(3, 1, 1, 1), opts)
             return levels
@@ -161,9 +164,23 @@ class EngineMinkUNet:
 
         names = {l["name"] for l in self.table}
         self.inflight.before_forward()
+        finish = None
         if base.map_reuse:
-            self._prepare_maps(t, base)
+            if self.mapping_stream is not None:
+                self._prepare_maps(t, base)
+            else:
+                # level-0 map and the k2/s2 coordinate chain are queued first;
+                # the chain's count read is collected after stem.0 is queued,
+                # so it costs no GPU idle time
+                from .execution import LayerSpec, prepare_layer_maps, prepare_strided_chain
+                prepare_layer_maps(t.coordset, LayerSpec(3, 1, 1, 1), base)
+                finish = prepare_strided_chain(t.coordset, self._down_specs(), base,
+                                               deferred=True)
         x = conv(t, "stem.0", 3, 1)
+        if finish is not None:
+            from .execution import LayerSpec, prepare_layer_maps
+            for lvl in finish():
+                prepare_layer_maps(lvl, LayerSpec(3, 1, 1, 1), base)
         x = conv(x, "stem.1", 3, 1)
         skips = [x]
         for i in range(1, 5):
