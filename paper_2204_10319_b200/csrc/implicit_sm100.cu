@@ -61,7 +61,10 @@ struct Params {
   uint32_t a_stage_bytes, stage_bytes;
   uint32_t b_tx;            // bytes one offset's B load delivers
   long long ldf, ldh;       // feature row stride, hit-matrix row stride
-  const __half* feat;       // [n_in][ldf]
+  const __half* feat;       // [n_in][ldf]: input channels [0, c_split)
+  const __half* feat2;      // nullable: channels [c_split, c_in) (skip concat), [n_in][ldf2]
+  long long ldf2;
+  int c_split;
   const int* hits;          // [V][ldh] input row or -1 (unused for V = 1)
   const float* scale;       // nullable (with shift)
   const float* shift;
@@ -209,7 +212,8 @@ __global__ void __launch_bounds__(64 + 128 * P + 128, MINB)
       const int rxr = SWZ == 128 ? (r & 7) : (SWZ == 64 ? ((r >> 1) & 3) : ((r >> 2) & 1));
       roff[it] = (uint32_t)(r * (KC * 2)) + ((uint32_t)(cc ^ rxr) << 4);
     }
-    const uint32_t ldfb = (uint32_t)(p.ldf * 2);  // feature row stride in bytes (host-checked < 2^32)
+    const uint32_t ldfb1 = (uint32_t)(p.ldf * 2);   // row strides in bytes (host-checked < 2^32)
+    const uint32_t ldfb2 = (uint32_t)(p.ldf2 * 2);
     for (int t = t_begin; t < t_end; ++t) {
       // the table is read by other threads: rewrite it only after every
       // producer finished the previous tile (the first barrier also orders
@@ -246,7 +250,13 @@ __global__ void __launch_bounds__(64 + 128 * P + 128, MINB)
           uint32_t* wm = wmask + stage * NPROD + pt;
           uint32_t now = *wm;
           const uint32_t nbc = nb_s0 + (uint32_t)((g * p.ops * BM + cr) * 4);
-          const uint64_t fbase = reinterpret_cast<uint64_t>(p.feat) + (uint64_t)((col0 + cc * 8) * 2);
+          // this lane's 8 columns come from the first or (concat) second input
+          const int col = col0 + cc * 8;
+          const bool second = p.feat2 != nullptr && col >= p.c_split;
+          const uint64_t fbase = second
+              ? reinterpret_cast<uint64_t>(p.feat2) + (uint64_t)((col - p.c_split) * 2)
+              : reinterpret_cast<uint64_t>(p.feat) + (uint64_t)(col * 2);
+          const uint32_t ldfb = second ? ldfb2 : ldfb1;
           const bool live_c = cc < live && !(p.debug & 1);
           for (int o = 0; o < nv; ++o) {
             int jj[IT];  // index loads first (volatile asm keeps the order): latencies overlap
@@ -441,13 +451,38 @@ int device_sms();
 
 using namespace scb;
 
+extern "C" int32_t scb_conv_implicit_cat(const void* features, int64_t ldf, int32_t c_split,
+                                         const void* features2, int64_t ldf2, int64_t n_in,
+                                         int32_t c_in, const int32_t* hits, int32_t volume,
+                                         int64_t n_out, const void* weights_packed,
+                                         int32_t c_out, void* out, const float* scale,
+                                         const float* shift, const float* bias,
+                                         const void* residual, int32_t relu,
+                                         scb_stream_t stream);
+
 extern "C" int32_t scb_conv_implicit(const void* features, int64_t n_in, int32_t c_in,
                                      int64_t ldf, const int32_t* hits, int32_t volume,
                                      int64_t n_out, const void* weights_packed, int32_t c_out,
                                      void* out, const float* scale, const float* shift,
                                      const float* bias, const void* residual, int32_t relu,
                                      scb_stream_t stream) {
+  return scb_conv_implicit_cat(features, ldf, c_in, nullptr, 0, n_in, c_in, hits, volume, n_out,
+                               weights_packed, c_out, out, scale, shift, bias, residual, relu,
+                               stream);
+}
+
+extern "C" int32_t scb_conv_implicit_cat(const void* features, int64_t ldf, int32_t c_split,
+                                         const void* features2, int64_t ldf2, int64_t n_in,
+                                         int32_t c_in, const int32_t* hits, int32_t volume,
+                                         int64_t n_out, const void* weights_packed,
+                                         int32_t c_out, void* out, const float* scale,
+                                         const float* shift, const float* bias,
+                                         const void* residual, int32_t relu,
+                                         scb_stream_t stream) {
   using namespace ic;
+  SCB_CHECK_ARG(features2 == nullptr || (c_split % 8 == 0 && c_split > 0 && c_split < c_in &&
+                                         ldf2 % 8 == 0 && ldf2 * 2 < (1LL << 32)),
+                "concat split must be a positive multiple of 8 inside C_in, second stride % 8");
   SCB_CHECK_ARG(volume == 1 || volume == 8 || volume == 27,
                 "implicit conv supports K^3 = 1, 8 or 27 offsets");
   SCB_CHECK_ARG(volume == 1 || hits != nullptr, "hit matrix required for K > 1");
@@ -507,6 +542,9 @@ extern "C" int32_t scb_conv_implicit(const void* features, int64_t n_in, int32_t
   p.ldf = ldf;
   p.ldh = hits_ld(n_out);
   p.feat = (const __half*)features;
+  p.feat2 = (const __half*)features2;
+  p.ldf2 = ldf2;
+  p.c_split = features2 ? c_split : c_in;
   p.hits = hits;
   p.scale = scale;
   p.shift = shift;

@@ -535,19 +535,30 @@ def _pad_channels(f: torch.Tensor) -> torch.Tensor:
 
 
 def _run_fused(features: torch.Tensor, kmap: KernelMap | None, w: WeightTensor,
-               opts: ExecOptions, epilogue: dict | None) -> torch.Tensor:
-    """One scb_conv_implicit launch; ``kmap`` None = the K=1 identity map."""
+               opts: ExecOptions, epilogue: dict | None, concat: torch.Tensor | None = None
+               ) -> torch.Tensor:
+    """One scb_conv_implicit launch; ``kmap`` None = the K=1 identity map.
+    ``concat``: more input channels (same rows), read in place."""
     label, timer = opts.layer_label, opts.timer
     packed, _, _ = w.packed_f16()
     volume = 1 if kmap is None else kmap.offsets.volume
     n_out = features.shape[0] if kmap is None else kmap.n_out
     out = torch.empty((n_out, w.c_out), dtype=features.dtype, device=features.device)
     scale, shift, bias, res, relu = _epi_args(epilogue)
+    hits = None if kmap is None else nat.ptr(kmap.hits)
     with _timed(timer, label, "fused"):
-        f = _pad_channels(features)
-        nat.call("scb_conv_implicit", nat.ptr(f), f.shape[0], f.shape[1], f.shape[1],
-                 None if kmap is None else nat.ptr(kmap.hits), volume, n_out, nat.ptr(packed),
-                 w.c_out, nat.ptr(out), scale, shift, bias, res, relu, nat.stream_handle())
+        if concat is not None and features.shape[1] % 8 == 0 and concat.shape[1] % 8 == 0 \
+                and features.is_contiguous() and concat.is_contiguous():
+            ca, cb = features.shape[1], concat.shape[1]
+            nat.call("scb_conv_implicit_cat", nat.ptr(features), ca, ca, nat.ptr(concat), cb,
+                     features.shape[0], ca + cb, hits, volume, n_out, nat.ptr(packed), w.c_out,
+                     nat.ptr(out), scale, shift, bias, res, relu, nat.stream_handle())
+        else:
+            f = features if concat is None else torch.cat([features, concat], dim=1)
+            f = _pad_channels(f)
+            nat.call("scb_conv_implicit", nat.ptr(f), f.shape[0], f.shape[1], f.shape[1], hits,
+                     volume, n_out, nat.ptr(packed), w.c_out, nat.ptr(out), scale, shift, bias,
+                     res, relu, nat.stream_handle())
     if opts.traffic_log is not None:
         e = 2
         opts.traffic_log.append((label, {
@@ -602,12 +613,16 @@ def _run_staged_device(features: torch.Tensor, kmap: KernelMap, w: WeightTensor,
 
 def _run_dataflow(features: torch.Tensor, kmap: KernelMap, w: WeightTensor,
                   strat: LayerStrategy, schedule, symmetric: bool, opts: ExecOptions,
-                  center: int | None, epilogue: dict | None = None, record=None) -> torch.Tensor:
-    """One layer's gather -> GEMM -> scatter; returns storage-dtype rows."""
+                  center: int | None, epilogue: dict | None = None, record=None,
+                  concat: torch.Tensor | None = None) -> torch.Tensor:
+    """One layer's gather -> GEMM -> scatter; returns storage-dtype rows.
+    ``concat``: more input channels of the same rows (fused: read in place)."""
     if choose_dataflow(opts, features.dtype, kmap, w) == "fused":
         if record is not None and opts.workload_log is not None:
             record(kmap.sizes)
-        return _run_fused(features, kmap, w, opts, epilogue)
+        return _run_fused(features, kmap, w, opts, epilogue, concat)
+    if concat is not None:
+        features = torch.cat([features, concat], dim=1)
     if opts.sync_free and opts.workload_log is None and opts.plan_log is None \
             and opts.traffic_log is None:
         return _run_staged_device(features, kmap, w, opts, center, epilogue)
@@ -653,11 +668,12 @@ def _run_dataflow(features: torch.Tensor, kmap: KernelMap, w: WeightTensor,
     return out
 
 
-def _pointwise_matmul(t: SparseTensor, w: WeightTensor, opts: ExecOptions, epilogue=None):
+def _pointwise_matmul(t: SparseTensor, w: WeightTensor, opts: ExecOptions, epilogue=None,
+                      concat=None):
     """K=1, s=1 fast path (execution.py:472-477): out = features @ W[0]."""
     if choose_dataflow(opts, t.features.dtype, None, w) == "fused":
-        return _run_fused(t.features, None, w, opts, epilogue)
-    f = t.features
+        return _run_fused(t.features, None, w, opts, epilogue, concat)
+    f = t.features if concat is None else torch.cat([t.features, concat], dim=1)
     dt = f.dtype
     n = f.shape[0]
     n_rows = (n + nat.TILE_ROWS - 1) // nat.TILE_ROWS * nat.TILE_ROWS
@@ -719,10 +735,11 @@ def _record_traffic(opts, plan, c_in, c_out, dtype, n_in, n_out, n_center, m_tot
         + 4 * n_center * c_out}))
 
 
-def _check_channels(t, w, spec, msg=None):
-    if t.num_channels != spec.c_in or w.c_in != spec.c_in or w.c_out != spec.c_out:
+def _check_channels(t, w, spec, msg=None, extra=0):
+    c = t.num_channels + extra
+    if c != spec.c_in or w.c_in != spec.c_in or w.c_out != spec.c_out:
         raise ValueError(msg or (
-            f"channel mismatch: tensor {t.num_channels}, spec {spec.c_in}->{spec.c_out}, "
+            f"channel mismatch: tensor {c}, spec {spec.c_in}->{spec.c_out}, "
             f"weights {w.c_in}->{w.c_out}"))
 
 
@@ -877,25 +894,34 @@ def prepare_maps_on_stream(t, stream: torch.cuda.Stream, build, timer=None) -> N
 def sparse_conv_forward(t: SparseTensor, w: WeightTensor, spec: LayerSpec,
                         strategy: LayerStrategy | None = None, map_cache: dict | None = None,
                         options: ExecOptions | None = None, *,
-                        epilogue: dict | None = None) -> SparseTensor:
+                        epilogue: dict | None = None, concat=None) -> SparseTensor:
     """One sparse convolution layer on the B200 (execution.py:450-509).
 
     ``epilogue`` (B200 extension) fuses
-    ``{"scale", "shift", "bias", "relu"}`` into the scatter's single write."""
+    ``{"scale", "shift", "bias", "residual", "relu"}`` into the single write
+    of each output row.  ``concat`` (B200 extension): a SparseTensor or
+    feature matrix on the same coordinates whose channels follow ``t``'s —
+    the layer input is their channel concatenation (a U-Net skip), which the
+    fused kernel reads in place instead of materialising."""
     flush_saturation_warnings()
     opts = options or ExecOptions()
-    _check_channels(t, w, spec)
+    cat = None
+    if concat is not None:
+        cat = concat.features if isinstance(concat, SparseTensor) else concat
+        if cat.shape[0] != t.num_points or cat.dtype != t.features.dtype:
+            raise ValueError("concat input must match the tensor's rows and dtype")
+    _check_channels(t, w, spec, extra=0 if cat is None else cat.shape[1])
     label, timer = opts.layer_label, opts.timer
     strat = resolve_strategy(spec, strategy)
     if spec.kernel_size == 1 and spec.stride == 1:
         if choose_dataflow(opts, t.features.dtype, None, w) == "fused":
-            out = _pointwise_matmul(t, w, opts, epilogue)
+            out = _pointwise_matmul(t, w, opts, epilogue, cat)
         else:
             with _timed(timer, label, "matmul"):
-                out = _pointwise_matmul(t, w, opts, epilogue)
+                out = _pointwise_matmul(t, w, opts, epilogue, cat)
         _record_workload(opts, spec, np.array([t.num_points]), False, [0], t.coords, t.coords,
                          t.boundary, t.batch_size)
-        return t.replace_features(out)
+        return SparseTensor._wrap(out, t.stride, t.boundary, t.batch_size, t.coordset)
 
     offsets = enumerate_offsets(t.spatial_dims, spec.kernel_size)
     cset = t.coordset
@@ -908,7 +934,7 @@ def sparse_conv_forward(t: SparseTensor, w: WeightTensor, spec: LayerSpec,
     record = lambda sizes: _record_workload(opts, spec, sizes, symmetric, schedule, t.coords,
                                             out_cset.coords, t.boundary, t.batch_size)
     out = _run_dataflow(t.features, kmap, w, strat, schedule, symmetric, opts, center, epilogue,
-                        record)
+                        record, cat)
     return SparseTensor._wrap(out, t.stride * spec.stride, out_cset.boundary, t.batch_size,
                               out_cset)
 

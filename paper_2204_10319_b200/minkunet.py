@@ -138,7 +138,7 @@ class EngineMinkUNet:
         base = replace(options) if options is not None else ExecOptions()  # private copy
         cache = {}
 
-        def conv(x, name, k, s, relu=True, reuse=None, kind="conv", residual=None):
+        def conv(x, name, k, s, relu=True, reuse=None, kind="conv", residual=None, concat=None):
             w = self.w[name]
             opts = base
             opts.layer_label = name
@@ -149,18 +149,15 @@ class EngineMinkUNet:
                 spec = LayerSpec(k, 1, w.c_in, w.c_out, transposed=True, reuse_key=reuse)
                 return inverse_conv_forward(x, w, spec, cache, None, opts, epilogue=ep)
             spec = LayerSpec(k, s, w.c_in, w.c_out, reuse_key=name)
-            return sparse_conv_forward(x, w, spec, None, cache, opts, epilogue=ep)
+            return sparse_conv_forward(x, w, spec, None, cache, opts, epilogue=ep, concat=concat)
 
-        def res(x, prefix, has_proj):
+        def res(x, prefix, has_proj, skip=None):
             # relu(BN(conv2(h)) + shortcut): the residual add and ReLU run in
-            # conv2's epilogue (one write of the block output)
-            h = conv(x, prefix + ".c1", 3, 1)
-            sc = conv(x, prefix + ".proj", 1, 1, relu=False) if has_proj else x
+            # conv2's epilogue (one write of the block output).  ``skip``: the
+            # decoder's concatenated skip input, read in place by c1 and proj
+            h = conv(x, prefix + ".c1", 3, 1, concat=skip)
+            sc = conv(x, prefix + ".proj", 1, 1, relu=False, concat=skip) if has_proj else x
             return conv(h, prefix + ".c2", 3, 1, relu=True, residual=sc)
-
-        def concat(a, b):
-            import torch
-            return a.replace_features(torch.cat([a.features, b.features], dim=1))
 
         names = {l["name"] for l in self.table}
         self.inflight.before_forward()
@@ -190,8 +187,7 @@ class EngineMinkUNet:
             skips.append(x)
         for j in range(1, 5):
             x = conv(x, f"up{j}", 2, 1, reuse=f"down{5 - j}", kind="inverse")
-            x = concat(x, skips[4 - j])
-            x = res(x, f"dec{j}.r0", True)
+            x = res(x, f"dec{j}.r0", True, skip=skips[4 - j])
             x = res(x, f"dec{j}.r1", f"dec{j}.r1.proj" in names)
         out = conv(x, "head", 1, 1)
         self.inflight.after_forward()

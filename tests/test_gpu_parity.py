@@ -479,6 +479,24 @@ def test_fused_narrow_input_channels(sc, rng, c_in):
     assert rel_l2(out.features_numpy(), want) <= 1e-2
 
 
+@pytest.mark.parametrize("dataflow", ["staged", "fused"])
+@pytest.mark.parametrize("k,ca,cb", [(3, 32, 16), (1, 64, 32), (3, 8, 24)])
+def test_concat_input_vs_oracle(sc, rng, dataflow, k, ca, cb):
+    """concat= (a U-Net skip read in place by the fused kernel) equals the
+    layer on the materialised channel concatenation."""
+    coords = random_coords(rng, (20, 20, 20), 0.15)
+    n = coords.shape[0]
+    fa = O.quantize(rng.standard_normal((n, ca)).astype(np.float32), "fp16")
+    fb = O.quantize(rng.standard_normal((n, cb)).astype(np.float32), "fp16")
+    w = rng.normal(0, 1 / np.sqrt(k ** 3 * (ca + cb)), (k ** 3, ca + cb, 48)).astype(np.float32)
+    _, want, _ = O.conv_forward(coords, np.concatenate([fa, fb], 1), (20, 20, 20), w, k, 1)
+    t = sc.SparseTensor(coords, fa, 1, (20, 20, 20))
+    skip = sc.SparseTensor(coords, fb, 1, (20, 20, 20))
+    out = sc.sparse_conv_forward(t, sc.WeightTensor(w, k, 3), sc.LayerSpec(k, 1, ca + cb, 48),
+                                 None, None, sc.ExecOptions(dataflow=dataflow), concat=skip)
+    assert rel_l2(out.features_numpy(), want) <= 1e-2
+
+
 def test_lazy_map_needs_no_compaction_for_fused(sc, rng):
     coords = random_coords(rng, (16, 16, 16), 0.1)
     t = sc.SparseTensor(coords, rng.standard_normal((coords.shape[0], 16)).astype(np.float16),
