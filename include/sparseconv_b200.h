@@ -274,11 +274,13 @@ int32_t scb_conv_implicit(const void* features, int64_t n_in, int32_t c_in, int6
 /* scb_conv_implicit with the input split channel-wise over two row-aligned
  * matrices: channels [0, c_split) from `features` (row stride ldf), [c_split,
  * c_in) from `features2` (row stride ldf2) — the skip concatenation of a
- * U-Net decoder without materialising it.  `features2` NULL = scb_conv_implicit. */
+ * U-Net decoder without materialising it.  `features2` NULL = scb_conv_implicit.
+ * `ldo`: output row stride in elements (multiple of 8, >= c_out), so C_out
+ * need not be a multiple of 8 (e.g. a 19-class head into 24-wide rows). */
 int32_t scb_conv_implicit_cat(const void* features, int64_t ldf, int32_t c_split,
                               const void* features2, int64_t ldf2, int64_t n_in, int32_t c_in,
                               const int32_t* hits, int32_t volume, int64_t n_out,
-                              const void* weights_packed, int32_t c_out, void* out,
+                              const void* weights_packed, int32_t c_out, void* out, int64_t ldo,
                               const float* scale, const float* shift, const float* bias,
                               const void* residual, int32_t relu, scb_stream_t stream);
 

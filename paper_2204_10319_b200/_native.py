@@ -83,7 +83,7 @@ _SIGS = {
     "scb_conv_implicit": (_I32, [_P, _I64, _I32, _I64, _P, _I32, _I64, _P, _I32, _P, _P, _P, _P,
                                  _P, _I32, _P]),
     "scb_conv_implicit_cat": (_I32, [_P, _I64, _I32, _P, _I64, _I64, _I32, _P, _I32, _I64, _P,
-                                     _I32, _P, _P, _P, _P, _P, _I32, _P]),
+                                     _I32, _P, _I64, _P, _P, _P, _P, _I32, _P]),
 }
 
 _lib = None

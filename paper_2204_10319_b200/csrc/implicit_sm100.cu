@@ -455,9 +455,9 @@ extern "C" int32_t scb_conv_implicit_cat(const void* features, int64_t ldf, int3
                                          const void* features2, int64_t ldf2, int64_t n_in,
                                          int32_t c_in, const int32_t* hits, int32_t volume,
                                          int64_t n_out, const void* weights_packed,
-                                         int32_t c_out, void* out, const float* scale,
-                                         const float* shift, const float* bias,
-                                         const void* residual, int32_t relu,
+                                         int32_t c_out, void* out, int64_t ldo,
+                                         const float* scale, const float* shift,
+                                         const float* bias, const void* residual, int32_t relu,
                                          scb_stream_t stream);
 
 extern "C" int32_t scb_conv_implicit(const void* features, int64_t n_in, int32_t c_in,
@@ -467,17 +467,17 @@ extern "C" int32_t scb_conv_implicit(const void* features, int64_t n_in, int32_t
                                      const float* bias, const void* residual, int32_t relu,
                                      scb_stream_t stream) {
   return scb_conv_implicit_cat(features, ldf, c_in, nullptr, 0, n_in, c_in, hits, volume, n_out,
-                               weights_packed, c_out, out, scale, shift, bias, residual, relu,
-                               stream);
+                               weights_packed, c_out, out, c_out, scale, shift, bias, residual,
+                               relu, stream);
 }
 
 extern "C" int32_t scb_conv_implicit_cat(const void* features, int64_t ldf, int32_t c_split,
                                          const void* features2, int64_t ldf2, int64_t n_in,
                                          int32_t c_in, const int32_t* hits, int32_t volume,
                                          int64_t n_out, const void* weights_packed,
-                                         int32_t c_out, void* out, const float* scale,
-                                         const float* shift, const float* bias,
-                                         const void* residual, int32_t relu,
+                                         int32_t c_out, void* out, int64_t ldo,
+                                         const float* scale, const float* shift,
+                                         const float* bias, const void* residual, int32_t relu,
                                          scb_stream_t stream) {
   using namespace ic;
   SCB_CHECK_ARG(features2 == nullptr || (c_split % 8 == 0 && c_split > 0 && c_split < c_in &&
@@ -488,7 +488,9 @@ extern "C" int32_t scb_conv_implicit_cat(const void* features, int64_t ldf, int3
   SCB_CHECK_ARG(volume == 1 || hits != nullptr, "hit matrix required for K > 1");
   SCB_CHECK_ARG(volume != 1 || n_in == n_out, "K = 1: identity map needs n_in == n_out");
   SCB_CHECK_ARG(c_in % 8 == 0 && ldf % 8 == 0, "C_in and its row stride must be multiples of 8");
-  SCB_CHECK_ARG(c_out % 8 == 0, "C_out must be a multiple of 8");
+  SCB_CHECK_ARG(ldo % 8 == 0 && ldo >= c_out && ldo * 2 < (1LL << 32),
+                "output row stride must be a multiple of 8 elements, >= C_out");
+  SCB_CHECK_ARG(residual == nullptr || c_out % 8 == 0, "a residual needs C_out % 8 == 0");
   SCB_CHECK_ARG(ldf * 2 < (1LL << 32), "feature row stride too large");
   SCB_CHECK_ARG((scale == nullptr) == (shift == nullptr), "scale and shift go together");
   SCB_CHECK_ARG(n_in < (1LL << 31) - 1 && (long long)volume * hits_ld(n_out) < (1LL << 31),
@@ -581,7 +583,7 @@ extern "C" int32_t scb_conv_implicit_cat(const void* features, int64_t ldf, int3
   std::string err;
   if (!encode_map_2d(&mB, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, weights_packed, k_pad,
                      (long long)volume * n_pad, k_pad, p.kc, n_pad, p.swz, err) ||
-      !encode_map_2d(&mO, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, out, c_out, n_out, c_out,
+      !encode_map_2d(&mO, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, out, c_out, n_out, ldo,
                      p.epi_cols, 32, p.epi_cols * 2, err)) {
     set_error(std::string("scb_conv_implicit: ") + err);
     return SCB_ECUDA;

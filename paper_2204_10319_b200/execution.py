@@ -504,11 +504,11 @@ def _epi_args(ep: dict | None):
 
 
 def _fused_eligible(dtype, volume: int, w: WeightTensor) -> bool:
-    """The implicit-GEMM kernel: FP16 storage, K^3 in {1, 8, 27}, C_out a
-    multiple of 8 (16-B TMA rows of the output) up to 256.  C_in that is not
-    a multiple of 8 (the 4-channel stem) is zero-padded to one."""
-    return (dtype == torch.float16 and volume in (1, 8, 27) and w.c_out % 8 == 0
-            and w.c_out <= 256)
+    """The implicit-GEMM kernel: FP16 storage, K^3 in {1, 8, 27}, C_out up to
+    256 (C_out not a multiple of 8, e.g. the 19-class head, is written into
+    8-aligned rows and returned as a view).  C_in that is not a multiple of 8
+    (the 4-channel stem) is zero-padded to one."""
+    return dtype == torch.float16 and volume in (1, 8, 27) and w.c_out <= 256
 
 
 def choose_dataflow(opts: ExecOptions, dtype, kmap: KernelMap | None, w: WeightTensor) -> str:
@@ -543,22 +543,24 @@ def _run_fused(features: torch.Tensor, kmap: KernelMap | None, w: WeightTensor,
     packed, _, _ = w.packed_f16()
     volume = 1 if kmap is None else kmap.offsets.volume
     n_out = features.shape[0] if kmap is None else kmap.n_out
-    out = torch.empty((n_out, w.c_out), dtype=features.dtype, device=features.device)
+    ldo = (w.c_out + 7) // 8 * 8
+    out = torch.empty((n_out, ldo), dtype=features.dtype, device=features.device)
     scale, shift, bias, res, relu = _epi_args(epilogue)
     hits = None if kmap is None else nat.ptr(kmap.hits)
     with _timed(timer, label, "fused"):
         if concat is not None and features.shape[1] % 8 == 0 and concat.shape[1] % 8 == 0 \
                 and features.is_contiguous() and concat.is_contiguous():
-            ca, cb = features.shape[1], concat.shape[1]
-            nat.call("scb_conv_implicit_cat", nat.ptr(features), ca, ca, nat.ptr(concat), cb,
-                     features.shape[0], ca + cb, hits, volume, n_out, nat.ptr(packed), w.c_out,
-                     nat.ptr(out), scale, shift, bias, res, relu, nat.stream_handle())
+            f, ca, f2, cb = features, features.shape[1], concat, concat.shape[1]
         else:
             f = features if concat is None else torch.cat([features, concat], dim=1)
-            f = _pad_channels(f)
-            nat.call("scb_conv_implicit", nat.ptr(f), f.shape[0], f.shape[1], f.shape[1], hits,
-                     volume, n_out, nat.ptr(packed), w.c_out, nat.ptr(out), scale, shift, bias,
-                     res, relu, nat.stream_handle())
+            f, ca, f2, cb = _pad_channels(f), None, None, 0
+            ca = f.shape[1]
+        nat.call("scb_conv_implicit_cat", nat.ptr(f), f.shape[1], ca, nat.ptr(f2),
+                 0 if f2 is None else f2.shape[1], f.shape[0], ca + cb, hits, volume, n_out,
+                 nat.ptr(packed), w.c_out, nat.ptr(out), ldo, scale, shift, bias, res, relu,
+                 nat.stream_handle())
+    if ldo != w.c_out:
+        out = out[:, : w.c_out]  # 8-aligned rows for the TMA store; a strided view
     if opts.traffic_log is not None:
         e = 2
         opts.traffic_log.append((label, {

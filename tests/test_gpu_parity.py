@@ -394,7 +394,8 @@ def test_4d_and_2d_layers_vs_oracle(sc):
             assert rel_l2(out.features_numpy(), of) <= 1e-4
 
 
-@pytest.mark.parametrize("c_in,c_out", [(64, 64), (32, 48), (16, 16), (96, 128), (256, 256)])
+@pytest.mark.parametrize("c_in,c_out", [(64, 64), (32, 48), (16, 16), (96, 128), (256, 256),
+                                         (16, 20)])
 def test_fused_dataflow_vs_oracle(sc, c_in, c_out):
     """The implicit-GEMM kernel (gather fused into the tcgen05 operand load)
     against the oracle: k3 s1, k2 s2 and the transposed k2 layer."""
@@ -446,7 +447,7 @@ def test_epilogue_bn_residual_relu(sc, rng, dataflow):
     assert (got >= 0).all()
 
 
-@pytest.mark.parametrize("c_in,c_out", [(64, 96), (128, 256), (32, 32)])
+@pytest.mark.parametrize("c_in,c_out", [(64, 96), (128, 256), (32, 32), (96, 19)])
 def test_fused_pointwise_layer(sc, rng, c_in, c_out):
     """K=1 layer through the implicit kernel (V = 1, identity map, BN + ReLU
     in the epilogue) against the oracle (execution.py:472-477)."""
