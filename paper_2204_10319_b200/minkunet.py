@@ -174,11 +174,11 @@ class EngineMinkUNet:
                 finish = prepare_strided_chain(t.coordset, self._down_specs(), base,
                                                deferred=True)
         x = conv(t, "stem.0", 3, 1)
-        if finish is not None:
+        x = conv(x, "stem.1", 3, 1)
+        if finish is not None:  # both level-0 stems are queued: the GPU stays busy meanwhile
             from .execution import LayerSpec, prepare_layer_maps
             for lvl in finish():
                 prepare_layer_maps(lvl, LayerSpec(3, 1, 1, 1), base)
-        x = conv(x, "stem.1", 3, 1)
         skips = [x]
         for i in range(1, 5):
             x = conv(x, f"down{i}", 2, 2)
