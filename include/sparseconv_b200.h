@@ -284,6 +284,21 @@ int32_t scb_conv_implicit_cat(const void* features, int64_t ldf, int32_t c_split
                               const float* scale, const float* shift, const float* bias,
                               const void* residual, int32_t relu, scb_stream_t stream);
 
+/* ---------------------------------------------------------------- voxelisation
+ * Replaces voxelize (core.py:174-216), the step in front of the path
+ * (SURVEY.md §8(f) row 2): `points` f64 [n][cols] (first spatial_dims
+ * columns are positions), cells = floor((p - min) / voxel_size), boundary =
+ * max + 1, rows in ascending flat-key order, features merged by the f64 mean
+ * in point order (reduce_first = 0) or taken from the first point (1) and
+ * rounded once to f32 — bit-exact with the reference.  `out_coords` int32
+ * [n][1+D] and `out_features` f32 [n][cols-D] need room for n rows; `meta`
+ * (device int64 [1+D]) receives the voxel count and the boundary. */
+int64_t scb_voxelize_workspace(int64_t n_points, int32_t spatial_dims);
+int32_t scb_voxelize(const double* points, int64_t n_points, int32_t cols, int32_t spatial_dims,
+                     double voxel_size, int32_t reduce_first, void* workspace, int64_t ws_bytes,
+                     int32_t* out_coords, float* out_features, int64_t* meta,
+                     scb_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

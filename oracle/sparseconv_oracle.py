@@ -62,6 +62,32 @@ def unflatten(keys, boundary):
     return out
 
 
+def voxelize(points, voxel_size, reduce="mean", spatial_dims=3):
+    """core.py:174-216: cells = floor((p - min) / voxel_size) in f64, boundary
+    = max + 1, rows sorted by flat key; duplicates merged by the f64 mean
+    (np.bincount: sequential sum in point order, core.py:207-211) or the
+    first point (core.py:205-206).  Returns (coords int64, features f32,
+    boundary)."""
+    pts = np.asarray(points, dtype=np.float64)
+    xyz, feats = pts[:, :spatial_dims], pts[:, spatial_dims:]
+    cells = np.floor((xyz - xyz.min(axis=0)) / voxel_size).astype(np.int64)
+    boundary = tuple(int(m) + 1 for m in cells.max(axis=0))
+    key = np.zeros(cells.shape[0], dtype=np.int64)
+    for d, b in enumerate(boundary):
+        key = key * b + cells[:, d]
+    uniq, first, inverse = np.unique(key, return_index=True, return_inverse=True)
+    if reduce == "first":
+        merged = feats[first].astype(np.float32)
+    else:
+        counts = np.bincount(inverse, minlength=uniq.shape[0]).astype(np.float64)
+        merged = np.empty((uniq.shape[0], feats.shape[1]), dtype=np.float32)
+        for c in range(feats.shape[1]):
+            merged[:, c] = (np.bincount(inverse, weights=feats[:, c], minlength=uniq.shape[0])
+                            / counts).astype(np.float32)
+    return np.concatenate([np.zeros((uniq.shape[0], 1), np.int64),
+                           unflatten(uniq, boundary)[:, 1:]], axis=1), merged, boundary
+
+
 def offsets(dim, kernel_size):
     """Lexicographic K**D window; centred for odd K, {0..K-1} for even K
     (mapping.py:63-79, EVEN_KERNEL_OFFSET_BASE = 0 at mapping.py:26)."""

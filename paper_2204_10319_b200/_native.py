@@ -57,6 +57,8 @@ _SIGS = {
     "scb_output_keys_next": (_I32, [_P, _P, _I64, _GP, _GP, _I32, _I32, _I32, _P, _I64, _P, _P,
                                     _P]),
     "scb_unflatten": (_I32, [_P, _I64, _GP, _P, _P]),
+    "scb_voxelize_workspace": (_I64, [_I64, _I32]),
+    "scb_voxelize": (_I32, [_P, _I64, _I32, _I32, ctypes.c_double, _I32, _P, _I64, _P, _P, _P, _P]),
     "scb_map_search": (_I32, [_I32, _P, _I64, _GP, _I32, _I32, _I32, _I32, _P, _P, _I64, _P, _P]),
     "scb_map_workspace": (_I64, [_I32, _I64]),
     "scb_map_count": (_I32, [_P, _I32, _I64, _P, _P, _P]),

@@ -289,6 +289,45 @@ class WeightTensor:
         return self._packed
 
 
+def voxelize(points, voxel_size: float, reduce: str = "mean",
+             spatial_dims: int = 3) -> SparseTensor:
+    """Quantize a raw point cloud onto the voxel lattice on the device
+    (reference core.py:174-216, same errors): cells = floor((p - min) /
+    voxel_size), duplicates merged by the f64 mean or the first point, rows
+    in ascending flat-key order — bit-exact with the reference.  ``points``:
+    (n, cols) array or tensor (host or device), first ``spatial_dims``
+    columns are positions.  One host read (the voxel count and boundary)."""
+    if isinstance(points, torch.Tensor):
+        p = points.to(device=_device(), dtype=torch.float64).contiguous()
+    else:
+        arr = np.asarray(points, dtype=np.float64)
+        p = torch.from_numpy(np.ascontiguousarray(arr)).to(_device())
+    if p.ndim != 2 or p.shape[0] == 0:
+        raise ValueError("empty cloud")
+    if p.shape[1] < spatial_dims:
+        raise ValueError(f"points need at least {spatial_dims} columns")
+    if voxel_size <= 0:
+        raise ValueError("voxel_size must be positive")
+    if reduce not in ("mean", "first"):
+        raise ValueError(f"unknown reduce {reduce!r}")
+    n, cols = p.shape
+    lib = nat.load()
+    ws = torch.empty(int(lib.scb_voxelize_workspace(n, spatial_dims)), dtype=torch.uint8,
+                     device=p.device)
+    coords = torch.empty((n, 1 + spatial_dims), dtype=torch.int32, device=p.device)
+    feats = torch.empty((n, cols - spatial_dims), dtype=torch.float32, device=p.device)
+    meta = torch.empty(1 + spatial_dims, dtype=torch.int64, device=p.device)
+    nat.call("scb_voxelize", nat.ptr(p), n, cols, spatial_dims, float(voxel_size),
+             int(reduce == "first"), nat.ptr(ws), ws.numel(), nat.ptr(coords),
+             nat.ptr(feats) if feats.numel() else None, nat.ptr(meta), nat.stream_handle())
+    m = meta.tolist()
+    nv = int(m[0])
+    boundary = tuple(int(b) for b in m[1:])
+    c = coords[:nv]
+    cset = CoordinateSet(c, boundary, 1)
+    return SparseTensor._wrap(feats[:nv], 1, boundary, 1, cset)
+
+
 def quantize_features(t: SparseTensor, mode: PrecisionMode) -> SparseTensor:
     """Convert feature storage precision (reference core.py:219-238): FP16
     rounds to nearest and saturates to +-65504 with a warning."""

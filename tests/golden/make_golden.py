@@ -240,7 +240,29 @@ def gen_config1():
     print("config1.npz n =", t.num_points, "|M| =", int(kmap.sizes.sum()))
 
 
+def gen_voxelize():
+    """sparseconv.core.voxelize (core.py:174-216) on seeded clouds: mean and
+    first reduction, 2-D and 3-D, clouds with many duplicate cells."""
+    cases = {}
+    rng = np.random.default_rng(777)
+    for i, (n, dims, ch, vs, reduce) in enumerate([
+            (4000, 3, 4, 4.0, "mean"), (4000, 3, 4, 4.0, "first"), (3000, 3, 2, 1.5, "mean"),
+            (2000, 2, 3, 1.0, "mean"), (1, 3, 1, 1.0, "mean"), (3000, 3, 5, 8.0, "first"),
+            (3000, 3, 0, 2.0, "mean")]):
+        xyz = rng.uniform(-20, 20, size=(n, dims))
+        pts = np.concatenate([xyz, rng.standard_normal((n, ch))], axis=1)
+        t = sc.voxelize(pts, vs, reduce=reduce, spatial_dims=dims)
+        cases[f"v{i}_points"] = pts
+        cases[f"v{i}_meta"] = np.array([dims, 1 if reduce == "first" else 0], dtype=np.int64)
+        cases[f"v{i}_vs"] = np.array([vs], dtype=np.float64)
+        cases[f"v{i}_coords"] = np.asarray(t.coords, dtype=np.int64)
+        cases[f"v{i}_feats"] = np.asarray(t.features, dtype=np.float32)
+        cases[f"v{i}_boundary"] = np.asarray(t.boundary, dtype=np.int64)
+    np.savez_compressed(OUT / "voxelize.npz", **cases)
+
+
 if __name__ == "__main__":
+    gen_voxelize()
     gen_maps()
     gen_layers()
     gen_plans()

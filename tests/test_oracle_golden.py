@@ -8,7 +8,7 @@ import re
 import numpy as np
 import pytest
 
-from conftest import unpack_pairs
+from conftest import GOLDEN, unpack_pairs
 from oracle import sparseconv_oracle as O
 
 
@@ -144,3 +144,19 @@ def test_partition_hand_trace():
     assert O.partition([100, 95, 90, 50, 48], 0.1, range(5)) == [(0, 3), (3, 5)]
     with pytest.raises(ValueError):
         O.partition([1, 2], 1.5, range(2))
+
+
+def test_voxelize_matches_reference_golden():
+    """oracle.voxelize == the unmodified reference's core.voxelize
+    (tests/golden/voxelize.npz), bit-exact coordinates and features."""
+    g = np.load(GOLDEN / "voxelize.npz")
+    i = 0
+    while f"v{i}_points" in g.files:
+        dims, first = (int(x) for x in g[f"v{i}_meta"])
+        c, f, b = O.voxelize(g[f"v{i}_points"], float(g[f"v{i}_vs"][0]),
+                             "first" if first else "mean", dims)
+        np.testing.assert_array_equal(c, g[f"v{i}_coords"])
+        np.testing.assert_array_equal(f, g[f"v{i}_feats"])
+        assert tuple(b) == tuple(int(x) for x in g[f"v{i}_boundary"])
+        i += 1
+    assert i >= 6
