@@ -53,6 +53,7 @@ struct Params {
   int n_in, c_in, c_out, V, n_pad, kc, n_kchunks, stages, swz, epi_cols, total_tiles, relu;
   int ops;                  // offsets per stage (small C_in -> several)
   int epi_bufs;             // epilogue staging buffers per warp (1 or 2)
+  int nacc;                 // TMEM accumulator buffers (2: epilogue overlaps the next tile)
   int debug;                // SCB_IMPLICIT_DEBUG: 1 no A loads, 16 wait counters, 32 no B loads
   int groups;               // ceil(V / ops) offset groups per tile
   uint32_t idesc, tmem_cols;
@@ -332,7 +333,7 @@ __global__ void __launch_bounds__(64 + 128 * P + 128, MINB)
       }
       if (elect_one()) mma_commit(tfull + acc);
       __syncwarp();
-      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      if (++acc == p.nacc) { acc = 0; acc_phase ^= 1; }
     }
   } else if (warp >= EPI0) {
     // ============ epilogue
@@ -421,7 +422,7 @@ __global__ void __launch_bounds__(64 + 128 * P + 128, MINB)
       tc_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(tempty + acc);
-      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      if (++acc == p.nacc) { acc = 0; acc_phase ^= 1; }
     }
     if (lane == 0) bulk_wait_all();
   }
@@ -520,8 +521,13 @@ extern "C" int32_t scb_conv_implicit_cat(const void* features, int64_t ldf, int3
   // Launch shape: two CTAs per SM when both accumulator pairs fit in TMEM
   // (C_out <= 128) -- one CTA's producer / MMA-issue gaps are filled by the
   // other -- else one; P producer threads per output row.
+  // Two accumulators per CTA (the epilogue of tile i overlaps tile i+1).
+  // SCB_IC_NACC=1 trades that for two CTAs per SM at C_out > 128: measured
+  // 3-5 % slower on the 256-channel layers.
+  p.nacc = 2;
+  if (const char* e = getenv("SCB_IC_NACC")) p.nacc = atoi(e) == 1 ? 1 : 2;
   uint32_t cols = 32;
-  while (cols < (uint32_t)(2 * n_pad)) cols *= 2;
+  while (cols < (uint32_t)(p.nacc * n_pad)) cols *= 2;
   p.tmem_cols = cols;
   int ctas = cols <= 256 ? 2 : 1;
   ctas = env_int("SCB_IMPLICIT_CTAS", ctas) == 2 && cols <= 256 ? 2 : 1;
