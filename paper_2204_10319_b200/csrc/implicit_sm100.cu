@@ -572,9 +572,9 @@ extern "C" int32_t scb_conv_implicit_cat(const void* features, int64_t ldf, int3
   p.a_off_bytes = r1024((uint32_t)(BM * p.kc * 2));
   p.b_off_bytes = r1024(p.b_tx);
   const uint32_t op_bytes = p.a_off_bytes + p.b_off_bytes;
-  int ops = (int)((uint32_t)env_int("SCB_IC_STAGE_KB", ctas == 2 ? 32 : 48) * 1024u / op_bytes);
+  int ops = (int)((uint32_t)env_int("SCB_IC_STAGE_KB", ctas == 2 ? 42 : 96) * 1024u / op_bytes);
   ops = std::max(1, std::min(ops, std::min(MAX_OPS, volume)));
-  ops = std::max(1, std::min(env_int("SCB_IMPLICIT_OPS", ops), std::min(MAX_OPS, volume)));
+  if (env_int("SCB_IMPLICIT_OPS", 0) > 0) ops = std::min(env_int("SCB_IMPLICIT_OPS", 0), std::min(MAX_OPS, volume));
   ops = std::min(ops, 32 / (cpr / P));  // one presence bit per 16-B item of a producer thread
   p.ops = ops;
   p.stage_bytes = ops * op_bytes;
