@@ -55,6 +55,7 @@ struct Params {
   int epi_bufs;             // epilogue staging buffers per warp (1 or 2)
   int nacc;                 // TMEM accumulator buffers (2: epilogue overlaps the next tile)
   int zfill_all;            // 1: every A item is one cp.async (zero-size when absent)
+  int rowmode;              // 1: one producer thread per row (needs P = 1)
   int debug;                // SCB_IMPLICIT_DEBUG: 1 no A loads, 16 wait counters, 32 no B loads
   int groups;               // ceil(V / ops) offset groups per tile
   uint32_t idesc, tmem_cols;
@@ -214,6 +215,12 @@ __global__ void __launch_bounds__(64 + 128 * P + 128, MINB)
       const int rxr = SWZ == 128 ? (r & 7) : (SWZ == 64 ? ((r >> 1) & 3) : ((r >> 2) & 1));
       roff[it] = (uint32_t)(r * (KC * 2)) + ((uint32_t)(cc ^ rxr) << 4);
     }
+    uint32_t sw[CPR];                         // row mode: swizzled offset of chunk c in the row
+#pragma unroll
+    for (int c = 0; c < CPR; ++c) {
+      const int rx = SWZ == 128 ? (row & 7) : (SWZ == 64 ? ((row >> 1) & 3) : ((row >> 2) & 1));
+      sw[c] = (uint32_t)((c ^ rx) << 4);
+    }
     const uint32_t ldfb1 = (uint32_t)(p.ldf * 2);   // row strides in bytes (host-checked < 2^32)
     const uint32_t ldfb2 = (uint32_t)(p.ldf2 * 2);
     for (int t = t_begin; t < t_end; ++t) {
@@ -250,7 +257,7 @@ __global__ void __launch_bounds__(64 + 128 * P + 128, MINB)
           // absent but written by the slot's previous use -> zero-fill;
           // absent and already zero -> nothing.  Chunks past C_in stay zero.
           uint32_t* wm = wmask + stage * NPROD + pt;
-          uint32_t now = p.zfill_all ? 0u : *wm;
+          uint32_t now = (p.zfill_all || p.rowmode) ? 0u : *wm;
           const uint32_t nbc = nb_s0 + (uint32_t)((g * p.ops * BM + cr) * 4);
           // this lane's 8 columns come from the first or (concat) second input
           const int col = col0 + cc * 8;
@@ -260,7 +267,46 @@ __global__ void __launch_bounds__(64 + 128 * P + 128, MINB)
               : reinterpret_cast<uint64_t>(p.feat) + (uint64_t)(col * 2);
           const uint32_t ldfb = second ? ldfb2 : ldfb1;
           const bool live_c = cc < live && !(p.debug & 1);
-          if (p.zfill_all) {
+          if (p.rowmode) {
+            // row per thread: one index load, one address and CPR cp.async
+            // (immediate chunk offsets) per (row, offset) -- ~2 instructions
+            // per 16-B item; chunks past C_in are skipped (they stay zero)
+            const bool mixed = p.feat2 != nullptr && col0 < p.c_split && col0 + KC > p.c_split;
+            const bool sec0 = p.feat2 != nullptr && col0 >= p.c_split;
+            const uint64_t fb0 = sec0
+                ? reinterpret_cast<uint64_t>(p.feat2) + (uint64_t)((col0 - p.c_split) * 2)
+                : reinterpret_cast<uint64_t>(p.feat) + (uint64_t)(col0 * 2);
+            const uint32_t ld0 = sec0 ? ldfb2 : ldfb1;
+            const int nlive = (p.debug & 1) ? 0 : live;
+            for (int o = 0; o < nv; ++o) {
+              int j;
+              asm volatile("ld.shared.b32 %0, [%1];" : "=r"(j) : "r"(nb_s0 + (uint32_t)(((g * p.ops + o) * BM + row) * 4)));
+              const uint32_t base = dst + o * p.a_off_bytes + row * (KC * 2);
+              const uint32_t jj = (uint32_t)max(j, 0);
+              if (!mixed) {
+                const uint64_t src = fb0 + (uint64_t)jj * (uint64_t)ld0;
+#pragma unroll
+                for (int c = 0; c < CPR; ++c)  // chunks past C_in: zero-filled (slots are reused)
+                  asm volatile(
+                      "{ .reg .pred q; setp.lt.s32 q, %2, 0;\n"
+                      "  cp.async.cg.shared.global [%0], [%1], 16, q; }" ::"r"(base + sw[c]),
+                      "l"(src + (uint64_t)(c * 16)), "r"(c < nlive ? j : -1) : "memory");
+              } else {
+                const uint64_t s1 = reinterpret_cast<uint64_t>(p.feat) + (uint64_t)jj * ldfb1;
+                const uint64_t s2 = reinterpret_cast<uint64_t>(p.feat2) + (uint64_t)jj * ldfb2;
+#pragma unroll
+                for (int c = 0; c < CPR; ++c) {
+                  const int col = col0 + c * 8;
+                  const uint64_t src = col < p.c_split ? s1 + (uint64_t)(col * 2)
+                                                       : s2 + (uint64_t)((col - p.c_split) * 2);
+                  asm volatile(
+                      "{ .reg .pred q; setp.lt.s32 q, %2, 0;\n"
+                      "  cp.async.cg.shared.global [%0], [%1], 16, q; }" ::"r"(base + sw[c]),
+                      "l"(src), "r"(c < nlive ? j : -1) : "memory");
+                }
+              }
+            }
+          } else if (p.zfill_all) {
             // lean form: every item is one cp.async whose source size is 16
             // (present) or 0 (zero-fill) -- no presence bookkeeping; the
             // producer is issue-bound, and this is ~3x fewer instructions
@@ -300,7 +346,7 @@ __global__ void __launch_bounds__(64 + 128 * P + 128, MINB)
               now = present ? (now | bit) : (now & ~bit);
             }
           }
-          if (!p.zfill_all) *wm = now;
+          if (!p.zfill_all && !p.rowmode) *wm = now;
           if ((p.debug & 16) && blockIdx.x == 0 && pt == 0) atomicAdd(&g_ic_prof[11], (unsigned long long)(clock64() - a_t0));
           if (p.debug & 128) {  // debug: wait for the copies, then a plain arrive
             cp_async_wait<0>();
@@ -556,6 +602,7 @@ extern "C" int32_t scb_conv_implicit_cat(const void* features, int64_t ldf, int3
   // 3-5 % slower on the 256-channel layers.
   p.nacc = 2;
   p.zfill_all = env_int("SCB_IC_ZFILL", 1) ? 1 : 0;  // measured faster on every shape
+  p.rowmode = env_int("SCB_IC_ROW", 0) ? 1 : 0;
   if (const char* e = getenv("SCB_IC_NACC")) p.nacc = atoi(e) == 1 ? 1 : 2;
   uint32_t cols = 32;
   while (cols < (uint32_t)(p.nacc * n_pad)) cols *= 2;
@@ -564,6 +611,7 @@ extern "C" int32_t scb_conv_implicit_cat(const void* features, int64_t ldf, int3
   ctas = env_int("SCB_IMPLICIT_CTAS", ctas) == 2 && cols <= 256 ? 2 : 1;
   const int cpr = p.kc / 8;
   int P = env_int("SCB_IC_P", 1) >= 2 ? 2 : 1;
+  if (p.rowmode) P = 1;
   if (cpr < P) P = 1;
   const int nprod = 128 * P;
   p.total_tiles = (int)((n_out + BM - 1) / BM);
