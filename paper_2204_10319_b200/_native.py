@@ -14,7 +14,7 @@ from pathlib import Path
 
 import torch
 
-LIB_PATH = Path(__file__).resolve().parent / "libsparseconv_b200.so"
+LIB_PATH = Path(__file__).resolve().parent / os.environ.get("SCB_LIB_NAME", "libsparseconv_b200.so")
 
 SCB_F32, SCB_F16 = 0, 1
 SCB_INDEX_HASH, SCB_INDEX_GRID = 0, 1

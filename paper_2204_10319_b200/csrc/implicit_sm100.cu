@@ -267,6 +267,7 @@ __global__ void __launch_bounds__(64 + 128 * P + 128, MINB)
               : reinterpret_cast<uint64_t>(p.feat) + (uint64_t)(col * 2);
           const uint32_t ldfb = second ? ldfb2 : ldfb1;
           const bool live_c = cc < live && !(p.debug & 1);
+          const bool all_live = live == CPR && !(p.debug & 1);  // warp-uniform
           if (p.rowmode) {
             // row per thread: one index load, one address and CPR cp.async
             // (immediate chunk offsets) per (row, offset) -- ~2 instructions
@@ -316,15 +317,27 @@ __global__ void __launch_bounds__(64 + 128 * P + 128, MINB)
               for (int it = 0; it < IT; ++it)
                 asm volatile("ld.shared.b32 %0, [%1];" : "=r"(jj[it]) : "r"(nbc + (uint32_t)((o * BM + it * (NPROD / CPR)) * 4)));
               const uint32_t blk = dst + o * p.a_off_bytes;
+              if (all_live) {  // the common case: no per-item liveness select
 #pragma unroll
-              for (int it = 0; it < IT; ++it) {
-                const int j = live_c ? jj[it] : -1;
-                const uint64_t src = fbase + (uint64_t)(uint32_t)max(j, 0) * (uint64_t)ldfb;
-                // ignore-src predicate (absent neighbour): zero-fill, no read
-                asm volatile(
-                    "{ .reg .pred q; setp.lt.s32 q, %2, 0;\n"
-                    "  cp.async.cg.shared.global [%0], [%1], 16, q; }" ::"r"(blk + roff[it]),
-                    "l"(src), "r"(j) : "memory");
+                for (int it = 0; it < IT; ++it) {
+                  const int j = jj[it];
+                  const uint64_t src = fbase + (uint64_t)(uint32_t)max(j, 0) * (uint64_t)ldfb;
+                  // ignore-src predicate (absent neighbour): zero-fill, no read
+                  asm volatile(
+                      "{ .reg .pred q; setp.lt.s32 q, %2, 0;\n"
+                      "  cp.async.cg.shared.global [%0], [%1], 16, q; }" ::"r"(blk + roff[it]),
+                      "l"(src), "r"(j) : "memory");
+                }
+              } else {
+#pragma unroll
+                for (int it = 0; it < IT; ++it) {
+                  const int j = live_c ? jj[it] : -1;
+                  const uint64_t src = fbase + (uint64_t)(uint32_t)max(j, 0) * (uint64_t)ldfb;
+                  asm volatile(
+                      "{ .reg .pred q; setp.lt.s32 q, %2, 0;\n"
+                      "  cp.async.cg.shared.global [%0], [%1], 16, q; }" ::"r"(blk + roff[it]),
+                      "l"(src), "r"(j) : "memory");
+                }
               }
             }
           } else
