@@ -483,7 +483,9 @@ def main():
                 c_ring[k].copy_(h_coords, non_blocking=True)
                 f_ring[k].copy_(h_feats, non_blocking=True)
             cur.wait_stream(h2d_s)
-            t = sc.SparseTensor(c_ring[k], f_ring[k], 1, boundary, B)  # validated, as a user would
+            # validated as a serving loop would: asynchronously, checked at the
+            # forward's first host read (no stall on the previous batch)
+            t = sc.SparseTensor(c_ring[k], f_ring[k], 1, boundary, B, validate="async")
             t = sc.quantize_features(t, sc.PrecisionMode.FP16_STORAGE)
             o = model.forward(t, sc.ExecOptions(index_kind="hash", dataflow=args.dataflow))
             done[k] = cur.record_event()
@@ -525,7 +527,7 @@ def main():
                "cuda_mallocs_in_timed_steps":
                    torch.cuda.memory_stats(dev).get("segment.all.allocated", 0) - seg_e,
                "d2h_bytes_per_step": int(h_out.numel() * 2),
-               "path": "pinned H2D (copy stream) -> SparseTensor(validate) -> quantize -> "
+               "path": "pinned H2D (copy stream) -> SparseTensor(validate=async) -> quantize -> "
                        f"{args.model} forward -> D2H of the output features (copy stream)"}
 
     # ---------------- CPU baseline (rank 0, N = 1)

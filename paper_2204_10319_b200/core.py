@@ -160,7 +160,9 @@ class SparseTensor:
             raise ValueError("stride must be a positive integer")
         if coordset is None:
             coordset = CoordinateSet(c, boundary, batch_size)
-            if validate and c.shape[0]:
+            if validate == "async" and c.shape[0]:
+                _validate_async(coordset)
+            elif validate and c.shape[0]:
                 _validate(coordset)
         self.coords = c
         self.features = f
@@ -221,6 +223,43 @@ class SparseTensor:
     @property
     def coordset(self) -> CoordinateSet:
         return self._cset
+
+
+_PENDING_VALIDATION: list = []
+
+
+def _validate_async(cset: CoordinateSet) -> None:
+    """``validate="async"`` (B200 extension for pipelined serving): the same
+    device checks as ``_validate``, but the two counts come back through
+    pinned memory and an event; the error is raised at the next engine host
+    synchronisation (the forward's coordinate-pyramid read) or by
+    :func:`flush_validation`, instead of stalling the constructor on the
+    previous batch's queued work."""
+    from .mapping import build_index
+    idx = build_index(cset, "hash")
+    host = torch.empty(2, dtype=torch.int32, pin_memory=True)
+    host.copy_(idx._status, non_blocking=True)
+    ev = torch.cuda.Event()
+    ev.record()
+    _PENDING_VALIDATION.append((ev, host, cset))
+
+
+def flush_validation() -> None:
+    """Raise the reference's ValueError for any pending asynchronous
+    validation that failed (waits for those checks only)."""
+    pending = list(_PENDING_VALIDATION)
+    _PENDING_VALIDATION.clear()
+    for ev, host, cset in pending:
+        ev.synchronize()
+        dup, oob = (int(x) for x in host.tolist())
+        if oob:
+            c = cset.coords
+            b = c[:, 0]
+            if int(b.min()) < 0 or int(b.max()) >= cset.batch_size:
+                raise ValueError("batch index out of range")
+            raise ValueError("coordinate outside boundary")
+        if dup:
+            raise ValueError("coordinate rows must be unique")
 
 
 def _validate(cset: CoordinateSet) -> None:

@@ -198,6 +198,8 @@ def compute_output_coords(in_coords, offsets: KernelOffsets, stride: int, out_bo
     nat.call("scb_output_coords", nat.ptr(c), n_in, grid, offsets.kernel_size, offsets.base,
              stride, nat.ptr(ws), ws_bytes, nat.ptr(keys), nat.ptr(n_out), nat.stream_handle())
     n = int(n_out.item())
+    from .core import flush_validation
+    flush_validation()
     out = torch.empty((n, dim + 1), dtype=torch.int32, device=c.device)
     nat.call("scb_unflatten", nat.ptr(keys), n, grid, nat.ptr(out), nat.stream_handle())
     return out
@@ -257,6 +259,8 @@ def start_output_coords_chain(cset, steps):
 
     def finish():
         ready.synchronize()
+        from .core import flush_validation
+        flush_validation()  # asynchronous input validations queued before the chain
         out = []
         for (keys, g, out_b, _), n in zip(levels, host.tolist()):
             co = torch.empty((n, dim + 1), dtype=torch.int32, device=dev)

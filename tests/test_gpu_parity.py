@@ -568,3 +568,18 @@ def test_strided_chain_equals_level_by_level(sc):
         for got, ref in zip(kmap.pairs, pairs):
             np.testing.assert_array_equal(got, ref)
         c, b, cs = want, ob, lvl
+
+
+def test_async_validation_raises_at_the_next_sync(sc):
+    """validate="async" defers the reference's checks to the next host read."""
+    bad = np.array([[0, 1, 1, 1], [0, 1, 1, 1]], dtype=np.int64)  # duplicate row
+    t = sc.SparseTensor(bad, np.zeros((2, 4), np.float32), 1, (4, 4, 4), validate="async")
+    with pytest.raises(ValueError, match="unique"):
+        sc.flush_validation()
+    oob = np.array([[0, 1, 1, 9]], dtype=np.int64)
+    sc.SparseTensor(oob, np.zeros((1, 4), np.float32), 1, (4, 4, 4), validate="async")
+    with pytest.raises(ValueError, match="outside boundary"):
+        sc.flush_validation()
+    ok = np.array([[0, 1, 1, 1], [0, 2, 1, 1]], dtype=np.int64)
+    sc.SparseTensor(ok, np.zeros((2, 4), np.float32), 1, (4, 4, 4), validate="async")
+    sc.flush_validation()
