@@ -47,8 +47,14 @@ __global__ void __launch_bounds__(256) gather_kernel(const VT* __restrict__ feat
 #pragma unroll
     for (int u = 0; u < UNROLL; ++u) {
       const long long t = base + u * stride;
-      r[u] = t / vecs_per_row;
-      v[u] = (int)(t - r[u] * vecs_per_row);
+      if (total < (1LL << 31)) {  // 32-bit division (a 64-bit one is ~4x the instructions)
+        const unsigned q = (unsigned)t / (unsigned)vecs_per_row;
+        r[u] = q;
+        v[u] = (int)((unsigned)t - q * (unsigned)vecs_per_row);
+      } else {
+        r[u] = t / vecs_per_row;
+        v[u] = (int)(t - r[u] * vecs_per_row);
+      }
       src[u] = t < total ? __ldg(buf_in + r[u]) : -1;
     }
     VT val[UNROLL];
@@ -58,8 +64,8 @@ __global__ void __launch_bounds__(256) gather_kernel(const VT* __restrict__ feat
       else memset(&val[u], 0, sizeof(VT));
     }
 #pragma unroll
-    for (int u = 0; u < UNROLL; ++u)
-      if (base + u * stride < total) buf[r[u] * ldb_v + v[u]] = val[u];
+    for (int u = 0; u < UNROLL; ++u)  // streaming stores: the buffer is read once, by the GEMM
+      if (base + u * stride < total) __stcs(buf + r[u] * ldb_v + v[u], val[u]);
   }
 }
 
@@ -158,6 +164,21 @@ __global__ void __launch_bounds__(256) scatter_kernel(const float* __restrict__ 
 #pragma unroll
       for (int i = 0; i < VEC; ++i)
         if (c0 + i < c_out) acc[i] += __ldg(src + i);
+    }
+    if constexpr (VEC == 4 && sizeof(OutT) == 2) {
+      // one 8-byte store of the four channels (row starts are 8-byte aligned
+      // when the row stride is a multiple of 4; checked by the launcher)
+      if (c0 + 4 <= c_out && (ldo & 3) == 0) {
+        __half2 lo = __floats2half2_rn(epilogue<OutT>(acc[0], k, c0, ldo, e),
+                                       epilogue<OutT>(acc[1], k, c0 + 1, ldo, e));
+        __half2 hi = __floats2half2_rn(epilogue<OutT>(acc[2], k, c0 + 2, ldo, e),
+                                       epilogue<OutT>(acc[3], k, c0 + 3, ldo, e));
+        uint2 w;
+        w.x = *reinterpret_cast<uint32_t*>(&lo);
+        w.y = *reinterpret_cast<uint32_t*>(&hi);
+        *reinterpret_cast<uint2*>(out + k * ldo + c0) = w;
+        continue;
+      }
     }
 #pragma unroll
     for (int i = 0; i < VEC; ++i)
