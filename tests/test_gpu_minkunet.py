@@ -21,8 +21,9 @@ def scan():
     return _crop(workloads.semantickitti_scan(0), 0.25)
 
 
-@pytest.mark.parametrize("width", [0.5, 1.0])
-def test_minkunet_matches_oracle(scan, width):
+@pytest.mark.parametrize("width,dataflow", [(0.5, "staged"), (1.0, "staged"), (0.5, "auto"),
+                                            (1.0, "auto")])
+def test_minkunet_matches_oracle(scan, width, dataflow):
     import paper_2204_10319_b200 as sc
     from oracle import sparseconv_oracle as O
     from paper_2204_10319_b200.minkunet import EngineMinkUNet, forward_oracle
@@ -31,7 +32,7 @@ def test_minkunet_matches_oracle(scan, width):
     model = EngineMinkUNet(width, 4, 0)
     t = sc.quantize_features(sc.SparseTensor(coords, feats, 1, boundary, 1),
                              sc.PrecisionMode.FP16_STORAGE)
-    out = model.forward(t)
+    out = model.forward(t, sc.ExecOptions(dataflow=dataflow, index_kind="hash"))
     oc, of, ob = forward_oracle(model.params, width, coords, O.quantize(feats, "fp16"), boundary)
     np.testing.assert_array_equal(out.coords_numpy(), oc)
     got = out.features_numpy().astype(np.float64)
