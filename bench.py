@@ -66,7 +66,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--dataflow", choices=("staged", "fused", "auto"), default="auto")
-    ap.add_argument("--clock-ms", type=int, default=100, help="nvidia-smi sampling period (0: off)")
+    ap.add_argument("--clock-ms", type=int, default=10, help="clock sampling period (0: off)")
     return ap.parse_args()
 
 
@@ -235,11 +235,49 @@ def workload_config(args, world):
 # ------------------------------------------------------------------ clocks
 
 class Clocks:
+    """SM clock and throttle-reason samples during the timed region: an
+    in-process NVML thread (sub-millisecond queries, so a ~100 ms region
+    still gets tens of samples); nvidia-smi -lms as the fallback."""
+
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+               "sw_power_cap": 0x4}
+
     def __init__(self, path):
         self.path = path
         self.proc = None
+        self.thread = None
+        self.samples = []
+        self.window = None
 
-    def start(self, period_ms=100):
+    def start(self, period_ms=10, gpu_index=0):
+        import threading
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(gpu_index)
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+        except Exception:  # no NVML: nvidia-smi
+            return self._start_smi(max(period_ms, 20))
+        self.stop_flag = False
+
+        def run():
+            while not self.stop_flag:
+                t = time.perf_counter()
+                try:
+                    mhz = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                    rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                except Exception:
+                    break
+                self.samples.append((t, float(mhz), int(rs)))
+                time.sleep(period_ms / 1e3)
+        self.thread = threading.Thread(target=run, daemon=True)
+        self.thread.start()
+
+    def mark(self, t0, t1):
+        """The timed region, in time.perf_counter() seconds."""
+        self.window = (t0, t1)
+
+    def _start_smi(self, period_ms):
         try:
             self.fh = open(self.path, "w")
             self.proc = subprocess.Popen(
@@ -252,6 +290,16 @@ class Clocks:
             self.proc = None
 
     def stop(self, gpu_index):
+        if self.thread is not None:
+            self.stop_flag = True
+            self.thread.join()
+            lo, hi = self.window or (-1e30, 1e30)
+            inside = [x for x in self.samples if lo <= x[0] <= hi]
+            sel = inside or self.samples[-3:]
+            reasons = sorted(n for n, bit in self.REASONS.items() if any(r & bit for _, _, r in sel))
+            return {"sm_mhz": float(np.median([m for _, m, _ in sel])) if sel else None,
+                    "sm_max_mhz": self.max_mhz, "reasons": reasons, "samples": len(inside),
+                    "source": "NVML thread, samples inside the timed region"}
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.proc.terminate()
@@ -272,7 +320,7 @@ class Clocks:
                 if v.lower() == "active":
                     reasons.add(name)
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "source": "nvidia-smi -lms"}
 
 
 # ------------------------------------------------------------------ engine
@@ -346,7 +394,7 @@ def main():
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(args.steps)]
     if args.clock_ms > 0:
-        clocks.start(args.clock_ms)
+        clocks.start(args.clock_ms, local)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -361,6 +409,7 @@ def main():
     # flushes (and any mapping overlapping the previous step) are inside the
     # timed region.
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    hw0 = time.perf_counter()
     t_start.record()
     ms.wait_event(t_start)
     for i in range(args.steps):
@@ -373,6 +422,7 @@ def main():
         evs[i][1].record()
     t_end.record()
     torch.cuda.synchronize()
+    clocks.mark(hw0, time.perf_counter())
     if world > 1:
         dist.barrier()
     gc.enable()
