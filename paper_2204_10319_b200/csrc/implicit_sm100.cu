@@ -54,7 +54,6 @@ struct Params {
   int ops;                  // offsets per stage (small C_in -> several)
   int epi_bufs;             // epilogue staging buffers per warp (1 or 2)
   int nacc;                 // TMEM accumulator buffers (2: epilogue overlaps the next tile)
-  int zfill_all;            // 1: every A item is one cp.async (zero-size when absent)
   int rowmode;              // 1: one producer thread per row (needs P = 1)
   int debug;                // SCB_IMPLICIT_DEBUG: 1 no A loads, 16 wait counters, 32 no B loads
   int groups;               // ceil(V / ops) offset groups per tile
@@ -125,7 +124,6 @@ __global__ void __launch_bounds__(64 + 128 * P + 128, MINB)
   uint64_t* tfull = empty + p.stages;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
-  uint32_t* wmask = tmem_slot + 4;  // [stages][NPROD]: which of a thread's items hold data
 
   const long long k_t0 = clock64();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -202,7 +200,6 @@ __global__ void __launch_bounds__(64 + 128 * P + 128, MINB)
       const uint32_t base = smem_u32(smem + (size_t)s * p.stage_bytes);
       for (uint32_t b = (uint32_t)pt * 16u; b < p.a_stage_bytes; b += NPROD * 16u)
         asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(base + b), "r"(0) : "memory");
-      wmask[s * NPROD + pt] = 0u;
     }
     int stage = 0;
     uint32_t phase = 0;
@@ -252,12 +249,10 @@ __global__ void __launch_bounds__(64 + 128 * P + 128, MINB)
           const uint32_t dst = smem_u32(smem + (size_t)stage * p.stage_bytes);
           const int col0 = kk * KC;
           const int live = min(CPR, (p.c_in - col0) / 8);  // chunks inside C_in
-          // Stage buffers start zeroed and each 16-B item has one owner
-          // thread, so a thread only writes what changes: present -> copy;
-          // absent but written by the slot's previous use -> zero-fill;
-          // absent and already zero -> nothing.  Chunks past C_in stay zero.
-          uint32_t* wm = wmask + stage * NPROD + pt;
-          uint32_t now = (p.zfill_all || p.rowmode) ? 0u : *wm;
+          // Every 16-B item of the stage is written each time: a copy of a
+          // present neighbour's chunk or a zero-fill (absent neighbour, or a
+          // chunk past C_in).  (Tracking which slots already hold zeros halves
+          // the copies but costs more instructions: measured slower.)
           const uint32_t nbc = nb_s0 + (uint32_t)((g * p.ops * BM + cr) * 4);
           // this lane's 8 columns come from the first or (concat) second input
           const int col = col0 + cc * 8;
@@ -307,7 +302,7 @@ __global__ void __launch_bounds__(64 + 128 * P + 128, MINB)
                 }
               }
             }
-          } else if (p.zfill_all) {
+          } else {
             // lean form: every item is one cp.async whose source size is 16
             // (present) or 0 (zero-fill) -- no presence bookkeeping; the
             // producer is issue-bound, and this is ~3x fewer instructions
@@ -340,26 +335,7 @@ __global__ void __launch_bounds__(64 + 128 * P + 128, MINB)
                 }
               }
             }
-          } else
-          for (int o = 0; o < nv; ++o) {
-            int jj[IT];  // index loads first (volatile asm keeps the order): latencies overlap
-#pragma unroll
-            for (int it = 0; it < IT; ++it)
-              asm volatile("ld.shared.b32 %0, [%1];" : "=r"(jj[it]) : "r"(nbc + (uint32_t)((o * BM + it * (NPROD / CPR)) * 4)));
-            const uint32_t blk = dst + o * p.a_off_bytes;
-#pragma unroll
-            for (int it = 0; it < IT; ++it) {
-              const int j = jj[it];
-              const bool present = j >= 0;
-              const uint32_t bit = 1u << (it * MAXO + o);
-              const bool rezero = !present && (now & bit);
-              const void* src = reinterpret_cast<const void*>(
-                  fbase + (uint64_t)(uint32_t)max(j, 0) * (uint64_t)ldfb);
-              cp_async16_zfill_if(blk + roff[it], src, present, (present || rezero) && live_c);
-              now = present ? (now | bit) : (now & ~bit);
-            }
           }
-          if (!p.zfill_all && !p.rowmode) *wm = now;
           if ((p.debug & 16) && blockIdx.x == 0 && pt == 0) atomicAdd(&g_ic_prof[11], (unsigned long long)(clock64() - a_t0));
           if (p.debug & 128) {  // debug: wait for the copies, then a plain arrive
             cp_async_wait<0>();
@@ -614,7 +590,6 @@ extern "C" int32_t scb_conv_implicit_cat(const void* features, int64_t ldf, int3
   // SCB_IC_NACC=1 trades that for two CTAs per SM at C_out > 128: measured
   // 3-5 % slower on the 256-channel layers.
   p.nacc = 2;
-  p.zfill_all = env_int("SCB_IC_ZFILL", 1) ? 1 : 0;  // measured faster on every shape
   p.rowmode = env_int("SCB_IC_ROW", 0) ? 1 : 0;
   if (const char* e = getenv("SCB_IC_NACC")) p.nacc = atoi(e) == 1 ? 1 : 2;
   uint32_t cols = 32;
@@ -628,10 +603,7 @@ extern "C" int32_t scb_conv_implicit_cat(const void* features, int64_t ldf, int3
     ctas = (want >= 3 && cols <= 128) ? 3 : (want >= 2 && cols <= 256 ? 2 : 1);
   }
   const int cpr = p.kc / 8;
-  int P = env_int("SCB_IC_P", 1) >= 2 ? 2 : 1;
-  if (ctas == 3) P = 1;
-  if (p.rowmode) P = 1;
-  if (cpr < P) P = 1;
+  const int P = 1;  // producer threads per row (2 measured slower: more warps, same issue stream)
   const int nprod = 128 * P;
   p.total_tiles = (int)((n_out + BM - 1) / BM);
   auto r1024 = [](uint32_t x) { return (x + 1023u) / 1024u * 1024u; };
@@ -643,7 +615,6 @@ extern "C" int32_t scb_conv_implicit_cat(const void* features, int64_t ldf, int3
                   1024u / op_bytes);
   ops = std::max(1, std::min(ops, std::min(MAX_OPS, volume)));
   if (env_int("SCB_IMPLICIT_OPS", 0) > 0) ops = std::min(env_int("SCB_IMPLICIT_OPS", 0), std::min(MAX_OPS, volume));
-  ops = std::min(ops, 32 / (cpr / P));  // one presence bit per 16-B item of a producer thread
   p.ops = ops;
   p.stage_bytes = ops * op_bytes;
   p.ldf = ldf;
@@ -664,7 +635,7 @@ extern "C" int32_t scb_conv_implicit_cat(const void* features, int64_t ldf, int3
     return 1024 + 4 * epi_bufs * EPI_BUF + volume * BM * 4 + 40 * 8 + 64;
   };
   int smem_cap = ctas == 3 ? 75 * 1024 : (ctas == 2 ? 113 * 1024 : 227 * 1024);
-  auto fit = [&](int e) { return (smem_cap - fixed_bytes(e)) / (int)(p.stage_bytes + nprod * 4); };
+  auto fit = [&](int e) { return (smem_cap - fixed_bytes(e)) / (int)p.stage_bytes; };
   while (fit(1) < 2 && p.ops > 1) {  // fewer offsets per stage, then one CTA per SM
     --p.ops;
     p.stage_bytes = p.ops * op_bytes;
@@ -686,7 +657,7 @@ extern "C" int32_t scb_conv_implicit_cat(const void* features, int64_t ldf, int3
   stages = std::min(stages, std::max(2, env_int("SCB_IC_STAGES", 16)));
   SCB_CHECK_ARG(stages >= 2, "stage does not fit in shared memory");
   p.stages = stages;
-  const int smem = fixed_bytes(p.epi_bufs) + stages * (nprod * 4 + (int)p.stage_bytes);
+  const int smem = fixed_bytes(p.epi_bufs) + stages * (int)p.stage_bytes;
 
   CUtensorMap mB, mO;
   std::string err;
@@ -706,14 +677,9 @@ extern "C" int32_t scb_conv_implicit_cat(const void* features, int64_t ldf, int3
   };
   int rc = SCB_EINVAL;
 #define SCB_IC_LAUNCH_P(VV, KK)                                                                \
-  if (P == 2) {                                                                                \
-    rc = ctas == 2 ? launch(implicit_conv_f16_kernel<VV, KK, 2, 2>)                            \
-                   : launch(implicit_conv_f16_kernel<VV, KK, 2, 1>);                           \
-  } else {                                                                                     \
-    rc = ctas == 3 ? launch(implicit_conv_f16_kernel<VV, KK, 1, 3>)                            \
-       : ctas == 2 ? launch(implicit_conv_f16_kernel<VV, KK, 1, 2>)                            \
-                   : launch(implicit_conv_f16_kernel<VV, KK, 1, 1>);                           \
-  }
+  rc = ctas == 3 ? launch(implicit_conv_f16_kernel<VV, KK, 1, 3>)                              \
+     : ctas == 2 ? launch(implicit_conv_f16_kernel<VV, KK, 1, 2>)                              \
+                 : launch(implicit_conv_f16_kernel<VV, KK, 1, 1>);
 #define SCB_IC_LAUNCH_K(VV)                                                                    \
   if (p.kc == 64) { SCB_IC_LAUNCH_P(VV, 64) }                                                  \
   else if (p.kc == 32) { SCB_IC_LAUNCH_P(VV, 32) }                                             \
