@@ -66,7 +66,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--dataflow", choices=("staged", "fused", "auto"), default="auto")
-    ap.add_argument("--clock-ms", type=int, default=10, help="clock sampling period (0: off)")
+    ap.add_argument("--clock-ms", type=int, default=5, help="clock sampling period (0: off)")
     return ap.parse_args()
 
 
@@ -260,14 +260,22 @@ class Clocks:
             return self._start_smi(max(period_ms, 20))
         self.stop_flag = False
 
+        self.errors = 0
+
         def run():
             while not self.stop_flag:
                 t = time.perf_counter()
                 try:
                     mhz = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                except Exception:
+                    self.errors += 1
+                    time.sleep(period_ms / 1e3)
+                    continue
+                try:
                     rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
                 except Exception:
-                    break
+                    rs = 0
+                    self.errors += 1
                 self.samples.append((t, float(mhz), int(rs)))
                 time.sleep(period_ms / 1e3)
         self.thread = threading.Thread(target=run, daemon=True)
@@ -299,6 +307,7 @@ class Clocks:
             reasons = sorted(n for n, bit in self.REASONS.items() if any(r & bit for _, _, r in sel))
             return {"sm_mhz": float(np.median([m for _, m, _ in sel])) if sel else None,
                     "sm_max_mhz": self.max_mhz, "reasons": reasons, "samples": len(inside),
+                    "samples_total": len(self.samples), "nvml_errors": self.errors,
                     "source": "NVML thread, samples inside the timed region"}
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
@@ -409,6 +418,8 @@ def main():
     # flushes (and any mapping overlapping the previous step) are inside the
     # timed region.
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    switch0 = sys.getswitchinterval()
+    sys.setswitchinterval(5e-4)  # let the clock-sampler thread in between host issues
     hw0 = time.perf_counter()
     t_start.record()
     ms.wait_event(t_start)
@@ -423,6 +434,7 @@ def main():
     t_end.record()
     torch.cuda.synchronize()
     clocks.mark(hw0, time.perf_counter())
+    sys.setswitchinterval(switch0)
     if world > 1:
         dist.barrier()
     gc.enable()
