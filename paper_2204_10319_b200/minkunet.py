@@ -111,6 +111,7 @@ class EngineMinkUNet:
                                if __import__("os").environ.get("SCB_MAP_STREAM") == "1" else None)
         from .execution import InflightLimiter
         self.inflight = InflightLimiter(3)
+        self._specs = {}
 
     def _down_specs(self):
         from .execution import LayerSpec
@@ -138,17 +139,24 @@ class EngineMinkUNet:
         base = replace(options) if options is not None else ExecOptions()  # private copy
         cache = {}
 
+        specs = self._specs
+
         def conv(x, name, k, s, relu=True, reuse=None, kind="conv", residual=None, concat=None):
             w = self.w[name]
             opts = base
             opts.layer_label = name
             ep = {"relu": relu, "residual": residual}
             if name in self.bn:
-                ep.update(scale=self.bn[name][0], shift=self.bn[name][1])
+                ep["scale"], ep["shift"] = self.bn[name]
+            spec = specs.get(name)
+            if spec is None:  # static per layer: built once
+                if kind == "inverse":
+                    spec = LayerSpec(k, 1, w.c_in, w.c_out, transposed=True, reuse_key=reuse)
+                else:  # only strided maps are replayed (by the transposed layers)
+                    spec = LayerSpec(k, s, w.c_in, w.c_out, reuse_key=name if s > 1 else None)
+                specs[name] = spec
             if kind == "inverse":
-                spec = LayerSpec(k, 1, w.c_in, w.c_out, transposed=True, reuse_key=reuse)
                 return inverse_conv_forward(x, w, spec, cache, None, opts, epilogue=ep)
-            spec = LayerSpec(k, s, w.c_in, w.c_out, reuse_key=name)
             return sparse_conv_forward(x, w, spec, None, cache, opts, epilogue=ep, concat=concat)
 
         def res(x, prefix, has_proj, skip=None):
