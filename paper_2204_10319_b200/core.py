@@ -76,6 +76,40 @@ def unflatten_coords(keys, boundary, batch_size: int = 1):
     return torch.stack(cols, 1) if is_t else np.stack(cols, 1)
 
 
+class _PinnedRing:
+    """Small pinned host buffers for asynchronous device->host reads of
+    counts, reused round-robin (a fresh pinned allocation per read costs
+    ~0.1 ms of host time at the start of every forward).  A slot is reused
+    only after the event recorded with its last copy has completed."""
+
+    def __init__(self, slots: int = 64, words: int = 16):
+        self.buf = None
+        self.events = [None] * slots
+        self.slots, self.words, self.next = slots, words, 0
+
+    def take(self, n: int, dtype) -> torch.Tensor:
+        if n * torch.empty((), dtype=dtype).element_size() > self.words * 8:
+            return torch.empty(n, dtype=dtype, pin_memory=True)
+        if self.buf is None:
+            self.buf = torch.empty(self.slots * self.words, dtype=torch.int64, pin_memory=True)
+        i = self.next
+        self.next = (i + 1) % self.slots
+        ev = self.events[i]
+        if ev is not None:
+            ev.synchronize()  # (practically always done: 64 reads ago)
+        self.events[i] = None
+        return self.buf[i * self.words:(i + 1) * self.words].view(dtype)[:n]
+
+    def record(self, t: torch.Tensor, ev) -> None:
+        if self.buf is not None and t.untyped_storage().data_ptr() == \
+                self.buf.untyped_storage().data_ptr():
+            i = (t.data_ptr() - self.buf.data_ptr()) // (self.words * 8)
+            self.events[i] = ev
+
+
+PINNED = _PinnedRing()
+
+
 def _device() -> torch.device:
     nat.require_cuda()
     return torch.device("cuda", torch.cuda.current_device())
@@ -237,10 +271,11 @@ def _validate_async(cset: CoordinateSet) -> None:
     previous batch's queued work."""
     from .mapping import build_index
     idx = build_index(cset, "hash")
-    host = torch.empty(2, dtype=torch.int32, pin_memory=True)
+    host = PINNED.take(2, torch.int32)
     host.copy_(idx._status, non_blocking=True)
     ev = torch.cuda.Event()
     ev.record()
+    PINNED.record(host, ev)
     _PENDING_VALIDATION.append((ev, host, cset))
 
 
@@ -384,10 +419,11 @@ def quantize_features(t: SparseTensor, mode: PrecisionMode) -> SparseTensor:
     # The saturation count comes back asynchronously (pinned copy + event) so
     # quantising a network input does not stall the stream; the warning is
     # raised as soon as the count is known (next engine call, or any host read).
-    host = torch.empty(1, dtype=torch.int64, pin_memory=True)
+    host = PINNED.take(1, torch.int64)
     host.copy_(sat, non_blocking=True)
     ev = torch.cuda.Event()
     ev.record()
+    PINNED.record(host, ev)
     _PENDING_SATURATION.append((ev, host))
     return t.replace_features(out)
 

@@ -117,7 +117,7 @@ class CoordinateIndex:
         self.size = cset.num_points
         self._grid = nat.make_grid(self.boundary, self.batch_size)
         dev = cset.coords.device
-        status = torch.zeros(2, dtype=torch.int32, device=dev)
+        status = torch.empty(2, dtype=torch.int32, device=dev)  # zeroed by scb_index_build
         if kind == "hash":
             self.slots = int(nat.load().scb_hash_slots(self.size))
             self.keys = torch.empty(self.slots, dtype=torch.int64, device=dev)
@@ -225,7 +225,7 @@ def start_output_coords_chain(cset, steps):
     dev = c.device
     dim = c.shape[1] - 1
     n_cap = c.shape[0]
-    counts = torch.zeros(max(len(steps), 1), dtype=torch.int64, device=dev)
+    counts = torch.empty(max(len(steps), 1), dtype=torch.int64, device=dev)  # written by each level
     boundary, prev = cset.boundary, None
     levels = []
     for i, (offsets, stride) in enumerate(steps):
@@ -252,10 +252,12 @@ def start_output_coords_chain(cset, steps):
         boundary, n_cap = out_b, cap
     # the chain's one host read, asynchronous: the caller can queue other work
     # (e.g. the first convolutions) before calling the returned finisher
-    host = torch.empty(counts.shape, dtype=torch.int64, pin_memory=True)
+    from .core import PINNED
+    host = PINNED.take(counts.shape[0], torch.int64)
     host.copy_(counts, non_blocking=True)
     ready = torch.cuda.Event()
     ready.record()
+    PINNED.record(host, ready)
 
     def finish():
         ready.synchronize()

@@ -49,6 +49,17 @@ def main():
     busy += cur_e - cur_s
     print(f"span {(end - start) / 3e3:.2f} ms/step, GPU busy {busy / 3e3:.2f} ms/step "
           f"({100 * busy / (end - start):.0f}%)")
+    # the largest idle gaps of the last profiled step, with the kernels around them
+    seq = sorted(kern, key=lambda e: e.time_range.start)
+    gaps = []
+    for a, b in zip(seq, seq[1:]):
+        g = b.time_range.start - a.time_range.end
+        if g > 0:
+            gaps.append((g, a.name[:40], b.name[:40]))
+    gaps.sort(reverse=True)
+    for g, a, b in gaps[:12]:
+        print(f"gap {g:8.1f} us  after {a}  before {b}")
+    print(f"gaps > 5 us: {sum(1 for g in gaps if g[0] > 5)}, total {sum(g[0] for g in gaps) / 3e3:.3f} ms/step")
     agg = {}
     for e in kern:
         k = e.name[:60]
