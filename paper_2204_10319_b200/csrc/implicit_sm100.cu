@@ -153,6 +153,12 @@ __global__ void __launch_bounds__(64 + 128 * P + 128, MINB)
   __syncthreads();
   tc_after();
   const uint32_t tmem_base = *tmem_slot;
+  // Programmatic dependent launch: the prologue above (barriers, TMEM,
+  // tensor-map prefetch) overlapped the previous kernel's tail; wait for it
+  // (all its writes visible) before reading any input, and let the next
+  // layer's kernel start its own prologue as soon as SMs free up.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   if (warp == 0) {
     // ============ B producer: the stage's weight slices via TMA
@@ -672,7 +678,17 @@ extern "C" int32_t scb_conv_implicit_cat(const void* features, int64_t ldf, int3
   cudaStream_t s = as_stream(stream);
   auto launch = [&](auto kernel) -> int {
     SCB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_cap));
-    kernel<<<grid, 64 + nprod + 128, smem, s>>>(mB, mO, p);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(64 + nprod + 128);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = env_int("SCB_IC_PDL", 1) ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    SCB_CUDA(cudaLaunchKernelEx(&cfg, kernel, mB, mO, p));
     return SCB_OK;
   };
   int rc = SCB_EINVAL;

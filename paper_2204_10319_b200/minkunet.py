@@ -110,7 +110,7 @@ class EngineMinkUNet:
         self.mapping_stream = (torch.cuda.Stream(priority=-1)
                                if __import__("os").environ.get("SCB_MAP_STREAM") == "1" else None)
         from .execution import InflightLimiter
-        self.inflight = InflightLimiter(3)
+        self.inflight = InflightLimiter(int(__import__("os").environ.get("SCB_INFLIGHT", "3")))
         self._specs = {}
 
     def _down_specs(self):
