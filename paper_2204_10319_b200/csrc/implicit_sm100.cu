@@ -202,11 +202,7 @@ __global__ void __launch_bounds__(64 + 128 * P + 128, MINB)
                      ? (V == 1 ? (int)k : __ldg(p.hits + (long long)n * p.ldh + k)) : -1;
       }
     }
-    for (int s = 0; s < p.stages; ++s) {
-      const uint32_t base = smem_u32(smem + (size_t)s * p.stage_bytes);
-      for (uint32_t b = (uint32_t)pt * 16u; b < p.a_stage_bytes; b += NPROD * 16u)
-        asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(base + b), "r"(0) : "memory");
-    }
+    // (no stage zeroing: every 16-B item of a stage is rewritten each use)
     int stage = 0;
     uint32_t phase = 0;
     const uint32_t nb_s0 = smem_u32(nbr_s);
