@@ -57,6 +57,7 @@ struct Params {
   int rowmode;              // 1: one producer thread per row (needs P = 1)
   int debug;                // SCB_IMPLICIT_DEBUG: 1 no A loads, 16 wait counters, 32 no B loads
   int groups;               // ceil(V / ops) offset groups per tile
+  int bsleep, esleep;       // poll back-off (ns) of the weight producer / the epilogue
   uint32_t idesc, tmem_cols;
   uint32_t a_off_bytes;     // one offset's A block [128 rows][kc] (1024-aligned)
   uint32_t b_off_bytes;     // one offset's B block [n_pad][kc]   (1024-aligned)
@@ -100,6 +101,104 @@ __device__ __forceinline__ uint32_t pack_half2(float a, float b) {
 
 __device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// ============ epilogue role (4 warps; warp w reads TMEM lanes 32 (w % 4)..):
+// accumulator acc of tile t -> scale/shift, bias, residual, ReLU -> fp16 ->
+// swizzled staging buffer -> TMA store of 32 rows x epi_cols.
+__device__ __forceinline__ void epilogue_role(const Params& p, const CUtensorMap* tmOut_,
+                                              uint32_t tmem_base, uint64_t* tfull,
+                                              uint64_t* tempty, uint8_t* epi_base, int warp,
+                                              int epi0, int lane, int t_begin, int t_end) {
+  // ============ epilogue
+  const int q = warp & 3;
+  uint8_t* bufs = epi_base + (warp - epi0) * p.epi_bufs * EPI_BUF;
+  int acc = 0, nbuf = 0;
+  uint32_t acc_phase = 0;
+  const int chunks = p.n_pad / p.epi_cols;
+  for (int t = t_begin; t < t_end; ++t) {
+    IC_PROF(5, warp == epi0 && lane == 0, mbar_wait_sleep(tfull + acc, acc_phase, p.esleep));
+    tc_after();
+    const long long row0 = (long long)t * BM + 32 * q;
+    const long long k = row0 + lane;
+    const bool row_ok = k < p.n_out;
+    for (int j = 0; j < chunks && row0 < p.n_out; ++j) {
+      const int c0 = j * p.epi_cols;
+      const uint32_t taddr = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * p.n_pad + c0);
+      uint32_t r[32];
+      TMEM_LD_X16(taddr, r);
+      if (p.epi_cols == 32) TMEM_LD_X16(taddr + 16, (r + 16));
+      tmem_wait_ld();
+      float v[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+      const int ncol = p.epi_cols;
+      if (p.scale) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (i < ncol && c0 + i < p.c_out)
+            v[i] = v[i] * __ldg(p.scale + c0 + i) + __ldg(p.shift + c0 + i);
+      }
+      if (p.bias) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (i < ncol && c0 + i < p.c_out) v[i] += __ldg(p.bias + c0 + i);
+      }
+      if (p.residual && row_ok) {
+        const uint4* rp = reinterpret_cast<const uint4*>(p.residual + k * p.c_out + c0);
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          if (g * 8 < ncol && c0 + g * 8 < p.c_out) {
+            const uint4 w = __ldg(rp + g);
+            const __half2* hh = reinterpret_cast<const __half2*>(&w);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 f = __half22float2(hh[e]);
+              v[g * 8 + 2 * e] += f.x;
+              v[g * 8 + 2 * e + 1] += f.y;
+            }
+          }
+        }
+      }
+      if (p.relu) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
+      }
+      uint8_t* buf = bufs + nbuf * EPI_BUF;
+      if (lane == 0) {
+        if (p.epi_bufs == 2) IC_PROF(6, warp == epi0, bulk_wait_read1());
+        else bulk_wait_read0();
+      }
+      __syncwarp();
+      if (ncol == 32) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint4 w = make_uint4(pack_half2(v[8 * c], v[8 * c + 1]), pack_half2(v[8 * c + 2], v[8 * c + 3]),
+                               pack_half2(v[8 * c + 4], v[8 * c + 5]), pack_half2(v[8 * c + 6], v[8 * c + 7]));
+          *reinterpret_cast<uint4*>(buf + swz_off(lane, c, 64)) = w;
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          uint4 w = make_uint4(pack_half2(v[8 * c], v[8 * c + 1]), pack_half2(v[8 * c + 2], v[8 * c + 3]),
+                               pack_half2(v[8 * c + 4], v[8 * c + 5]), pack_half2(v[8 * c + 6], v[8 * c + 7]));
+          *reinterpret_cast<uint4*>(buf + swz_off(lane, c, 32)) = w;
+        }
+      }
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        tma_store_2d(tmOut_, buf, c0, (int)row0);
+        bulk_commit();
+      }
+      nbuf ^= p.epi_bufs - 1;
+    }
+    tc_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(tempty + acc);
+    if (++acc == p.nacc) { acc = 0; acc_phase ^= 1; }
+  }
+  if (lane == 0) bulk_wait_all();
 }
 
 template <int V, int KC, int P, int MINB>
@@ -169,7 +268,7 @@ __global__ void __launch_bounds__(64 + 128 * P + 128, MINB)
         for (int g = 0; g < p.groups; ++g) {
           const int nv = min(p.ops, p.V - g * p.ops);
           for (int kk = 0; kk < p.n_kchunks; ++kk) {
-            IC_PROF(2, true, mbar_wait_sleep(empty + stage, phase ^ 1, 32));
+            IC_PROF(2, true, mbar_wait_sleep(empty + stage, phase ^ 1, p.bsleep));
             if (p.debug & 32) {
               mbar_arrive(full + stage);
             } else {
@@ -403,95 +502,256 @@ __global__ void __launch_bounds__(64 + 128 * P + 128, MINB)
       if (++acc == p.nacc) { acc = 0; acc_phase ^= 1; }
     }
   } else if (warp >= EPI0) {
-    // ============ epilogue
-    const int q = warp & 3;
-    uint8_t* bufs = epi_base + (warp - EPI0) * p.epi_bufs * EPI_BUF;
-    int acc = 0, nbuf = 0;
-    uint32_t acc_phase = 0;
-    const int chunks = p.n_pad / p.epi_cols;
-    for (int t = t_begin; t < t_end; ++t) {
-      IC_PROF(5, warp == EPI0 && lane == 0, mbar_wait_sleep(tfull + acc, acc_phase, 256));
-      tc_after();
-      const long long row0 = (long long)t * BM + 32 * q;
-      const long long k = row0 + lane;
-      const bool row_ok = k < p.n_out;
-      for (int j = 0; j < chunks && row0 < p.n_out; ++j) {
-        const int c0 = j * p.epi_cols;
-        const uint32_t taddr = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * p.n_pad + c0);
-        uint32_t r[32];
-        TMEM_LD_X16(taddr, r);
-        if (p.epi_cols == 32) TMEM_LD_X16(taddr + 16, (r + 16));
-        tmem_wait_ld();
-        float v[32];
-#pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-        const int ncol = p.epi_cols;
-        if (p.scale) {
-#pragma unroll
-          for (int i = 0; i < 32; ++i)
-            if (i < ncol && c0 + i < p.c_out)
-              v[i] = v[i] * __ldg(p.scale + c0 + i) + __ldg(p.shift + c0 + i);
-        }
-        if (p.bias) {
-#pragma unroll
-          for (int i = 0; i < 32; ++i)
-            if (i < ncol && c0 + i < p.c_out) v[i] += __ldg(p.bias + c0 + i);
-        }
-        if (p.residual && row_ok) {
-          const uint4* rp = reinterpret_cast<const uint4*>(p.residual + k * p.c_out + c0);
-#pragma unroll
-          for (int g = 0; g < 4; ++g) {
-            if (g * 8 < ncol && c0 + g * 8 < p.c_out) {
-              const uint4 w = __ldg(rp + g);
-              const __half2* hh = reinterpret_cast<const __half2*>(&w);
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const float2 f = __half22float2(hh[e]);
-                v[g * 8 + 2 * e] += f.x;
-                v[g * 8 + 2 * e + 1] += f.y;
-              }
+    epilogue_role(p, &tmOut, tmem_base, tfull, tempty, epi_base, warp, EPI0, lane, t_begin, t_end);
+  }
+
+  tc_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(p.tmem_cols));
+  }
+  if ((p.debug & 16) && blockIdx.x == 0 && threadIdx.x == 0) {
+    atomicAdd(&g_ic_prof[7], (unsigned long long)(clock64() - k_t0));
+    atomicAdd(&g_ic_prof[9], (unsigned long long)(t_end - t_begin));
+  }
+}
+
+// ------------------------------------------------------------------ TS form
+// The same convolution with the gathered A operand in TENSOR memory
+// (tcgen05.mma A-from-TMEM): producer threads own one output row each
+// (row = TMEM lane), load its present neighbours' channels straight into
+// registers and tcgen05.st them into a TMEM ring; only the weights (B) pass
+// through shared memory.  The SS form's per-MMA shared-memory reads of A
+// (4 KB per K = 16 step, plus the cp.async writes) were the bound at
+// C_out <= 128; here shared memory carries B alone.
+//
+// TMEM: [0, nacc n_pad) accumulators, then `stages` A blocks of 32 columns
+// (one stage = 64 / KC offsets x one K chunk = 128 rows x 64 fp16).
+// Warps: 0 B TMA, 1 TMEM alloc + MMA issue, 2 .. 2 + 4 PW A producers (PW
+// warps per TMEM lane quarter take stages round-robin), then 4 epilogue warps.
+// absent neighbours of the TS form read this (L1-resident) zero row
+__device__ __align__(128) uint4 g_zero_row[32];
+
+template <int V, int KC, int PW>
+__global__ void __launch_bounds__(64 + 128 * PW + 128, 1)
+    implicit_conv_ts_kernel(const __grid_constant__ CUtensorMap tmB,
+                            const __grid_constant__ CUtensorMap tmOut,
+                            const __grid_constant__ Params p) {
+  constexpr int OPS = 64 / KC;             // offsets per stage
+  constexpr int CPR = KC / 8;              // 16-B chunks per row per K chunk
+  constexpr int EPI0 = 2 + 4 * PW;
+  constexpr int NT = (V + PW - 1) / PW;    // offsets whose index a thread prefetches
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* epi_base = smem + (size_t)p.stages * p.stage_bytes;
+  int* nbr_s = (int*)(epi_base + 4 * p.epi_bufs * EPI_BUF);      // [V][BM]
+  uint64_t* full = (uint64_t*)(nbr_s + V * BM);
+  uint64_t* empty = full + p.stages;
+  uint64_t* tfull = empty + p.stages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+
+  const long long k_t0 = clock64();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t_begin = (int)((long long)p.total_tiles * blockIdx.x / gridDim.x);
+  const int t_end = (int)((long long)p.total_tiles * (blockIdx.x + 1) / gridDim.x);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < p.stages; ++s) {
+      mbar_init(full + s, 4 + 1);   // one arrive per lane-quarter warp + the B expect_tx
+      mbar_init(empty + s, 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull + a, 1);
+      mbar_init(tempty + a, 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmOut) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(p.tmem_cols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_before();
+  __syncthreads();
+  tc_after();
+  const uint32_t tmem_base = *tmem_slot;
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const uint32_t a_col0 = (uint32_t)(p.nacc * p.n_pad);
+
+  if (warp == 0) {
+    // ============ B producer (TMA): the stage's weight slices
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = t_begin; t < t_end; ++t)
+        for (int g = 0; g < p.groups; ++g) {
+          const int nv = min(OPS, V - g * OPS);
+          for (int kk = 0; kk < p.n_kchunks; ++kk) {
+            IC_PROF(2, true, mbar_wait_sleep(empty + stage, phase ^ 1, p.bsleep));
+            if (p.debug & 4) {   // debug: no weight loads
+              mbar_arrive(full + stage);
+            } else {
+              mbar_expect_tx(full + stage, nv * p.b_tx);
+              uint8_t* sb = smem + (size_t)stage * p.stage_bytes;
+              for (int o = 0; o < nv; ++o)
+                tma_load_2d(sb + o * p.b_off_bytes, &tmB, full + stage, kk * KC,
+                            (g * OPS + o) * p.n_pad);
             }
+            if (++stage == p.stages) { stage = 0; phase ^= 1; }
           }
         }
-        if (p.relu) {
+    }
+  } else if (warp >= 2 && warp < EPI0) {
+    // ============ A producers: thread = output row (TMEM lane 32 q + lane).
+    // Warp (q, sub) fills stages i = sub (mod PW) of the CTA's stage
+    // sequence; two stages' rows are in flight per thread (register double
+    // buffer) and each stage's neighbour indices are fetched a stage-pair
+    // earlier.  The producer is issue-bound, so the per-stage bookkeeping is
+    // incremental (no divisions) and each 16-B chunk is one load with an
+    // immediate offset; absent neighbours read a zero row.
+    const int q = warp & 3, sub = (warp - 2) >> 2;
+    const int row = 32 * q + lane;
+    const int nk = p.n_kchunks, ntiles = t_end - t_begin;
+    const uint32_t t_row = tmem_base + ((uint32_t)(32 * q) << 16) + a_col0;
+    // position of the next stage whose indices are fetched (sequence order)
+    int it_t = 0, it_g = 0, it_k = sub;
+    while (it_k >= nk) { it_k -= nk; if (++it_g == p.groups) { it_g = 0; ++it_t; } }
+    // chunks of the K chunk: all from one input unless a concat split is inside
+    const uint64_t zrow = reinterpret_cast<uint64_t>(g_zero_row);
+    auto load_idx = [&](int (&j)[OPS], int& kk_out) {
+      const long long k = (long long)(t_begin + it_t) * BM + row;
+      const bool ok = it_t < ntiles && k < p.n_out;
 #pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
-        }
-        uint8_t* buf = bufs + nbuf * EPI_BUF;
-        if (lane == 0) {
-          if (p.epi_bufs == 2) IC_PROF(6, warp == EPI0, bulk_wait_read1());
-          else bulk_wait_read0();
-        }
-        __syncwarp();
-        if (ncol == 32) {
+      for (int o = 0; o < OPS; ++o) {
+        const int n = it_g * OPS + o;
+        j[o] = (ok && n < V) ? ((V == 1 || (p.debug & 32)) ? (int)k : __ldg(p.hits + (long long)n * p.ldh + k)) : -1;
+      }
+      kk_out = it_k;
+      it_k += PW;
+      while (it_k >= nk) { it_k -= nk; if (++it_g == p.groups) { it_g = 0; ++it_t; } }
+    };
+    auto load_rows = [&](const int (&j)[OPS], int kk, uint4 (&v)[OPS][CPR]) {
+      const int col0 = kk * KC;
+      const int live = (p.debug & 1) ? 0 : min(CPR, (p.c_in - col0) / 8);
+      const bool split = p.feat2 != nullptr && col0 < p.c_split && col0 + KC > p.c_split;
+      if (live == CPR && !split) {   // warp-uniform fast path
+        const bool second = p.feat2 != nullptr && col0 >= p.c_split;
+        const uint64_t base = second
+            ? reinterpret_cast<uint64_t>(p.feat2) + (uint64_t)((col0 - p.c_split) * 2)
+            : reinterpret_cast<uint64_t>(p.feat) + (uint64_t)(col0 * 2);
+        const uint64_t ldb = (uint64_t)(second ? p.ldf2 : p.ldf) * 2u;
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            uint4 w = make_uint4(pack_half2(v[8 * c], v[8 * c + 1]), pack_half2(v[8 * c + 2], v[8 * c + 3]),
-                                 pack_half2(v[8 * c + 4], v[8 * c + 5]), pack_half2(v[8 * c + 6], v[8 * c + 7]));
-            *reinterpret_cast<uint4*>(buf + swz_off(lane, c, 64)) = w;
+        for (int o = 0; o < OPS; ++o) {
+          const uint64_t r = j[o] >= 0 ? base + (uint64_t)(uint32_t)j[o] * ldb : zrow;
+          const uint4* rp = reinterpret_cast<const uint4*>(r);
+#pragma unroll
+          for (int c = 0; c < CPR; ++c) v[o][c] = __ldg(rp + c);
+        }
+      } else {
+#pragma unroll
+        for (int o = 0; o < OPS; ++o)
+#pragma unroll
+          for (int c = 0; c < CPR; ++c) {
+            const int col = col0 + c * 8;
+            const bool sec = p.feat2 != nullptr && col >= p.c_split;
+            const uint64_t r = (j[o] >= 0 && c < live)
+                ? (sec ? reinterpret_cast<uint64_t>(p.feat2) + ((uint64_t)(uint32_t)j[o] * p.ldf2 + (col - p.c_split)) * 2u
+                       : reinterpret_cast<uint64_t>(p.feat) + ((uint64_t)(uint32_t)j[o] * p.ldf + col) * 2u)
+                : zrow;
+            v[o][c] = __ldg(reinterpret_cast<const uint4*>(r));
           }
-        } else {
+      }
+    };
+    int st_stage = sub;
+    uint32_t st_phase = 0;
+    auto store = [&](uint4 (&v)[OPS][CPR]) {
+      IC_PROF(0, row == 0, mbar_wait(empty + st_stage, st_phase ^ 1));   // the MMAs that read this slot are done
+      tc_after();
+      const uint32_t ta = t_row + (uint32_t)(st_stage * 32);
+      if (!(p.debug & 8)) {   // debug 8: no TMEM stores
+        const uint32_t* w = reinterpret_cast<const uint32_t*>(&v[0][0]);
 #pragma unroll
-          for (int c = 0; c < 2; ++c) {
-            uint4 w = make_uint4(pack_half2(v[8 * c], v[8 * c + 1]), pack_half2(v[8 * c + 2], v[8 * c + 3]),
-                                 pack_half2(v[8 * c + 4], v[8 * c + 5]), pack_half2(v[8 * c + 6], v[8 * c + 7]));
-            *reinterpret_cast<uint4*>(buf + swz_off(lane, c, 32)) = w;
-          }
-        }
-        fence_async_smem();
-        __syncwarp();
-        if (lane == 0) {
-          tma_store_2d(&tmOut, buf, c0, (int)row0);
-          bulk_commit();
-        }
-        nbuf ^= p.epi_bufs - 1;
+        for (int h = 0; h < 2; ++h) TMEM_ST_X16(ta + 16 * h, (w + 16 * h));
+        tmem_wait_st();
       }
       tc_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(tempty + acc);
+      if (lane == 0) mbar_arrive(full + st_stage);
+      st_stage += PW;
+      if (st_stage >= p.stages) { st_stage -= p.stages; st_phase ^= 1; }
+    };
+    const int total = ntiles * p.groups * nk;
+    int ja[OPS], jb[OPS], ka, kb;
+    uint4 va[OPS][CPR], vb[OPS][CPR];
+    load_idx(ja, ka);
+    load_idx(jb, kb);
+    load_rows(ja, ka, va);
+    load_rows(jb, kb, vb);
+    load_idx(ja, ka);
+    load_idx(jb, kb);
+    for (int i = sub; i < total; i += 2 * PW) {
+      store(va);
+      load_rows(ja, ka, va);
+      load_idx(ja, ka);
+      if (i + PW < total) {
+        store(vb);
+        load_rows(jb, kb, vb);
+        load_idx(jb, kb);
+      }
+    }
+  } else if (warp == 1) {
+    // ============ MMA issuer (A from TMEM, B from shared memory)
+    const uint32_t layout = p.swz == 128 ? 2u : (p.swz == 64 ? 4u : 6u);
+    const uint32_t sbo = 8u * (uint32_t)p.swz;
+    const uint64_t bdesc_base = make_sdesc(smem_u32(smem), sbo, layout);
+    const uint32_t stage_d = p.stage_bytes >> 4, b_off_d = p.b_off_bytes >> 4;
+    const uint32_t idesc = p.idesc, n_pad = p.n_pad;
+    const uint32_t tmem0 = __shfl_sync(0xffffffffu, tmem_base, 0);
+    int stage = 0, acc = 0;
+    uint32_t phase = 0, acc_phase = 0;
+    for (int t = t_begin; t < t_end; ++t) {
+      IC_PROF(4, lane == 0, mbar_wait(tempty + acc, acc_phase ^ 1));
+      tc_after();
+      const uint32_t d = tmem0 + (uint32_t)acc * n_pad;
+      for (int g = 0; g < p.groups; ++g) {
+        const int nv = min(OPS, V - g * OPS);
+        for (int kk = 0; kk < p.n_kchunks; ++kk) {
+          IC_PROF(3, lane == 0, mbar_wait(full + stage, phase));
+          tc_after();
+          const uint64_t bd = bdesc_base + (uint64_t)(stage * stage_d);
+          const uint32_t ta = tmem0 + a_col0 + (uint32_t)(stage * 32);
+          const uint32_t acc0 = (g | kk) ? 1u : 0u;
+          if (elect_one()) {
+#pragma unroll
+            for (int o = 0; o < OPS; ++o) {
+              if (o < nv) {
+                const uint64_t b = bd + (uint64_t)(o * b_off_d);
+#pragma unroll
+                for (int k = 0; k < KC / 16; ++k)
+                  if (!(p.debug & 2) || (o | k | g | kk) == 0)   // debug 2: first MMA only
+                    mma_f16_ts(d, ta + o * (KC / 2) + 8 * k, b + 2u * k, idesc, (o | k) ? 1u : acc0);
+              }
+            }
+            if (p.debug & 64) mbar_arrive(empty + stage);   // debug (with 2): plain arrive
+            else mma_commit(empty + stage);
+          }
+          __syncwarp();
+          if (++stage == p.stages) { stage = 0; phase ^= 1; }
+        }
+      }
+      if (elect_one()) mma_commit(tfull + acc);
+      __syncwarp();
       if (++acc == p.nacc) { acc = 0; acc_phase ^= 1; }
     }
-    if (lane == 0) bulk_wait_all();
+  } else if (warp >= EPI0) {
+    epilogue_role(p, &tmOut, tmem_base, tfull, tempty, epi_base, warp, EPI0, lane, t_begin, t_end);
   }
 
   tc_before();
@@ -631,6 +891,83 @@ extern "C" int32_t scb_conv_implicit_cat(const void* features, int64_t ldf, int3
   p.bias = bias;
   p.residual = (const __half*)residual;
   if (const char* dbg = getenv("SCB_IMPLICIT_DEBUG")) p.debug = atoi(dbg);
+  p.bsleep = env_int("SCB_IC_BSLEEP", 32);
+  p.esleep = env_int("SCB_IC_ESLEEP", 256);
+  // A-in-TMEM form: K chunks of 32 / 64 channels only.  Measured faster than
+  // the shared-memory form at C_out = 256 (L3/L4 MinkUNet layers: 0.197 vs
+  // 0.209 ms, 0.086 vs 0.097 ms), slower below (its producers are latency-
+  // bound: 0.71 vs 0.70 ms at 96->96, 0.26 vs 0.22 at 32->32).  SCB_IC_TS=0 / 1
+  // forces the choice.
+  const int ts_env = env_int("SCB_IC_TS", -1);
+  const bool ts = (p.kc == 64 || p.kc == 32) && (ts_env < 0 ? n_pad >= 256 : ts_env != 0);
+  if (ts) {
+    p.nacc = (2 * n_pad + 2 * 32 <= 512) ? 2 : 1;
+    p.tmem_cols = 512;
+    p.ops = 64 / p.kc;
+    p.groups = (volume + p.ops - 1) / p.ops;
+    p.a_off_bytes = 0;
+    p.a_stage_bytes = 0;
+    p.stage_bytes = p.ops * p.b_off_bytes;
+    p.epi_bufs = 2;
+    const int fixed = 1024 + 4 * p.epi_bufs * EPI_BUF + volume * BM * 4 + 40 * 8 + 64;
+    int stages = std::min((512 - p.nacc * n_pad) / 32, (227 * 1024 - fixed) / (int)p.stage_bytes);
+    stages = std::min(stages, std::min(16, std::max(2, env_int("SCB_IC_STAGES", 16))));
+    SCB_CHECK_ARG(stages >= 2, "TS: stage does not fit");
+    p.stages = stages;
+    const int smem_ts = fixed + stages * (int)p.stage_bytes;
+    CUtensorMap mB, mO;
+    std::string err;
+    if (!encode_map_2d(&mB, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, weights_packed, k_pad,
+                       (long long)volume * n_pad, k_pad, p.kc, n_pad, p.swz, err) ||
+        !encode_map_2d(&mO, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, out, c_out, n_out, ldo,
+                       p.epi_cols, 32, p.epi_cols * 2, err)) {
+      set_error(std::string("scb_conv_implicit: ") + err);
+      return SCB_ECUDA;
+    }
+    const int grid = std::min(p.total_tiles, device_sms());
+    const int pw = std::min(4, std::max(2, env_int("SCB_IC_PW", 2)));
+    cudaStream_t s = as_stream(stream);
+    auto launch = [&](auto kernel, int threads) -> int {
+      SCB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(grid);
+      cfg.blockDim = dim3(threads);
+      cfg.dynamicSmemBytes = smem_ts;
+      cfg.stream = s;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[0].val.programmaticStreamSerializationAllowed = env_int("SCB_IC_PDL", 1) ? 1 : 0;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      SCB_CUDA(cudaLaunchKernelEx(&cfg, kernel, mB, mO, p));
+      return SCB_OK;
+    };
+    int rc = SCB_EINVAL;
+#define SCB_TS_LAUNCH_PW(VV, KK)                                                               \
+  rc = pw == 2   ? launch(implicit_conv_ts_kernel<VV, KK, 2>, 64 + 256 + 128)                 \
+       : pw == 3 ? launch(implicit_conv_ts_kernel<VV, KK, 3>, 64 + 384 + 128)                 \
+                 : launch(implicit_conv_ts_kernel<VV, KK, 4>, 64 + 512 + 128);
+#define SCB_TS_LAUNCH_K(VV)                                                                    \
+  if (p.kc == 64) { SCB_TS_LAUNCH_PW(VV, 64) } else { SCB_TS_LAUNCH_PW(VV, 32) }
+    if (volume == 27) { SCB_TS_LAUNCH_K(27) }
+    else if (volume == 8) { SCB_TS_LAUNCH_K(8) }
+    else { SCB_TS_LAUNCH_K(1) }
+#undef SCB_TS_LAUNCH_K
+#undef SCB_TS_LAUNCH_PW
+    if (rc != SCB_OK) return rc;
+    if (p.debug & 16) {
+      unsigned long long prof[16];
+      cudaStreamSynchronize(s);
+      cudaMemcpyFromSymbol(prof, g_ic_prof, sizeof(prof));
+      fprintf(stderr, "[ts prof cta0] tiles=%llu total=%llu Aempty(row0)=%llu Bempty=%llu MMAfull=%llu "
+              "MMAtempty=%llu EPItfull=%llu (stages=%d pw=%d nacc=%d)\n", prof[9], prof[7], prof[0],
+              prof[2], prof[3], prof[4], prof[5], p.stages, pw, p.nacc);
+      static const unsigned long long zero[16] = {0};
+      cudaMemcpyToSymbol(g_ic_prof, zero, sizeof(zero));
+    }
+    SCB_LAUNCHED();
+    return SCB_OK;
+  }
   // shared memory: stages (A + B blocks, one presence word per producer
   // thread) + epilogue staging + the tile's neighbour table + barriers
   auto fixed_bytes = [&](int epi_bufs) {

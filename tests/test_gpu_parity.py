@@ -583,3 +583,33 @@ def test_async_validation_raises_at_the_next_sync(sc):
     ok = np.array([[0, 1, 1, 1], [0, 2, 1, 1]], dtype=np.int64)
     sc.SparseTensor(ok, np.zeros((2, 4), np.float32), 1, (4, 4, 4), validate="async")
     sc.flush_validation()
+
+
+@pytest.mark.parametrize("c_in,c_out,split", [(64, 64, None), (96, 96, None), (24, 32, None),
+                                              (256, 256, None), (48, 128, 16), (128, 96, 96)])
+def test_fused_tmem_operand_form(sc, rng, monkeypatch, c_in, c_out, split):
+    """The A-in-tensor-memory form of the implicit kernel (SCB_IC_TS=1: rows
+    loaded to registers, tcgen05.st into TMEM, tcgen05.mma A from TMEM)
+    against the oracle, with a BN + residual + ReLU epilogue and a concat
+    split inside a K chunk."""
+    monkeypatch.setenv("SCB_IC_TS", "1")
+    coords = random_coords(rng, (20, 20, 20), 0.15)
+    n = coords.shape[0]
+    f = O.quantize(rng.standard_normal((n, c_in)).astype(np.float32), "fp16")
+    r = O.quantize(rng.standard_normal((n, c_out)).astype(np.float32), "fp16")
+    w = rng.normal(0, 1 / np.sqrt(27 * c_in), (27, c_in, c_out)).astype(np.float32)
+    s = rng.uniform(0.8, 1.2, c_out).astype(np.float32)
+    h = rng.normal(0, 0.05, c_out).astype(np.float32)
+    _, base, _ = O.conv_forward(coords, f, (20, 20, 20), w, 3, 1)
+    want = np.maximum(base.astype(np.float32) * s + h + r.astype(np.float32), 0)
+    if split is None:
+        t, skip = sc.SparseTensor(coords, f, 1, (20, 20, 20)), None
+    else:
+        t = sc.SparseTensor(coords, np.ascontiguousarray(f[:, :split]), 1, (20, 20, 20))
+        skip = sc.SparseTensor(coords, np.ascontiguousarray(f[:, split:]), 1, (20, 20, 20))
+    ep = {"scale": torch.from_numpy(s).cuda(), "shift": torch.from_numpy(h).cuda(),
+          "residual": sc.SparseTensor(coords, r, 1, (20, 20, 20)), "relu": True}
+    out = sc.sparse_conv_forward(t, sc.WeightTensor(w, 3, 3), sc.LayerSpec(3, 1, c_in, c_out),
+                                 None, None, sc.ExecOptions(dataflow="fused"), epilogue=ep,
+                                 concat=skip)
+    assert rel_l2(out.features_numpy().astype(np.float32), want) <= 1e-2

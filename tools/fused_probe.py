@@ -14,6 +14,11 @@ from bench import load_scans, pack  # noqa: E402
 
 def main():
     c, f, b = pack(load_scans(range(int(os.environ.get("NSCANS", "8")))))
+    lv = int(os.environ.get("LEVEL", "0"))
+    if lv:  # emulate pyramid level lv: coordinates // 2^lv, unique
+        cc = c.astype(np.int64).copy()
+        cc[:, 1:] >>= lv
+        c = np.unique(cc, axis=0).astype(c.dtype)
     cin = int(os.environ.get("CIN", "32"))
     cout = int(os.environ.get("COUT", "32"))
     k = int(os.environ.get("K", "3"))
