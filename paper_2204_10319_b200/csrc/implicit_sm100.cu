@@ -902,6 +902,7 @@ extern "C" int32_t scb_conv_implicit_cat(const void* features, int64_t ldf, int3
   const bool ts = (p.kc == 64 || p.kc == 32) && (ts_env < 0 ? n_pad >= 256 : ts_env != 0);
   if (ts) {
     p.nacc = (2 * n_pad + 2 * 32 <= 512) ? 2 : 1;
+    if (env_int("SCB_IC_NACC", 2) == 1) p.nacc = 1;
     p.tmem_cols = 512;
     p.ops = 64 / p.kc;
     p.groups = (volume + p.ops - 1) / p.ops;
