@@ -284,6 +284,18 @@ int32_t scb_conv_implicit_cat(const void* features, int64_t ldf, int32_t c_split
                               const float* scale, const float* shift, const float* bias,
                               const void* residual, int32_t relu, scb_stream_t stream);
 
+/* Same layer with the weights in the virtual-K layout: weights_vk is fp16
+ * [n_pad][ceil64(volume * c_in)] K-major, element (col, n * c_in + ci) =
+ * W[n][ci][col] (zero padded), so the K loop runs over 64-wide chunks of the
+ * offset-major channel concatenation (128-B-swizzled operand rows for any
+ * C_in that is a multiple of 8).  volume must be 8 or 27. */
+int32_t scb_conv_implicit_vk(const void* features, int64_t ldf, int32_t c_split,
+                             const void* features2, int64_t ldf2, int64_t n_in, int32_t c_in,
+                             const int32_t* hits, int32_t volume, int64_t n_out,
+                             const void* weights_vk, int32_t c_out, void* out, int64_t ldo,
+                             const float* scale, const float* shift, const float* bias,
+                             const void* residual, int32_t relu, scb_stream_t stream);
+
 /* ---------------------------------------------------------------- voxelisation
  * Replaces voxelize (core.py:174-216), the step in front of the path
  * (SURVEY.md §8(f) row 2): `points` f64 [n][cols] (first spatial_dims

@@ -86,6 +86,8 @@ _SIGS = {
                                  _P, _I32, _P]),
     "scb_conv_implicit_cat": (_I32, [_P, _I64, _I32, _P, _I64, _I64, _I32, _P, _I32, _I64, _P,
                                      _I32, _P, _I64, _P, _P, _P, _P, _I32, _P]),
+    "scb_conv_implicit_vk": (_I32, [_P, _I64, _I32, _P, _I64, _I64, _I32, _P, _I32, _I64, _P,
+                                    _I32, _P, _I64, _P, _P, _P, _P, _I32, _P]),
 }
 
 _lib = None

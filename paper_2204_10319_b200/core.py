@@ -321,7 +321,7 @@ class WeightTensor:
     ``(V, C_in, C_out)`` for the FP32 path and the K-major padded fp16 pack of
     the tcgen05 path."""
 
-    __slots__ = ("weights", "kernel_size", "dim", "_dev32", "_packed")
+    __slots__ = ("weights", "kernel_size", "dim", "_dev32", "_packed", "_packed_vk")
 
     def __init__(self, weights, kernel_size: int, dim: int):
         if isinstance(weights, torch.Tensor):
@@ -337,6 +337,7 @@ class WeightTensor:
         self.dim = int(dim)
         self._dev32 = None
         self._packed = None
+        self._packed_vk = {}
 
     @property
     def c_in(self) -> int:
@@ -361,6 +362,23 @@ class WeightTensor:
                      k_pad, n_pad, nat.stream_handle())
             self._packed = (out, k_pad, n_pad)
         return self._packed
+
+    def packed_vk_f16(self, c_kernel: int) -> torch.Tensor:
+        """[n_pad][ceil64(V c_kernel)] fp16, K-major over the offset-major
+        channel concatenation (virtual K; scb_conv_implicit_vk): element
+        (col, n c_kernel + ci) = W[n][ci][col], zero for ci >= C_in (padded
+        input channels) and past V c_kernel.  A one-time layout transform."""
+        cache = self._packed_vk
+        if c_kernel not in cache:
+            v, ci, co = self.weights.shape
+            n_pad = (co + 15) // 16 * 16
+            kv = (v * c_kernel + 63) // 64 * 64
+            w = torch.zeros((v, c_kernel, n_pad), dtype=torch.float32, device=_device())
+            w[:, :ci, :co] = self.device_f32()
+            flat = torch.zeros((kv, n_pad), dtype=torch.float32, device=_device())
+            flat[: v * c_kernel] = w.reshape(v * c_kernel, n_pad)
+            cache[c_kernel] = flat.t().contiguous().to(torch.float16)
+        return cache[c_kernel]
 
 
 def voxelize(points, voxel_size: float, reduce: str = "mean",

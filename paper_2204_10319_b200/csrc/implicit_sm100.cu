@@ -58,6 +58,8 @@ struct Params {
   int debug;                // SCB_IMPLICIT_DEBUG: 1 no A loads, 16 wait counters, 32 no B loads
   int groups;               // ceil(V / ops) offset groups per tile
   int bsleep, esleep;       // poll back-off (ns) of the weight producer / the epilogue
+  int vk;                   // virtual-K: K = the V x C_in concatenation in 64-wide chunks
+  int nblk;                 // A/B blocks per tile: V (per-offset K chunks) or ceil(V C_in / 64)
   uint32_t idesc, tmem_cols;
   uint32_t a_off_bytes;     // one offset's A block [128 rows][kc] (1024-aligned)
   uint32_t b_off_bytes;     // one offset's B block [n_pad][kc]   (1024-aligned)
@@ -266,7 +268,7 @@ __global__ void __launch_bounds__(64 + 128 * P + 128, MINB)
       uint32_t phase = 0;
       for (int t = t_begin; t < t_end; ++t)
         for (int g = 0; g < p.groups; ++g) {
-          const int nv = min(p.ops, p.V - g * p.ops);
+          const int nv = min(p.ops, p.nblk - g * p.ops);
           for (int kk = 0; kk < p.n_kchunks; ++kk) {
             IC_PROF(2, true, mbar_wait_sleep(empty + stage, phase ^ 1, p.bsleep));
             if (p.debug & 32) {
@@ -274,9 +276,13 @@ __global__ void __launch_bounds__(64 + 128 * P + 128, MINB)
             } else {
               mbar_expect_tx(full + stage, nv * p.b_tx);
               uint8_t* sb = smem + (size_t)stage * p.stage_bytes + p.a_stage_bytes;
-              for (int o = 0; o < nv; ++o)
-                tma_load_2d(sb + o * p.b_off_bytes, &tmB, full + stage, kk * p.kc,
-                            (g * p.ops + o) * p.n_pad);
+              for (int o = 0; o < nv; ++o) {
+                if (p.vk)   // [n_pad][V C_in] K-major: block = 64 consecutive virtual channels
+                  tma_load_2d(sb + o * p.b_off_bytes, &tmB, full + stage, (g * p.ops + o) * 64, 0);
+                else
+                  tma_load_2d(sb + o * p.b_off_bytes, &tmB, full + stage, kk * p.kc,
+                              (g * p.ops + o) * p.n_pad);
+              }
             }
             if (++stage == p.stages) { stage = 0; phase ^= 1; }
           }
@@ -343,13 +349,13 @@ __global__ void __launch_bounds__(64 + 128 * P + 128, MINB)
         }
       }
       for (int g = 0; g < p.groups; ++g) {
-        const int nv = min(p.ops, V - g * p.ops);
+        const int nv = min(p.ops, p.nblk - g * p.ops);
         for (int kk = 0; kk < p.n_kchunks; ++kk) {
           IC_PROF(0, pt == 0, mbar_wait(empty + stage, phase ^ 1));
           const long long a_t0 = clock64();
           const uint32_t dst = smem_u32(smem + (size_t)stage * p.stage_bytes);
           const int col0 = kk * KC;
-          const int live = min(CPR, (p.c_in - col0) / 8);  // chunks inside C_in
+          const int live = p.vk ? CPR : min(CPR, (p.c_in - col0) / 8);  // chunks inside C_in
           // Every 16-B item of the stage is written each time: a copy of a
           // present neighbour's chunk or a zero-fill (absent neighbour, or a
           // chunk past C_in).  (Tracking which slots already hold zeros halves
@@ -409,15 +415,34 @@ __global__ void __launch_bounds__(64 + 128 * P + 128, MINB)
             // producer is issue-bound, and this is ~3x fewer instructions
             for (int o = 0; o < nv; ++o) {
               int jj[IT];
+              uint64_t fb = fbase;
+              uint32_t ldb = ldfb;
+              if (p.vk) {
+                // virtual K: this lane's 8 channels are channel ch of offset n
+                const int vc = (g * p.ops + o) * 64 + cc * 8;
+                const int n = vc / p.c_in, ch = vc - n * p.c_in;
+                const bool sec = p.feat2 != nullptr && ch >= p.c_split;
+                fb = sec ? reinterpret_cast<uint64_t>(p.feat2) + (uint64_t)((ch - p.c_split) * 2)
+                         : reinterpret_cast<uint64_t>(p.feat) + (uint64_t)(ch * 2);
+                ldb = sec ? ldfb2 : ldfb1;
+                const uint32_t nbn = nb_s0 + (uint32_t)((n * BM + cr) * 4);
 #pragma unroll
-              for (int it = 0; it < IT; ++it)
-                asm volatile("ld.shared.b32 %0, [%1];" : "=r"(jj[it]) : "r"(nbc + (uint32_t)((o * BM + it * (NPROD / CPR)) * 4)));
+                for (int it = 0; it < IT; ++it) {
+                  jj[it] = -1;
+                  if (n < V)
+                    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(jj[it]) : "r"(nbn + (uint32_t)(it * (NPROD / CPR) * 4)));
+                }
+              } else {
+#pragma unroll
+                for (int it = 0; it < IT; ++it)
+                  asm volatile("ld.shared.b32 %0, [%1];" : "=r"(jj[it]) : "r"(nbc + (uint32_t)((o * BM + it * (NPROD / CPR)) * 4)));
+              }
               const uint32_t blk = dst + o * p.a_off_bytes;
               if (all_live) {  // the common case: no per-item liveness select
 #pragma unroll
                 for (int it = 0; it < IT; ++it) {
                   const int j = jj[it];
-                  const uint64_t src = fbase + (uint64_t)(uint32_t)max(j, 0) * (uint64_t)ldfb;
+                  const uint64_t src = fb + (uint64_t)(uint32_t)max(j, 0) * (uint64_t)ldb;
                   // ignore-src predicate (absent neighbour): zero-fill, no read
                   asm volatile(
                       "{ .reg .pred q; setp.lt.s32 q, %2, 0;\n"
@@ -428,7 +453,7 @@ __global__ void __launch_bounds__(64 + 128 * P + 128, MINB)
 #pragma unroll
                 for (int it = 0; it < IT; ++it) {
                   const int j = live_c ? jj[it] : -1;
-                  const uint64_t src = fbase + (uint64_t)(uint32_t)max(j, 0) * (uint64_t)ldfb;
+                  const uint64_t src = fb + (uint64_t)(uint32_t)max(j, 0) * (uint64_t)ldb;
                   asm volatile(
                       "{ .reg .pred q; setp.lt.s32 q, %2, 0;\n"
                       "  cp.async.cg.shared.global [%0], [%1], 16, q; }" ::"r"(blk + roff[it]),
@@ -469,7 +494,7 @@ __global__ void __launch_bounds__(64 + 128 * P + 128, MINB)
       tc_after();
       const uint32_t d = tmem0 + (uint32_t)acc * n_pad;
       for (int g = 0; g < p.groups; ++g) {
-        const int nv = min(p.ops, V - g * p.ops);
+        const int nv = min(p.ops, p.nblk - g * p.ops);
         for (int kk = 0; kk < p.n_kchunks; ++kk) {
           IC_PROF(3, lane == 0, mbar_wait(full + stage, phase));
           const long long m_t0 = clock64();
@@ -799,14 +824,15 @@ extern "C" int32_t scb_conv_implicit(const void* features, int64_t n_in, int32_t
                                relu, stream);
 }
 
-extern "C" int32_t scb_conv_implicit_cat(const void* features, int64_t ldf, int32_t c_split,
+static int32_t conv_implicit_impl(const void* features, int64_t ldf, int32_t c_split,
                                          const void* features2, int64_t ldf2, int64_t n_in,
                                          int32_t c_in, const int32_t* hits, int32_t volume,
                                          int64_t n_out, const void* weights_packed,
                                          int32_t c_out, void* out, int64_t ldo,
                                          const float* scale, const float* shift,
                                          const float* bias, const void* residual, int32_t relu,
-                                         scb_stream_t stream) {
+                                         scb_stream_t stream,
+                                  int vk) {
   using namespace ic;
   SCB_CHECK_ARG(features2 == nullptr || (c_split % 8 == 0 && c_split > 0 && c_split < c_in &&
                                          ldf2 % 8 == 0 && ldf2 * 2 < (1LL << 32)),
@@ -838,6 +864,19 @@ extern "C" int32_t scb_conv_implicit_cat(const void* features, int64_t ldf, int3
   p.kc = (k_pad % 64 == 0) ? 64 : ((k_pad % 32 == 0) ? 32 : 16);
   p.swz = p.kc * 2;
   p.n_kchunks = k_pad / p.kc;
+  // virtual K (weights packed [n_pad][ceil64(V C_in)]): 64-wide chunks of the
+  // offset-major channel concatenation, so every K = 16 MMA step reads a
+  // 128-B-swizzled A block (measured ~84 cycles per M128 K16 step against
+  // ~146 with 64-B rows, whatever N <= 128: tools/mma_probe.cu)
+  const int kv = (int)(((long long)volume * c_in + 63) / 64 * 64);
+  if (vk) {
+    SCB_CHECK_ARG(volume > 1, "virtual K needs K > 1");
+    p.kc = 64;
+    p.swz = 128;
+    p.n_kchunks = 1;
+  }
+  p.vk = vk ? 1 : 0;
+  p.nblk = vk ? kv / 64 : volume;
   p.epi_cols = (n_pad % 32 == 0) ? 32 : 16;
   p.relu = relu;
   p.idesc = (1u << 4) | ((uint32_t)(n_pad >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
@@ -852,7 +891,7 @@ extern "C" int32_t scb_conv_implicit_cat(const void* features, int64_t ldf, int3
   // SCB_IC_NACC=1 trades that for two CTAs per SM at C_out > 128: measured
   // 3-5 % slower on the 256-channel layers.
   p.nacc = 2;
-  p.rowmode = env_int("SCB_IC_ROW", 0) ? 1 : 0;
+  p.rowmode = (env_int("SCB_IC_ROW", 0) && !vk) ? 1 : 0;
   if (const char* e = getenv("SCB_IC_NACC")) p.nacc = atoi(e) == 1 ? 1 : 2;
   uint32_t cols = 32;
   while (cols < (uint32_t)(p.nacc * n_pad)) cols *= 2;
@@ -875,8 +914,8 @@ extern "C" int32_t scb_conv_implicit_cat(const void* features, int64_t ldf, int3
   const uint32_t op_bytes = p.a_off_bytes + p.b_off_bytes;
   int ops = (int)((uint32_t)env_int("SCB_IC_STAGE_KB", ctas == 3 ? 24 : (ctas == 2 ? 42 : 96)) *
                   1024u / op_bytes);
-  ops = std::max(1, std::min(ops, std::min(MAX_OPS, volume)));
-  if (env_int("SCB_IMPLICIT_OPS", 0) > 0) ops = std::min(env_int("SCB_IMPLICIT_OPS", 0), std::min(MAX_OPS, volume));
+  ops = std::max(1, std::min(ops, std::min(MAX_OPS, p.nblk)));
+  if (env_int("SCB_IMPLICIT_OPS", 0) > 0) ops = std::min(env_int("SCB_IMPLICIT_OPS", 0), std::min(MAX_OPS, p.nblk));
   p.ops = ops;
   p.stage_bytes = ops * op_bytes;
   p.ldf = ldf;
@@ -899,7 +938,7 @@ extern "C" int32_t scb_conv_implicit_cat(const void* features, int64_t ldf, int3
   // bound: 0.71 vs 0.70 ms at 96->96, 0.26 vs 0.22 at 32->32).  SCB_IC_TS=0 / 1
   // forces the choice.
   const int ts_env = env_int("SCB_IC_TS", -1);
-  const bool ts = (p.kc == 64 || p.kc == 32) && (ts_env < 0 ? n_pad >= 256 : ts_env != 0);
+  const bool ts = !vk && (p.kc == 64 || p.kc == 32) && (ts_env < 0 ? n_pad >= 256 : ts_env != 0);
   if (ts) {
     p.nacc = (2 * n_pad + 2 * 32 <= 512) ? 2 : 1;
     if (env_int("SCB_IC_NACC", 2) == 1) p.nacc = 1;
@@ -991,7 +1030,7 @@ extern "C" int32_t scb_conv_implicit_cat(const void* features, int64_t ldf, int3
   // double-buffered epilogue staging unless the second buffer costs a stage
   p.epi_bufs = fit(2) >= fit(1) ? 2 : 1;
   if (const char* e = getenv("SCB_IC_EPI_BUFS")) p.epi_bufs = atoi(e) == 1 ? 1 : 2;
-  p.groups = (volume + p.ops - 1) / p.ops;
+  p.groups = (p.nblk + p.ops - 1) / p.ops;
   p.a_stage_bytes = p.ops * p.a_off_bytes;
   int stages = std::min(fit(p.epi_bufs), 16);
   stages = std::min(stages, std::max(2, env_int("SCB_IC_STAGES", 16)));
@@ -1001,8 +1040,10 @@ extern "C" int32_t scb_conv_implicit_cat(const void* features, int64_t ldf, int3
 
   CUtensorMap mB, mO;
   std::string err;
-  if (!encode_map_2d(&mB, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, weights_packed, k_pad,
-                     (long long)volume * n_pad, k_pad, p.kc, n_pad, p.swz, err) ||
+  if (!(vk ? encode_map_2d(&mB, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, weights_packed, kv, n_pad,
+                           kv, 64, n_pad, 128, err)
+           : encode_map_2d(&mB, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, weights_packed, k_pad,
+                           (long long)volume * n_pad, k_pad, p.kc, n_pad, p.swz, err)) ||
       !encode_map_2d(&mO, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, out, c_out, n_out, ldo,
                      p.epi_cols, 32, p.epi_cols * 2, err)) {
     set_error(std::string("scb_conv_implicit: ") + err);
@@ -1059,4 +1100,30 @@ extern "C" int32_t scb_conv_implicit_cat(const void* features, int64_t ldf, int3
   }
   SCB_LAUNCHED();
   return SCB_OK;
+}
+
+extern "C" int32_t scb_conv_implicit_cat(const void* features, int64_t ldf, int32_t c_split,
+                                         const void* features2, int64_t ldf2, int64_t n_in,
+                                         int32_t c_in, const int32_t* hits, int32_t volume,
+                                         int64_t n_out, const void* weights_packed,
+                                         int32_t c_out, void* out, int64_t ldo,
+                                         const float* scale, const float* shift,
+                                         const float* bias, const void* residual, int32_t relu,
+                                         scb_stream_t stream) {
+  return conv_implicit_impl(features, ldf, c_split, features2, ldf2, n_in, c_in, hits, volume,
+                            n_out, weights_packed, c_out, out, ldo, scale, shift, bias, residual,
+                            relu, stream, 0);
+}
+
+extern "C" int32_t scb_conv_implicit_vk(const void* features, int64_t ldf, int32_t c_split,
+                                        const void* features2, int64_t ldf2, int64_t n_in,
+                                        int32_t c_in, const int32_t* hits, int32_t volume,
+                                        int64_t n_out, const void* weights_vk, int32_t c_out,
+                                        void* out, int64_t ldo, const float* scale,
+                                        const float* shift, const float* bias,
+                                        const void* residual, int32_t relu,
+                                        scb_stream_t stream) {
+  return conv_implicit_impl(features, ldf, c_split, features2, ldf2, n_in, c_in, hits, volume,
+                            n_out, weights_vk, c_out, out, ldo, scale, shift, bias, residual,
+                            relu, stream, 1);
 }

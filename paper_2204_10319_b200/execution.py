@@ -20,6 +20,8 @@ storage runs an exact-f32 FMA GEMM (tolerance 1e-4).  The grouping strategy
 
 from __future__ import annotations
 
+import os
+
 import warnings
 from contextlib import contextmanager, nullcontext
 from dataclasses import dataclass
@@ -555,10 +557,14 @@ def _run_fused(features: torch.Tensor, kmap: KernelMap | None, w: WeightTensor,
             f = features if concat is None else torch.cat([features, concat], dim=1)
             f, ca, f2, cb = _pad_channels(f), None, None, 0
             ca = f.shape[1]
-        nat.call("scb_conv_implicit_cat", nat.ptr(f), f.shape[1], ca, nat.ptr(f2),
-                 0 if f2 is None else f2.shape[1], f.shape[0], ca + cb, hits, volume, n_out,
-                 nat.ptr(packed), w.c_out, nat.ptr(out), ldo, scale, shift, bias, res, relu,
-                 nat.stream_handle())
+        # virtual K (opt-in, SCB_IC_VK=1) for C_in not a multiple of 64: 128-B
+        # operand rows; measured slower on the MinkUNet layers
+        vk = volume > 1 and (ca + cb) % 64 != 0 and os.environ.get("SCB_IC_VK", "0") == "1"
+        wp = w.packed_vk_f16(ca + cb) if vk else packed
+        nat.call("scb_conv_implicit_vk" if vk else "scb_conv_implicit_cat", nat.ptr(f),
+                 f.shape[1], ca, nat.ptr(f2), 0 if f2 is None else f2.shape[1], f.shape[0],
+                 ca + cb, hits, volume, n_out, nat.ptr(wp), w.c_out, nat.ptr(out), ldo, scale,
+                 shift, bias, res, relu, nat.stream_handle())
     if ldo != w.c_out:
         out = out[:, : w.c_out]  # 8-aligned rows for the TMA store; a strided view
     if opts.traffic_log is not None:

@@ -613,3 +613,30 @@ def test_fused_tmem_operand_form(sc, rng, monkeypatch, c_in, c_out, split):
                                  None, None, sc.ExecOptions(dataflow="fused"), epilogue=ep,
                                  concat=skip)
     assert rel_l2(out.features_numpy().astype(np.float32), want) <= 1e-2
+
+
+@pytest.mark.parametrize("c_in,c_out,split", [(32, 32, None), (96, 96, None), (24, 40, None),
+                                              (48, 64, 16), (8, 16, None)])
+def test_fused_virtual_k_form(sc, rng, monkeypatch, c_in, c_out, split):
+    """The virtual-K form of the implicit kernel (SCB_IC_VK=1: weights packed
+    [n_pad][V C_in], K chunks of 64 channels of the offset-major concatenation,
+    chunks straddling offsets) against the oracle, with BN + ReLU and a concat."""
+    monkeypatch.setenv("SCB_IC_VK", "1")
+    coords = random_coords(rng, (20, 20, 20), 0.15)
+    n = coords.shape[0]
+    f = O.quantize(rng.standard_normal((n, c_in)).astype(np.float32), "fp16")
+    w = rng.normal(0, 1 / np.sqrt(27 * c_in), (27, c_in, c_out)).astype(np.float32)
+    s = rng.uniform(0.8, 1.2, c_out).astype(np.float32)
+    h = rng.normal(0, 0.05, c_out).astype(np.float32)
+    _, base, _ = O.conv_forward(coords, f, (20, 20, 20), w, 3, 1)
+    want = np.maximum(base.astype(np.float32) * s + h, 0)
+    if split is None:
+        t, skip = sc.SparseTensor(coords, f, 1, (20, 20, 20)), None
+    else:
+        t = sc.SparseTensor(coords, np.ascontiguousarray(f[:, :split]), 1, (20, 20, 20))
+        skip = sc.SparseTensor(coords, np.ascontiguousarray(f[:, split:]), 1, (20, 20, 20))
+    ep = {"scale": torch.from_numpy(s).cuda(), "shift": torch.from_numpy(h).cuda(), "relu": True}
+    out = sc.sparse_conv_forward(t, sc.WeightTensor(w, 3, 3), sc.LayerSpec(3, 1, c_in, c_out),
+                                 None, None, sc.ExecOptions(dataflow="fused"), epilogue=ep,
+                                 concat=skip)
+    assert rel_l2(out.features_numpy().astype(np.float32), want) <= 1e-2
