@@ -11,14 +11,17 @@
 
 using namespace scb::ptx;
 
-__global__ void probe(int n, int kc, int nacc, int rounds, int chain, long long* out) {
+__global__ void probe(int n, int kc, int nacc, int rounds, int chain, int mode, long long* out) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  __shared__ uint64_t bar;
+  __shared__ uint64_t bar, done, spare;
   __shared__ uint32_t slot;
   const int warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
+    mbar_init(&done, 1);
+    mbar_init(&spare, 1);
+    mbar_arrive(&done);   // phase 0 completes
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -41,18 +44,37 @@ __global__ void probe(int n, int kc, int nacc, int rounds, int chain, long long*
     __syncwarp();
     const long long t0 = clock64();
     uint32_t acc = 0, sel = 0, first = (uint32_t)nacc;
-    for (int r = 0; r < rounds; ++r) {
-      const uint64_t a = ad + (uint64_t)(sel * a_step);
-      const uint64_t b = bd + (uint64_t)(sel * b_step);
+    if (mode == 1 || mode >= 3) {   // one elected lane runs the whole loop (3: + poll, commit; 4: commit; 5: poll)
       if (elect_one()) {
-        for (int k = 0; k < kc / 16; ++k) {
-          mma_f16(tmem + acc * (uint32_t)n, a + 2u * k, b + 2u * k, idesc, first ? 0u : 1u);
+        for (int r = 0; r < rounds; ++r) {
+          const uint64_t a = ad + (uint64_t)(sel * a_step);
+          const uint64_t b = bd + (uint64_t)(sel * b_step);
+          if (mode == 3 || mode == 5) mbar_wait(&done, 0);
+          for (int k = 0; k < kc / 16; ++k)
+            mma_f16(tmem + acc * (uint32_t)n, a + 2u * k, b + 2u * k, idesc, first ? 0u : 1u);
+          if (mode == 3 || mode == 4) mma_commit(&spare);
+          if (first) --first;
+          if (++acc == (uint32_t)nacc) acc = 0;
+          if (++sel == (uint32_t)chain) sel = 0;
         }
       }
       __syncwarp();
-      if (first) --first;
-      if (++acc == (uint32_t)nacc) acc = 0;
-      if (++sel == (uint32_t)chain) sel = 0;
+    } else {
+      for (int r = 0; r < rounds; ++r) {
+        const uint64_t a = ad + (uint64_t)(sel * a_step);
+        const uint64_t b = bd + (uint64_t)(sel * b_step);
+        if (mode == 2) mbar_wait(&done, 0);   // a completed barrier, like the stage-full poll
+        if (elect_one()) {
+          for (int k = 0; k < kc / 16; ++k) {
+            mma_f16(tmem + acc * (uint32_t)n, a + 2u * k, b + 2u * k, idesc, first ? 0u : 1u);
+          }
+          if (mode == 2) mma_commit(&spare);
+        }
+        __syncwarp();
+        if (first) --first;
+        if (++acc == (uint32_t)nacc) acc = 0;
+        if (++sel == (uint32_t)chain) sel = 0;
+      }
     }
     if (elect_one()) mma_commit(&bar);
     __syncwarp();
@@ -72,20 +94,20 @@ int main() {
   cudaMalloc(&d, 148 * sizeof(long long));
   cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   const int rounds = 2000;
-  for (int kc : {64, 32})
-    for (int n : {32, 64, 96, 128, 256})
-      for (int nacc : {1, 2, 4})
-        for (int chain : {1, 2}) {
-          if (n * nacc > 512) continue;
-          probe<<<148, 128, 200 * 1024>>>(n, kc, nacc, rounds, chain, d);
-          cudaError_t e = cudaDeviceSynchronize();
-          long long h[148];
-          cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
-          double s = 0;
-          for (int i = 0; i < 148; ++i) s += h[i];
-          const double per = s / 148 / (rounds * (kc / 16));
-          printf("kc=%d N=%3d nacc=%d chain=%d: %7.1f cycles/MMA (nominal %5.1f) %s\n", kc, n, nacc,
-                 chain, per, 128.0 * n / 256, e == cudaSuccess ? "" : cudaGetErrorString(e));
-        }
+  for (int mode : {1, 4, 5})
+    for (int kc : {64, 32})
+      for (int n : {96}) {
+        const int nacc = 1, chain = 2;
+        probe<<<148, 128, 200 * 1024>>>(n, kc, nacc, rounds, chain, mode, d);
+        cudaError_t e = cudaDeviceSynchronize();
+        long long h[148];
+        cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+        double s = 0;
+        for (int i = 0; i < 148; ++i) s += h[i];
+        const double per = s / 148 / (rounds * (kc / 16));
+        printf("mode=%d kc=%d N=%3d: %7.1f cycles/MMA, %7.1f per iteration (nominal %5.1f/MMA) %s\n",
+               mode, kc, n, per, per * (kc / 16), 128.0 * n / 256,
+               e == cudaSuccess ? "" : cudaGetErrorString(e));
+      }
   return 0;
 }
