@@ -61,3 +61,29 @@ def test_packed_batch_equals_separate(scan):
     pfn = packed.features_numpy()
     np.testing.assert_array_equal(pfn[pcn[:, 0] == 0], outs[0])
     np.testing.assert_array_equal(pfn[pcn[:, 0] == 1], outs[1])
+
+
+def test_prefetched_pyramid_is_identical(scan):
+    """model.prefetch(t_next) before forward(t) (the serving loop's pipelining
+    of the coordinate pyramid) changes nothing: both outputs are bit-identical
+    to plain forwards."""
+    import paper_2204_10319_b200 as sc
+    from paper_2204_10319_b200 import workloads
+    from paper_2204_10319_b200.minkunet import EngineMinkUNet
+    model = EngineMinkUNet(0.5, 4, 0)
+    opts = sc.ExecOptions(dataflow="auto", index_kind="hash")
+    c2, f2, b2 = _crop(workloads.semantickitti_scan(1), 0.25)
+
+    def tensor(c, f, b):
+        return sc.quantize_features(sc.SparseTensor(c, f, 1, b, 1), sc.PrecisionMode.FP16_STORAGE)
+
+    ref1 = model.forward(tensor(*scan), opts).features_numpy()
+    ref2 = model.forward(tensor(c2, f2, b2), opts)
+    t1, t2 = tensor(*scan), tensor(c2, f2, b2)
+    model.prefetch(t1, opts)
+    model.prefetch(t2, opts)
+    o1 = model.forward(t1, opts)
+    o2 = model.forward(t2, opts)
+    np.testing.assert_array_equal(o1.features_numpy(), ref1)
+    np.testing.assert_array_equal(o2.coords_numpy(), ref2.coords_numpy())
+    np.testing.assert_array_equal(o2.features_numpy(), ref2.features_numpy())
