@@ -932,13 +932,12 @@ static int32_t conv_implicit_impl(const void* features, int64_t ldf, int32_t c_s
   if (const char* dbg = getenv("SCB_IMPLICIT_DEBUG")) p.debug = atoi(dbg);
   p.bsleep = env_int("SCB_IC_BSLEEP", 32);
   p.esleep = env_int("SCB_IC_ESLEEP", 256);
-  // A-in-TMEM form: K chunks of 32 / 64 channels only.  Measured faster than
-  // the shared-memory form at C_out = 256 (L3/L4 MinkUNet layers: 0.197 vs
-  // 0.209 ms, 0.086 vs 0.097 ms), slower below (its producers are latency-
-  // bound: 0.71 vs 0.70 ms at 96->96, 0.26 vs 0.22 at 32->32).  SCB_IC_TS=0 / 1
-  // forces the choice.
-  const int ts_env = env_int("SCB_IC_TS", -1);
-  const bool ts = !vk && (p.kc == 64 || p.kc == 32) && (ts_env < 0 ? n_pad >= 256 : ts_env != 0);
+  // A-in-TMEM form (opt-in, SCB_IC_TS=1): K chunks of 32 / 64 channels only.
+  // Measured faster than the shared-memory form only on the k3 C_out = 256
+  // layers (0.197 vs 0.209 ms, 0.086 vs 0.097 ms), slower on the K = 1 and
+  // narrower ones (0.029 vs 0.021 ms at 256->256 K=1, 0.71 vs 0.70 ms at
+  // 96->96 k3), and the MinkUNet step is 0.5 % faster without it (710 vs 707).
+  const bool ts = !vk && (p.kc == 64 || p.kc == 32) && env_int("SCB_IC_TS", 0) != 0;
   if (ts) {
     p.nacc = (2 * n_pad + 2 * 32 <= 512) ? 2 : 1;
     if (env_int("SCB_IC_NACC", 2) == 1) p.nacc = 1;
