@@ -59,6 +59,7 @@ struct Params {
   int groups;               // ceil(V / ops) offset groups per tile
   int bsleep, esleep;       // poll back-off (ns) of the weight producer / the epilogue
   int vk;                   // virtual-K: K = the V x C_in concatenation in 64-wide chunks
+  int nsplit, n_unit;       // work unit = (row tile, one of nsplit n_unit-column slices)
   int nblk;                 // A/B blocks per tile: V (per-offset K chunks) or ceil(V C_in / 64)
   uint32_t idesc, tmem_cols;
   uint32_t a_off_bytes;     // one offset's A block [128 rows][kc] (1024-aligned)
@@ -117,16 +118,18 @@ __device__ __forceinline__ void epilogue_role(const Params& p, const CUtensorMap
   uint8_t* bufs = epi_base + (warp - epi0) * p.epi_bufs * EPI_BUF;
   int acc = 0, nbuf = 0;
   uint32_t acc_phase = 0;
-  const int chunks = p.n_pad / p.epi_cols;
+  const int chunks = p.n_unit / p.epi_cols;
   for (int t = t_begin; t < t_end; ++t) {
     IC_PROF(5, warp == epi0 && lane == 0, mbar_wait_sleep(tfull + acc, acc_phase, p.esleep));
     tc_after();
-    const long long row0 = (long long)t * BM + 32 * q;
+    const int rt = p.nsplit == 2 ? (t >> 1) : t;
+    const int cb = p.nsplit == 2 ? (t & 1) * p.n_unit : 0;   // first output column of the unit
+    const long long row0 = (long long)rt * BM + 32 * q;
     const long long k = row0 + lane;
     const bool row_ok = k < p.n_out;
     for (int j = 0; j < chunks && row0 < p.n_out; ++j) {
-      const int c0 = j * p.epi_cols;
-      const uint32_t taddr = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * p.n_pad + c0);
+      const uint32_t taddr = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * p.n_unit + j * p.epi_cols);
+      const int c0 = cb + j * p.epi_cols;   // output column
       uint32_t r[32];
       TMEM_LD_X16(taddr, r);
       if (p.epi_cols == 32) TMEM_LD_X16(taddr + 16, (r + 16));
@@ -281,7 +284,7 @@ __global__ void __launch_bounds__(64 + 128 * P + 128, MINB)
                   tma_load_2d(sb + o * p.b_off_bytes, &tmB, full + stage, (g * p.ops + o) * 64, 0);
                 else
                   tma_load_2d(sb + o * p.b_off_bytes, &tmB, full + stage, kk * p.kc,
-                              (g * p.ops + o) * p.n_pad);
+                              (g * p.ops + o) * p.n_pad + (p.nsplit == 2 ? (t & 1) * p.n_unit : 0));
               }
             }
             if (++stage == p.stages) { stage = 0; phase ^= 1; }
@@ -299,7 +302,7 @@ __global__ void __launch_bounds__(64 + 128 * P + 128, MINB)
     const int h = pt >> 7;
     int nxt[NT];
     {
-      const long long k = (long long)t_begin * BM + row;
+      const long long k = (long long)(p.nsplit == 2 ? (t_begin >> 1) : t_begin) * BM + row;
 #pragma unroll
       for (int i = 0; i < NT; ++i) {
         const int n = h + i * P;
@@ -340,7 +343,7 @@ __global__ void __launch_bounds__(64 + 128 * P + 128, MINB)
       }
       asm volatile("bar.sync 1, %0;" ::"n"(NPROD) : "memory");
       {
-        const long long k = (long long)(t + 1) * BM + row;
+        const long long k = (long long)(p.nsplit == 2 ? ((t + 1) >> 1) : (t + 1)) * BM + row;
         const bool ok = (t + 1 < t_end) && k < p.n_out;
 #pragma unroll
         for (int i = 0; i < NT; ++i) {
@@ -492,7 +495,7 @@ __global__ void __launch_bounds__(64 + 128 * P + 128, MINB)
     for (int t = t_begin; t < t_end; ++t) {
       IC_PROF(4, lane == 0, mbar_wait(tempty + acc, acc_phase ^ 1));
       tc_after();
-      const uint32_t d = tmem0 + (uint32_t)acc * n_pad;
+      const uint32_t d = tmem0 + (uint32_t)acc * (uint32_t)p.n_unit;
       for (int g = 0; g < p.groups; ++g) {
         const int nv = min(p.ops, p.nblk - g * p.ops);
         for (int kk = 0; kk < p.n_kchunks; ++kk) {
@@ -877,13 +880,24 @@ static int32_t conv_implicit_impl(const void* features, int64_t ldf, int32_t c_s
   }
   p.vk = vk ? 1 : 0;
   p.nblk = vk ? kv / 64 : volume;
-  p.epi_cols = (n_pad % 32 == 0) ? 32 : 16;
-  p.relu = relu;
-  p.idesc = (1u << 4) | ((uint32_t)(n_pad >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
   auto env_int = [](const char* name, int dflt) {
     const char* e = getenv(name);
     return e ? atoi(e) : dflt;
   };
+  // Column split (opt-in, SCB_IC_NSPLIT=2, C_out = 256): work units of (row
+  // tile, 128-column half), two CTAs per SM -- against the tile quantisation
+  // of the deepest levels (~177 row tiles for 148 SMs).  Measured slower:
+  // 0.142 vs 0.099 ms at L4 256->256 k3, 0.279 vs 0.209 at L3 (a half-width
+  // unit costs nearly the MMA-issue time of a full one), step 711 vs 718.
+  {
+    const bool ts_req = env_int("SCB_IC_TS", 0) != 0;
+    const bool split = !vk && !ts_req && n_pad == 256 && env_int("SCB_IC_NSPLIT", 1) == 2;
+    p.nsplit = split ? 2 : 1;
+    p.n_unit = split ? 128 : n_pad;
+  }
+  p.epi_cols = (p.n_unit % 32 == 0) ? 32 : 16;
+  p.relu = relu;
+  p.idesc = (1u << 4) | ((uint32_t)(p.n_unit >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
   // Launch shape: two CTAs per SM when both accumulator pairs fit in TMEM
   // (C_out <= 128) -- one CTA's producer / MMA-issue gaps are filled by the
   // other -- else one; P producer threads per output row.
@@ -894,7 +908,7 @@ static int32_t conv_implicit_impl(const void* features, int64_t ldf, int32_t c_s
   p.rowmode = (env_int("SCB_IC_ROW", 0) && !vk) ? 1 : 0;
   if (const char* e = getenv("SCB_IC_NACC")) p.nacc = atoi(e) == 1 ? 1 : 2;
   uint32_t cols = 32;
-  while (cols < (uint32_t)(p.nacc * n_pad)) cols *= 2;
+  while (cols < (uint32_t)(p.nacc * p.n_unit)) cols *= 2;
   p.tmem_cols = cols;
   // 3 CTAs per SM measured 12 % faster for 64->64 (K chunks of 64) and
   // slower for narrower inputs; 2 whenever both accumulator pairs fit
@@ -906,9 +920,9 @@ static int32_t conv_implicit_impl(const void* features, int64_t ldf, int32_t c_s
   const int cpr = p.kc / 8;
   const int P = 1;  // producer threads per row (2 measured slower: more warps, same issue stream)
   const int nprod = 128 * P;
-  p.total_tiles = (int)((n_out + BM - 1) / BM);
+  p.total_tiles = (int)((n_out + BM - 1) / BM) * p.nsplit;
   auto r1024 = [](uint32_t x) { return (x + 1023u) / 1024u * 1024u; };
-  p.b_tx = (uint32_t)(n_pad * p.kc * 2);
+  p.b_tx = (uint32_t)(p.n_unit * p.kc * 2);
   p.a_off_bytes = r1024((uint32_t)(BM * p.kc * 2));
   p.b_off_bytes = r1024(p.b_tx);
   const uint32_t op_bytes = p.a_off_bytes + p.b_off_bytes;
@@ -1042,7 +1056,7 @@ static int32_t conv_implicit_impl(const void* features, int64_t ldf, int32_t c_s
   if (!(vk ? encode_map_2d(&mB, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, weights_packed, kv, n_pad,
                            kv, 64, n_pad, 128, err)
            : encode_map_2d(&mB, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, weights_packed, k_pad,
-                           (long long)volume * n_pad, k_pad, p.kc, n_pad, p.swz, err)) ||
+                           (long long)volume * n_pad, k_pad, p.kc, p.n_unit, p.swz, err)) ||
       !encode_map_2d(&mO, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, out, c_out, n_out, ldo,
                      p.epi_cols, 32, p.epi_cols * 2, err)) {
     set_error(std::string("scb_conv_implicit: ") + err);

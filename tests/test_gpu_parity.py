@@ -640,3 +640,26 @@ def test_fused_virtual_k_form(sc, rng, monkeypatch, c_in, c_out, split):
                                  None, None, sc.ExecOptions(dataflow="fused"), epilogue=ep,
                                  concat=skip)
     assert rel_l2(out.features_numpy().astype(np.float32), want) <= 1e-2
+
+
+@pytest.mark.parametrize("k,c_in", [(3, 64), (3, 256), (1, 256)])
+def test_fused_column_split(sc, rng, monkeypatch, k, c_in):
+    """C_out = 256 as two 128-column work units per row tile
+    (SCB_IC_NSPLIT=2) against the oracle, BN + residual + ReLU epilogue."""
+    monkeypatch.setenv("SCB_IC_NSPLIT", "2")
+    c_out = 256
+    coords = random_coords(rng, (20, 20, 20), 0.15)
+    n = coords.shape[0]
+    f = O.quantize(rng.standard_normal((n, c_in)).astype(np.float32), "fp16")
+    r = O.quantize(rng.standard_normal((n, c_out)).astype(np.float32), "fp16")
+    w = rng.normal(0, 1 / np.sqrt(k ** 3 * c_in), (k ** 3, c_in, c_out)).astype(np.float32)
+    s = rng.uniform(0.8, 1.2, c_out).astype(np.float32)
+    h = rng.normal(0, 0.05, c_out).astype(np.float32)
+    _, base, _ = O.conv_forward(coords, f, (20, 20, 20), w, k, 1)
+    want = np.maximum(base.astype(np.float32) * s + h + r.astype(np.float32), 0)
+    ep = {"scale": torch.from_numpy(s).cuda(), "shift": torch.from_numpy(h).cuda(),
+          "residual": sc.SparseTensor(coords, r, 1, (20, 20, 20)), "relu": True}
+    out = sc.sparse_conv_forward(sc.SparseTensor(coords, f, 1, (20, 20, 20)),
+                                 sc.WeightTensor(w, k, 3), sc.LayerSpec(k, 1, c_in, c_out), None,
+                                 None, sc.ExecOptions(dataflow="fused"), epilogue=ep)
+    assert rel_l2(out.features_numpy().astype(np.float32), want) <= 1e-2
