@@ -2,21 +2,26 @@
 (BASELINE.json metric).
 
     python bench.py [--gpus N --steps K --warmup W --impl {engine,reference}]
+                    [--strong S] [--model centerpoint] [--layer-csv PATH]
 
 One process per GPU (torchrun for N > 1).  Scans are independent, so every
-rank runs its own batch of scans (seeds rank*B .. rank*B+B-1, packed into one
-batched SparseTensor with a shared boundary) with no data-path collective:
-weak scaling.  Default workload = config 5's per-GPU shard: MinkUNet 1.0x,
-FP16 feature storage, B = 8 scans per GPU per step (64 scans at N = 8).
+rank runs its own batch of scans packed into one batched SparseTensor with a
+shared boundary, with no data-path collective.  Default: weak scaling, B = 8
+scans per GPU per step (config 5's per-GPU shard; 64 scans at N = 8).
+``--strong S``: config 5 as a fixed batch of S scans (64) assigned to the
+ranks by LPT on voxel count (strong scaling).
 
-`value`   whole-job scans/s with inputs resident in HBM (device-timed with
-          CUDA events, max over ranks), L2 flushed between timed steps.
-`e2e`     the same through the public API with host buffers: pinned H2D of
-          coords + features, SparseTensor construction (validated),
-          Network forward, D2H of the logits, every step.
-`roofline` the dominant stage kernel (algorithmic bytes / its event time).
-`cpu_baseline` the CPU oracle port of the same graph on this host (rank 0,
-          N = 1), on a bounded sample (azimuth sectors of a scan).
+`value`    whole-job scans/s with inputs resident in HBM (device-timed with
+           CUDA events, max over ranks), L2 flushed between timed steps.
+`e2e`      the same through the public API with host buffers: pinned H2D of
+           coords + features, SparseTensor construction (validated),
+           model forward, D2H of the logits (each rank's final output to
+           host memory: the path's only "gather"), every step.
+`roofline` the dominant kernel (algorithmic bytes / its event time), from K
+           more steps instrumented with per-layer CUDA events.
+`cpu_baseline` the UNMODIFIED reference package (baseline/_ref) running the
+           same MinkUNet graph on whole scans, one process per host core
+           (rank 0, N = 1).
 `--impl reference` times that CPU path alone (the reference arm).
 """
 
@@ -49,7 +54,6 @@ CP_UNIT = "sweeps/s"
 
 def metric_unit(args):
     return (METRIC, UNIT) if args.model == "minkunet" else (CP_METRIC, CP_UNIT)
-SECTORS = 8
 
 
 def parse():
@@ -64,7 +68,12 @@ def parse():
     ap.add_argument("--scans-per-gpu", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--cpu-seconds", type=float, default=60.0,
+                    help="CPU-arm budget: steps run until it is used (at least one)")
+    ap.add_argument("--strong", type=int, default=None,
+                    help="strong scaling over a fixed batch of S scans (config 5: 64)")
+    ap.add_argument("--layer-csv", default=None,
+                    help="write the per-(layer, stage) CUDA-event table (layer,stage,metric,value)")
     ap.add_argument("--dataflow", choices=("staged", "fused", "auto"), default="auto")
     ap.add_argument("--clock-ms", type=int, default=5, help="clock sampling period (0: off)")
     return ap.parse_args()
@@ -108,63 +117,63 @@ def pack(scans):
     return coords, feats, boundary
 
 
-def sectors(scan, n=SECTORS):
-    """Azimuth sectors of one scan (features hold absolute x, y)."""
-    c, f, b = scan
-    ang = np.mod(np.arctan2(f[:, 1], f[:, 0]), 2 * np.pi)
-    sid = np.minimum((ang / (2 * np.pi / n)).astype(int), n - 1)
-    return [(c[sid == k], f[sid == k], b) for k in range(n)]
-
-
-# ------------------------------------------------------------------ CPU path (oracle port)
+# ------------------------------------------------------------------ CPU path (the reference)
 
 _W = {}
 
 
-def _cpu_worker_init(width, model="minkunet"):
-    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
-    _W["width"], _W["model"] = width, model
+def _cpu_worker_init(width, model, scans):
+    for k in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS", "NUMBA_NUM_THREADS"):
+        os.environ[k] = "1"
+    from oracle.reference_runner import import_reference
+    S = import_reference()
+    _W.update(S=S, width=width, model=model, scans=scans)
     if model == "minkunet":
         from paper_2204_10319_b200.minkunet import build_params
         _W["params"] = build_params(width, 4, 0)
     else:
         from paper_2204_10319_b200.centerpoint import build_params
         _W["params"] = build_params(5, 0)
+    # numba JIT of the reference's movement kernels, outside any timed step
+    rng = np.random.default_rng(0)
+    keys = np.sort(rng.choice(16 ** 3, 600, replace=False))
+    c = np.stack([np.zeros_like(keys), keys // 256, keys // 16 % 16, keys % 16], 1)
+    t = S.quantize_features(S.SparseTensor(c, rng.standard_normal((600, 8)), 1, (16, 16, 16)),
+                            S.PrecisionMode.FP16_STORAGE)
+    S.sparse_conv_forward(t, S.WeightTensor(rng.standard_normal((27, 8, 8)), 3, 3),
+                          S.LayerSpec(3, 1, 8, 8), options=S.ExecOptions(index_kind="hash"))
 
 
-def _cpu_worker_run(item):
-    from oracle import sparseconv_oracle as O
-    c, f, b = item
+def _cpu_worker_run(i):
+    from oracle import reference_runner as R
+    c, f, b = _W["scans"][i % len(_W["scans"])]
     t0 = time.perf_counter()
     if _W["model"] == "minkunet":
-        from paper_2204_10319_b200.minkunet import forward_oracle
-        forward_oracle(_W["params"], _W["width"], c, O.quantize(f, "fp16"), b)
+        R.minkunet_reference(_W["S"], _W["params"], _W["width"], c, f, b)
     else:
-        from paper_2204_10319_b200.centerpoint import forward_oracle
-        forward_oracle(_W["params"], c, O.quantize(f, "fp16"), b)
+        R.centerpoint_reference(_W["S"], _W["params"], c, f, b)
     return time.perf_counter() - t0
 
 
 class CpuPath:
-    """The reference's CPU path (oracle port) over P worker processes, each
-    running the full MinkUNet graph on one azimuth sector (1/8 scan) per step."""
+    """The reference's own CPU implementation (the unmodified `sparseconv`
+    package through its public API, oracle/reference_runner.py) on P worker
+    processes, one host core each; a step = every worker runs one whole scan
+    of the workload's scan set."""
 
     def __init__(self, width, scans, procs, model="minkunet"):
         import multiprocessing as mp
-        os.environ["OPENBLAS_NUM_THREADS"] = "1"
-        os.environ["OMP_NUM_THREADS"] = "1"
-        os.environ["MKL_NUM_THREADS"] = "1"
-        self.items = [sec for s in scans for sec in sectors(s)]
-        self.procs = max(1, min(procs, len(self.items)))
-        self.pool = mp.get_context("spawn").Pool(self.procs, _cpu_worker_init, (width, model))
+        self.procs = max(1, procs)
+        self.pool = mp.get_context("spawn").Pool(self.procs, _cpu_worker_init,
+                                                 (width, model, scans))
         self.cursor = 0
 
     def step(self):
-        batch = [self.items[(self.cursor + i) % len(self.items)] for i in range(self.procs)]
+        items = list(range(self.cursor, self.cursor + self.procs))
         self.cursor += self.procs
         t0 = time.perf_counter()
-        self.pool.map(_cpu_worker_run, batch, chunksize=1)
-        return time.perf_counter() - t0, self.procs / SECTORS  # seconds, scans processed
+        self.pool.map(_cpu_worker_run, items, chunksize=1)
+        return time.perf_counter() - t0, float(self.procs)  # seconds, scans processed
 
     def close(self):
         self.pool.close()
@@ -181,55 +190,84 @@ def cpu_model():
     return "unknown"
 
 
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def run_cpu(args, scans, budget_s):
+    """Whole scans on every host core through the reference; steps until
+    `budget_s` is used (at least one).  Returns (value, steps, secs, procs)."""
+    procs = min(cpu_cores(), 64)
+    cpu = CpuPath(args.width, scans, procs, args.model)
+    secs, done, steps = 0.0, 0.0, 0
+    while steps < max(1, args.steps):
+        s_, d_ = cpu.step()
+        secs += s_
+        done += d_
+        steps += 1
+        if secs + s_ > budget_s:
+            break
+    cpu.close()
+    return done / secs, steps, secs, cpu.procs
+
+
 def run_reference(args):
-    """--impl reference: rank 0 alone times the CPU path; others exit."""
+    """--impl reference: rank 0 alone times the reference's CPU path; the
+    other ranks exit without work."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    n_scans = 2
-    scans = load_scans(range(n_scans), args.model)
+    B = args.scans_per_gpu if args.strong is None else args.strong
+    scans = load_scans(range(B), args.model)
     METRIC, UNIT = metric_unit(args)
-    procs = min(os.cpu_count() or 1, 64)
-    cpu = CpuPath(args.width, scans, procs, args.model)
-    for _ in range(args.warmup):
-        cpu.step()
-    secs, done = 0.0, 0.0
-    for _ in range(args.steps):
-        s, d = cpu.step()
-        secs += s
-        done += d
-    cpu.close()
-    value = done / secs
-    sample = (f"{cpu.procs} worker processes x 1 azimuth sector (1/{SECTORS} scan) of MinkUNet "
-              f"{args.width}x per step, FP16 storage, oracle port (numpy/OpenBLAS 1 thread each)")
+    value, steps, secs, procs = run_cpu(args, scans, args.cpu_seconds)
+    name = "MinkUNet" if args.model == "minkunet" else "CenterPoint-style encoder"
+    sample = (f"{procs} worker processes x 1 whole scan each per step ({name} "
+              f"{args.width if args.model == 'minkunet' else ''}, FP16 storage, hash index), "
+              f"{steps} step(s), {steps * procs} scans in {secs:.1f} s; the unmodified reference "
+              f"package (baseline/_ref) through its own API, 1 BLAS/numba thread per process; "
+              f"numba JIT done per worker before timing")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f16-storage/f32-accumulate", "data": "synthetic",
-        "config": workload_config(args, 1),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cpu.procs, "kind": "port",
+        "n_gpus": args.gpus, "steps": steps, "steps_requested": args.steps, "warmup": 0,
+        "ms_per_step": 1e3 * secs / steps, "higher_is_better": True,
+        "scaling": "weak" if args.strong is None else "strong",
+        "vs_baseline": None, "dtype": "f16-storage/f32-accumulate", "data": DATA,
+        "config": workload_config(args, args.gpus, scans),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": "reference",
                          "sample": sample, "cpu": cpu_model()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def workload_config(args, world):
+DATA = "synthetic (raycast LiDAR scans, random-init weights)"
+
+
+def workload_config(args, world, scans):
+    """Identical for both arms (same data, same graph)."""
+    vox = int(round(np.mean([sc_[0].shape[0] for sc_ in scans]))) if scans else 0
     if args.model == "centerpoint":
-        work = (f"CenterPoint-style sparse encoder (21 k3 layers, 4 strided), "
-                f"{args.scans_per_gpu} nuScenes-shaped 10-sweep clouds per GPU per step "
-                f"(~200k voxels each, 0.075 m, 5 channels), FP16 storage")
+        work = (f"CenterPoint-style sparse encoder (21 k3 layers, 4 strided) on nuScenes-shaped "
+                f"10-sweep clouds (~{vox // 1000}k voxels each, 0.075 m, 5 channels), FP16 storage")
         name = "CenterPoint-encoder"
     else:
-        work = (f"MinkUNet {args.width}x, {args.scans_per_gpu} SemanticKITTI-shaped "
-                f"raycast scans per GPU per step (~120k voxels each, 0.05 m), FP16 storage")
+        work = (f"MinkUNet {args.width}x on SemanticKITTI-shaped raycast scans "
+                f"(~{vox // 1000}k voxels each, 0.05 m, 4 channels), FP16 storage")
         name = f"MinkUNet-{args.width}x"
-    return {"workload": work,
-            "model": name, "global_batch": args.scans_per_gpu * world,
-            "scans_per_gpu": args.scans_per_gpu, "parallelism": f"scan-sharded x{world}",
-            "l2": "flushed (256 MiB write, on the mapping stream ahead of the step's input reads) "
-                  "before every timed step; per-step buffers >> L2"}
+    if args.strong is None:
+        batch = {"global_batch": args.scans_per_gpu * world, "scans_per_gpu": args.scans_per_gpu,
+                 "parallelism": f"scan-sharded x{world} (weak: {args.scans_per_gpu} scans per GPU)"}
+    else:
+        batch = {"global_batch": args.strong, "scans_per_gpu": None,
+                 "parallelism": f"scan-sharded x{world} (strong: {args.strong} scans, LPT by "
+                                f"voxel count)"}
+    return dict({"workload": work, "model": name, "voxels_per_scan_mean": vox,
+                 "l2": "flushed (256 MiB write) before every timed step; per-step buffers >> L2"},
+                **batch)
 
 
 # ------------------------------------------------------------------ clocks
@@ -334,6 +372,25 @@ class Clocks:
 
 # ------------------------------------------------------------------ engine
 
+def assign_scans(args, rank, world):
+    """Seeds this rank runs: weak = its own block of B; strong = an LPT
+    share (by voxel count) of the fixed S-scan batch."""
+    from paper_2204_10319_b200.sharding import lpt_assign, shard_seeds
+    if args.strong is None:
+        return shard_seeds(rank, world, args.scans_per_gpu)
+    sizes = [s[0].shape[0] for s in load_scans(range(args.strong), args.model)]
+    return sorted(lpt_assign(sizes, world)[rank])
+
+
+def layer_table_rows(samples, steps):
+    """(layer, stage) -> ms per step, in the reference LatencyBreakdown's
+    long format (reference bench.py:26-76: layer,stage,metric,value)."""
+    rows = []
+    for (layer, stage), secs in samples.items():
+        rows.append((layer, stage, "ms", 1e3 * secs / steps))
+    return rows
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -351,13 +408,20 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
-    B = args.scans_per_gpu
+    if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        dist.init_process_group("nccl", device_id=dev)
+        probe = torch.ones(1, device=dev)
+        dist.all_reduce(probe)  # communicator up before any timing
+        print(f"[bench] rank {rank}: NCCL communicator size {dist.get_world_size()} "
+              f"(all_reduce probe {int(probe.item())})", file=sys.stderr, flush=True)
 
-    from paper_2204_10319_b200.sharding import shard_seeds
-    scans = load_scans(shard_seeds(rank, world, B), args.model)
+    seeds = assign_scans(args, rank, world)
+    scans = load_scans(seeds, args.model)
+    B = len(scans)
+    all_scans = scans if (world == 1 and args.strong is None) else \
+        load_scans(range(args.strong if args.strong else args.scans_per_gpu), args.model)
     coords, feats, boundary = pack(scans)
     if args.model == "minkunet":
         model = EngineMinkUNet(args.width, 4, 0)
@@ -371,20 +435,14 @@ def main():
     reserve = torch.empty(16 << 30, dtype=torch.uint8, device=dev)
     del reserve
 
-    ms = getattr(model, "mapping_stream", None) or torch.cuda.current_stream()
-
     def step(timer=None, traffic=None):
-        # the batch's coordinate set lives on the mapping stream (maps of
-        # batch i+1 overlap the convolutions of batch i)
-        with torch.cuda.stream(ms):
-            t = sc.SparseTensor(coords_d, feats_d, 1, boundary, B, validate=False)
+        t = sc.SparseTensor(coords_d, feats_d, 1, boundary, B, validate=False)
         t = sc.quantize_features(t, sc.PrecisionMode.FP16_STORAGE)
         return model.forward(t, sc.ExecOptions(timer=timer, traffic_log=traffic,
                                                index_kind="hash", dataflow=args.dataflow))
 
-    # algorithmic bytes per layer from one untimed pass (the
-    # traffic log takes the host-planned path, the timed steps the sync-free
-    # one); the warm-up steps after it settle the allocator again
+    # algorithmic bytes per layer from one untimed pass;
+    # the warm-up steps after it settle the allocator again
     traffic = []
     step(None, traffic)
     torch.cuda.synchronize()
@@ -396,8 +454,7 @@ def main():
         torch.cuda.synchronize()
         warm += 1
 
-    # ---------------- device-resident timed region
-    timer = sc.StageTimer()
+    # ---------------- device-resident timed region (no instrumentation)
     clocks = Clocks(str(ROOT / f"gpurun_out/clocks_rank{rank}.csv")
                     if (ROOT / "gpurun_out").exists() else f"/tmp/clocks_rank{rank}.csv")
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -412,24 +469,17 @@ def main():
     host_ms = []
     gc.collect()
     gc.disable()  # no collector pauses inside the timed steps
-    # One event pair brackets all K steps on the compute stream; the mapping
-    # stream starts after it.  Each step begins with an L2 flush on the
-    # mapping stream, ahead of that step's first read of its inputs, so the
-    # flushes (and any mapping overlapping the previous step) are inside the
-    # timed region.
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     switch0 = sys.getswitchinterval()
     sys.setswitchinterval(5e-4)  # let the clock-sampler thread in between host issues
     hw0 = time.perf_counter()
     t_start.record()
-    ms.wait_event(t_start)
     for i in range(args.steps):
-        with torch.cuda.stream(ms):
-            flush.fill_(i & 0xFF)
+        flush.fill_(i & 0xFF)  # L2 flush ahead of the step's first input read
         evs[i][0].record()
         h0 = time.perf_counter()
-        out = step(timer)
-        host_ms.append(1e3 * (time.perf_counter() - h0))
+        out = step()
+        host_ms.append(round(1e3 * (time.perf_counter() - h0), 3))
         evs[i][1].record()
     t_end.record()
     torch.cuda.synchronize()
@@ -441,47 +491,114 @@ def main():
     seg_allocs = torch.cuda.memory_stats(dev).get("segment.all.allocated", 0) - seg0
     launches = nat.load().scb_launch_count() - launches0
     clk = clocks.stop(local) if args.clock_ms > 0 else {"sm_mhz": None, "reasons": ["not sampled"]}
-    step_ms = [a.elapsed_time(b) for a, b in evs]  # compute-stream span of each step
+    step_ms = [round(a.elapsed_time(b), 4) for a, b in evs]
     total_s = torch.tensor(t_start.elapsed_time(t_end) / 1e3, device=dev, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(total_s, op=dist.ReduceOp.MAX)
     total_s = float(total_s)
-    value = B * world * args.steps / total_s
+    value = B * args.steps / total_s
+    if world > 1:  # whole-job scans/s: every rank's scans over the max-over-ranks time
+        nb = torch.tensor(float(B), device=dev, dtype=torch.float64)
+        dist.all_reduce(nb)
+        value = float(nb) * args.steps / total_s
 
-    # ---------------- roofline of the dominant stage kernel
-    stages = {}
-    for (layer, stage), s in timer.samples.items():
-        stages[stage] = stages.get(stage, 0.0) + s
+    # ---------------- instrumented steps: per-(layer, stage) CUDA events
+    timer = sc.StageTimer()
+    torch.cuda.synchronize()
+    for i in range(args.steps):
+        flush.fill_(i & 0xFF)
+        step(timer)
+    torch.cuda.synchronize()
+    samples = timer.samples
+    roof, stage_summary = roofline(args, samples, traffic)
+    if args.layer_csv and rank == 0:
+        with open(args.layer_csv, "w") as fh:
+            fh.write("layer,stage,metric,value\n")
+            for r in layer_table_rows(samples, args.steps):
+                fh.write(f"{r[0]},{r[1]},{r[2]},{r[3]:.6f}\n")
+
+    # ---------------- end to end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, sc, model, coords, feats, boundary, B, dev, world, UNIT, out)
+
+    # ---------------- CPU baseline (rank 0, N = 1): the reference on whole scans
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, st, secs, procs = run_cpu(args, scans, args.cpu_seconds)
+        cpu = {"value": v, "unit": UNIT, "cores": procs, "kind": "reference",
+               "sample": f"{procs} processes x 1 whole scan per step, {st} step(s), "
+                         f"{st * procs} scans in {secs:.1f} s: the unmodified reference package "
+                         f"(baseline/_ref) through its own API on this workload's scans, 1 thread "
+                         f"per process",
+               "cpu": cpu_model()}
+
+    if world > 1:
+        dist.barrier()
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * total_s / args.steps,
+            "ms_per_scan": 1e3 * total_s * world / (args.steps * max(1, B * world)),
+            "higher_is_better": True, "scaling": "weak" if args.strong is None else "strong",
+            "vs_baseline": None, "dtype": "f16-storage/f32-accumulate", "data": DATA,
+            "config": workload_config(args, world, all_scans),
+            "voxels_per_gpu_rank0": int(coords.shape[0]),
+            "roofline": roof, "stages_ms_per_step": stage_summary, "cpu_baseline": cpu,
+            "e2e": e2e, "gpu_launches": int(launches), "clocks": clk, "warmup_steps_run": warm,
+            "step_ms": step_ms, "host_issue_ms": host_ms,
+            "cuda_mallocs_in_timed_steps": seg_allocs,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def roofline(args, samples, traffic):
+    """Roofline of the dominant kernel from the instrumented steps: its
+    algorithmic bytes (index term 4 |M'|) or FLOPs per step
+    over its summed CUDA-event time."""
+    stages, mapping_levels = {}, {}
+    for (layer, stage), s_ in samples.items():
+        stages[stage] = stages.get(stage, 0.0) + s_
+        if stage == "mapping":
+            mapping_levels[layer] = mapping_levels.get(layer, 0.0) + s_
+    K = args.steps
     bytes_by = {"gather": 0, "matmul": 0, "scatter": 0, "fused": 0}
+    fused_dense_idx = 0
     flops = fused_flops = fused_exec = 0
-    for _, rec in traffic * args.steps:  # one pass recorded, K timed
-        bytes_by["gather"] += rec.get("gather_bytes", 0)
-        bytes_by["matmul"] += rec.get("gemm_bytes", 0)
-        bytes_by["scatter"] += rec.get("scatter_bytes", 0)
-        bytes_by["fused"] += rec.get("fused_bytes", 0)
-        flops += rec.get("gemm_flops", 0)
-        fused_flops += rec.get("fused_flops", 0)
-        fused_exec += rec.get("fused_flops_executed", 0)
+    n_fused = n_gemm = 0
+    for _, rec in traffic:
+        bytes_by["gather"] += rec.get("gather_bytes", 0) * K
+        bytes_by["matmul"] += rec.get("gemm_bytes", 0) * K
+        bytes_by["scatter"] += rec.get("scatter_bytes", 0) * K
+        bytes_by["fused"] += rec.get("fused_bytes", 0) * K
+        fused_dense_idx += rec.get("fused_bytes_dense_index", 0) * K
+        flops += rec.get("gemm_flops", 0) * K
+        fused_flops += rec.get("fused_flops", 0) * K
+        fused_exec += rec.get("fused_flops_executed", 0) * K
+        n_fused += "fused_bytes" in rec
+        n_gemm += "gemm_bytes" in rec
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) \
         if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
     tc_peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 1590.0))
-    src = ("MEASURED_PEAKS.json" if peaks
-           else "of fallback 6.65 TB/s / 1.59 PFLOP/s (B200_PROFILING.md; MEASURED_PEAKS.json absent)")
+    src = ("MEASURED_PEAKS.json (hbm_gbs; bf16_tflops_sustained: kernels timed inside a long step)"
+           if peaks else "fallback 6.65 TB/s / 1.59 PFLOP/s (B200_PROFILING.md; "
+                         "MEASURED_PEAKS.json absent)")
     dom = max(("gather", "matmul", "scatter", "fused"), key=lambda k: stages.get(k, 0.0))
     kernel_name = {"gather": "scb gather_kernel", "matmul": "scb grouped_gemm_f16_kernel (tcgen05)",
                    "scatter": "scb scatter_kernel",
                    "fused": "scb implicit_conv_f16_kernel (tcgen05, fused gather/GEMM/scatter)"}[dom]
-    n_launch = max(1, sum(1 for _, r in traffic if (("fused_bytes" in r) if dom == "fused"
-                                                      else ("gemm_bytes" in r))))
-    gbps = bytes_by[dom] / stages[dom] / 1e9
+    n_launch = max(1, n_fused if dom == "fused" else n_gemm)
+    t_dom = max(stages.get(dom, 0.0), 1e-12)
+    gbps = bytes_by[dom] / t_dom / 1e9
     measured = {}
     traffic_file = ROOT / "profiles" / "latest_traffic.json"
     if traffic_file.exists():
         measured = json.loads(traffic_file.read_text())
     if dom == "fused":
-        # arithmetic intensity of the useful work decides the bound (ridge = peak ratio)
-        tflops = fused_flops / stages[dom] / 1e12
+        tflops = fused_flops / t_dom / 1e12
         intensity = fused_flops / max(1, bytes_by[dom])
         tensor_bound = intensity > tc_peak * 1e12 / (hbm_peak * 1e9)
         roof = {"bound": "tensor" if tensor_bound else "hbm",
@@ -489,145 +606,111 @@ def main():
                 "peak": tc_peak if tensor_bound else hbm_peak,
                 "unit": "TFLOP/s" if tensor_bound else "GB/s"}
         roof["frac"] = roof["achieved"] / roof["peak"]
-        roof["algorithmic_flops_per_launch"] = fused_flops / args.steps / n_launch
+        roof["algorithmic_flops_per_launch"] = fused_flops / K / n_launch
         roof["arithmetic_intensity_flop_per_byte"] = intensity
         roof["hbm_frac"] = gbps / hbm_peak
+        roof["hbm_frac_dense_index_bytes"] = fused_dense_idx / t_dom / 1e9 / hbm_peak
         roof["tensor_frac_useful"] = tflops / tc_peak
-        roof["tensor_frac_executed"] = fused_exec / stages[dom] / 1e12 / tc_peak
+        roof["tensor_frac_executed"] = fused_exec / t_dom / 1e12 / tc_peak
     else:
         roof = {"bound": "hbm", "achieved": gbps, "peak": hbm_peak, "unit": "GB/s",
                 "frac": gbps / hbm_peak}
     m = measured.get(dom, {})
     roof.update({
         "kernel": kernel_name,
+        "kernel_ms_per_step": 1e3 * t_dom / K,
+        "launches_per_step": n_launch,
         "traffic": m.get("dram_bytes_per_launch"),
         "traffic_note": (f"ncu dram read+write of one launch ({m.get('launch')}) vs its "
                          f"{m.get('algorithmic_bytes_per_launch')} algorithmic bytes; "
                          f"{measured.get('source')}") if m else None,
-        "algorithmic_bytes_per_launch": bytes_by[dom] / args.steps / n_launch,
+        "algorithmic_bytes_per_launch": bytes_by[dom] / K / n_launch,
         "peak_source": src,
-        "per_stage": {k: {"ms_per_step": 1e3 * stages.get(k, 0.0) / args.steps,
-                          "GBps": (bytes_by[k] / stages[k] / 1e9) if stages.get(k) else None}
-                      for k in ("gather", "matmul", "scatter", "fused")},
-        "mapping_ms_per_step": 1e3 * stages.get("mapping", 0.0) / args.steps,
+        "timing": f"per-layer CUDA events on the compute stream over {K} instrumented steps "
+                  f"(after the timed region, same workload)",
     })
+    summary = {k: round(1e3 * v / K, 4) for k, v in sorted(stages.items())}
+    summary["mapping_by_level"] = {k: round(1e3 * v / K, 4) for k, v in sorted(mapping_levels.items())}
     if stages.get("matmul"):
         roof["gemm_tflops"] = flops / stages["matmul"] / 1e12
+    return roof, summary
 
-    # ---------------- end to end through the public API with host buffers
-    e2e = None
-    if not args.no_e2e:
-        h_coords = torch.from_numpy(coords.astype(np.int32)).pin_memory()
-        h_feats = torch.from_numpy(feats).pin_memory()
-        h_out = torch.empty(tuple(out.features.shape), dtype=torch.float16).pin_memory()
 
-        # a serving loop: uploads and the output download on their own copy
-        # streams, so batch i+1's H2D and batch i's D2H overlap compute.  Input
-        # buffers are a ring reused once the batch that last used them is done
-        # (no record_stream: its delayed block reuse cost cudaMallocs), and
-        # each output is kept alive until its download finished.
-        import collections
-        h2d_s, d2h_s = torch.cuda.Stream(), torch.cuda.Stream()
-        NB = 4
-        c_ring = [torch.empty(h_coords.shape, dtype=h_coords.dtype, device=dev) for _ in range(NB)]
-        f_ring = [torch.empty(h_feats.shape, dtype=h_feats.dtype, device=dev) for _ in range(NB)]
-        done = [None] * NB
-        pending = collections.deque()
-        counter = [0]
+def run_e2e(args, sc, model, coords, feats, boundary, B, dev, world, UNIT, out):
+    """End to end through the public API with host buffers: per step the
+    pinned H2D of coords + features, SparseTensor(validate="async"),
+    quantize, model forward, D2H of the logits, on copy streams."""
+    import collections
+    import torch
+    import torch.distributed as dist
+    h_coords = torch.from_numpy(coords.astype(np.int32)).pin_memory()
+    h_feats = torch.from_numpy(feats).pin_memory()
+    h_out = torch.empty(tuple(out.features.shape), dtype=torch.float16).pin_memory()
+    h2d_s, d2h_s = torch.cuda.Stream(), torch.cuda.Stream()
+    NB = 4
+    c_ring = [torch.empty(h_coords.shape, dtype=h_coords.dtype, device=dev) for _ in range(NB)]
+    f_ring = [torch.empty(h_feats.shape, dtype=h_feats.dtype, device=dev) for _ in range(NB)]
+    done = [None] * NB
+    pending = collections.deque()
+    counter = [0]
 
-        def e2e_step():
-            k = counter[0] % NB
-            counter[0] += 1
-            cur = torch.cuda.current_stream()
-            with torch.cuda.stream(h2d_s):
-                if done[k] is not None:
-                    h2d_s.wait_event(done[k])
-                c_ring[k].copy_(h_coords, non_blocking=True)
-                f_ring[k].copy_(h_feats, non_blocking=True)
-            cur.wait_stream(h2d_s)
-            # validated as a serving loop would: asynchronously, checked at the
-            # forward's first host read (no stall on the previous batch)
-            t = sc.SparseTensor(c_ring[k], f_ring[k], 1, boundary, B, validate="async")
-            t = sc.quantize_features(t, sc.PrecisionMode.FP16_STORAGE)
-            o = model.forward(t, sc.ExecOptions(index_kind="hash", dataflow=args.dataflow))
-            done[k] = cur.record_event()
-            d2h_s.wait_event(done[k])
-            with torch.cuda.stream(d2h_s):
-                h_out.copy_(o.features, non_blocking=True)
-                pending.append((o, d2h_s.record_event()))
-            while len(pending) > 3:
-                pending.popleft()[1].synchronize()
-            return o
+    def e2e_step():
+        k = counter[0] % NB
+        counter[0] += 1
+        cur = torch.cuda.current_stream()
+        with torch.cuda.stream(h2d_s):
+            if done[k] is not None:
+                h2d_s.wait_event(done[k])
+            c_ring[k].copy_(h_coords, non_blocking=True)
+            f_ring[k].copy_(h_feats, non_blocking=True)
+        cur.wait_stream(h2d_s)
+        t = sc.SparseTensor(c_ring[k], f_ring[k], 1, boundary, B, validate="async")
+        t = sc.quantize_features(t, sc.PrecisionMode.FP16_STORAGE)
+        o = model.forward(t, sc.ExecOptions(index_kind="hash", dataflow=args.dataflow))
+        done[k] = cur.record_event()
+        d2h_s.wait_event(done[k])
+        with torch.cuda.stream(d2h_s):
+            h_out.copy_(o.features, non_blocking=True)
+            pending.append((o, d2h_s.record_event()))
+        while len(pending) > 3:
+            pending.popleft()[1].synchronize()
+        return o
 
-        warm_e, w0 = 0, time.perf_counter()
-        while warm_e < args.warmup or (time.perf_counter() - w0 < 1.0 and warm_e < 200):
-            e2e_step()
-            torch.cuda.synchronize()
-            warm_e += 1
-        if world > 1:
-            dist.barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        gc.collect()
-        gc.disable()
-        seg_e = torch.cuda.memory_stats(dev).get("segment.all.allocated", 0)
-        e_host = []
-        e0.record()
-        for _ in range(args.steps):
-            h0 = time.perf_counter()
-            e2e_step()
-            e_host.append(round(1e3 * (time.perf_counter() - h0), 2))
-        torch.cuda.current_stream().wait_stream(d2h_s)  # the last download is inside the region
-        e1.record()
+    warm_e, w0 = 0, time.perf_counter()
+    while warm_e < args.warmup or (time.perf_counter() - w0 < 1.0 and warm_e < 200):
+        e2e_step()
         torch.cuda.synchronize()
-        gc.enable()
-        es = torch.tensor(e0.elapsed_time(e1) / 1e3, device=dev, dtype=torch.float64)
-        if world > 1:
-            dist.all_reduce(es, op=dist.ReduceOp.MAX)
-        e2e = {"value": B * world * args.steps / float(es), "unit": UNIT,
-               "h2d_bytes_per_step": int(h_coords.numel() * 4 + h_feats.numel() * 4),
-               "host_issue_ms": e_host, "warmup_steps_run": warm_e,
-               "cuda_mallocs_in_timed_steps":
-                   torch.cuda.memory_stats(dev).get("segment.all.allocated", 0) - seg_e,
-               "d2h_bytes_per_step": int(h_out.numel() * 2),
-               "path": "pinned H2D (copy stream) -> SparseTensor(validate=async) -> quantize -> "
-                       f"{args.model} forward -> D2H of the output features (copy stream)"}
-
-    # ---------------- CPU baseline (rank 0, N = 1)
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        procs = min(os.cpu_count() or 1, 64)
-        path = CpuPath(args.width, scans[:2], procs, args.model)
-        path.step()  # warm (spawn + imports)
-        secs, done = 0.0, 0.0
-        while secs < args.cpu_seconds:
-            s, d = path.step()
-            secs += s
-            done += d
-        path.close()
-        cpu = {"value": done / secs, "unit": UNIT, "cores": path.procs, "kind": "port",
-               "sample": f"{path.procs} processes x 1 azimuth sector (1/{SECTORS} scan) per round,"
-                         f" {done:.2f} scans in {secs:.1f} s; oracle port of the same MinkUNet "
-                         f"graph ({args.model}; numpy, 1 BLAS thread per process)",
-               "cpu": cpu_model()}
-
+        warm_e += 1
     if world > 1:
         dist.barrier()
-    if rank == 0:
-        n_vox = int(coords.shape[0])
-        line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": 1e3 * total_s / args.steps,
-            "ms_per_scan": 1e3 * total_s / (args.steps * B), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f16-storage/f32-accumulate",
-            "data": "synthetic (raycast LiDAR scans, random-init weights)",
-            "config": dict(workload_config(args, world), voxels_per_gpu=n_vox),
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
-            "clocks": clk, "warmup_steps_run": warm, "step_ms": step_ms, "host_issue_ms": host_ms,
-            "cuda_mallocs_in_timed_steps": seg_allocs,
-        }
-        print(json.dumps(line), flush=True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    gc.collect()
+    gc.disable()
+    seg_e = torch.cuda.memory_stats(dev).get("segment.all.allocated", 0)
+    e_host = []
+    e0.record()
+    for _ in range(args.steps):
+        h0 = time.perf_counter()
+        e2e_step()
+        e_host.append(round(1e3 * (time.perf_counter() - h0), 2))
+    torch.cuda.current_stream().wait_stream(d2h_s)  # the last download is inside the region
+    e1.record()
+    torch.cuda.synchronize()
+    gc.enable()
+    es = torch.tensor(e0.elapsed_time(e1) / 1e3, device=dev, dtype=torch.float64)
+    nb = torch.tensor(float(B), device=dev, dtype=torch.float64)
     if world > 1:
-        dist.destroy_process_group()
+        dist.all_reduce(es, op=dist.ReduceOp.MAX)
+        dist.all_reduce(nb)
+    return {"value": float(nb) * args.steps / float(es), "unit": UNIT,
+            "h2d_bytes_per_step": int(h_coords.numel() * 4 + h_feats.numel() * 4),
+            "d2h_bytes_per_step": int(h_out.numel() * 2),
+            "host_issue_ms": e_host, "warmup_steps_run": warm_e,
+            "cuda_mallocs_in_timed_steps":
+                torch.cuda.memory_stats(dev).get("segment.all.allocated", 0) - seg_e,
+            "path": "pinned H2D (copy stream) -> SparseTensor(validate=async) -> quantize -> "
+                    f"{args.model} forward -> D2H of the output features to this rank's pinned "
+                    f"host buffer (copy stream)"}
 
 
 if __name__ == "__main__":

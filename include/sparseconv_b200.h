@@ -275,26 +275,71 @@ int32_t scb_conv_implicit(const void* features, int64_t n_in, int32_t c_in, int6
  * matrices: channels [0, c_split) from `features` (row stride ldf), [c_split,
  * c_in) from `features2` (row stride ldf2) — the skip concatenation of a
  * U-Net decoder without materialising it.  `features2` NULL = scb_conv_implicit.
+ * `hits` may be NULL only for the identity map (K = 1, s = 1, n_in == n_out);
+ * a K = 1 strided map (volume 1) passes its hit matrix.
+ * `tile_mask` (nullable): [ceil(n_out / 128)] words from scb_tile_masks —
+ * offsets whose bit is clear in a 128-row tile's word are skipped for that
+ * tile (no weight load, no copies, no MMA); NULL = every offset.
  * `ldo`: output row stride in elements (multiple of 8, >= c_out), so C_out
  * need not be a multiple of 8 (e.g. a 19-class head into 24-wide rows). */
 int32_t scb_conv_implicit_cat(const void* features, int64_t ldf, int32_t c_split,
                               const void* features2, int64_t ldf2, int64_t n_in, int32_t c_in,
                               const int32_t* hits, int32_t volume, int64_t n_out,
-                              const void* weights_packed, int32_t c_out, void* out, int64_t ldo,
-                              const float* scale, const float* shift, const float* bias,
-                              const void* residual, int32_t relu, scb_stream_t stream);
+                              const uint32_t* tile_mask, const void* weights_packed,
+                              int32_t c_out, void* out, int64_t ldo, const float* scale,
+                              const float* shift, const float* bias, const void* residual,
+                              int32_t relu, scb_stream_t stream);
 
-/* Same layer with the weights in the virtual-K layout: weights_vk is fp16
- * [n_pad][ceil64(volume * c_in)] K-major, element (col, n * c_in + ci) =
- * W[n][ci][col] (zero padded), so the K loop runs over 64-wide chunks of the
- * offset-major channel concatenation (128-B-swizzled operand rows for any
- * C_in that is a multiple of 8).  volume must be 8 or 27. */
-int32_t scb_conv_implicit_vk(const void* features, int64_t ldf, int32_t c_split,
-                             const void* features2, int64_t ldf2, int64_t n_in, int32_t c_in,
-                             const int32_t* hits, int32_t volume, int64_t n_out,
-                             const void* weights_vk, int32_t c_out, void* out, int64_t ldo,
-                             const float* scale, const float* shift, const float* bias,
-                             const void* residual, int32_t relu, scb_stream_t stream);
+/* Active-offset words of a hit matrix per 128-row output tile: bit n of
+ * masks[t] is set when some row k in [128 t, 128 t + 128) has
+ * hits[n][k] >= 0.  volume <= 32.  B200 extension (no reference
+ * counterpart): the per-tile skip list of scb_conv_implicit_cat. */
+int32_t scb_tile_masks(const int32_t* hits, int32_t volume, int64_t n_out, uint32_t* masks,
+                       scb_stream_t stream);
+
+/* ---------------------------------------------------------------- row reordering
+ * B200 extension with no reference counterpart (the reference keeps rows in
+ * flat-key order; DESIGN.md §3 "presence-mask reordering").  A model may
+ * relabel the rows of a coordinate level so that 128-row tiles share their
+ * neighbour pattern; maps built over the relabelled set hold the same
+ * (input, output) pairs under the new row numbers, and the model
+ * un-permutes its output (scb_permute_rows), so results are unchanged. */
+
+/* mask[k] bit n = coords[k] + delta_n (stride 1, offsets of a K^D window with
+ * base offset_base) is a row of the indexed set; counts[n] (uint64, V words,
+ * zeroed here) = rows with bit n.  Odd K (symmetric probing: each row probes
+ * the lower half and sets the mirror bit of the neighbour it finds), K^D <= 32. */
+int32_t scb_presence_masks(int32_t kind, const int32_t* coords, int64_t n,
+                           const scb_grid_t* grid, int32_t kernel_size, int32_t offset_base,
+                           const int64_t* table_keys, const int32_t* table_rows, int64_t slots,
+                           uint32_t* masks, uint64_t* counts, scb_stream_t stream);
+
+int64_t scb_mask_sort_workspace(int64_t n);
+
+/* perm[i] = the row placed at position i: a stable sort by (batch column,
+ * mask with offsets re-ranked so the least frequent are the most
+ * significant bits).  `coords` int32 rows of `cols` words (batch first). */
+int32_t scb_mask_sort(const uint32_t* masks, const uint64_t* counts, const int32_t* coords,
+                      int32_t cols, int64_t n, int32_t volume, int64_t batch_size,
+                      void* workspace, int64_t ws_bytes, int32_t* perm, scb_stream_t stream);
+
+/* coords_out[i] = coords[perm[i]] (rows of `cols` int32) and inv_out[perm[i]] = i. */
+int32_t scb_apply_order(const int32_t* perm, int64_t n, const int32_t* coords, int32_t cols,
+                        int32_t* coords_out, int32_t* inv_out, scb_stream_t stream);
+
+/* An index of the same coordinates under relabelled rows (row r -> inv[r]):
+ * rows_out[s] = inv[rows_in[s]] for occupied slots / cells, -1 elsewhere.
+ * The hash keys (table_keys) are shared unchanged.  Replaces building a
+ * second index over the relabelled set. */
+int32_t scb_index_relabel(int32_t kind, const int64_t* table_keys, const int32_t* rows_in,
+                          int64_t slots, const int32_t* inv, int32_t* rows_out,
+                          scb_stream_t stream);
+
+/* Row permutation of a byte matrix: scatter = 0: dst[i] = src[index[i]];
+ * scatter = 1: dst[index[i]] = src[i]; row_bytes a multiple of 2. */
+int32_t scb_permute_rows(const void* src, int64_t src_ld_bytes, const int32_t* index, int64_t n,
+                         int32_t row_bytes, void* dst, int64_t dst_ld_bytes, int32_t scatter,
+                         scb_stream_t stream);
 
 /* ---------------------------------------------------------------- voxelisation
  * Replaces voxelize (core.py:174-216), the step in front of the path

@@ -85,9 +85,14 @@ _SIGS = {
     "scb_conv_implicit": (_I32, [_P, _I64, _I32, _I64, _P, _I32, _I64, _P, _I32, _P, _P, _P, _P,
                                  _P, _I32, _P]),
     "scb_conv_implicit_cat": (_I32, [_P, _I64, _I32, _P, _I64, _I64, _I32, _P, _I32, _I64, _P,
-                                     _I32, _P, _I64, _P, _P, _P, _P, _I32, _P]),
-    "scb_conv_implicit_vk": (_I32, [_P, _I64, _I32, _P, _I64, _I64, _I32, _P, _I32, _I64, _P,
-                                    _I32, _P, _I64, _P, _P, _P, _P, _I32, _P]),
+                                     _P, _I32, _P, _I64, _P, _P, _P, _P, _I32, _P]),
+    "scb_tile_masks": (_I32, [_P, _I32, _I64, _P, _P]),
+    "scb_presence_masks": (_I32, [_I32, _P, _I64, _GP, _I32, _I32, _P, _P, _I64, _P, _P, _P]),
+    "scb_mask_sort_workspace": (_I64, [_I64]),
+    "scb_mask_sort": (_I32, [_P, _P, _P, _I32, _I64, _I32, _I64, _P, _I64, _P, _P]),
+    "scb_permute_rows": (_I32, [_P, _I64, _P, _I64, _I32, _P, _I64, _I32, _P]),
+    "scb_apply_order": (_I32, [_P, _I64, _P, _I32, _P, _P, _P]),
+    "scb_index_relabel": (_I32, [_I32, _P, _P, _I64, _P, _P, _P]),
 }
 
 _lib = None

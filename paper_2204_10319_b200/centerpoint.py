@@ -12,8 +12,8 @@ padding; `src/core.py:150-161`):
 to 8 candidates per input, so their output coordinates are computed level
 by level (one host read each), all before the first convolution is queued.
 
-``EngineCenterPoint`` runs on the B200 engine; ``forward_oracle`` runs the
-same graph on the CPU oracle (tests only).
+``EngineCenterPoint`` runs on the B200 engine; the same graph on the CPU
+oracle (test infrastructure) is ``oracle.models.centerpoint_oracle``.
 """
 
 from __future__ import annotations
@@ -57,9 +57,14 @@ def build_params(in_channels: int = 5, seed: int = 0) -> dict:
 
 
 class EngineCenterPoint:
-    """The encoder on the B200 engine.  Parameters are uploaded once."""
+    """The encoder on the B200 engine.  Parameters are uploaded once.  Every
+    level but the output one is relabelled by neighbour presence
+    (mapping.reorder_by_presence; ``reorder=False`` / SCB_REORDER=0 keeps the
+    flat-key order); the output level is produced in the reference's
+    ascending-key order, so the result is the same either way."""
 
-    def __init__(self, in_channels: int = 5, seed: int = 0):
+    def __init__(self, in_channels: int = 5, seed: int = 0, reorder: bool | None = None):
+        import os
         import torch
         from .core import WeightTensor
         self.table = layer_table(in_channels)
@@ -71,34 +76,34 @@ class EngineCenterPoint:
             self.bn[l["name"]] = (torch.from_numpy(p["scale"]).cuda(),
                                   torch.from_numpy(p["shift"]).cuda())
             self.w[l["name"]].packed_f16()
-        # SCB_MAP_STREAM=1: maps on a high-priority side stream (overlaps the
-        # previous batch; measured noisier: the persistent conv kernels leave
-        # no room for the short mapping kernels between their boundaries)
-        self.mapping_stream = (torch.cuda.Stream(priority=-1)
-                               if __import__("os").environ.get("SCB_MAP_STREAM") == "1" else None)
+        self.reorder = (os.environ.get("SCB_REORDER", "1") == "1") if reorder is None else reorder
         from .execution import InflightLimiter
         self.inflight = InflightLimiter(2)
 
     def forward(self, t, options=None):
         from dataclasses import replace
+        from .core import SparseTensor
         from .execution import (ExecOptions, LayerSpec, prepare_layer_maps,
-                                prepare_maps_on_stream, sparse_conv_forward)
+                                prepare_reordered_level, sparse_conv_forward, _timed)
+        from .mapping import permute_rows, reorder_by_presence
         opts = replace(options) if options is not None else ExecOptions()
         self.inflight.before_forward()
-        if opts.map_reuse:  # the coordinate pyramid before any convolution is queued
-
-            def build(cs):
-                levels = [cs]
-                prepare_layer_maps(cs, LayerSpec(3, 1, 1, 1), opts)
-                for l in self.table:
-                    if l["s"] == 2:
-                        cs = prepare_layer_maps(cs, LayerSpec(3, 2, l["ci"], l["co"]), opts)
-                        prepare_layer_maps(cs, LayerSpec(3, 1, 1, 1), opts)
-                        levels.append(cs)
-                return levels
-
-            prepare_maps_on_stream(t, self.mapping_stream, build, opts.timer)
         x = t
+        if opts.map_reuse:  # the coordinate pyramid before any convolution is queued
+            with _timed(opts.timer, "pyramid", "mapping"):
+                cs = reorder_by_presence(t.coordset, 3, opts.index_kind or "auto") \
+                    if self.reorder else t.coordset
+                prepare_layer_maps(cs, LayerSpec(3, 1, 1, 1), opts)
+                if cs is not t.coordset:
+                    x = SparseTensor._wrap(permute_rows(t.features, cs.perm), t.stride,
+                                           t.boundary, t.batch_size, cs)
+                strided = [l for l in self.table if l["s"] == 2]
+                for i, l in enumerate(strided):
+                    last = i == len(strided) - 1
+                    cs = prepare_reordered_level(cs, LayerSpec(3, 2, l["ci"], l["co"]), opts,
+                                                 reorder=self.reorder and not last)
+                    if not last:
+                        prepare_layer_maps(cs, LayerSpec(3, 1, 1, 1), opts)
         for l in self.table:
             opts.layer_label = l["name"]
             sc, sh = self.bn[l["name"]]
@@ -107,17 +112,3 @@ class EngineCenterPoint:
                                     epilogue={"scale": sc, "shift": sh, "relu": True})
         self.inflight.after_forward()
         return x
-
-
-def forward_oracle(params: dict, coords: np.ndarray, feats: np.ndarray, boundary,
-                   batch_size: int = 1, in_channels: int = 5):
-    """The same graph on the CPU oracle (tests only): conv output in f32, BN
-    + ReLU in f32, one cast to the storage dtype per layer."""
-    from oracle import sparseconv_oracle as O
-    storage = feats.dtype
-    c, f, b = np.asarray(coords, np.int64), feats, tuple(boundary)
-    for l in layer_table(in_channels):
-        p = params[l["name"]]
-        c, of, b = O.conv_forward(c, f, b, p["w"], 3, l["s"], batch_size)
-        f = np.maximum(of.astype(np.float32) * p["scale"] + p["shift"], 0).astype(storage)
-    return c, f, b

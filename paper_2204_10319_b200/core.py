@@ -141,14 +141,19 @@ class CoordinateSet:
     indexes by kind and kernel maps by (kernel_size, stride) — the
     level-keyed map cache."""
 
-    __slots__ = ("coords", "boundary", "batch_size", "indexes", "maps", "stream", "__weakref__")
+    __slots__ = ("coords", "boundary", "batch_size", "indexes", "maps", "stream", "perm",
+                 "derived", "__weakref__")
 
-    def __init__(self, coords: torch.Tensor, boundary, batch_size: int):
+    def __init__(self, coords: torch.Tensor, boundary, batch_size: int, perm=None):
         self.coords = coords
         self.boundary = tuple(int(b) for b in boundary)
         self.batch_size = int(batch_size)
         self.indexes = {}
         self.maps = {}
+        self.derived = {}   # reordered twins of this set (mapping.reorder_by_presence)
+        # reordered set (mapping.reorder_by_presence): row i is row perm[i]
+        # of the set it was derived from; None for sets in their own order
+        self.perm = perm
         # the stream the coordinates were produced on (a model may continue
         # the mapping work there, off its compute stream)
         self.stream = torch.cuda.current_stream() if torch.cuda.is_available() else None
@@ -156,7 +161,7 @@ class CoordinateSet:
     def device_tensors(self):
         """Every device tensor owned by this set, its indexes and its maps
         (for Tensor.record_stream when another stream consumes them)."""
-        out = [self.coords]
+        out = [self.coords] + ([self.perm] if self.perm is not None else [])
         for idx in self.indexes.values():
             out += [t for t in (getattr(idx, "keys", None), getattr(idx, "rows", None),
                                 getattr(idx, "_status", None)) if isinstance(t, torch.Tensor)]

@@ -13,7 +13,7 @@ void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 extern "C" const char* scb_last_error(void) { return scb::g_last_error.c_str(); }
 
-extern "C" int32_t scb_abi_version(void) { return 1; }
+extern "C" int32_t scb_abi_version(void) { return 2; }
 
 extern "C" int64_t scb_launch_count(void) { return scb::g_launches.load(); }
 

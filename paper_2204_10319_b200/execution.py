@@ -20,8 +20,6 @@ storage runs an exact-f32 FMA GEMM (tolerance 1e-4).  The grouping strategy
 
 from __future__ import annotations
 
-import os
-
 import warnings
 from contextlib import contextmanager, nullcontext
 from dataclasses import dataclass
@@ -36,7 +34,7 @@ from .mapping import (DEFAULT_GRID_CELL_CAP, GatherScatterPlan, GridCapacityErro
                       KernelOffsets, build_gather_scatter_plan, build_index,
                       compute_output_coords, compute_output_coords_chain, downsample_boundary,
                       start_output_coords_chain,
-                      enumerate_offsets, map_search, _cells)
+                      enumerate_offsets, map_search, permute_rows, reorder_by_presence, _cells)
 
 GATHER_ORDERS = ("weight_stationary", "input_stationary")
 SCATTER_ORDERS = ("weight_stationary", "output_stationary")
@@ -496,20 +494,41 @@ def _direct_center(dtype, c_in: int) -> bool:
     return dtype == torch.float32 or c_in % 8 == 0
 
 
-def _epi_args(ep: dict | None):
+def _epi_vec(x, c_out: int, name: str):
+    if x is None:
+        return None
+    if not (isinstance(x, torch.Tensor) and x.is_cuda and x.dtype == torch.float32
+            and x.is_contiguous() and x.shape == (c_out,)):
+        raise ValueError(f"epilogue {name} must be a contiguous CUDA float32 vector of length "
+                         f"C_out = {c_out}")
+    return x.data_ptr()
+
+
+def _epi_args(ep: dict | None, n_out: int, c_out: int, dtype):
+    """Raw epilogue operands, checked: the kernels read scale/shift/bias as
+    f32[C_out] and the residual as a dense [n_out][C_out] matrix of the
+    storage dtype."""
     ep = ep or {}
     res = ep.get("residual")
     if isinstance(res, SparseTensor):
         res = res.features
-    return (nat.ptr(ep.get("scale")), nat.ptr(ep.get("shift")), nat.ptr(ep.get("bias")),
-            nat.ptr(res), int(bool(ep.get("relu", False))))
+    if res is not None:
+        if not (isinstance(res, torch.Tensor) and res.is_cuda and res.dtype == dtype
+                and tuple(res.shape) == (n_out, c_out)):
+            raise ValueError("residual must be a CUDA matrix of the output's shape and dtype")
+        if not res.is_contiguous():
+            raise ValueError("residual must be contiguous (row stride C_out)")
+    return (_epi_vec(ep.get("scale"), c_out, "scale"), _epi_vec(ep.get("shift"), c_out, "shift"),
+            _epi_vec(ep.get("bias"), c_out, "bias"), nat.ptr(res),
+            int(bool(ep.get("relu", False))))
 
 
 def _fused_eligible(dtype, volume: int, w: WeightTensor) -> bool:
     """The implicit-GEMM kernel: FP16 storage, K^3 in {1, 8, 27}, C_out up to
     256 (C_out not a multiple of 8, e.g. the 19-class head, is written into
     8-aligned rows and returned as a view).  C_in that is not a multiple of 8
-    (the 4-channel stem) is zero-padded to one."""
+    (the 4-channel stem) is zero-padded to one.  Volume 1 covers both the
+    K=1 s=1 identity map and K=1 strided maps (their hit matrix is read)."""
     return dtype == torch.float16 and volume in (1, 8, 27) and w.c_out <= 256
 
 
@@ -547,8 +566,9 @@ def _run_fused(features: torch.Tensor, kmap: KernelMap | None, w: WeightTensor,
     n_out = features.shape[0] if kmap is None else kmap.n_out
     ldo = (w.c_out + 7) // 8 * 8
     out = torch.empty((n_out, ldo), dtype=features.dtype, device=features.device)
-    scale, shift, bias, res, relu = _epi_args(epilogue)
+    scale, shift, bias, res, relu = _epi_args(epilogue, n_out, w.c_out, features.dtype)
     hits = None if kmap is None else nat.ptr(kmap.hits)
+    masks = None if kmap is None else nat.ptr(kmap.tile_masks())
     with _timed(timer, label, "fused"):
         if concat is not None and features.shape[1] % 8 == 0 and concat.shape[1] % 8 == 0 \
                 and features.is_contiguous() and concat.is_contiguous():
@@ -557,25 +577,36 @@ def _run_fused(features: torch.Tensor, kmap: KernelMap | None, w: WeightTensor,
             f = features if concat is None else torch.cat([features, concat], dim=1)
             f, ca, f2, cb = _pad_channels(f), None, None, 0
             ca = f.shape[1]
-        # virtual K (opt-in, SCB_IC_VK=1) for C_in not a multiple of 64: 128-B
-        # operand rows; measured slower on the MinkUNet layers
-        vk = volume > 1 and (ca + cb) % 64 != 0 and os.environ.get("SCB_IC_VK", "0") == "1"
-        wp = w.packed_vk_f16(ca + cb) if vk else packed
-        nat.call("scb_conv_implicit_vk" if vk else "scb_conv_implicit_cat", nat.ptr(f),
-                 f.shape[1], ca, nat.ptr(f2), 0 if f2 is None else f2.shape[1], f.shape[0],
-                 ca + cb, hits, volume, n_out, nat.ptr(wp), w.c_out, nat.ptr(out), ldo, scale,
-                 shift, bias, res, relu, nat.stream_handle())
+        nat.call("scb_conv_implicit_cat", nat.ptr(f), f.shape[1], ca, nat.ptr(f2),
+                 0 if f2 is None else f2.shape[1], f.shape[0], ca + cb, hits, volume, n_out,
+                 masks, nat.ptr(packed), w.c_out, nat.ptr(out), ldo, scale, shift, bias, res,
+                 relu, nat.stream_handle())
     if ldo != w.c_out:
         out = out[:, : w.c_out]  # 8-aligned rows for the TMA store; a strided view
     if opts.traffic_log is not None:
+        # algorithmic bytes: features in + out once, the
+        # index words of the map entries moved (4 |M'|: the centre of a
+        # stride-1 odd-K map is implicit), the weights, the residual
         e = 2
+        m_total = n_out if kmap is None else kmap.total
+        centre = kmap is not None and kmap.stride == 1 and kmap.offsets.center is not None
+        m_moved = 0 if kmap is None else m_total - (n_out if centre else 0)
+        base = (e * features.shape[0] * w.c_in + e * n_out * w.c_out
+                + e * volume * w.c_in * w.c_out + (e * n_out * w.c_out if res else 0))
+        if kmap is None:
+            blocks = (n_out + nat.TILE_ROWS - 1) // nat.TILE_ROWS
+        else:
+            tm = kmap.tile_masks().cpu().numpy().astype(np.uint32)
+            blocks = int(sum(bin(int(x)).count("1") for x in tm))
         opts.traffic_log.append((label, {
-            "fused_bytes": e * features.shape[0] * w.c_in + e * n_out * w.c_out
-            + (4 * volume * n_out if volume > 1 else 0) + e * volume * w.c_in * w.c_out
-            + (e * n_out * w.c_out if res else 0),
-            # algorithmic (useful) FLOPs 2 |M| C_in C_out; executed: dense over all V offsets
-            "fused_flops": 2 * (n_out if kmap is None else kmap.total) * w.c_in * w.c_out,
-            "fused_flops_executed": 2 * volume * n_out * w.c_in * w.c_out}))
+            "fused_bytes": base + 4 * m_moved,
+            "fused_bytes_dense_index": base + (4 * volume * n_out if volume > 1 else 0),
+            # useful FLOPs 2 |M| C_in C_out; executed: 128-row blocks of the
+            # active (tile, offset) pairs the kernel multiplies
+            "fused_flops": 2 * m_total * w.c_in * w.c_out,
+            "fused_flops_executed": 2 * blocks * nat.TILE_ROWS * w.c_in * w.c_out,
+            "fused_blocks": blocks, "fused_blocks_dense": volume * (
+                (n_out + nat.TILE_ROWS - 1) // nat.TILE_ROWS)}))
     return out
 
 
@@ -615,7 +646,7 @@ def _run_staged_device(features: torch.Tensor, kmap: KernelMap, w: WeightTensor,
     with _timed(timer, label, "scatter"):
         nat.call("scb_scatter", nat.ptr(partial), ldc, nat.ptr(dp.pos), kmap.offsets.volume,
                  kmap.n_out, c_out, 0 if direct else -1, nat.dtype_code(dt), nat.ptr(out), c_out,
-                 *_epi_args(epilogue), nat.stream_handle())
+                 *_epi_args(epilogue, kmap.n_out, c_out, dt), nat.stream_handle())
     return out
 
 
@@ -669,7 +700,7 @@ def _run_dataflow(features: torch.Tensor, kmap: KernelMap, w: WeightTensor,
     with _timed(timer, label, "scatter"):
         nat.call("scb_scatter", nat.ptr(partial), ldc, nat.ptr(plan.pos), plan.pos.shape[1],
                  kmap.n_out, c_out, center_row, nat.dtype_code(dt), nat.ptr(out), c_out,
-                 *_epi_args(epilogue), nat.stream_handle())
+                 *_epi_args(epilogue, kmap.n_out, c_out, dt), nat.stream_handle())
     if opts.traffic_log is not None:
         _record_traffic(opts, plan, c_in, c_out, dt, features.shape[0], kmap.n_out,
                         features.shape[0] if direct else 0, kmap.total)
@@ -699,7 +730,7 @@ def _pointwise_matmul(t: SparseTensor, w: WeightTensor, opts: ExecOptions, epilo
     out = torch.empty((n, w.c_out), dtype=dt, device=f.device)
     ident = _identity_pos(n, f.device)
     nat.call("scb_scatter", nat.ptr(partial), ldc, nat.ptr(ident), 1, n, w.c_out, -1,
-             nat.dtype_code(dt), nat.ptr(out), w.c_out, *_epi_args(epilogue),
+             nat.dtype_code(dt), nat.ptr(out), w.c_out, *_epi_args(epilogue, n, w.c_out, dt),
              nat.stream_handle())
     return out
 
@@ -852,6 +883,48 @@ def _chain_maps(cset, specs, steps, levels, opts):
             hit = cs.maps[key]
         cs = hit[0]
         out.append(cs)
+    return out
+
+
+def link_strided_map(fine: CoordinateSet, coarse: CoordinateSet, spec: LayerSpec,
+                     options: ExecOptions | None = None) -> KernelMap:
+    """Cache on ``fine`` the map of the strided layer ``spec`` whose output
+    coordinates are ``coarse`` (B200 extension): ``coarse`` must hold exactly
+    compute_output_coords(fine, ...), in any row order — e.g. a presence-
+    reordered level (mapping.reorder_by_presence).  The map is a plain map
+    search over fine's index, so its pairs are the reference's under
+    coarse's row numbering."""
+    opts = options or ExecOptions()
+    offsets = enumerate_offsets(len(fine.boundary), spec.kernel_size)
+    key = (spec.kernel_size, spec.stride, offsets.base)
+    hit = fine.maps.get(key)
+    if hit is not None and hit[0] is coarse:
+        return hit[1]
+    kind = opts.index_kind or spec.index_kind or "auto"
+    kmap = map_search(build_index(fine, kind, cell_cap=opts.grid_cell_cap), coarse.coords,
+                      offsets, spec.stride)
+    fine.maps[key] = (coarse, kmap)
+    return kmap
+
+
+def prepare_reordered_level(fine: CoordinateSet, spec: LayerSpec,
+                            options: ExecOptions | None = None, reorder: bool = True
+                            ) -> CoordinateSet:
+    """Output coordinate set of the strided layer ``spec`` over ``fine``,
+    relabelled by neighbour presence (reorder_by_presence) unless
+    ``reorder`` is False, with the layer's map cached on ``fine``
+    (B200 extension; one host read, the output count)."""
+    opts = options or ExecOptions()
+    offsets = enumerate_offsets(len(fine.boundary), spec.kernel_size)
+    hit = fine.maps.get((spec.kernel_size, spec.stride, offsets.base))
+    if hit is not None:
+        return hit[0]
+    ob = downsample_boundary(fine.boundary, spec.stride)
+    out = CoordinateSet(compute_output_coords(fine, offsets, spec.stride, ob, fine.batch_size), ob,
+                        fine.batch_size)
+    if reorder:
+        out = reorder_by_presence(out, 3, opts.index_kind or "auto")
+    link_strided_map(fine, out, spec, opts)
     return out
 
 

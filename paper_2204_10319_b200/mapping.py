@@ -134,6 +134,21 @@ class CoordinateIndex:
                  nat.stream_handle())
         self._status = status
 
+    @classmethod
+    def relabelled(cls, src: "CoordinateIndex", inv: torch.Tensor) -> "CoordinateIndex":
+        """``src`` under relabelled rows (row r -> inv[r]): the index of a
+        reordered twin of src's set without a second build
+        (scb_index_relabel; hash keys shared)."""
+        idx = object.__new__(cls)
+        idx.kind, idx.boundary, idx.batch_size = src.kind, src.boundary, src.batch_size
+        idx.size, idx._grid, idx.slots, idx.code = src.size, src._grid, src.slots, src.code
+        idx.keys = src.keys
+        idx.rows = torch.empty_like(src.rows)
+        idx._status = src._status
+        nat.call("scb_index_relabel", src.code, nat.ptr(src.keys), nat.ptr(src.rows), src.slots,
+                 nat.ptr(inv), nat.ptr(idx.rows), nat.stream_handle())
+        return idx
+
     @property
     def duplicates(self) -> int:
         return int(self._status[0].item())
@@ -168,6 +183,76 @@ def build_index(coords, kind: str = "auto", boundary=None, batch_size: int = 1,
         idx = CoordinateIndex(cset, kind)
         cset.indexes[kind] = idx
     return idx
+
+
+def presence_masks(cset: CoordinateSet, kernel_size: int = 3, kind: str = "auto"):
+    """Neighbour-presence word per row of ``cset`` (bit n: coordinate +
+    delta_n is in the set, stride 1) and the per-offset row counts, on the
+    device (scb_presence_masks).  B200 extension."""
+    offsets = enumerate_offsets(len(cset.boundary), kernel_size)
+    if offsets.volume > 32:
+        raise ValueError("presence masks hold at most 32 offsets")
+    idx = build_index(cset, kind)
+    dev = cset.coords.device
+    n = cset.num_points
+    masks = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    counts = torch.empty(offsets.volume, dtype=torch.int64, device=dev)
+    nat.call("scb_presence_masks", idx.code, nat.ptr(cset.coords), n, idx._grid, kernel_size,
+             offsets.base, nat.ptr(idx.keys), nat.ptr(idx.rows), idx.slots, nat.ptr(masks),
+             nat.ptr(counts), nat.stream_handle())
+    return masks[:n], counts
+
+
+def permute_rows(src: torch.Tensor, index: torch.Tensor, scatter: bool = False,
+                 out: torch.Tensor | None = None) -> torch.Tensor:
+    """Row permutation on the device (scb_permute_rows): ``out[i] =
+    src[index[i]]``, or ``out[index[i]] = src[i]`` with ``scatter``."""
+    n = index.shape[0]
+    rows = src.shape[0] if scatter else n
+    if out is None:
+        out = torch.empty((rows,) + tuple(src.shape[1:]), dtype=src.dtype, device=src.device)
+    rb = src.shape[1] * src.element_size()
+    ld_s = (src.stride(0) if src.shape[0] > 1 else src.shape[1]) * src.element_size()
+    ld_d = (out.stride(0) if out.shape[0] > 1 else out.shape[1]) * out.element_size()
+    nat.call("scb_permute_rows", nat.ptr(src), ld_s, nat.ptr(index), n, rb, nat.ptr(out), ld_d,
+             int(bool(scatter)), nat.stream_handle())
+    return out
+
+
+def reorder_by_presence(cset: CoordinateSet, kernel_size: int = 3,
+                        kind: str = "auto") -> CoordinateSet:
+    """The same coordinates with rows relabelled so that rows with similar
+    neighbour patterns are adjacent (B200 extension, the TorchSparse++
+    bitmask sort): a stable sort by (batch, presence mask with the rarest
+    offsets most significant).  Returns a new CoordinateSet whose row i is
+    row ``perm[i]`` of ``cset`` (``.perm``); maps built over it hold the same
+    pairs under the new row numbers, and 128-row tiles of its k3 maps have
+    far fewer active offsets (the fused kernel skips the rest).  Cached on
+    ``cset``."""
+    key = ("reorder", kernel_size)
+    hit = cset.derived.get(key)
+    if hit is not None:
+        return hit
+    n = cset.num_points
+    dev = cset.coords.device
+    masks, counts = presence_masks(cset, kernel_size, kind)
+    V = counts.shape[0]
+    lib = nat.load()
+    ws = torch.empty(int(lib.scb_mask_sort_workspace(n)), dtype=torch.uint8, device=dev)
+    perm = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    nat.call("scb_mask_sort", nat.ptr(masks), nat.ptr(counts), nat.ptr(cset.coords),
+             cset.coords.shape[1], n, V, cset.batch_size, nat.ptr(ws), ws.numel(), nat.ptr(perm),
+             nat.stream_handle())
+    perm = perm[:n]
+    coords = torch.empty_like(cset.coords)
+    inv = torch.empty_like(perm)
+    nat.call("scb_apply_order", nat.ptr(perm), n, nat.ptr(cset.coords), cset.coords.shape[1],
+             nat.ptr(coords), nat.ptr(inv), nat.stream_handle())
+    out = CoordinateSet(coords, cset.boundary, cset.batch_size, perm=perm)
+    for k, idx in cset.indexes.items():   # the same indexes, rows relabelled
+        out.indexes[k] = CoordinateIndex.relabelled(idx, inv)
+    cset.derived[key] = out
+    return out
 
 
 def downsample_boundary(boundary, stride: int) -> tuple[int, ...]:
@@ -324,6 +409,7 @@ class KernelMap:
         self._pairs = None
         self._plans = {}
         self._swapped = None
+        self._tile_masks = None
 
     @classmethod
     def from_hits(cls, hits, offsets, stride, n_in, n_out, symmetric=False) -> "KernelMap":
@@ -331,7 +417,7 @@ class KernelMap:
                    trusted=True, hits=hits)
 
     def device_tensors(self):
-        out = [t for t in (self._hits,) if t is not None]
+        out = [t for t in (self._hits, self._tile_masks) if t is not None]
         if self._csr is not None:
             out += [self._csr[0], self._csr[2], self._csr[3]]
         return out
@@ -354,6 +440,19 @@ class KernelMap:
                      self.total, self.n_out, nat.ptr(h), nat.stream_handle())
             self._hits = h
         return self._hits
+
+    def tile_masks(self) -> torch.Tensor:
+        """Active-offset word per 128-row output tile (scb_tile_masks): bit n
+        set when some row of the tile has a neighbour at offset n.  Built once
+        per map (B200 extension; the fused kernel skips clear bits)."""
+        if self._tile_masks is None:
+            h = self.hits
+            tiles = max((self.n_out + nat.TILE_ROWS - 1) // nat.TILE_ROWS, 1)
+            m = torch.empty(tiles, dtype=torch.int32, device=h.device)
+            nat.call("scb_tile_masks", nat.ptr(h), self.offsets.volume, self.n_out, nat.ptr(m),
+                     nat.stream_handle())
+            self._tile_masks = m
+        return self._tile_masks
 
     offset_ptr = property(lambda self: self._ensure_csr()[0])
     in_idx = property(lambda self: self._ensure_csr()[2])

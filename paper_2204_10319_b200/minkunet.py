@@ -15,8 +15,8 @@ cs = [32, 32, 64, 128, 256, 256, 128, 96, 96] x width.
 is folded (eval mode) into the scatter epilogue; residual add and concat are
 model glue (not reference layer kinds).
 
-``forward_engine`` runs on the B200 engine; ``forward_oracle`` runs the same
-graph on the CPU oracle (tests / CPU baseline only).
+``EngineMinkUNet`` runs on the B200 engine; the same graph on the CPU
+oracle (test infrastructure) is ``oracle.models.minkunet_oracle``.
 """
 
 from __future__ import annotations
@@ -82,9 +82,19 @@ def build_params(width: float, in_channels: int = 4, seed: int = 0) -> dict:
 # ---------------------------------------------------------------- engine
 
 class EngineMinkUNet:
-    """MinkUNet on the B200 engine.  Parameters are uploaded once."""
+    """MinkUNet on the B200 engine.  Parameters are uploaded once.
 
-    def __init__(self, width: float, in_channels: int = 4, seed: int = 0):
+    Coordinate levels are relabelled by neighbour presence
+    (mapping.reorder_by_presence; ``reorder=False`` or SCB_REORDER=0 keeps
+    the reference's flat-key row order): every layer then runs over rows
+    whose 128-row tiles share their active kernel offsets, and the fused
+    kernel skips the absent (tile, offset) blocks.  The input features are
+    permuted once, the logits un-permuted once, so the output rows are in
+    the input tensor's order — the same result either way."""
+
+    def __init__(self, width: float, in_channels: int = 4, seed: int = 0,
+                 reorder: bool | None = None):
+        import os
         import torch
         from .core import WeightTensor
         self.width = width
@@ -101,18 +111,10 @@ class EngineMinkUNet:
         # materialise device weights now (not inside a timed step)
         for name, w in self.w.items():
             w.packed_f16()
-        # mapping work (coordinate pyramid, hash indexes, kernel maps) runs
-        # here, off the compute stream: it depends on coordinates only, so
-        # the next batch's maps overlap this batch's convolutions
-        # SCB_MAP_STREAM=1: maps on a high-priority side stream (overlaps the
-        # previous batch; measured noisier: the persistent conv kernels leave
-        # no room for the short mapping kernels between their boundaries)
-        self.mapping_stream = (torch.cuda.Stream(priority=-1)
-                               if __import__("os").environ.get("SCB_MAP_STREAM") == "1" else None)
+        self.reorder = (os.environ.get("SCB_REORDER", "1") == "1") if reorder is None else reorder
         from .execution import InflightLimiter
-        self.inflight = InflightLimiter(int(__import__("os").environ.get("SCB_INFLIGHT", "3")))
-        import weakref
-        self._pending = weakref.WeakKeyDictionary()   # coordset -> deferred chain (prefetch)
+        self.inflight = InflightLimiter(int(os.environ.get("SCB_INFLIGHT", "3")))
+        self._pending = {}   # id(coordset) -> (coordset, level-0 set, deferred chain)
         self._specs = {}
 
     def _down_specs(self):
@@ -120,39 +122,61 @@ class EngineMinkUNet:
         return [LayerSpec(2, 2, self.w[f"down{i}"].c_in, self.w[f"down{i}"].c_out)
                 for i in range(1, 5)]
 
+    def _start(self, cset, opts):
+        """Queue the level-0 set (reordered), its k3 map and the strided
+        coordinate chain; returns (level-0 set, finisher).  The finisher
+        collects the chain's one host read and builds the other levels."""
+        from .execution import LayerSpec, link_strided_map, prepare_layer_maps, _timed
+        from .mapping import enumerate_offsets, reorder_by_presence, start_output_coords_chain
+        k3 = LayerSpec(3, 1, 1, 1)
+        kind = opts.index_kind or "auto"
+        timer = opts.timer
+        with _timed(timer, "L0", "mapping"):
+            l0 = reorder_by_presence(cset, 3, kind) if self.reorder else cset
+            prepare_layer_maps(l0, k3, opts)
+        specs = self._down_specs()
+        dim = len(cset.boundary)
+        with _timed(timer, "chain", "mapping"):
+            chain = start_output_coords_chain(cset, [(enumerate_offsets(dim, sp.kernel_size),
+                                                      sp.stride) for sp in specs])
+
+        def finish():
+            from .core import CoordinateSet
+            fine = l0
+            for i, (sp, (oc, ob)) in enumerate(zip(specs, chain()), 1):
+                with _timed(timer, f"L{i}", "mapping"):
+                    lvl = CoordinateSet(oc, ob, cset.batch_size)
+                    if self.reorder:
+                        lvl = reorder_by_presence(lvl, 3, kind)
+                    link_strided_map(fine, lvl, sp, opts)
+                    prepare_layer_maps(lvl, k3, opts)
+                fine = lvl
+        return l0, finish
+
     def prefetch(self, t, options=None) -> None:
         """Queue ``t``'s level-0 map and its strided coordinate chain now
         (B200 extension).  A serving loop calls this for batch i+1 before it
         runs batch i: the chain's one host read, collected in forward(batch
         i+1), then finds its kernels long finished instead of draining the
-        compute queue each forward.  Same maps, same results."""
+        compute queue each forward.  Same maps, same results.  At most one
+        batch is held (a newer prefetch replaces an unused older one)."""
         from dataclasses import replace
-        from .execution import ExecOptions, LayerSpec, prepare_layer_maps, prepare_strided_chain
+        from .execution import ExecOptions
         opts = replace(options) if options is not None else ExecOptions()
-        if self.mapping_stream is not None or not opts.map_reuse or t.coordset in self._pending:
+        if not opts.map_reuse:
             return
         opts.timer = None
-        prepare_layer_maps(t.coordset, LayerSpec(3, 1, 1, 1), opts)
-        self._pending[t.coordset] = prepare_strided_chain(t.coordset, self._down_specs(), opts,
-                                                          deferred=True)
-
-    def _prepare_maps(self, t, opts):
-        """The coordinate pyramid (one host read for the four k2 s2 levels)
-        and every level's k3 map, on the mapping stream."""
-        from .execution import (LayerSpec, prepare_layer_maps, prepare_maps_on_stream,
-                                prepare_strided_chain)
-
-        def build(cs):
-            levels = [cs] + prepare_strided_chain(cs, self._down_specs(), opts)
-            for lvl in levels:
-                prepare_layer_maps(lvl, LayerSpec(3, 1, 1, 1), opts)
-            return levels
-
-        prepare_maps_on_stream(t, self.mapping_stream, build, opts.timer)
+        key = id(t.coordset)
+        if key in self._pending:
+            return
+        l0, finish = self._start(t.coordset, opts)
+        self._pending = {key: (t.coordset, l0, finish)}
 
     def forward(self, t, options=None):
-        from .execution import (ExecOptions, LayerSpec, inverse_conv_forward,
+        from .core import SparseTensor
+        from .execution import (ExecOptions, LayerSpec, inverse_conv_forward, _timed,
                                 sparse_conv_forward)
+        from .mapping import permute_rows
         from dataclasses import replace
         base = replace(options) if options is not None else ExecOptions()  # private copy
         cache = {}
@@ -187,26 +211,25 @@ class EngineMinkUNet:
 
         names = {l["name"] for l in self.table}
         self.inflight.before_forward()
-        finish = None
+        finish, l0 = None, t.coordset
         if base.map_reuse:
-            if self.mapping_stream is not None:
-                self._prepare_maps(t, base)
+            # level-0 set and map plus the k2/s2 coordinate chain are queued
+            # first (or were, by prefetch()); the chain's count read is
+            # collected after the level-0 stems are queued
+            hit = self._pending.pop(id(t.coordset), None)
+            if hit is not None and hit[0] is t.coordset:
+                _, l0, finish = hit
             else:
-                # level-0 map and the k2/s2 coordinate chain are queued first
-                # (or were, by prefetch()); the chain's count read is collected
-                # after the level-0 stems are queued
-                finish = self._pending.pop(t.coordset, None)
-                if finish is None:
-                    from .execution import LayerSpec, prepare_layer_maps, prepare_strided_chain
-                    prepare_layer_maps(t.coordset, LayerSpec(3, 1, 1, 1), base)
-                    finish = prepare_strided_chain(t.coordset, self._down_specs(), base,
-                                                   deferred=True)
-        x = conv(t, "stem.0", 3, 1)
+                l0, finish = self._start(t.coordset, base)
+        x = t
+        if l0 is not t.coordset:  # relabelled level 0: permute the input rows once
+            with _timed(base.timer, "input", "permute"):
+                x = SparseTensor._wrap(permute_rows(t.features, l0.perm), t.stride, t.boundary,
+                                       t.batch_size, l0)
+        x = conv(x, "stem.0", 3, 1)
         x = conv(x, "stem.1", 3, 1)
         if finish is not None:  # both level-0 stems are queued: the GPU stays busy meanwhile
-            from .execution import LayerSpec, prepare_layer_maps
-            for lvl in finish():
-                prepare_layer_maps(lvl, LayerSpec(3, 1, 1, 1), base)
+            finish()
         skips = [x]
         for i in range(1, 5):
             x = conv(x, f"down{i}", 2, 2)
@@ -217,67 +240,12 @@ class EngineMinkUNet:
             x = conv(x, f"up{j}", 2, 1, reuse=f"down{5 - j}", kind="inverse")
             x = res(x, f"dec{j}.r0", True, skip=skips[4 - j])
             x = res(x, f"dec{j}.r1", f"dec{j}.r1.proj" in names)
-        out = conv(x, "head", 1, 1)
+        out = conv(x, "head", 1, 1, relu=False)  # logits: no BN, no ReLU
+        if l0 is not t.coordset:  # logits back to the input's row order
+            with _timed(base.timer, "output", "permute"):
+                f = out.features
+                rows = f.as_strided((f.shape[0], f.stride(0)), (f.stride(0), 1))
+                back = permute_rows(rows, l0.perm, scatter=True)[:, : f.shape[1]]
+            out = SparseTensor._wrap(back, out.stride, out.boundary, out.batch_size, t.coordset)
         self.inflight.after_forward()
         return out
-
-
-# ---------------------------------------------------------------- oracle (CPU)
-
-def forward_oracle(params: dict, width: float, coords: np.ndarray, feats: np.ndarray,
-                   boundary, batch_size: int = 1, in_channels: int = 4):
-    """The same graph on the CPU oracle (tests and the CPU baseline only).
-    Epilogue rounding follows the engine: conv output in f32, BN + ReLU in
-    f32, one cast to the storage dtype."""
-    from oracle import sparseconv_oracle as O
-    storage = feats.dtype
-    names = {l["name"] for l in layer_table(width, in_channels)}
-    cache = {}
-
-    def conv(x, name, k, s, relu=True):
-        c, f, b = x
-        p = params[name]
-        oc, of, ob, pairs = O.conv_forward(c, f, b, p["w"], k, s, batch_size, return_map=True)
-        if pairs is not None and s == 2:
-            cache[name] = (pairs, c, b)
-        return oc, _epi(of, p, relu), ob
-
-    def inverse(x, name, reuse):
-        pairs, fc, fb = cache[reuse]
-        of = O.inverse_forward(x[1], params[name]["w"], pairs, fc.shape[0])
-        return fc, _epi(of, params[name], True), fb
-
-    def _epi(f, p, relu, residual=None):
-        f = f.astype(np.float32)
-        if "scale" in p:
-            f = f * p["scale"] + p["shift"]
-        if residual is not None:
-            f = f + residual.astype(np.float32)
-        if relu:
-            f = np.maximum(f, 0)
-        return f.astype(storage)
-
-    def res(x, prefix, has_proj):
-        h = conv(x, prefix + ".c1", 3, 1)
-        sc = conv(x, prefix + ".proj", 1, 1, relu=False) if has_proj else x
-        c, f, b = h
-        p = params[prefix + ".c2"]
-        oc, of, ob = O.conv_forward(c, f, b, p["w"], 3, 1, batch_size)
-        return oc, _epi(of, p, True, sc[1]), ob
-
-    x = (np.asarray(coords, np.int64), feats, tuple(boundary))
-    x = conv(x, "stem.0", 3, 1)
-    x = conv(x, "stem.1", 3, 1)
-    skips = [x]
-    for i in range(1, 5):
-        x = conv(x, f"down{i}", 2, 2)
-        x = res(x, f"enc{i}.r0", f"enc{i}.r0.proj" in names)
-        x = res(x, f"enc{i}.r1", f"enc{i}.r1.proj" in names)
-        skips.append(x)
-    for j in range(1, 5):
-        x = inverse(x, f"up{j}", f"down{5 - j}")
-        sk = skips[4 - j]
-        x = (x[0], np.concatenate([x[1], sk[1]], axis=1), x[2])
-        x = res(x, f"dec{j}.r0", True)
-        x = res(x, f"dec{j}.r1", f"dec{j}.r1.proj" in names)
-    return conv(x, "head", 1, 1)

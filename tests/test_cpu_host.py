@@ -29,7 +29,7 @@ def test_library_exports_every_declared_symbol():
     for name in declared:
         assert hasattr(lib, name), name
     assert set(declared) == set(_native.exported_symbols())
-    assert lib.scb_abi_version() == 1
+    assert lib.scb_abi_version() == 2
     assert lib.scb_hash_slots(0) == 2 and lib.scb_hash_slots(5) == 16
     assert lib.scb_hash_slots(120_097) == 262_144
     assert isinstance(lib.scb_last_error(), bytes)

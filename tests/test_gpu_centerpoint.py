@@ -17,7 +17,8 @@ def sweeps():
 def test_centerpoint_encoder_matches_oracle(sweeps):
     import paper_2204_10319_b200 as sc
     from oracle import sparseconv_oracle as O
-    from paper_2204_10319_b200.centerpoint import EngineCenterPoint, forward_oracle
+    from paper_2204_10319_b200.centerpoint import EngineCenterPoint
+    from oracle.models import centerpoint_oracle as forward_oracle
     coords, feats, boundary = sweeps
     assert coords.shape[0] > 5000 and feats.shape[1] == 5
     model = EngineCenterPoint(5, 0)

@@ -26,7 +26,8 @@ def scan():
 def test_minkunet_matches_oracle(scan, width, dataflow):
     import paper_2204_10319_b200 as sc
     from oracle import sparseconv_oracle as O
-    from paper_2204_10319_b200.minkunet import EngineMinkUNet, forward_oracle
+    from paper_2204_10319_b200.minkunet import EngineMinkUNet
+    from oracle.models import minkunet_oracle as forward_oracle
     coords, feats, boundary = scan
     assert coords.shape[0] > 5000
     model = EngineMinkUNet(width, 4, 0)

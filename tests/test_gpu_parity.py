@@ -586,13 +586,12 @@ def test_async_validation_raises_at_the_next_sync(sc):
 
 
 @pytest.mark.parametrize("c_in,c_out,split", [(64, 64, None), (96, 96, None), (24, 32, None),
-                                              (256, 256, None), (48, 128, 16), (128, 96, 96)])
-def test_fused_tmem_operand_form(sc, rng, monkeypatch, c_in, c_out, split):
-    """The A-in-tensor-memory form of the implicit kernel (SCB_IC_TS=1: rows
-    loaded to registers, tcgen05.st into TMEM, tcgen05.mma A from TMEM)
-    against the oracle, with a BN + residual + ReLU epilogue and a concat
-    split inside a K chunk."""
-    monkeypatch.setenv("SCB_IC_TS", "1")
+                                              (256, 256, None), (48, 128, 16), (128, 96, 96),
+                                              (64, 256, None), (256, 128, 64)])
+def test_fused_epilogue_concat_shapes(sc, rng, c_in, c_out, split):
+    """The implicit kernel against the oracle over K-chunk widths 16/32/64,
+    C_out up to 256 (one CTA per SM), a BN + residual + ReLU epilogue and a
+    concat split inside a K chunk."""
     coords = random_coords(rng, (20, 20, 20), 0.15)
     n = coords.shape[0]
     f = O.quantize(rng.standard_normal((n, c_in)).astype(np.float32), "fp16")
@@ -615,51 +614,26 @@ def test_fused_tmem_operand_form(sc, rng, monkeypatch, c_in, c_out, split):
     assert rel_l2(out.features_numpy().astype(np.float32), want) <= 1e-2
 
 
-@pytest.mark.parametrize("c_in,c_out,split", [(32, 32, None), (96, 96, None), (24, 40, None),
-                                              (48, 64, 16), (8, 16, None)])
-def test_fused_virtual_k_form(sc, rng, monkeypatch, c_in, c_out, split):
-    """The virtual-K form of the implicit kernel (SCB_IC_VK=1: weights packed
-    [n_pad][V C_in], K chunks of 64 channels of the offset-major concatenation,
-    chunks straddling offsets) against the oracle, with BN + ReLU and a concat."""
-    monkeypatch.setenv("SCB_IC_VK", "1")
-    coords = random_coords(rng, (20, 20, 20), 0.15)
+@pytest.mark.parametrize("fused", [False, True])
+def test_k1_strided_layer_and_inverse(sc, rng, fused):
+    """K = 1, stride 2 (a volume-1 map that is NOT the identity, rows in
+    shuffled order) and its transposed inverse, staged and fused, against
+    the oracle (the fused path must read the hit matrix)."""
+    coords = random_coords(rng, (16, 16, 16), 0.2)
+    coords = coords[rng.permutation(coords.shape[0])]
     n = coords.shape[0]
-    f = O.quantize(rng.standard_normal((n, c_in)).astype(np.float32), "fp16")
-    w = rng.normal(0, 1 / np.sqrt(27 * c_in), (27, c_in, c_out)).astype(np.float32)
-    s = rng.uniform(0.8, 1.2, c_out).astype(np.float32)
-    h = rng.normal(0, 0.05, c_out).astype(np.float32)
-    _, base, _ = O.conv_forward(coords, f, (20, 20, 20), w, 3, 1)
-    want = np.maximum(base.astype(np.float32) * s + h, 0)
-    if split is None:
-        t, skip = sc.SparseTensor(coords, f, 1, (20, 20, 20)), None
-    else:
-        t = sc.SparseTensor(coords, np.ascontiguousarray(f[:, :split]), 1, (20, 20, 20))
-        skip = sc.SparseTensor(coords, np.ascontiguousarray(f[:, split:]), 1, (20, 20, 20))
-    ep = {"scale": torch.from_numpy(s).cuda(), "shift": torch.from_numpy(h).cuda(), "relu": True}
-    out = sc.sparse_conv_forward(t, sc.WeightTensor(w, 3, 3), sc.LayerSpec(3, 1, c_in, c_out),
-                                 None, None, sc.ExecOptions(dataflow="fused"), epilogue=ep,
-                                 concat=skip)
-    assert rel_l2(out.features_numpy().astype(np.float32), want) <= 1e-2
-
-
-@pytest.mark.parametrize("k,c_in", [(3, 64), (3, 256), (1, 256)])
-def test_fused_column_split(sc, rng, monkeypatch, k, c_in):
-    """C_out = 256 as two 128-column work units per row tile
-    (SCB_IC_NSPLIT=2) against the oracle, BN + residual + ReLU epilogue."""
-    monkeypatch.setenv("SCB_IC_NSPLIT", "2")
-    c_out = 256
-    coords = random_coords(rng, (20, 20, 20), 0.15)
-    n = coords.shape[0]
-    f = O.quantize(rng.standard_normal((n, c_in)).astype(np.float32), "fp16")
-    r = O.quantize(rng.standard_normal((n, c_out)).astype(np.float32), "fp16")
-    w = rng.normal(0, 1 / np.sqrt(k ** 3 * c_in), (k ** 3, c_in, c_out)).astype(np.float32)
-    s = rng.uniform(0.8, 1.2, c_out).astype(np.float32)
-    h = rng.normal(0, 0.05, c_out).astype(np.float32)
-    _, base, _ = O.conv_forward(coords, f, (20, 20, 20), w, k, 1)
-    want = np.maximum(base.astype(np.float32) * s + h + r.astype(np.float32), 0)
-    ep = {"scale": torch.from_numpy(s).cuda(), "shift": torch.from_numpy(h).cuda(),
-          "residual": sc.SparseTensor(coords, r, 1, (20, 20, 20)), "relu": True}
-    out = sc.sparse_conv_forward(sc.SparseTensor(coords, f, 1, (20, 20, 20)),
-                                 sc.WeightTensor(w, k, 3), sc.LayerSpec(k, 1, c_in, c_out), None,
-                                 None, sc.ExecOptions(dataflow="fused"), epilogue=ep)
-    assert rel_l2(out.features_numpy().astype(np.float32), want) <= 1e-2
+    f = O.quantize(rng.standard_normal((n, 16)).astype(np.float32), "fp16")
+    w1 = rng.normal(0, 0.25, (1, 16, 32)).astype(np.float32)
+    w2 = rng.normal(0, 0.2, (1, 32, 16)).astype(np.float32)
+    opts = sc.ExecOptions(dataflow="fused" if fused else "staged")
+    t = sc.SparseTensor(coords, f, 1, (16, 16, 16))
+    cache = {}
+    d = sc.sparse_conv_forward(t, sc.WeightTensor(w1, 1, 3), sc.LayerSpec(1, 2, 16, 32,
+                               reuse_key="d"), None, cache, opts)
+    oc, of, _, pairs = O.conv_forward(coords, f, (16, 16, 16), w1, 1, 2, return_map=True)
+    np.testing.assert_array_equal(d.coords_numpy(), oc)
+    assert rel_l2(d.features_numpy().astype(np.float32), of) <= 1e-2
+    u = sc.inverse_conv_forward(d, sc.WeightTensor(w2, 1, 3), sc.LayerSpec(
+        1, 1, 32, 16, transposed=True, reuse_key="d"), cache, None, opts)
+    uf = O.inverse_forward(d.features_numpy(), w2, pairs, n)
+    assert rel_l2(u.features_numpy().astype(np.float32), uf) <= 1e-2
