@@ -206,6 +206,15 @@ int32_t scb_scatter(const float* partial, int64_t ldp, const int32_t* pos, int32
                     int64_t n_out, int32_t c_out, int64_t center_row, int32_t out_dtype, void* out,
                     int64_t ld_out, const float* scale, const float* shift, const float* bias,
                     const void* residual, int32_t relu, scb_stream_t stream);
+/* scatter_accumulate for ANY plan (execution.py:183-218, kernels.py:38-50):
+ * out[k] = sum over e in [out_ptr[k], out_ptr[k+1]) of buffer[out_rows[e]],
+ * folded in that order in f32, one write per row.  Buffer in the reference's
+ * compact layout (`plan.total` rows, stride ldb).  Used where a hand-built
+ * map has several entries per (output, offset) pair, which scb_scatter's
+ * fixed-width position table cannot hold. */
+int32_t scb_scatter_csr(int32_t in_dtype, const void* buffer, int64_t ldb, const int64_t* out_ptr,
+                        const int32_t* out_rows, int64_t n_out, int32_t channels,
+                        int32_t out_dtype, void* out, int64_t ld_out, scb_stream_t stream);
 /* pointwise_apply (execution.py:554-576) on a feature matrix in place:
  * op 0 = relu, 1 = bias_add, 2 = bn_fold (scale, shift).  f32 compute, cast
  * back to the storage dtype. */

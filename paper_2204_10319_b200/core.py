@@ -79,12 +79,15 @@ def unflatten_coords(keys, boundary, batch_size: int = 1):
 class _PinnedRing:
     """Small pinned host buffers for asynchronous device->host reads of
     counts, reused round-robin (a fresh pinned allocation per read costs
-    ~0.1 ms of host time at the start of every forward).  A slot is reused
-    only after the event recorded with its last copy has completed."""
+    ~0.1 ms of host time at the start of every forward).  A slot is busy from
+    ``take`` until its consumer calls ``release`` after reading it (deferred
+    readers -- saturation warnings, async validation, the coordinate-chain
+    finisher -- may read long after the copy landed); ``take`` skips busy
+    slots and falls back to a fresh pinned buffer when all are busy."""
 
     def __init__(self, slots: int = 64, words: int = 16):
         self.buf = None
-        self.events = [None] * slots
+        self.busy = [False] * slots
         self.slots, self.words, self.next = slots, words, 0
 
     def take(self, n: int, dtype) -> torch.Tensor:
@@ -92,19 +95,29 @@ class _PinnedRing:
             return torch.empty(n, dtype=dtype, pin_memory=True)
         if self.buf is None:
             self.buf = torch.empty(self.slots * self.words, dtype=torch.int64, pin_memory=True)
-        i = self.next
-        self.next = (i + 1) % self.slots
-        ev = self.events[i]
-        if ev is not None:
-            ev.synchronize()  # (practically always done: 64 reads ago)
-        self.events[i] = None
-        return self.buf[i * self.words:(i + 1) * self.words].view(dtype)[:n]
+        for _ in range(self.slots):
+            i = self.next
+            self.next = (i + 1) % self.slots
+            if not self.busy[i]:
+                self.busy[i] = True
+                return self.buf[i * self.words:(i + 1) * self.words].view(dtype)[:n]
+        return torch.empty(n, dtype=dtype, pin_memory=True)  # every slot still unread
 
-    def record(self, t: torch.Tensor, ev) -> None:
+    def _slot(self, t: torch.Tensor):
         if self.buf is not None and t.untyped_storage().data_ptr() == \
                 self.buf.untyped_storage().data_ptr():
-            i = (t.data_ptr() - self.buf.data_ptr()) // (self.words * 8)
-            self.events[i] = ev
+            return (t.data_ptr() - self.buf.data_ptr()) // (self.words * 8)
+        return None
+
+    def record(self, t: torch.Tensor, ev) -> None:
+        """(Kept for call-site symmetry: the consumer synchronises on ``ev``
+        before reading, and ``release`` frees the slot afterwards.)"""
+
+    def release(self, t: torch.Tensor) -> None:
+        """The consumer has read ``t``: its slot may be reused."""
+        i = self._slot(t)
+        if i is not None:
+            self.busy[i] = False
 
 
 PINNED = _PinnedRing()
@@ -292,6 +305,7 @@ def flush_validation() -> None:
     for ev, host, cset in pending:
         ev.synchronize()
         dup, oob = (int(x) for x in host.tolist())
+        PINNED.release(host)
         if oob:
             c = cset.coords
             b = c[:, 0]
@@ -463,6 +477,7 @@ def flush_saturation_warnings(block: bool = False) -> None:
             ev.synchronize()
         if block or ev.query():
             n_sat = int(host.item())
+            PINNED.release(host)
             if n_sat:
                 warnings.warn(f"{n_sat} feature element(s) saturated to the fp16 range")
         else:

@@ -187,6 +187,31 @@ __global__ void __launch_bounds__(256) scatter_kernel(const float* __restrict__ 
   }
 }
 
+// General output-stationary fold over a CSR (reference
+// scatter_accumulate with any plan, execution.py:183-218): output k sums
+// buffer rows out_rows[out_ptr[k] .. out_ptr[k+1]) in that (ascending
+// buffer-row) order in f32 and writes its row once.  Unlike scatter_kernel's
+// fixed-width position table this takes any number of entries per
+// (output, offset) pair -- maps built by hand through the reference API.
+template <typename InT, typename OutT>
+__global__ void __launch_bounds__(256) scatter_csr_kernel(const InT* __restrict__ buffer,
+                                                          long long ldb,
+                                                          const long long* __restrict__ out_ptr,
+                                                          const int* __restrict__ out_rows,
+                                                          long long n_out, int c,
+                                                          OutT* __restrict__ out, long long ldo) {
+  const long long total = n_out * c;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long k = t / c;
+    const int ch = (int)(t - k * c);
+    float acc = 0.f;
+    for (long long e = __ldg(out_ptr + k), end = __ldg(out_ptr + k + 1); e < end; ++e)
+      acc += ld_f<InT>(buffer + (long long)__ldg(out_rows + e) * ldb + ch);
+    store_out<OutT>(out + k * ldo + ch, acc);
+  }
+}
+
 // ------------------------------------------------------------------ pointwise
 template <typename T>
 __global__ void pointwise_kernel(T* __restrict__ x, long long n, int c, int op,
@@ -303,6 +328,28 @@ extern "C" int32_t scb_scatter(const float* partial, int64_t ldp, const int32_t*
       scatter_kernel<__half, 1><<<nb, 256, 0, s>>>(partial, ldp, pos, volume, n_out, c_out, groups,
                                                    center_row, (__half*)out, ld_out, e);
   }
+  SCB_LAUNCHED();
+  return SCB_OK;
+}
+
+extern "C" int32_t scb_scatter_csr(int32_t in_dtype, const void* buffer, int64_t ldb,
+                                   const int64_t* out_ptr, const int32_t* out_rows, int64_t n_out,
+                                   int32_t channels, int32_t out_dtype, void* out, int64_t ld_out,
+                                   scb_stream_t stream) {
+  SCB_CHECK_ARG(in_dtype == SCB_F32 || in_dtype == SCB_F16, "dtype must be f32 or f16");
+  SCB_CHECK_ARG(out_dtype == SCB_F32 || out_dtype == SCB_F16, "dtype must be f32 or f16");
+  SCB_CHECK_ARG(channels >= 1 && ldb >= channels && ld_out >= channels, "bad row strides");
+  if (n_out == 0) return SCB_OK;
+  cudaStream_t s = as_stream(stream);
+  const int nb = blocks_for(n_out * channels, 256, 16);
+#define SCB_SC_LAUNCH(IT, OT)                                                                  \
+  scatter_csr_kernel<IT, OT><<<nb, 256, 0, s>>>((const IT*)buffer, ldb, (const long long*)out_ptr, \
+                                                out_rows, n_out, channels, (OT*)out, ld_out)
+  if (in_dtype == SCB_F32 && out_dtype == SCB_F32) SCB_SC_LAUNCH(float, float);
+  else if (in_dtype == SCB_F32) SCB_SC_LAUNCH(float, __half);
+  else if (out_dtype == SCB_F32) SCB_SC_LAUNCH(__half, float);
+  else SCB_SC_LAUNCH(__half, __half);
+#undef SCB_SC_LAUNCH
   SCB_LAUNCHED();
   return SCB_OK;
 }

@@ -304,14 +304,23 @@ def scatter_accumulate(buffer, plan: GatherScatterPlan, n_out: int,
     (execution.py:183-218): one f32 output-stationary pass on the device."""
     if order not in SCATTER_ORDERS:
         raise ValueError(f"unknown scatter order {order!r}")
-    b = _features_of(buffer).to(torch.float32)
+    b = _features_of(buffer)
     if b.shape[0] != plan.total:
         raise ValueError("buffer rows do not match the plan")
     c = b.shape[1]
+    odt = torch.float16 if np.dtype(out_dtype) == np.float16 else torch.float32
+    if plan.general:  # several entries per (output, offset): CSR fold
+        b = b.contiguous()
+        out = torch.empty((n_out, c), dtype=odt, device=b.device)
+        ptr, rows = plan.device_out_csr()
+        nat.call("scb_scatter_csr", nat.dtype_code(b.dtype), nat.ptr(b), c, nat.ptr(ptr),
+                 nat.ptr(rows), n_out, c, nat.dtype_code(odt), nat.ptr(out), c,
+                 nat.stream_handle())
+        return out
+    b = b.to(torch.float32)
     padded = torch.zeros((max(plan.rows_pad, 1), c), dtype=torch.float32, device=b.device)
     if plan.total:
         padded[plan.padded_rows(b)] = b
-    odt = torch.float16 if np.dtype(out_dtype) == np.float16 else torch.float32
     out = torch.empty((n_out, c), dtype=odt, device=b.device)
     nat.call("scb_scatter", nat.ptr(padded), c, nat.ptr(plan.pos), plan.pos.shape[1], n_out, c, -1,
              nat.dtype_code(odt), nat.ptr(out), c, None, None, None, None, 0, nat.stream_handle())
@@ -1016,8 +1025,9 @@ def sparse_conv_forward(t: SparseTensor, w: WeightTensor, spec: LayerSpec,
                                             out_cset.coords, t.boundary, t.batch_size)
     out = _run_dataflow(t.features, kmap, w, strat, schedule, symmetric, opts, center, epilogue,
                         record, cat)
-    return SparseTensor._wrap(out, t.stride * spec.stride, out_cset.boundary, t.batch_size,
-                              out_cset)
+    with _timed(timer, label, "other"):  # result assembly (reference execution.py:503-508)
+        return SparseTensor._wrap(out, t.stride * spec.stride, out_cset.boundary, t.batch_size,
+                                  out_cset)
 
 
 def inverse_conv_forward(t: SparseTensor, w: WeightTensor, spec: LayerSpec, map_cache: dict,
@@ -1044,8 +1054,11 @@ def inverse_conv_forward(t: SparseTensor, w: WeightTensor, spec: LayerSpec, map_
                                             entry.in_coords, entry.in_boundary, t.batch_size)
     out = _run_dataflow(t.features, swapped, w, strat, schedule, False, opts, None, epilogue,
                         record)
-    cset = entry.in_coordset or CoordinateSet(entry.in_coords, entry.in_boundary, t.batch_size)
-    return SparseTensor._wrap(out, entry.in_stride, tuple(entry.in_boundary), t.batch_size, cset)
+    with _timed(timer, label, "other"):  # result assembly (reference execution.py:545-550)
+        cset = entry.in_coordset or CoordinateSet(entry.in_coords, entry.in_boundary,
+                                                  t.batch_size)
+        return SparseTensor._wrap(out, entry.in_stride, tuple(entry.in_boundary), t.batch_size,
+                                  cset)
 
 
 _POINTWISE = {"relu": 0, "bias_add": 1, "bn_fold": 2}

@@ -349,7 +349,9 @@ def start_output_coords_chain(cset, steps):
         from .core import flush_validation
         flush_validation()  # asynchronous input validations queued before the chain
         out = []
-        for (keys, g, out_b, _), n in zip(levels, host.tolist()):
+        ns = host.tolist()
+        PINNED.release(host)
+        for (keys, g, out_b, _), n in zip(levels, ns):
             co = torch.empty((n, dim + 1), dtype=torch.int32, device=dev)
             nat.call("scb_unflatten", nat.ptr(keys), n, g, nat.ptr(co), nat.stream_handle())
             out.append((co, out_b))
@@ -593,9 +595,12 @@ class GatherScatterPlan:
                  nat.ptr(kmap.out_idx), V, kmap.total, self.n_out,
                  -1 if skipped is None else skipped, self.tile_rows, nat.ptr(self.buf_in),
                  self.rows_pad, nat.ptr(self.pos), nat.ptr(status), nat.stream_handle())
-        if status is not None and int(status.item()):
-            raise ValueError("kernel map has more than one entry for an (output, offset) pair")
+        # A hand-built map (reference API) may hold several entries for one
+        # (output, offset) pair; the fixed-width `pos` table cannot, so such
+        # a plan scatters through the output CSR instead (scb_scatter_csr).
+        self.general = bool(status is not None and int(status.item()))
         self._csr = None
+        self._dev_csr = None
 
     @property
     def sizes(self) -> np.ndarray:
@@ -632,6 +637,14 @@ class GatherScatterPlan:
     out_rows = property(lambda self: self._views()["out_rows"])
     in_counts = property(lambda self: np.diff(self.in_indptr))
     out_counts = property(lambda self: np.diff(self.out_indptr))
+
+    def device_out_csr(self):
+        """(out_indptr int64[n_out+1], out_rows int32[total]) on the device."""
+        if self._dev_csr is None:
+            dev = self.buf_in.device
+            self._dev_csr = (torch.from_numpy(self.out_indptr).to(dev),
+                             torch.from_numpy(self.out_rows.astype(np.int32)).to(dev))
+        return self._dev_csr
 
     def padded_rows(self, compact: torch.Tensor) -> torch.Tensor:
         """Index of each compact (reference-layout) buffer row in the padded

@@ -88,12 +88,31 @@ def _from_pairs(sc, pairs, off, n, n_out=None, stride=1):
                         n if n_out is None else n_out)
 
 
-def test_plan_rejects_duplicate_output_per_offset(sc):
-    # two entries for output 0 in the same offset cannot come from a real map
-    pairs = [np.array([[0, 0], [1, 0]], np.int64)]
+def test_plan_with_duplicate_output_per_offset(sc):
+    """A hand-built map with several entries for one (output, offset) pair
+    (the reference's scatter tests build these) cannot use the fixed-width
+    position table: the plan is marked general and scatters through the
+    output CSR (scb_scatter_csr), folding 2048 x 0.5 exactly in f32
+    (reference tests/test_execution.py::test_fp16_accumulates_in_fp32)."""
+    m = 2048
+    pairs = [np.stack([np.arange(m), np.zeros(m, np.int64)], 1)]
     off = sc.KernelOffsets(np.zeros((1, 3), np.int64), 1, 3)
-    with pytest.raises(ValueError, match="more than one entry"):
-        sc.build_gather_scatter_plan(_from_pairs(sc, pairs, off, 2, n_out=1, stride=2))
+    plan = sc.build_gather_scatter_plan(_from_pairs(sc, pairs, off, m, n_out=1, stride=2))
+    assert plan.general
+    buf = torch.full((m, 3), 0.5, dtype=torch.float16, device="cuda")
+    for order in ("weight_stationary", "output_stationary"):
+        out = sc.scatter_accumulate(buf, plan, 1, order).cpu().numpy()
+        np.testing.assert_array_equal(out, np.full((1, 3), 1024.0, np.float32))
+    # mixed: ascending buffer-row fold over a random many-to-one map
+    rng = np.random.default_rng(3)
+    k = np.sort(rng.integers(0, 5, 300))
+    pairs = [np.stack([np.arange(300), k], 1)]
+    plan = sc.build_gather_scatter_plan(_from_pairs(sc, pairs, off, 300, n_out=5, stride=2))
+    vals = rng.standard_normal((300, 7)).astype(np.float32)
+    got = sc.scatter_accumulate(torch.from_numpy(vals).cuda(), plan, 5).cpu().numpy()
+    want = np.zeros((5, 7), np.float64)
+    np.add.at(want, k, vals.astype(np.float64))
+    np.testing.assert_allclose(got, want, rtol=1e-5, atol=1e-5)
 
 
 def test_dense_block_and_worked_example(sc, golden):
