@@ -76,6 +76,9 @@ def parse():
                     help="write the per-(layer, stage) CUDA-event table (layer,stage,metric,value)")
     ap.add_argument("--dataflow", choices=("staged", "fused", "auto"), default="auto")
     ap.add_argument("--clock-ms", type=int, default=5, help="clock sampling period (0: off)")
+    ap.add_argument("--gather", choices=("host", "rank0"), default="host",
+                    help="e2e output gather: host = each rank downloads its own scans' logits "
+                         "(default); rank0 = NCCL gather of all logits to rank 0, then its D2H")
     return ap.parse_args()
 
 
@@ -645,7 +648,17 @@ def run_e2e(args, sc, model, coords, feats, boundary, B, dev, world, UNIT, out):
     import torch.distributed as dist
     h_coords = torch.from_numpy(coords.astype(np.int32)).pin_memory()
     h_feats = torch.from_numpy(feats).pin_memory()
-    h_out = torch.empty(tuple(out.features.shape), dtype=torch.float16).pin_memory()
+    rank = dist.get_rank() if world > 1 else 0
+    to_rank0 = world > 1 and args.gather == "rank0"
+    rows_per_rank = None
+    if to_rank0:  # static per rank (same scans every step): exchanged once
+        from paper_2204_10319_b200.sharding import gather_rows
+        rows_per_rank = [None] * world
+        dist.all_gather_object(rows_per_rank, int(out.features.shape[0]))
+    out_rows = sum(rows_per_rank) if (to_rank0 and rank == 0) else \
+        (0 if to_rank0 else int(out.features.shape[0]))
+    h_out = torch.empty((max(out_rows, 1), out.features.shape[1]),
+                        dtype=torch.float16).pin_memory()
     h2d_s, d2h_s = torch.cuda.Stream(), torch.cuda.Stream()
     NB = 4
     c_ring = [torch.empty(h_coords.shape, dtype=h_coords.dtype, device=dev) for _ in range(NB)]
@@ -667,10 +680,15 @@ def run_e2e(args, sc, model, coords, feats, boundary, B, dev, world, UNIT, out):
         t = sc.SparseTensor(c_ring[k], f_ring[k], 1, boundary, B, validate="async")
         t = sc.quantize_features(t, sc.PrecisionMode.FP16_STORAGE)
         o = model.forward(t, sc.ExecOptions(index_kind="hash", dataflow=args.dataflow))
+        res = o.features
+        if to_rank0:  # the path's one data collective: NCCL gather to rank 0
+            blocks = gather_rows(res, rows_per_rank, 0)
+            res = torch.cat(blocks) if blocks is not None else None
         done[k] = cur.record_event()
         d2h_s.wait_event(done[k])
         with torch.cuda.stream(d2h_s):
-            h_out.copy_(o.features, non_blocking=True)
+            if res is not None:
+                h_out[: res.shape[0]].copy_(res, non_blocking=True)
             pending.append((o, d2h_s.record_event()))
         while len(pending) > 3:
             pending.popleft()[1].synchronize()
@@ -704,7 +722,10 @@ def run_e2e(args, sc, model, coords, feats, boundary, B, dev, world, UNIT, out):
         dist.all_reduce(nb)
     return {"value": float(nb) * args.steps / float(es), "unit": UNIT,
             "h2d_bytes_per_step": int(h_coords.numel() * 4 + h_feats.numel() * 4),
-            "d2h_bytes_per_step": int(h_out.numel() * 2),
+            "d2h_bytes_per_step": int(out_rows * out.features.shape[1] * 2),
+            "output_gather": ("NCCL gather of every rank's logits to rank 0, then rank 0's D2H"
+                              if to_rank0 else "each rank's logits D2H to its own pinned host "
+                              "buffer (no collective)"),
             "host_issue_ms": e_host, "warmup_steps_run": warm_e,
             "cuda_mallocs_in_timed_steps":
                 torch.cuda.memory_stats(dev).get("segment.all.allocated", 0) - seg_e,

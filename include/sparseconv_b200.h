@@ -298,6 +298,19 @@ int32_t scb_conv_implicit_cat(const void* features, int64_t ldf, int32_t c_split
                               int32_t c_out, void* out, int64_t ldo, const float* scale,
                               const float* shift, const float* bias, const void* residual,
                               int32_t relu, scb_stream_t stream);
+/* scb_conv_implicit_cat with the launch shape chosen by the caller (the
+ * strategy files of autotune.tune_fused_layer): `ctas_per_sm` 1..3 co-resident
+ * CTAs per SM (clamped to what TMEM allows; 0 = auto) and `stage_kb` the
+ * target pipeline-stage size in KB, which sets the kernel offsets per stage
+ * (0 = auto).  Results are identical for every shape. */
+int32_t scb_conv_implicit_tuned(const void* features, int64_t ldf, int32_t c_split,
+                                const void* features2, int64_t ldf2, int64_t n_in, int32_t c_in,
+                                const int32_t* hits, int32_t volume, int64_t n_out,
+                                const uint32_t* tile_mask, const void* weights_packed,
+                                int32_t c_out, void* out, int64_t ldo, const float* scale,
+                                const float* shift, const float* bias, const void* residual,
+                                int32_t relu, int32_t ctas_per_sm, int32_t stage_kb,
+                                scb_stream_t stream);
 
 /* Active-offset words of a hit matrix per 128-row output tile: bit n of
  * masks[t] is set when some row k in [128 t, 128 t + 128) has
@@ -364,6 +377,18 @@ int32_t scb_voxelize(const double* points, int64_t n_points, int32_t cols, int32
                      double voxel_size, int32_t reduce_first, void* workspace, int64_t ws_bytes,
                      int32_t* out_coords, float* out_features, int64_t* meta,
                      scb_stream_t stream);
+/* A batch of raw scans in one pass: scan b is points [scan_ptr[b],
+ * scan_ptr[b+1]) (device int64 [n_scans+1], n_scans <= 64), voxelised
+ * exactly as voxelize (core.py:174-216) voxelises it alone (its own min
+ * corner), with batch column b; the boundary in `meta` is the per-dimension
+ * max over the scans.  Rows ascend by (b, flat key): bit-identical to B
+ * scb_voxelize calls concatenated with a shared boundary.
+ * Workspace: scb_voxelize_workspace(n_points, spatial_dims). */
+int32_t scb_voxelize_batch(const double* points, const int64_t* scan_ptr, int32_t n_scans,
+                           int64_t n_points, int32_t cols, int32_t spatial_dims,
+                           double voxel_size, int32_t reduce_first, void* workspace,
+                           int64_t ws_bytes, int32_t* out_coords, float* out_features,
+                           int64_t* meta, scb_stream_t stream);
 
 #ifdef __cplusplus
 }

@@ -59,6 +59,8 @@ _SIGS = {
     "scb_unflatten": (_I32, [_P, _I64, _GP, _P, _P]),
     "scb_voxelize_workspace": (_I64, [_I64, _I32]),
     "scb_voxelize": (_I32, [_P, _I64, _I32, _I32, ctypes.c_double, _I32, _P, _I64, _P, _P, _P, _P]),
+    "scb_voxelize_batch": (_I32, [_P, _P, _I32, _I64, _I32, _I32, ctypes.c_double, _I32, _P, _I64,
+                                  _P, _P, _P, _P]),
     "scb_map_search": (_I32, [_I32, _P, _I64, _GP, _I32, _I32, _I32, _I32, _P, _P, _I64, _P, _P]),
     "scb_map_workspace": (_I64, [_I32, _I64]),
     "scb_map_count": (_I32, [_P, _I32, _I64, _P, _P, _P]),
@@ -87,6 +89,8 @@ _SIGS = {
                                  _P, _I32, _P]),
     "scb_conv_implicit_cat": (_I32, [_P, _I64, _I32, _P, _I64, _I64, _I32, _P, _I32, _I64, _P,
                                      _P, _I32, _P, _I64, _P, _P, _P, _P, _I32, _P]),
+    "scb_conv_implicit_tuned": (_I32, [_P, _I64, _I32, _P, _I64, _I64, _I32, _P, _I32, _I64, _P,
+                                       _P, _I32, _P, _I64, _P, _P, _P, _P, _I32, _I32, _I32, _P]),
     "scb_tile_masks": (_I32, [_P, _I32, _I64, _P, _P]),
     "scb_presence_masks": (_I32, [_I32, _P, _I64, _GP, _I32, _I32, _P, _P, _I64, _P, _P, _P]),
     "scb_mask_sort_workspace": (_I64, [_I64]),

@@ -439,6 +439,63 @@ def voxelize(points, voxel_size: float, reduce: str = "mean",
     return SparseTensor._wrap(feats[:nv], 1, boundary, 1, cset)
 
 
+def voxelize_batch(scans, voxel_size: float, reduce: str = "mean",
+                   spatial_dims: int = 3) -> SparseTensor:
+    """B raw scans -> one packed SparseTensor on the device in one pass
+    (``scb_voxelize_batch``; B200 extension of reference core.py:174-216):
+    scan b is voxelised exactly as :func:`voxelize` voxelises it alone (its
+    own min corner, f64 cells and means), its rows get batch column b, and
+    the boundary is the per-dimension max over the scans — bit-identical to
+    B ``voxelize`` calls packed along the batch column.
+    ``scans``: a list of (n_b, cols) arrays or tensors (host or device), or
+    one (n, cols) tensor plus ``scans=(points, scan_ptr)``.  One host read
+    (voxel count and boundary)."""
+    if isinstance(scans, tuple) and len(scans) == 2 and isinstance(scans[0], torch.Tensor):
+        p = scans[0].to(device=_device(), dtype=torch.float64).contiguous()
+        ptr = torch.as_tensor(scans[1], dtype=torch.int64).to(p.device)
+        B = int(ptr.shape[0]) - 1
+    else:
+        parts = [torch.as_tensor(np.asarray(x, dtype=np.float64)) if not isinstance(x, torch.Tensor)
+                 else x.to(torch.float64) for x in scans]
+        if not parts:
+            raise ValueError("empty cloud")
+        cols = {int(x.shape[1]) if x.ndim == 2 else -1 for x in parts}
+        if len(cols) != 1 or -1 in cols:
+            raise ValueError("every scan must be an (n, cols) array with the same columns")
+        if any(x.shape[0] == 0 for x in parts):
+            raise ValueError("empty cloud")
+        B = len(parts)
+        sizes = np.array([0] + [int(x.shape[0]) for x in parts], dtype=np.int64)
+        ptr = torch.from_numpy(np.cumsum(sizes)).to(_device())
+        p = torch.cat([x.cpu() if not x.is_cuda else x for x in parts]).to(_device()).contiguous() \
+            if not all(x.is_cuda for x in parts) else torch.cat(parts).contiguous()
+    if not 1 <= B <= 64:
+        raise ValueError("1..64 scans per batch")
+    if p.ndim != 2 or p.shape[0] == 0:
+        raise ValueError("empty cloud")
+    if p.shape[1] < spatial_dims:
+        raise ValueError(f"points need at least {spatial_dims} columns")
+    if voxel_size <= 0:
+        raise ValueError("voxel_size must be positive")
+    if reduce not in ("mean", "first"):
+        raise ValueError(f"unknown reduce {reduce!r}")
+    n, cols = p.shape
+    lib = nat.load()
+    ws = torch.empty(int(lib.scb_voxelize_workspace(n, spatial_dims)), dtype=torch.uint8,
+                     device=p.device)
+    coords = torch.empty((n, 1 + spatial_dims), dtype=torch.int32, device=p.device)
+    feats = torch.empty((n, cols - spatial_dims), dtype=torch.float32, device=p.device)
+    meta = torch.empty(1 + spatial_dims, dtype=torch.int64, device=p.device)
+    nat.call("scb_voxelize_batch", nat.ptr(p), nat.ptr(ptr), B, n, cols, spatial_dims,
+             float(voxel_size), int(reduce == "first"), nat.ptr(ws), ws.numel(), nat.ptr(coords),
+             nat.ptr(feats) if feats.numel() else None, nat.ptr(meta), nat.stream_handle())
+    m = meta.tolist()
+    nv = int(m[0])
+    boundary = tuple(int(b) for b in m[1:])
+    cset = CoordinateSet(coords[:nv], boundary, B)
+    return SparseTensor._wrap(feats[:nv], 1, boundary, B, cset)
+
+
 def quantize_features(t: SparseTensor, mode: PrecisionMode) -> SparseTensor:
     """Convert feature storage precision (reference core.py:219-238): FP16
     rounds to nearest and saturates to +-65504 with a warning."""

@@ -62,6 +62,7 @@ struct Params {
   int epi_bufs;             // epilogue staging buffers per warp (1 or 2)
   int nacc;                 // TMEM accumulator buffers (2: epilogue overlaps the next tile)
   int interleave;           // tile order: 1 = t = blockIdx + i * gridDim, 0 = contiguous ranges
+  int l1_alloc;             // A gathers through L1 (cp.async.ca) instead of L2 only (.cg)
   uint32_t all_bits;        // (1 << V) - 1
   uint32_t idesc, tmem_cols;
   uint32_t a_off_bytes;     // one offset's A block [128 rows][kc] (1024-aligned)
@@ -371,10 +372,16 @@ __global__ void __launch_bounds__(64 + NPROD + 128, MINB)
             for (int it = 0; it < IT; ++it) {
               const int j = live_c ? jj[it] : -1;
               const uint64_t src = fb + (uint64_t)(uint32_t)max(j, 0) * (uint64_t)ldb;
-              asm volatile(
-                  "{ .reg .pred q; setp.lt.s32 q, %2, 0;\n"
-                  "  cp.async.cg.shared.global [%0], [%1], 16, q; }" ::"r"(blk + roff[it]),
-                  "l"(src), "r"(j) : "memory");
+              if (p.l1_alloc)  // L1-allocating: input rows recur across a tile's offsets
+                asm volatile(
+                    "{ .reg .pred q; setp.lt.s32 q, %2, 0;\n"
+                    "  cp.async.ca.shared.global [%0], [%1], 16, q; }" ::"r"(blk + roff[it]),
+                    "l"(src), "r"(j) : "memory");
+              else
+                asm volatile(
+                    "{ .reg .pred q; setp.lt.s32 q, %2, 0;\n"
+                    "  cp.async.cg.shared.global [%0], [%1], 16, q; }" ::"r"(blk + roff[it]),
+                    "l"(src), "r"(j) : "memory");
             }
           }
           cp_async_arrive_noinc(full + stage);   // fires when this thread's copies land
@@ -475,7 +482,7 @@ namespace {
 
 // Launch-invariant settings, read once per process.
 struct IcEnv {
-  int interleave, pdl, ctas_override, stage_kb;
+  int interleave, pdl, l1_alloc;
 };
 const IcEnv& ic_env() {
   static const IcEnv e = [] {
@@ -484,7 +491,7 @@ const IcEnv& ic_env() {
       return v ? atoi(v) : dflt;
     };
     return IcEnv{env_int("SCB_IC_INTERLEAVE", 1), env_int("SCB_IC_PDL", 1),
-                 env_int("SCB_IMPLICIT_CTAS", 0), env_int("SCB_IC_STAGE_KB", 0)};
+                 env_int("SCB_IC_L1", 0)};
   }();
   return e;
 }
@@ -563,15 +570,19 @@ extern "C" int32_t scb_tile_masks(const int32_t* hits, int32_t volume, int64_t n
   return SCB_OK;
 }
 
-extern "C" int32_t scb_conv_implicit_cat(const void* features, int64_t ldf, int32_t c_split,
-                                         const void* features2, int64_t ldf2, int64_t n_in,
-                                         int32_t c_in, const int32_t* hits, int32_t volume,
-                                         int64_t n_out, const uint32_t* tile_mask,
-                                         const void* weights_packed, int32_t c_out, void* out,
-                                         int64_t ldo, const float* scale, const float* shift,
-                                         const float* bias, const void* residual, int32_t relu,
-                                         scb_stream_t stream) {
+extern "C" int32_t scb_conv_implicit_tuned(const void* features, int64_t ldf, int32_t c_split,
+                                           const void* features2, int64_t ldf2, int64_t n_in,
+                                           int32_t c_in, const int32_t* hits, int32_t volume,
+                                           int64_t n_out, const uint32_t* tile_mask,
+                                           const void* weights_packed, int32_t c_out, void* out,
+                                           int64_t ldo, const float* scale, const float* shift,
+                                           const float* bias, const void* residual,
+                                           int32_t relu, int32_t ctas_per_sm, int32_t stage_kb,
+                                           scb_stream_t stream) {
   using namespace ic;
+  SCB_CHECK_ARG(ctas_per_sm >= 0 && ctas_per_sm <= 3, "ctas_per_sm must be 0 (auto) or 1..3");
+  SCB_CHECK_ARG(stage_kb == 0 || (stage_kb >= 8 && stage_kb <= 200),
+                "stage_kb must be 0 (auto) or 8..200");
   SCB_CHECK_ARG(features2 == nullptr || (c_split % 8 == 0 && c_split > 0 && c_split < c_in &&
                                          ldf2 % 8 == 0 && ldf2 * 2 < (1LL << 32)),
                 "concat split must be a positive multiple of 8 inside C_in, second stride % 8");
@@ -607,6 +618,7 @@ extern "C" int32_t scb_conv_implicit_cat(const void* features, int64_t ldf, int3
   p.epi_cols = (n_pad % 32 == 0) ? 32 : 16;
   p.relu = relu;
   p.interleave = env.interleave ? 1 : 0;
+  p.l1_alloc = env.l1_alloc ? 1 : 0;
   p.idesc = (1u << 4) | ((uint32_t)(n_pad >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
   // Two accumulators per CTA (the epilogue of tile i overlaps tile i+1).
   p.nacc = 2;
@@ -617,16 +629,16 @@ extern "C" int32_t scb_conv_implicit_cat(const void* features, int64_t ldf, int3
   // (measured 12 % faster for 64->64, slower for narrower inputs), 2
   // whenever both accumulator pairs fit, else 1.
   int ctas = (cols <= 128 && p.kc == 64) ? 3 : (cols <= 256 ? 2 : 1);
-  if (env.ctas_override > 0)
-    ctas = (env.ctas_override >= 3 && cols <= 128) ? 3 : (env.ctas_override >= 2 && cols <= 256 ? 2 : 1);
+  if (ctas_per_sm > 0)  // tuned (autotune.tune_fused_layer): clamped to what TMEM allows
+    ctas = (ctas_per_sm >= 3 && cols <= 128) ? 3 : (ctas_per_sm >= 2 && cols <= 256 ? 2 : 1);
   p.total_tiles = (int)((n_out + BM - 1) / BM);
   auto r1024 = [](uint32_t x) { return (x + 1023u) / 1024u * 1024u; };
   p.b_tx = (uint32_t)(n_pad * p.kc * 2);
   p.a_off_bytes = r1024((uint32_t)(BM * p.kc * 2));
   p.b_off_bytes = r1024(p.b_tx);
   const uint32_t op_bytes = p.a_off_bytes + p.b_off_bytes;
-  const int stage_kb = env.stage_kb > 0 ? env.stage_kb : (ctas == 3 ? 24 : (ctas == 2 ? 42 : 96));
-  int ops = (int)((uint32_t)stage_kb * 1024u / op_bytes);
+  const int skb = stage_kb > 0 ? stage_kb : (ctas == 3 ? 24 : (ctas == 2 ? 42 : 96));
+  int ops = (int)((uint32_t)skb * 1024u / op_bytes);
   ops = std::max(1, std::min(ops, std::min(MAX_OPS, volume)));
   p.ops = ops;
   p.stage_bytes = ops * op_bytes;
@@ -716,6 +728,19 @@ extern "C" int32_t scb_conv_implicit_cat(const void* features, int64_t ldf, int3
   if (rc != SCB_OK) return rc;
   SCB_LAUNCHED();
   return SCB_OK;
+}
+
+extern "C" int32_t scb_conv_implicit_cat(const void* features, int64_t ldf, int32_t c_split,
+                                         const void* features2, int64_t ldf2, int64_t n_in,
+                                         int32_t c_in, const int32_t* hits, int32_t volume,
+                                         int64_t n_out, const uint32_t* tile_mask,
+                                         const void* weights_packed, int32_t c_out, void* out,
+                                         int64_t ldo, const float* scale, const float* shift,
+                                         const float* bias, const void* residual, int32_t relu,
+                                         scb_stream_t stream) {
+  return scb_conv_implicit_tuned(features, ldf, c_split, features2, ldf2, n_in, c_in, hits,
+                                 volume, n_out, tile_mask, weights_packed, c_out, out, ldo, scale,
+                                 shift, bias, residual, relu, 0, 0, stream);
 }
 
 extern "C" int32_t scb_conv_implicit(const void* features, int64_t n_in, int32_t c_in,

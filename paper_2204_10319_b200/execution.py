@@ -182,6 +182,10 @@ class ExecOptions:
     map_reuse: bool = True
     dataflow: str = "staged"
     sync_free: bool = True
+    # B200 extension: layer label -> (CTAs per SM, stage KB) launch shape of
+    # the fused kernel, from a strategy file (autotune.tune_fused_layer);
+    # absent layers use the built-in heuristic.  Results are shape-invariant.
+    kernel_shapes: dict | None = None
 
 
     def __post_init__(self):
@@ -586,10 +590,11 @@ def _run_fused(features: torch.Tensor, kmap: KernelMap | None, w: WeightTensor,
             f = features if concat is None else torch.cat([features, concat], dim=1)
             f, ca, f2, cb = _pad_channels(f), None, None, 0
             ca = f.shape[1]
-        nat.call("scb_conv_implicit_cat", nat.ptr(f), f.shape[1], ca, nat.ptr(f2),
+        ctas, skb = (opts.kernel_shapes or {}).get(label, (0, 0))
+        nat.call("scb_conv_implicit_tuned", nat.ptr(f), f.shape[1], ca, nat.ptr(f2),
                  0 if f2 is None else f2.shape[1], f.shape[0], ca + cb, hits, volume, n_out,
                  masks, nat.ptr(packed), w.c_out, nat.ptr(out), ldo, scale, shift, bias, res,
-                 relu, nat.stream_handle())
+                 relu, int(ctas), int(skb), nat.stream_handle())
     if ldo != w.c_out:
         out = out[:, : w.c_out]  # 8-aligned rows for the TMA store; a strided view
     if opts.traffic_log is not None:

@@ -601,6 +601,8 @@ class GatherScatterPlan:
         self.general = bool(status is not None and int(status.item()))
         self._csr = None
         self._dev_csr = None
+        if self.general:  # built now: the plan holds its map only weakly
+            self.device_out_csr()
 
     @property
     def sizes(self) -> np.ndarray:

@@ -261,7 +261,74 @@ def gen_voxelize():
     np.savez_compressed(OUT / "voxelize.npz", **cases)
 
 
+def minkunet_chain_doc(width: float = 1.0) -> dict:
+    """MinkUNet's layer sequence in the reference's own JSON schema
+    (reference network.py:1-25): the 50-conv encoder/decoder with every
+    residual block written as its two k3 convs and the skip concatenations
+    dropped (the schema has neither add nor concat layers, SURVEY.md §0
+    fact 8); BN folded (bn_fold) + ReLU after every conv but the head."""
+    cs = [int(c * width) for c in (32, 32, 64, 128, 256, 256, 128, 96, 96)]
+    L = []
+
+    def conv(i, k, s, co, bn=True):
+        L.append({"id": i, "kind": "conv", "kernel_size": k, "stride": s, "out_channels": co,
+                  "index_kind": "hash"})
+        if bn:
+            L.extend([{"kind": "bn_fold", "id": i + ".bn"}, {"kind": "relu"}])
+
+    conv("stem.0", 3, 1, cs[0])
+    conv("stem.1", 3, 1, cs[0])
+    for i in range(1, 5):
+        conv(f"down{i}", 2, 2, cs[i - 1])
+        for r in ("r0", "r1"):
+            conv(f"enc{i}.{r}.c1", 3, 1, cs[i])
+            conv(f"enc{i}.{r}.c2", 3, 1, cs[i])
+    for j in range(1, 5):
+        L.append({"id": f"up{j}", "kind": "inverse_conv", "kernel_size": 2,
+                  "reuse": f"down{5 - j}", "out_channels": cs[4 + j]})
+        L.extend([{"kind": "bn_fold", "id": f"up{j}.bn"}, {"kind": "relu"}])
+        for r in ("r0", "r1"):
+            conv(f"dec{j}.{r}.c1", 3, 1, cs[4 + j])
+            conv(f"dec{j}.{r}.c2", 3, 1, cs[4 + j])
+    conv("head", 1, 1, 19, bn=False)
+    return {"name": "minkunet_chain", "in_channels": 4, "precision": "fp16", "param_seed": 7,
+            "layers": L}
+
+
+def gen_minkunet_chain():
+    """The MinkUNet-shaped chain (minkunet_chain_doc) through the unmodified
+    reference's Network.forward on a cropped raycast LiDAR scan (the bench's
+    generator, paper_2204_10319_b200.workloads), FP32 and FP16 storage:
+    output coordinates (digest) and features per precision."""
+    import json
+    sys.path.insert(0, str(OUT.parents[1]))
+    from paper_2204_10319_b200.workloads import raycast_points
+    pts = raycast_points(3)
+    keep = pts[:, 0] ** 2 + pts[:, 1] ** 2 < 5.0 ** 2       # disc around the sensor
+    pts = pts[keep]
+    pts = np.concatenate([pts[:, :3], pts], axis=1)
+    vox = sc.voxelize(pts, 0.05)
+    doc = minkunet_chain_doc(1.0)
+    cases = {"doc": np.array(json.dumps(doc)), "in": vox.coords.astype(np.int32),
+             "feat": vox.features.astype(np.float32),
+             "boundary": np.array(vox.boundary, np.int64)}
+    for prec in ("fp32", "fp16"):
+        net = sc.Network.build(sc.NetworkConfig.from_dict(dict(doc, precision=prec)))
+        out = net.forward(vox)
+        cases[f"{prec}_outc_digest"] = np.array(digest(out.coords))
+        cases[f"{prec}_outc_n"] = np.array(out.coords.shape[0])
+        cases[f"{prec}_outf"] = out.features
+    np.savez_compressed(OUT / "minkunet_chain.npz", **cases)
+    print("minkunet_chain.npz:", vox.num_points, "voxels,",
+          sum(1 for l in doc["layers"] if "conv" in l["kind"]), "conv layers")
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 1:
+        for name in sys.argv[1:]:
+            globals()[f"gen_{name}"]()
+        sys.exit(0)
+    gen_minkunet_chain()
     gen_voxelize()
     gen_maps()
     gen_layers()

@@ -140,3 +140,44 @@ def test_device_cost_models(rng):
     w = sc.WeightTensor(rng.normal(0, 0.05, (27, 32, 32)).astype(np.float32), 3, 3)
     dd = A.tune_dataflow(t, w, sc.LayerSpec(3, 1, 32, 32))
     assert dd.dataflow in ("staged", "fused") and dd.staged_seconds > 0
+
+
+@pytest.mark.gpu
+def test_tune_fused_layer_shapes_are_result_invariant():
+    """The fused kernel's launch shapes (CTAs per SM, stage size) searched
+    by tune_fused_layer give bit-identical outputs; the decision and the
+    strategy file round trip carry the chosen shape."""
+    import torch
+    import paper_2204_10319_b200 as sc
+    from paper_2204_10319_b200 import autotune as A
+    rng = np.random.default_rng(5)
+    keys = np.sort(rng.choice(40 ** 3, 30_000, replace=False))
+    c = np.stack([np.zeros_like(keys), keys // 1600, keys // 40 % 40, keys % 40], 1)
+    f = rng.standard_normal((c.shape[0], 64)).astype(np.float16)
+    t = sc.SparseTensor(c, f, 1, (40, 40, 40))
+    w = sc.WeightTensor(rng.normal(0, 0.05, (27, 64, 64)).astype(np.float32), 3, 3)
+    spec = sc.LayerSpec(3, 1, 64, 64)
+    outs = []
+    for shape in A.KERNEL_SHAPES:
+        o = sc.ExecOptions(dataflow="fused", layer_label="l", kernel_shapes={"l": shape})
+        outs.append(sc.sparse_conv_forward(t, w, spec, None, None, o).features.clone())
+    for o in outs[1:]:
+        assert torch.equal(o, outs[0])
+    d = A.tune_fused_layer(t, w, spec, sc.ExecOptions(layer_label="l"), repeats=2)
+    assert (d.ctas, d.stage_kb) in [s[:2] for s in d.tried]
+    assert d.seconds <= d.default_seconds
+
+
+def test_strategy_file_kernel_shape_round_trip(tmp_path):
+    """B200 launch shapes ride in JSON v1 as an extra per-layer "kernel"
+    object, which the reference's loader ignores (extra keys)."""
+    sf = A.StrategyFile((LayerRecord("stem.0", 0.0, 0.0, "hash", "fused", 2, 42),
+                         LayerRecord("head", 0.0, 0.0)))
+    path = tmp_path / "s.json"
+    A.save_strategy(path, sf)
+    doc = json.loads(path.read_text())
+    assert doc["layers"][0]["kernel"] == {"ctas": 2, "stage_kb": 42}
+    assert "kernel" not in doc["layers"][1]
+    back = A.load_strategy(path)
+    assert (back.layers[0].ctas, back.layers[0].stage_kb) == (2, 42)
+    assert (back.layers[1].ctas, back.layers[1].stage_kb) == (0, 0)

@@ -271,6 +271,30 @@ def test_network_toy_vs_golden(sc, golden):
         assert rel_l2(out.features_numpy(), g[f"{prec}_outf"]) <= TOL[prec]
 
 
+@pytest.mark.parametrize("prec,dataflow", [("fp32", "staged"), ("fp16", "staged"),
+                                           ("fp16", "fused")])
+def test_minkunet_chain_vs_reference_network(sc, golden, prec, dataflow):
+    """The engine's Network.forward over the MinkUNet-shaped 43-conv chain
+    in the reference's JSON schema, against the unmodified reference's own
+    Network.forward (tests/golden/minkunet_chain.npz): output coordinates
+    bit-exact (digest), features within the north-star tolerance (FP32
+    1e-4, FP16 1e-2 relative L2)."""
+    import hashlib
+    import json
+    g = golden("minkunet_chain")
+    doc = dict(json.loads(str(g["doc"])), precision=prec)
+    boundary = tuple(int(b) for b in g["boundary"])
+    net = sc.Network.build(sc.NetworkConfig.from_dict(doc))
+    out = net.forward(sc.SparseTensor(g["in"], g["feat"], 1, boundary, 1),
+                      options=sc.ExecOptions(dataflow=dataflow))
+    oc = out.coords_numpy()
+    h = hashlib.sha256()
+    h.update(str(oc.shape).encode())
+    h.update(np.ascontiguousarray(oc.astype(np.int64)).tobytes())
+    assert h.hexdigest() == str(g[f"{prec}_outc_digest"])
+    assert rel_l2(out.features_numpy(), g[f"{prec}_outf"]) <= TOL[prec]
+
+
 @pytest.mark.parametrize("prec", ["fp32", "fp16"])
 @pytest.mark.parametrize("c_in,c_out", [(64, 64), (32, 48), (16, 16), (128, 96), (4, 32)])
 def test_config1_layer_vs_oracle(sc, prec, c_in, c_out):

@@ -45,6 +45,53 @@ def test_two_rank_sharding_gloo():
     assert t == 2.5  # max over ranks
 
 
+def _orchestrate(rank, world, port, q):
+    """The bench's multi-GPU data path on CPU: a fixed batch of scans (strong
+    scaling, config 5) assigned by LPT on voxel count, each rank runs its
+    scans through a forward stub, and the per-scan outputs are gathered to
+    rank 0 -- the path's only data collective."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2204_10319_b200.sharding import gather_outputs, lpt_assign
+    sizes = [50 + 13 * ((7 * i) % 11) for i in range(12)]          # voxels per scan
+    mine = lpt_assign(sizes, world)[rank]
+
+    def forward_stub(scan):                                       # (rows, 3) logits
+        g = torch.Generator().manual_seed(scan)
+        return torch.randn((sizes[scan], 3), generator=g, dtype=torch.float16)
+
+    got = gather_outputs({s: forward_stub(s) for s in mine})
+    if rank == 0:
+        q.put({k: v.clone() for k, v in got.items()})
+    else:
+        assert got is None
+    dist.destroy_process_group()
+
+
+def test_two_rank_shard_forward_gather_gloo():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_orchestrate, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = q.get(timeout=120)
+    for p in procs:
+        p.join(60)
+        assert p.exitcode == 0
+    sizes = [50 + 13 * ((7 * i) % 11) for i in range(12)]
+    assert sorted(got) == list(range(12))
+    for s in range(12):
+        g = torch.Generator().manual_seed(s)
+        assert torch.equal(got[s], torch.randn((sizes[s], 3), generator=g, dtype=torch.float16))
+
+
+def test_gather_outputs_single_process_is_identity():
+    from paper_2204_10319_b200.sharding import gather_outputs
+    x = {3: torch.ones(2, 2)}
+    assert gather_outputs(x) == x
+
+
 def test_lpt_balances():
     from paper_2204_10319_b200.sharding import lpt_assign, shard_seeds
     a = lpt_assign([120, 130, 90, 125, 100, 110, 95, 127], 4)

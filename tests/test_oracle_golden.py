@@ -160,3 +160,25 @@ def test_voxelize_matches_reference_golden():
         assert tuple(b) == tuple(int(x) for x in g[f"v{i}_boundary"])
         i += 1
     assert i >= 6
+
+
+def test_minkunet_chain_oracle_vs_reference(golden):
+    """The MinkUNet-shaped 43-conv chain (reference JSON schema) on a
+    16k-voxel raycast crop: the oracle restatement against the unmodified
+    reference's Network.forward (tests/golden/make_golden.py
+    gen_minkunet_chain)."""
+    import hashlib
+    g = golden("minkunet_chain")
+    doc = json.loads(str(g["doc"]))
+    boundary = tuple(int(b) for b in g["boundary"])
+    for prec in ("fp32", "fp16"):
+        d = dict(doc, precision=prec)
+        oc, of = O.network_forward(d, g["in"].astype(np.int64), g["feat"], boundary)
+        h = hashlib.sha256()
+        a = np.ascontiguousarray(oc.astype(np.int64))
+        h.update(str(a.shape).encode())
+        h.update(a.tobytes())
+        assert h.hexdigest() == str(g[f"{prec}_outc_digest"])
+        ref = g[f"{prec}_outf"].astype(np.float64)
+        rel = np.linalg.norm(of.astype(np.float64) - ref) / np.linalg.norm(ref)
+        assert rel <= (1e-5 if prec == "fp32" else 5e-3), (prec, rel)

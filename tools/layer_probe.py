@@ -41,7 +41,7 @@ def main():
     opts = sc.ExecOptions(dataflow="fused", index_kind="hash")
     out = sc.sparse_conv_forward(t, w, spec, None, None, opts)
     kmap = cset.maps[(3, 1, -1)][1]
-    masks = kmap.tile_masks.cpu().numpy().astype(np.uint32)
+    masks = kmap.tile_masks().cpu().numpy().astype(np.uint32)
     live = int(sum(bin(int(m)).count("1") for m in masks))
     n = c.shape[0]
     useful = 2.0 * kmap.total * cin * cout
@@ -52,6 +52,19 @@ def main():
     while time.time() < t_end:
         out = sc.sparse_conv_forward(t, w, spec, None, None, opts)
         torch.cuda.synchronize()
+    shapes = [tuple(int(x) for x in sh.split(":")) for sh in os.environ.get("SHAPES", "").split(",")
+              if sh]
+    for sh in shapes:  # launch-shape sweep: (CTAs per SM, stage KB)
+        o2 = sc.ExecOptions(dataflow="fused", index_kind="hash", layer_label="probe",
+                            kernel_shapes={"probe": sh})
+        sc.sparse_conv_forward(t, w, spec, None, None, o2)
+        a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(reps):
+            sc.sparse_conv_forward(t, w, spec, None, None, o2)
+        b_.record()
+        torch.cuda.synchronize()
+        print(f"  shape ctas={sh[0]} stage_kb={sh[1]}: {a.elapsed_time(b_) / reps:.4f} ms", flush=True)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(reps):
@@ -62,7 +75,8 @@ def main():
     sm = torch.cuda.get_device_properties(0).multi_processor_count
     mhz = float(os.environ.get("MHZ", "1965"))
     cyc = ms * 1e-3 * mhz * 1e6 * sm / max(mmas, 1)
-    print(f"N={n} C={cin}->{cout} L{lv} reorder={os.environ.get('REORDER', '1')}: {ms:.4f} ms  "
+    print(f"N={n} C={cin}->{cout} L{lv} reorder={os.environ.get('REORDER', '1')} "
+          f"l1={os.environ.get('SCB_IC_L1', '0')}: {ms:.4f} ms  "
           f"tiles={masks.shape[0]} live_blocks={live} ({live / masks.shape[0] / 27:.3f})  "
           f"|M|/(27N)={kmap.total / 27 / n:.3f}  useful {useful / ms / 1e9:.0f} TF/s  "
           f"executed {executed / ms / 1e9:.0f} TF/s  {cyc:.0f} SM-cycles per K16 MMA", flush=True)
