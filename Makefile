@@ -17,7 +17,16 @@ build/%.o: $(CSRC)/%.cu $(CSRC)/common.cuh $(CSRC)/sm100_ptx.cuh include/sparsec
 $(LIB): $(OBJS)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJS)
 
+# per-stage timeline build of the fused conv (tools/ic_trace.py); not shipped
+TRACE_LIB := paper_2204_10319_b200/libsparseconv_b200_trace.so
+trace: $(TRACE_LIB)
+$(TRACE_LIB): $(SRCS) $(CSRC)/common.cuh $(CSRC)/sm100_ptx.cuh include/sparseconv_b200.h
+	@mkdir -p build/trace
+	for f in $(SRCS); do b=$$(basename $$f .cu); \
+	  $(NVCC) $(FLAGS) -DSCB_IC_TRACE -c $$f -o build/trace/$$b.o 2> build/trace/$$b.log || exit 1; done
+	$(NVCC) $(ARCH) -shared -o $@ build/trace/*.o
+
 clean:
 	rm -rf build $(LIB)
 
-.PHONY: all clean
+.PHONY: all clean trace

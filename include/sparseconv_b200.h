@@ -215,6 +215,12 @@ int32_t scb_scatter(const float* partial, int64_t ldp, const int32_t* pos, int32
 int32_t scb_scatter_csr(int32_t in_dtype, const void* buffer, int64_t ldb, const int64_t* out_ptr,
                         const int32_t* out_rows, int64_t n_out, int32_t channels,
                         int32_t out_dtype, void* out, int64_t ld_out, scb_stream_t stream);
+/* Small device -> pinned-host read (counts, status words) written by the SMs
+ * through the pinned buffer's host pointer (UVA-mapped) on `stream`, so it
+ * never waits behind a large DMA transfer on the copy engine; visible to
+ * the host once an event recorded after it completes.  bytes % 4 == 0,
+ * <= 1 MiB.  B200 plumbing (the reference reads numpy values directly). */
+int32_t scb_store_to_host(const void* src, void* host_dst, int64_t bytes, scb_stream_t stream);
 /* pointwise_apply (execution.py:554-576) on a feature matrix in place:
  * op 0 = relu, 1 = bias_add, 2 = bn_fold (scale, shift).  f32 compute, cast
  * back to the storage dtype. */

@@ -79,6 +79,7 @@ _SIGS = {
     "scb_scatter": (_I32, [_P, _I64, _P, _I32, _I64, _I32, _I64, _I32, _P, _I64, _P, _P, _P,
                            _P, _I32, _P]),
     "scb_scatter_csr": (_I32, [_I32, _P, _I64, _P, _P, _I64, _I32, _I32, _P, _I64, _P]),
+    "scb_store_to_host": (_I32, [_P, _P, _I64, _P]),
     "scb_pointwise": (_I32, [_I32, _P, _I64, _I32, _I32, _P, _P, _P]),
     "scb_add": (_I32, [_I32, _P, _P, _P, _I64, _I32, _P]),
     "scb_quantize_f16": (_I32, [_P, _P, _I64, _P, _P]),

@@ -103,15 +103,27 @@ class _PinnedRing:
                 return self.buf[i * self.words:(i + 1) * self.words].view(dtype)[:n]
         return torch.empty(n, dtype=dtype, pin_memory=True)  # every slot still unread
 
+    def read_async(self, src: torch.Tensor, n: int | None = None):
+        """Start a read of ``src`` (a small device tensor, 4-byte elements
+        or wider) into a pinned slot: the SMs write it through the slot's
+        host pointer (scb_store_to_host), not a DMA copy, so it never waits
+        behind a large transfer on the copy engine.  Returns (host view,
+        event); read the view after ``event.synchronize()``, then
+        ``release`` it."""
+        n = src.numel() if n is None else n
+        host = self.take(n, src.dtype)
+        src = src.contiguous()
+        nat.call("scb_store_to_host", nat.ptr(src), host.data_ptr(), n * src.element_size(),
+                 nat.stream_handle())
+        ev = torch.cuda.Event()
+        ev.record()
+        return host, ev
+
     def _slot(self, t: torch.Tensor):
         if self.buf is not None and t.untyped_storage().data_ptr() == \
                 self.buf.untyped_storage().data_ptr():
             return (t.data_ptr() - self.buf.data_ptr()) // (self.words * 8)
         return None
-
-    def record(self, t: torch.Tensor, ev) -> None:
-        """(Kept for call-site symmetry: the consumer synchronises on ``ev``
-        before reading, and ``release`` frees the slot afterwards.)"""
 
     def release(self, t: torch.Tensor) -> None:
         """The consumer has read ``t``: its slot may be reused."""
@@ -289,11 +301,7 @@ def _validate_async(cset: CoordinateSet) -> None:
     previous batch's queued work."""
     from .mapping import build_index
     idx = build_index(cset, "hash")
-    host = PINNED.take(2, torch.int32)
-    host.copy_(idx._status, non_blocking=True)
-    ev = torch.cuda.Event()
-    ev.record()
-    PINNED.record(host, ev)
+    host, ev = PINNED.read_async(idx._status, 2)
     _PENDING_VALIDATION.append((ev, host, cset))
 
 
@@ -513,11 +521,7 @@ def quantize_features(t: SparseTensor, mode: PrecisionMode) -> SparseTensor:
     # The saturation count comes back asynchronously (pinned copy + event) so
     # quantising a network input does not stall the stream; the warning is
     # raised as soon as the count is known (next engine call, or any host read).
-    host = PINNED.take(1, torch.int64)
-    host.copy_(sat, non_blocking=True)
-    ev = torch.cuda.Event()
-    ev.record()
-    PINNED.record(host, ev)
+    host, ev = PINNED.read_async(sat, 1)
     _PENDING_SATURATION.append((ev, host))
     return t.replace_features(out)
 

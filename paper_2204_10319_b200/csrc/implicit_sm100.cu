@@ -57,17 +57,18 @@ constexpr int EPI0 = 6;                 // first epilogue warp
 
 struct Params {
   long long n_out;
-  int n_in, c_in, c_out, V, n_pad, kc, n_kchunks, stages, swz, epi_cols, total_tiles, relu;
+  int n_in, c_in, c_out, V, n_pad, kc, n_kchunks, swz, epi_cols, total_tiles, relu;
   int ops;                  // active offsets per stage (small C_in -> several)
+  int a_stages, b_stages;   // ring depths: A (gathered rows) and B (weights) separately
   int epi_bufs;             // epilogue staging buffers per warp (1 or 2)
   int nacc;                 // TMEM accumulator buffers (2: epilogue overlaps the next tile)
   int interleave;           // tile order: 1 = t = blockIdx + i * gridDim, 0 = contiguous ranges
-  int l1_alloc;             // A gathers through L1 (cp.async.ca) instead of L2 only (.cg)
+  int debug;                // EXPERIMENT (SCB_IC_DEBUG): 1 = B loaded once, 2 = no A copies
   uint32_t all_bits;        // (1 << V) - 1
   uint32_t idesc, tmem_cols;
   uint32_t a_off_bytes;     // one offset's A block [128 rows][kc] (1024-aligned)
   uint32_t b_off_bytes;     // one offset's B block [n_pad][kc]   (1024-aligned)
-  uint32_t a_stage_bytes, stage_bytes;
+  uint32_t a_stage_bytes, b_stage_bytes;
   uint32_t b_tx;            // bytes one offset's B load delivers
   long long ldf, ldh;       // feature row stride, hit-matrix row stride
   const __half* feat;       // [n_in][ldf]: input channels [0, c_split)
@@ -81,6 +82,12 @@ struct Params {
   const float* bias;        // nullable
   const __half* residual;   // nullable, [n_out][c_out]
 };
+
+// Index registers a producer thread holds per offset group: ops x IT <=
+// MAX_IDX (IT = K-chunk / 8 rows per thread), for the current group and the
+// next; 8 at three CTAs per SM (64 registers per thread).
+constexpr int MAX_IDX = 16;
+__host__ __device__ constexpr int max_idx(int minb) { return minb >= 3 ? 8 : MAX_IDX; }
 
 // Active offsets of row tile t (never empty: an all-absent tile still needs
 // its accumulator zeroed, so it runs offset 0 with every row zero-filled).
@@ -110,6 +117,47 @@ __device__ __forceinline__ TileSeq tile_seq(const Params& p) {
   const int e = (int)((long long)p.total_tiles * (blockIdx.x + 1) / gridDim.x);
   return {b, 1, e};
 }
+
+// Walks the CTA's (tile, offset group) sequence: every role iterates it in
+// the same order, so stage i of every ring refers to the same work.
+struct GroupIter {
+  int t;          // current tile (>= lim: done)
+  uint32_t rem;   // active offsets of tile t not yet grouped
+  uint32_t mg;    // current group
+  bool first;     // the group is tile t's first
+  __device__ __forceinline__ void start(const Params& p, const TileSeq& ts) {
+    t = ts.t0;
+    rem = t < ts.lim ? tile_bits(p, t) : 0u;
+    mg = next_group(rem, p.ops);
+    first = true;
+  }
+  __device__ __forceinline__ void advance(const Params& p, const TileSeq& ts) {
+    first = rem == 0u;
+    if (first) {
+      t += ts.step;
+      rem = t < ts.lim ? tile_bits(p, t) : 0u;
+    }
+    mg = next_group(rem, p.ops);
+  }
+  __device__ __forceinline__ bool done(const TileSeq& ts) const { return t >= ts.lim; }
+  __device__ __forceinline__ bool last_of_tile() const { return rem == 0u; }
+};
+
+#ifdef SCB_IC_TRACE
+// Per-stage timeline of the first CTAs (tools/ic_trace.py; trace builds
+// only: make trace): [cta][stage][event] clock64 stamps, events
+//   0 producer 0 passed the empty wait (starts issuing the stage's copies)
+//   1 MMA warp passed the full wait (A + B landed)
+//   2 MMA warp committed the stage's MMAs
+constexpr int TR_CTAS = 4, TR_STAGES = 512;
+__device__ long long g_ic_trace[TR_CTAS][TR_STAGES][3];
+__device__ __forceinline__ void trace_stamp(int idx, int ev) {
+  if (blockIdx.x < TR_CTAS && idx < TR_STAGES) g_ic_trace[blockIdx.x][idx][ev] = clock64();
+}
+#define IC_TRACE(idx, ev) trace_stamp((idx), (ev))
+#else
+#define IC_TRACE(idx, ev) ((void)0)
+#endif
 
 __device__ __forceinline__ uint32_t pack_half2(float a, float b) {
   __half2 h = __floats2half2_rn(a, b);
@@ -226,13 +274,17 @@ __global__ void __launch_bounds__(64 + NPROD + 128, MINB)
   constexpr int IT = CPR;                  // chunks a producer thread copies per offset
   constexpr int SWZ = KC * 2;              // swizzle span = row bytes
   constexpr int RPI = NPROD / CPR;         // rows one warp-wide item sweep covers
+  constexpr int MI = max_idx(MINB);
+  constexpr int MAXO = MI / IT;            // offsets per stage the index registers hold
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint8_t* epi_base = smem + (size_t)p.stages * p.stage_bytes;
-  int* nbr_s = (int*)(epi_base + 4 * p.epi_bufs * EPI_BUF);      // [V][BM] neighbour rows of the tile
-  uint64_t* full = (uint64_t*)(nbr_s + V * BM);
-  uint64_t* empty = full + p.stages;
-  uint64_t* tfull = empty + p.stages;
+  uint8_t* b_base = smem + (size_t)p.a_stages * p.a_stage_bytes;
+  uint8_t* epi_base = b_base + (size_t)p.b_stages * p.b_stage_bytes;
+  uint64_t* afull = (uint64_t*)(epi_base + 4 * p.epi_bufs * EPI_BUF);
+  uint64_t* aempty = afull + p.a_stages;
+  uint64_t* bfull = aempty + p.a_stages;
+  uint64_t* bempty = bfull + p.b_stages;
+  uint64_t* tfull = bempty + p.b_stages;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
 
@@ -240,9 +292,13 @@ __global__ void __launch_bounds__(64 + NPROD + 128, MINB)
   const TileSeq ts = tile_seq(p);
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < p.stages; ++s) {
-      mbar_init(full + s, NPROD + 1);  // one async (noinc) arrive per producer + the B expect_tx
-      mbar_init(empty + s, 1);
+    for (int s = 0; s < p.a_stages; ++s) {
+      mbar_init(afull + s, NPROD);  // one async (noinc) arrive per producer thread
+      mbar_init(aempty + s, 1);
+    }
+    for (int s = 0; s < p.b_stages; ++s) {
+      mbar_init(bfull + s, 1);      // the B expect_tx arrive
+      mbar_init(bempty + s, 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull + a, 1);
@@ -270,54 +326,43 @@ __global__ void __launch_bounds__(64 + NPROD + 128, MINB)
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   if (warp == 0) {
-    // ============ B producer: the stage's weight slices via TMA
+    // ============ B producer: the stage's weight slices via TMA, own ring
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = ts.t0; t < ts.lim; t += ts.step) {
-        uint32_t rem = tile_bits(p, t);
-        while (rem) {
-          const uint32_t mg = next_group(rem, p.ops);
-          const int nv = __popc(mg);
-          for (int kk = 0; kk < p.n_kchunks; ++kk) {
-            mbar_wait_sleep(empty + stage, phase ^ 1, 32);
-            mbar_expect_tx(full + stage, nv * p.b_tx);
-            uint8_t* sb = smem + (size_t)stage * p.stage_bytes + p.a_stage_bytes;
-            uint32_t x = mg;
-            for (int o = 0; o < nv; ++o) {
-              const int n = __ffs(x) - 1;
-              x &= x - 1;
-              tma_load_2d(sb + o * p.b_off_bytes, &tmB, full + stage, kk * p.kc, n * p.n_pad);
-            }
-            if (++stage == p.stages) { stage = 0; phase ^= 1; }
+      GroupIter g;
+      for (g.start(p, ts); !g.done(ts); g.advance(p, ts)) {
+        const int nv = __popc(g.mg);
+        for (int kk = 0; kk < p.n_kchunks; ++kk) {
+          mbar_wait_sleep(bempty + stage, phase ^ 1, 32);
+          if ((p.debug & 1) && (phase || g.t != ts.t0)) {
+            mbar_arrive(bfull + stage);
+            if (++stage == p.b_stages) { stage = 0; phase ^= 1; }
+            continue;
           }
+          mbar_expect_tx(bfull + stage, nv * p.b_tx);
+          uint8_t* sb = b_base + (size_t)stage * p.b_stage_bytes;
+          uint32_t x = g.mg;
+          for (int o = 0; o < nv; ++o) {
+            const int n = __ffs(x) - 1;
+            x &= x - 1;
+            tma_load_2d(sb + o * p.b_off_bytes, &tmB, bfull + stage, kk * p.kc, n * p.n_pad);
+          }
+          if (++stage == p.b_stages) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp >= 2 && warp < EPI0) {
-    // ============ A producers.  Thread `row` prefetches the neighbour rows
-    // of output row `row` of the next tile (active offsets only) and parks
-    // them in the tile's index table.  Copies are lane-per-chunk: item `it`
-    // of thread pt is chunk (pt % CPR) of row it * RPI + pt / CPR, so
-    // consecutive lanes copy consecutive 16-B chunks of a row.
+    // ============ A producers.  Item `it` of thread pt is 16-B chunk
+    // (pt % CPR) of tile row it * RPI + pt / CPR (consecutive lanes copy
+    // consecutive chunks of a row).  The input row of every item of a group
+    // is loaded straight from the hit matrix into registers one group ahead
+    // (no shared index table, no producer barrier); each stage is one K
+    // chunk of the group's offsets, written with one cp.async per item
+    // (ignore-src zero-fill for absent neighbours), completion tracked by a
+    // noinc arrive on the stage's full barrier.
     const int pt = threadIdx.x - 64;
-    const int row = pt;
-    int nxt[V];
-    uint32_t m_next = 0;
-    auto prefetch = [&](int t) {
-      const long long k = (long long)t * BM + row;
-      const bool ok = t < ts.lim && k < p.n_out;
-      m_next = t < ts.lim ? tile_bits(p, t) : 0u;
-#pragma unroll
-      for (int n = 0; n < V; ++n)
-        nxt[n] = (ok && ((m_next >> n) & 1u))
-                     ? (p.hits ? __ldg(p.hits + (long long)n * p.ldh + k) : (int)k) : -1;
-    };
-    prefetch(ts.t0);
-    int stage = 0;
-    uint32_t phase = 0;
-    const uint32_t nb_s0 = smem_u32(nbr_s);
-    const int cr = pt / CPR, cc = pt % CPR;   // row group / chunk of this lane
+    const int cr = pt / CPR, cc = pt % CPR;
     uint32_t roff[IT];                        // smem offset of item it inside a block
 #pragma unroll
     for (int it = 0; it < IT; ++it) {
@@ -325,118 +370,144 @@ __global__ void __launch_bounds__(64 + NPROD + 128, MINB)
       const int rxr = SWZ == 128 ? (r & 7) : (SWZ == 64 ? ((r >> 1) & 3) : ((r >> 2) & 1));
       roff[it] = (uint32_t)(r * (KC * 2)) + ((uint32_t)(cc ^ rxr) << 4);
     }
+    int cur[MI], nxt[MI];
+    // input rows of group (t, mg) for this thread's items; -1 = absent
+    auto load_idx = [&](int t, uint32_t mg, int* dst) {
+      const long long r0 = (long long)t * BM + cr;
+      uint32_t x = mg;
+#pragma unroll
+      for (int o = 0; o < MAXO; ++o) {
+        const int n = x ? __ffs(x) - 1 : 0;
+        const bool on = x != 0u;
+        x &= x - 1;
+#pragma unroll
+        for (int it = 0; it < IT; ++it) {
+          const long long k = r0 + it * RPI;
+          int j = -1;
+          if (on && k < p.n_out) j = p.hits ? __ldg(p.hits + (long long)n * p.ldh + k) : (int)k;
+          dst[o * IT + it] = j;
+        }
+      }
+    };
     const uint32_t ldfb1 = (uint32_t)(p.ldf * 2);   // row strides in bytes (host-checked < 2^32)
     const uint32_t ldfb2 = (uint32_t)(p.ldf2 * 2);
-    for (int t = ts.t0; t < ts.lim; t += ts.step) {
-      const uint32_t m_cur = m_next;
-      // the table is read by other threads: rewrite it only after every
-      // producer finished the previous tile
-      asm volatile("bar.sync 1, %0;" ::"n"(NPROD) : "memory");
+    int stage = 0;
+    uint32_t phase = 0;
+#ifdef SCB_IC_TRACE
+    int nstage = 0;
+#endif
+    GroupIter g;
+    g.start(p, ts);
+    if (!g.done(ts)) load_idx(g.t, g.mg, cur);
+    while (!g.done(ts)) {
+      GroupIter gn = g;   // the next group: its rows load while this one copies
+      gn.advance(p, ts);
+      if (!gn.done(ts)) load_idx(gn.t, gn.mg, nxt);
+      const int nv = __popc(g.mg);
+      for (int kk = 0; kk < p.n_kchunks; ++kk) {
+        mbar_wait(aempty + stage, phase ^ 1);
+        if (pt == 0) IC_TRACE(nstage, 0);
+        const uint32_t dst = smem_u32(smem + (size_t)stage * p.a_stage_bytes);
+        const int col0 = kk * KC;
+        const int live = min(CPR, (p.c_in - col0) / 8);  // chunks inside C_in
+        // this lane's 8 columns come from the first or (concat) second input
+        const int col = col0 + cc * 8;
+        const bool second = p.feat2 != nullptr && col >= p.c_split;
+        const uint64_t fb = second
+            ? reinterpret_cast<uint64_t>(p.feat2) + (uint64_t)((col - p.c_split) * 2)
+            : reinterpret_cast<uint64_t>(p.feat) + (uint64_t)(col * 2);
+        const uint32_t ldb = second ? ldfb2 : ldfb1;
+        const bool live_c = cc < live;
 #pragma unroll
-      for (int n = 0; n < V; ++n)
-        if ((m_cur >> n) & 1u)
-          asm volatile("st.shared.b32 [%0], %1;" ::"r"(nb_s0 + (uint32_t)((n * BM + row) * 4)), "r"(nxt[n]) : "memory");
-      asm volatile("bar.sync 1, %0;" ::"n"(NPROD) : "memory");
-      prefetch(t + ts.step);
-      uint32_t rem = m_cur;
-      while (rem) {
-        const uint32_t mg = next_group(rem, p.ops);
-        const int nv = __popc(mg);
-        for (int kk = 0; kk < p.n_kchunks; ++kk) {
-          mbar_wait(empty + stage, phase ^ 1);
-          const uint32_t dst = smem_u32(smem + (size_t)stage * p.stage_bytes);
-          const int col0 = kk * KC;
-          const int live = min(CPR, (p.c_in - col0) / 8);  // chunks inside C_in
-          // this lane's 8 columns come from the first or (concat) second input
-          const int col = col0 + cc * 8;
-          const bool second = p.feat2 != nullptr && col >= p.c_split;
-          const uint64_t fb = second
-              ? reinterpret_cast<uint64_t>(p.feat2) + (uint64_t)((col - p.c_split) * 2)
-              : reinterpret_cast<uint64_t>(p.feat) + (uint64_t)(col * 2);
-          const uint32_t ldb = second ? ldfb2 : ldfb1;
-          const bool live_c = cc < live;
-          // Every 16-B item of the stage is written each time: a copy of a
-          // present neighbour's chunk or a zero-fill (absent neighbour, or a
-          // chunk past C_in) -- one cp.async with an ignore-src predicate.
-          uint32_t x = mg;
-          for (int o = 0; o < nv; ++o) {
-            const int n = __ffs(x) - 1;
-            x &= x - 1;
-            const uint32_t nbc = nb_s0 + (uint32_t)((n * BM + cr) * 4);
-            int jj[IT];
-#pragma unroll
-            for (int it = 0; it < IT; ++it)
-              asm volatile("ld.shared.b32 %0, [%1];" : "=r"(jj[it]) : "r"(nbc + (uint32_t)(it * RPI * 4)));
+        for (int o = 0; o < MAXO; ++o) {
+          if (o < nv && !(p.debug & 2)) {
             const uint32_t blk = dst + o * p.a_off_bytes;
 #pragma unroll
             for (int it = 0; it < IT; ++it) {
-              const int j = live_c ? jj[it] : -1;
+              const int j = live_c ? cur[o * IT + it] : -1;
               const uint64_t src = fb + (uint64_t)(uint32_t)max(j, 0) * (uint64_t)ldb;
-              if (p.l1_alloc)  // L1-allocating: input rows recur across a tile's offsets
-                asm volatile(
-                    "{ .reg .pred q; setp.lt.s32 q, %2, 0;\n"
-                    "  cp.async.ca.shared.global [%0], [%1], 16, q; }" ::"r"(blk + roff[it]),
-                    "l"(src), "r"(j) : "memory");
-              else
-                asm volatile(
-                    "{ .reg .pred q; setp.lt.s32 q, %2, 0;\n"
-                    "  cp.async.cg.shared.global [%0], [%1], 16, q; }" ::"r"(blk + roff[it]),
-                    "l"(src), "r"(j) : "memory");
+              // L2-only (.cg): an L1-allocating .ca gather measured 4-13 % slower
+              asm volatile(
+                  "{ .reg .pred q; setp.lt.s32 q, %2, 0;\n"
+                  "  cp.async.cg.shared.global [%0], [%1], 16, q; }" ::"r"(blk + roff[it]),
+                  "l"(src), "r"(j) : "memory");
             }
           }
-          cp_async_arrive_noinc(full + stage);   // fires when this thread's copies land
-          if (++stage == p.stages) { stage = 0; phase ^= 1; }
         }
+        cp_async_arrive_noinc(afull + stage);   // fires when this thread's copies land
+#ifdef SCB_IC_TRACE
+        ++nstage;
+#endif
+        if (++stage == p.a_stages) { stage = 0; phase ^= 1; }
       }
+#pragma unroll
+      for (int i = 0; i < MI; ++i) cur[i] = nxt[i];
+      g = gn;
     }
   } else if (warp == 1) {
     // ============ MMA issuer.  The whole warp runs the loop (so stage
     // indices and descriptors stay warp-uniform, in uniform registers) and
-    // one elected lane issues.
+    // one elected lane issues; each stage's MMAs release their A and B
+    // slots with one commit each.
     const uint32_t layout = p.swz == 128 ? 2u : (p.swz == 64 ? 4u : 6u);
     const uint32_t sbo = 8u * (uint32_t)p.swz;
     const uint64_t adesc_base = make_sdesc(smem_u32(smem), sbo, layout);
-    const uint32_t stage_d = p.stage_bytes >> 4, a_stage_d = p.a_stage_bytes >> 4;
+    const uint64_t bdesc_base = make_sdesc(smem_u32(b_base), sbo, layout);
+    const uint32_t a_stage_d = p.a_stage_bytes >> 4, b_stage_d = p.b_stage_bytes >> 4;
     const uint32_t a_off_d = p.a_off_bytes >> 4, b_off_d = p.b_off_bytes >> 4;
     const uint32_t idesc = p.idesc;
     const uint32_t tmem0 = __shfl_sync(0xffffffffu, tmem_base, 0);
-    int stage = 0, acc = 0;
-    uint32_t phase = 0, acc_phase = 0;
-    for (int t = ts.t0; t < ts.lim; t += ts.step) {
-      mbar_wait(tempty + acc, acc_phase ^ 1);
-      tc_after();
-      const uint32_t d = tmem0 + (uint32_t)acc * (uint32_t)p.n_pad;
-      uint32_t rem = tile_bits(p, t);
-      uint32_t acc0 = 0u;   // the tile's first MMA overwrites the accumulator
-      while (rem) {
-        const int nv = __popc(next_group(rem, p.ops));
-        for (int kk = 0; kk < p.n_kchunks; ++kk) {
-          mbar_wait(full + stage, phase);
-          const uint64_t ad = adesc_base + (uint64_t)(stage * stage_d);
-          const uint64_t bd = ad + a_stage_d;
-          if (elect_one()) {
-            fence_async_smem();  // cp.async (generic proxy) data -> tcgen05 reads
-            tc_after();
-#pragma unroll
-            for (int o = 0; o < MAX_OPS; ++o) {
-              if (o < nv) {
-                const uint64_t a = ad + (uint64_t)(o * a_off_d);
-                const uint64_t b = bd + (uint64_t)(o * b_off_d);
-                mma_f16(d, a, b, idesc, o ? 1u : acc0);
-#pragma unroll
-                for (int k = 1; k < KC / 16; ++k) mma_f16(d, a + 2u * k, b + 2u * k, idesc, 1u);
-              }
-            }
-            mma_commit(empty + stage);
-          }
-          __syncwarp();
-          acc0 = 1u;
-          if (++stage == p.stages) { stage = 0; phase ^= 1; }
-        }
+#ifdef SCB_IC_TRACE
+    int nstage = 0;
+#endif
+    int as = 0, bs = 0, acc = 0;
+    uint32_t aph = 0, bph = 0, acc_phase = 0;
+    uint32_t d = 0, acc0 = 0;
+    GroupIter g;
+    for (g.start(p, ts); !g.done(ts); g.advance(p, ts)) {
+      if (g.first) {
+        mbar_wait(tempty + acc, acc_phase ^ 1);
+        tc_after();
+        d = tmem0 + (uint32_t)acc * (uint32_t)p.n_pad;
+        acc0 = 0u;   // the tile's first MMA overwrites the accumulator
       }
-      if (elect_one()) mma_commit(tfull + acc);
-      __syncwarp();
-      if (++acc == p.nacc) { acc = 0; acc_phase ^= 1; }
+      const int nv = __popc(g.mg);
+      for (int kk = 0; kk < p.n_kchunks; ++kk) {
+        mbar_wait(afull + as, aph);
+        mbar_wait(bfull + bs, bph);
+        if (lane == 0) IC_TRACE(nstage, 1);
+        const uint64_t ad = adesc_base + (uint64_t)(as * a_stage_d);
+        const uint64_t bd = bdesc_base + (uint64_t)(bs * b_stage_d);
+        if (elect_one()) {
+          fence_async_smem();  // cp.async (generic proxy) data -> tcgen05 reads
+          tc_after();
+#pragma unroll
+          for (int o = 0; o < MAX_OPS; ++o) {
+            if (o < nv) {
+              const uint64_t a = ad + (uint64_t)(o * a_off_d);
+              const uint64_t b = bd + (uint64_t)(o * b_off_d);
+              mma_f16(d, a, b, idesc, o ? 1u : acc0);
+#pragma unroll
+              for (int k = 1; k < KC / 16; ++k) mma_f16(d, a + 2u * k, b + 2u * k, idesc, 1u);
+            }
+          }
+          mma_commit(aempty + as);
+          mma_commit(bempty + bs);
+        }
+        __syncwarp();
+        if (lane == 0) IC_TRACE(nstage, 2);
+#ifdef SCB_IC_TRACE
+        ++nstage;
+#endif
+        acc0 = 1u;
+        if (++as == p.a_stages) { as = 0; aph ^= 1; }
+        if (++bs == p.b_stages) { bs = 0; bph ^= 1; }
+      }
+      if (g.last_of_tile()) {
+        if (elect_one()) mma_commit(tfull + acc);
+        __syncwarp();
+        if (++acc == p.nacc) { acc = 0; acc_phase ^= 1; }
+      }
     }
   } else if (warp >= EPI0) {
     epilogue_role(p, &tmOut, tmem_base, tfull, tempty, epi_base, warp, lane, ts);
@@ -482,7 +553,7 @@ namespace {
 
 // Launch-invariant settings, read once per process.
 struct IcEnv {
-  int interleave, pdl, l1_alloc;
+  int interleave, pdl, debug;
 };
 const IcEnv& ic_env() {
   static const IcEnv e = [] {
@@ -491,7 +562,7 @@ const IcEnv& ic_env() {
       return v ? atoi(v) : dflt;
     };
     return IcEnv{env_int("SCB_IC_INTERLEAVE", 1), env_int("SCB_IC_PDL", 1),
-                 env_int("SCB_IC_L1", 0)};
+                 env_int("SCB_IC_DEBUG", 0)};
   }();
   return e;
 }
@@ -558,6 +629,20 @@ int set_smem_once(K kernel, int bytes) {
 
 using namespace scb;
 
+#ifdef SCB_IC_TRACE
+// trace builds only (not part of the ABI): copy the stamp table to host
+extern "C" int32_t scb_ic_trace_read(long long* host, int64_t n) {
+  const int64_t cap = (int64_t)ic::TR_CTAS * ic::TR_STAGES * 3;
+  SCB_CUDA(cudaMemcpyFromSymbol(host, ic::g_ic_trace, sizeof(long long) * (n < cap ? n : cap)));
+  return SCB_OK;
+}
+extern "C" int32_t scb_ic_trace_clear() {
+  static long long zero[ic::TR_CTAS * ic::TR_STAGES * 3];
+  SCB_CUDA(cudaMemcpyToSymbol(ic::g_ic_trace, zero, sizeof(zero)));
+  return SCB_OK;
+}
+#endif
+
 extern "C" int32_t scb_tile_masks(const int32_t* hits, int32_t volume, int64_t n_out,
                                   uint32_t* masks, scb_stream_t stream) {
   SCB_CHECK_ARG(volume >= 1 && volume <= 32, "tile masks hold at most 32 offsets");
@@ -618,7 +703,7 @@ extern "C" int32_t scb_conv_implicit_tuned(const void* features, int64_t ldf, in
   p.epi_cols = (n_pad % 32 == 0) ? 32 : 16;
   p.relu = relu;
   p.interleave = env.interleave ? 1 : 0;
-  p.l1_alloc = env.l1_alloc ? 1 : 0;
+  p.debug = env.debug;
   p.idesc = (1u << 4) | ((uint32_t)(n_pad >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
   // Two accumulators per CTA (the epilogue of tile i overlaps tile i+1).
   p.nacc = 2;
@@ -638,10 +723,13 @@ extern "C" int32_t scb_conv_implicit_tuned(const void* features, int64_t ldf, in
   p.b_off_bytes = r1024(p.b_tx);
   const uint32_t op_bytes = p.a_off_bytes + p.b_off_bytes;
   const int skb = stage_kb > 0 ? stage_kb : (ctas == 3 ? 24 : (ctas == 2 ? 42 : 96));
+  const int it_per_op = p.kc / 8;  // index registers one offset needs per producer thread
   int ops = (int)((uint32_t)skb * 1024u / op_bytes);
-  ops = std::max(1, std::min(ops, std::min(MAX_OPS, volume)));
-  p.ops = ops;
-  p.stage_bytes = ops * op_bytes;
+  auto clamp_ops = [&]() {
+    ops = std::max(1, std::min(ops, std::min(std::min(MAX_OPS, volume),
+                                             max_idx(ctas) / it_per_op)));
+  };
+  clamp_ops();
   p.ldf = ldf;
   p.ldh = hits_ld(n_out);
   p.feat = (const __half*)features;
@@ -654,32 +742,48 @@ extern "C" int32_t scb_conv_implicit_tuned(const void* features, int64_t ldf, in
   p.shift = shift;
   p.bias = bias;
   p.residual = (const __half*)residual;
-  // shared memory: stages (A + B blocks) + epilogue staging + the tile's
-  // neighbour table + barriers
-  auto fixed_bytes = [&](int epi_bufs) {
-    return 1024 + 4 * epi_bufs * EPI_BUF + volume * BM * 4 + 40 * 8 + 64;
-  };
+  // shared memory: the A ring (gathered rows) and the B ring (weights) with
+  // their own depths -- the A ring as deep as the CTA's share allows (the
+  // gather latency is what it hides), the B ring 3 deep (L2-resident weights
+  // by TMA) -- + epilogue staging + barriers.
+  auto fixed_bytes = [&](int epi_bufs) { return 1024 + 4 * epi_bufs * EPI_BUF + 52 * 8 + 64; };
   int smem_cap = ctas == 3 ? 75 * 1024 : (ctas == 2 ? 113 * 1024 : 227 * 1024);
-  auto fit = [&](int e) { return (smem_cap - fixed_bytes(e)) / (int)p.stage_bytes; };
-  while (fit(1) < 2 && p.ops > 1) {  // fewer offsets per stage, then fewer CTAs per SM
-    --p.ops;
-    p.stage_bytes = p.ops * op_bytes;
+  int a_st = 0, b_st = 0, epi_bufs = 1;
+  auto plan = [&]() -> bool {
+    const int a_bytes = ops * (int)p.a_off_bytes, b_bytes = ops * (int)p.b_off_bytes;
+    for (int bs = 3; bs >= 2; --bs) {
+      for (int eb = 2; eb >= 1; --eb) {
+        const int as = (smem_cap - fixed_bytes(eb) - bs * b_bytes) / a_bytes;
+        // a second epilogue buffer only when it costs no A stage
+        if (eb == 2 && as < (smem_cap - fixed_bytes(1) - bs * b_bytes) / a_bytes) continue;
+        if (as >= std::max(2, bs)) {
+          a_st = std::min(as, 16);
+          b_st = bs;
+          epi_bufs = eb;
+          return true;
+        }
+      }
+    }
+    return false;
+  };
+  while (!plan()) {  // fewer offsets per stage, then fewer CTAs per SM
+    if (ops > 1) {
+      --ops;
+    } else if (ctas > 1) {
+      --ctas;
+      smem_cap = ctas == 2 ? 113 * 1024 : 227 * 1024;
+      clamp_ops();
+    } else {
+      SCB_CHECK_ARG(false, "stage does not fit in shared memory");
+    }
   }
-  if (fit(1) < 2 && ctas == 3) {
-    ctas = 2;
-    smem_cap = 113 * 1024;
-  }
-  if (fit(1) < 2 && ctas == 2) {
-    ctas = 1;
-    smem_cap = 227 * 1024;
-  }
-  // double-buffered epilogue staging unless the second buffer costs a stage
-  p.epi_bufs = fit(2) >= fit(1) ? 2 : 1;
-  p.a_stage_bytes = p.ops * p.a_off_bytes;
-  const int stages = std::min(fit(p.epi_bufs), 16);
-  SCB_CHECK_ARG(stages >= 2, "stage does not fit in shared memory");
-  p.stages = stages;
-  const int smem = fixed_bytes(p.epi_bufs) + stages * (int)p.stage_bytes;
+  p.ops = ops;
+  p.a_stages = a_st;
+  p.b_stages = b_st;
+  p.epi_bufs = epi_bufs;
+  p.a_stage_bytes = ops * p.a_off_bytes;
+  p.b_stage_bytes = ops * p.b_off_bytes;
+  const int smem = fixed_bytes(epi_bufs) + a_st * (int)p.a_stage_bytes + b_st * (int)p.b_stage_bytes;
 
   CUtensorMap mB, mO;
   std::string err;

@@ -212,6 +212,16 @@ __global__ void __launch_bounds__(256) scatter_csr_kernel(const InT* __restrict_
   }
 }
 
+// Small device -> pinned-host reads written by the SMs through the host
+// pointer (UVA-mapped pinned memory) instead of a DMA copy: the copy engine
+// may be busy with a large transfer on another stream (a batch's logits),
+// and a count the compute stream needs must not queue behind it.
+__global__ void store_to_host_kernel(const unsigned int* __restrict__ src,
+                                     volatile unsigned int* dst, long long words) {
+  for (long long i = threadIdx.x; i < words; i += blockDim.x) dst[i] = src[i];
+  __threadfence_system();
+}
+
 // ------------------------------------------------------------------ pointwise
 template <typename T>
 __global__ void pointwise_kernel(T* __restrict__ x, long long n, int c, int op,
@@ -350,6 +360,19 @@ extern "C" int32_t scb_scatter_csr(int32_t in_dtype, const void* buffer, int64_t
   else if (out_dtype == SCB_F32) SCB_SC_LAUNCH(__half, float);
   else SCB_SC_LAUNCH(__half, __half);
 #undef SCB_SC_LAUNCH
+  SCB_LAUNCHED();
+  return SCB_OK;
+}
+
+extern "C" int32_t scb_store_to_host(const void* src, void* host_dst, int64_t bytes,
+                                     scb_stream_t stream) {
+  SCB_CHECK_ARG(bytes >= 0 && bytes % 4 == 0 && bytes <= (1 << 20),
+                "bytes must be a multiple of 4, at most 1 MiB");
+  SCB_CHECK_ARG(((uintptr_t)src | (uintptr_t)host_dst) % 4 == 0, "4-byte aligned buffers");
+  if (bytes == 0) return SCB_OK;
+  store_to_host_kernel<<<1, 128, 0, as_stream(stream)>>>((const unsigned int*)src,
+                                                         (volatile unsigned int*)host_dst,
+                                                         bytes / 4);
   SCB_LAUNCHED();
   return SCB_OK;
 }

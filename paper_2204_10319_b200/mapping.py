@@ -338,11 +338,7 @@ def start_output_coords_chain(cset, steps):
     # the chain's one host read, asynchronous: the caller can queue other work
     # (e.g. the first convolutions) before calling the returned finisher
     from .core import PINNED
-    host = PINNED.take(counts.shape[0], torch.int64)
-    host.copy_(counts, non_blocking=True)
-    ready = torch.cuda.Event()
-    ready.record()
-    PINNED.record(host, ready)
+    host, ready = PINNED.read_async(counts)
 
     def finish():
         ready.synchronize()
