@@ -318,6 +318,31 @@ int32_t scb_conv_implicit_tuned(const void* features, int64_t ldf, int32_t c_spl
                                 int32_t relu, int32_t ctas_per_sm, int32_t stage_kb,
                                 scb_stream_t stream);
 
+/* scb_conv_implicit_tuned over a permutation of the output rows: tile row r
+ * computes output row out_rows[r] (nullable = identity), so `hits` and
+ * `tile_mask` are in tile-row order (scb_onehot_order) and the epilogue
+ * stores (and reads the residual at) row out_rows[r].  Lets a one-hot map
+ * (the transposed k2 s2 layer) run with one active offset per tile. */
+int32_t scb_conv_implicit_rows(const void* features, int64_t ldf, int32_t c_split,
+                               const void* features2, int64_t ldf2, int64_t n_in, int32_t c_in,
+                               const int32_t* hits, int32_t volume, int64_t n_out,
+                               const uint32_t* tile_mask, const int32_t* out_rows,
+                               const void* weights_packed, int32_t c_out, void* out, int64_t ldo,
+                               const float* scale, const float* shift, const float* bias,
+                               const void* residual, int32_t relu, int32_t ctas_per_sm,
+                               int32_t stage_kb, scb_stream_t stream);
+
+/* Row order for a one-hot hit matrix (every output row has at most one
+ * entry, e.g. the transposed map of a K = s strided layer): perm = the rows
+ * stably sorted by the offset of their entry (rows without one last),
+ * hits_out[n][r] = hits[n][perm[r]] and tile_masks[t] its 128-row tile words.
+ * B200 extension (the reference keeps output-row order); results of
+ * scb_conv_implicit_rows with out_rows = perm are unchanged. */
+int64_t scb_onehot_order_workspace(int64_t n);
+int32_t scb_onehot_order(const int32_t* hits, int32_t volume, int64_t n, void* workspace,
+                         int64_t ws_bytes, int32_t* perm, int32_t* hits_out, uint32_t* tile_masks,
+                         scb_stream_t stream);
+
 /* Active-offset words of a hit matrix per 128-row output tile: bit n of
  * masks[t] is set when some row k in [128 t, 128 t + 128) has
  * hits[n][k] >= 0.  volume <= 32.  B200 extension (no reference
@@ -341,6 +366,20 @@ int32_t scb_presence_masks(int32_t kind, const int32_t* coords, int64_t n,
                            const scb_grid_t* grid, int32_t kernel_size, int32_t offset_base,
                            const int64_t* table_keys, const int32_t* table_rows, int64_t slots,
                            uint32_t* masks, uint64_t* counts, scb_stream_t stream);
+
+/* The stride-1 map of an indexed set onto itself from its presence words
+ * (mask[k] of scb_presence_masks, in the set's row order): row k probes
+ * only the offsets its word marks present, hits[n][k] = -1 elsewhere; the
+ * same [V][hits_ld(n)] hit matrix as scb_map_search(..., symmetric=1) for
+ * odd K.  tile_masks (nullable, [ceil(n / 128)]) receives the OR of the row
+ * words of each 128-row tile — scb_tile_masks of that hit matrix.  K^D <= 32.
+ * B200 extension: half the probes of a symmetric search at LiDAR occupancy,
+ * and no tile-mask pass over the hit matrix. */
+int32_t scb_map_search_masked(int32_t kind, const int32_t* coords, int64_t n,
+                              const scb_grid_t* grid, int32_t kernel_size, int32_t offset_base,
+                              const int64_t* table_keys, const int32_t* table_rows, int64_t slots,
+                              const uint32_t* masks, int32_t* hits, uint32_t* tile_masks,
+                              scb_stream_t stream);
 
 int64_t scb_mask_sort_workspace(int64_t n);
 

@@ -92,8 +92,14 @@ _SIGS = {
                                      _P, _I32, _P, _I64, _P, _P, _P, _P, _I32, _P]),
     "scb_conv_implicit_tuned": (_I32, [_P, _I64, _I32, _P, _I64, _I64, _I32, _P, _I32, _I64, _P,
                                        _P, _I32, _P, _I64, _P, _P, _P, _P, _I32, _I32, _I32, _P]),
+    "scb_conv_implicit_rows": (_I32, [_P, _I64, _I32, _P, _I64, _I64, _I32, _P, _I32, _I64, _P,
+                                      _P, _P, _I32, _P, _I64, _P, _P, _P, _P, _I32, _I32, _I32,
+                                      _P]),
+    "scb_onehot_order_workspace": (_I64, [_I64]),
+    "scb_onehot_order": (_I32, [_P, _I32, _I64, _P, _I64, _P, _P, _P, _P]),
     "scb_tile_masks": (_I32, [_P, _I32, _I64, _P, _P]),
     "scb_presence_masks": (_I32, [_I32, _P, _I64, _GP, _I32, _I32, _P, _P, _I64, _P, _P, _P]),
+    "scb_map_search_masked": (_I32, [_I32, _P, _I64, _GP, _I32, _I32, _P, _P, _I64, _P, _P, _P, _P]),
     "scb_mask_sort_workspace": (_I64, [_I64]),
     "scb_mask_sort": (_I32, [_P, _P, _P, _I32, _I64, _I32, _I64, _P, _I64, _P, _P]),
     "scb_permute_rows": (_I32, [_P, _I64, _P, _I64, _I32, _P, _I64, _I32, _P]),

@@ -63,7 +63,7 @@ struct Params {
   int epi_bufs;             // epilogue staging buffers per warp (1 or 2)
   int nacc;                 // TMEM accumulator buffers (2: epilogue overlaps the next tile)
   int interleave;           // tile order: 1 = t = blockIdx + i * gridDim, 0 = contiguous ranges
-  int debug;                // EXPERIMENT (SCB_IC_DEBUG): 1 = B loaded once, 2 = no A copies
+  int debug;                // EXPERIMENT (SCB_IC_DEBUG): 1 = B loaded once, 2 = no A copies, 4 = no proxy fence
   uint32_t all_bits;        // (1 << V) - 1
   uint32_t idesc, tmem_cols;
   uint32_t a_off_bytes;     // one offset's A block [128 rows][kc] (1024-aligned)
@@ -81,6 +81,9 @@ struct Params {
   const float* shift;
   const float* bias;        // nullable
   const __half* residual;   // nullable, [n_out][c_out]
+  const int* orow;          // nullable: tile row r holds output row orow[r] (stored row by row)
+  long long ldo;            // output row stride (elements), for the orow stores
+  __half* out;              // output base, for the orow stores
 };
 
 // Index registers a producer thread holds per offset group: ops x IT <=
@@ -124,10 +127,13 @@ struct GroupIter {
   int t;          // current tile (>= lim: done)
   uint32_t rem;   // active offsets of tile t not yet grouped
   uint32_t mg;    // current group
+  uint32_t nmask; // the next tile's offsets, loaded a whole tile ahead (no
+                  // dependent global load at tile boundaries)
   bool first;     // the group is tile t's first
   __device__ __forceinline__ void start(const Params& p, const TileSeq& ts) {
     t = ts.t0;
     rem = t < ts.lim ? tile_bits(p, t) : 0u;
+    nmask = t + ts.step < ts.lim ? tile_bits(p, t + ts.step) : 0u;
     mg = next_group(rem, p.ops);
     first = true;
   }
@@ -135,7 +141,8 @@ struct GroupIter {
     first = rem == 0u;
     if (first) {
       t += ts.step;
-      rem = t < ts.lim ? tile_bits(p, t) : 0u;
+      rem = t < ts.lim ? nmask : 0u;
+      nmask = t + ts.step < ts.lim ? tile_bits(p, t + ts.step) : 0u;
     }
     mg = next_group(rem, p.ops);
   }
@@ -149,8 +156,10 @@ struct GroupIter {
 //   0 producer 0 passed the empty wait (starts issuing the stage's copies)
 //   1 MMA warp passed the full wait (A + B landed)
 //   2 MMA warp committed the stage's MMAs
-constexpr int TR_CTAS = 4, TR_STAGES = 512;
-__device__ long long g_ic_trace[TR_CTAS][TR_STAGES][3];
+//   3 MMA warp passed the A-full wait (before the B-full wait)
+//   4 elected MMA lane passed the proxy fence, 5 issued the stage's MMAs
+constexpr int TR_CTAS = 4, TR_STAGES = 512, TR_EV = 6;
+__device__ long long g_ic_trace[TR_CTAS][TR_STAGES][TR_EV];
 __device__ __forceinline__ void trace_stamp(int idx, int ev) {
   if (blockIdx.x < TR_CTAS && idx < TR_STAGES) g_ic_trace[blockIdx.x][idx][ev] = clock64();
 }
@@ -184,8 +193,11 @@ __device__ __forceinline__ void epilogue_role(const Params& p, const CUtensorMap
     mbar_wait_sleep(tfull + acc, acc_phase, 256);
     tc_after();
     const long long row0 = (long long)t * BM + 32 * q;
-    const long long k = row0 + lane;
-    const bool row_ok = k < p.n_out;
+    const long long r = row0 + lane;        // tile row
+    const bool row_ok = r < p.n_out;
+    // output row of this lane: the tile row itself, or orow[r] when the
+    // tiles run over a permutation of the output rows (one-hot maps)
+    const long long k = (p.orow && row_ok) ? (long long)__ldg(p.orow + r) : r;
     for (int j = 0; j < chunks && row0 < p.n_out; ++j) {
       const uint32_t taddr = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * p.n_pad + j * p.epi_cols);
       const int c0 = j * p.epi_cols;   // output column
@@ -227,6 +239,19 @@ __device__ __forceinline__ void epilogue_role(const Params& p, const CUtensorMap
       if (p.relu) {
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
+      }
+      if (p.orow) {
+        // permuted rows: each lane stores its own row's columns (16-B stores)
+        if (row_ok) {
+          uint4* dst = reinterpret_cast<uint4*>(p.out + k * p.ldo + c0);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            if (c * 8 < ncol && c0 + c * 8 < p.c_out)
+              dst[c] = make_uint4(pack_half2(v[8 * c], v[8 * c + 1]), pack_half2(v[8 * c + 2], v[8 * c + 3]),
+                                  pack_half2(v[8 * c + 4], v[8 * c + 5]), pack_half2(v[8 * c + 6], v[8 * c + 7]));
+          }
+        }
+        continue;
       }
       uint8_t* buf = bufs + nbuf * EPI_BUF;
       if (lane == 0) {
@@ -474,13 +499,15 @@ __global__ void __launch_bounds__(64 + NPROD + 128, MINB)
       const int nv = __popc(g.mg);
       for (int kk = 0; kk < p.n_kchunks; ++kk) {
         mbar_wait(afull + as, aph);
+        if (lane == 0) IC_TRACE(nstage, 3);
         mbar_wait(bfull + bs, bph);
         if (lane == 0) IC_TRACE(nstage, 1);
         const uint64_t ad = adesc_base + (uint64_t)(as * a_stage_d);
         const uint64_t bd = bdesc_base + (uint64_t)(bs * b_stage_d);
         if (elect_one()) {
-          fence_async_smem();  // cp.async (generic proxy) data -> tcgen05 reads
+          if (!(p.debug & 4)) fence_async_smem();  // cp.async (generic proxy) data -> tcgen05 reads
           tc_after();
+          IC_TRACE(nstage, 4);
 #pragma unroll
           for (int o = 0; o < MAX_OPS; ++o) {
             if (o < nv) {
@@ -491,6 +518,7 @@ __global__ void __launch_bounds__(64 + NPROD + 128, MINB)
               for (int k = 1; k < KC / 16; ++k) mma_f16(d, a + 2u * k, b + 2u * k, idesc, 1u);
             }
           }
+          IC_TRACE(nstage, 5);
           mma_commit(aempty + as);
           mma_commit(bempty + bs);
         }
@@ -632,12 +660,12 @@ using namespace scb;
 #ifdef SCB_IC_TRACE
 // trace builds only (not part of the ABI): copy the stamp table to host
 extern "C" int32_t scb_ic_trace_read(long long* host, int64_t n) {
-  const int64_t cap = (int64_t)ic::TR_CTAS * ic::TR_STAGES * 3;
+  const int64_t cap = (int64_t)ic::TR_CTAS * ic::TR_STAGES * ic::TR_EV;
   SCB_CUDA(cudaMemcpyFromSymbol(host, ic::g_ic_trace, sizeof(long long) * (n < cap ? n : cap)));
   return SCB_OK;
 }
 extern "C" int32_t scb_ic_trace_clear() {
-  static long long zero[ic::TR_CTAS * ic::TR_STAGES * 3];
+  static long long zero[ic::TR_CTAS * ic::TR_STAGES * ic::TR_EV];
   SCB_CUDA(cudaMemcpyToSymbol(ic::g_ic_trace, zero, sizeof(zero)));
   return SCB_OK;
 }
@@ -655,16 +683,17 @@ extern "C" int32_t scb_tile_masks(const int32_t* hits, int32_t volume, int64_t n
   return SCB_OK;
 }
 
-extern "C" int32_t scb_conv_implicit_tuned(const void* features, int64_t ldf, int32_t c_split,
-                                           const void* features2, int64_t ldf2, int64_t n_in,
-                                           int32_t c_in, const int32_t* hits, int32_t volume,
-                                           int64_t n_out, const uint32_t* tile_mask,
-                                           const void* weights_packed, int32_t c_out, void* out,
-                                           int64_t ldo, const float* scale, const float* shift,
-                                           const float* bias, const void* residual,
-                                           int32_t relu, int32_t ctas_per_sm, int32_t stage_kb,
-                                           scb_stream_t stream) {
+extern "C" int32_t scb_conv_implicit_rows(const void* features, int64_t ldf, int32_t c_split,
+                                          const void* features2, int64_t ldf2, int64_t n_in,
+                                          int32_t c_in, const int32_t* hits, int32_t volume,
+                                          int64_t n_out, const uint32_t* tile_mask,
+                                          const int32_t* out_rows, const void* weights_packed,
+                                          int32_t c_out, void* out, int64_t ldo, const float* scale,
+                                          const float* shift, const float* bias,
+                                          const void* residual, int32_t relu, int32_t ctas_per_sm,
+                                          int32_t stage_kb, scb_stream_t stream) {
   using namespace ic;
+  SCB_CHECK_ARG(out_rows == nullptr || hits != nullptr, "permuted output rows need a hit matrix");
   SCB_CHECK_ARG(ctas_per_sm >= 0 && ctas_per_sm <= 3, "ctas_per_sm must be 0 (auto) or 1..3");
   SCB_CHECK_ARG(stage_kb == 0 || (stage_kb >= 8 && stage_kb <= 200),
                 "stage_kb must be 0 (auto) or 8..200");
@@ -742,6 +771,9 @@ extern "C" int32_t scb_conv_implicit_tuned(const void* features, int64_t ldf, in
   p.shift = shift;
   p.bias = bias;
   p.residual = (const __half*)residual;
+  p.orow = out_rows;
+  p.ldo = ldo;
+  p.out = (__half*)out;
   // shared memory: the A ring (gathered rows) and the B ring (weights) with
   // their own depths -- the A ring as deep as the CTA's share allows (the
   // gather latency is what it hides), the B ring 3 deep (L2-resident weights
@@ -832,6 +864,20 @@ extern "C" int32_t scb_conv_implicit_tuned(const void* features, int64_t ldf, in
   if (rc != SCB_OK) return rc;
   SCB_LAUNCHED();
   return SCB_OK;
+}
+
+extern "C" int32_t scb_conv_implicit_tuned(const void* features, int64_t ldf, int32_t c_split,
+                                           const void* features2, int64_t ldf2, int64_t n_in,
+                                           int32_t c_in, const int32_t* hits, int32_t volume,
+                                           int64_t n_out, const uint32_t* tile_mask,
+                                           const void* weights_packed, int32_t c_out, void* out,
+                                           int64_t ldo, const float* scale, const float* shift,
+                                           const float* bias, const void* residual,
+                                           int32_t relu, int32_t ctas_per_sm, int32_t stage_kb,
+                                           scb_stream_t stream) {
+  return scb_conv_implicit_rows(features, ldf, c_split, features2, ldf2, n_in, c_in, hits, volume,
+                                n_out, tile_mask, nullptr, weights_packed, c_out, out, ldo, scale,
+                                shift, bias, residual, relu, ctas_per_sm, stage_kb, stream);
 }
 
 extern "C" int32_t scb_conv_implicit_cat(const void* features, int64_t ldf, int32_t c_split,

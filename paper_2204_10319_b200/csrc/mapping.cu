@@ -145,18 +145,28 @@ static int cand_per_input(int dim, int K, int s) {
 // Fused stages 1-4 of the downsampling pipeline (mapping.py:237-247): every
 // input proposes u = p - delta per offset, kept iff u % s == 0, 0 <= u and
 // u < s * b_out; survivors are flattened over the output grid.  Empty slots
-// get the sentinel (total output cells), which sorts last.
-template <int D>
-__global__ void out_candidates_kernel(const int* __restrict__ coords, long long n, Grid gout,
-                                      int K, int lo, int s, int cap, unsigned long long sentinel,
-                                      unsigned long long* __restrict__ cand) {
-  const int V = [&] { int v = 1; for (int d = 0; d < D; ++d) v *= K; return v; }();
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x) {
-    int p[D + 1];
+// get the sentinel (total output cells), which sorts last.  KT: the key type
+// the candidates are sorted in (32-bit whenever the sentinel fits).
+template <int D, typename KT>
+__device__ __forceinline__ void propose(const int* p, const Grid& gout, int K, int lo, int s,
+                                       int cap, KT sentinel, KT* __restrict__ out) {
+  int w = 0;
+  if (K == s) {
+    // one candidate per input: per dimension the single delta in
+    // [lo, lo + K) with (p - delta) % s == 0
+    bool keep = true;
+    long long key = p[0];
 #pragma unroll
-    for (int d = 0; d <= D; ++d) p[d] = coords[i * (D + 1) + d];
-    int w = 0;
+    for (int d = 0; d < D; ++d) {
+      int r = (p[d + 1] - lo) % s;
+      r += r < 0 ? s : 0;
+      const int u = p[d + 1] - lo - r;
+      keep = keep && u >= 0 && u < s * gout.ext[d];
+      key = key * gout.ext[d] + (u >= 0 ? u / s : 0);
+    }
+    if (keep && cap > 0) out[w++] = (KT)key;
+  } else {
+    const int V = [&] { int v = 1; for (int d = 0; d < D; ++d) v *= K; return v; }();
     for (int o = 0; o < V; ++o) {
       int delta[D];
       offset_of<D>(o, K, lo, delta);
@@ -168,9 +178,22 @@ __global__ void out_candidates_kernel(const int* __restrict__ coords, long long 
         keep = keep && u >= 0 && (u % s) == 0 && u < s * gout.ext[d];
         key = key * gout.ext[d] + (u >= 0 ? u / s : 0);
       }
-      if (keep && w < cap) cand[i * cap + (w++)] = (unsigned long long)key;
+      if (keep && w < cap) out[w++] = (KT)key;
     }
-    for (; w < cap; ++w) cand[i * cap + w] = sentinel;
+  }
+  for (; w < cap; ++w) out[w] = sentinel;
+}
+
+template <int D, typename KT>
+__global__ void out_candidates_kernel(const int* __restrict__ coords, long long n, Grid gout,
+                                      int K, int lo, int s, int cap, KT sentinel,
+                                      KT* __restrict__ cand) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    int p[D + 1];
+#pragma unroll
+    for (int d = 0; d <= D; ++d) p[d] = coords[i * (D + 1) + d];
+    propose<D, KT>(p, gout, K, lo, s, cap, sentinel, cand + i * cap);
   }
 }
 
@@ -178,17 +201,14 @@ __global__ void out_candidates_kernel(const int* __restrict__ coords, long long 
 // grid `gin`), for the first *n_dev of n_cap rows; rows past the live count
 // propose only sentinels.  Lets a chain of strided levels run with the
 // counts on the device (one host read for the whole chain).
-template <int D>
+template <int D, typename KT>
 __global__ void out_candidates_keys_kernel(const unsigned long long* __restrict__ keys,
                                            const long long* __restrict__ n_dev, long long n_cap,
                                            Grid gin, Grid gout, int K, int lo, int s, int cap,
-                                           unsigned long long sentinel,
-                                           unsigned long long* __restrict__ cand) {
-  const int V = [&] { int v = 1; for (int d = 0; d < D; ++d) v *= K; return v; }();
+                                           KT sentinel, KT* __restrict__ cand) {
   const long long n = *n_dev;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n_cap;
        i += (long long)gridDim.x * blockDim.x) {
-    int w = 0;
     if (i < n) {
       long long r = (long long)keys[i];
       int p[D + 1];
@@ -198,26 +218,30 @@ __global__ void out_candidates_keys_kernel(const unsigned long long* __restrict_
         r /= gin.ext[d];
       }
       p[0] = (int)r;
-      for (int o = 0; o < V; ++o) {
-        int delta[D];
-        offset_of<D>(o, K, lo, delta);
-        bool keep = true;
-        long long key = p[0];
-#pragma unroll
-        for (int d = 0; d < D; ++d) {
-          const int u = p[d + 1] - delta[d];
-          keep = keep && u >= 0 && (u % s) == 0 && u < s * gout.ext[d];
-          key = key * gout.ext[d] + (u >= 0 ? u / s : 0);
-        }
-        if (keep && w < cap) cand[i * cap + (w++)] = (unsigned long long)key;
-      }
+      propose<D, KT>(p, gout, K, lo, s, cap, sentinel, cand + i * cap);
+    } else {
+      for (int w = 0; w < cap; ++w) cand[i * cap + w] = sentinel;
     }
-    for (; w < cap; ++w) cand[i * cap + w] = sentinel;
+  }
+}
+
+// Sorted unique 32-bit keys -> the int64 output keys, dropping the sentinel.
+__global__ void widen_keys_kernel(const uint32_t* __restrict__ uniq, long long* __restrict__ count,
+                                  uint32_t sentinel, unsigned long long* __restrict__ out,
+                                  long long cap) {
+  const long long c = *count;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < cap;
+       i += (long long)gridDim.x * blockDim.x) {
+    if (i < c) out[i] = uniq[i];
   }
 }
 
 __global__ void drop_sentinel_kernel(const unsigned long long* uniq, long long* count,
                                      unsigned long long sentinel) {
+  long long c = *count;
+  if (c > 0 && uniq[c - 1] == sentinel) *count = c - 1;
+}
+__global__ void drop_sentinel_kernel32(const uint32_t* uniq, long long* count, uint32_t sentinel) {
   long long c = *count;
   if (c > 0 && uniq[c - 1] == sentinel) *count = c - 1;
 }
@@ -249,6 +273,13 @@ static OutCoordWs out_coord_ws(long long n_in, int dim, int K, int s) {
                                  (unsigned long long*)nullptr, (int64_t)items, 0, 64);
   cub::DeviceSelect::Unique(nullptr, w.uniq_tmp, (unsigned long long*)nullptr,
                             (unsigned long long*)nullptr, (long long*)nullptr, (int64_t)items);
+  size_t s32 = 0, u32 = 0;
+  cub::DeviceRadixSort::SortKeys(nullptr, s32, (uint32_t*)nullptr, (uint32_t*)nullptr,
+                                 (int64_t)items, 0, 32);
+  cub::DeviceSelect::Unique(nullptr, u32, (uint32_t*)nullptr, (uint32_t*)nullptr,
+                            (long long*)nullptr, (int64_t)items);
+  w.sort_tmp = w.sort_tmp > s32 ? w.sort_tmp : s32;
+  w.uniq_tmp = w.uniq_tmp > u32 ? w.uniq_tmp : u32;
   w.sort_tmp = (w.sort_tmp + 255) / 256 * 256;
   w.uniq_tmp = (w.uniq_tmp + 255) / 256 * 256;
   w.total = 2 * w.cand_bytes + (w.sort_tmp > w.uniq_tmp ? w.sort_tmp : w.uniq_tmp);
@@ -266,6 +297,49 @@ extern "C" int64_t scb_output_coords_workspace(int64_t n_in, int32_t dim, int32_
                                                int32_t stride) {
   return (int64_t)out_coord_ws(n_in, dim, kernel_size, stride).total;
 }
+
+namespace scb {
+
+// Sort + unique the candidates (KT keys; 32-bit when the sentinel fits) into
+// the int64 out_keys with the count on the device.
+template <typename KT>
+static int32_t sort_unique(void* workspace, const OutCoordWs& w, long long items,
+                           unsigned long long sentinel, int end_bit, int64_t* out_keys,
+                           int64_t* n_out, cudaStream_t s) {
+  char* base = (char*)workspace;
+  auto* cand = (KT*)base;
+  auto* sorted = (KT*)(base + w.cand_bytes);
+  void* tmp = base + 2 * w.cand_bytes;
+  size_t tb = w.sort_tmp;
+  SCB_CUDA(cub::DeviceRadixSort::SortKeys(tmp, tb, cand, sorted, (int64_t)items, 0, end_bit, s));
+  tb = w.uniq_tmp;
+  if (sizeof(KT) == 8) {
+    SCB_CUDA(cub::DeviceSelect::Unique(tmp, tb, sorted, (KT*)out_keys, (long long*)n_out,
+                                       (int64_t)items, s));
+    drop_sentinel_kernel<<<1, 1, 0, s>>>((const unsigned long long*)out_keys, (long long*)n_out,
+                                         sentinel);
+    SCB_LAUNCHED();
+  } else {
+    KT* uniq = cand;  // the candidates are dead once sorted
+    SCB_CUDA(cub::DeviceSelect::Unique(tmp, tb, sorted, uniq, (long long*)n_out, (int64_t)items, s));
+    drop_sentinel_kernel32<<<1, 1, 0, s>>>((const uint32_t*)uniq, (long long*)n_out,
+                                           (uint32_t)sentinel);
+    SCB_LAUNCHED();
+    widen_keys_kernel<<<grid_blocks(items, 256), 256, 0, s>>>(
+        (const uint32_t*)uniq, (long long*)n_out, (uint32_t)sentinel,
+        (unsigned long long*)out_keys, items);
+    SCB_LAUNCHED();
+  }
+  return SCB_OK;
+}
+
+static int key_end_bit(unsigned long long sentinel) {
+  int end_bit = 1;
+  while (end_bit < 64 && (sentinel >> end_bit) != 0) ++end_bit;
+  return end_bit;
+}
+
+}  // namespace scb
 
 extern "C" int32_t scb_output_coords(const int32_t* in_coords, int64_t n_in,
                                      const scb_grid_t* out_grid, int32_t kernel_size,
@@ -285,24 +359,19 @@ extern "C" int32_t scb_output_coords(const int32_t* in_coords, int64_t n_in,
   const int cap = cand_per_input(g.dim, kernel_size, stride);
   const long long items = n_in * cap;
   const unsigned long long sentinel = (unsigned long long)total_cells(g);
-  int end_bit = 1;
-  while (end_bit < 64 && (sentinel >> end_bit) != 0) ++end_bit;
-  char* base = (char*)workspace;
-  auto* cand = (unsigned long long*)base;
-  auto* sorted = (unsigned long long*)(base + w.cand_bytes);
-  void* tmp = base + 2 * w.cand_bytes;
-  SCB_DISPATCH_DIM(g.dim, out_candidates_kernel<D><<<grid_blocks(n_in, 256), 256, 0, s>>>(
-                              in_coords, n_in, g, kernel_size, offset_base, stride, cap, sentinel, cand));
+  const int end_bit = key_end_bit(sentinel);
+  if (end_bit <= 32) {
+    SCB_DISPATCH_DIM(g.dim, out_candidates_kernel<D, uint32_t><<<grid_blocks(n_in, 256), 256, 0, s>>>(
+                                in_coords, n_in, g, kernel_size, offset_base, stride, cap,
+                                (uint32_t)sentinel, (uint32_t*)workspace));
+    SCB_LAUNCHED();
+    return sort_unique<uint32_t>(workspace, w, items, sentinel, end_bit, out_keys, n_out, s);
+  }
+  SCB_DISPATCH_DIM(g.dim, out_candidates_kernel<D, unsigned long long><<<grid_blocks(n_in, 256), 256, 0, s>>>(
+                              in_coords, n_in, g, kernel_size, offset_base, stride, cap, sentinel,
+                              (unsigned long long*)workspace));
   SCB_LAUNCHED();
-  size_t tb = w.sort_tmp;
-  SCB_CUDA(cub::DeviceRadixSort::SortKeys(tmp, tb, cand, sorted, (int64_t)items, 0, end_bit, s));
-  tb = w.uniq_tmp;
-  SCB_CUDA(cub::DeviceSelect::Unique(tmp, tb, sorted, (unsigned long long*)out_keys,
-                                     (long long*)n_out, (int64_t)items, s));
-  drop_sentinel_kernel<<<1, 1, 0, s>>>((const unsigned long long*)out_keys, (long long*)n_out,
-                                       sentinel);
-  SCB_LAUNCHED();
-  return SCB_OK;
+  return sort_unique<unsigned long long>(workspace, w, items, sentinel, end_bit, out_keys, n_out, s);
 }
 
 extern "C" int32_t scb_output_keys_next(const int64_t* in_keys, const int64_t* n_in_dev,
@@ -325,25 +394,21 @@ extern "C" int32_t scb_output_keys_next(const int64_t* in_keys, const int64_t* n
   const int cap = cand_per_input(g.dim, kernel_size, stride);
   const long long items = n_cap * cap;
   const unsigned long long sentinel = (unsigned long long)total_cells(g);
-  int end_bit = 1;
-  while (end_bit < 64 && (sentinel >> end_bit) != 0) ++end_bit;
-  char* base = (char*)workspace;
-  auto* cand = (unsigned long long*)base;
-  auto* sorted = (unsigned long long*)(base + w.cand_bytes);
-  void* tmp = base + 2 * w.cand_bytes;
-  SCB_DISPATCH_DIM(g.dim, out_candidates_keys_kernel<D><<<grid_blocks(n_cap, 256), 256, 0, s>>>(
+  const int end_bit = key_end_bit(sentinel);
+  if (end_bit <= 32) {
+    SCB_DISPATCH_DIM(g.dim, out_candidates_keys_kernel<D, uint32_t><<<grid_blocks(n_cap, 256), 256, 0, s>>>(
+                                (const unsigned long long*)in_keys, (const long long*)n_in_dev,
+                                n_cap, gi, g, kernel_size, offset_base, stride, cap,
+                                (uint32_t)sentinel, (uint32_t*)workspace));
+    SCB_LAUNCHED();
+    return sort_unique<uint32_t>(workspace, w, items, sentinel, end_bit, out_keys, n_out, s);
+  }
+  SCB_DISPATCH_DIM(g.dim, out_candidates_keys_kernel<D, unsigned long long><<<grid_blocks(n_cap, 256), 256, 0, s>>>(
                               (const unsigned long long*)in_keys, (const long long*)n_in_dev,
-                              n_cap, gi, g, kernel_size, offset_base, stride, cap, sentinel, cand));
+                              n_cap, gi, g, kernel_size, offset_base, stride, cap, sentinel,
+                              (unsigned long long*)workspace));
   SCB_LAUNCHED();
-  size_t tb = w.sort_tmp;
-  SCB_CUDA(cub::DeviceRadixSort::SortKeys(tmp, tb, cand, sorted, (int64_t)items, 0, end_bit, s));
-  tb = w.uniq_tmp;
-  SCB_CUDA(cub::DeviceSelect::Unique(tmp, tb, sorted, (unsigned long long*)out_keys,
-                                     (long long*)n_out, (int64_t)items, s));
-  drop_sentinel_kernel<<<1, 1, 0, s>>>((const unsigned long long*)out_keys, (long long*)n_out,
-                                       sentinel);
-  SCB_LAUNCHED();
-  return SCB_OK;
+  return sort_unique<unsigned long long>(workspace, w, items, sentinel, end_bit, out_keys, n_out, s);
 }
 
 extern "C" int32_t scb_unflatten(const int64_t* keys, int64_t n, const scb_grid_t* grid,
@@ -385,6 +450,49 @@ __global__ void map_search_kernel(int kind, const int* __restrict__ out_coords, 
     // every (j, k) in M[n]; writing it at row j of the mirror column yields
     // the reference's "sorted by new output row" order for free.
     if (symmetric && n < center && j >= 0) hits[(long long)(V - 1 - n) * hits_ld(n_out) + j] = (int)k;
+  }
+}
+
+// Stride-1 map of a set onto itself when every row's neighbour-presence word
+// is already known (scb_presence_masks, carried through the presence
+// reordering): a row probes only the offsets its word marks present (each
+// probe is a hit), writes -1 for the others without probing, and the
+// 128-row tile words (scb_tile_masks) fall out as the OR of the row words.
+// One block of 128 threads per output tile, grid-stride over tiles.
+template <int D>
+__global__ void __launch_bounds__(128) map_search_masked_kernel(
+    int kind, const int* __restrict__ coords, long long n, Grid g, int K, int lo, int V,
+    const long long* __restrict__ keys, const int* __restrict__ rows, unsigned long long smask,
+    const uint32_t* __restrict__ masks, int* __restrict__ hits, uint32_t* __restrict__ tmask) {
+  __shared__ uint32_t acc[4];
+  const long long ld = hits_ld(n);
+  const long long tiles = (n + 127) / 128;
+  for (long long t = blockIdx.x; t < tiles; t += gridDim.x) {
+    const long long k = t * 128 + threadIdx.x;
+    uint32_t m = 0;
+    if (k < n) {
+      m = __ldg(masks + k);
+      int c[D + 1];
+#pragma unroll
+      for (int d = 0; d <= D; ++d) c[d] = __ldg(coords + k * (D + 1) + d);
+      for (int v = 0; v < V; ++v) {
+        int j = -1;
+        if ((m >> v) & 1u) {
+          int delta[D], p[D + 1];
+          offset_of<D>(v, K, lo, delta);
+          p[0] = c[0];
+#pragma unroll
+          for (int d = 0; d < D; ++d) p[d + 1] = c[d + 1] + delta[d];
+          j = index_lookup<D>(kind, p, g, keys, rows, smask);
+        }
+        hits[(long long)v * ld + k] = j;
+      }
+    }
+    const uint32_t w = __reduce_or_sync(0xffffffffu, m);
+    if ((threadIdx.x & 31) == 0) acc[threadIdx.x >> 5] = w;
+    __syncthreads();
+    if (threadIdx.x == 0 && tmask) tmask[t] = acc[0] | acc[1] | acc[2] | acc[3];
+    __syncthreads();
   }
 }
 
@@ -771,6 +879,29 @@ extern "C" int32_t scb_plan_build(const int64_t* offset_ptr, const int32_t* in_i
   plan_build_kernel<<<grid_blocks(total, 256), 256, (2 * volume + 1) * sizeof(long long), s>>>(
       (const long long*)offset_ptr, in_idx, out_idx, volume, total, skip_offset, tile_rows,
       buf_in, pos, status);
+  SCB_LAUNCHED();
+  return SCB_OK;
+}
+
+extern "C" int32_t scb_map_search_masked(int32_t kind, const int32_t* coords, int64_t n,
+                                         const scb_grid_t* grid, int32_t kernel_size,
+                                         int32_t offset_base, const int64_t* table_keys,
+                                         const int32_t* table_rows, int64_t slots,
+                                         const uint32_t* masks, int32_t* hits,
+                                         uint32_t* tile_masks, scb_stream_t stream) {
+  SCB_CHECK_ARG(grid && grid->dim >= 1 && grid->dim <= 4, "bad grid");
+  SCB_CHECK_ARG(masks != nullptr && hits != nullptr, "presence masks and hits are required");
+  Grid g = to_grid(grid);
+  int V = 1;
+  for (int d = 0; d < g.dim; ++d) V *= kernel_size;
+  SCB_CHECK_ARG(V <= 32, "presence masks hold at most 32 offsets");
+  if (n == 0) return SCB_OK;
+  const long long tiles = (n + 127) / 128;
+  const int blocks = (int)(tiles < 148 * 16 ? tiles : 148 * 16);
+  SCB_DISPATCH_DIM(g.dim, map_search_masked_kernel<D><<<blocks, 128, 0, as_stream(stream)>>>(
+                              kind, coords, n, g, kernel_size, offset_base, V,
+                              (const long long*)table_keys, table_rows,
+                              (unsigned long long)(slots - 1), masks, hits, tile_masks));
   SCB_LAUNCHED();
   return SCB_OK;
 }

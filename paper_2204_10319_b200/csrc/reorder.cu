@@ -140,6 +140,47 @@ __global__ void relabel_kernel(const long long* __restrict__ keys, const int* __
   }
 }
 
+// One-hot maps (every output row has at most one entry, e.g. the transposed
+// k2 s2 map: each fine voxel has one parent): key[k] = the offset of row k's
+// entry (V when it has none), to be stably sorted so that 128-row tiles hold
+// rows of one offset.
+__global__ void onehot_keys_kernel(const int* __restrict__ hits, long long ld, int V, long long n,
+                                   uint32_t* __restrict__ keys, int* __restrict__ vals) {
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+       k += (long long)gridDim.x * blockDim.x) {
+    uint32_t off = (uint32_t)V;
+    for (int v = V - 1; v >= 0; --v)
+      if (__ldg(hits + (long long)v * ld + k) >= 0) off = (uint32_t)v;
+    keys[k] = off;
+    vals[k] = (int)k;
+  }
+}
+
+// The hit matrix in the sorted row order (tile row r = output row perm[r])
+// and its tile words.  128 threads per block, one tile per iteration.
+__global__ void __launch_bounds__(128) onehot_apply_kernel(
+    const int* __restrict__ hits, long long ld, int V, long long n, const uint32_t* __restrict__ skeys,
+    const int* __restrict__ perm, int* __restrict__ hits_out, uint32_t* __restrict__ tmask) {
+  __shared__ uint32_t acc[4];
+  const long long tiles = (n + 127) / 128;
+  for (long long t = blockIdx.x; t < tiles; t += gridDim.x) {
+    const long long r = t * 128 + threadIdx.x;
+    uint32_t m = 0;
+    if (r < n) {
+      const long long k = perm[r];
+      const uint32_t off = skeys[r];
+      for (int v = 0; v < V; ++v)
+        hits_out[(long long)v * ld + r] = (uint32_t)v == off ? __ldg(hits + (long long)v * ld + k) : -1;
+      m = off < (uint32_t)V ? (1u << off) : 0u;
+    }
+    const uint32_t w = __reduce_or_sync(0xffffffffu, m);
+    if ((threadIdx.x & 31) == 0) acc[threadIdx.x >> 5] = w;
+    __syncthreads();
+    if (threadIdx.x == 0) tmask[t] = acc[0] | acc[1] | acc[2] | acc[3];
+    __syncthreads();
+  }
+}
+
 int blocks_for(long long n, int threads) {
   long long b = (n + threads - 1) / threads;
   if (b < 1) b = 1;
@@ -285,6 +326,36 @@ extern "C" int32_t scb_permute_rows(const void* src, int64_t src_ld_bytes, const
   else
     permute_rows_kernel<uint16_t><<<blocks, RT, 0, s>>>((const uint8_t*)src, src_ld_bytes, index, n,
                                                         words, (uint8_t*)dst, dst_ld_bytes, scatter);
+  SCB_LAUNCHED();
+  return SCB_OK;
+}
+
+extern "C" int64_t scb_onehot_order_workspace(int64_t n) { return (int64_t)sort_ws(n).total; }
+
+extern "C" int32_t scb_onehot_order(const int32_t* hits, int32_t volume, int64_t n, void* workspace,
+                                    int64_t ws_bytes, int32_t* perm, int32_t* hits_out,
+                                    uint32_t* tile_masks, scb_stream_t stream) {
+  SCB_CHECK_ARG(volume >= 1 && volume <= 32, "one-hot order supports at most 32 offsets");
+  SCB_CHECK_ARG(hits && perm && hits_out && tile_masks, "hits, perm, hits_out, tile_masks required");
+  const SortWs w = sort_ws(n);
+  SCB_CHECK_ARG(ws_bytes >= (int64_t)w.total, "workspace too small");
+  if (n == 0) return SCB_OK;
+  cudaStream_t s = as_stream(stream);
+  char* base = (char*)(((uintptr_t)workspace + 255) & ~(uintptr_t)255);
+  auto* kin = (uint32_t*)base;
+  auto* kout = (uint32_t*)(base + w.keys_in);
+  auto* vin = (int*)(base + w.keys_in + w.keys_out);
+  void* tmp = base + w.keys_in + w.keys_out + w.vals_in;
+  size_t tb = w.tmp;
+  const long long ld = hits_ld(n);
+  onehot_keys_kernel<<<blocks_for(n, RT), RT, 0, s>>>(hits, ld, volume, n, kin, vin);
+  SCB_LAUNCHED();
+  int end_bit = 1;
+  while ((volume >> end_bit) != 0) ++end_bit;
+  SCB_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, kin, kout, vin, perm, (int64_t)n, 0, end_bit, s));
+  const long long tiles = (n + 127) / 128;
+  onehot_apply_kernel<<<(int)(tiles < 148 * 16 ? tiles : 148 * 16), 128, 0, s>>>(
+      hits, ld, volume, n, kout, perm, hits_out, tile_masks);
   SCB_LAUNCHED();
   return SCB_OK;
 }

@@ -24,6 +24,8 @@ import warnings
 from contextlib import contextmanager, nullcontext
 from dataclasses import dataclass
 
+import os
+
 import numpy as np
 import torch
 
@@ -34,7 +36,8 @@ from .mapping import (DEFAULT_GRID_CELL_CAP, GatherScatterPlan, GridCapacityErro
                       KernelOffsets, build_gather_scatter_plan, build_index,
                       compute_output_coords, compute_output_coords_chain, downsample_boundary,
                       start_output_coords_chain,
-                      enumerate_offsets, map_search, permute_rows, reorder_by_presence, _cells)
+                      enumerate_offsets, map_search, map_search_masked, permute_rows,
+                      reorder_by_presence, _cells)
 
 GATHER_ORDERS = ("weight_stationary", "input_stationary")
 SCATTER_ORDERS = ("weight_stationary", "output_stationary")
@@ -580,8 +583,14 @@ def _run_fused(features: torch.Tensor, kmap: KernelMap | None, w: WeightTensor,
     ldo = (w.c_out + 7) // 8 * 8
     out = torch.empty((n_out, ldo), dtype=features.dtype, device=features.device)
     scale, shift, bias, res, relu = _epi_args(epilogue, n_out, w.c_out, features.dtype)
-    hits = None if kmap is None else nat.ptr(kmap.hits)
-    masks = None if kmap is None else nat.ptr(kmap.tile_masks())
+    rows = None
+    if kmap is not None and kmap.onehot and os.environ.get("SCB_ONEHOT", "1") == "1":
+        # one entry per output row: tiles over the rows sorted by offset
+        perm, h, m = kmap.onehot_order()
+        hits, masks, rows = nat.ptr(h), nat.ptr(m), nat.ptr(perm)
+    else:
+        hits = None if kmap is None else nat.ptr(kmap.hits)
+        masks = None if kmap is None else nat.ptr(kmap.tile_masks())
     with _timed(timer, label, "fused"):
         if concat is not None and features.shape[1] % 8 == 0 and concat.shape[1] % 8 == 0 \
                 and features.is_contiguous() and concat.is_contiguous():
@@ -591,10 +600,10 @@ def _run_fused(features: torch.Tensor, kmap: KernelMap | None, w: WeightTensor,
             f, ca, f2, cb = _pad_channels(f), None, None, 0
             ca = f.shape[1]
         ctas, skb = (opts.kernel_shapes or {}).get(label, (0, 0))
-        nat.call("scb_conv_implicit_tuned", nat.ptr(f), f.shape[1], ca, nat.ptr(f2),
+        nat.call("scb_conv_implicit_rows", nat.ptr(f), f.shape[1], ca, nat.ptr(f2),
                  0 if f2 is None else f2.shape[1], f.shape[0], ca + cb, hits, volume, n_out,
-                 masks, nat.ptr(packed), w.c_out, nat.ptr(out), ldo, scale, shift, bias, res,
-                 relu, int(ctas), int(skb), nat.stream_handle())
+                 masks, rows, nat.ptr(packed), w.c_out, nat.ptr(out), ldo, scale, shift, bias,
+                 res, relu, int(ctas), int(skb), nat.stream_handle())
     if ldo != w.c_out:
         out = out[:, : w.c_out]  # 8-aligned rows for the TMA store; a strided view
     if opts.traffic_log is not None:
@@ -610,7 +619,8 @@ def _run_fused(features: torch.Tensor, kmap: KernelMap | None, w: WeightTensor,
         if kmap is None:
             blocks = (n_out + nat.TILE_ROWS - 1) // nat.TILE_ROWS
         else:
-            tm = kmap.tile_masks().cpu().numpy().astype(np.uint32)
+            tm = (kmap.onehot_order()[2] if rows is not None else kmap.tile_masks()
+                  ).cpu().numpy().astype(np.uint32)
             blocks = int(sum(bin(int(x)).count("1") for x in tm))
         opts.traffic_log.append((label, {
             "fused_bytes": base + 4 * m_moved,
@@ -818,7 +828,12 @@ def _layer_maps(cset: CoordinateSet, spec: LayerSpec, strat: LayerStrategy,
                                        cset.batch_size)
             out_cset = CoordinateSet(oc, out_boundary, cset.batch_size)
         index = build_index(cset, kind, cell_cap=opts.grid_cell_cap)
-        kmap = map_search(index, out_cset.coords, offsets, spec.stride)
+        pres = cset.derived.get(("presence", spec.kernel_size)) if spec.stride == 1 else None
+        if pres is not None and offsets.center is not None and offsets.volume <= 32:
+            # a presence-reordered level: probe only the present offsets
+            kmap = map_search_masked(index, cset, offsets, pres)
+        else:
+            kmap = map_search(index, out_cset.coords, offsets, spec.stride)
         # stride 1: the output set IS this set; store None, not a
         # self-reference (a cycle would pin the maps until the cyclic GC)
         hit = (None if out_cset is cset else out_cset, kmap)

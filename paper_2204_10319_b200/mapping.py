@@ -251,6 +251,9 @@ def reorder_by_presence(cset: CoordinateSet, kernel_size: int = 3,
     out = CoordinateSet(coords, cset.boundary, cset.batch_size, perm=perm)
     for k, idx in cset.indexes.items():   # the same indexes, rows relabelled
         out.indexes[k] = CoordinateIndex.relabelled(idx, inv)
+    # the presence words in the new row order: the level's stride-1 map is
+    # then searched from them (map_search_masked)
+    out.derived[("presence", kernel_size)] = permute_rows(masks.view(n, 1), perm).view(n)
     cset.derived[key] = out
     return out
 
@@ -263,8 +266,9 @@ def downsample_boundary(boundary, stride: int) -> tuple[int, ...]:
 def compute_output_coords(in_coords, offsets: KernelOffsets, stride: int, out_boundary,
                           batch_size: int = 1) -> torch.Tensor:
     """Active output coordinates (mapping.py:216-248).  Stride 1 returns the
-    input coordinates; stride > 1 runs the fused candidate kernel and a 64-bit
-    radix sort + unique, so rows come out in ascending flat-key order.
+    input coordinates; stride > 1 runs the fused candidate kernel and a radix
+    sort + unique (32-bit keys whenever the output grid has < 2^32 cells, else
+    64-bit), so rows come out in ascending flat-key order.
     Returns an int32 device tensor."""
     if stride < 1:
         raise ValueError("stride must be >= 1")
@@ -408,6 +412,8 @@ class KernelMap:
         self._plans = {}
         self._swapped = None
         self._tile_masks = None
+        self.onehot = False   # at most one entry per output row (transposed K = s map)
+        self._onehot_order = None
 
     @classmethod
     def from_hits(cls, hits, offsets, stride, n_in, n_out, symmetric=False) -> "KernelMap":
@@ -451,6 +457,25 @@ class KernelMap:
                      nat.stream_handle())
             self._tile_masks = m
         return self._tile_masks
+
+    def onehot_order(self):
+        """(perm, hits, tile_masks) of a one-hot map in tile-row order: rows
+        stably sorted by the offset of their entry, so each 128-row tile of
+        the fused kernel has one active offset (scb_onehot_order; B200
+        extension).  Built once per map."""
+        if self._onehot_order is None:
+            h = self.hits
+            n, dev = self.n_out, h.device
+            ws = torch.empty(int(nat.load().scb_onehot_order_workspace(n)), dtype=torch.uint8,
+                             device=dev)
+            perm = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+            hp = _hit_matrix(self.offsets.volume, n, dev)
+            tiles = max((n + nat.TILE_ROWS - 1) // nat.TILE_ROWS, 1)
+            tm = torch.zeros(tiles, dtype=torch.int32, device=dev)
+            nat.call("scb_onehot_order", nat.ptr(h), self.offsets.volume, n, nat.ptr(ws), ws.numel(),
+                     nat.ptr(perm), nat.ptr(hp), nat.ptr(tm), nat.stream_handle())
+            self._onehot_order = (perm, hp, tm)
+        return self._onehot_order
 
     offset_ptr = property(lambda self: self._ensure_csr()[0])
     in_idx = property(lambda self: self._ensure_csr()[2])
@@ -502,6 +527,8 @@ class KernelMap:
                          nat.stream_handle())
             self._swapped = KernelMap(None, None, None, None, self.offsets, self.stride,
                                       self.n_out, self.n_in, trusted=self.trusted, hits=ht)
+            # K = s windows tile the fine grid: every fine row has one parent
+            self._swapped.onehot = self.stride > 1 and self.offsets.kernel_size == self.stride
         return self._swapped
 
 
@@ -528,6 +555,29 @@ def map_search(in_index: CoordinateIndex, out_coords, offsets: KernelOffsets, st
              nat.ptr(in_index.rows), in_index.slots, nat.ptr(hits), nat.stream_handle())
     return KernelMap.from_hits(hits, offsets, stride, in_index.size, n_out,
                                symmetric=bool(use_symmetry))
+
+
+def map_search_masked(in_index: CoordinateIndex, cset: CoordinateSet, offsets: KernelOffsets,
+                      masks: torch.Tensor) -> KernelMap:
+    """The stride-1 map of ``cset`` onto itself (= map_search(..., stride 1),
+    symmetric) from the rows' presence words (presence_masks in cset's row
+    order): only present offsets are probed, and the map's tile masks come
+    with it (scb_map_search_masked; B200 extension)."""
+    n = cset.num_points
+    if offsets.volume > 32 or offsets.center is None:
+        raise ValueError("masked search needs an odd kernel of at most 32 offsets")
+    if masks.shape[0] != n or n != in_index.size:
+        raise ValueError("masked search needs the set's own presence words and index")
+    hits = _hit_matrix(offsets.volume, n, cset.coords.device)
+    tiles = max((n + nat.TILE_ROWS - 1) // nat.TILE_ROWS, 1)
+    tm = torch.zeros(tiles, dtype=torch.int32, device=cset.coords.device)
+    grid = nat.make_grid(in_index.boundary, in_index.batch_size)
+    nat.call("scb_map_search_masked", in_index.code, nat.ptr(cset.coords), n, grid,
+             offsets.kernel_size, offsets.base, nat.ptr(in_index.keys), nat.ptr(in_index.rows),
+             in_index.slots, nat.ptr(masks), nat.ptr(hits), nat.ptr(tm), nat.stream_handle())
+    kmap = KernelMap.from_hits(hits, offsets, 1, n, n, symmetric=True)
+    kmap._tile_masks = tm
+    return kmap
 
 
 def derive_symmetric_maps(half_map: KernelMap) -> KernelMap:

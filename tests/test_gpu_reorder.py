@@ -135,3 +135,95 @@ def test_model_reorder_is_identical(sc, model):
     np.testing.assert_array_equal(outs[0][0], outs[1][0])
     a, b = outs[0][1].astype(np.float64), outs[1][1].astype(np.float64)
     assert np.linalg.norm(a - b) / np.linalg.norm(a) <= 1e-3
+
+
+def test_masked_search_equals_symmetric_search(sc, rng):
+    """scb_map_search_masked (probe only the present offsets) = the
+    symmetric map search, hit matrix and tile words, on a relabelled level."""
+    from paper_2204_10319_b200.mapping import map_search_masked, reorder_by_presence
+    for coords, boundary, bs in _clouds(rng):
+        t = sc.SparseTensor(coords, np.zeros((coords.shape[0], 1), np.float32), 1, boundary, bs)
+        p = reorder_by_presence(t.coordset, 3, "hash")
+        idx = sc.build_index(p, "hash")
+        off = sc.enumerate_offsets(3, 3)
+        ref = sc.map_search(idx, p.coords, off, 1)
+        got = map_search_masked(idx, p, off, p.derived[("presence", 3)])
+        n = coords.shape[0]
+        assert torch.equal(got.hits[:, :n], ref.hits[:, :n])
+        assert torch.equal(got.tile_masks(), ref.tile_masks())
+        # the engine's cached k3 map of a relabelled level is the masked one
+        out = sc.sparse_conv_forward(
+            sc.SparseTensor._wrap(torch.zeros((n, 8), dtype=torch.float16, device="cuda"), 1,
+                                  boundary, bs, p),
+            sc.WeightTensor(np.zeros((27, 8, 8), np.float32), 3, 3), sc.LayerSpec(3, 1, 8, 8),
+            None, None, sc.ExecOptions(dataflow="fused", index_kind="hash"))
+        assert out.features.shape[0] == n
+        assert torch.equal(p.maps[(3, 1, -1)][1].hits[:, :n], ref.hits[:, :n])
+
+
+def test_onehot_order_transposed_layer(sc, rng):
+    """The transposed k2 layer runs over rows sorted by their parent offset
+    (scb_onehot_order + scb_conv_implicit_rows): one active offset per tile,
+    and the output equals the output-row-order run bit for bit."""
+    import os
+    from paper_2204_10319_b200 import workloads
+    c, _, b = workloads.semantickitti_scan(1)
+    n = c.shape[0]
+    t = sc.SparseTensor(c, np.zeros((n, 1), np.float32), 1, b, 1)
+    f = torch.from_numpy(rng.standard_normal((n, 32)).astype(np.float16)).cuda()
+    wd = sc.WeightTensor(rng.normal(0, 0.1, (8, 32, 64)).astype(np.float32), 2, 3)
+    wu = sc.WeightTensor(rng.normal(0, 0.1, (8, 64, 48)).astype(np.float32), 2, 3)
+    opts = sc.ExecOptions(dataflow="fused", index_kind="hash")
+    cache = {}
+    d = sc.sparse_conv_forward(t.replace_features(f), wd,
+                               sc.LayerSpec(2, 2, 32, 64, reuse_key="d"), None, cache, opts)
+    kmap = cache["d"].kmap.swap_roles()
+    assert kmap.onehot
+    perm, hp, tm = kmap.onehot_order()
+    p = perm.cpu().numpy().astype(np.int64)
+    np.testing.assert_array_equal(np.sort(p), np.arange(n))
+    h = kmap.hits[:, :n].cpu().numpy()
+    off = np.where((h >= 0).any(0), (h >= 0).argmax(0), 8)
+    np.testing.assert_array_equal(off[p], np.sort(off, kind="stable"))
+    np.testing.assert_array_equal(p, np.argsort(off, kind="stable"))
+    np.testing.assert_array_equal(hp[:, :n].cpu().numpy(), h[:, p])
+    bits = tm.cpu().numpy().astype(np.int64)
+    assert np.mean([bin(int(v)).count("1") for v in bits]) < 1.1
+    ep = {"scale": torch.full((48,), 1.1, device="cuda"),
+          "shift": torch.full((48,), 0.01, device="cuda"), "relu": True}
+    spec = sc.LayerSpec(2, 1, 64, 48, transposed=True, reuse_key="d")
+    got = sc.inverse_conv_forward(d, wu, spec, cache, None, opts, epilogue=ep).features
+    os.environ["SCB_ONEHOT"] = "0"
+    try:
+        want = sc.inverse_conv_forward(d, wu, spec, cache, None, opts, epilogue=ep).features
+    finally:
+        os.environ.pop("SCB_ONEHOT")
+    assert torch.equal(got, want)
+
+
+@pytest.mark.parametrize("boundary,bs", [((40, 40, 12), 2), ((8192, 8192, 256), 4)])
+def test_output_coords_key_widths(sc, rng, boundary, bs):
+    """k2 s2 output coordinates with 32-bit sort keys (small grids) and
+    64-bit keys (> 2^32 output cells) equal the oracle, incl. the chain."""
+    from paper_2204_10319_b200.mapping import compute_output_coords_chain
+    n = 20000
+    keys = np.unique(rng.integers(0, bs * int(np.prod(boundary)), size=n))
+    coords = np.empty((keys.shape[0], 4), np.int64)
+    rem = keys
+    for d in range(2, -1, -1):
+        coords[:, d + 1] = rem % boundary[d]
+        rem = rem // boundary[d]
+    coords[:, 0] = rem
+    t = sc.SparseTensor(coords, np.zeros((coords.shape[0], 1), np.float32), 1, boundary, bs)
+    off = sc.enumerate_offsets(3, 2)
+    levels = compute_output_coords_chain(t.coordset, [(off, 2)] * 3)
+    cur, cb = coords, boundary
+    for oc, ob in levels:
+        nb = O.downsample_boundary(cb, 2)
+        want = O.output_coords(cur, 2, 2, nb, bs)
+        np.testing.assert_array_equal(oc.cpu().numpy(), want)
+        assert tuple(ob) == tuple(nb)
+        cur, cb = want, nb
+    ob = O.downsample_boundary(boundary, 2)
+    got = sc.compute_output_coords(t, off, 2, ob, bs)
+    np.testing.assert_array_equal(got.cpu().numpy(), O.output_coords(coords, 2, 2, ob, bs))

@@ -40,25 +40,30 @@ def main():
     lib.scb_ic_trace_clear()
     sc.sparse_conv_forward(t, w, spec, None, None, opts)
     torch.cuda.synchronize()
-    buf = np.zeros(CTAS * STAGES * 3, dtype=np.int64)
+    buf = np.zeros(CTAS * STAGES * 6, dtype=np.int64)
     lib.scb_ic_trace_read(buf.ctypes.data, buf.size)
-    tr = buf.reshape(CTAS, STAGES, 3)
+    tr = buf.reshape(CTAS, STAGES, 6)
     for cta in range(2):
         x = tr[cta]
         n = int(np.count_nonzero(x[:, 2]))
         x = x[:n].astype(np.float64)
         x -= x[0, 0]
-        lat = x[:, 1] - x[:, 0]          # copies issued -> stage full (gather latency)
+        lat = x[:, 3] - x[:, 0]          # copies issued -> A full (gather latency)
+        bwait = x[:, 1] - x[:, 3]        # A full -> B full (weights later than rows)
+        work = x[:, 2] - x[:, 1]         # full -> committed (issue time)
+        fence = x[:, 4] - x[:, 1]        # full -> past the proxy fence
+        issue = x[:, 5] - x[:, 4]        # the stage's MMA instructions
         mma_gap = np.diff(x[:, 1])       # MMA-side period
         commit_to_next_issue = x[2:, 0] - x[:-2, 2]  # (2-stage ring) slot freed -> reissue
         print(f"CTA {cta}: {n} stages over {x[-1, 2]:.0f} cycles = {x[-1, 2] / n:.0f} cyc/stage")
-        for name, v in (("issue->full (gather latency)", lat), ("full->full (MMA period)", mma_gap),
+        for name, v in (("issue->A full (gather latency)", lat), ("A full->B full", bwait),
+                        ("full->commit", work), ("full->fenced", fence), ("MMA issue", issue), ("full->full (MMA period)", mma_gap),
                         ("commit(s)->issue(s+2)", commit_to_next_issue)):
             q = np.percentile(v[5:], [10, 50, 90]) if v.size > 10 else v
             print(f"   {name:32s} p10 {q[0]:7.0f}  p50 {q[1]:7.0f}  p90 {q[2]:7.0f}")
         print("   first stages (issue, full, commit):")
         for i in range(10, 16):
-            print(f"     {i:3d} {x[i, 0]:8.0f} {x[i, 1]:8.0f} {x[i, 2]:8.0f}")
+            print(f"     {i:3d} {x[i, 0]:8.0f} {x[i, 3]:8.0f} {x[i, 1]:8.0f} {x[i, 2]:8.0f}")
 
 
 if __name__ == "__main__":

@@ -13,7 +13,7 @@
 using namespace scb::ptx;
 
 template <int U, bool TS>
-__global__ void rate(int n, int rounds, int commit_every, long long* out) {
+__global__ void rate(int n, int rounds, int commit_every, long long* out, int noise) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   __shared__ uint64_t bar, spare;
@@ -34,6 +34,30 @@ __global__ void rate(int n, int rounds, int commit_every, long long* out) {
   __syncthreads();
   tc_after();
   const uint32_t tmem = slot;
+  __shared__ volatile int stop;
+  if (threadIdx.x == 0) stop = 0;
+  __syncthreads();
+  if (warp > 0 && noise) {
+    // smem write traffic beside the MMAs: 16-B stores into a region the MMAs
+    // do not read (noise = 1), or cp.async 16-B copies from global (noise = 2)
+    uint8_t* region = smem + 48 * 1024;
+    const uint32_t off = (threadIdx.x - 32) * 16;
+    int it = 0;
+    while (!stop) {
+      if (noise == 1) {
+#pragma unroll
+        for (int r = 0; r < 8; ++r)
+          *reinterpret_cast<uint4*>(region + ((off + r * 1536) & 16383)) = make_uint4(it, r, 0, 0);
+      } else {
+#pragma unroll
+        for (int r = 0; r < 8; ++r)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(region + ((off + r * 1536) & 16383))),
+                       "l"(out + 512 + ((threadIdx.x * 8 + r + it * 64) & 4095) * 2) : "memory");
+        asm volatile("cp.async.commit_group;\ncp.async.wait_group 4;" ::: "memory");
+      }
+      ++it;
+    }
+  }
   if (warp == 0) {
     const uint64_t ad = make_sdesc(smem_u32(smem), 8u * 128, 2u);
     const uint64_t bd = make_sdesc(smem_u32(smem + 16384), 8u * 128, 2u);
@@ -56,6 +80,7 @@ __global__ void rate(int n, int rounds, int commit_every, long long* out) {
     __syncwarp();
     mbar_wait(&bar, 0);
     if (threadIdx.x == 0) out[blockIdx.x] = clock64() - t0;
+    if (threadIdx.x == 0) stop = 1;
   }
   tc_before();
   __syncthreads();
@@ -66,35 +91,30 @@ __global__ void rate(int n, int rounds, int commit_every, long long* out) {
 }
 
 template <int U, bool TS>
-void run(int n, int ctas_per_sm, int commit_every) {
+void run(int n, int ctas_per_sm, int commit_every, int noise = 0) {
   static long long* d = nullptr;
   const int grid = 148 * ctas_per_sm;
-  if (!d) cudaMalloc(&d, 148 * 4 * sizeof(long long));
+  if (!d) cudaMalloc(&d, 148 * 4 * sizeof(long long) + 64 * 1024);
   const int smem = ctas_per_sm == 1 ? 200 * 1024 : 100 * 1024;
   cudaFuncSetAttribute(rate<U, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const int rounds = 16384 / U;
-  rate<U, TS><<<grid, 128, smem>>>(n, rounds, commit_every, d);
+  rate<U, TS><<<grid, noise ? 256 : 128, smem>>>(n, rounds, commit_every, d, noise);
   cudaError_t e = cudaDeviceSynchronize();
   long long h[148 * 4];
   cudaMemcpy(h, d, grid * sizeof(long long), cudaMemcpyDeviceToHost);
   double s = 0;
   for (int i = 0; i < grid; ++i) s += h[i];
   const double per = s / grid / (rounds * U);
-  printf("%s U=%2d N=%3d ctas/SM=%d commit/%d: %6.1f cyc/MMA per CTA, %6.1f per SM (floor %5.1f) %s\n",
-         TS ? "TS" : "SS", U, n, ctas_per_sm, commit_every, per, per / ctas_per_sm, 128.0 * n / 256,
+  printf("%s noise=%d U=%2d N=%3d ctas/SM=%d commit/%d: %6.1f cyc/MMA per CTA, %6.1f per SM (floor %5.1f) %s\n",
+         TS ? "TS" : "SS", noise, U, n, ctas_per_sm, commit_every, per, per / ctas_per_sm, 128.0 * n / 256,
          e == cudaSuccess ? "" : cudaGetErrorString(e));
 }
 
 int main() {
-  for (int n : {32, 64, 96, 128, 256}) {
-    run<4, false>(n, 1, 1);
-    run<16, false>(n, 1, 1);
-    run<64, false>(n, 1, 0);
-    run<64, false>(n, 2, 0);
-    if (n <= 128) {
-      run<16, true>(n, 1, 1);
-      run<64, true>(n, 1, 0);
-      run<64, true>(n, 2, 0);
+  for (int n : {64, 96, 128}) {
+    for (int noise : {0, 1, 2}) {
+      run<16, false>(n, 1, 1, noise);
+      run<16, true>(n, 1, 1, noise);
     }
   }
   return 0;
