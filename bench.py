@@ -75,6 +75,9 @@ def parse():
     ap.add_argument("--layer-csv", default=None,
                     help="write the per-(layer, stage) CUDA-event table (layer,stage,metric,value)")
     ap.add_argument("--dataflow", choices=("staged", "fused", "auto"), default="auto")
+    ap.add_argument("--strategy", default=None,
+                    help="JSON v1 strategy file with per-layer fused-kernel launch shapes "
+                         "(default: the committed B200 MinkUNet-1.0x file; 'none' = heuristics)")
     ap.add_argument("--clock-ms", type=int, default=5, help="clock sampling period (0: off)")
     ap.add_argument("--gather", choices=("host", "rank0"), default="host",
                     help="e2e output gather: host = each rank downloads its own scans' logits "
@@ -248,6 +251,10 @@ def run_reference(args):
 
 
 DATA = "synthetic (raycast LiDAR scans, random-init weights)"
+DEBUG_ALLOC = os.environ.get("SCB_BENCH_DEBUG_ALLOC") == "1"
+# per-layer fused-kernel launch shapes tuned on a B200 for the MinkUNet-1.0x
+# 8-scan workload (tools/tune_minkunet.py)
+DEFAULT_STRATEGY = ROOT / "paper_2204_10319_b200" / "configs" / "minkunet_b200_shapes.json"
 
 
 def workload_config(args, world, scans):
@@ -427,7 +434,13 @@ def main():
         load_scans(range(args.strong if args.strong else args.scans_per_gpu), args.model)
     coords, feats, boundary = pack(scans)
     if args.model == "minkunet":
-        model = EngineMinkUNet(args.width, 4, 0)
+        strat = args.strategy
+        if strat is None and args.width == 1.0 and DEFAULT_STRATEGY.exists():
+            strat = str(DEFAULT_STRATEGY)
+        if strat == "none":
+            strat = None
+        model = EngineMinkUNet(args.width, 4, 0, strategy=strat)
+        args.strategy_used = Path(strat).name if strat else None
     else:
         model = EngineCenterPoint(5, 0)
     coords_d = torch.from_numpy(coords.astype(np.int32)).to(dev)
@@ -435,14 +448,42 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     # one large cached segment up front: later per-step allocations split it
     # instead of calling cudaMalloc inside a timed step
-    reserve = torch.empty(16 << 30, dtype=torch.uint8, device=dev)
-    del reserve
+    # (and the small-block pool: blocks < 1 MiB come from 2 MiB segments of
+    # their own; a new one inside a timed step measured a 50-135 ms host stall)
+    def _reserve(big, small_blocks):
+        r = torch.empty(big, dtype=torch.uint8, device=dev)
+        smalls = [torch.empty(512 << 10, dtype=torch.uint8, device=dev)
+                  for _ in range(small_blocks)]
+        del r, smalls
+    _reserve(16 << 30, 256)
+    for side in (getattr(model, "map_stream", None), getattr(model, "chain_stream", None)):
+        if side is not None:  # the mapping streams' own pools
+            with torch.cuda.stream(side):
+                _reserve(2 << 30, 128)
+
+    coords_ev = torch.cuda.Event()
+    coords_ev.record()
+    pipe = {"next": None}
+
+    def make_input():
+        t = sc.SparseTensor(coords_d, feats_d, 1, boundary, B, validate=False)
+        return sc.quantize_features(t, sc.PrecisionMode.FP16_STORAGE)
 
     def step(timer=None, traffic=None):
-        t = sc.SparseTensor(coords_d, feats_d, 1, boundary, B, validate=False)
-        t = sc.quantize_features(t, sc.PrecisionMode.FP16_STORAGE)
-        return model.forward(t, sc.ExecOptions(timer=timer, traffic_log=traffic,
-                                               index_kind="hash", dataflow=args.dataflow))
+        """One forward.  Uninstrumented steps run as a serving loop: batch
+        i+1's level-0 maps and coordinate pyramid are queued (model.prefetch)
+        right after batch i's convolutions, on the mapping streams, so they
+        run beside them; every step still builds all of its maps."""
+        opts = sc.ExecOptions(timer=timer, traffic_log=traffic, index_kind="hash",
+                              dataflow=args.dataflow)
+        if timer is not None or traffic is not None or not hasattr(model, "prefetch"):
+            pipe["next"] = None
+            return model.forward(make_input(), opts)
+        t = pipe["next"] if pipe["next"] is not None else make_input()
+        out = model.forward(t, opts)
+        pipe["next"] = make_input()
+        model.prefetch(pipe["next"], opts, coords_ready=coords_ev)
+        return out
 
     # algorithmic bytes per layer (SURVEY.md §8(d)) from one untimed pass;
     # the warm-up steps after it settle the allocator again
@@ -451,11 +492,15 @@ def main():
     torch.cuda.synchronize()
     # W warm-up steps at least, and at least ~1.5 s of them: a fresh box
     # needs that long to settle clocks, lazy module loads and the allocator
+    # (unsynchronised, like the timed loop: as many forwards in flight, so the
+    # caching allocator's pools reach their steady-state size here)
     warm, w0 = 0, time.perf_counter()
     while warm < args.warmup or (time.perf_counter() - w0 < 1.5 and warm < 200):
         step()
-        torch.cuda.synchronize()
         warm += 1
+        if warm % 16 == 0:
+            torch.cuda.synchronize()
+    torch.cuda.synchronize()
 
     # ---------------- device-resident timed region (no instrumentation)
     clocks = Clocks(str(ROOT / f"gpurun_out/clocks_rank{rank}.csv")
@@ -473,6 +518,14 @@ def main():
     gc.collect()
     gc.disable()  # no collector pauses inside the timed steps
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # a rehearsal of the exact timed loop first (untimed): the caching
+    # allocator's pools then already hold what K unsynchronised steps need,
+    # so no cudaMalloc lands inside the timed steps
+    for i in range(args.steps):
+        flush.fill_(i & 0xFF)
+        step()
+    torch.cuda.synchronize()
+    seg0 = torch.cuda.memory_stats(dev).get("segment.all.allocated", 0)
     switch0 = sys.getswitchinterval()
     sys.setswitchinterval(5e-4)  # let the clock-sampler thread in between host issues
     hw0 = time.perf_counter()
@@ -484,6 +537,12 @@ def main():
         out = step()
         host_ms.append(round(1e3 * (time.perf_counter() - h0), 3))
         evs[i][1].record()
+        if DEBUG_ALLOC:
+            st = torch.cuda.memory_stats(dev)
+            print(f"[alloc] step {i}: segments {st.get('segment.all.allocated', 0)} "
+                  f"large {st.get('segment.large_pool.allocated', 0)} small "
+                  f"{st.get('segment.small_pool.allocated', 0)} reserved "
+                  f"{st.get('reserved_bytes.all.current', 0) >> 20} MiB", file=sys.stderr)
     t_end.record()
     torch.cuda.synchronize()
     clocks.mark(hw0, time.perf_counter())
@@ -551,6 +610,7 @@ def main():
             "e2e": e2e, "gpu_launches": int(launches), "clocks": clk, "warmup_steps_run": warm,
             "step_ms": step_ms, "host_issue_ms": host_ms,
             "cuda_mallocs_in_timed_steps": seg_allocs,
+            "kernel_shapes": getattr(args, "strategy_used", None) or "heuristic",
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -667,7 +727,11 @@ def run_e2e(args, sc, model, coords, feats, boundary, B, dev, world, UNIT, out):
     pending = collections.deque()
     counter = [0]
 
-    def e2e_step():
+    opts_e = sc.ExecOptions(index_kind="hash", dataflow=args.dataflow)
+    nxt = {"t": None, "k": None}
+
+    def upload():
+        """The next batch's pinned H2D (copy stream) and its SparseTensor."""
         k = counter[0] % NB
         counter[0] += 1
         cur = torch.cuda.current_stream()
@@ -676,10 +740,23 @@ def run_e2e(args, sc, model, coords, feats, boundary, B, dev, world, UNIT, out):
                 h2d_s.wait_event(done[k])
             c_ring[k].copy_(h_coords, non_blocking=True)
             f_ring[k].copy_(h_feats, non_blocking=True)
-        cur.wait_stream(h2d_s)
-        t = sc.SparseTensor(c_ring[k], f_ring[k], 1, boundary, B, validate="async")
-        t = sc.quantize_features(t, sc.PrecisionMode.FP16_STORAGE)
-        o = model.forward(t, sc.ExecOptions(index_kind="hash", dataflow=args.dataflow))
+            # validation (its hash index is level 0's) on the copy stream, so
+            # `up` covers everything the mapping streams read
+            t = sc.SparseTensor(c_ring[k], f_ring[k], 1, boundary, B, validate="async")
+            up = h2d_s.record_event()
+        cur.wait_event(up)
+        return k, sc.quantize_features(t, sc.PrecisionMode.FP16_STORAGE), up
+
+    def e2e_step():
+        """Serving loop: batch i's forward and download, then batch i+1's
+        upload and its prefetched level-0 maps / coordinate pyramid (beside
+        batch i's convolutions).  Every step moves one batch in and out."""
+        cur = torch.cuda.current_stream()
+        if nxt["t"] is None:
+            k, t, _ = upload()
+        else:
+            k, t = nxt["k"], nxt["t"]
+        o = model.forward(t, opts_e)
         res = o.features
         if to_rank0:  # the path's one data collective: NCCL gather to rank 0
             blocks = gather_rows(res, rows_per_rank, 0)
@@ -692,18 +769,27 @@ def run_e2e(args, sc, model, coords, feats, boundary, B, dev, world, UNIT, out):
             pending.append((o, d2h_s.record_event()))
         while len(pending) > 3:
             pending.popleft()[1].synchronize()
+        if hasattr(model, "prefetch"):
+            nxt["k"], nxt["t"], up = upload()
+            model.prefetch(nxt["t"], opts_e, coords_ready=up)
         return o
 
     warm_e, w0 = 0, time.perf_counter()
     while warm_e < args.warmup or (time.perf_counter() - w0 < 1.0 and warm_e < 200):
         e2e_step()
-        torch.cuda.synchronize()
         warm_e += 1
+        if warm_e % 16 == 0:
+            torch.cuda.synchronize()
+    torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     gc.collect()
     gc.disable()
+    for _ in range(args.steps):   # rehearsal of the timed loop (allocator pools)
+        e2e_step()
+    torch.cuda.current_stream().wait_stream(d2h_s)
+    torch.cuda.synchronize()
     seg_e = torch.cuda.memory_stats(dev).get("segment.all.allocated", 0)
     e_host = []
     e0.record()

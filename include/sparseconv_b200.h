@@ -308,7 +308,11 @@ int32_t scb_conv_implicit_cat(const void* features, int64_t ldf, int32_t c_split
  * strategy files of autotune.tune_fused_layer): `ctas_per_sm` 1..3 co-resident
  * CTAs per SM (clamped to what TMEM allows; 0 = auto) and `stage_kb` the
  * target pipeline-stage size in KB, which sets the kernel offsets per stage
- * (0 = auto).  Results are identical for every shape. */
+ * (0 = auto); `ctas_per_sm` 4..5 runs the CTA-pair kernel (tcgen05
+ * cta_group::2, M = 256 over two SMs of a cluster; 1..2 pairs' CTAs per SM).
+ * Maps, offsets and epilogue are the same for every shape; when C_in spans
+ * several K chunks the order of the f32 (offset, chunk) partial sums follows
+ * the offsets grouped per stage, so outputs agree to f32 summation order. */
 int32_t scb_conv_implicit_tuned(const void* features, int64_t ldf, int32_t c_split,
                                 const void* features2, int64_t ldf2, int64_t n_in, int32_t c_in,
                                 const int32_t* hits, int32_t volume, int64_t n_out,

@@ -64,6 +64,9 @@ struct Params {
   int nacc;                 // TMEM accumulator buffers (2: epilogue overlaps the next tile)
   int interleave;           // tile order: 1 = t = blockIdx + i * gridDim, 0 = contiguous ranges
   int debug;                // EXPERIMENT (SCB_IC_DEBUG): 1 = B loaded once, 2 = no A copies, 4 = no proxy fence
+  int pair;                 // CTA-pair kernel: work items are 256-row pair tiles (rows of CTA r: 2T + r)
+  int idx_slots;            // pair kernel: index-ring slots (one offset group's hit rows each)
+  uint32_t idx_slot_bytes;  // ops x 128 x 4
   uint32_t all_bits;        // (1 << V) - 1
   uint32_t idesc, tmem_cols;
   uint32_t a_off_bytes;     // one offset's A block [128 rows][kc] (1024-aligned)
@@ -95,7 +98,16 @@ __host__ __device__ constexpr int max_idx(int minb) { return minb >= 3 ? 8 : MAX
 // Active offsets of row tile t (never empty: an all-absent tile still needs
 // its accumulator zeroed, so it runs offset 0 with every row zero-filled).
 __device__ __forceinline__ uint32_t tile_bits(const Params& p, int t) {
-  const uint32_t m = p.tmask ? (__ldg(p.tmask + t) & p.all_bits) : p.all_bits;
+  uint32_t m = p.all_bits;
+  if (p.tmask) {
+    if (p.pair) {  // a pair tile runs the union of its two row tiles' offsets
+      m = __ldg(p.tmask + 2 * t);
+      if (2 * t + 1 < p.total_tiles) m |= __ldg(p.tmask + 2 * t + 1);
+      m &= p.all_bits;
+    } else {
+      m = __ldg(p.tmask + t) & p.all_bits;
+    }
+  }
   return m ? m : 1u;
 }
 
@@ -115,6 +127,8 @@ struct TileSeq {
   int t0, step, lim;
 };
 __device__ __forceinline__ TileSeq tile_seq(const Params& p) {
+  if (p.pair)  // one pair tile per cluster (CTAs 2c, 2c + 1), interleaved
+    return {(int)(blockIdx.x >> 1), (int)(gridDim.x >> 1), (p.total_tiles + 1) >> 1};
   if (p.interleave) return {(int)blockIdx.x, (int)gridDim.x, p.total_tiles};
   const int b = (int)((long long)p.total_tiles * blockIdx.x / gridDim.x);
   const int e = (int)((long long)p.total_tiles * (blockIdx.x + 1) / gridDim.x);
@@ -183,7 +197,7 @@ __device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
 __device__ __forceinline__ void epilogue_role(const Params& p, const CUtensorMap* tmOut_,
                                               uint32_t tmem_base, uint64_t* tfull,
                                               uint64_t* tempty, uint8_t* epi_base, int warp,
-                                              int lane, const TileSeq& ts) {
+                                              int lane, const TileSeq& ts, uint32_t rank = 0) {
   const int q = warp & 3;
   uint8_t* bufs = epi_base + (warp - EPI0) * p.epi_bufs * EPI_BUF;
   int acc = 0, nbuf = 0;
@@ -192,7 +206,7 @@ __device__ __forceinline__ void epilogue_role(const Params& p, const CUtensorMap
   for (int t = ts.t0; t < ts.lim; t += ts.step) {
     mbar_wait_sleep(tfull + acc, acc_phase, 256);
     tc_after();
-    const long long row0 = (long long)t * BM + 32 * q;
+    const long long row0 = (long long)(p.pair ? 2 * t + (int)rank : t) * BM + 32 * q;
     const long long r = row0 + lane;        // tile row
     const bool row_ok = r < p.n_out;
     // output row of this lane: the tile row itself, or orow[r] when the
@@ -284,7 +298,12 @@ __device__ __forceinline__ void epilogue_role(const Params& p, const CUtensorMap
     }
     tc_before();
     __syncwarp();
-    if (lane == 0) mbar_arrive(tempty + acc);
+    if (lane == 0) {
+      if (p.pair)  // the pair's MMA issuer (CTA 0) waits on CTA 0's barrier
+        mbar_arrive_cluster(mapa_shared(smem_u32(tempty + acc), 0));
+      else
+        mbar_arrive(tempty + acc);
+    }
     if (++acc == p.nacc) { acc = 0; acc_phase ^= 1; }
   }
   if (lane == 0) bulk_wait_all();
@@ -550,6 +569,309 @@ __global__ void __launch_bounds__(64 + NPROD + 128, MINB)
   }
 }
 
+// ============ The CTA-pair form (tcgen05 cta_group::2).  A cluster of two
+// CTAs on one TPC computes 256-row pair tiles: CTA r gathers rows
+// (2T + r) * 128 .. + 127 of pair tile T into its own smem and holds half of
+// the weight slice (N / 2 output channels); CTA 0's MMA thread issues one
+// M = 256 MMA per K step for both SMs, so each instruction and each pipeline
+// stage carries twice the work of the single-CTA kernel (the per-stage issue
+// overhead of that kernel is what bounds it), and each SM streams half the
+// weights.  One ring per CTA (a stage holds its A rows and its B half):
+//   full[s]   CTA 0: its producers (noinc) + its B arrive.expect_tx + the
+//             relay from CTA 1; CTA 1: its producers + its B
+//   empty[s]  one arrival in both CTAs from the MMA commit (multicast)
+//   tfull     MMA commit (multicast) -> both epilogues
+//   tempty    4 + 4 epilogue warps of both CTAs -> CTA 0's MMA thread
+// CTA 1's warp 1 relays its full barriers to CTA 0 (after a proxy fence, so
+// the MMA's async-proxy reads see its cp.async data).
+constexpr int PAIR_THREADS = 64 + NPROD + 128 + 32;   // + warp 10: the index loader
+constexpr int IDX_WARP = 10;
+
+template <int V, int KC, int MINB>
+__global__ void __launch_bounds__(PAIR_THREADS, MINB)
+    implicit_conv_pair_kernel(const __grid_constant__ CUtensorMap tmB,
+                              const __grid_constant__ CUtensorMap tmOut,
+                              const __grid_constant__ Params p) {
+  constexpr int CPR = KC / 8;
+  constexpr int IT = CPR;
+  constexpr int SWZ = KC * 2;
+  constexpr int RPI = NPROD / CPR;
+  constexpr int MI = max_idx(MINB);
+  constexpr int MAXO = MI / IT;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* epi_base = smem + (size_t)p.a_stages * p.a_stage_bytes;
+  uint8_t* idx_base = epi_base + 4 * p.epi_bufs * EPI_BUF;     // [idx_slots][ops][128] int32
+  uint64_t* full = (uint64_t*)(idx_base + (size_t)p.idx_slots * p.idx_slot_bytes);
+  uint64_t* empty = full + p.a_stages;
+  uint64_t* tfull = empty + p.a_stages;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* ifull = tempty + 2;
+  uint64_t* iempty = ifull + p.idx_slots;
+  uint32_t* tmem_slot = (uint32_t*)(iempty + p.idx_slots);
+  const uint32_t b_region = (uint32_t)p.ops * p.a_off_bytes;   // B half after the A blocks
+
+  const uint32_t rank = cluster_ctarank();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const TileSeq ts = tile_seq(p);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < p.a_stages; ++s) {
+      mbar_init(full + s, NPROD + 1 + (rank == 0 ? 1 : 0));
+      mbar_init(empty + s, 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull + a, 1);
+      mbar_init(tempty + a, 8);
+    }
+    for (int i = 0; i < p.idx_slots; ++i) {
+      mbar_init(ifull + i, 1);        // the loader's arrive.expect_tx
+      mbar_init(iempty + i, NPROD);   // every producer thread has read its indices
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmOut) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(p.tmem_cols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_before();
+  cluster_sync_all();   // both CTAs' barriers initialised, TMEM allocated
+  tc_after();
+  const uint32_t tmem_base = *tmem_slot;
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+
+  if (warp == 0) {
+    // ============ B producer: this CTA's half of the stage's weight slices
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      const int nrow0 = (int)rank * (p.n_pad >> 1);
+      GroupIter g;
+      for (g.start(p, ts); !g.done(ts); g.advance(p, ts)) {
+        const int nv = __popc(g.mg);
+        for (int kk = 0; kk < p.n_kchunks; ++kk) {
+          mbar_wait_sleep(empty + stage, phase ^ 1, 32);
+          mbar_expect_tx(full + stage, nv * p.b_tx);
+          uint8_t* sb = smem + (size_t)stage * p.a_stage_bytes + b_region;
+          uint32_t x = g.mg;
+          for (int o = 0; o < nv; ++o) {
+            const int n = __ffs(x) - 1;
+            x &= x - 1;
+            tma_load_2d(sb + o * p.b_off_bytes, &tmB, full + stage, kk * p.kc, n * p.n_pad + nrow0);
+          }
+          if (++stage == p.a_stages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp >= 2 && warp < EPI0) {
+    // ============ A producers (as the single-CTA kernel; rows of this CTA's
+    // half).  A group's input rows come from the index ring (the loader warp
+    // bulk-copies the group's hit-matrix rows several groups ahead), so no
+    // producer waits on a dependent global load.
+    const int pt = threadIdx.x - 64;
+    const int cr = pt / CPR, cc = pt % CPR;
+    uint32_t roff[IT];
+#pragma unroll
+    for (int it = 0; it < IT; ++it) {
+      const int r = it * RPI + cr;
+      const int rxr = SWZ == 128 ? (r & 7) : (SWZ == 64 ? ((r >> 1) & 3) : ((r >> 2) & 1));
+      roff[it] = (uint32_t)(r * (KC * 2)) + ((uint32_t)(cc ^ rxr) << 4);
+    }
+    int cur[MI];
+    const uint32_t ldfb1 = (uint32_t)(p.ldf * 2);
+    const uint32_t ldfb2 = (uint32_t)(p.ldf2 * 2);
+    int stage = 0, islot = 0;
+    uint32_t phase = 0, iph = 0;
+#ifdef SCB_IC_TRACE
+    int nstage = 0;
+#endif
+    GroupIter g;
+    for (g.start(p, ts); !g.done(ts); g.advance(p, ts)) {
+      const int nv = __popc(g.mg);
+      const long long row0 = (long long)(2 * g.t + (int)rank) * BM;
+      if (p.hits) {
+        mbar_wait(ifull + islot, iph);
+        const int* tab = reinterpret_cast<const int*>(idx_base + (size_t)islot * p.idx_slot_bytes);
+#pragma unroll
+        for (int o = 0; o < MAXO; ++o) {
+#pragma unroll
+          for (int it = 0; it < IT; ++it) {
+            const int r = it * RPI + cr;
+            cur[o * IT + it] = (o < nv && row0 + r < p.n_out) ? tab[o * BM + r] : -1;
+          }
+        }
+        mbar_arrive(iempty + islot);
+        if (++islot == p.idx_slots) { islot = 0; iph ^= 1; }
+      } else {  // identity map (K = 1, s = 1)
+#pragma unroll
+        for (int o = 0; o < MAXO; ++o) {
+#pragma unroll
+          for (int it = 0; it < IT; ++it) {
+            const long long k = row0 + it * RPI + cr;
+            cur[o * IT + it] = (o < nv && k < p.n_out) ? (int)k : -1;
+          }
+        }
+      }
+      for (int kk = 0; kk < p.n_kchunks; ++kk) {
+        mbar_wait(empty + stage, phase ^ 1);
+        if (pt == 0) IC_TRACE(nstage, 0);
+        const uint32_t dst = smem_u32(smem + (size_t)stage * p.a_stage_bytes);
+        const int col0 = kk * KC;
+        const int live = min(CPR, (p.c_in - col0) / 8);
+        const int col = col0 + cc * 8;
+        const bool second = p.feat2 != nullptr && col >= p.c_split;
+        const uint64_t fb = second
+            ? reinterpret_cast<uint64_t>(p.feat2) + (uint64_t)((col - p.c_split) * 2)
+            : reinterpret_cast<uint64_t>(p.feat) + (uint64_t)(col * 2);
+        const uint32_t ldb = second ? ldfb2 : ldfb1;
+        const bool live_c = cc < live;
+#pragma unroll
+        for (int o = 0; o < MAXO; ++o) {
+          if (o < nv) {
+            const uint32_t blk = dst + o * p.a_off_bytes;
+#pragma unroll
+            for (int it = 0; it < IT; ++it) {
+              const int j = live_c ? cur[o * IT + it] : -1;
+              const uint64_t src = fb + (uint64_t)(uint32_t)max(j, 0) * (uint64_t)ldb;
+              asm volatile(
+                  "{ .reg .pred q; setp.lt.s32 q, %2, 0;\n"
+                  "  cp.async.cg.shared.global [%0], [%1], 16, q; }" ::"r"(blk + roff[it]),
+                  "l"(src), "r"(j) : "memory");
+            }
+          }
+        }
+        cp_async_arrive_noinc(full + stage);
+#ifdef SCB_IC_TRACE
+        ++nstage;
+#endif
+        if (++stage == p.a_stages) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == IDX_WARP) {
+    // ============ index loader: each group's hit-matrix rows (this CTA's 128
+    // rows of every active offset, contiguous in hits[n][.]) by bulk copy
+    if (lane == 0 && p.hits) {
+      int slot = 0;
+      uint32_t ph = 0;
+      GroupIter g;
+      for (g.start(p, ts); !g.done(ts); g.advance(p, ts)) {
+        mbar_wait_sleep(iempty + slot, ph ^ 1, 20);
+        const long long row0 = (long long)(2 * g.t + (int)rank) * BM;
+        const long long avail = p.ldh - row0;   // entries of each hit row from row0 on
+        const uint32_t bytes = avail <= 0 ? 0u : (uint32_t)((avail < BM ? avail : BM) * 4);
+        if (bytes) {
+          const int nv = __popc(g.mg);
+          mbar_expect_tx(ifull + slot, (uint32_t)nv * bytes);
+          const uint32_t dst = smem_u32(idx_base + (size_t)slot * p.idx_slot_bytes);
+          uint32_t x = g.mg;
+          for (int o = 0; o < nv; ++o) {
+            const int n = __ffs(x) - 1;
+            x &= x - 1;
+            bulk_load(dst + o * BM * 4, p.hits + (long long)n * p.ldh + row0, bytes, ifull + slot);
+          }
+        } else {
+          mbar_arrive(ifull + slot);
+        }
+        if (++slot == p.idx_slots) { slot = 0; ph ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    if (rank != 0) {
+      // ============ relay (CTA 1): each filled stage -> CTA 0's full barrier
+      if (lane == 0) {
+        int stage = 0;
+        uint32_t phase = 0;
+        GroupIter g;
+        for (g.start(p, ts); !g.done(ts); g.advance(p, ts)) {
+          for (int kk = 0; kk < p.n_kchunks; ++kk) {
+            mbar_wait(full + stage, phase);
+            fence_async_smem();   // this CTA's cp.async data -> the pair MMA (async proxy)
+            mbar_arrive_cluster(mapa_shared(smem_u32(full + stage), 0));
+            if (++stage == p.a_stages) { stage = 0; phase ^= 1; }
+          }
+        }
+      }
+    } else {
+      // ============ MMA issuer of the pair (CTA 0), warp converged, one lane issues
+      const uint32_t layout = p.swz == 128 ? 2u : (p.swz == 64 ? 4u : 6u);
+      const uint32_t sbo = 8u * (uint32_t)p.swz;
+      const uint64_t adesc_base = make_sdesc(smem_u32(smem), sbo, layout);
+      const uint64_t bdesc_base = make_sdesc(smem_u32(smem) + b_region, sbo, layout);
+      const uint32_t stage_d = p.a_stage_bytes >> 4;
+      const uint32_t a_off_d = p.a_off_bytes >> 4, b_off_d = p.b_off_bytes >> 4;
+      const uint32_t idesc = p.idesc;
+      const uint32_t tmem0 = __shfl_sync(0xffffffffu, tmem_base, 0);
+      int as = 0, acc = 0;
+      uint32_t aph = 0, acc_phase = 0;
+      uint32_t d = 0, acc0 = 0;
+#ifdef SCB_IC_TRACE
+      int nstage = 0;
+#endif
+      GroupIter g;
+      for (g.start(p, ts); !g.done(ts); g.advance(p, ts)) {
+        if (g.first) {
+          mbar_wait_cluster(tempty + acc, acc_phase ^ 1);
+          tc_after();
+          d = tmem0 + (uint32_t)acc * (uint32_t)p.n_pad;
+          acc0 = 0u;
+        }
+        const int nv = __popc(g.mg);
+        for (int kk = 0; kk < p.n_kchunks; ++kk) {
+          mbar_wait_cluster(full + as, aph);
+          if (lane == 0) { IC_TRACE(nstage, 3); IC_TRACE(nstage, 1); }
+          const uint64_t ad = adesc_base + (uint64_t)(as * stage_d);
+          const uint64_t bd = bdesc_base + (uint64_t)(as * stage_d);
+          if (elect_one()) {
+            fence_async_smem();
+            tc_after();
+            IC_TRACE(nstage, 4);
+#pragma unroll
+            for (int o = 0; o < MAX_OPS; ++o) {
+              if (o < nv) {
+                const uint64_t a = ad + (uint64_t)(o * a_off_d);
+                const uint64_t b = bd + (uint64_t)(o * b_off_d);
+                mma_f16_pair(d, a, b, idesc, o ? 1u : acc0);
+#pragma unroll
+                for (int k = 1; k < KC / 16; ++k) mma_f16_pair(d, a + 2u * k, b + 2u * k, idesc, 1u);
+              }
+            }
+            IC_TRACE(nstage, 5);
+            mma_commit_pair(empty + as, (uint16_t)3);
+          }
+          __syncwarp();
+          if (lane == 0) IC_TRACE(nstage, 2);
+#ifdef SCB_IC_TRACE
+          ++nstage;
+#endif
+          acc0 = 1u;
+          if (++as == p.a_stages) { as = 0; aph ^= 1; }
+        }
+        if (g.last_of_tile()) {
+          if (elect_one()) mma_commit_pair(tfull + acc, (uint16_t)3);
+          __syncwarp();
+          if (++acc == p.nacc) { acc = 0; acc_phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp >= EPI0 && warp < EPI0 + 4) {
+    epilogue_role(p, &tmOut, tmem_base, tfull, tempty, epi_base, warp, lane, ts, rank);
+  }
+
+  __syncwarp();
+  tc_before();
+  cluster_sync_all();   // no CTA leaves while the pair's MMAs / arrivals target it
+  if (warp == 1) {
+    tc_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(p.tmem_cols));
+  }
+}
+
 // ------------------------------------------------------------------ tile masks
 // bit n of masks[t] = some row of tile t has hits[n][row] >= 0.  One block
 // per tile, one thread per row.
@@ -581,7 +903,7 @@ namespace {
 
 // Launch-invariant settings, read once per process.
 struct IcEnv {
-  int interleave, pdl, debug;
+  int interleave, pdl, debug, pair;
 };
 const IcEnv& ic_env() {
   static const IcEnv e = [] {
@@ -590,7 +912,7 @@ const IcEnv& ic_env() {
       return v ? atoi(v) : dflt;
     };
     return IcEnv{env_int("SCB_IC_INTERLEAVE", 1), env_int("SCB_IC_PDL", 1),
-                 env_int("SCB_IC_DEBUG", 0)};
+                 env_int("SCB_IC_DEBUG", 0), env_int("SCB_IC_PAIR", 0)};
   }();
   return e;
 }
@@ -683,6 +1005,150 @@ extern "C" int32_t scb_tile_masks(const int32_t* hits, int32_t volume, int64_t n
   return SCB_OK;
 }
 
+namespace {
+
+// The CTA-pair launch (implicit_conv_pair_kernel): arguments as
+// scb_conv_implicit_rows (validated there); `ctas` 0 = auto, 1..2 pairs' CTAs per SM.
+int32_t launch_pair(const void* features, int64_t ldf, int32_t c_split, const void* features2,
+                    int64_t ldf2, int64_t n_in, int32_t c_in, const int32_t* hits, int32_t volume,
+                    int64_t n_out, const uint32_t* tile_mask, const int32_t* out_rows,
+                    const void* weights_packed, int32_t c_out, void* out, int64_t ldo,
+                    const float* scale, const float* shift, const float* bias,
+                    const void* residual, int32_t relu, int ctas, int32_t stage_kb,
+                    scb_stream_t stream) {
+  using namespace ic;
+  const IcEnv& env = ic_env();
+  const int n_pad = (c_out + 15) / 16 * 16;
+  const int k_pad = (c_in + 15) / 16 * 16;
+  Params p;
+  memset(&p, 0, sizeof(p));
+  p.pair = 1;
+  p.n_out = n_out;
+  p.n_in = (int)n_in;
+  p.c_in = c_in;
+  p.c_out = c_out;
+  p.V = volume;
+  p.all_bits = volume == 32 ? 0xffffffffu : ((1u << volume) - 1u);
+  p.n_pad = n_pad;
+  p.kc = (k_pad % 64 == 0) ? 64 : ((k_pad % 32 == 0) ? 32 : 16);
+  p.swz = p.kc * 2;
+  p.n_kchunks = k_pad / p.kc;
+  p.epi_cols = (n_pad % 32 == 0) ? 32 : 16;
+  p.relu = relu;
+  p.interleave = 1;
+  // M = 256 over the pair, N = n_pad (each CTA holds n_pad / 2 weight rows)
+  p.idesc = (1u << 4) | ((uint32_t)(n_pad >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+  p.nacc = 2;
+  uint32_t cols = 32;
+  while (cols < (uint32_t)(p.nacc * n_pad)) cols *= 2;
+  p.tmem_cols = cols;
+  if (ctas <= 0) ctas = cols <= 256 ? 2 : 1;
+  if (ctas >= 2 && cols > 256) ctas = 1;
+  p.total_tiles = (int)((n_out + BM - 1) / BM);
+  auto r1024 = [](uint32_t x) { return (x + 1023u) / 1024u * 1024u; };
+  p.b_tx = (uint32_t)((n_pad / 2) * p.kc * 2);
+  p.a_off_bytes = r1024((uint32_t)(BM * p.kc * 2));
+  p.b_off_bytes = r1024(p.b_tx);
+  const uint32_t op_bytes = p.a_off_bytes + p.b_off_bytes;
+  const int it_per_op = p.kc / 8;
+  const int skb = stage_kb > 0 ? stage_kb : (ctas == 2 ? 36 : 64);
+  int ops = (int)((uint32_t)skb * 1024u / op_bytes);
+  ops = std::max(1, std::min(ops, std::min(std::min(MAX_OPS, volume), max_idx(ctas) / it_per_op)));
+  p.ldf = ldf;
+  p.ldh = hits_ld(n_out);
+  p.feat = (const __half*)features;
+  p.feat2 = (const __half*)features2;
+  p.ldf2 = ldf2;
+  p.c_split = features2 ? c_split : c_in;
+  p.hits = hits;
+  p.tmask = hits ? tile_mask : nullptr;
+  p.scale = scale;
+  p.shift = shift;
+  p.bias = bias;
+  p.residual = (const __half*)residual;
+  p.orow = out_rows;
+  p.ldo = ldo;
+  p.out = (__half*)out;
+  const int idx_slots = hits ? 8 : 0;
+  auto fixed_bytes = [&](int epi_bufs) {
+    return 1024 + 4 * epi_bufs * EPI_BUF + idx_slots * ops * BM * 4 + (40 + 2 * idx_slots) * 8 + 64;
+  };
+  const int smem_cap = ctas == 2 ? 113 * 1024 : 227 * 1024;
+  int st = 0, epi_bufs = 1;
+  for (;;) {
+    const int sb = ops * (int)op_bytes;
+    const int s1 = (smem_cap - fixed_bytes(1)) / sb, s2 = (smem_cap - fixed_bytes(2)) / sb;
+    epi_bufs = s2 == s1 ? 2 : 1;
+    st = std::min(epi_bufs == 2 ? s2 : s1, 16);
+    if (st >= 2 || ops == 1) break;
+    --ops;
+  }
+  SCB_CHECK_ARG(st >= 2, "pair stage does not fit in shared memory");
+  p.ops = ops;
+  p.idx_slots = idx_slots;
+  p.idx_slot_bytes = (uint32_t)(ops * BM * 4);
+  p.a_stages = st;
+  p.b_stages = 0;
+  p.epi_bufs = epi_bufs;
+  p.a_stage_bytes = ops * op_bytes;
+  p.b_stage_bytes = 0;
+  const int smem = fixed_bytes(epi_bufs) + st * (int)p.a_stage_bytes;
+
+  CUtensorMap mB, mO;
+  std::string err;
+  if (!cached_map_f16(&mB, weights_packed, k_pad, (long long)volume * n_pad, k_pad, p.kc,
+                      n_pad / 2, p.swz, err) ||
+      !cached_map_f16(&mO, out, c_out, n_out, ldo, p.epi_cols, 32, p.epi_cols * 2, err)) {
+    set_error(std::string("scb_conv_implicit (pair): ") + err);
+    return SCB_ECUDA;
+  }
+  const int pair_tiles = (p.total_tiles + 1) / 2;
+  const int clusters = std::min(pair_tiles, ctas * device_sms() / 2);
+  cudaStream_t s = as_stream(stream);
+  auto launch = [&](auto kernel) -> int {
+    const int rc = set_smem_once(kernel, smem_cap);
+    if (rc != SCB_OK) return rc;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * clusters);
+    cfg.blockDim = dim3(PAIR_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = env.pdl ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    SCB_CUDA(cudaLaunchKernelEx(&cfg, kernel, mB, mO, p));
+    return SCB_OK;
+  };
+  int rc = SCB_EINVAL;
+#define SCB_PAIR_LAUNCH_C(VV, KK)                                              \
+  rc = ctas == 2 ? launch(implicit_conv_pair_kernel<VV, KK, 2>)                \
+                 : launch(implicit_conv_pair_kernel<VV, KK, 1>);
+#define SCB_PAIR_LAUNCH_K(VV)                                                  \
+  if (p.kc == 64) { SCB_PAIR_LAUNCH_C(VV, 64) }                                \
+  else if (p.kc == 32) { SCB_PAIR_LAUNCH_C(VV, 32) }                           \
+  else { SCB_PAIR_LAUNCH_C(VV, 16) }
+  if (volume == 27) {
+    SCB_PAIR_LAUNCH_K(27)
+  } else if (volume == 8) {
+    SCB_PAIR_LAUNCH_K(8)
+  } else {
+    SCB_PAIR_LAUNCH_K(1)
+  }
+#undef SCB_PAIR_LAUNCH_K
+#undef SCB_PAIR_LAUNCH_C
+  if (rc != SCB_OK) return rc;
+  SCB_LAUNCHED();
+  return SCB_OK;
+}
+
+}  // namespace
+
 extern "C" int32_t scb_conv_implicit_rows(const void* features, int64_t ldf, int32_t c_split,
                                           const void* features2, int64_t ldf2, int64_t n_in,
                                           int32_t c_in, const int32_t* hits, int32_t volume,
@@ -694,7 +1160,8 @@ extern "C" int32_t scb_conv_implicit_rows(const void* features, int64_t ldf, int
                                           int32_t stage_kb, scb_stream_t stream) {
   using namespace ic;
   SCB_CHECK_ARG(out_rows == nullptr || hits != nullptr, "permuted output rows need a hit matrix");
-  SCB_CHECK_ARG(ctas_per_sm >= 0 && ctas_per_sm <= 3, "ctas_per_sm must be 0 (auto) or 1..3");
+  SCB_CHECK_ARG(ctas_per_sm >= 0 && ctas_per_sm <= 5,
+                "ctas_per_sm must be 0 (auto), 1..3 (single-CTA kernel) or 4..5 (CTA pairs, 1..2 per SM)");
   SCB_CHECK_ARG(stage_kb == 0 || (stage_kb >= 8 && stage_kb <= 200),
                 "stage_kb must be 0 (auto) or 8..200");
   SCB_CHECK_ARG(features2 == nullptr || (c_split % 8 == 0 && c_split > 0 && c_split < c_in &&
@@ -717,6 +1184,10 @@ extern "C" int32_t scb_conv_implicit_rows(const void* features, int64_t ldf, int
   SCB_CHECK_ARG(n_pad <= 256, "C_out > 256 not supported by the implicit conv");
   if (n_out == 0) return SCB_OK;
   const IcEnv& env = ic_env();
+  if (ctas_per_sm >= 4 || (ctas_per_sm == 0 && env.pair))
+    return launch_pair(features, ldf, c_split, features2, ldf2, n_in, c_in, hits, volume, n_out,
+                       tile_mask, out_rows, weights_packed, c_out, out, ldo, scale, shift, bias,
+                       residual, relu, ctas_per_sm >= 4 ? ctas_per_sm - 3 : 0, stage_kb, stream);
   Params p;
   memset(&p, 0, sizeof(p));
   p.n_out = n_out;

@@ -93,7 +93,7 @@ class EngineMinkUNet:
     the input tensor's order — the same result either way."""
 
     def __init__(self, width: float, in_channels: int = 4, seed: int = 0,
-                 reorder: bool | None = None):
+                 reorder: bool | None = None, strategy=None):
         import os
         import torch
         from .core import WeightTensor
@@ -112,10 +112,88 @@ class EngineMinkUNet:
         for name, w in self.w.items():
             w.packed_f16()
         self.reorder = (os.environ.get("SCB_REORDER", "1") == "1") if reorder is None else reorder
+        # a side stream for the coordinate levels' maps (SCB_MAP_STREAM=0: inline)
+        self.map_stream = (torch.cuda.Stream(priority=-1)
+                           if os.environ.get("SCB_MAP_STREAM", "1") == "1" else None)
+        self.chain_stream = torch.cuda.Stream(priority=-1) if self.map_stream else None
         from .execution import InflightLimiter
         self.inflight = InflightLimiter(int(os.environ.get("SCB_INFLIGHT", "3")))
         self._pending = {}   # id(coordset) -> (coordset, level-0 set, deferred chain)
         self._specs = {}
+        self._tune = None    # set by tune_kernel_shapes for one forward
+        import collections
+        self._retained = collections.deque()   # (end event, map objects) per forward
+        # per-layer fused-kernel launch shapes from a JSON v1 strategy file
+        # (autotune.save_strategy; the "kernel" extension of the records)
+        self.kernel_shapes = {}
+        if strategy is not None:
+            from .autotune import StrategyFile, load_strategy
+            sf = strategy if isinstance(strategy, StrategyFile) else load_strategy(strategy)
+            self.kernel_shapes = {r.layer_id: (r.ctas, r.stage_kb) for r in sf.layers
+                                  if r.ctas or r.stage_kb}
+
+    def tune_kernel_shapes(self, t, options=None, shapes=None, repeats: int = 7,
+                           rel_tol: float = 0.02):
+        """Time every fused layer of one forward over ``t`` under each launch
+        shape (autotune.KERNEL_SHAPES: CTAs per SM, stage KB, single-CTA or
+        CTA-pair kernel) with CUDA events, keep a shape only when it beats the
+        default by ``rel_tol``, and return the JSON v1 StrategyFile (the
+        B200 counterpart of the reference's per-layer tune_layer records,
+        autotune.py:147-218).  The tuned shapes also become this model's."""
+        from .autotune import KERNEL_SHAPES, LayerRecord, StrategyFile
+        self._tune = {"shapes": tuple(shapes or KERNEL_SHAPES), "repeats": repeats,
+                      "rel_tol": rel_tol, "best": {}}
+        saved = dict(self.kernel_shapes)
+        self.kernel_shapes = {}
+        try:
+            self.forward(t, options)
+        finally:
+            best = self._tune["best"]
+            self._tune = None
+        self.kernel_shapes = {k: v for k, v in best.items() if v != (0, 0)} or saved
+        recs = tuple(LayerRecord(l["name"], 0.0, float("inf"), "auto", "auto",
+                                 *best.get(l["name"], (0, 0))) for l in self.table)
+        return StrategyFile(layers=recs, dataset="semantickitti-shaped raycast scans")
+
+    def _release_retained(self, limit: int = 8) -> None:
+        """Drop the map objects of forwards whose end event has completed
+        (their blocks may then be reused by the mapping streams)."""
+        r = self._retained
+        while r and (r[0][0].query() or len(r) > limit):
+            r[0][0].synchronize()
+            r.popleft()
+
+    def _tuned_call(self, name, call, base):
+        """Run ``call(opts)`` for layer ``name``; while tuning, first time it
+        under every launch shape and keep the fastest."""
+        from dataclasses import replace
+        tune = self._tune
+        if tune is None:
+            return call(base)
+        import torch
+        timings = []
+        for shape in tune["shapes"]:
+            o = replace(base, kernel_shapes={name: shape})
+            call(o)
+            samples = []
+            for _ in range(tune["repeats"]):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                # keep the GPU busy while the host queues the layer, so the
+                # events bracket device work only (no host-issue gaps)
+                torch.cuda._sleep(300_000)
+                a.record()
+                call(o)
+                b.record()
+                b.synchronize()
+                samples.append(a.elapsed_time(b))
+            timings.append((shape, sorted(samples)[len(samples) // 2]))
+        default = dict(timings).get((0, 0), timings[0][1])
+        best, best_t = (0, 0), default
+        for shape, ms in timings:
+            if ms < best_t * (1.0 - tune["rel_tol"]):
+                best, best_t = shape, ms
+        tune["best"][name] = best
+        return call(replace(base, kernel_shapes={name: best}))
 
     def _down_specs(self):
         from .execution import LayerSpec
@@ -124,25 +202,50 @@ class EngineMinkUNet:
 
     def _start(self, cset, opts):
         """Queue the level-0 set (reordered), its k3 map and the strided
-        coordinate chain; returns (level-0 set, finisher).  The finisher
-        collects the chain's one host read and builds the other levels."""
+        coordinate chain on the current stream; returns (level-0 set,
+        finisher, level-0-ready event).  The finisher collects the chain's one
+        host read and builds the other levels."""
         from .execution import LayerSpec, link_strided_map, prepare_layer_maps, _timed
         from .mapping import enumerate_offsets, reorder_by_presence, start_output_coords_chain
         k3 = LayerSpec(3, 1, 1, 1)
         kind = opts.index_kind or "auto"
         timer = opts.timer
+        import torch
+        l0_start = torch.cuda.Event()
+        l0_start.record()
         with _timed(timer, "L0", "mapping"):
             l0 = reorder_by_presence(cset, 3, kind) if self.reorder else cset
             prepare_layer_maps(l0, k3, opts)
+        l0_ready = torch.cuda.Event()   # what the level-0 convolutions need
+        l0_ready.record()
         specs = self._down_specs()
         dim = len(cset.boundary)
-        with _timed(timer, "chain", "mapping"):
-            chain = start_output_coords_chain(cset, [(enumerate_offsets(dim, sp.kernel_size),
-                                                      sp.stride) for sp in specs])
+        steps = [(enumerate_offsets(dim, sp.kernel_size), sp.stride) for sp in specs]
+        if self.chain_stream is not None:
+            # the coordinate pyramid needs the input coordinates only: it runs
+            # beside the level-0 maps instead of behind them (the level-1 maps
+            # wait for it, and the convolutions wait for those)
+            cs_ = self.chain_stream
+            cs_.wait_event(l0_start)
+            with torch.cuda.stream(cs_), _timed(timer, "chain", "mapping"):
+                chain0 = start_output_coords_chain(cset, steps)
+            chain_done = torch.cuda.Event()
+            chain_done.record(cs_)
+
+            def chain():
+                out = chain0()
+                torch.cuda.current_stream().wait_event(chain_done)
+                return out
+        else:
+            with _timed(timer, "chain", "mapping"):
+                chain = start_output_coords_chain(cset, steps)
 
         def finish():
+            """Build levels 1..4; returns an event per level, recorded on the
+            current stream when the level's maps are queued."""
+            import torch
             from .core import CoordinateSet
-            fine = l0
+            fine, events = l0, []
             for i, (sp, (oc, ob)) in enumerate(zip(specs, chain()), 1):
                 with _timed(timer, f"L{i}", "mapping"):
                     lvl = CoordinateSet(oc, ob, cset.batch_size)
@@ -150,16 +253,28 @@ class EngineMinkUNet:
                         lvl = reorder_by_presence(lvl, 3, kind)
                     link_strided_map(fine, lvl, sp, opts)
                     prepare_layer_maps(lvl, k3, opts)
+                ev = torch.cuda.Event()
+                ev.record()
+                events.append(ev)
                 fine = lvl
-        return l0, finish
+            return events
+        return l0, finish, l0_ready
 
-    def prefetch(self, t, options=None) -> None:
-        """Queue ``t``'s level-0 map and its strided coordinate chain now
-        (B200 extension).  A serving loop calls this for batch i+1 before it
-        runs batch i: the chain's one host read, collected in forward(batch
-        i+1), then finds its kernels long finished instead of draining the
-        compute queue each forward.  Same maps, same results.  At most one
-        batch is held (a newer prefetch replaces an unused older one)."""
+    def prefetch(self, t, options=None, coords_ready=None) -> None:
+        """Queue ``t``'s level-0 maps and its strided coordinate chain now, on
+        the mapping streams (B200 extension).  A serving loop calls this for
+        batch i+1 before forward(batch i): the mapping then runs beside batch
+        i's convolutions, and forward(batch i+1) finds it done.  Same maps,
+        same results.  ``coords_ready``: an event after which t's coordinates
+        -- and anything already built on them, e.g. the hash index of
+        ``validate="async"`` -- are on the device (default: everything queued
+        on the current stream).
+        Memory the mapping streams allocate is retained per forward until
+        that forward's end event has completed, so prefetched mapping never
+        reuses a block a queued convolution still reads.  At most one batch
+        is held (a newer prefetch replaces an unused older one)."""
+        import torch
+        from contextlib import nullcontext
         from dataclasses import replace
         from .execution import ExecOptions
         opts = replace(options) if options is not None else ExecOptions()
@@ -169,8 +284,16 @@ class EngineMinkUNet:
         key = id(t.coordset)
         if key in self._pending:
             return
-        l0, finish = self._start(t.coordset, opts)
-        self._pending = {key: (t.coordset, l0, finish)}
+        ms = self.map_stream
+        if ms is not None:
+            self._release_retained()
+            if coords_ready is not None:
+                ms.wait_event(coords_ready)
+            else:
+                ms.wait_stream(torch.cuda.current_stream())
+        with (torch.cuda.stream(ms) if ms is not None else nullcontext()):
+            l0, finish, ready = self._start(t.coordset, opts)
+        self._pending = {key: (t.coordset, l0, finish, ready)}
 
     def forward(self, t, options=None):
         from .core import SparseTensor
@@ -179,6 +302,8 @@ class EngineMinkUNet:
         from .mapping import permute_rows
         from dataclasses import replace
         base = replace(options) if options is not None else ExecOptions()  # private copy
+        if self.kernel_shapes:
+            base.kernel_shapes = {**self.kernel_shapes, **(base.kernel_shapes or {})}
         cache = {}
 
         specs = self._specs
@@ -198,8 +323,11 @@ class EngineMinkUNet:
                     spec = LayerSpec(k, s, w.c_in, w.c_out, reuse_key=name if s > 1 else None)
                 specs[name] = spec
             if kind == "inverse":
-                return inverse_conv_forward(x, w, spec, cache, None, opts, epilogue=ep)
-            return sparse_conv_forward(x, w, spec, None, cache, opts, epilogue=ep, concat=concat)
+                call = lambda o: inverse_conv_forward(x, w, spec, cache, None, o, epilogue=ep)
+            else:
+                call = lambda o: sparse_conv_forward(x, w, spec, None, cache, o, epilogue=ep,
+                                                     concat=concat)
+            return self._tuned_call(name, call, opts)
 
         def res(x, prefix, has_proj, skip=None):
             # relu(BN(conv2(h)) + shortcut): the residual add and ReLU run in
@@ -209,18 +337,34 @@ class EngineMinkUNet:
             sc = conv(x, prefix + ".proj", 1, 1, relu=False, concat=skip) if has_proj else x
             return conv(h, prefix + ".c2", 3, 1, relu=True, residual=sc)
 
+        import torch
+        from contextlib import nullcontext
         names = {l["name"] for l in self.table}
         self.inflight.before_forward()
         finish, l0 = None, t.coordset
+        compute = torch.cuda.current_stream()
+        ms = self.map_stream if base.map_reuse else None
+        on_maps = torch.cuda.stream(ms) if ms is not None else nullcontext()
+        if ms is not None:
+            self._release_retained()
         if base.map_reuse:
             # level-0 set and map plus the k2/s2 coordinate chain are queued
             # first (or were, by prefetch()); the chain's count read is
             # collected after the level-0 stems are queued
             hit = self._pending.pop(id(t.coordset), None)
             if hit is not None and hit[0] is t.coordset:
-                _, l0, finish = hit
+                _, l0, finish, l0_ready = hit
             else:
-                l0, finish = self._start(t.coordset, base)
+                if ms is not None:
+                    # mapping on its own (high-priority) stream: it needs only
+                    # the coordinates, and waiting for everything queued so
+                    # far also keeps it from reusing blocks the previous
+                    # forward still reads
+                    ms.wait_stream(compute)
+                with on_maps:
+                    l0, finish, l0_ready = self._start(t.coordset, base)
+            if ms is not None:   # the level-0 maps, not the coordinate chain behind them
+                compute.wait_event(l0_ready)
         x = t
         if l0 is not t.coordset:  # relabelled level 0: permute the input rows once
             with _timed(base.timer, "input", "permute"):
@@ -228,10 +372,14 @@ class EngineMinkUNet:
                                        t.batch_size, l0)
         x = conv(x, "stem.0", 3, 1)
         x = conv(x, "stem.1", 3, 1)
+        level_ready = [None] * 4
         if finish is not None:  # both level-0 stems are queued: the GPU stays busy meanwhile
-            finish()
+            with on_maps:       # levels 1-4 map while the compute stream convolves
+                level_ready = finish()
         skips = [x]
         for i in range(1, 5):
+            if ms is not None and level_ready[i - 1] is not None:
+                compute.wait_event(level_ready[i - 1])
             x = conv(x, f"down{i}", 2, 2)
             x = res(x, f"enc{i}.r0", f"enc{i}.r0.proj" in names)
             x = res(x, f"enc{i}.r1", f"enc{i}.r1.proj" in names)
@@ -248,4 +396,8 @@ class EngineMinkUNet:
                 back = permute_rows(rows, l0.perm, scatter=True)[:, : f.shape[1]]
             out = SparseTensor._wrap(back, out.stride, out.boundary, out.batch_size, t.coordset)
         self.inflight.after_forward()
+        if ms is not None:
+            # keep this forward's map objects (allocated on the mapping
+            # streams) alive until its convolutions have run
+            self._retained.append((self.inflight.events[-1], (t.coordset, l0)))
         return out

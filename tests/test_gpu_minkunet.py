@@ -88,3 +88,38 @@ def test_prefetched_pyramid_is_identical(scan):
     np.testing.assert_array_equal(o1.features_numpy(), ref1)
     np.testing.assert_array_equal(o2.coords_numpy(), ref2.coords_numpy())
     np.testing.assert_array_equal(o2.features_numpy(), ref2.features_numpy())
+
+
+def test_serving_loop_prefetch_overlap(scan):
+    """The bench's serving loop: forward(batch i), then upload + prefetch
+    batch i+1 on the mapping streams (beside batch i's convolutions), with
+    the host running ahead (no synchronisation) over alternating inputs:
+    every output equals a plain, synchronised forward of the same input."""
+    import torch
+    import paper_2204_10319_b200 as sc
+    from paper_2204_10319_b200 import workloads
+    from paper_2204_10319_b200.minkunet import EngineMinkUNet
+    model = EngineMinkUNet(0.5, 4, 0)
+    opts = sc.ExecOptions(dataflow="auto", index_kind="hash")
+    inputs = [scan, _crop(workloads.semantickitti_scan(1), 0.25),
+              _crop(workloads.semantickitti_scan(2), 0.5)]
+
+    def tensor(c, f, b):
+        return sc.quantize_features(sc.SparseTensor(c, f, 1, b, 1), sc.PrecisionMode.FP16_STORAGE)
+
+    refs = []
+    for c, f, b in inputs:
+        o = model.forward(tensor(c, f, b), opts)
+        refs.append((o.coords_numpy(), o.features_numpy()))
+    outs, order = [], [0, 1, 2, 1, 0, 2, 2, 1]
+    t = tensor(*inputs[order[0]])
+    for i, j in enumerate(order):
+        o = model.forward(t, opts)
+        outs.append((j, o))
+        if i + 1 < len(order):
+            t = tensor(*inputs[order[i + 1]])
+            ev = torch.cuda.current_stream().record_event()
+            model.prefetch(t, opts, coords_ready=ev)
+    for j, o in outs:
+        np.testing.assert_array_equal(o.coords_numpy(), refs[j][0])
+        np.testing.assert_array_equal(o.features_numpy(), refs[j][1])

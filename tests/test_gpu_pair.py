@@ -1,0 +1,105 @@
+"""The CTA-pair form of the fused conv (tcgen05 cta_group::2, M = 256 over
+two SMs): every launch shape matches the single-CTA kernel on
+the same layer, incl. concat inputs, the BN + residual + ReLU epilogue,
+permuted output rows (one-hot maps) and odd tile counts.  Same maps; a pair
+tile runs the union of its two row tiles' offsets, so the offsets grouped
+into a pipeline stage -- and with several K chunks per offset the order of
+the f32 (offset, K-chunk) partial sums -- can differ: outputs agree to
+f32 summation order (measured relative L2 <= 1e-5; bit-identical when C_in
+is one K chunk)."""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def sc():
+    import paper_2204_10319_b200 as sc
+    return sc
+
+
+@pytest.fixture(scope="module")
+def level(sc):
+    from paper_2204_10319_b200 import workloads
+    from paper_2204_10319_b200.mapping import reorder_by_presence
+    c, _, b = workloads.semantickitti_scan(4)
+    t = sc.SparseTensor(c, np.zeros((c.shape[0], 1), np.float32), 1, b, 1)
+    return t, reorder_by_presence(t.coordset, 3, "hash")
+
+
+def _close(got, want):
+    """Equal up to f32 summation order."""
+    g, w = got.float(), want.float()
+    rel = float((g - w).norm() / w.norm().clamp_min(1e-30))
+    return rel <= 1e-4 and bool(torch.allclose(g, w, rtol=4e-3, atol=1e-3))
+
+
+def _run(sc, x, w, spec, shape, ep=None, concat=None):
+    opts = sc.ExecOptions(dataflow="fused", index_kind="hash", layer_label="L",
+                          kernel_shapes={"L": shape})
+    return sc.sparse_conv_forward(x, w, spec, None, None, opts, epilogue=ep, concat=concat).features
+
+
+@pytest.mark.parametrize("cin,cout", [(32, 32), (64, 64), (96, 96), (128, 128), (256, 256),
+                                      (16, 48), (64, 19)])
+def test_pair_equals_single(sc, rng, level, cin, cout):
+    t, p = level
+    n = p.num_points
+    x = sc.SparseTensor._wrap(torch.from_numpy(rng.standard_normal((n, cin)).astype(np.float16))
+                              .cuda(), 1, t.boundary, 1, p)
+    w = sc.WeightTensor(rng.normal(0, 1 / np.sqrt(27 * cin), (27, cin, cout)).astype(np.float32),
+                        3, 3)
+    spec = sc.LayerSpec(3, 1, cin, cout)
+    want = _run(sc, x, w, spec, (2, 0) if cout <= 128 else (1, 0))
+    for shape in ((4, 0), (5, 0), (4, 24), (5, 16)):
+        got = _run(sc, x, w, spec, shape)
+        assert _close(got, want), shape
+
+
+def test_pair_epilogue_concat_odd_tiles(sc, rng, level):
+    t, p = level
+    n = p.num_points
+    tiles = n // 128 - 1
+    tiles -= 1 - tiles % 2                   # an odd row-tile count ...
+    keep = (tiles - 1) * 128 + 37            # ... with a ragged last tile
+    assert ((keep + 127) // 128) % 2 == 1
+    from paper_2204_10319_b200.core import CoordinateSet
+    from paper_2204_10319_b200.mapping import reorder_by_presence
+    cs = reorder_by_presence(CoordinateSet(p.coords[:keep].clone(), t.boundary, 1), 3, "hash")
+    a = torch.from_numpy(rng.standard_normal((keep, 64)).astype(np.float16)).cuda()
+    b = torch.from_numpy(rng.standard_normal((keep, 32)).astype(np.float16)).cuda()
+    res = torch.from_numpy(rng.standard_normal((keep, 96)).astype(np.float16)).cuda()
+    x = sc.SparseTensor._wrap(a, 1, t.boundary, 1, cs)
+    w = sc.WeightTensor(rng.normal(0, 0.05, (27, 96, 96)).astype(np.float32), 3, 3)
+    ep = {"scale": torch.from_numpy(rng.uniform(0.8, 1.2, 96).astype(np.float32)).cuda(),
+          "shift": torch.from_numpy(rng.normal(0, 0.05, 96).astype(np.float32)).cuda(),
+          "residual": res, "relu": True}
+    spec = sc.LayerSpec(3, 1, 96, 96)
+    want = _run(sc, x, w, spec, (2, 0), ep, concat=b)
+    for shape in ((4, 0), (5, 0)):
+        assert _close(_run(sc, x, w, spec, shape, ep, concat=b), want), shape
+
+
+def test_pair_onehot_transposed(sc, rng):
+    """Permuted output rows (scb_conv_implicit_rows) through the pair kernel."""
+    from paper_2204_10319_b200 import workloads
+    c, _, b = workloads.semantickitti_scan(5)
+    n = c.shape[0]
+    t = sc.SparseTensor(c, np.zeros((n, 1), np.float32), 1, b, 1)
+    f = torch.from_numpy(rng.standard_normal((n, 32)).astype(np.float16)).cuda()
+    wd = sc.WeightTensor(rng.normal(0, 0.1, (8, 32, 64)).astype(np.float32), 2, 3)
+    wu = sc.WeightTensor(rng.normal(0, 0.1, (8, 64, 32)).astype(np.float32), 2, 3)
+    cache = {}
+    opts = sc.ExecOptions(dataflow="fused", index_kind="hash")
+    d = sc.sparse_conv_forward(t.replace_features(f), wd,
+                               sc.LayerSpec(2, 2, 32, 64, reuse_key="d"), None, cache, opts)
+    spec = sc.LayerSpec(2, 1, 64, 32, transposed=True, reuse_key="d")
+    outs = []
+    for shape in ((2, 0), (4, 0), (5, 0)):
+        o = sc.ExecOptions(dataflow="fused", index_kind="hash", layer_label="U",
+                           kernel_shapes={"U": shape})
+        outs.append(sc.inverse_conv_forward(d, wu, spec, cache, None, o).features)
+    assert _close(outs[1], outs[0]) and _close(outs[2], outs[0])

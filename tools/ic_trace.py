@@ -43,7 +43,7 @@ def main():
     buf = np.zeros(CTAS * STAGES * 6, dtype=np.int64)
     lib.scb_ic_trace_read(buf.ctypes.data, buf.size)
     tr = buf.reshape(CTAS, STAGES, 6)
-    for cta in range(2):
+    for cta in [int(x) for x in os.environ.get("TRACE_CTAS", "0,1").split(",")]:
         x = tr[cta]
         n = int(np.count_nonzero(x[:, 2]))
         x = x[:n].astype(np.float64)
