@@ -79,7 +79,7 @@ def _engine_levels(cloud, reorder):
     model = EngineMinkUNet(0.5, 4, 0, reorder=reorder)
     t = sc.SparseTensor(coords, feats, 1, boundary, bs)
     opts = sc.ExecOptions(index_kind="hash")
-    l0, finish = model._start(t.coordset, opts)
+    l0, finish, _ = model._start(t.coordset, opts)
     finish()
     levels, cs = [], l0
     for i in range(5):
