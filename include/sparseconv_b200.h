@@ -129,6 +129,17 @@ int32_t scb_map_search(int32_t kind, const int32_t* out_coords, int64_t n_out,
                        const scb_grid_t* in_grid, int32_t kernel_size, int32_t offset_base,
                        int32_t stride, int32_t symmetric, const int64_t* table_keys, const int32_t* table_rows,
                        int64_t slots, int32_t* hits, scb_stream_t stream);
+
+/* scb_map_search over a dilated window (B200 extension; the reference has no
+ * dilation, north_star's SparseConv3d has): entry (j, k) whenever
+ * stride*q_k + dilation*delta_n is input j.  dilation = 1 is scb_map_search;
+ * symmetric probing is valid for stride 1 and odd K at any dilation. */
+int32_t scb_map_search_dilated(int32_t kind, const int32_t* out_coords, int64_t n_out,
+                               const scb_grid_t* in_grid, int32_t kernel_size,
+                               int32_t offset_base, int32_t stride, int32_t dilation,
+                               int32_t symmetric, const int64_t* table_keys,
+                               const int32_t* table_rows, int64_t slots, int32_t* hits,
+                               scb_stream_t stream);
 /* Per-offset compaction of a hit matrix into the canonical CSR map
  * (offset_ptr[V+1] int64, in_idx/out_idx int32, entries of each offset sorted
  * by output row).  Two phases so the caller can size in_idx/out_idx:

@@ -156,7 +156,7 @@ def _lookup(sorted_keys, order, in_boundary, batch_size, probe):
 
 
 def kernel_map(in_coords, in_boundary, out_coords, kernel_size, stride,
-               batch_size=1, use_symmetry=None):
+               batch_size=1, use_symmetry=None, dilation=1):
     """Per-offset (j, k) pairs with p_j == s*q_k + delta_n, rows sorted by k
     (mapping.py:289-319); stride-1 odd-K maps derive the upper half from the
     lower half (mapping.py:322-339).  Returns a list of (m_n, 2) int64."""
@@ -175,7 +175,7 @@ def kernel_map(in_coords, in_boundary, out_coords, kernel_size, stride,
     pairs = [np.empty((0, 2), dtype=np.int64) for _ in range(volume)]
     for n in searched:
         probe = cout.copy()
-        probe[:, 1:] = stride * cout[:, 1:] + off[n]
+        probe[:, 1:] = stride * cout[:, 1:] + dilation * off[n]   # dilation: B200 extension
         j = _lookup(sorted_keys, order, in_boundary, batch_size, probe)
         k = np.nonzero(j != MISS)[0]
         pairs[n] = np.stack([j[k], k], axis=1).astype(np.int64)
@@ -331,7 +331,7 @@ def quantize(features, precision):
 
 
 def conv_forward(coords, features, boundary, weights, kernel_size, stride,
-                 batch_size=1, return_map=False):
+                 batch_size=1, return_map=False, dilation=1):
     """One sparse conv layer (execution.py:450-509).
 
     Returns (out_coords, out_features[storage dtype], out_boundary) and, with
@@ -350,7 +350,8 @@ def conv_forward(coords, features, boundary, weights, kernel_size, stride,
     else:
         out_boundary = downsample_boundary(boundary, stride)
         out_coords = output_coords(coords, kernel_size, stride, out_boundary, batch_size)
-    pairs = kernel_map(coords, boundary, out_coords, kernel_size, stride, batch_size)
+    pairs = kernel_map(coords, boundary, out_coords, kernel_size, stride, batch_size,
+                       dilation=dilation)
     center = center_of(kernel_size, dim)
     skip = center if stride == 1 else None
     pl = plan(pairs, coords.shape[0], out_coords.shape[0], skip)

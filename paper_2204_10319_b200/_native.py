@@ -62,6 +62,8 @@ _SIGS = {
     "scb_voxelize_batch": (_I32, [_P, _P, _I32, _I64, _I32, _I32, ctypes.c_double, _I32, _P, _I64,
                                   _P, _P, _P, _P]),
     "scb_map_search": (_I32, [_I32, _P, _I64, _GP, _I32, _I32, _I32, _I32, _P, _P, _I64, _P, _P]),
+    "scb_map_search_dilated": (_I32, [_I32, _P, _I64, _GP, _I32, _I32, _I32, _I32, _I32, _P, _P,
+                                      _I64, _P, _P]),
     "scb_map_workspace": (_I64, [_I32, _I64]),
     "scb_map_count": (_I32, [_P, _I32, _I64, _P, _P, _P]),
     "scb_map_compact": (_I32, [_P, _I32, _I64, _P, _P, _P, _P, _P]),

@@ -430,13 +430,15 @@ namespace scb {
 // input row.  blockIdx.y is the offset so hit-matrix writes are coalesced.
 template <int D>
 __global__ void map_search_kernel(int kind, const int* __restrict__ out_coords, long long n_out,
-                                  Grid gin, int K, int lo, int s, int V, int symmetric,
+                                  Grid gin, int K, int lo, int s, int dil, int V, int symmetric,
                                   const long long* __restrict__ keys,
                                   const int* __restrict__ rows, unsigned long long mask,
                                   int* __restrict__ hits) {
   const int n = blockIdx.y;
   int delta[D];
   offset_of<D>(n, K, lo, delta);
+#pragma unroll
+  for (int d = 0; d < D; ++d) delta[d] *= dil;   // dilated window (dil = 1: the reference's)
   const int center = (V - 1) / 2;
   for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n_out;
        k += (long long)gridDim.x * blockDim.x) {
@@ -736,12 +738,14 @@ __global__ void plan_build_kernel(const long long* __restrict__ offset_ptr,
 
 }  // namespace scb
 
-extern "C" int32_t scb_map_search(int32_t kind, const int32_t* out_coords, int64_t n_out,
-                                  const scb_grid_t* in_grid, int32_t kernel_size,
-                                  int32_t offset_base, int32_t stride, int32_t symmetric, const int64_t* table_keys,
-                                  const int32_t* table_rows, int64_t slots, int32_t* hits,
-                                  scb_stream_t stream) {
+extern "C" int32_t scb_map_search_dilated(int32_t kind, const int32_t* out_coords, int64_t n_out,
+                                          const scb_grid_t* in_grid, int32_t kernel_size,
+                                          int32_t offset_base, int32_t stride, int32_t dilation,
+                                          int32_t symmetric, const int64_t* table_keys,
+                                          const int32_t* table_rows, int64_t slots, int32_t* hits,
+                                          scb_stream_t stream) {
   SCB_CHECK_ARG(in_grid && in_grid->dim >= 1 && in_grid->dim <= 4, "bad grid");
+  SCB_CHECK_ARG(dilation >= 1, "dilation must be >= 1");
   Grid g = to_grid(in_grid);
   int V = 1;
   for (int d = 0; d < g.dim; ++d) V *= kernel_size;
@@ -761,11 +765,20 @@ extern "C" int32_t scb_map_search(int32_t kind, const int32_t* out_coords, int64
   }
   dim3 grid(grid_blocks(n_out, 256, 4096), searched);
   SCB_DISPATCH_DIM(g.dim, map_search_kernel<D><<<grid, 256, 0, s>>>(
-                              kind, out_coords, n_out, g, kernel_size, offset_base, stride, V, sym ? 1 : 0,
-                              (const long long*)table_keys, table_rows,
+                              kind, out_coords, n_out, g, kernel_size, offset_base, stride, dilation,
+                              V, sym ? 1 : 0, (const long long*)table_keys, table_rows,
                               (unsigned long long)(slots - 1), hits));
   SCB_LAUNCHED();
   return SCB_OK;
+}
+
+extern "C" int32_t scb_map_search(int32_t kind, const int32_t* out_coords, int64_t n_out,
+                                  const scb_grid_t* in_grid, int32_t kernel_size,
+                                  int32_t offset_base, int32_t stride, int32_t symmetric,
+                                  const int64_t* table_keys, const int32_t* table_rows,
+                                  int64_t slots, int32_t* hits, scb_stream_t stream) {
+  return scb_map_search_dilated(kind, out_coords, n_out, in_grid, kernel_size, offset_base, stride,
+                                1, symmetric, table_keys, table_rows, slots, hits, stream);
 }
 
 extern "C" int64_t scb_map_workspace(int32_t volume, int64_t n_out) {

@@ -135,12 +135,17 @@ class LayerSpec:
     reuse_key: str | None = None
     index_kind: str | None = None
     strategy: LayerStrategy | None = None
+    dilation: int = 1   # B200 extension (north_star SparseConv3d; the reference has none)
 
     def __post_init__(self):
         if self.stride not in (1, 2):
             raise ValueError(f"unsupported stride {self.stride}")
         if self.transposed and not self.reuse_key:
             raise ValueError("transposed layers need the reuse key of a strided layer")
+        if int(self.dilation) < 1:
+            raise ValueError("dilation must be >= 1")
+        if self.dilation != 1 and (self.stride != 1 or self.transposed):
+            raise ValueError("dilation > 1 is supported for stride-1 (submanifold) layers only")
 
 
 def resolve_strategy(spec: LayerSpec, strategy: LayerStrategy | None) -> LayerStrategy:
@@ -817,7 +822,8 @@ def _layer_maps(cset: CoordinateSet, spec: LayerSpec, strat: LayerStrategy,
         raise GridCapacityError(
             f"grid index needs {_cells(cset.boundary, cset.batch_size)} cells "
             f"(cap {opts.grid_cell_cap}); use the hash index")
-    key = (spec.kernel_size, spec.stride, offsets.base)
+    dil = int(spec.dilation)
+    key = (spec.kernel_size, spec.stride, offsets.base) + ((("dilation", dil),) if dil != 1 else ())
     hit = cset.maps.get(key) if opts.map_reuse else None
     if hit is None:
         if spec.stride == 1:
@@ -828,12 +834,13 @@ def _layer_maps(cset: CoordinateSet, spec: LayerSpec, strat: LayerStrategy,
                                        cset.batch_size)
             out_cset = CoordinateSet(oc, out_boundary, cset.batch_size)
         index = build_index(cset, kind, cell_cap=opts.grid_cell_cap)
-        pres = cset.derived.get(("presence", spec.kernel_size)) if spec.stride == 1 else None
+        pres = (cset.derived.get(("presence", spec.kernel_size))
+                if spec.stride == 1 and dil == 1 else None)
         if pres is not None and offsets.center is not None and offsets.volume <= 32:
             # a presence-reordered level: probe only the present offsets
             kmap = map_search_masked(index, cset, offsets, pres)
         else:
-            kmap = map_search(index, out_cset.coords, offsets, spec.stride)
+            kmap = map_search(index, out_cset.coords, offsets, spec.stride, dilation=dil)
         # stride 1: the output set IS this set; store None, not a
         # self-reference (a cycle would pin the maps until the cyclic GC)
         hit = (None if out_cset is cset else out_cset, kmap)

@@ -533,10 +533,11 @@ class KernelMap:
 
 
 def map_search(in_index: CoordinateIndex, out_coords, offsets: KernelOffsets, stride: int,
-               use_symmetry: bool | None = None) -> KernelMap:
+               use_symmetry: bool | None = None, dilation: int = 1) -> KernelMap:
     """Kernel map: entry (j, k) whenever stride*q_k + delta_n is input j
     (mapping.py:289-319).  Stride-1 odd-K maps probe only offsets up to the
     centre and fill the mirrored half in the same pass (mapping.py:322-339).
+    ``dilation`` (B200 extension): the window's offsets are scaled by it.
     Returns a map holding the hit matrix; the CSR form is compacted on first
     use."""
     oc = out_coords.coords if hasattr(out_coords, "coords") else as_device_coords(out_coords)
@@ -550,11 +551,19 @@ def map_search(in_index: CoordinateIndex, out_coords, offsets: KernelOffsets, st
         raise ValueError("symmetric search needs the output set to equal the input set")
     hits = _hit_matrix(volume, n_out, oc.device)
     grid = nat.make_grid(in_index.boundary, in_index.batch_size)
-    nat.call("scb_map_search", in_index.code, nat.ptr(oc), n_out, grid, offsets.kernel_size,
-             offsets.base, stride, int(bool(use_symmetry)), nat.ptr(in_index.keys),
-             nat.ptr(in_index.rows), in_index.slots, nat.ptr(hits), nat.stream_handle())
-    return KernelMap.from_hits(hits, offsets, stride, in_index.size, n_out,
+    if dilation == 1:
+        nat.call("scb_map_search", in_index.code, nat.ptr(oc), n_out, grid, offsets.kernel_size,
+                 offsets.base, stride, int(bool(use_symmetry)), nat.ptr(in_index.keys),
+                 nat.ptr(in_index.rows), in_index.slots, nat.ptr(hits), nat.stream_handle())
+    else:  # dilated window (B200 extension): probes stride*q + dilation*delta
+        nat.call("scb_map_search_dilated", in_index.code, nat.ptr(oc), n_out, grid,
+                 offsets.kernel_size, offsets.base, stride, int(dilation),
+                 int(bool(use_symmetry)), nat.ptr(in_index.keys), nat.ptr(in_index.rows),
+                 in_index.slots, nat.ptr(hits), nat.stream_handle())
+    kmap = KernelMap.from_hits(hits, offsets, stride, in_index.size, n_out,
                                symmetric=bool(use_symmetry))
+    kmap.dilation = int(dilation)
+    return kmap
 
 
 def map_search_masked(in_index: CoordinateIndex, cset: CoordinateSet, offsets: KernelOffsets,

@@ -156,3 +156,14 @@ def test_workload_generators_are_deterministic():
     keys = O.flatten(c, bnd)
     assert (np.diff(keys) > 0).all()  # unique and sorted by key
     assert f.shape == (c.shape[0], 4)
+
+
+def test_dilation_spec_validation():
+    """Dilation (B200 extension for north_star's SparseConv3d) is a stride-1
+    option; the map cache keys keep dilated and plain maps apart."""
+    import paper_2204_10319_b200 as sc
+    sc.LayerSpec(3, 1, 8, 8, dilation=2)
+    with pytest.raises(ValueError, match="dilation"):
+        sc.LayerSpec(3, 1, 8, 8, dilation=0)
+    with pytest.raises(ValueError, match="stride-1"):
+        sc.LayerSpec(2, 2, 8, 8, dilation=2)
