@@ -20,9 +20,12 @@ ranks by LPT on voxel count (strong scaling).
 `roofline` the dominant kernel (algorithmic bytes / its event time), from K
            more steps instrumented with per-layer CUDA events.
 `cpu_baseline` the UNMODIFIED reference package (baseline/_ref) running the
-           same MinkUNet graph on whole scans, one process per host core
-           (rank 0, N = 1).
-`--impl reference` times that CPU path alone (the reference arm).
+           same MinkUNet graph, one process per host core (rank 0, N = 1); a
+           step's bounded sample is one azimuth sector (1/16 of a scan's
+           voxels, equal-count cuts) per worker, counted as that fraction of
+           a scan (~28 s per whole scan per core otherwise).
+`--impl reference` times that CPU path alone (the reference arm): W warm-up
+           and K timed steps of the same samples.
 """
 
 from __future__ import annotations
@@ -68,7 +71,7 @@ def parse():
     ap.add_argument("--scans-per-gpu", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=60.0,
+    ap.add_argument("--cpu-seconds", type=float, default=30.0,
                     help="CPU-arm budget: steps run until it is used (at least one)")
     ap.add_argument("--strong", type=int, default=None,
                     help="strong scaling over a fixed batch of S scans (config 5: 64)")
@@ -150,36 +153,73 @@ def _cpu_worker_init(width, model, scans):
                           S.LayerSpec(3, 1, 8, 8), options=S.ExecOptions(index_kind="hash"))
 
 
+# The reference's CPU path needs ~28 s per whole MinkUNet-1.0x scan per core,
+# so a step's sample is one azimuth sector per worker: each scan's voxels
+# sorted by azimuth around the scan's centroid and cut into CPU_SECTORS runs of
+# equal voxel count (balanced workers); throughput counts processed voxels as
+# fractions of their scan.  Measured single-process, one thread: a 1/16 sector
+# costs 29 s per scan-equivalent, a whole scan 28 s (1/48: 38 s, fixed per-layer
+# overheads), so 1/16 sectors sample the whole-scan rate.
+CPU_SECTORS = 16
+
+
+def scan_sectors(scan, sectors=CPU_SECTORS):
+    c, f, b = scan
+    x, y = c[:, 1].astype(np.float64), c[:, 2].astype(np.float64)
+    order = np.argsort(np.arctan2(y - y.mean(), x - x.mean()), kind="stable")
+    return [(c[np.sort(part)], f[np.sort(part)], b, part.shape[0] / c.shape[0])
+            for part in np.array_split(order, sectors)]
+
+
 def _cpu_worker_run(i):
+    """Item i: sector (i // scans) % CPU_SECTORS of scan i % scans.
+    Returns (seconds, fraction of a scan processed)."""
     from oracle import reference_runner as R
-    c, f, b = _W["scans"][i % len(_W["scans"])]
+    scans = _W["scans"]
+    if "sectors" not in _W:
+        _W["sectors"] = [scan_sectors(sc_) for sc_ in scans]
+    c, f, b, frac = _W["sectors"][i % len(scans)][(i // len(scans)) % CPU_SECTORS]
     t0 = time.perf_counter()
     if _W["model"] == "minkunet":
         R.minkunet_reference(_W["S"], _W["params"], _W["width"], c, f, b)
     else:
         R.centerpoint_reference(_W["S"], _W["params"], c, f, b)
-    return time.perf_counter() - t0
+    return time.perf_counter() - t0, frac
 
 
 class CpuPath:
     """The reference's own CPU implementation (the unmodified `sparseconv`
     package through its public API, oracle/reference_runner.py) on P worker
-    processes, one host core each; a step = every worker runs one whole scan
-    of the workload's scan set."""
+    processes, one host core each; a step = every worker runs one azimuth
+    sector (1/CPU_SECTORS of a scan's voxels) of the workload's scans."""
 
     def __init__(self, width, scans, procs, model="minkunet"):
         import multiprocessing as mp
         self.procs = max(1, procs)
-        self.pool = mp.get_context("spawn").Pool(self.procs, _cpu_worker_init,
-                                                 (width, model, scans))
+        # one thread per worker process: the BLAS / OpenMP / numba pools size
+        # themselves when the child imports numpy, before any initializer runs,
+        # so the limits go into the environment the children are spawned with
+        # (measured: a sector took ~20 s in an oversubscribed pool, 0.55 s alone)
+        keys = ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS", "NUMBA_NUM_THREADS")
+        saved = {k: os.environ.get(k) for k in keys}
+        os.environ.update({k: "1" for k in keys})
+        try:
+            self.pool = mp.get_context("spawn").Pool(self.procs, _cpu_worker_init,
+                                                     (width, model, scans))
+        finally:
+            for k, v in saved.items():
+                if v is None:
+                    os.environ.pop(k, None)
+                else:
+                    os.environ[k] = v
         self.cursor = 0
 
     def step(self):
         items = list(range(self.cursor, self.cursor + self.procs))
         self.cursor += self.procs
         t0 = time.perf_counter()
-        self.pool.map(_cpu_worker_run, items, chunksize=1)
-        return time.perf_counter() - t0, float(self.procs)  # seconds, scans processed
+        res = self.pool.map(_cpu_worker_run, items, chunksize=1)
+        return time.perf_counter() - t0, float(sum(r[1] for r in res))  # seconds, scans
 
     def close(self):
         self.pool.close()
@@ -203,21 +243,26 @@ def cpu_cores():
         return os.cpu_count() or 1
 
 
-def run_cpu(args, scans, budget_s):
-    """Whole scans on every host core through the reference; steps until
-    `budget_s` is used (at least one).  Returns (value, steps, secs, procs)."""
+def run_cpu(args, scans, budget_s=None, steps=None, warmup=0):
+    """Scan sectors on every host core through the reference: ``warmup``
+    untimed steps, then ``steps`` timed steps (or steps until ``budget_s``
+    seconds, at least one).  Returns (value, steps, secs, procs, scans done)."""
     procs = min(cpu_cores(), 64)
     cpu = CpuPath(args.width, scans, procs, args.model)
-    secs, done, steps = 0.0, 0.0, 0
-    while steps < max(1, args.steps):
+    for _ in range(warmup):
+        cpu.step()
+    secs, done, k = 0.0, 0.0, 0
+    while True:
         s_, d_ = cpu.step()
         secs += s_
         done += d_
-        steps += 1
-        if secs + s_ > budget_s:
+        k += 1
+        if steps is not None and k >= steps:
+            break
+        if steps is None and (secs + s_ > budget_s or k >= 200):
             break
     cpu.close()
-    return done / secs, steps, secs, cpu.procs
+    return done / secs, k, secs, cpu.procs, done
 
 
 def run_reference(args):
@@ -229,16 +274,17 @@ def run_reference(args):
     B = args.scans_per_gpu if args.strong is None else args.strong
     scans = load_scans(range(B), args.model)
     METRIC, UNIT = metric_unit(args)
-    value, steps, secs, procs = run_cpu(args, scans, args.cpu_seconds)
+    value, steps, secs, procs, done = run_cpu(args, scans, steps=args.steps,
+                                              warmup=args.warmup)
     name = "MinkUNet" if args.model == "minkunet" else "CenterPoint-style encoder"
-    sample = (f"{procs} worker processes x 1 whole scan each per step ({name} "
-              f"{args.width if args.model == 'minkunet' else ''}, FP16 storage, hash index), "
-              f"{steps} step(s), {steps * procs} scans in {secs:.1f} s; the unmodified reference "
-              f"package (baseline/_ref) through its own API, 1 BLAS/numba thread per process; "
-              f"numba JIT done per worker before timing")
+    sample = (f"{procs} worker processes x 1 azimuth sector (1/{CPU_SECTORS} of a scan's voxels) "
+              f"per step ({name} {args.width if args.model == 'minkunet' else ''}, FP16 storage, "
+              f"hash index), {steps} timed steps after {args.warmup} warm-up: {done:.2f} scans "
+              f"in {secs:.1f} s; the unmodified reference package (baseline/_ref) through its "
+              f"own API, 1 BLAS/numba thread per process")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
-        "n_gpus": args.gpus, "steps": steps, "steps_requested": args.steps, "warmup": 0,
+        "n_gpus": args.gpus, "steps": steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * secs / steps, "higher_is_better": True,
         "scaling": "weak" if args.strong is None else "strong",
         "vs_baseline": None, "dtype": "f16-storage/f32-accumulate", "data": DATA,
@@ -587,12 +633,12 @@ def main():
     # ---------------- CPU baseline (rank 0, N = 1): the reference on whole scans
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, st, secs, procs = run_cpu(args, scans, args.cpu_seconds)
+        v, st, secs, procs, done = run_cpu(args, scans, budget_s=args.cpu_seconds)
         cpu = {"value": v, "unit": UNIT, "cores": procs, "kind": "reference",
-               "sample": f"{procs} processes x 1 whole scan per step, {st} step(s), "
-                         f"{st * procs} scans in {secs:.1f} s: the unmodified reference package "
-                         f"(baseline/_ref) through its own API on this workload's scans, 1 thread "
-                         f"per process",
+               "sample": f"{procs} processes x 1 azimuth sector (1/{CPU_SECTORS} scan) per step, "
+                         f"{st} step(s), {done:.2f} scans in {secs:.1f} s: the unmodified "
+                         f"reference package (baseline/_ref) through its own API on this "
+                         f"workload's scans, 1 thread per process",
                "cpu": cpu_model()}
 
     if world > 1:
