@@ -134,15 +134,13 @@ _W = {}
 def _cpu_worker_init(width, model, scans):
     for k in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS", "NUMBA_NUM_THREADS"):
         os.environ[k] = "1"
-    from oracle.reference_runner import import_reference
+    from oracle.reference_runner import import_reference, model_tables
     S = import_reference()
     _W.update(S=S, width=width, model=model, scans=scans)
-    if model == "minkunet":
-        from paper_2204_10319_b200.minkunet import build_params
-        _W["params"] = build_params(width, 4, 0)
+    if model == "minkunet":  # numpy-only module: workers never import torch
+        _W["params"] = model_tables("minkunet").build_params(width, 4, 0)
     else:
-        from paper_2204_10319_b200.centerpoint import build_params
-        _W["params"] = build_params(5, 0)
+        _W["params"] = model_tables("centerpoint").build_params(5, 0)
     # numba JIT of the reference's movement kernels, outside any timed step
     rng = np.random.default_rng(0)
     keys = np.sort(rng.choice(16 ** 3, 600, replace=False))
@@ -214,15 +212,22 @@ class CpuPath:
                     os.environ[k] = v
         self.cursor = 0
 
-    def step(self):
-        items = list(range(self.cursor, self.cursor + self.procs))
-        self.cursor += self.procs
+    def run(self, steps: int, timeout_s: float = 900.0):
+        """``steps`` x P samples through the pool as one stream (a worker
+        takes the next sample when it finishes one; no barrier between
+        steps).  Returns (seconds, scans processed)."""
+        items = list(range(self.cursor, self.cursor + steps * self.procs))
+        self.cursor += len(items)
         t0 = time.perf_counter()
-        res = self.pool.map(_cpu_worker_run, items, chunksize=1)
-        return time.perf_counter() - t0, float(sum(r[1] for r in res))  # seconds, scans
+        # a bounded wait: a worker that died would otherwise hang the pool
+        res = self.pool.map_async(_cpu_worker_run, items, chunksize=1).get(timeout_s)
+        return time.perf_counter() - t0, float(sum(r[1] for r in res))
+
+    def step(self, timeout_s: float = 600.0):
+        return self.run(1, timeout_s)
 
     def close(self):
-        self.pool.close()
+        self.pool.terminate()
         self.pool.join()
 
 
@@ -249,18 +254,18 @@ def run_cpu(args, scans, budget_s=None, steps=None, warmup=0):
     seconds, at least one).  Returns (value, steps, secs, procs, scans done)."""
     procs = min(cpu_cores(), 64)
     cpu = CpuPath(args.width, scans, procs, args.model)
-    for _ in range(warmup):
-        cpu.step()
-    secs, done, k = 0.0, 0.0, 0
-    while True:
-        s_, d_ = cpu.step()
-        secs += s_
-        done += d_
-        k += 1
-        if steps is not None and k >= steps:
-            break
-        if steps is None and (secs + s_ > budget_s or k >= 200):
-            break
+    if warmup:
+        cpu.run(warmup)
+    if steps is not None:
+        secs, done = cpu.run(steps)
+        k = steps
+    else:  # steps until the budget is used (at least one)
+        secs, done, k = 0.0, 0.0, 0
+        while True:
+            s_, d_ = cpu.step()
+            secs, done, k = secs + s_, done + d_, k + 1
+            if secs + s_ > budget_s or k >= 200:
+                break
     cpu.close()
     return done / secs, k, secs, cpu.procs, done
 
@@ -277,11 +282,11 @@ def run_reference(args):
     value, steps, secs, procs, done = run_cpu(args, scans, steps=args.steps,
                                               warmup=args.warmup)
     name = "MinkUNet" if args.model == "minkunet" else "CenterPoint-style encoder"
-    sample = (f"{procs} worker processes x 1 azimuth sector (1/{CPU_SECTORS} of a scan's voxels) "
-              f"per step ({name} {args.width if args.model == 'minkunet' else ''}, FP16 storage, "
-              f"hash index), {steps} timed steps after {args.warmup} warm-up: {done:.2f} scans "
-              f"in {secs:.1f} s; the unmodified reference package (baseline/_ref) through its "
-              f"own API, 1 BLAS/numba thread per process")
+    sample = (f"{procs} single-threaded worker processes x 1 azimuth sector (1/{CPU_SECTORS} of a "
+              f"scan's voxels) per step, streamed ({name} "
+              f"{args.width if args.model == 'minkunet' else ''}, FP16 storage, hash index), "
+              f"{steps} timed steps after {args.warmup} warm-up: {done:.2f} scans in {secs:.1f} s; "
+              f"the unmodified reference package (baseline/_ref) through its own API")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": steps, "warmup": args.warmup,
@@ -449,6 +454,9 @@ def layer_table_rows(samples, steps):
 
 def main():
     args = parse()
+    import faulthandler
+    # a stuck run leaves its stacks in the log instead of only a timeout
+    faulthandler.dump_traceback_later(900, exit=False)
     if args.impl == "reference":
         return run_reference(args)
     import torch

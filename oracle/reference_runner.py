@@ -37,11 +37,28 @@ def import_reference():
                       + ", ".join(str(p) for p in _CANDIDATES))
 
 
+def model_tables(name: str):
+    """The engine's model module (layer table, parameters: numpy only)
+    loaded standalone, so CPU worker processes never import torch or the
+    engine package."""
+    import importlib.util
+    from pathlib import Path
+    key = "_scb_tables_" + name
+    mod = sys.modules.get(key)
+    if mod is None:
+        path = Path(__file__).resolve().parent.parent / "paper_2204_10319_b200" / f"{name}.py"
+        spec = importlib.util.spec_from_file_location(key, path)
+        mod = importlib.util.module_from_spec(spec)
+        sys.modules[key] = mod
+        spec.loader.exec_module(mod)
+    return mod
+
+
 def minkunet_reference(S, params: dict, width: float, coords, feats, boundary,
                        batch_size: int = 1, in_channels: int = 4):
     """MinkUNet (paper_2204_10319_b200.minkunet.layer_table) on reference
     ``S``: FP16 storage, hash index; returns (coords, logits, boundary)."""
-    from paper_2204_10319_b200.minkunet import layer_table
+    layer_table = model_tables("minkunet").layer_table
     names = {l["name"] for l in layer_table(width, in_channels)}
     t = S.quantize_features(S.SparseTensor(np.asarray(coords, np.int64), feats, 1,
                                            tuple(boundary), batch_size),
@@ -98,7 +115,7 @@ def centerpoint_reference(S, params: dict, coords, feats, boundary, batch_size: 
                           in_channels: int = 5):
     """The CenterPoint-style encoder (paper_2204_10319_b200.centerpoint) on
     reference ``S``: FP16 storage, hash index."""
-    from paper_2204_10319_b200.centerpoint import layer_table
+    layer_table = model_tables("centerpoint").layer_table
     x = S.quantize_features(S.SparseTensor(np.asarray(coords, np.int64), feats, 1,
                                            tuple(boundary), batch_size),
                             S.PrecisionMode.FP16_STORAGE)
