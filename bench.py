@@ -71,8 +71,8 @@ def parse():
     ap.add_argument("--scans-per-gpu", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=30.0,
-                    help="CPU-arm budget: steps run until it is used (at least one)")
+    ap.add_argument("--cpu-steps", type=int, default=12,
+                    help="steps of the in-line cpu_baseline (each: one 1/16-scan sector per core)")
     ap.add_argument("--strong", type=int, default=None,
                     help="strong scaling over a fixed batch of S scans (config 5: 64)")
     ap.add_argument("--layer-csv", default=None,
@@ -248,26 +248,19 @@ def cpu_cores():
         return os.cpu_count() or 1
 
 
-def run_cpu(args, scans, budget_s=None, steps=None, warmup=0):
+def run_cpu(args, scans, steps, warmup=0):
     """Scan sectors on every host core through the reference: ``warmup``
-    untimed steps, then ``steps`` timed steps (or steps until ``budget_s``
-    seconds, at least one).  Returns (value, steps, secs, procs, scans done)."""
+    then ``steps`` steps' worth of samples streamed through the pool.
+    Returns (value, steps, secs, procs, scans done)."""
     procs = min(cpu_cores(), 64)
     cpu = CpuPath(args.width, scans, procs, args.model)
-    if warmup:
-        cpu.run(warmup)
-    if steps is not None:
+    try:
+        if warmup:
+            cpu.run(warmup)
         secs, done = cpu.run(steps)
-        k = steps
-    else:  # steps until the budget is used (at least one)
-        secs, done, k = 0.0, 0.0, 0
-        while True:
-            s_, d_ = cpu.step()
-            secs, done, k = secs + s_, done + d_, k + 1
-            if secs + s_ > budget_s or k >= 200:
-                break
-    cpu.close()
-    return done / secs, k, secs, cpu.procs, done
+    finally:
+        cpu.close()
+    return done / secs, steps, secs, cpu.procs, done
 
 
 def run_reference(args):
@@ -641,12 +634,12 @@ def main():
     # ---------------- CPU baseline (rank 0, N = 1): the reference on whole scans
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, st, secs, procs, done = run_cpu(args, scans, budget_s=args.cpu_seconds)
+        v, st, secs, procs, done = run_cpu(args, scans, steps=args.cpu_steps, warmup=2)
         cpu = {"value": v, "unit": UNIT, "cores": procs, "kind": "reference",
-               "sample": f"{procs} processes x 1 azimuth sector (1/{CPU_SECTORS} scan) per step, "
-                         f"{st} step(s), {done:.2f} scans in {secs:.1f} s: the unmodified "
-                         f"reference package (baseline/_ref) through its own API on this "
-                         f"workload's scans, 1 thread per process",
+               "sample": f"{procs} single-threaded processes x 1 azimuth sector (1/{CPU_SECTORS} "
+                         f"scan) per step, streamed, {st} steps after 2 warm-up: {done:.2f} scans "
+                         f"in {secs:.1f} s: the unmodified reference package (baseline/_ref) "
+                         f"through its own API on this workload's scans",
                "cpu": cpu_model()}
 
     if world > 1:
