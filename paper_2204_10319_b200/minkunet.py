@@ -113,9 +113,13 @@ class EngineMinkUNet:
             w.packed_f16()
         self.reorder = (os.environ.get("SCB_REORDER", "1") == "1") if reorder is None else reorder
         # a side stream for the coordinate levels' maps (SCB_MAP_STREAM=0: inline)
-        self.map_stream = (torch.cuda.Stream(priority=-1)
+        prio = int(os.environ.get("SCB_MAP_PRIORITY", "-1"))
+        # a prefetched batch's mapping starts when the previous batch enters
+        # this level (the deeper levels leave SMs idle); measured best at 2
+        self.prefetch_level = int(os.environ.get("SCB_PREFETCH_LEVEL", "2"))
+        self.map_stream = (torch.cuda.Stream(priority=prio)
                            if os.environ.get("SCB_MAP_STREAM", "1") == "1" else None)
-        self.chain_stream = torch.cuda.Stream(priority=-1) if self.map_stream else None
+        self.chain_stream = torch.cuda.Stream(priority=prio) if self.map_stream else None
         from .execution import InflightLimiter
         self.inflight = InflightLimiter(int(os.environ.get("SCB_INFLIGHT", "3")))
         self._pending = {}   # id(coordset) -> (coordset, level-0 set, deferred chain)
@@ -258,6 +262,7 @@ class EngineMinkUNet:
                 events.append(ev)
                 fine = lvl
             return events
+        finish.chain_done = chain_done if self.chain_stream is not None else None
         return l0, finish, l0_ready
 
     def prefetch(self, t, options=None, coords_ready=None) -> None:
@@ -273,6 +278,7 @@ class EngineMinkUNet:
         that forward's end event has completed, so prefetched mapping never
         reuses a block a queued convolution still reads.  At most one batch
         is held (a newer prefetch replaces an unused older one)."""
+        import os
         import torch
         from contextlib import nullcontext
         from dataclasses import replace
@@ -289,6 +295,9 @@ class EngineMinkUNet:
             self._release_retained()
             if coords_ready is not None:
                 ms.wait_event(coords_ready)
+                deep = getattr(self, "_deep_event", None)
+                if deep is not None and os.environ.get("SCB_PREFETCH_DEEP", "1") == "1":
+                    ms.wait_event(deep)   # behind the last forward's shallow levels
             else:
                 ms.wait_stream(torch.cuda.current_stream())
         with (torch.cuda.stream(ms) if ms is not None else nullcontext()):
@@ -370,16 +379,26 @@ class EngineMinkUNet:
             with _timed(base.timer, "input", "permute"):
                 x = SparseTensor._wrap(permute_rows(t.features, l0.perm), t.stride, t.boundary,
                                        t.batch_size, l0)
+        level_ready = [None] * 4
+        early = (finish is not None and ms is not None
+                 and getattr(finish, "chain_done", None) is not None and finish.chain_done.query())
+        if early:  # a prefetched pyramid is already counted: queue levels 1-4 now
+            with on_maps:
+                level_ready = finish()
         x = conv(x, "stem.0", 3, 1)
         x = conv(x, "stem.1", 3, 1)
-        level_ready = [None] * 4
-        if finish is not None:  # both level-0 stems are queued: the GPU stays busy meanwhile
+        if finish is not None and not early:  # both level-0 stems are queued first
             with on_maps:       # levels 1-4 map while the compute stream convolves
                 level_ready = finish()
         skips = [x]
         for i in range(1, 5):
             if ms is not None and level_ready[i - 1] is not None:
                 compute.wait_event(level_ready[i - 1])
+            if i == self.prefetch_level and ms is not None:
+                # the deep levels leave SMs idle (few tiles): the next batch's
+                # prefetched mapping starts here (prefetch waits on this event)
+                self._deep_event = torch.cuda.Event()
+                self._deep_event.record()
             x = conv(x, f"down{i}", 2, 2)
             x = res(x, f"enc{i}.r0", f"enc{i}.r0.proj" in names)
             x = res(x, f"enc{i}.r1", f"enc{i}.r1.proj" in names)
