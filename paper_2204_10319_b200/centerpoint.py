@@ -64,6 +64,7 @@ class EngineCenterPoint:
     ascending-key order, so the result is the same either way."""
 
     def __init__(self, in_channels: int = 5, seed: int = 0, reorder: bool | None = None):
+        import collections
         import os
         import torch
         from .core import WeightTensor
@@ -79,36 +80,111 @@ class EngineCenterPoint:
         self.reorder = (os.environ.get("SCB_REORDER", "1") == "1") if reorder is None else reorder
         from .execution import InflightLimiter
         self.inflight = InflightLimiter(2)
+        # the coordinate pyramid on a high-priority side stream (SCB_MAP_STREAM=0: inline)
+        self.map_stream = (torch.cuda.Stream(priority=-1)
+                           if os.environ.get("SCB_MAP_STREAM", "1") == "1" else None)
+        self._pending = {}
+        self._retained = collections.deque()   # (end event, map objects) per forward
+        self._deep_event = None
+        self.prefetch_layer = os.environ.get("SCB_CP_PREFETCH_LAYER", "down2")
+
+    def _pyramid(self, cset, opts):
+        """Level-0 set (reordered) and every level's maps, on the current
+        stream; returns (level-0 set, ready event).  Strided k3 levels need
+        one host read of their output count each."""
+        import torch
+        from .execution import LayerSpec, prepare_layer_maps, prepare_reordered_level, _timed
+        from .mapping import reorder_by_presence
+        with _timed(opts.timer, "pyramid", "mapping"):
+            cs0 = reorder_by_presence(cset, 3, opts.index_kind or "auto") \
+                if self.reorder else cset
+            prepare_layer_maps(cs0, LayerSpec(3, 1, 1, 1), opts)
+            cs = cs0
+            strided = [l for l in self.table if l["s"] == 2]
+            for i, l in enumerate(strided):
+                last = i == len(strided) - 1
+                cs = prepare_reordered_level(cs, LayerSpec(3, 2, l["ci"], l["co"]), opts,
+                                             reorder=self.reorder and not last)
+                if not last:
+                    prepare_layer_maps(cs, LayerSpec(3, 1, 1, 1), opts)
+        ev = torch.cuda.Event()
+        ev.record()
+        return cs0, ev
+
+    def _release_retained(self, limit: int = 8) -> None:
+        r = self._retained
+        while r and (r[0][0].query() or len(r) > limit):
+            r[0][0].synchronize()
+            r.popleft()
+
+    def prefetch(self, t, options=None, coords_ready=None) -> None:
+        """Build ``t``'s coordinate pyramid now, on the mapping stream (B200
+        extension, as EngineMinkUNet.prefetch): a serving loop calls it for
+        batch i+1 after forward(batch i), so the pyramid's kernels and host
+        reads overlap batch i's convolutions.  ``coords_ready``: an event
+        after which t's coordinates (and anything built on them) are on the
+        device; default: everything queued on the current stream."""
+        import torch
+        from dataclasses import replace
+        from .execution import ExecOptions
+        opts = replace(options) if options is not None else ExecOptions()
+        ms = self.map_stream
+        if not opts.map_reuse or ms is None:
+            return
+        opts.timer = None
+        key = id(t.coordset)
+        if key in self._pending:
+            return
+        self._release_retained()
+        if coords_ready is not None:
+            ms.wait_event(coords_ready)
+            if self._deep_event is not None:
+                ms.wait_event(self._deep_event)
+        else:
+            ms.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(ms):
+            cs0, ev = self._pyramid(t.coordset, opts)
+        self._pending = {key: (t.coordset, cs0, ev)}
 
     def forward(self, t, options=None):
+        import torch
         from dataclasses import replace
         from .core import SparseTensor
-        from .execution import (ExecOptions, LayerSpec, prepare_layer_maps,
-                                prepare_reordered_level, sparse_conv_forward, _timed)
-        from .mapping import permute_rows, reorder_by_presence
+        from .execution import ExecOptions, LayerSpec, sparse_conv_forward
+        from .mapping import permute_rows
         opts = replace(options) if options is not None else ExecOptions()
         self.inflight.before_forward()
-        x = t
+        compute = torch.cuda.current_stream()
+        ms = self.map_stream if opts.map_reuse else None
+        x, cs0 = t, None
         if opts.map_reuse:  # the coordinate pyramid before any convolution is queued
-            with _timed(opts.timer, "pyramid", "mapping"):
-                cs = reorder_by_presence(t.coordset, 3, opts.index_kind or "auto") \
-                    if self.reorder else t.coordset
-                prepare_layer_maps(cs, LayerSpec(3, 1, 1, 1), opts)
-                if cs is not t.coordset:
-                    x = SparseTensor._wrap(permute_rows(t.features, cs.perm), t.stride,
-                                           t.boundary, t.batch_size, cs)
-                strided = [l for l in self.table if l["s"] == 2]
-                for i, l in enumerate(strided):
-                    last = i == len(strided) - 1
-                    cs = prepare_reordered_level(cs, LayerSpec(3, 2, l["ci"], l["co"]), opts,
-                                                 reorder=self.reorder and not last)
-                    if not last:
-                        prepare_layer_maps(cs, LayerSpec(3, 1, 1, 1), opts)
+            hit = self._pending.pop(id(t.coordset), None)
+            if hit is not None and hit[0] is t.coordset:
+                _, cs0, ev = hit
+            elif ms is not None:
+                self._release_retained()
+                ms.wait_stream(compute)
+                with torch.cuda.stream(ms):
+                    cs0, ev = self._pyramid(t.coordset, opts)
+            else:
+                cs0, ev = self._pyramid(t.coordset, opts)
+            if ms is not None:
+                compute.wait_event(ev)
+            if cs0 is not t.coordset:
+                x = SparseTensor._wrap(permute_rows(t.features, cs0.perm), t.stride,
+                                       t.boundary, t.batch_size, cs0)
         for l in self.table:
             opts.layer_label = l["name"]
+            if l["name"] == self.prefetch_layer and ms is not None:
+                # a prefetched batch's pyramid starts when this forward reaches
+                # its deeper, narrower levels (prefetch waits on this event)
+                self._deep_event = torch.cuda.Event()
+                self._deep_event.record()
             sc, sh = self.bn[l["name"]]
             x = sparse_conv_forward(x, self.w[l["name"]], LayerSpec(3, l["s"], l["ci"], l["co"]),
                                     None, None, opts,
                                     epilogue={"scale": sc, "shift": sh, "relu": True})
         self.inflight.after_forward()
+        if ms is not None and cs0 is not None:
+            self._retained.append((self.inflight.events[-1], (t.coordset, cs0)))
         return x
