@@ -694,7 +694,20 @@ __global__ void __launch_bounds__(PAIR_THREADS, MINB)
     for (g.start(p, ts); !g.done(ts); g.advance(p, ts)) {
       const int nv = __popc(g.mg);
       const long long row0 = (long long)(2 * g.t + (int)rank) * BM;
-      if (p.hits) {
+      if (p.hits && (p.debug & 16)) {   // EXPERIMENT: hit rows straight from global
+        uint32_t x = g.mg;
+#pragma unroll
+        for (int o = 0; o < MAXO; ++o) {
+          const int n = x ? __ffs(x) - 1 : 0;
+          const bool on = x != 0u;
+          x &= x - 1;
+#pragma unroll
+          for (int it = 0; it < IT; ++it) {
+            const long long k = row0 + it * RPI + cr;
+            cur[o * IT + it] = (on && k < p.n_out) ? __ldg(p.hits + (long long)n * p.ldh + k) : -1;
+          }
+        }
+      } else if (p.hits) {
         mbar_wait(ifull + islot, iph);
         const int* tab = reinterpret_cast<const int*>(idx_base + (size_t)islot * p.idx_slot_bytes);
 #pragma unroll
@@ -705,6 +718,9 @@ __global__ void __launch_bounds__(PAIR_THREADS, MINB)
             cur[o * IT + it] = (o < nv && row0 + r < p.n_out) ? tab[o * BM + r] : -1;
           }
         }
+        // the slot's next fill is an async-proxy (bulk copy) write: order this
+        // thread's generic reads of it before that write (WAR across proxies)
+        fence_async_smem();
         mbar_arrive(iempty + islot);
         if (++islot == p.idx_slots) { islot = 0; iph ^= 1; }
       } else {  // identity map (K = 1, s = 1)
@@ -755,7 +771,7 @@ __global__ void __launch_bounds__(PAIR_THREADS, MINB)
   } else if (warp == IDX_WARP) {
     // ============ index loader: each group's hit-matrix rows (this CTA's 128
     // rows of every active offset, contiguous in hits[n][.]) by bulk copy
-    if (lane == 0 && p.hits) {
+    if (lane == 0 && p.hits && !(p.debug & 16)) {
       int slot = 0;
       uint32_t ph = 0;
       GroupIter g;
@@ -1023,6 +1039,7 @@ int32_t launch_pair(const void* features, int64_t ldf, int32_t c_split, const vo
   Params p;
   memset(&p, 0, sizeof(p));
   p.pair = 1;
+  p.debug = env.debug;
   p.n_out = n_out;
   p.n_in = (int)n_in;
   p.c_in = c_in;
