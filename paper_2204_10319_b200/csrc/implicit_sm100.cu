@@ -694,20 +694,7 @@ __global__ void __launch_bounds__(PAIR_THREADS, MINB)
     for (g.start(p, ts); !g.done(ts); g.advance(p, ts)) {
       const int nv = __popc(g.mg);
       const long long row0 = (long long)(2 * g.t + (int)rank) * BM;
-      if (p.hits && (p.debug & 16)) {   // EXPERIMENT: hit rows straight from global
-        uint32_t x = g.mg;
-#pragma unroll
-        for (int o = 0; o < MAXO; ++o) {
-          const int n = x ? __ffs(x) - 1 : 0;
-          const bool on = x != 0u;
-          x &= x - 1;
-#pragma unroll
-          for (int it = 0; it < IT; ++it) {
-            const long long k = row0 + it * RPI + cr;
-            cur[o * IT + it] = (on && k < p.n_out) ? __ldg(p.hits + (long long)n * p.ldh + k) : -1;
-          }
-        }
-      } else if (p.hits) {
+      if (p.hits) {
         mbar_wait(ifull + islot, iph);
         const int* tab = reinterpret_cast<const int*>(idx_base + (size_t)islot * p.idx_slot_bytes);
 #pragma unroll
@@ -771,7 +758,7 @@ __global__ void __launch_bounds__(PAIR_THREADS, MINB)
   } else if (warp == IDX_WARP) {
     // ============ index loader: each group's hit-matrix rows (this CTA's 128
     // rows of every active offset, contiguous in hits[n][.]) by bulk copy
-    if (lane == 0 && p.hits && !(p.debug & 16)) {
+    if (lane == 0 && p.hits) {
       int slot = 0;
       uint32_t ph = 0;
       GroupIter g;
