@@ -309,8 +309,12 @@ __device__ __forceinline__ void epilogue_role(const Params& p, const CUtensorMap
   if (lane == 0) bulk_wait_all();
 }
 
+constexpr int PAIR_THREADS = 64 + NPROD + 128 + 32;   // + warp 10: the index loader
+constexpr int IC_THREADS = PAIR_THREADS;
+constexpr int IDX_WARP = 10;
+
 template <int V, int KC, int MINB>
-__global__ void __launch_bounds__(64 + NPROD + 128, MINB)
+__global__ void __launch_bounds__(IC_THREADS, MINB)
     implicit_conv_f16_kernel(const __grid_constant__ CUtensorMap tmB,
                              const __grid_constant__ CUtensorMap tmOut,
                              const __grid_constant__ Params p) {
@@ -324,13 +328,16 @@ __global__ void __launch_bounds__(64 + NPROD + 128, MINB)
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* b_base = smem + (size_t)p.a_stages * p.a_stage_bytes;
   uint8_t* epi_base = b_base + (size_t)p.b_stages * p.b_stage_bytes;
-  uint64_t* afull = (uint64_t*)(epi_base + 4 * p.epi_bufs * EPI_BUF);
+  uint8_t* idx_base = epi_base + 4 * p.epi_bufs * EPI_BUF;   // [idx_slots][ops][128] int32
+  uint64_t* afull = (uint64_t*)(idx_base + (size_t)p.idx_slots * p.idx_slot_bytes);
   uint64_t* aempty = afull + p.a_stages;
   uint64_t* bfull = aempty + p.a_stages;
   uint64_t* bempty = bfull + p.b_stages;
   uint64_t* tfull = bempty + p.b_stages;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+  uint64_t* ifull = tempty + 2;
+  uint64_t* iempty = ifull + p.idx_slots;
+  uint32_t* tmem_slot = (uint32_t*)(iempty + p.idx_slots);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const TileSeq ts = tile_seq(p);
@@ -347,6 +354,10 @@ __global__ void __launch_bounds__(64 + NPROD + 128, MINB)
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull + a, 1);
       mbar_init(tempty + a, 4);
+    }
+    for (int i = 0; i < p.idx_slots; ++i) {
+      mbar_init(ifull + i, 1);        // the loader's arrive.expect_tx
+      mbar_init(iempty + i, NPROD);   // every producer thread has read its indices
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
@@ -415,7 +426,8 @@ __global__ void __launch_bounds__(64 + NPROD + 128, MINB)
       roff[it] = (uint32_t)(r * (KC * 2)) + ((uint32_t)(cc ^ rxr) << 4);
     }
     int cur[MI], nxt[MI];
-    // input rows of group (t, mg) for this thread's items; -1 = absent
+    // input rows of group (t, mg) for this thread's items straight from the
+    // hit matrix (-1 = absent): the path without the index ring, one group ahead
     auto load_idx = [&](int t, uint32_t mg, int* dst) {
       const long long r0 = (long long)t * BM + cr;
       uint32_t x = mg;
@@ -435,19 +447,43 @@ __global__ void __launch_bounds__(64 + NPROD + 128, MINB)
     };
     const uint32_t ldfb1 = (uint32_t)(p.ldf * 2);   // row strides in bytes (host-checked < 2^32)
     const uint32_t ldfb2 = (uint32_t)(p.ldf2 * 2);
-    int stage = 0;
-    uint32_t phase = 0;
+    int stage = 0, islot = 0;
+    uint32_t phase = 0, iph = 0;
 #ifdef SCB_IC_TRACE
     int nstage = 0;
 #endif
+    const bool ring = p.hits && p.idx_slots > 0;
     GroupIter g;
     g.start(p, ts);
-    if (!g.done(ts)) load_idx(g.t, g.mg, cur);
-    while (!g.done(ts)) {
-      GroupIter gn = g;   // the next group: its rows load while this one copies
-      gn.advance(p, ts);
-      if (!gn.done(ts)) load_idx(gn.t, gn.mg, nxt);
+    if (!ring && !g.done(ts)) load_idx(g.t, g.mg, nxt);
+    for (; !g.done(ts); g.advance(p, ts)) {
       const int nv = __popc(g.mg);
+      const long long row0 = (long long)g.t * BM;
+      if (!ring) {
+#pragma unroll
+        for (int i = 0; i < MI; ++i) cur[i] = nxt[i];
+        GroupIter gn = g;   // the next group's rows load while this one copies
+        gn.advance(p, ts);
+        if (!gn.done(ts)) load_idx(gn.t, gn.mg, nxt);
+      } else {
+        // the group's input rows from the index ring (the loader warp bulk-
+        // copies the hit-matrix rows several groups ahead)
+        mbar_wait(ifull + islot, iph);
+        const int* tab = reinterpret_cast<const int*>(idx_base + (size_t)islot * p.idx_slot_bytes);
+#pragma unroll
+        for (int o = 0; o < MAXO; ++o) {
+#pragma unroll
+          for (int it = 0; it < IT; ++it) {
+            const int r = it * RPI + cr;
+            cur[o * IT + it] = (o < nv && row0 + r < p.n_out) ? tab[o * BM + r] : -1;
+          }
+        }
+        // the slot's next fill is an async-proxy (bulk copy) write: order this
+        // thread's generic reads of it before that write (WAR across proxies)
+        fence_async_smem();
+        mbar_arrive(iempty + islot);
+        if (++islot == p.idx_slots) { islot = 0; iph ^= 1; }
+      }
       for (int kk = 0; kk < p.n_kchunks; ++kk) {
         mbar_wait(aempty + stage, phase ^ 1);
         if (pt == 0) IC_TRACE(nstage, 0);
@@ -484,9 +520,34 @@ __global__ void __launch_bounds__(64 + NPROD + 128, MINB)
 #endif
         if (++stage == p.a_stages) { stage = 0; phase ^= 1; }
       }
-#pragma unroll
-      for (int i = 0; i < MI; ++i) cur[i] = nxt[i];
-      g = gn;
+    }
+  } else if (warp == IDX_WARP) {
+    // ============ index loader: each group's hit-matrix rows (the tile's 128
+    // rows of every active offset, contiguous in hits[n][.]) by bulk copy
+    if (lane == 0 && p.hits && p.idx_slots > 0) {
+      int slot = 0;
+      uint32_t ph = 0;
+      GroupIter g;
+      for (g.start(p, ts); !g.done(ts); g.advance(p, ts)) {
+        mbar_wait_sleep(iempty + slot, ph ^ 1, 20);
+        const long long row0 = (long long)g.t * BM;
+        const long long avail = p.ldh - row0;   // entries of each hit row from row0 on
+        const uint32_t bytes = avail <= 0 ? 0u : (uint32_t)((avail < BM ? avail : BM) * 4);
+        if (bytes) {
+          const int nv = __popc(g.mg);
+          mbar_expect_tx(ifull + slot, (uint32_t)nv * bytes);
+          const uint32_t dst = smem_u32(idx_base + (size_t)slot * p.idx_slot_bytes);
+          uint32_t x = g.mg;
+          for (int o = 0; o < nv; ++o) {
+            const int n = __ffs(x) - 1;
+            x &= x - 1;
+            bulk_load(dst + o * BM * 4, p.hits + (long long)n * p.ldh + row0, bytes, ifull + slot);
+          }
+        } else {
+          mbar_arrive(ifull + slot);
+        }
+        if (++slot == p.idx_slots) { slot = 0; ph ^= 1; }
+      }
     }
   } else if (warp == 1) {
     // ============ MMA issuer.  The whole warp runs the loop (so stage
@@ -556,7 +617,7 @@ __global__ void __launch_bounds__(64 + NPROD + 128, MINB)
         if (++acc == p.nacc) { acc = 0; acc_phase ^= 1; }
       }
     }
-  } else if (warp >= EPI0) {
+  } else if (warp >= EPI0 && warp < EPI0 + 4) {
     epilogue_role(p, &tmOut, tmem_base, tfull, tempty, epi_base, warp, lane, ts);
   }
 
@@ -584,9 +645,6 @@ __global__ void __launch_bounds__(64 + NPROD + 128, MINB)
 //   tempty    4 + 4 epilogue warps of both CTAs -> CTA 0's MMA thread
 // CTA 1's warp 1 relays its full barriers to CTA 0 (after a proxy fence, so
 // the MMA's async-proxy reads see its cp.async data).
-constexpr int PAIR_THREADS = 64 + NPROD + 128 + 32;   // + warp 10: the index loader
-constexpr int IDX_WARP = 10;
-
 template <int V, int KC, int MINB>
 __global__ void __launch_bounds__(PAIR_THREADS, MINB)
     implicit_conv_pair_kernel(const __grid_constant__ CUtensorMap tmB,
@@ -906,7 +964,7 @@ namespace {
 
 // Launch-invariant settings, read once per process.
 struct IcEnv {
-  int interleave, pdl, debug, pair;
+  int interleave, pdl, debug, pair, ring;
 };
 const IcEnv& ic_env() {
   static const IcEnv e = [] {
@@ -915,7 +973,7 @@ const IcEnv& ic_env() {
       return v ? atoi(v) : dflt;
     };
     return IcEnv{env_int("SCB_IC_INTERLEAVE", 1), env_int("SCB_IC_PDL", 1),
-                 env_int("SCB_IC_DEBUG", 0), env_int("SCB_IC_PAIR", 0)};
+                 env_int("SCB_IC_DEBUG", 0), env_int("SCB_IC_PAIR", 0), env_int("SCB_IC_RING", 1)};
   }();
   return e;
 }
@@ -1214,10 +1272,11 @@ extern "C" int32_t scb_conv_implicit_rows(const void* features, int64_t ldf, int
   uint32_t cols = 32;
   while (cols < (uint32_t)(p.nacc * n_pad)) cols *= 2;
   p.tmem_cols = cols;
-  // CTAs per SM: 3 when three accumulator pairs fit and K chunks are 64 wide
-  // (measured 12 % faster for 64->64, slower for narrower inputs), 2
-  // whenever both accumulator pairs fit, else 1.
-  int ctas = (cols <= 128 && p.kc == 64) ? 3 : (cols <= 256 ? 2 : 1);
+  // CTAs per SM: one for gathering layers with 64-wide K chunks (deep A
+  // ring; measured 5-15 % faster than two or three since the index ring
+  // removed the index-load stalls), two whenever both accumulator pairs
+  // fit, else one.
+  int ctas = (p.kc == 64 && hits) ? 1 : (cols <= 256 ? 2 : 1);
   if (ctas_per_sm > 0)  // tuned (autotune.tune_fused_layer): clamped to what TMEM allows
     ctas = (ctas_per_sm >= 3 && cols <= 128) ? 3 : (ctas_per_sm >= 2 && cols <= 256 ? 2 : 1);
   p.total_tiles = (int)((n_out + BM - 1) / BM);
@@ -1253,7 +1312,14 @@ extern "C" int32_t scb_conv_implicit_rows(const void* features, int64_t ldf, int
   // their own depths -- the A ring as deep as the CTA's share allows (the
   // gather latency is what it hides), the B ring 3 deep (L2-resident weights
   // by TMA) -- + epilogue staging + barriers.
-  auto fixed_bytes = [&](int epi_bufs) { return 1024 + 4 * epi_bufs * EPI_BUF + 52 * 8 + 64; };
+  // the index ring: 8 group slots (4 at three CTAs per SM), ops x 512 B each
+  // (not for one-hot maps: one offset per tile, so a ring round trip per
+  // tile costs more than the one-group-ahead register prefetch saves)
+  auto idx_slots_for = [&]() { return (hits && !out_rows && env.ring) ? (ctas >= 3 ? 4 : 8) : 0; };
+  auto fixed_bytes = [&](int epi_bufs) {
+    return 1024 + 4 * epi_bufs * EPI_BUF + idx_slots_for() * ops * BM * 4 +
+           (52 + 2 * idx_slots_for()) * 8 + 64;
+  };
   int smem_cap = ctas == 3 ? 75 * 1024 : (ctas == 2 ? 113 * 1024 : 227 * 1024);
   int a_st = 0, b_st = 0, epi_bufs = 1;
   auto plan = [&]() -> bool {
@@ -1285,6 +1351,8 @@ extern "C" int32_t scb_conv_implicit_rows(const void* features, int64_t ldf, int
     }
   }
   p.ops = ops;
+  p.idx_slots = idx_slots_for();
+  p.idx_slot_bytes = (uint32_t)(ops * BM * 4);
   p.a_stages = a_st;
   p.b_stages = b_st;
   p.epi_bufs = epi_bufs;
@@ -1307,7 +1375,7 @@ extern "C" int32_t scb_conv_implicit_rows(const void* features, int64_t ldf, int
     if (rc != SCB_OK) return rc;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(64 + NPROD + 128);
+    cfg.blockDim = dim3(IC_THREADS);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
