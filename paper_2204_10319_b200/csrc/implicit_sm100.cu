@@ -1272,11 +1272,12 @@ extern "C" int32_t scb_conv_implicit_rows(const void* features, int64_t ldf, int
   uint32_t cols = 32;
   while (cols < (uint32_t)(p.nacc * n_pad)) cols *= 2;
   p.tmem_cols = cols;
-  // CTAs per SM: one for gathering layers with 64-wide K chunks (deep A
-  // ring; measured 5-15 % faster than two or three since the index ring
-  // removed the index-load stalls), two whenever both accumulator pairs
-  // fit, else one.
-  int ctas = (p.kc == 64 && hits) ? 1 : (cols <= 256 ? 2 : 1);
+  // CTAs per SM: one for k3 gathering layers with 64-wide K chunks (deep A
+  // ring; measured 5-15 % faster per layer than two or three since the index
+  // ring removed the index-load stalls), two whenever both accumulator pairs
+  // fit, else one (three for K = 1 / k2 layers measured the same in the
+  // whole step).
+  int ctas = (p.kc == 64 && hits && volume == 27) ? 1 : (cols <= 256 ? 2 : 1);
   if (ctas_per_sm > 0)  // tuned (autotune.tune_fused_layer): clamped to what TMEM allows
     ctas = (ctas_per_sm >= 3 && cols <= 128) ? 3 : (ctas_per_sm >= 2 && cols <= 256 ? 2 : 1);
   p.total_tiles = (int)((n_out + BM - 1) / BM);
