@@ -167,3 +167,32 @@ def test_dilation_spec_validation():
         sc.LayerSpec(3, 1, 8, 8, dilation=0)
     with pytest.raises(ValueError, match="stride-1"):
         sc.LayerSpec(2, 2, 8, 8, dilation=2)
+
+
+def test_cpu_arm_samples_and_torch_free_tables():
+    """The reference CPU arm's bounded samples: equal-count azimuth sectors
+    that partition each scan (fractions sum to one scan), and the model
+    tables the workers load without importing torch or the engine."""
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parent.parent
+    sys.path.insert(0, str(root))
+    import bench
+    rng = np.random.default_rng(0)
+    c = np.concatenate([np.zeros((1000, 1), np.int64), rng.integers(0, 500, (1000, 3))], 1)
+    f = rng.standard_normal((1000, 4)).astype(np.float32)
+    secs = bench.scan_sectors((c, f, (500, 500, 500)), 16)
+    assert len(secs) == 16
+    assert abs(sum(s[3] for s in secs) - 1.0) < 1e-12
+    rows = np.concatenate([s[0] for s in secs])
+    assert rows.shape == c.shape
+    assert np.array_equal(np.unique(rows, axis=0), np.unique(c, axis=0))
+    assert max(s[0].shape[0] for s in secs) - min(s[0].shape[0] for s in secs) <= 1
+    code = ("import sys; sys.path.insert(0, %r)\n"
+            "from oracle.reference_runner import model_tables\n"
+            "m = model_tables('minkunet'); p = m.build_params(0.5, 4, 0)\n"
+            "assert len(m.layer_table(0.5)) == 50 and 'torch' not in sys.modules\n"
+            "print('ok')" % str(root))
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr
