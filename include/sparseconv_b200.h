@@ -398,9 +398,12 @@ int32_t scb_map_search_masked(int32_t kind, const int32_t* coords, int64_t n,
 
 int64_t scb_mask_sort_workspace(int64_t n);
 
-/* perm[i] = the row placed at position i: a stable sort by (batch column,
- * mask with offsets re-ranked so the least frequent are the most
- * significant bits).  `coords` int32 rows of `cols` words (batch first). */
+/* perm[i] = the row placed at position i: a stable sort by the mask with
+ * offsets re-ranked so the least frequent are the most significant bits.
+ * Rows of different batch entries interleave (maps never cross batch
+ * entries; grouping equal words across the batch leaves fewer live tile
+ * blocks).  `coords` int32 rows of `cols` words (batch first); batch_size is
+ * validated only. */
 int32_t scb_mask_sort(const uint32_t* masks, const uint64_t* counts, const int32_t* coords,
                       int32_t cols, int64_t n, int32_t volume, int64_t batch_size,
                       void* workspace, int64_t ws_bytes, int32_t* perm, scb_stream_t stream);

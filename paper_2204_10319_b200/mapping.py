@@ -223,8 +223,9 @@ def reorder_by_presence(cset: CoordinateSet, kernel_size: int = 3,
                         kind: str = "auto") -> CoordinateSet:
     """The same coordinates with rows relabelled so that rows with similar
     neighbour patterns are adjacent (B200 extension, the TorchSparse++
-    bitmask sort): a stable sort by (batch, presence mask with the rarest
-    offsets most significant).  Returns a new CoordinateSet whose row i is
+    bitmask sort): a stable sort by the presence mask with the rarest
+    offsets most significant (batch entries interleave: maps never cross
+    them).  Returns a new CoordinateSet whose row i is
     row ``perm[i]`` of ``cset`` (``.perm``); maps built over it hold the same
     pairs under the new row numbers, and 128-row tiles of its k3 maps have
     far fewer active offsets (the fused kernel skips the rest).  Cached on

@@ -27,15 +27,15 @@ def _oracle_masks(coords, boundary, batch_size=1):
 
 
 def _oracle_perm(masks, batch, V=27):
-    """Stable sort by (batch, mask with offsets ranked by decreasing
-    frequency: most frequent -> bit 0, rarest -> bit V-1)."""
+    """Stable sort by the mask with offsets ranked by decreasing frequency
+    (most frequent -> bit 0, rarest -> bit V-1); the batch column is not part
+    of the key (rows of different batch entries interleave)."""
     counts = np.array([((masks >> n) & 1).sum() for n in range(V)])
     pos = np.array([sum(1 for u in range(V) if counts[u] > counts[n]
                         or (counts[u] == counts[n] and u < n)) for n in range(V)])
     key = np.zeros_like(masks)
     for n in range(V):
         key |= ((masks >> n) & 1) << pos[n]
-    key |= batch.astype(np.int64) << V
     return np.argsort(key, kind="stable")
 
 
