@@ -399,7 +399,8 @@ int32_t scb_map_search_masked(int32_t kind, const int32_t* coords, int64_t n,
 int64_t scb_mask_sort_workspace(int64_t n);
 
 /* perm[i] = the row placed at position i: a stable sort by the mask with
- * offsets re-ranked so the least frequent are the most significant bits.
+ * offsets re-ranked so the least frequent are the most significant bits,
+ * the masks visited in reflected-Gray-code order.
  * Rows of different batch entries interleave (maps never cross batch
  * entries; grouping equal words across the batch leaves fewer live tile
  * blocks).  `coords` int32 rows of `cols` words (batch first); batch_size is

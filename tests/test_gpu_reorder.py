@@ -28,15 +28,21 @@ def _oracle_masks(coords, boundary, batch_size=1):
 
 def _oracle_perm(masks, batch, V=27):
     """Stable sort by the mask with offsets ranked by decreasing frequency
-    (most frequent -> bit 0, rarest -> bit V-1); the batch column is not part
-    of the key (rows of different batch entries interleave)."""
+    (most frequent -> bit 0, rarest -> bit V-1), words visited in Gray-code
+    order; the batch column is not part of the key (rows of different batch
+    entries interleave)."""
     counts = np.array([((masks >> n) & 1).sum() for n in range(V)])
     pos = np.array([sum(1 for u in range(V) if counts[u] > counts[n]
                         or (counts[u] == counts[n] and u < n)) for n in range(V)])
     key = np.zeros_like(masks)
     for n in range(V):
         key |= ((masks >> n) & 1) << pos[n]
-    return np.argsort(key, kind="stable")
+    g = key.copy()   # Gray-code order: sort by the word's index along the Gray sequence
+    shift = key >> 1
+    while shift.any():
+        g ^= shift
+        shift >>= 1
+    return np.argsort(g, kind="stable")
 
 
 def _clouds(rng):
