@@ -21,6 +21,9 @@ wd = sc.WeightTensor(rng.normal(0, 0.05, (8, 96, 96)).astype(np.float32), 2, 3)
 wu = sc.WeightTensor(rng.normal(0, 0.05, (8, 96, 96)).astype(np.float32), 2, 3)
 cache = {}
 opts = sc.ExecOptions(dataflow="fused", index_kind="hash")
+if os.environ.get("L1_REORDER", "0") == "1":   # the model's level 1: presence-relabelled
+    from paper_2204_10319_b200.execution import prepare_reordered_level
+    prepare_reordered_level(p, sc.LayerSpec(2, 2, 96, 96), opts)
 d = sc.sparse_conv_forward(x, wd, sc.LayerSpec(2, 2, 96, 96, reuse_key="d"), None, cache, opts)
 spec = sc.LayerSpec(2, 1, 96, 96, transposed=True, reuse_key="d")
 for _ in range(5):
@@ -32,4 +35,4 @@ for _ in range(20):
     sc.inverse_conv_forward(d, wu, spec, cache, None, opts)
 e.record()
 torch.cuda.synchronize()
-print(f"up 96->96 L1->L0 ({n} rows): {a.elapsed_time(e) / 20:.4f} ms  onehot={os.environ.get('SCB_ONEHOT', '1')} ring={os.environ.get('SCB_IC_RING', '1')}")
+print(f"up 96->96 L1->L0 ({n} rows): {a.elapsed_time(e) / 20:.4f} ms  onehot={os.environ.get('SCB_ONEHOT', '1')} L1_reorder={os.environ.get('L1_REORDER', '0')}")
