@@ -589,7 +589,7 @@ def _run_fused(features: torch.Tensor, kmap: KernelMap | None, w: WeightTensor,
     out = torch.empty((n_out, ldo), dtype=features.dtype, device=features.device)
     scale, shift, bias, res, relu = _epi_args(epilogue, n_out, w.c_out, features.dtype)
     rows = None
-    if kmap is not None and kmap.onehot and os.environ.get("SCB_ONEHOT", "1") == "1":
+    if kmap is not None and kmap.onehot and os.environ.get("SCB_ONEHOT", "0") == "1":
         # one entry per output row: tiles over the rows sorted by offset
         perm, h, m = kmap.onehot_order()
         hits, masks, rows = nat.ptr(h), nat.ptr(m), nat.ptr(perm)

@@ -105,11 +105,16 @@ def test_pair_onehot_transposed(sc, rng):
     d = sc.sparse_conv_forward(t.replace_features(f), wd,
                                sc.LayerSpec(2, 2, 32, 64, reuse_key="d"), None, cache, opts)
     spec = sc.LayerSpec(2, 1, 64, 32, transposed=True, reuse_key="d")
+    import os
     outs = []
-    for shape in ((2, 0), (4, 0), (5, 0)):
-        o = sc.ExecOptions(dataflow="fused", index_kind="hash", layer_label="U",
-                           kernel_shapes={"U": shape})
-        outs.append(sc.inverse_conv_forward(d, wu, spec, cache, None, o).features)
+    os.environ["SCB_ONEHOT"] = "1"   # the permuted-output-row path (opt-in)
+    try:
+        for shape in ((2, 0), (4, 0), (5, 0)):
+            o = sc.ExecOptions(dataflow="fused", index_kind="hash", layer_label="U",
+                               kernel_shapes={"U": shape})
+            outs.append(sc.inverse_conv_forward(d, wu, spec, cache, None, o).features)
+    finally:
+        os.environ.pop("SCB_ONEHOT")
     assert _close(outs[1], outs[0]) and _close(outs[2], outs[0])
 
 

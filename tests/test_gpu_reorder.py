@@ -198,10 +198,10 @@ def test_onehot_order_transposed_layer(sc, rng):
     ep = {"scale": torch.full((48,), 1.1, device="cuda"),
           "shift": torch.full((48,), 0.01, device="cuda"), "relu": True}
     spec = sc.LayerSpec(2, 1, 64, 48, transposed=True, reuse_key="d")
-    got = sc.inverse_conv_forward(d, wu, spec, cache, None, opts, epilogue=ep).features
-    os.environ["SCB_ONEHOT"] = "0"
+    want = sc.inverse_conv_forward(d, wu, spec, cache, None, opts, epilogue=ep).features
+    os.environ["SCB_ONEHOT"] = "1"   # opt-in (the whole MinkUNet step measured no gain)
     try:
-        want = sc.inverse_conv_forward(d, wu, spec, cache, None, opts, epilogue=ep).features
+        got = sc.inverse_conv_forward(d, wu, spec, cache, None, opts, epilogue=ep).features
     finally:
         os.environ.pop("SCB_ONEHOT")
     assert torch.equal(got, want)
