@@ -972,7 +972,7 @@ const IcEnv& ic_env() {
       const char* v = getenv(name);
       return v ? atoi(v) : dflt;
     };
-    return IcEnv{env_int("SCB_IC_INTERLEAVE", 1), env_int("SCB_IC_PDL", 1),
+    return IcEnv{env_int("SCB_IC_INTERLEAVE", 1), env_int("SCB_IC_PDL", 0),
                  env_int("SCB_IC_DEBUG", 0), env_int("SCB_IC_PAIR", 0), env_int("SCB_IC_RING", 1)};
   }();
   return e;
