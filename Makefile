@@ -3,7 +3,8 @@ NVCC ?= nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
 CSRC := paper_2204_10319_b200/csrc
 SRCS := $(CSRC)/capi.cu $(CSRC)/mapping.cu $(CSRC)/movement.cu $(CSRC)/gemm_sm100.cu \
-        $(CSRC)/implicit_sm100.cu $(CSRC)/voxelize.cu $(CSRC)/reorder.cu
+        $(CSRC)/implicit_sm100.cu $(CSRC)/voxelize.cu $(CSRC)/reorder.cu \
+        $(CSRC)/upconv_sm100.cu
 OBJS := $(patsubst $(CSRC)/%.cu,build/%.o,$(SRCS))
 LIB  := paper_2204_10319_b200/libsparseconv_b200.so
 FLAGS := -O3 -std=c++17 -lineinfo $(ARCH) -Xcompiler -fPIC -Iinclude -Xptxas -v

@@ -347,6 +347,23 @@ int32_t scb_conv_implicit_rows(const void* features, int64_t ldf, int32_t c_spli
                                const void* residual, int32_t relu, int32_t ctas_per_sm,
                                int32_t stage_kb, scb_stream_t stream);
 
+/* Transposed K = s layer in scatter form (replaces inverse_conv_forward,
+ * execution.py:512-551, for a map made by swap_roles of a K = s strided map,
+ * mapping.py:277-286): `child` is that strided map's hit matrix
+ * [volume][hits_ld(n_in)] (child[n][p] = the fine row k whose parent is
+ * coarse row p at offset n, or -1), so out[child[n][p]] = epilogue(x[p] . W[n]).
+ * Every fine row must have exactly one (p, n) (true for K = s maps); each row
+ * of `out` [n_out][ldo] is written once.  features [n_in][ldf] fp16, c_in and
+ * c_out multiples of 8 up to 256, weights packed as for scb_conv_implicit.
+ * BN scale/shift (together), bias, ReLU as scb_conv_implicit; no residual.
+ * B200 extension: one dense tcgen05 tile of x per 128 coarse rows, no gather. */
+int32_t scb_conv_transposed_scatter(const void* features, int64_t ldf, int64_t n_in, int32_t c_in,
+                                    const int32_t* child, int32_t volume,
+                                    const void* weights_packed, int32_t c_out, void* out,
+                                    int64_t ldo, int64_t n_out, const float* scale,
+                                    const float* shift, const float* bias, int32_t relu,
+                                    scb_stream_t stream);
+
 /* Row order for a one-hot hit matrix (every output row has at most one
  * entry, e.g. the transposed map of a K = s strided layer): perm = the rows
  * stably sorted by the offset of their entry (rows without one last),

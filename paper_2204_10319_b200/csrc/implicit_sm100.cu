@@ -1001,6 +1001,9 @@ struct MapKeyHash {
 std::mutex g_map_mu;
 std::unordered_map<MapKey, CUtensorMap, MapKeyHash> g_maps;
 
+}  // namespace
+
+// shared with the transposed scatter conv (upconv_sm100.cu)
 bool cached_map_f16(CUtensorMap* out, const void* base, long long inner, long long rows, long long ld,
                     int box_inner, int box_rows, int swz, std::string& err) {
   const MapKey key{base, inner, rows, ld, box_inner, box_rows, swz};
@@ -1017,6 +1020,8 @@ bool cached_map_f16(CUtensorMap* out, const void* base, long long inner, long lo
   g_maps.emplace(key, *out);
   return true;
 }
+
+namespace {
 
 // cudaFuncSetAttribute once per kernel instantiation (a driver call per
 // launch otherwise).

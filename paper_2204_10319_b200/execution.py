@@ -544,6 +544,11 @@ def _epi_args(ep: dict | None, n_out: int, c_out: int, dtype):
             int(bool(ep.get("relu", False))))
 
 
+# Transposed K = s layers in scatter form (scb_conv_transposed_scatter);
+# SCB_UPSCATTER=0 runs them through the gather-form fused kernel instead.
+_UPSCATTER = os.environ.get("SCB_UPSCATTER", "1") != "0"
+
+
 def _fused_eligible(dtype, volume: int, w: WeightTensor) -> bool:
     """The implicit-GEMM kernel: FP16 storage, K^3 in {1, 8, 27}, C_out up to
     256 (C_out not a multiple of 8, e.g. the 19-class head, is written into
@@ -589,26 +594,37 @@ def _run_fused(features: torch.Tensor, kmap: KernelMap | None, w: WeightTensor,
     out = torch.empty((n_out, ldo), dtype=features.dtype, device=features.device)
     scale, shift, bias, res, relu = _epi_args(epilogue, n_out, w.c_out, features.dtype)
     rows = None
-    if kmap is not None and kmap.onehot and os.environ.get("SCB_ONEHOT", "0") == "1":
+    scatter = (kmap is not None and kmap.onehot and kmap._parent is not None and concat is None
+               and res is None and _UPSCATTER and w.c_in % 8 == 0 and w.c_out % 8 == 0
+               and features.shape[1] == w.c_in and features.is_contiguous())
+    if scatter:
+        # transposed K = s layer: coarse tiles scattered to their one fine row each
+        child = kmap._parent.hits
+        with _timed(timer, label, "fused"):
+            nat.call("scb_conv_transposed_scatter", nat.ptr(features), features.shape[1],
+                     features.shape[0], w.c_in, nat.ptr(child), volume, nat.ptr(packed), w.c_out,
+                     nat.ptr(out), ldo, n_out, scale, shift, bias, relu, nat.stream_handle())
+    elif kmap is not None and kmap.onehot and os.environ.get("SCB_ONEHOT", "0") == "1":
         # one entry per output row: tiles over the rows sorted by offset
         perm, h, m = kmap.onehot_order()
         hits, masks, rows = nat.ptr(h), nat.ptr(m), nat.ptr(perm)
     else:
         hits = None if kmap is None else nat.ptr(kmap.hits)
         masks = None if kmap is None else nat.ptr(kmap.tile_masks())
-    with _timed(timer, label, "fused"):
-        if concat is not None and features.shape[1] % 8 == 0 and concat.shape[1] % 8 == 0 \
-                and features.is_contiguous() and concat.is_contiguous():
-            f, ca, f2, cb = features, features.shape[1], concat, concat.shape[1]
-        else:
-            f = features if concat is None else torch.cat([features, concat], dim=1)
-            f, ca, f2, cb = _pad_channels(f), None, None, 0
-            ca = f.shape[1]
-        ctas, skb = (opts.kernel_shapes or {}).get(label, (0, 0))
-        nat.call("scb_conv_implicit_rows", nat.ptr(f), f.shape[1], ca, nat.ptr(f2),
-                 0 if f2 is None else f2.shape[1], f.shape[0], ca + cb, hits, volume, n_out,
-                 masks, rows, nat.ptr(packed), w.c_out, nat.ptr(out), ldo, scale, shift, bias,
-                 res, relu, int(ctas), int(skb), nat.stream_handle())
+    if not scatter:
+        with _timed(timer, label, "fused"):
+            if concat is not None and features.shape[1] % 8 == 0 and concat.shape[1] % 8 == 0 \
+                    and features.is_contiguous() and concat.is_contiguous():
+                f, ca, f2, cb = features, features.shape[1], concat, concat.shape[1]
+            else:
+                f = features if concat is None else torch.cat([features, concat], dim=1)
+                f, ca, f2, cb = _pad_channels(f), None, None, 0
+                ca = f.shape[1]
+            ctas, skb = (opts.kernel_shapes or {}).get(label, (0, 0))
+            nat.call("scb_conv_implicit_rows", nat.ptr(f), f.shape[1], ca, nat.ptr(f2),
+                     0 if f2 is None else f2.shape[1], f.shape[0], ca + cb, hits, volume, n_out,
+                     masks, rows, nat.ptr(packed), w.c_out, nat.ptr(out), ldo, scale, shift, bias,
+                     res, relu, int(ctas), int(skb), nat.stream_handle())
     if ldo != w.c_out:
         out = out[:, : w.c_out]  # 8-aligned rows for the TMA store; a strided view
     if opts.traffic_log is not None:
@@ -623,6 +639,8 @@ def _run_fused(features: torch.Tensor, kmap: KernelMap | None, w: WeightTensor,
                 + e * volume * w.c_in * w.c_out + (e * n_out * w.c_out if res else 0))
         if kmap is None:
             blocks = (n_out + nat.TILE_ROWS - 1) // nat.TILE_ROWS
+        elif scatter:  # every (coarse tile, offset) block is multiplied
+            blocks = volume * ((features.shape[0] + nat.TILE_ROWS - 1) // nat.TILE_ROWS)
         else:
             tm = (kmap.onehot_order()[2] if rows is not None else kmap.tile_masks()
                   ).cpu().numpy().astype(np.uint32)

@@ -414,6 +414,8 @@ class KernelMap:
         self._swapped = None
         self._tile_masks = None
         self.onehot = False   # at most one entry per output row (transposed K = s map)
+        self._parent = None   # the K = s map this one-hot map was swapped from
+        self._lazy_hits = None  # builds the hit matrix on first use (one-hot swapped maps)
         self._onehot_order = None
 
     @classmethod
@@ -423,6 +425,8 @@ class KernelMap:
 
     def device_tensors(self):
         out = [t for t in (self._hits, self._tile_masks) if t is not None]
+        if self._parent is not None and self._parent._hits is not None:
+            out.append(self._parent._hits)  # the scatter form's child table
         if self._csr is not None:
             out += [self._csr[0], self._csr[2], self._csr[3]]
         return out
@@ -430,12 +434,14 @@ class KernelMap:
     # ---- representations ------------------------------------------------
     def _ensure_csr(self):
         if self._csr is None:
-            self._csr = _compact(self._hits, self.offsets.volume, self.n_out)
+            self._csr = _compact(self.hits, self.offsets.volume, self.n_out)
         return self._csr
 
     @property
     def hits(self) -> torch.Tensor:
         """[V][max(n_out,1)] int32 hit matrix on the device."""
+        if self._hits is None and self._lazy_hits is not None:
+            self._hits, self._lazy_hits = self._lazy_hits(), None
         if self._hits is None:
             ptr, _, ii, oi = self._ensure_csr()
             V = self.offsets.volume
@@ -499,6 +505,8 @@ class KernelMap:
 
     @property
     def device(self):
+        if self._hits is None and self._csr is None and self._parent is not None:
+            return self._parent.device
         return (self._hits if self._hits is not None else self._csr[2]).device
 
     @property
@@ -518,18 +526,30 @@ class KernelMap:
         re-sorted order directly: the new hit matrix is indexed by new output row."""
         if self._swapped is None:
             V = self.offsets.volume
-            ht = _hit_matrix(V, self.n_in, self.device)
-            if self._hits is not None:
-                nat.call("scb_hits_transpose", nat.ptr(self._hits), V, self.n_out, self.n_in,
-                         nat.ptr(ht), nat.stream_handle())
-            else:
-                nat.call("scb_map_transpose", nat.ptr(self.offset_ptr), nat.ptr(self.in_idx),
-                         nat.ptr(self.out_idx), V, self.total, self.n_in, nat.ptr(ht),
-                         nat.stream_handle())
-            self._swapped = KernelMap(None, None, None, None, self.offsets, self.stride,
-                                      self.n_out, self.n_in, trusted=self.trusted, hits=ht)
+
+            def transposed():
+                ht = _hit_matrix(V, self.n_in, self.device)
+                if self._hits is not None:
+                    nat.call("scb_hits_transpose", nat.ptr(self._hits), V, self.n_out, self.n_in,
+                             nat.ptr(ht), nat.stream_handle())
+                else:
+                    nat.call("scb_map_transpose", nat.ptr(self.offset_ptr), nat.ptr(self.in_idx),
+                             nat.ptr(self.out_idx), V, self.total, self.n_in, nat.ptr(ht),
+                             nat.stream_handle())
+                return ht
+
             # K = s windows tile the fine grid: every fine row has one parent
-            self._swapped.onehot = self.stride > 1 and self.offsets.kernel_size == self.stride
+            onehot = self.stride > 1 and self.offsets.kernel_size == self.stride
+            self._swapped = KernelMap(None, None, None, None, self.offsets, self.stride,
+                                      self.n_out, self.n_in, trusted=self.trusted,
+                                      hits=None if onehot else transposed())
+            self._swapped.onehot = onehot
+            if onehot:
+                # the scatter-form transposed layer reads this map's hit matrix
+                # as its child table (scb_conv_transposed_scatter); the
+                # transposed hit matrix is built only if something asks for it
+                self._swapped._parent = self
+                self._swapped._lazy_hits = transposed
         return self._swapped
 
 

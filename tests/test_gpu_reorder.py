@@ -198,12 +198,18 @@ def test_onehot_order_transposed_layer(sc, rng):
     ep = {"scale": torch.full((48,), 1.1, device="cuda"),
           "shift": torch.full((48,), 0.01, device="cuda"), "relu": True}
     spec = sc.LayerSpec(2, 1, 64, 48, transposed=True, reuse_key="d")
-    want = sc.inverse_conv_forward(d, wu, spec, cache, None, opts, epilogue=ep).features
-    os.environ["SCB_ONEHOT"] = "1"   # opt-in (the whole MinkUNet step measured no gain)
+    from paper_2204_10319_b200 import execution as X
+    saved = X._UPSCATTER
+    X._UPSCATTER = False   # the gather-form kernel (the scatter form takes precedence)
     try:
-        got = sc.inverse_conv_forward(d, wu, spec, cache, None, opts, epilogue=ep).features
+        want = sc.inverse_conv_forward(d, wu, spec, cache, None, opts, epilogue=ep).features
+        os.environ["SCB_ONEHOT"] = "1"   # opt-in (the whole MinkUNet step measured no gain)
+        try:
+            got = sc.inverse_conv_forward(d, wu, spec, cache, None, opts, epilogue=ep).features
+        finally:
+            os.environ.pop("SCB_ONEHOT")
     finally:
-        os.environ.pop("SCB_ONEHOT")
+        X._UPSCATTER = saved
     assert torch.equal(got, want)
 
 
