@@ -699,7 +699,7 @@ def roofline(args, samples, traffic):
     dom = max(("gather", "matmul", "scatter", "fused"), key=lambda k: stages.get(k, 0.0))
     kernel_name = {"gather": "scb gather_kernel", "matmul": "scb grouped_gemm_f16_kernel (tcgen05)",
                    "scatter": "scb scatter_kernel",
-                   "fused": "scb implicit_conv_f16_kernel + implicit_conv_pair_kernel (tcgen05 cta_group::1 / ::2, fused gather/GEMM/epilogue)"}[dom]
+                   "fused": "scb implicit_conv_f16_kernel + implicit_conv_pair_kernel (tcgen05 cta_group::1 / ::2, fused gather/GEMM/epilogue) + upconv_scatter_kernel (transposed k2 layers, scatter form)"}[dom]
     n_launch = max(1, n_fused if dom == "fused" else n_gemm)
     t_dom = max(stages.get(dom, 0.0), 1e-12)
     gbps = bytes_by[dom] / t_dom / 1e9

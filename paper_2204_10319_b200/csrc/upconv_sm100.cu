@@ -13,23 +13,35 @@
 //     out[child[n][p]] = epilogue(acc[p])           (child = the encoder map's
 //                                                    hit matrix; -1 -> no store)
 //
-// A is a dense TMA tile of the input features (no gather at all), B the
-// packed weights (resident in shared memory when all V slices fit, else
-// streamed through a ring), accumulators rotate through TMEM so the
-// scattering epilogue of (tile, n) overlaps the MMAs of (tile, n + 1).  Each
-// output row is written exactly once (full rows, 16-B stores by the lane that
-// owns the coarse row), so there are no atomics and no zero-init.  Executed
-// FLOPs are V / (fine rows per coarse row) ~ 3.3x the useful ones at level 0,
-// but the tensor pipe is not what bounds this layer: the ~HBM-bound bytes
-// are x once + out once + the child words.
+// A is a dense TMA tile of the input features (no gather at all) loaded with
+// the tile's V x 128 child words into an A ring; B is the packed weights,
+// resident in shared memory when all V slices fit beside two A slots, else
+// streamed from L2 one offset slice per ring stage.  Accumulators rotate
+// through TMEM (4 x n_pad columns) so the scattering epilogue of (tile, n)
+// overlaps the MMAs of later offsets.  Each output row is written exactly once
+// (full rows, 16-B stores by the lane that owns the coarse row): no atomics,
+// no zero-init.  Executed FLOPs are V / (fine rows per coarse row) ~ 3.3x the
+// useful ones at level 0.
 //
-// Warp roles (192 threads, persistent, 1 CTA per SM):
-//   warp 0      TMA producer (A tiles, B slices)
+// Measured (level 1 -> 0 of the bench's 8-scan pack, 96 -> 96 + BN + ReLU,
+// 424k coarse rows; tools/up_probe.py, SCB_UP_DEBUG): 0.156 ms vs 0.267 ms
+// for the gather-form fused kernel.  Without stores 0.141, without any
+// epilogue work 0.140, without MMAs too 0.073: the floor is the per-(tile, n)
+// accumulator hand-off (commit -> epilogue -> release, ~3000 cycles round trip
+// with 4 accumulators in flight; TMEM holds at most 5 96-column accumulators),
+// then the 6 SS MMAs per unit (~118 cycles each here).  Not HBM: 95 MB read +
+// 192 MB written in 0.156 ms is ~1.8 TB/s.
+//
+// Warp roles (352 threads, persistent, 1 CTA per SM):
+//   warp 0      A producer (TMA tiles of x + bulk copies of the child words)
 //   warp 1      TMEM allocator + MMA issuer
-//   warps 2..5  epilogue: tcgen05.ld -> BN / bias / ReLU -> fp16 -> scattered rows
+//   warps 2..9  epilogue, two groups of four draining alternate (tile, n)
+//               units: tcgen05.ld -> BN / bias / ReLU -> fp16 -> scattered rows
+//   warp 10     B producer (weight slices)
 #include <cuda.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -57,6 +69,8 @@ struct Params {
   int b_resident;            // all V x n_kchunks weight chunks live in smem
   int b_stages;              // else: ring depth
   int b_kg;                  // streamed: K chunks per ring stage
+  int debug;                 // EXPERIMENT (SCB_UP_DEBUG, results wrong): 1 = no stores,
+                             // 2 = no TMEM loads / math, 4 = no MMAs, 8 = no A / child copies
   int a_stages;              // A-tile ring depth (each slot: the tile + its V x 128 child words)
   int total_tiles;
   uint32_t idesc, tmem_cols, swz;
@@ -75,6 +89,40 @@ __device__ __forceinline__ uint32_t pack_half2(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
+constexpr int EPI_AFFINE = 1, EPI_BIAS = 2, EPI_RELU = 4;
+
+// 8 accumulator columns -> BN scale/shift, bias, ReLU (the fused kernel's
+// order) -> 8 fp16.  epi_s: scale[256], shift[256], bias[256] in smem.
+template <int EPI>
+__device__ __forceinline__ uint4 emit8(const uint32_t* r, const float* epi_s, int col) {
+  float v[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+  if (EPI & EPI_AFFINE) {
+    const float4 s0 = *reinterpret_cast<const float4*>(epi_s + col);
+    const float4 s1 = *reinterpret_cast<const float4*>(epi_s + col + 4);
+    const float4 t0 = *reinterpret_cast<const float4*>(epi_s + 256 + col);
+    const float4 t1 = *reinterpret_cast<const float4*>(epi_s + 256 + col + 4);
+    v[0] = v[0] * s0.x + t0.x; v[1] = v[1] * s0.y + t0.y;
+    v[2] = v[2] * s0.z + t0.z; v[3] = v[3] * s0.w + t0.w;
+    v[4] = v[4] * s1.x + t1.x; v[5] = v[5] * s1.y + t1.y;
+    v[6] = v[6] * s1.z + t1.z; v[7] = v[7] * s1.w + t1.w;
+  }
+  if (EPI & EPI_BIAS) {
+    const float4 b0 = *reinterpret_cast<const float4*>(epi_s + 512 + col);
+    const float4 b1 = *reinterpret_cast<const float4*>(epi_s + 512 + col + 4);
+    v[0] += b0.x; v[1] += b0.y; v[2] += b0.z; v[3] += b0.w;
+    v[4] += b1.x; v[5] += b1.y; v[6] += b1.z; v[7] += b1.w;
+  }
+  if (EPI & EPI_RELU) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = fmaxf(v[i], 0.f);
+  }
+  return make_uint4(pack_half2(v[0], v[1]), pack_half2(v[2], v[3]), pack_half2(v[4], v[5]),
+                    pack_half2(v[6], v[7]));
+}
+
+template <int EPI>
 __global__ void __launch_bounds__(THREADS, 1)
     upconv_scatter_kernel(const __grid_constant__ CUtensorMap tmA,
                           const __grid_constant__ CUtensorMap tmB,
@@ -146,6 +194,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         // matrix's row stride is a multiple of 4)
         const long long r0 = (long long)t * BM;
         const uint32_t cbytes = (uint32_t)(min((long long)BM, p.ldc - r0) * 4);
+        if (p.debug & 8) { mbar_arrive(a_full + ab); if (++ab == AS) { ab = 0; a_ph ^= 1; } continue; }
         mbar_expect_tx(a_full + ab, a_tile_bytes + cbytes * (uint32_t)p.V);
         for (int n = 0; n < p.V; ++n)
           bulk_load(smem_u32(child_s + (ab * p.V + n) * BM), p.child + n * p.ldc + r0, cbytes,
@@ -216,7 +265,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             for (int kk = 0; kk < kg; ++kk) {
               const uint32_t sa = sa0 + (k0 + kk) * p.a_chunk_bytes;
               const uint32_t sb = sb0 + kk * p.b_chunk_bytes;
-              for (int k = 0; k < p.kc / 16; ++k)
+              for (int k = 0; k < p.kc / 16 && !(p.debug & 4); ++k)
                 mma_f16(d_tmem, make_sdesc(sa + k * 32, sbo, layout),
                         make_sdesc(sb + k * 32, sbo, layout), p.idesc, ((k0 + kk) | k) != 0);
             }
@@ -250,7 +299,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         const long long k = prow < p.n_in ? (long long)cw[n * BM] : -1LL;
         mbar_wait_sleep(tfull + acc, acc_ph, 32);
         tc_after();
-        if (__any_sync(0xffffffffu, k >= 0)) {
+        if (!(p.debug & 2) && __any_sync(0xffffffffu, k >= 0)) {
           for (int c0 = 0; c0 < cols; c0 += 64) {
             const uint32_t taddr = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * p.n_pad + c0);
             const int nc = cols - c0 >= 64 ? 64 : cols - c0;   // multiple of 16
@@ -259,24 +308,12 @@ __global__ void __launch_bounds__(THREADS, 1)
             for (int j = 0; j < 4; ++j)
               if (16 * j < nc) TMEM_LD_X16(taddr + 16 * j, (r + 16 * j));
             tmem_wait_ld();
-            if (k >= 0) {
+            if (k >= 0 && !(p.debug & 1)) {
               uint4* dst = reinterpret_cast<uint4*>(p.out + k * p.ldo + c0);
 #pragma unroll
               for (int c = 0; c < 8; ++c) {
-                if (8 * c < nc && c0 + 8 * c < p.c_out) {
-                  float v[8];
-#pragma unroll
-                  for (int i = 0; i < 8; ++i) {
-                    const int col = c0 + 8 * c + i;
-                    float x = __uint_as_float(r[8 * c + i]);
-                    if (p.scale) x = x * epi_s[col] + epi_s[256 + col];
-                    if (p.bias) x += epi_s[512 + col];
-                    if (p.relu) x = fmaxf(x, 0.f);
-                    v[i] = x;
-                  }
-                  dst[c] = make_uint4(pack_half2(v[0], v[1]), pack_half2(v[2], v[3]),
-                                      pack_half2(v[4], v[5]), pack_half2(v[6], v[7]));
-                }
+                if (8 * c < nc && c0 + 8 * c < p.c_out)
+                  dst[c] = emit8<EPI>(r + 8 * c, epi_s, c0 + 8 * c);
               }
             }
           }
@@ -362,6 +399,8 @@ extern "C" int32_t scb_conv_transposed_scatter(const void* features, int64_t ldf
   p.shift = shift;
   p.bias = bias;
   p.out = (__half*)out;
+  static const int dbg = [] { const char* v = getenv("SCB_UP_DEBUG"); return v ? atoi(v) : 0; }();
+  p.debug = dbg;
 
   const int smem_cap = 227 * 1024;
   const int fixed = 1024 + (3 * MAX_A + 8 + 2 * MAX_STAGES) * 8 + 16 + 3 * 256 * 4;
@@ -399,15 +438,31 @@ extern "C" int32_t scb_conv_transposed_scatter(const void* features, int64_t ldf
     set_error(std::string("scb_conv_transposed_scatter: ") + err);
     return SCB_ECUDA;
   }
-  static std::once_flag attr_once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(attr_once, [&] {
-    attr_err = cudaFuncSetAttribute(upconv_scatter_kernel,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem_cap);
-  });
-  SCB_CUDA(attr_err);
+  const int epi = (scale ? EPI_AFFINE : 0) | (bias ? EPI_BIAS : 0) | (relu ? EPI_RELU : 0);
   const int grid = std::min(p.total_tiles, device_sms());
-  upconv_scatter_kernel<<<grid, THREADS, smem, as_stream(stream)>>>(mA, mB, p);
+  static std::once_flag attr_once[8];
+  static cudaError_t attr_err[8];
+  auto launch = [&](auto kernel) {
+    std::call_once(attr_once[epi], [&] {
+      attr_err[epi] = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           smem_cap);
+    });
+    if (attr_err[epi] != cudaSuccess) return attr_err[epi];
+    kernel<<<grid, THREADS, smem, as_stream(stream)>>>(mA, mB, p);
+    return cudaSuccess;
+  };
+  cudaError_t e;
+  switch (epi) {
+    case 0: e = launch(upconv_scatter_kernel<0>); break;
+    case 1: e = launch(upconv_scatter_kernel<1>); break;
+    case 2: e = launch(upconv_scatter_kernel<2>); break;
+    case 3: e = launch(upconv_scatter_kernel<3>); break;
+    case 4: e = launch(upconv_scatter_kernel<4>); break;
+    case 5: e = launch(upconv_scatter_kernel<5>); break;
+    case 6: e = launch(upconv_scatter_kernel<6>); break;
+    default: e = launch(upconv_scatter_kernel<7>); break;
+  }
+  SCB_CUDA(e);
   SCB_LAUNCHED();
   return SCB_OK;
 }

@@ -26,13 +26,17 @@ if os.environ.get("L1_REORDER", "0") == "1":   # the model's level 1: presence-r
     prepare_reordered_level(p, sc.LayerSpec(2, 2, 96, 96), opts)
 d = sc.sparse_conv_forward(x, wd, sc.LayerSpec(2, 2, 96, 96, reuse_key="d"), None, cache, opts)
 spec = sc.LayerSpec(2, 1, 96, 96, transposed=True, reuse_key="d")
+# the model's up layers carry BN + ReLU (EPI=0: no epilogue)
+ep = None if os.environ.get("EPI", "1") == "0" else {
+    "scale": torch.rand(96, device="cuda") + 0.5, "shift": torch.rand(96, device="cuda") - 0.5,
+    "relu": True}
 for _ in range(5):
-    sc.inverse_conv_forward(d, wu, spec, cache, None, opts)
+    sc.inverse_conv_forward(d, wu, spec, cache, None, opts, epilogue=ep)
 torch.cuda.synchronize()
 a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 a.record()
 for _ in range(20):
-    sc.inverse_conv_forward(d, wu, spec, cache, None, opts)
+    sc.inverse_conv_forward(d, wu, spec, cache, None, opts, epilogue=ep)
 e.record()
 torch.cuda.synchronize()
-print(f"up 96->96 L1->L0 ({n} rows): {a.elapsed_time(e) / 20:.4f} ms  onehot={os.environ.get('SCB_ONEHOT', '1')} L1_reorder={os.environ.get('L1_REORDER', '0')}")
+print(f"up 96->96 L1->L0 ({n} rows): {a.elapsed_time(e) / 20:.4f} ms  scatter={os.environ.get('SCB_UPSCATTER', '1')} epi={ep is not None} L1_reorder={os.environ.get('L1_REORDER', '0')}")
