@@ -364,6 +364,20 @@ int32_t scb_conv_transposed_scatter(const void* features, int64_t ldf, int64_t n
                                     const float* shift, const float* bias, int32_t relu,
                                     scb_stream_t stream);
 
+/* K = 1, s = 1 layer (sparse_conv_forward on a pointwise kernel, execution.py:
+ * 456-459: out = x . W[0] with the identity map) as a dense tcgen05 GEMM: TMA
+ * tiles of x (channels [0, c_split) from `features`, the rest from
+ * `features2` when given — the decoder's skip concatenation, read in place),
+ * weights packed as for scb_conv_implicit, BN scale/shift (together), bias and
+ * ReLU fused, each row of `out` [n][ldo] written once.  c_in and c_out
+ * multiples of 8 up to 256, c_split a multiple of 16.  B200 extension of the
+ * fused dataflow (the same kernel as scb_conv_transposed_scatter). */
+int32_t scb_conv_pointwise(const void* features, int64_t ldf, int32_t c_split,
+                           const void* features2, int64_t ldf2, int64_t n, int32_t c_in,
+                           const void* weights_packed, int32_t c_out, void* out, int64_t ldo,
+                           const float* scale, const float* shift, const float* bias,
+                           int32_t relu, scb_stream_t stream);
+
 /* Row order for a one-hot hit matrix (every output row has at most one
  * entry, e.g. the transposed map of a K = s strided layer): perm = the rows
  * stably sorted by the offset of their entry (rows without one last),

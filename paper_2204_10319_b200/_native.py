@@ -102,6 +102,8 @@ _SIGS = {
     "scb_tile_masks": (_I32, [_P, _I32, _I64, _P, _P]),
     "scb_conv_transposed_scatter": (_I32, [_P, _I64, _I64, _I32, _P, _I32, _P, _I32, _P, _I64,
                                             _I64, _P, _P, _P, _I32, _P]),
+    "scb_conv_pointwise": (_I32, [_P, _I64, _I32, _P, _I64, _I64, _I32, _P, _I32, _P, _I64, _P,
+                                   _P, _P, _I32, _P]),
     "scb_presence_masks": (_I32, [_I32, _P, _I64, _GP, _I32, _I32, _P, _P, _I64, _P, _P, _P]),
     "scb_map_search_masked": (_I32, [_I32, _P, _I64, _GP, _I32, _I32, _P, _P, _I64, _P, _P, _P, _P]),
     "scb_mask_sort_workspace": (_I64, [_I64]),

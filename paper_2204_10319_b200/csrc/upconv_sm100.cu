@@ -77,7 +77,8 @@ struct Params {
   uint32_t a_chunk_bytes;    // one K chunk of an A tile: 128 x kc fp16
   uint32_t b_chunk_bytes;    // slot stride of one K chunk of a weight slice (1024-aligned)
   uint32_t b_tx;             // bytes one weight-chunk load delivers: n_pad x kc fp16
-  const int* child;          // [V][ldc] fine output row or -1
+  const int* child;          // [V][ldc] fine output row or -1; NULL = identity (V = 1)
+  int a_split;               // K chunks read from x (the rest from x2, the concatenation)
   const float* scale;        // nullable (with shift)
   const float* shift;
   const float* bias;         // nullable
@@ -125,6 +126,7 @@ __device__ __forceinline__ uint4 emit8(const uint32_t* r, const float* epi_s, in
 template <int EPI>
 __global__ void __launch_bounds__(THREADS, 1)
     upconv_scatter_kernel(const __grid_constant__ CUtensorMap tmA,
+                          const __grid_constant__ CUtensorMap tmA2,
                           const __grid_constant__ CUtensorMap tmB,
                           const __grid_constant__ Params p) {
   extern __shared__ uint8_t smem_raw[];
@@ -164,6 +166,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA2) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
   }
   if (warp == 1) {
@@ -193,15 +196,17 @@ __global__ void __launch_bounds__(THREADS, 1)
         // child words: V rows of 128 (bulk copies; 16-B multiples, the hit
         // matrix's row stride is a multiple of 4)
         const long long r0 = (long long)t * BM;
-        const uint32_t cbytes = (uint32_t)(min((long long)BM, p.ldc - r0) * 4);
+        const uint32_t cbytes = p.child ? (uint32_t)(min((long long)BM, p.ldc - r0) * 4) : 0u;
         if (p.debug & 8) { mbar_arrive(a_full + ab); if (++ab == AS) { ab = 0; a_ph ^= 1; } continue; }
         mbar_expect_tx(a_full + ab, a_tile_bytes + cbytes * (uint32_t)p.V);
-        for (int n = 0; n < p.V; ++n)
+        for (int n = 0; n < p.V && cbytes; ++n)
           bulk_load(smem_u32(child_s + (ab * p.V + n) * BM), p.child + n * p.ldc + r0, cbytes,
                     a_full + ab);
+        // K chunks [0, a_split) from x, the rest from the concatenated x2
         for (int kk = 0; kk < p.n_kchunks; ++kk)
-          tma_load_2d(a_base + (size_t)ab * a_tile_bytes + (size_t)kk * p.a_chunk_bytes, &tmA,
-                      a_full + ab, kk * p.kc, t * BM);
+          tma_load_2d(a_base + (size_t)ab * a_tile_bytes + (size_t)kk * p.a_chunk_bytes,
+                      kk < p.a_split ? &tmA : &tmA2, a_full + ab,
+                      (kk < p.a_split ? kk : kk - p.a_split) * p.kc, t * BM);
         if (++ab == AS) { ab = 0; a_ph ^= 1; }
       }
     }
@@ -296,7 +301,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int* cw = child_s + cb * p.V * BM + 32 * q + lane;
       for (int n = 0; n < p.V; ++n, ++u) {
         if ((u & 1) != g) continue;
-        const long long k = prow < p.n_in ? (long long)cw[n * BM] : -1LL;
+        const long long k = prow >= p.n_in ? -1LL : (p.child ? (long long)cw[n * BM] : prow);
         mbar_wait_sleep(tfull + acc, acc_ph, 32);
         tc_after();
         if (!(p.debug & 2) && __any_sync(0xffffffffu, k >= 0)) {
@@ -349,27 +354,16 @@ int device_sms();
 
 using namespace scb;
 
-extern "C" int32_t scb_conv_transposed_scatter(const void* features, int64_t ldf, int64_t n_in,
-                                               int32_t c_in, const int32_t* child, int32_t volume,
-                                               const void* weights_packed, int32_t c_out,
-                                               void* out, int64_t ldo, int64_t n_out,
-                                               const float* scale, const float* shift,
-                                               const float* bias, int32_t relu,
-                                               scb_stream_t stream) {
-  using namespace up;
-  SCB_CHECK_ARG(features != nullptr && child != nullptr && weights_packed != nullptr &&
-                    out != nullptr,
-                "features, child, weights and out are required");
-  SCB_CHECK_ARG(volume >= 1 && volume <= 32, "volume must be in [1, 32]");
-  SCB_CHECK_ARG(c_in >= 8 && c_in % 8 == 0 && c_in <= 256, "c_in must be a multiple of 8 in [8, 256]");
-  SCB_CHECK_ARG(c_out >= 8 && c_out % 8 == 0 && c_out <= 256,
-                "c_out must be a multiple of 8 in [8, 256]");
-  SCB_CHECK_ARG(ldf >= c_in && ldf % 8 == 0, "ldf must be >= c_in and a multiple of 8");
-  SCB_CHECK_ARG(ldo >= c_out && ldo % 8 == 0, "ldo must be >= c_out and a multiple of 8");
-  SCB_CHECK_ARG((scale == nullptr) == (shift == nullptr), "scale and shift go together");
-  if (n_in <= 0 || n_out <= 0) return SCB_OK;
-  SCB_CHECK_ARG(n_in < (1LL << 31) - BM, "n_in too large");
+namespace {
 
+// Shared launcher: the transposed scatter form (child != NULL) and the dense
+// pointwise form (child == NULL: identity rows, V = 1, optional concat).
+int32_t launch_dense(const char* name, const void* features, int64_t ldf, int32_t c_split,
+                     const void* features2, int64_t ldf2, int64_t n_in, int32_t c_in,
+                     const int32_t* child, int32_t volume, const void* weights_packed,
+                     int32_t c_out, void* out, int64_t ldo, const float* scale,
+                     const float* shift, const float* bias, int32_t relu, scb_stream_t stream) {
+  using namespace up;
   const int n_pad = (c_out + 15) / 16 * 16;
   const int k_pad = (c_in + 15) / 16 * 16;
   Params p;
@@ -380,9 +374,17 @@ extern "C" int32_t scb_conv_transposed_scatter(const void* features, int64_t ldf
   p.c_out = c_out;
   p.V = volume;
   p.n_pad = n_pad;
-  p.kc = (k_pad % 64 == 0) ? 64 : ((k_pad % 32 == 0) ? 32 : 16);
+  // K chunk: the widest dividing k_pad (and the concat split, so no chunk
+  // straddles the two sources)
+  p.kc = 64;
+  while (p.kc > 16 && (k_pad % p.kc != 0 || (features2 && c_split % p.kc != 0))) p.kc /= 2;
+  if (features2 && c_split % p.kc != 0) {
+    set_error(std::string(name) + ": the concat split must be a multiple of 16 channels");
+    return SCB_EINVAL;
+  }
   p.swz = (uint32_t)p.kc * 2;
   p.n_kchunks = k_pad / p.kc;
+  p.a_split = features2 ? c_split / p.kc : p.n_kchunks;
   p.relu = relu;
   p.idesc = (1u << 4) | ((uint32_t)(n_pad >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
   p.nacc = std::min(4, 512 / n_pad) & ~1;   // even: the two epilogue groups alternate
@@ -430,12 +432,15 @@ extern "C" int32_t scb_conv_transposed_scatter(const void* features, int64_t ldf
   const int smem = fixed + p.a_stages * a_slot +
                    (p.b_resident ? b_all : p.b_stages * p.b_kg * (int)p.b_chunk_bytes);
 
-  CUtensorMap mA, mB;
+  CUtensorMap mA, mA2, mB;
   std::string err;
-  if (!cached_map_f16(&mA, features, c_in, n_in, ldf, p.kc, BM, (int)p.swz, err) ||
+  const int ca = features2 ? c_split : c_in;
+  if (!cached_map_f16(&mA, features, ca, n_in, ldf, p.kc, BM, (int)p.swz, err) ||
+      !cached_map_f16(&mA2, features2 ? features2 : features, features2 ? c_in - c_split : ca,
+                      n_in, features2 ? ldf2 : ldf, p.kc, BM, (int)p.swz, err) ||
       !cached_map_f16(&mB, weights_packed, k_pad, (long long)volume * n_pad, k_pad, p.kc, n_pad,
                       (int)p.swz, err)) {
-    set_error(std::string("scb_conv_transposed_scatter: ") + err);
+    set_error(std::string(name) + ": " + err);
     return SCB_ECUDA;
   }
   const int epi = (scale ? EPI_AFFINE : 0) | (bias ? EPI_BIAS : 0) | (relu ? EPI_RELU : 0);
@@ -448,7 +453,7 @@ extern "C" int32_t scb_conv_transposed_scatter(const void* features, int64_t ldf
                                            smem_cap);
     });
     if (attr_err[epi] != cudaSuccess) return attr_err[epi];
-    kernel<<<grid, THREADS, smem, as_stream(stream)>>>(mA, mB, p);
+    kernel<<<grid, THREADS, smem, as_stream(stream)>>>(mA, mA2, mB, p);
     return cudaSuccess;
   };
   cudaError_t e;
@@ -465,4 +470,34 @@ extern "C" int32_t scb_conv_transposed_scatter(const void* features, int64_t ldf
   SCB_CUDA(e);
   SCB_LAUNCHED();
   return SCB_OK;
+}
+
+}  // namespace
+
+extern "C" int32_t scb_conv_transposed_scatter(const void* features, int64_t ldf, int64_t n_in,
+                                               int32_t c_in, const int32_t* child, int32_t volume,
+                                               const void* weights_packed, int32_t c_out,
+                                               void* out, int64_t ldo, int64_t n_out,
+                                               const float* scale, const float* shift,
+                                               const float* bias, int32_t relu,
+                                               scb_stream_t stream) {
+  SCB_CHECK_ARG(child != nullptr, "child is required");
+  if (n_out <= 0) return SCB_OK;
+  return launch_dense("scb_conv_transposed_scatter", features, ldf, c_in, nullptr, 0, n_in, c_in,
+                      child, volume, weights_packed, c_out, out, ldo, scale, shift, bias, relu,
+                      stream);
+}
+
+extern "C" int32_t scb_conv_pointwise(const void* features, int64_t ldf, int32_t c_split,
+                                      const void* features2, int64_t ldf2, int64_t n,
+                                      int32_t c_in, const void* weights_packed, int32_t c_out,
+                                      void* out, int64_t ldo, const float* scale,
+                                      const float* shift, const float* bias, int32_t relu,
+                                      scb_stream_t stream) {
+  SCB_CHECK_ARG(!features2 || (c_split > 0 && c_split < c_in && c_split % 8 == 0 &&
+                               ldf2 >= c_in - c_split && ldf2 % 8 == 0),
+                "concat: 0 < c_split < c_in, multiples of 8");
+  return launch_dense("scb_conv_pointwise", features, ldf, c_split, features2, ldf2, n, c_in,
+                      nullptr, 1, weights_packed, c_out, out, ldo, scale, shift, bias, relu,
+                      stream);
 }

@@ -547,6 +547,9 @@ def _epi_args(ep: dict | None, n_out: int, c_out: int, dtype):
 # Transposed K = s layers in scatter form (scb_conv_transposed_scatter);
 # SCB_UPSCATTER=0 runs them through the gather-form fused kernel instead.
 _UPSCATTER = os.environ.get("SCB_UPSCATTER", "1") != "0"
+# K = 1 layers as dense TMA-fed GEMMs (scb_conv_pointwise); SCB_DENSE_K1=0 runs
+# them through the gather-form fused kernel's identity map instead.
+_DENSE_K1 = os.environ.get("SCB_DENSE_K1", "1") != "0"
 
 
 def _fused_eligible(dtype, volume: int, w: WeightTensor) -> bool:
@@ -597,7 +600,20 @@ def _run_fused(features: torch.Tensor, kmap: KernelMap | None, w: WeightTensor,
     scatter = (kmap is not None and kmap.onehot and kmap._parent is not None and concat is None
                and res is None and _UPSCATTER and w.c_in % 8 == 0 and w.c_out % 8 == 0
                and features.shape[1] == w.c_in and features.is_contiguous())
-    if scatter:
+    cb = 0 if concat is None else concat.shape[1]
+    pointwise = (kmap is None and _DENSE_K1 and res is None and not scatter
+                 and w.c_in <= 256 and w.c_out % 8 == 0 and features.is_contiguous()
+                 and features.shape[1] % (8 if concat is None else 16) == 0
+                 and (concat is None or (concat.is_contiguous() and cb % 8 == 0))
+                 and features.shape[1] + cb == w.c_in)
+    if pointwise:
+        # K = 1 layer: dense TMA tiles of x (and the concatenated skip) -> tcgen05
+        with _timed(timer, label, "fused"):
+            nat.call("scb_conv_pointwise", nat.ptr(features), features.shape[1],
+                     features.shape[1], nat.ptr(concat), cb, features.shape[0], w.c_in,
+                     nat.ptr(packed), w.c_out, nat.ptr(out), ldo, scale, shift, bias, relu,
+                     nat.stream_handle())
+    elif scatter:
         # transposed K = s layer: coarse tiles scattered to their one fine row each
         child = kmap._parent.hits
         with _timed(timer, label, "fused"):
@@ -611,7 +627,7 @@ def _run_fused(features: torch.Tensor, kmap: KernelMap | None, w: WeightTensor,
     else:
         hits = None if kmap is None else nat.ptr(kmap.hits)
         masks = None if kmap is None else nat.ptr(kmap.tile_masks())
-    if not scatter:
+    if not (scatter or pointwise):
         with _timed(timer, label, "fused"):
             if concat is not None and features.shape[1] % 8 == 0 and concat.shape[1] % 8 == 0 \
                     and features.is_contiguous() and concat.is_contiguous():

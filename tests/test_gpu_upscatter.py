@@ -107,3 +107,46 @@ def test_scatter_keeps_transposed_hits_lazy(sc, rng):
         p = np.nonzero(hd[n] >= 0)[0]
         np.testing.assert_array_equal(h[n][hd[n][p]], p)
     assert ((h >= 0).sum(0) == 1).all()   # one-hot: every fine row has one parent
+
+
+def _pointwise(sc, f, w, ep=None, concat=None, dense=True):
+    from paper_2204_10319_b200 import execution as X
+    saved = X._DENSE_K1
+    X._DENSE_K1 = dense
+    try:
+        return X._run_fused(f, None, w, sc.ExecOptions(dataflow="fused"), ep, concat)
+    finally:
+        X._DENSE_K1 = saved
+
+
+@pytest.mark.parametrize("c_in,c_split,c_out", [(64, None, 128), (128, None, 96), (96, None, 48),
+                                                (128, 96, 96), (160, 96, 96), (256, None, 256),
+                                                (48, 32, 64)])
+def test_pointwise_dense_equals_gather_form_and_oracle(sc, rng, c_in, c_split, c_out):
+    """K = 1 s = 1 layers through scb_conv_pointwise (dense TMA tiles, the skip
+    concatenation read in place) against the gather-form kernel's identity map
+    and the oracle's matmul (reference execution.py:456-459)."""
+    n = 20000 + 77
+    x = rng.standard_normal((n, c_in)).astype(np.float16)
+    w = sc.WeightTensor(rng.normal(0, 0.1, (1, c_in, c_out)).astype(np.float32), 1, 3)
+    ep = {"scale": torch.linspace(0.5, 1.5, c_out, device="cuda"),
+          "shift": torch.linspace(-0.1, 0.1, c_out, device="cuda"), "relu": True}
+    xt = torch.from_numpy(x).cuda()
+    f, cat = (xt, None) if c_split is None else (xt[:, :c_split].contiguous(),
+                                                 xt[:, c_split:].contiguous())
+    got = _pointwise(sc, f, w, ep, cat)
+    want = _pointwise(sc, f, w, ep, cat, dense=False)
+    assert got.shape == (n, c_out)
+    assert torch.equal(got, want)
+    ref = np.maximum((x.astype(np.float32) @ w.weights[0]) * np.linspace(0.5, 1.5, c_out,
+                     dtype=np.float32) + np.linspace(-0.1, 0.1, c_out, dtype=np.float32), 0)
+    assert _rel(got.float().cpu().numpy(), ref) < 1e-2
+
+
+def test_pointwise_no_epilogue_small(sc, rng):
+    """Fewer rows than one tile, no epilogue operands."""
+    x = torch.from_numpy(rng.standard_normal((37, 32)).astype(np.float16)).cuda()
+    w = sc.WeightTensor(rng.normal(0, 0.1, (1, 32, 16)).astype(np.float32), 1, 3)
+    got = _pointwise(sc, x, w)
+    want = _pointwise(sc, x, w, dense=False)
+    assert torch.equal(got, want)
