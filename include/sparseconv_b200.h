@@ -369,8 +369,9 @@ int32_t scb_conv_transposed_scatter(const void* features, int64_t ldf, int64_t n
  * tiles of x (channels [0, c_split) from `features`, the rest from
  * `features2` when given — the decoder's skip concatenation, read in place),
  * weights packed as for scb_conv_implicit, BN scale/shift (together), bias and
- * ReLU fused, each row of `out` [n][ldo] written once.  c_in and c_out
- * multiples of 8 up to 256, c_split a multiple of 16.  B200 extension of the
+ * ReLU fused, each row of `out` [n][ldo] written once.  c_in a multiple of 8
+ * up to 256, c_split a multiple of 16, c_out up to 256 (not a multiple of 8:
+ * the padding columns of the 8-aligned rows are written too, ldo >= that).  B200 extension of the
  * fused dataflow (the same kernel as scb_conv_transposed_scatter). */
 int32_t scb_conv_pointwise(const void* features, int64_t ldf, int32_t c_split,
                            const void* features2, int64_t ldf2, int64_t n, int32_t c_in,

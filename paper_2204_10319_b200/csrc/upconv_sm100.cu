@@ -175,10 +175,11 @@ __global__ void __launch_bounds__(THREADS, 1)
                  "r"(p.tmem_cols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  for (int i = threadIdx.x; i < p.c_out; i += THREADS) {
-    epi_s[i] = p.scale ? p.scale[i] : 1.f;
-    epi_s[256 + i] = p.shift ? p.shift[i] : 0.f;
-    epi_s[512 + i] = p.bias ? p.bias[i] : 0.f;
+  for (int i = threadIdx.x; i < p.n_pad; i += THREADS) {   // padding columns: identity
+    const bool c = i < p.c_out;
+    epi_s[i] = p.scale && c ? p.scale[i] : 1.f;
+    epi_s[256 + i] = p.shift && c ? p.shift[i] : 0.f;
+    epi_s[512 + i] = p.bias && c ? p.bias[i] : 0.f;
   }
   tc_before();
   __syncthreads();
@@ -364,6 +365,24 @@ int32_t launch_dense(const char* name, const void* features, int64_t ldf, int32_
                      int32_t c_out, void* out, int64_t ldo, const float* scale,
                      const float* shift, const float* bias, int32_t relu, scb_stream_t stream) {
   using namespace up;
+  auto bad = [&](const char* msg) {
+    set_error(std::string(name) + ": " + msg);
+    return SCB_EINVAL;
+  };
+  if (!features || !weights_packed || !out) return bad("features, weights and out are required");
+  if (!child && volume != 1) return bad("the identity form has volume 1");
+  if (volume < 1 || volume > 32) return bad("volume must be in [1, 32]");
+  if (c_in < 8 || c_in % 8 != 0 || c_in > 256) return bad("c_in must be a multiple of 8 in [8, 256]");
+  if (c_out < 1 || c_out > 256) return bad("c_out must be in [1, 256]");
+  if (ldf < (features2 ? c_split : c_in) || ldf % 8 != 0)
+    return bad("ldf must cover the channels and be a multiple of 8");
+  // rows are stored in 8-column groups: a C_out that is not a multiple of 8
+  // (the 19-class head) also writes the padding columns of its 8-aligned rows
+  if (ldo < (c_out + 7) / 8 * 8 || ldo % 8 != 0)
+    return bad("ldo must be a multiple of 8 covering c_out rounded up to 8");
+  if ((scale == nullptr) != (shift == nullptr)) return bad("scale and shift go together");
+  if (n_in <= 0) return SCB_OK;
+  if (n_in >= (1LL << 31) - BM) return bad("n_in too large");
   const int n_pad = (c_out + 15) / 16 * 16;
   const int k_pad = (c_in + 15) / 16 * 16;
   Params p;

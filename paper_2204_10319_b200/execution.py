@@ -602,7 +602,7 @@ def _run_fused(features: torch.Tensor, kmap: KernelMap | None, w: WeightTensor,
                and features.shape[1] == w.c_in and features.is_contiguous())
     cb = 0 if concat is None else concat.shape[1]
     pointwise = (kmap is None and _DENSE_K1 and res is None and not scatter
-                 and w.c_in <= 256 and w.c_out % 8 == 0 and features.is_contiguous()
+                 and w.c_in <= 256 and features.is_contiguous()
                  and features.shape[1] % (8 if concat is None else 16) == 0
                  and (concat is None or (concat.is_contiguous() and cb % 8 == 0))
                  and features.shape[1] + cb == w.c_in)

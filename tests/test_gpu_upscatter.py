@@ -119,7 +119,7 @@ def _pointwise(sc, f, w, ep=None, concat=None, dense=True):
         X._DENSE_K1 = saved
 
 
-@pytest.mark.parametrize("c_in,c_split,c_out", [(64, None, 128), (128, None, 96), (96, None, 48),
+@pytest.mark.parametrize("c_in,c_split,c_out", [(96, None, 19), (64, None, 128), (128, None, 96), (96, None, 48),
                                                 (128, 96, 96), (160, 96, 96), (256, None, 256),
                                                 (48, 32, 64)])
 def test_pointwise_dense_equals_gather_form_and_oracle(sc, rng, c_in, c_split, c_out):
@@ -150,3 +150,18 @@ def test_pointwise_no_epilogue_small(sc, rng):
     got = _pointwise(sc, x, w)
     want = _pointwise(sc, x, w, dense=False)
     assert torch.equal(got, want)
+
+
+def test_dense_forms_reject_bad_arguments(sc):
+    """The C ABI validates its arguments (reference error convention: the
+    Python layer re-raises the library message)."""
+    from paper_2204_10319_b200 import _native as nat
+    x = torch.zeros((10, 12), dtype=torch.float16, device="cuda")
+    w = torch.zeros((1, 16, 16), dtype=torch.float16, device="cuda")
+    out = torch.zeros((10, 16), dtype=torch.float16, device="cuda")
+    with pytest.raises(Exception, match="c_in"):
+        nat.call("scb_conv_pointwise", nat.ptr(x), 12, 12, None, 0, 10, 12, nat.ptr(w), 16,
+                 nat.ptr(out), 16, None, None, None, 0, nat.stream_handle())
+    with pytest.raises(Exception, match="child"):
+        nat.call("scb_conv_transposed_scatter", nat.ptr(x), 16, 10, 16, None, 8, nat.ptr(w), 16,
+                 nat.ptr(out), 16, 10, None, None, None, 0, nat.stream_handle())
