@@ -26,11 +26,10 @@
 // Measured (level 1 -> 0 of the bench's 8-scan pack, 96 -> 96 + BN + ReLU,
 // 424k coarse rows; tools/up_probe.py, SCB_UP_DEBUG): 0.156 ms vs 0.267 ms
 // for the gather-form fused kernel.  Without stores 0.141, without any
-// epilogue work 0.140, without MMAs too 0.073: the floor is the per-(tile, n)
-// accumulator hand-off (commit -> epilogue -> release, ~3000 cycles round trip
-// with 4 accumulators in flight; TMEM holds at most 5 96-column accumulators),
-// then the 6 SS MMAs per unit (~118 cycles each here).  Not HBM: 95 MB read +
-// 192 MB written in 0.156 ms is ~1.8 TB/s.
+// epilogue work 0.140, without MMAs too 0.125 (ncu): the epilogue warps wait
+// on the accumulator-full barrier most of the time while the MMA thread
+// rarely waits; not HBM (95 MB read + 192 MB written in 0.156 ms ~ 1.8 TB/s).
+// DESIGN.md §3 lists the variants measured slower.
 //
 // Warp roles (352 threads, persistent, 1 CTA per SM):
 //   warp 0      A producer (TMA tiles of x + bulk copies of the child words)
