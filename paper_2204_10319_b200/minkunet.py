@@ -336,7 +336,11 @@ class EngineMinkUNet:
             else:
                 call = lambda o: sparse_conv_forward(x, w, spec, None, cache, o, epilogue=ep,
                                                      concat=concat)
-            return self._tuned_call(name, call, opts)
+            # the dense forms (K = 1 layers, transposed K = s layers) have no
+            # launch-shape knobs: only gather-form layers are tuned
+            from . import execution as X
+            dense = (k == 1 and X._DENSE_K1) or (kind == "inverse" and X._UPSCATTER)
+            return call(opts) if dense else self._tuned_call(name, call, opts)
 
         def res(x, prefix, has_proj, skip=None):
             # relu(BN(conv2(h)) + shortcut): the residual add and ReLU run in
