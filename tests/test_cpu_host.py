@@ -196,3 +196,36 @@ def test_cpu_arm_samples_and_torch_free_tables():
             "print('ok')" % str(root))
     out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=120)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr
+
+
+def test_dense_forms_validate_arguments_before_touching_the_device():
+    """scb_conv_pointwise / scb_conv_transposed_scatter check their arguments
+    host-side (EINVAL + a message naming the entry point) before any CUDA
+    call, so the error convention holds without a GPU."""
+    import ctypes
+    from paper_2204_10319_b200 import _native
+    lib = _native.load()
+    fake = ctypes.c_void_p(0x1000)
+    pw = lib.scb_conv_pointwise
+    pw.restype = ctypes.c_int32
+    i64, i32, P = ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p
+    # c_in not a multiple of 8
+    rc = pw(fake, i64(16), i32(12), None, i64(0), i64(10), i32(12), fake, i32(16), fake,
+            i64(16), None, None, None, i32(0), None)
+    assert rc == 1 and b"scb_conv_pointwise" in lib.scb_last_error() and b"c_in" in lib.scb_last_error()
+    # scale without shift
+    rc = pw(fake, i64(16), i32(16), None, i64(0), i64(10), i32(16), fake, i32(16), fake,
+            i64(16), fake, None, None, i32(0), None)
+    assert rc == 1 and b"scale and shift" in lib.scb_last_error()
+    # output rows narrower than C_out rounded up to 8 (the 19-class head needs 24)
+    rc = pw(fake, i64(96), i32(96), None, i64(0), i64(10), i32(96), fake, i32(19), fake,
+            i64(19), None, None, None, i32(0), None)
+    assert rc == 1 and b"ldo" in lib.scb_last_error()
+    ts = lib.scb_conv_transposed_scatter
+    ts.restype = ctypes.c_int32
+    rc = ts(fake, i64(16), i64(10), i32(16), None, i32(8), fake, i32(16), fake, i64(16),
+            i64(10), None, None, None, i32(0), None)
+    assert rc == 1 and b"child" in lib.scb_last_error()
+    rc = ts(fake, i64(16), i64(10), i32(16), fake, i32(33), fake, i32(16), fake, i64(16),
+            i64(10), None, None, None, i32(0), None)
+    assert rc == 1 and b"volume" in lib.scb_last_error()
