@@ -1,0 +1,12 @@
+run() { tag=$1; shift; env "$@" timeout 300 python bench.py --steps 20 --warmup 5 --no-cpu-baseline $EXTRA > gpurun_out/ck_$tag.log 2>&1; tail -1 gpurun_out/ck_$tag.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(\"$tag\", round(d[\"value\"],1), round(d[\"e2e\"][\"value\"],1))"; }
+for i in 1 2; do
+run base$i X=1
+run prio0_$i SCB_MAP_PRIORITY=0
+run lvl1_$i SCB_PREFETCH_LEVEL=1
+run lvl3_$i SCB_PREFETCH_LEVEL=3
+run infl2_$i SCB_INFLIGHT=2
+run infl4_$i SCB_INFLIGHT=4
+run intl0_$i SCB_IC_INTERLEAVE=0
+EXTRA="--strategy none" run none_$i X=1
+EXTRA=""
+done
