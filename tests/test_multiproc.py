@@ -62,7 +62,9 @@ def _orchestrate(rank, world, port, q):
 
     got = gather_outputs({s: forward_stub(s) for s in mine})
     if rank == 0:
-        q.put({k: v.clone() for k, v in got.items()})
+        # numpy arrays travel by value (torch tensors would be shared through
+        # a file-descriptor socket that can vanish once this process exits)
+        q.put({k: v.numpy().copy() for k, v in got.items()})
     else:
         assert got is None
     dist.destroy_process_group()
@@ -83,7 +85,8 @@ def test_two_rank_shard_forward_gather_gloo():
     assert sorted(got) == list(range(12))
     for s in range(12):
         g = torch.Generator().manual_seed(s)
-        assert torch.equal(got[s], torch.randn((sizes[s], 3), generator=g, dtype=torch.float16))
+        assert torch.equal(torch.from_numpy(got[s]),
+                           torch.randn((sizes[s], 3), generator=g, dtype=torch.float16))
 
 
 def test_gather_outputs_single_process_is_identity():
