@@ -166,19 +166,40 @@ __device__ __forceinline__ void propose(const int* p, const Grid& gout, int K, i
     }
     if (keep && cap > 0) out[w++] = (KT)key;
   } else {
-    const int V = [&] { int v = 1; for (int d = 0; d < D; ++d) v *= K; return v; }();
-    for (int o = 0; o < V; ++o) {
-      int delta[D];
-      offset_of<D>(o, K, lo, delta);
-      bool keep = true;
-      long long key = p[0];
+    // per dimension the valid coarse coordinates q = (p - delta) / s, delta in
+    // [lo, lo + K), (p - delta) % s == 0, 0 <= q < ext, form one contiguous
+    // range: q_max = floor((p - lo) / s) and the (K - 1 - r) / s below it
+    // (r = (p - lo) mod s), clipped to the grid -- one division per dimension
+    // instead of the K^D offset walk's; the candidates are the ranges'
+    // Cartesian product (their order is irrelevant: sorted and deduplicated next)
+    int qlo[D], qhi[D];
+    bool any = true;
 #pragma unroll
-      for (int d = 0; d < D; ++d) {
-        const int u = p[d + 1] - delta[d];
-        keep = keep && u >= 0 && (u % s) == 0 && u < s * gout.ext[d];
-        key = key * gout.ext[d] + (u >= 0 ? u / s : 0);
+    for (int d = 0; d < D; ++d) {
+      const int x = p[d + 1] - lo;
+      int r = x % s;
+      r += r < 0 ? s : 0;
+      const int q = (x - r) / s;
+      qhi[d] = (int)min((long long)q, (long long)gout.ext[d] - 1);
+      qlo[d] = max(r <= K - 1 ? q - (K - 1 - r) / s : q + 1, 0);
+      any = any && qlo[d] <= qhi[d];
+    }
+    if (any) {
+      int idx[D];
+#pragma unroll
+      for (int d = 0; d < D; ++d) idx[d] = qlo[d];
+      while (w < cap) {
+        long long key = p[0];
+#pragma unroll
+        for (int d = 0; d < D; ++d) key = key * gout.ext[d] + idx[d];
+        out[w++] = (KT)key;
+        int d = D - 1;   // odometer over the per-dimension ranges
+        for (; d >= 0; --d) {
+          if (++idx[d] <= qhi[d]) break;
+          idx[d] = qlo[d];
+        }
+        if (d < 0) break;
       }
-      if (keep && w < cap) out[w++] = (KT)key;
     }
   }
   for (; w < cap; ++w) out[w] = sentinel;
